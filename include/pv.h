@@ -1,0 +1,253 @@
+/*
+ * pv.h — C ABI of the B200 hybrid-address-space (HAS) data plane.
+ *
+ * This is the drop-in boundary for the hot path of the devfsim reference
+ * (arXiv 1304.3771, "Paradice"): batched gva -> (gpa ->) hpa translation
+ * through guest / shadow / TDP / hybrid page tables and the page-chunked
+ * copy_to_user / copy_from_user gather/scatter between an operation buffer
+ * and guest pages.  Every entry point cites the reference interface it
+ * replaces (paths relative to the reference's pkg/src/devfsim/).
+ *
+ * Conventions
+ *   - plain pointers and sizes only; no exceptions cross the ABI.
+ *   - "device pointer" arguments are CUDA device memory owned by the caller;
+ *     "host pointer" arguments are host memory (pinned or pageable).
+ *   - every call is asynchronous on `stream` unless its comment says it
+ *     synchronises; a NULL stream is the legacy default stream.
+ *   - return value: 0 on success, negative on API / launch error
+ *     (PV_EINVAL, PV_ENOMEM, PV_ECUDA).  Per-lane / per-op outcomes are
+ *     reported through status arrays (PV_ST_* below), never as return codes.
+ *
+ * Memory image
+ *   The image is the reference's host physical memory (memvirt.py:124-188,
+ *   `PhysMem` over one flat bytearray): host-private region first, then the
+ *   guest slots (memvirt.py:433-480).  It lives in HBM as one flat byte array
+ *   of `image_bytes` bytes (a multiple of 4096).  A page-table node at pfn P
+ *   of a memory window with byte base B is at image offset B + P*4096; entry
+ *   i of it is the little-endian u64 at B + P*4096 + i*8 (memvirt.py:170-172).
+ *   Like the reference, node reads are bounded only by the image, not by the
+ *   window; a read past the image is reported as PV_ST_NODE_OOR (the
+ *   reference raises struct.error there).
+ */
+#ifndef PV_H_
+#define PV_H_
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PV_ABI_VERSION 1
+
+/* ---- return codes ------------------------------------------------------ */
+#define PV_SUCCESS 0
+#define PV_EINVAL (-22)
+#define PV_ENOMEM (-12)
+#define PV_ECUDA (-1000) /* PV_ECUDA - cudaError_t value */
+
+/* ---- per-lane / per-op status word --------------------------------------
+ * bits 0-3  : level (1 top, 2 mid, 3 leaf)            (memvirt.py:60-62)
+ * bits 4-11 : kind
+ * bits 16-24: entry index within the node (traps only; TrapExit.index)
+ * Rebuilt into the reference exception types by the Python layer
+ * (errors.py:15-45).
+ */
+#define PV_ST_OK 0x000u
+#define PV_ST_FAULT 0x010u     /* PageFault(va, level); value = va            */
+#define PV_ST_FAULT2 0x020u    /* PageFault in the TDP stage; value = gpa     */
+#define PV_ST_TRAP 0x040u      /* TrapExit(va, level, node, index); value=node */
+#define PV_ST_TRAP2 0x060u     /* TrapExit in the TDP stage; value = node,
+                                  aux = gpa (the TrapExit.va of that walk)     */
+#define PV_ST_NODE_OOR 0x080u  /* node read past the image; value = va        */
+#define PV_ST_NODE_OOR2 0x0A0u /* same, TDP stage; value = gpa                */
+#define PV_ST_DATA_OOR 0x100u  /* OutOfRange on the data access; value = hpa  */
+#define PV_ST_CONFLICT 0x400u  /* batch-level: two ops of one to_guest batch
+                                  write the same hpa page (host re-plans)      */
+#define PV_ST_KIND(s) ((s) & 0xFF0u)
+#define PV_ST_LEVEL(s) ((s) & 0xFu)
+#define PV_ST_INDEX(s) (((s) >> 16) & 0x1FFu)
+
+/* ---- translator description ----------------------------------------------
+ * One process address space as the reference's ProcessTranslator /
+ * _HybridResolver see it (memvirt.py:568-601, 677-696; backend.py:117-128).
+ *   PV_ONE_STAGE : walk(s1_base window, s1_root_pfn, va) -> hpa.  Shadow
+ *                  translation (memvirt.py:598-599), hybrid resolve
+ *                  (memvirt.py:677-682), host tables, and walk_guest
+ *                  (memvirt.py:262-267; s1_base = guest slot base, result is
+ *                  the gpa).
+ *   PV_TWO_STAGE : gpa = walk_guest(gva) in the guest window, then
+ *                  walk(host, s2_root_pfn, gpa) (memvirt.py:600-601).
+ */
+#define PV_ONE_STAGE 1u
+#define PV_TWO_STAGE 2u
+
+typedef struct pv_space {
+  uint64_t s1_base;     /* byte base of the stage-1 memory window          */
+  uint64_t s1_root_pfn; /* stage-1 root node pfn (window relative)          */
+  uint64_t s2_root_pfn; /* TDP root node pfn (host memory, base 0)          */
+  uint32_t mode;        /* PV_ONE_STAGE | PV_TWO_STAGE                      */
+  uint32_t reserved;
+} pv_space;
+
+/* A contiguous run of lanes translated through one space. */
+typedef struct pv_seg {
+  uint64_t begin;       /* first lane                                      */
+  uint64_t end;         /* one past the last lane                          */
+  uint64_t chunk0;      /* first global chunk id of this segment (exclusive
+                           prefix sum of ceil((end-begin)/pv_translate_chunk())) */
+  uint32_t space;       /* index into the spaces array                     */
+  uint32_t reserved;
+} pv_seg;
+
+/* ---- translate flags ---------------------------------------------------- */
+#define PV_VA32 0x1u    /* vas is uint32_t[] (else uint64_t[])             */
+#define PV_OUT_PFN 0x2u /* value = leaf pfn (walk); else address with the
+                           page offset of the va (translate / resolve)     */
+#define PV_HAS_TWO_STAGE 0x80000000u /* some space of the batch is
+                           PV_TWO_STAGE (selects the two-stage kernel)     */
+
+/* One user-buffer copy operation (memvirt.py:604-628). */
+typedef struct pv_op {
+  uint64_t gva;     /* first guest virtual address                         */
+  uint64_t len;     /* bytes                                               */
+  uint64_t buf_off; /* byte offset of this op's payload in the op buffer   */
+  uint32_t space;   /* index into the spaces array                         */
+  uint32_t reserved;
+} pv_op;
+
+/* Per-op outcome of a copy batch. */
+typedef struct pv_op_result {
+  uint64_t copied; /* bytes copied before the failing page (PageFault.bytes_copied) */
+  uint64_t value;  /* fault va / gpa, trap node pfn, or OOR hpa (per status)        */
+  uint64_t aux;    /* gpa of a TDP-stage trap                                       */
+  uint32_t status; /* PV_ST_*                                                        */
+  uint32_t fail_page; /* page index within the op of the failing page               */
+} pv_op_result;
+
+/* FIFO translation cache state of one process (memvirt.py:336-374). */
+#define PV_FIFO_MAX 32
+typedef struct pv_fifo {
+  uint64_t key[PV_FIFO_MAX]; /* gva >> 12 (unmasked)                        */
+  uint64_t val[PV_FIFO_MAX]; /* hpa >> 12                                   */
+  uint64_t hits;
+  uint64_t misses;
+  uint32_t capacity;         /* 1..PV_FIFO_MAX (reference default 10)       */
+  uint32_t len;              /* live entries                                */
+  uint32_t head;             /* ring index of the oldest entry              */
+  uint32_t reserved;
+} pv_fifo;
+
+#define PV_TO_GUEST 0u   /* copy_to_user  : buffer -> guest pages           */
+#define PV_FROM_GUEST 1u /* copy_from_user: guest pages -> buffer           */
+
+/* ---- library ------------------------------------------------------------ */
+int pv_abi_version(void);
+/* Lanes per translate chunk (for pv_seg.chunk0). */
+uint64_t pv_translate_chunk(void);
+/* Static name of a status kind ("ok", "page_fault", ...). */
+const char* pv_status_name(uint32_t status);
+
+/* ---- K1: batched translation ----------------------------------------------
+ * Replaces per-lane calls of walk (memvirt.py:244-259), walk_guest
+ * (memvirt.py:262-267), ProcessTranslator.translate with use_cache=False /
+ * _resolve_page (memvirt.py:585-601) and resolve_hybrid (memvirt.py:677-682).
+ * spaces / segs / vas / out_* are device pointers.  out_aux may be NULL
+ * (then TDP-stage trap gpas are not reported).  Lanes not covered by any
+ * segment are not written.
+ */
+int pv_translate(const uint8_t* image, uint64_t image_bytes,
+                 const pv_space* spaces, const pv_seg* segs, uint32_t n_segs,
+                 uint64_t n_chunks, const void* vas, uint32_t flags,
+                 uint64_t* out_value, uint32_t* out_status, uint64_t* out_aux,
+                 void* stream);
+
+/* ---- K4: FIFO cache replay --------------------------------------------------
+ * Applies the per-process FIFO-10 translation cache (memvirt.py:336-374,
+ * 585-594) to a batch of lanes that pv_translate resolved fresh: lanes of
+ * process p are lane_idx[proc_off[p] .. proc_off[p+1]) in lookup order.  A
+ * hit replaces the lane's value/status with the cached translation; a miss
+ * that resolved inserts (oldest-first eviction); a miss that faulted keeps
+ * the fault and inserts nothing.  fifo[] is updated in place (device).
+ * flags: PV_VA32 as for pv_translate.
+ */
+int pv_fifo_replay(const void* vas, uint32_t flags, const uint64_t* lane_idx,
+                   const uint64_t* proc_off, uint32_t n_procs, pv_fifo* fifo,
+                   uint64_t* value, uint32_t* status, void* stream);
+
+/* ---- K2/K3: batched user-buffer copy -------------------------------------
+ * Replaces copy_user_buffer (memvirt.py:604-628) as used by
+ * SoftwareHasAccess / HardwareHasAccess copy_to_user / copy_from_user
+ * (backend.py:92-104, 152-162).  Ops run with the reference's per-op
+ * semantics: one translation per page touched, chunk = min(remaining,
+ * 4096 - (cur & 0xFFF)), pages before the first failing page are copied and
+ * nothing after it, `copied` reports the completed prefix.
+ *
+ * pv_copy_plan translates every page of every op (page_off[] = exclusive
+ * prefix sum of page spans, n_ops+1 entries, device) into page_hpa[] /
+ * page_status[] (device, page_off[n_ops] entries each) and records each op's
+ * first failing page in op_first_bad[] (device, n_ops; the caller sets it to
+ * all-ones first).  For PV_TO_GUEST it also stamps destination pages in
+ * page_owner[] (device, one u64 per image page; NULL disables) with
+ * (epoch << 32 | op + 1) and sets *conflict (device u32) when two ops of the
+ * batch write one hpa page.
+ *
+ * pv_copy_exec moves the bytes for every page below its op's first failing
+ * page and fills results[] (device, n_ops).  dirty[] (device, one byte per
+ * image page; may be NULL) is set to 1 for every image page written.
+ * buf is the op buffer (device).  abort_flag (device, may be NULL): when
+ * *abort_flag != 0 at launch (the conflict word of the stamp pass) the
+ * kernel writes nothing, so the host can re-plan the batch in order.
+ */
+int pv_copy_plan(const uint8_t* image, uint64_t image_bytes,
+                 const pv_space* spaces, const pv_op* ops, uint64_t n_ops,
+                 const uint64_t* page_off, uint64_t n_pages, uint32_t direction,
+                 uint64_t* page_hpa, uint32_t* page_status, uint64_t* page_aux,
+                 uint64_t* op_first_bad, uint64_t* page_owner, uint32_t epoch,
+                 uint32_t* conflict, void* stream);
+
+int pv_copy_exec(uint8_t* image, uint64_t image_bytes, const pv_op* ops,
+                 uint64_t n_ops, const uint64_t* page_off, uint64_t n_pages,
+                 uint32_t direction, const uint64_t* page_hpa,
+                 const uint32_t* page_status, const uint64_t* page_aux,
+                 const uint64_t* op_first_bad, uint8_t* buf, uint64_t buf_bytes,
+                 pv_op_result* results, uint8_t* dirty,
+                 const uint32_t* abort_flag, void* stream);
+
+/* The conflict pass of pv_copy_plan on its own (run it after
+ * pv_copy_fifo_replay when the cache may have changed destinations).
+ * owner_pages = number of u64 entries in page_owner. */
+int pv_copy_stamp(const uint64_t* page_off, uint64_t n_ops, uint64_t n_pages,
+                  const uint64_t* page_hpa, const uint64_t* op_first_bad,
+                  uint64_t* page_owner, uint64_t owner_pages, uint32_t epoch,
+                  uint32_t* conflict, void* stream);
+
+/* Replays the FIFO cache over a copy plan (lookups in op order, page order,
+ * each op stopping at its first miss that fails to resolve), rewriting
+ * page_hpa / page_status / op_first_bad so pv_copy_exec sees cached
+ * translations.  op_idx lists the ops of process p at
+ * op_idx[proc_off[p] .. proc_off[p+1]) in program order. */
+int pv_copy_fifo_replay(const pv_op* ops, const uint64_t* page_off,
+                        const uint64_t* op_idx, const uint64_t* proc_off,
+                        uint32_t n_procs, pv_fifo* fifo, uint64_t image_bytes,
+                        uint32_t direction, uint64_t* page_hpa,
+                        uint32_t* page_status, uint64_t* op_first_bad,
+                        void* stream);
+
+/* ---- utility kernels used by the host runtime ---------------------------- */
+/* Scatter `n` whole pages from a (pinned) host staging area into the image:
+ * page i of src goes to image page pfns[i].  pfns device, src device. */
+int pv_scatter_pages(uint8_t* image, uint64_t image_bytes, const uint64_t* pfns,
+                     uint64_t n, const uint8_t* src, void* stream);
+/* Gather whole pages out of the image (inverse of pv_scatter_pages). */
+int pv_gather_pages(const uint8_t* image, uint64_t image_bytes,
+                    const uint64_t* pfns, uint64_t n, uint8_t* dst, void* stream);
+
+/* Synchronises `stream` and reports the first CUDA error seen (0 if none). */
+int pv_stream_sync(void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PV_H_ */

@@ -1,0 +1,120 @@
+"""ctypes binding of ``libpv.so`` (the C ABI declared in ``include/pv.h``).
+
+The library is built in-tree (``paper_1304_3771_b200/libpv.so``) by
+``__graft_entry__.build()`` / ``make -C paper_1304_3771_b200/csrc``.  Loading
+it does not need a GPU; calling a compute entry point does, and every such
+call goes through :func:`lib` which raises :class:`NativeUnavailable` when
+the library or a CUDA device is missing -- there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from .errors import NativeUnavailable
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpv.so")
+
+# ---- constants mirrored from include/pv.h --------------------------------
+ABI_VERSION = 1
+SUCCESS = 0
+EINVAL = -22
+ENOMEM = -12
+ECUDA = -1000
+
+ST_OK = 0x000
+ST_FAULT = 0x010
+ST_FAULT2 = 0x020
+ST_TRAP = 0x040
+ST_TRAP2 = 0x060
+ST_NODE_OOR = 0x080
+ST_NODE_OOR2 = 0x0A0
+ST_DATA_OOR = 0x100
+ST_CONFLICT = 0x400
+
+ONE_STAGE = 1
+TWO_STAGE = 2
+
+VA32 = 0x1
+OUT_PFN = 0x2
+HAS_TWO_STAGE = 0x80000000
+
+TO_GUEST = 0
+FROM_GUEST = 1
+
+FIFO_MAX = 32
+# struct sizes in 8-byte words (all structs are u64-aligned)
+SPACE_WORDS = 4    # pv_space
+SEG_WORDS = 4      # pv_seg
+OP_WORDS = 4       # pv_op
+RESULT_WORDS = 4   # pv_op_result
+FIFO_WORDS = 2 * FIFO_MAX + 4  # pv_fifo
+
+# every symbol include/pv.h declares
+EXPORTS = (
+    "pv_abi_version", "pv_translate_chunk", "pv_status_name", "pv_translate",
+    "pv_fifo_replay", "pv_copy_plan", "pv_copy_stamp", "pv_copy_exec",
+    "pv_copy_fifo_replay", "pv_scatter_pages", "pv_gather_pages", "pv_stream_sync",
+)
+
+_u64 = ctypes.c_uint64
+_u32 = ctypes.c_uint32
+_p = ctypes.c_void_p
+
+_SIGNATURES = {
+    "pv_abi_version": (ctypes.c_int, []),
+    "pv_translate_chunk": (_u64, []),
+    "pv_status_name": (ctypes.c_char_p, [_u32]),
+    "pv_translate": (ctypes.c_int, [_p, _u64, _p, _p, _u32, _u64, _p, _u32, _p, _p, _p, _p]),
+    "pv_fifo_replay": (ctypes.c_int, [_p, _u32, _p, _p, _u32, _p, _p, _p, _p]),
+    "pv_copy_plan": (ctypes.c_int, [_p, _u64, _p, _p, _u64, _p, _u64, _u32, _p, _p, _p, _p, _p, _u32, _p, _p]),
+    "pv_copy_stamp": (ctypes.c_int, [_p, _u64, _u64, _p, _p, _p, _u64, _u32, _p, _p]),
+    "pv_copy_exec": (ctypes.c_int, [_p, _u64, _p, _u64, _p, _u64, _u32, _p, _p, _p, _p, _p, _u64, _p, _p, _p, _p]),
+    "pv_copy_fifo_replay": (ctypes.c_int, [_p, _p, _p, _p, _u32, _p, _u64, _u32, _p, _p, _p, _p]),
+    "pv_scatter_pages": (ctypes.c_int, [_p, _u64, _p, _u64, _p, _p]),
+    "pv_gather_pages": (ctypes.c_int, [_p, _u64, _p, _u64, _p, _p]),
+    "pv_stream_sync": (ctypes.c_int, [_p]),
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libpv.so and bind its signatures (no GPU needed)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise NativeUnavailable(
+                f"{path} is missing: build it with __graft_entry__.build() "
+                "or `make -C paper_1304_3771_b200/csrc`")
+        cdll = ctypes.CDLL(path)
+        for name, (res, args) in _SIGNATURES.items():
+            fn = getattr(cdll, name)
+            fn.restype = res
+            fn.argtypes = args
+        if cdll.pv_abi_version() != ABI_VERSION:
+            raise NativeUnavailable("libpv.so ABI version mismatch; rebuild it")
+        _lib = cdll
+        return _lib
+
+
+def lib() -> ctypes.CDLL:
+    """The library, for a compute call: requires a CUDA device."""
+    import torch
+
+    if not torch.cuda.is_available():
+        raise NativeUnavailable("the HAS data plane runs on a CUDA device and none is visible")
+    return load()
+
+
+def check(rc: int, what: str) -> None:
+    if rc == SUCCESS:
+        return
+    if rc <= ECUDA:
+        raise RuntimeError(f"{what}: CUDA error {ECUDA - rc}")
+    raise ValueError(f"{what}: libpv returned {rc}")

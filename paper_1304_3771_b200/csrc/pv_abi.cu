@@ -1,0 +1,193 @@
+// pv_abi.cu — extern "C" entry points of libpv (declared in include/pv.h).
+//
+// Thin validation + launch layer: no allocation of user-visible memory, no
+// exceptions across the boundary, CUDA errors returned as PV_ECUDA - err.
+#include <mutex>
+#include <unordered_map>
+
+#include "pv_common.cuh"
+
+namespace pv {
+cudaError_t launch_translate(const uint8_t*, uint64_t, const pv_space*, const pv_seg*, uint32_t, uint64_t,
+                             const void*, uint32_t, bool, uint64_t*, uint32_t*, uint64_t*, cudaStream_t);
+uint64_t translate_chunk();
+cudaError_t launch_copy_plan(const uint8_t*, uint64_t, const pv_space*, const pv_op*, uint64_t, const uint64_t*,
+                             uint64_t, uint64_t*, uint32_t*, uint64_t*, uint64_t*, cudaStream_t);
+cudaError_t launch_copy_stamp(const uint64_t*, uint64_t, uint64_t, const uint64_t*, const uint64_t*, uint64_t*,
+                              uint64_t, uint32_t, uint32_t*, cudaStream_t);
+cudaError_t launch_copy_exec(uint8_t*, uint64_t, const pv_op*, uint64_t, const uint64_t*, uint64_t, uint32_t,
+                             const uint64_t*, const uint32_t*, const uint64_t*, const uint64_t*, uint8_t*,
+                             pv_op_result*, uint8_t*, const uint32_t*, cudaStream_t);
+cudaError_t launch_fifo_lanes(const void*, uint32_t, const uint64_t*, const uint64_t*, uint32_t, pv_fifo*,
+                              uint64_t*, uint32_t*, cudaStream_t);
+cudaError_t launch_fifo_copy(const pv_op*, const uint64_t*, const uint64_t*, const uint64_t*, uint32_t, pv_fifo*,
+                             uint64_t, uint64_t*, uint32_t*, uint64_t*, cudaStream_t);
+
+uint64_t resident_grid(const void* func, int tpb, size_t smem) {
+  static std::mutex mu;
+  static std::unordered_map<uint64_t, uint64_t> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t key = (reinterpret_cast<uint64_t>(func) << 8) ^ (uint64_t)dev ^ ((uint64_t)smem << 48);
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+  }
+  int sms = 148, per_sm = 1;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, func, tpb, smem);
+  if (per_sm < 1) per_sm = 1;
+  const uint64_t g = (uint64_t)sms * (uint64_t)per_sm;
+  std::lock_guard<std::mutex> lk(mu);
+  cache[key] = g;
+  return g;
+}
+
+__global__ void scatter_pages_kernel(uint8_t* __restrict__ image, uint64_t image_pages,
+                                     const uint64_t* __restrict__ pfns, uint64_t n, const uint8_t* __restrict__ src) {
+  for (uint64_t i = blockIdx.x; i < n; i += gridDim.x) {
+    const uint64_t pfn = pfns[i];
+    if (pfn >= image_pages) continue;
+    const uint4* s = reinterpret_cast<const uint4*>(src + i * kPageSize);
+    uint4* d = reinterpret_cast<uint4*>(image + pfn * kPageSize);
+    for (uint32_t j = threadIdx.x; j < kPageSize / 16; j += blockDim.x) d[j] = s[j];
+  }
+}
+
+__global__ void gather_pages_kernel(const uint8_t* __restrict__ image, uint64_t image_pages,
+                                    const uint64_t* __restrict__ pfns, uint64_t n, uint8_t* __restrict__ dst) {
+  for (uint64_t i = blockIdx.x; i < n; i += gridDim.x) {
+    const uint64_t pfn = pfns[i];
+    if (pfn >= image_pages) continue;
+    const uint4* s = reinterpret_cast<const uint4*>(image + pfn * kPageSize);
+    uint4* d = reinterpret_cast<uint4*>(dst + i * kPageSize);
+    for (uint32_t j = threadIdx.x; j < kPageSize / 16; j += blockDim.x) d[j] = s[j];
+  }
+}
+
+static inline int rc(cudaError_t e) { return e == cudaSuccess ? PV_SUCCESS : PV_ECUDA - (int)e; }
+
+}  // namespace pv
+
+using namespace pv;
+
+extern "C" {
+
+int pv_abi_version(void) { return PV_ABI_VERSION; }
+
+uint64_t pv_translate_chunk(void) { return translate_chunk(); }
+
+const char* pv_status_name(uint32_t status) {
+  switch (PV_ST_KIND(status)) {
+    case PV_ST_OK: return "ok";
+    case PV_ST_FAULT: return "page_fault";
+    case PV_ST_FAULT2: return "page_fault_tdp";
+    case PV_ST_TRAP: return "trap_exit";
+    case PV_ST_TRAP2: return "trap_exit_tdp";
+    case PV_ST_NODE_OOR: return "node_out_of_range";
+    case PV_ST_NODE_OOR2: return "node_out_of_range_tdp";
+    case PV_ST_DATA_OOR: return "out_of_range";
+    case PV_ST_CONFLICT: return "conflict";
+    default: return "unknown";
+  }
+}
+
+int pv_translate(const uint8_t* image, uint64_t image_bytes, const pv_space* spaces, const pv_seg* segs,
+                 uint32_t n_segs, uint64_t n_chunks, const void* vas, uint32_t flags, uint64_t* out_value,
+                 uint32_t* out_status, uint64_t* out_aux, void* stream) {
+  if (n_chunks == 0) return PV_SUCCESS;
+  if (!image || !spaces || !segs || !vas || !out_value || !out_status || n_segs == 0) return PV_EINVAL;
+  if (image_bytes % kPageSize) return PV_EINVAL;
+  if (flags & ~(uint32_t)(PV_VA32 | PV_OUT_PFN | PV_HAS_TWO_STAGE)) return PV_EINVAL;
+  const bool two = flags & PV_HAS_TWO_STAGE;
+  return rc(launch_translate(image, image_bytes, spaces, segs, n_segs, n_chunks, vas, flags & 0x3u, two, out_value,
+                             out_status, out_aux, (cudaStream_t)stream));
+}
+
+int pv_fifo_replay(const void* vas, uint32_t flags, const uint64_t* lane_idx, const uint64_t* proc_off,
+                   uint32_t n_procs, pv_fifo* fifo, uint64_t* value, uint32_t* status, void* stream) {
+  if (n_procs == 0) return PV_SUCCESS;
+  if (!vas || !lane_idx || !proc_off || !fifo || !value || !status) return PV_EINVAL;
+  return rc(launch_fifo_lanes(vas, flags, lane_idx, proc_off, n_procs, fifo, value, status, (cudaStream_t)stream));
+}
+
+int pv_copy_plan(const uint8_t* image, uint64_t image_bytes, const pv_space* spaces, const pv_op* ops,
+                 uint64_t n_ops, const uint64_t* page_off, uint64_t n_pages, uint32_t direction, uint64_t* page_hpa,
+                 uint32_t* page_status, uint64_t* page_aux, uint64_t* op_first_bad, uint64_t* page_owner,
+                 uint32_t epoch, uint32_t* conflict, void* stream) {
+  if (n_pages == 0) return PV_SUCCESS;
+  if (!image || !spaces || !ops || !page_off || !page_hpa || !page_status || !op_first_bad || n_ops == 0)
+    return PV_EINVAL;
+  if (direction != PV_TO_GUEST && direction != PV_FROM_GUEST) return PV_EINVAL;
+  if (image_bytes % kPageSize) return PV_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = launch_copy_plan(image, image_bytes, spaces, ops, n_ops, page_off, n_pages, page_hpa, page_status,
+                                   page_aux, op_first_bad, s);
+  if (e != cudaSuccess) return rc(e);
+  if (direction == PV_TO_GUEST && page_owner != nullptr) {
+    if (!conflict) return PV_EINVAL;
+    e = launch_copy_stamp(page_off, n_ops, n_pages, page_hpa, op_first_bad, page_owner, image_bytes / kPageSize,
+                          epoch, conflict, s);
+  }
+  return rc(e);
+}
+
+int pv_copy_stamp(const uint64_t* page_off, uint64_t n_ops, uint64_t n_pages, const uint64_t* page_hpa,
+                  const uint64_t* op_first_bad, uint64_t* page_owner, uint64_t owner_pages, uint32_t epoch,
+                  uint32_t* conflict, void* stream) {
+  if (n_pages == 0) return PV_SUCCESS;
+  if (!page_off || !page_hpa || !op_first_bad || !page_owner || !conflict) return PV_EINVAL;
+  return rc(launch_copy_stamp(page_off, n_ops, n_pages, page_hpa, op_first_bad, page_owner, owner_pages, epoch,
+                              conflict, (cudaStream_t)stream));
+}
+
+int pv_copy_exec(uint8_t* image, uint64_t image_bytes, const pv_op* ops, uint64_t n_ops, const uint64_t* page_off,
+                 uint64_t n_pages, uint32_t direction, const uint64_t* page_hpa, const uint32_t* page_status,
+                 const uint64_t* page_aux, const uint64_t* op_first_bad, uint8_t* buf, uint64_t buf_bytes,
+                 pv_op_result* results, uint8_t* dirty, const uint32_t* abort_flag, void* stream) {
+  (void)buf_bytes;
+  if (n_pages == 0) return PV_SUCCESS;
+  if (!image || !ops || !page_off || !page_hpa || !page_status || !op_first_bad || !buf || !results)
+    return PV_EINVAL;
+  if (direction != PV_TO_GUEST && direction != PV_FROM_GUEST) return PV_EINVAL;
+  return rc(launch_copy_exec(image, image_bytes, ops, n_ops, page_off, n_pages, direction, page_hpa, page_status,
+                             page_aux, op_first_bad, buf, results, dirty, abort_flag, (cudaStream_t)stream));
+}
+
+int pv_copy_fifo_replay(const pv_op* ops, const uint64_t* page_off, const uint64_t* op_idx, const uint64_t* proc_off,
+                        uint32_t n_procs, pv_fifo* fifo, uint64_t image_bytes, uint32_t direction,
+                        uint64_t* page_hpa, uint32_t* page_status, uint64_t* op_first_bad, void* stream) {
+  (void)direction;
+  if (n_procs == 0) return PV_SUCCESS;
+  if (!ops || !page_off || !op_idx || !proc_off || !fifo || !page_hpa || !page_status || !op_first_bad)
+    return PV_EINVAL;
+  return rc(launch_fifo_copy(ops, page_off, op_idx, proc_off, n_procs, fifo, image_bytes, page_hpa, page_status,
+                             op_first_bad, (cudaStream_t)stream));
+}
+
+int pv_scatter_pages(uint8_t* image, uint64_t image_bytes, const uint64_t* pfns, uint64_t n, const uint8_t* src,
+                     void* stream) {
+  if (n == 0) return PV_SUCCESS;
+  if (!image || !pfns || !src || image_bytes % kPageSize) return PV_EINVAL;
+  const uint64_t grid = n < 4096 ? n : 4096;
+  scatter_pages_kernel<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(image, image_bytes / kPageSize, pfns, n, src);
+  return rc(cudaGetLastError());
+}
+
+int pv_gather_pages(const uint8_t* image, uint64_t image_bytes, const uint64_t* pfns, uint64_t n, uint8_t* dst,
+                    void* stream) {
+  if (n == 0) return PV_SUCCESS;
+  if (!image || !pfns || !dst || image_bytes % kPageSize) return PV_EINVAL;
+  const uint64_t grid = n < 4096 ? n : 4096;
+  gather_pages_kernel<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(image, image_bytes / kPageSize, pfns, n, dst);
+  return rc(cudaGetLastError());
+}
+
+int pv_stream_sync(void* stream) {
+  cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  return rc(e);
+}
+
+}  // extern "C"

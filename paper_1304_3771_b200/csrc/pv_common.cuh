@@ -1,0 +1,125 @@
+// pv_common.cuh — shared device helpers of the HAS data plane.
+//
+// PTE codec and the three-level walk of the reference (memvirt.py:51-66,
+// 99-121, 244-259), restated for sm_100a: one u64 load per level, trapping
+// wins over present (memvirt.py:111-116), the writable bit is never
+// consulted (memvirt.py:244-259), bits 3-11 are ignored, the VA top index is
+// masked to 2 bits so VA bits >= 32 alias (memvirt.py:121).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "../../include/pv.h"
+
+namespace pv {
+
+constexpr uint32_t kPageShift = 12;
+constexpr uint64_t kPageSize = 4096;
+constexpr uint64_t kPageMask = kPageSize - 1;
+constexpr uint64_t kFlagPresent = 0x1;
+constexpr uint64_t kFlagTrapping = 0x4;
+constexpr uint64_t kNone = ~0ull;
+
+__host__ __device__ __forceinline__ uint32_t top_index(uint64_t va) { return (uint32_t)(va >> 30) & 0x3u; }
+__host__ __device__ __forceinline__ uint32_t mid_index(uint64_t va) { return (uint32_t)(va >> 21) & 0x1FFu; }
+__host__ __device__ __forceinline__ uint32_t leaf_index(uint64_t va) { return (uint32_t)(va >> 12) & 0x1FFu; }
+
+// Number of whole nodes addressable in a window with byte base `base`.
+__host__ __device__ __forceinline__ uint64_t node_limit(uint64_t image_bytes, uint64_t base) {
+  return base >= image_bytes ? 0 : (image_bytes - base) >> kPageShift;
+}
+
+__device__ __forceinline__ uint64_t ld_word(const uint8_t* image, uint64_t base, uint64_t pfn, uint32_t idx) {
+  return __ldg(reinterpret_cast<const unsigned long long*>(image + base + (pfn << kPageShift)) + idx);
+}
+
+// Classify one entry word at `level`.  Returns PV_ST_OK and advances *node,
+// or a status word (fault / trap) for the walk's stage.
+__device__ __forceinline__ uint32_t classify(uint64_t w, uint32_t level, uint32_t index, uint32_t stage2,
+                                             uint64_t* node, uint64_t* trap_node) {
+  if (w & kFlagTrapping) {
+    *trap_node = *node;
+    return (stage2 ? PV_ST_TRAP2 : PV_ST_TRAP) | level | (index << 16);
+  }
+  if (!(w & kFlagPresent)) return (stage2 ? PV_ST_FAULT2 : PV_ST_FAULT) | level;
+  *node = w >> kPageShift;
+  return PV_ST_OK;
+}
+
+// Full three-level walk through global memory (L1/L2 cached).  On success
+// returns PV_ST_OK with *out = leaf target pfn.  On a trap *out = node pfn.
+__device__ __forceinline__ uint32_t walk_global(const uint8_t* __restrict__ image, uint64_t image_bytes,
+                                                uint64_t base, uint64_t root, uint64_t va, uint32_t stage2,
+                                                uint64_t* out) {
+  const uint64_t lim = node_limit(image_bytes, base);
+  uint64_t node = root, trap_node = 0;
+  const uint32_t idx[3] = {top_index(va), mid_index(va), leaf_index(va)};
+#pragma unroll
+  for (uint32_t l = 0; l < 3; ++l) {
+    if (node >= lim) return (stage2 ? PV_ST_NODE_OOR2 : PV_ST_NODE_OOR) | (l + 1);
+    const uint64_t w = ld_word(image, base, node, idx[l]);
+    const uint32_t st = classify(w, l + 1, idx[l], stage2, &node, &trap_node);
+    if (st != PV_ST_OK) {
+      *out = trap_node;
+      return st;
+    }
+  }
+  *out = node;
+  return PV_ST_OK;
+}
+
+// Translate `va` through a space with global-memory walks.  On success
+// *value = leaf pfn of the final stage.  On failure *value / *aux follow the
+// pv.h status conventions (va or gpa for faults, node pfn for traps).
+__device__ __forceinline__ uint32_t translate_global(const uint8_t* __restrict__ image, uint64_t image_bytes,
+                                                     const pv_space& sp, uint64_t va, uint64_t* value,
+                                                     uint64_t* aux) {
+  uint64_t r = 0;
+  uint32_t st = walk_global(image, image_bytes, sp.s1_base, sp.s1_root_pfn, va, 0, &r);
+  if (st != PV_ST_OK) {
+    *value = (PV_ST_KIND(st) == PV_ST_TRAP) ? r : va;
+    return st;
+  }
+  if (sp.mode != PV_TWO_STAGE) {
+    *value = r;
+    return PV_ST_OK;
+  }
+  const uint64_t gpa = (r << kPageShift) | (va & kPageMask);
+  st = walk_global(image, image_bytes, 0, sp.s2_root_pfn, gpa, 1, &r);
+  if (st != PV_ST_OK) {
+    if (PV_ST_KIND(st) == PV_ST_TRAP2) {
+      *value = r;
+      *aux = gpa;
+    } else {
+      *value = gpa;
+    }
+    return st;
+  }
+  *value = r;
+  return PV_ST_OK;
+}
+
+__host__ __device__ __forceinline__ uint64_t page_span(uint64_t gva, uint64_t len) {
+  return len == 0 ? 0 : ((gva + len - 1) >> kPageShift) - (gva >> kPageShift) + 1;
+}
+
+// VA of page k of an op (the first chunk keeps the unaligned start;
+// memvirt.py:615-619).
+__host__ __device__ __forceinline__ uint64_t op_page_va(uint64_t gva, uint64_t k) {
+  return k == 0 ? gva : ((gva >> kPageShift) + k) << kPageShift;
+}
+
+// Largest i with off[i] <= p, searching [lo, hi).
+__device__ __forceinline__ uint64_t upper_search(const uint64_t* __restrict__ off, uint64_t lo, uint64_t hi,
+                                                 uint64_t p) {
+  while (hi - lo > 1) {
+    const uint64_t mid = lo + ((hi - lo) >> 1);
+    if (__ldg(off + mid) <= p) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// Grid size that fills every SM with resident CTAs of `func` (cached per
+// function and device; defined in pv_abi.cu).
+uint64_t resident_grid(const void* func, int tpb, size_t smem);
+
+}  // namespace pv

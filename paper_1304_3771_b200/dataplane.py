@@ -1,0 +1,427 @@
+"""Host runtime of the HBM data plane: batching, launch, status decoding.
+
+Everything here drives libpv kernels (``include/pv.h``) on the current CUDA
+stream; nothing computes a translation or moves a payload byte on the CPU.
+The functions are the batched forms of the reference's hot path:
+
+* :func:`translate_lanes` -- K1, a batch of walks / translations
+  (memvirt.py:244-267, 596-601, 677-682);
+* :func:`fifo_replay_lanes` -- K4, the FIFO-10 cache applied to a batch
+  (memvirt.py:336-374, 585-594);
+* :func:`copy_ops` -- K2/K3, a batch of copy_user_buffer operations with the
+  reference's prefix-on-fault semantics (memvirt.py:604-628);
+* :func:`translate_one` -- a batch of one, used by the per-address drop-in
+  entry points (walk, translate, resolve_hybrid).
+
+Status words are decoded back into the reference's exceptions by
+:func:`raise_for`.
+"""
+
+from __future__ import annotations
+
+import struct
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .errors import OutOfRange, PageFault, TrapExit
+
+PAGE_SIZE = 4096
+PAGE_SHIFT = 12
+PAGE_MASK = PAGE_SIZE - 1
+U64 = (1 << 64) - 1
+
+
+@dataclass(frozen=True)
+class Space:
+    """A translator as the kernels see it (pv_space)."""
+
+    s1_base: int
+    s1_root_pfn: int
+    s2_root_pfn: int = 0
+    mode: int = N.ONE_STAGE
+
+    def words(self) -> list[int]:
+        return [self.s1_base, self.s1_root_pfn, self.s2_root_pfn, self.mode]
+
+
+def _i64(values) -> np.ndarray:
+    """uint64 bit patterns as an int64 array (torch has no uint64 math)."""
+    return np.asarray(values, dtype=np.uint64).view(np.int64)
+
+
+def _to_dev(arr: np.ndarray, stream=None):
+    import torch
+
+    t = torch.from_numpy(np.ascontiguousarray(arr))
+    if t.numel() * t.element_size() >= 1 << 16:
+        t = t.pin_memory()
+    return t.to("cuda", non_blocking=True)
+
+
+def _stream():
+    import torch
+
+    return torch.cuda.current_stream()
+
+
+# ---- status decoding ---------------------------------------------------------
+
+def kind(status: int) -> int:
+    return status & 0xFF0
+
+
+def raise_for(status: int, value: int, aux: int, va: int, image_bytes: int, chunk: int = 0,
+              bytes_copied: int | None = None) -> None:
+    """Raise the reference exception a lane / op status stands for."""
+    k = kind(status)
+    level = status & 0xF
+    if k == N.ST_OK:
+        return
+    if k in (N.ST_FAULT, N.ST_FAULT2):
+        fault = PageFault(value, level)
+        if bytes_copied is not None:
+            fault.bytes_copied = bytes_copied
+        raise fault
+    if k == N.ST_TRAP:
+        raise TrapExit(va, level, value, (status >> 16) & 0x1FF)
+    if k == N.ST_TRAP2:
+        raise TrapExit(aux, level, value, (status >> 16) & 0x1FF)
+    if k in (N.ST_NODE_OOR, N.ST_NODE_OOR2):
+        # The reference's unchecked read_word (memvirt.py:170-172) fails inside
+        # struct.unpack_from for a node past the buffer.
+        raise struct.error(f"page-table node read past the end of a {image_bytes}-byte memory "
+                           f"(walk of {value:#x}, level {level})")
+    if k == N.ST_DATA_OOR:
+        raise OutOfRange(f"access [{value:#x}, +{chunk}) beyond {image_bytes:#x}")
+    raise RuntimeError(f"unknown data-plane status {status:#x}")
+
+
+# ---- single-lane fast path ---------------------------------------------------
+
+class _OneLane:
+    """Reusable pinned + device words for batch-of-one translations."""
+
+    def __init__(self):
+        import torch
+
+        self.host = torch.zeros(16, dtype=torch.int64).pin_memory()
+        self.dev = torch.zeros(16, dtype=torch.int64, device="cuda")
+        self.out = torch.zeros(4, dtype=torch.int64).pin_memory()
+
+
+_tls = threading.local()
+
+
+def translate_one(image, space: Space, va: int, *, out_pfn: bool = False) -> tuple[int, int, int]:
+    """One walk/translation on the device: returns (status, value, aux)."""
+    lib = N.lib()
+    dev_img = image.device()
+    one = getattr(_tls, "one", None)
+    if one is None:
+        one = _tls.one = _OneLane()
+    h = one.host.numpy().view(np.uint64)
+    chunk0 = 0
+    h[0:4] = space.words()
+    h[4:8] = [0, 1, chunk0, 0]
+    h[8] = va & U64
+    h[9:12] = 0
+    s = _stream()
+    one.dev.copy_(one.host, non_blocking=True)
+    base = one.dev.data_ptr()
+    flags = (N.OUT_PFN if out_pfn else 0) | (N.HAS_TWO_STAGE if space.mode == N.TWO_STAGE else 0)
+    N.check(lib.pv_translate(dev_img.data_ptr(), image.nbytes, base, base + 32, 1, 1, base + 64, flags,
+                             base + 72, base + 88, base + 80, s.cuda_stream), "pv_translate")
+    one.out.copy_(one.dev[9:13], non_blocking=True)
+    s.synchronize()
+    o = one.out.numpy().view(np.uint64)
+    return int(o[2]) & 0xFFFFFFFF, int(o[0]), int(o[1])
+
+
+# ---- K1: batched translation -------------------------------------------------
+
+def build_segments(bounds: list[tuple[int, int, int]]) -> np.ndarray:
+    """(begin, end, space) runs -> pv_seg rows with chunk0 prefix sums."""
+    lib = N.load()
+    chunk = int(lib.pv_translate_chunk())
+    rows = []
+    c0 = 0
+    for begin, end, sp in bounds:
+        if end <= begin:
+            continue
+        rows.append((begin, end, c0, sp))
+        c0 += (end - begin + chunk - 1) // chunk
+    return np.array(rows, dtype=np.uint64).reshape(-1, 4), c0
+
+
+class TranslatePlan:
+    """Device-resident descriptors of a translate batch (reusable)."""
+
+    def __init__(self, spaces: list[Space], bounds: list[tuple[int, int, int]]):
+        segs, n_chunks = build_segments(bounds)
+        self.spaces = _to_dev(_i64([sp.words() for sp in spaces]).reshape(-1, 4))
+        self.segs = _to_dev(segs.view(np.int64))
+        self.n_segs = len(segs)
+        self.n_chunks = n_chunks
+        self.two = any(sp.mode == N.TWO_STAGE for sp in spaces)
+
+
+def translate_lanes(image, plan: TranslatePlan, vas, *, out_pfn: bool = False, out=None):
+    """Translate every lane of ``vas`` (int64 or int32 cuda tensor).
+
+    Returns ``(value int64, status int32, aux int64)`` device tensors, written
+    asynchronously on the current stream.  ``out`` may pass preallocated
+    tensors of the same shapes.
+    """
+    import torch
+
+    lib = N.lib()
+    dev_img = image.device()
+    n = vas.numel()
+    if out is None:
+        value = torch.empty(n, dtype=torch.int64, device="cuda")
+        status = torch.empty(n, dtype=torch.int32, device="cuda")
+        aux = torch.zeros(n, dtype=torch.int64, device="cuda")
+    else:
+        value, status, aux = out
+    flags = (N.VA32 if vas.dtype == torch.int32 else 0) | (N.OUT_PFN if out_pfn else 0)
+    if plan.two:
+        flags |= N.HAS_TWO_STAGE
+    N.check(lib.pv_translate(dev_img.data_ptr(), image.nbytes, plan.spaces.data_ptr(), plan.segs.data_ptr(),
+                             plan.n_segs, plan.n_chunks, vas.data_ptr(), flags, value.data_ptr(),
+                             status.data_ptr(), aux.data_ptr(), _stream().cuda_stream), "pv_translate")
+    return value, status, aux
+
+
+# ---- K4: FIFO cache state packing -------------------------------------------
+
+def pack_fifo(caches) -> np.ndarray:
+    """TranslationCache objects -> pv_fifo rows (int64 view)."""
+    rows = np.zeros((len(caches), N.FIFO_WORDS), dtype=np.uint64)
+    for i, c in enumerate(caches):
+        if not 1 <= c.capacity <= N.FIFO_MAX:
+            raise ValueError(f"device FIFO replay supports capacities 1..{N.FIFO_MAX}, got {c.capacity}")
+        entries = c.entries()
+        for j, (k, v) in enumerate(entries):
+            rows[i, j] = k & U64
+            rows[i, N.FIFO_MAX + j] = v & U64
+        rows[i, 2 * N.FIFO_MAX] = c.hits
+        rows[i, 2 * N.FIFO_MAX + 1] = c.misses
+        rows[i, 2 * N.FIFO_MAX + 2] = c.capacity | (len(entries) << 32)
+        rows[i, 2 * N.FIFO_MAX + 3] = 0  # head = 0
+    return rows.view(np.int64)
+
+
+def unpack_fifo(rows: np.ndarray, caches) -> None:
+    rows = rows.view(np.uint64)
+    for i, c in enumerate(caches):
+        cap = int(rows[i, 2 * N.FIFO_MAX + 2]) & 0xFFFFFFFF
+        length = int(rows[i, 2 * N.FIFO_MAX + 2]) >> 32
+        head = int(rows[i, 2 * N.FIFO_MAX + 3]) & 0xFFFFFFFF
+        entries = []
+        for j in range(length):
+            slot = (head + j) % cap
+            entries.append((int(rows[i, slot]), int(rows[i, N.FIFO_MAX + slot])))
+        c._load_state(entries, int(rows[i, 2 * N.FIFO_MAX]), int(rows[i, 2 * N.FIFO_MAX + 1]))
+
+
+def fifo_replay_lanes(vas, lane_idx, proc_off, fifo_dev, value, status) -> None:
+    import torch
+
+    lib = N.lib()
+    flags = N.VA32 if vas.dtype == torch.int32 else 0
+    N.check(lib.pv_fifo_replay(vas.data_ptr(), flags, lane_idx.data_ptr(), proc_off.data_ptr(),
+                               proc_off.numel() - 1, fifo_dev.data_ptr(), value.data_ptr(), status.data_ptr(),
+                               _stream().cuda_stream), "pv_fifo_replay")
+
+
+# ---- K2/K3: batched copy -----------------------------------------------------
+
+def page_spans(gva: np.ndarray, length: np.ndarray) -> np.ndarray:
+    gva = gva.astype(np.uint64)
+    length = length.astype(np.uint64)
+    span = np.zeros(len(gva), dtype=np.uint64)
+    nz = length > 0
+    span[nz] = ((gva[nz] + length[nz] - np.uint64(1)) >> np.uint64(PAGE_SHIFT)) - (gva[nz] >> np.uint64(PAGE_SHIFT)) \
+        + np.uint64(1)
+    return span
+
+
+class CopyPlan:
+    """Device-resident descriptors of a copy batch (reusable across runs)."""
+
+    def __init__(self, spaces: list[Space], ops: np.ndarray, *, fifo_groups=None):
+        """``ops``: uint64 rows (gva, len, buf_off, space).  ``fifo_groups``:
+        optional list of lists of op indices, one per process whose
+        TranslationCache applies (program order)."""
+        import torch
+
+        ops = np.ascontiguousarray(ops, dtype=np.uint64).reshape(-1, 4)
+        self.n_ops = len(ops)
+        spans = page_spans(ops[:, 0], ops[:, 1])
+        page_off = np.zeros(self.n_ops + 1, dtype=np.uint64)
+        np.cumsum(spans, out=page_off[1:])
+        self.n_pages = int(page_off[-1])
+        self.host_ops = ops
+        self.host_page_off = page_off
+        self.spaces = _to_dev(_i64([sp.words() for sp in spaces]).reshape(-1, 4))
+        self.ops = _to_dev(ops.view(np.int64))
+        self.page_off = _to_dev(page_off.view(np.int64))
+        np_ = max(self.n_pages, 1)
+        self.page_hpa = torch.empty(np_, dtype=torch.int64, device="cuda")
+        self.page_status = torch.empty(np_, dtype=torch.int32, device="cuda")
+        self.page_aux = torch.empty(np_, dtype=torch.int64, device="cuda")
+        self.first_bad = torch.empty(max(self.n_ops, 1), dtype=torch.int64, device="cuda")
+        self.results = torch.empty((max(self.n_ops, 1), 4), dtype=torch.int64, device="cuda")
+        self.conflict = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self.fifo_groups = fifo_groups
+        if fifo_groups is not None:
+            idx = np.concatenate([np.asarray(g, dtype=np.uint64) for g in fifo_groups]) if fifo_groups else \
+                np.zeros(0, np.uint64)
+            off = np.zeros(len(fifo_groups) + 1, dtype=np.uint64)
+            np.cumsum([len(g) for g in fifo_groups], out=off[1:])
+            self.fifo_idx = _to_dev(idx.view(np.int64)) if len(idx) else torch.zeros(1, dtype=torch.int64,
+                                                                                      device="cuda")
+            self.fifo_off = _to_dev(off.view(np.int64))
+
+
+def _owner_map(image):
+    """Per-image conflict stamp map (one u64 per page) and epoch counter."""
+    import torch
+
+    if getattr(image, "_owner", None) is None:
+        image._owner = torch.zeros(image.npages, dtype=torch.int64, device="cuda")
+        image._epoch = 0
+    image._epoch += 1
+    if image._epoch >= 1 << 24:
+        image._owner.zero_()
+        image._epoch = 1
+    return image._owner, image._epoch
+
+
+def copy_launch(image, plan: CopyPlan, direction: int, buf, *, fifo_dev=None, detect_conflicts: bool = True,
+                track_dirty: bool = True) -> None:
+    """Enqueue plan (+ FIFO replay) (+ conflict stamp) + exec on the current
+    stream.  Results land in ``plan.results`` / ``plan.conflict``."""
+    lib = N.lib()
+    dev_img = image.device()
+    s = _stream().cuda_stream
+    if plan.n_ops == 0:
+        return
+    plan.first_bad.fill_(-1)
+    plan.results.zero_()
+    plan.conflict.zero_()
+    if plan.n_pages:
+        N.check(lib.pv_copy_plan(dev_img.data_ptr(), image.nbytes, plan.spaces.data_ptr(), plan.ops.data_ptr(),
+                                 plan.n_ops, plan.page_off.data_ptr(), plan.n_pages, direction,
+                                 plan.page_hpa.data_ptr(), plan.page_status.data_ptr(), plan.page_aux.data_ptr(),
+                                 plan.first_bad.data_ptr(), None, 0, None, s), "pv_copy_plan")
+        if fifo_dev is not None:
+            N.check(lib.pv_copy_fifo_replay(plan.ops.data_ptr(), plan.page_off.data_ptr(), plan.fifo_idx.data_ptr(),
+                                            plan.fifo_off.data_ptr(), plan.fifo_off.numel() - 1,
+                                            fifo_dev.data_ptr(), image.nbytes, direction,
+                                            plan.page_hpa.data_ptr(), plan.page_status.data_ptr(),
+                                            plan.first_bad.data_ptr(), s), "pv_copy_fifo_replay")
+        abort = None
+        if direction == N.TO_GUEST and detect_conflicts:
+            owner, epoch = _owner_map(image)
+            N.check(lib.pv_copy_stamp(plan.page_off.data_ptr(), plan.n_ops, plan.n_pages, plan.page_hpa.data_ptr(),
+                                      plan.first_bad.data_ptr(), owner.data_ptr(), image.npages, epoch,
+                                      plan.conflict.data_ptr(), s), "pv_copy_stamp")
+            abort = plan.conflict.data_ptr()
+        dirty = image.dirty_map().data_ptr() if (direction == N.TO_GUEST and track_dirty) else None
+        N.check(lib.pv_copy_exec(dev_img.data_ptr(), image.nbytes, plan.ops.data_ptr(), plan.n_ops,
+                                 plan.page_off.data_ptr(), plan.n_pages, direction, plan.page_hpa.data_ptr(),
+                                 plan.page_status.data_ptr(), plan.page_aux.data_ptr(), plan.first_bad.data_ptr(),
+                                 buf.data_ptr(), buf.numel(), plan.results.data_ptr(), dirty, abort, s),
+                "pv_copy_exec")
+        if direction == N.TO_GUEST:
+            image.note_device_write()
+
+
+@dataclass
+class OpOutcome:
+    """Per-op outcome of a copy batch (decoded pv_op_result)."""
+
+    status: int
+    copied: int
+    value: int
+    aux: int
+    fail_page: int
+
+
+def decode_results(res: np.ndarray) -> list[OpOutcome]:
+    r = res.view(np.uint64)
+    out = []
+    for row in r:
+        out.append(OpOutcome(status=int(row[3]) & 0xFFFFFFFF, copied=int(row[0]), value=int(row[1]),
+                             aux=int(row[2]), fail_page=int(row[3]) >> 32))
+    return out
+
+
+def copy_ops(image, spaces: list[Space], ops: np.ndarray, direction: int, buf, *, caches=None, fifo_groups=None,
+             detect_conflicts: bool = True) -> list[OpOutcome]:
+    """Run a batch of copies with the reference's sequential semantics.
+
+    ``caches`` (with ``fifo_groups``) are host TranslationCache objects whose
+    state is replayed on the device and written back.  When the stamp pass
+    finds two pages of the batch writing one hpa page, the batch is re-run
+    one op at a time (in order), which reproduces last-writer-wins exactly.
+    """
+    import torch
+
+    plan = CopyPlan(spaces, ops, fifo_groups=fifo_groups if caches is not None else None)
+    fifo_dev = _to_dev(pack_fifo(caches)) if caches is not None else None
+    snapshot = fifo_dev.clone() if fifo_dev is not None else None
+    copy_launch(image, plan, direction, buf, fifo_dev=fifo_dev, detect_conflicts=detect_conflicts)
+    conflict = int(plan.conflict.item()) if (direction == N.TO_GUEST and detect_conflicts) else 0
+    if not conflict:
+        results = decode_results(plan.results.cpu().numpy())
+        if caches is not None:
+            unpack_fifo(fifo_dev.cpu().numpy(), caches)
+        return results
+    # Ordered re-run: one op (and, for ops whose own pages alias, one page) at
+    # a time.  The FIFO state restarts from the pre-batch snapshot.
+    fifo_dev = snapshot
+    ops = np.ascontiguousarray(ops, dtype=np.uint64).reshape(-1, 4)
+    proc_of = {}
+    if caches is not None:
+        for p, group in enumerate(fifo_groups):
+            for o in group:
+                proc_of[int(o)] = p
+    results = []
+    for i in range(len(ops)):
+        out = _copy_one_ordered(image, spaces, ops[i], direction, buf, fifo_dev, proc_of.get(i), caches)
+        results.append(out)
+    if caches is not None:
+        unpack_fifo(fifo_dev.cpu().numpy(), caches)
+    return results
+
+
+def _copy_one_ordered(image, spaces, op, direction, buf, fifo_dev, proc, caches) -> OpOutcome:
+    """One op, split into single-page sub-ops if its own pages alias."""
+    fifo_one = None
+    if caches is not None and proc is not None:
+        fifo_one = fifo_dev[proc:proc + 1]
+    groups = [[0]] if fifo_one is not None else None
+    plan = CopyPlan(spaces, op.reshape(1, 4), fifo_groups=groups)
+    copy_launch(image, plan, direction, buf, fifo_dev=fifo_one, detect_conflicts=True)
+    if not int(plan.conflict.item()):
+        return decode_results(plan.results.cpu().numpy())[0]
+    gva, length, buf_off, sp = (int(x) for x in op)
+    copied = 0
+    while copied < length:
+        cur = gva + copied
+        chunk = min(length - copied, PAGE_SIZE - (cur & PAGE_MASK))
+        sub = np.array([[cur, chunk, buf_off + copied, sp]], dtype=np.uint64)
+        splan = CopyPlan(spaces, sub, fifo_groups=groups)
+        copy_launch(image, splan, direction, buf, fifo_dev=fifo_one, detect_conflicts=False)
+        r = decode_results(splan.results.cpu().numpy())[0]
+        if r.status != N.ST_OK:
+            r.copied = copied
+            r.fail_page = (cur >> PAGE_SHIFT) - (gva >> PAGE_SHIFT)
+            return r
+        copied += chunk
+    return OpOutcome(N.ST_OK, length, 0, 0, 0)

@@ -1,0 +1,183 @@
+"""Physical-memory image: host mirror + HBM copy with page-granular coherence.
+
+The reference keeps host physical memory as one Python ``bytearray`` with
+guest memories as windows into it (memvirt.py:124-188, 433-480).  Here the
+bytes live twice:
+
+* ``host`` -- a numpy ``uint8`` array (lazily committed by the OS, so a
+  64 GiB image costs only the pages actually touched).  The control plane
+  (table editors, allocators zeroing frames, result pages, tests) reads and
+  writes it byte-exactly like the reference's bytearray.
+* ``device`` -- a flat ``torch.uint8`` tensor in HBM that every data-plane
+  kernel (translate / copy) reads and writes.
+
+Coherence is page-granular and lazy:
+
+* host writes mark pages in ``_host_dirty``; the next device operation
+  scatters exactly those pages into HBM (one H2D copy + ``pv_scatter_pages``);
+* kernels that write the image (``to_guest`` copies) set one byte per written
+  page in the device-side ``_dev_dirty`` map; the next host access downloads
+  the map and gathers exactly those pages back (``pv_gather_pages`` + one D2H).
+
+A timed data-plane loop therefore never synchronises with the host.
+"""
+
+from __future__ import annotations
+
+import threading
+
+import numpy as np
+
+from . import _native
+
+PAGE_SIZE = 4096
+PAGE_SHIFT = 12
+
+# Move at most this many pages per staging round trip (256 MiB).
+_STAGE_PAGES = 65536
+
+
+class MemoryImage:
+    """One physical memory (the reference's host ``bytearray``)."""
+
+    def __init__(self, nbytes: int, host: np.ndarray | None = None):
+        if nbytes % PAGE_SIZE:
+            raise ValueError("memory size must be a multiple of the page size")
+        self.nbytes = nbytes
+        self.npages = nbytes // PAGE_SIZE
+        self.host = np.zeros(nbytes, dtype=np.uint8) if host is None else host
+        self._host_dirty = np.zeros(self.npages, dtype=np.bool_)
+        self._host_dirty_any = False
+        # pages that may hold non-zero bytes (host or device side); frames
+        # that were never written need no work to be zeroed
+        self._maybe_nonzero = np.zeros(self.npages, dtype=np.bool_) if host is None else \
+            np.ones(self.npages, dtype=np.bool_)
+        self._dev = None          # torch.uint8 [nbytes]
+        self._dev_dirty = None    # torch.uint8 [npages]
+        self._dev_dirty_any = False
+        self._lock = threading.RLock()
+
+    @classmethod
+    def adopt(cls, buf) -> "MemoryImage":
+        """Wrap an existing bytes-like buffer (its contents are copied)."""
+        data = np.frombuffer(bytes(buf), dtype=np.uint8).copy()
+        img = cls(len(data), host=data)
+        img._host_dirty[:] = True
+        img._host_dirty_any = True
+        return img
+
+    def __len__(self) -> int:
+        return self.nbytes
+
+    # ---- host side --------------------------------------------------------
+    def host_for_read(self) -> np.ndarray:
+        if self._dev_dirty_any:
+            self.pull()
+        return self.host
+
+    def host_for_write(self, first: int, end: int) -> np.ndarray:
+        """Host array, after marking bytes [first, end) dirty."""
+        if self._dev_dirty_any:
+            self.pull()
+        if end > first:
+            span = slice(first >> PAGE_SHIFT, ((end - 1) >> PAGE_SHIFT) + 1)
+            self._host_dirty[span] = True
+            self._maybe_nonzero[span] = True
+            self._host_dirty_any = True
+        return self.host
+
+    def mark_host_pages(self, pages) -> None:
+        self._host_dirty[pages] = True
+        self._maybe_nonzero[pages] = True
+        self._host_dirty_any = True
+
+    def zero_pages(self, pages: np.ndarray) -> None:
+        """Zero whole pages (frame allocation); free for never-written ones."""
+        if self._dev_dirty_any:
+            self.pull()
+        pages = np.asarray(pages, dtype=np.int64)
+        hot = pages[self._maybe_nonzero[pages]]
+        if len(hot):
+            self.host.reshape(self.npages, PAGE_SIZE)[hot] = 0
+            self._host_dirty[hot] = True
+            self._host_dirty_any = True
+
+    # ---- device side ------------------------------------------------------
+    @property
+    def on_device(self) -> bool:
+        return self._dev is not None
+
+    def device(self):
+        """The HBM image, current with every host write (allocates lazily)."""
+        import torch
+
+        with self._lock:
+            if self._dev is None:
+                _native.lib()  # fail loudly without a GPU / the library
+                self._dev = torch.zeros(self.nbytes, dtype=torch.uint8, device="cuda")
+                self._dev_dirty = torch.zeros(self.npages, dtype=torch.uint8, device="cuda")
+            if self._host_dirty_any:
+                self.push()
+            return self._dev
+
+    def dirty_map(self):
+        """Device page map that writing kernels set (call after device())."""
+        return self._dev_dirty
+
+    def note_device_write(self) -> None:
+        self._dev_dirty_any = True
+
+    def push(self) -> None:
+        """Scatter host-dirty pages into HBM."""
+        import torch
+
+        with self._lock:
+            pages = np.flatnonzero(self._host_dirty)
+            if len(pages) == 0 or self._dev is None:
+                self._host_dirty_any = False
+                return
+            lib = _native.lib()
+            stream = torch.cuda.current_stream()
+            host2d = self.host.reshape(self.npages, PAGE_SIZE)
+            for s in range(0, len(pages), _STAGE_PAGES):
+                idx = pages[s:s + _STAGE_PAGES]
+                staging = torch.from_numpy(host2d[idx]).pin_memory()
+                src = staging.to("cuda", non_blocking=True)
+                pfns = torch.from_numpy(idx.astype(np.uint64).view(np.int64)).to("cuda", non_blocking=True)
+                _native.check(lib.pv_scatter_pages(self._dev.data_ptr(), self.nbytes, pfns.data_ptr(),
+                                                   len(idx), src.data_ptr(), stream.cuda_stream),
+                              "pv_scatter_pages")
+                stream.synchronize()  # staging buffers are freed at scope exit
+            self._host_dirty[:] = False
+            self._host_dirty_any = False
+
+    def pull(self) -> None:
+        """Gather device-written pages back into the host mirror."""
+        import torch
+
+        with self._lock:
+            if not self._dev_dirty_any or self._dev is None:
+                self._dev_dirty_any = False
+                return
+            lib = _native.lib()
+            stream = torch.cuda.current_stream()
+            dmap = self._dev_dirty.cpu().numpy()
+            pages = np.flatnonzero(dmap)
+            host2d = self.host.reshape(self.npages, PAGE_SIZE)
+            for s in range(0, len(pages), _STAGE_PAGES):
+                idx = pages[s:s + _STAGE_PAGES]
+                pfns = torch.from_numpy(idx.astype(np.uint64).view(np.int64)).to("cuda", non_blocking=True)
+                dst = torch.empty(len(idx) * PAGE_SIZE, dtype=torch.uint8, device="cuda")
+                _native.check(lib.pv_gather_pages(self._dev.data_ptr(), self.nbytes, pfns.data_ptr(), len(idx),
+                                                  dst.data_ptr(), stream.cuda_stream), "pv_gather_pages")
+                host2d[idx] = dst.cpu().numpy().reshape(len(idx), PAGE_SIZE)
+                self._maybe_nonzero[idx] = True
+            self._dev_dirty.zero_()
+            stream.synchronize()
+            self._dev_dirty_any = False
+
+    def sync(self) -> None:
+        """Make host and device agree (pull device writes, push host writes)."""
+        self.pull()
+        if self._dev is not None:
+            self.push()

@@ -1,0 +1,347 @@
+"""Scripted scenarios run identically against the reference and this package.
+
+Every function takes the module handles ``(mv, be, er)`` -- memvirt-like,
+backend-like (HAS access classes, GuestProcessRecord) and errors-like -- so
+``tests/golden/gen_golden.py`` can run them on the reference
+(``devfsim.memvirt`` / ``devfsim.backend`` / ``devfsim.errors``, imported
+from /root/reference in the build container only) to produce the committed
+fixtures, and the tests can run them on ``paper_1304_3771_b200`` and compare.
+
+Each scenario has a *build* phase (control plane only: table construction,
+allocators, raw word edits -- runs without a GPU) and a *query* phase (data
+plane: walks, translations, copies -- needs the GPU for this package).
+Outcomes are JSON-able lists.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import random
+import struct
+
+import numpy as np
+
+BUF = 0x2000_0000
+PAGE = 4096
+
+
+class _Guest:
+    """Stand-in for devfsim.guest.Guest: GuestProcessRecord reads .id and
+    .mem_mode only (backend.py:267-286)."""
+
+    def __init__(self, gid: int, mem_mode: str):
+        self.id = gid
+        self.mem_mode = mem_mode
+
+
+def outcome(fn, er):
+    try:
+        return ["ok", int(fn())]
+    except er.PageFault as f:
+        return ["fault", int(f.va), int(f.level), int(f.bytes_copied)]
+    except er.TrapFixupFailed:
+        return ["fixup_failed"]
+    except er.TrapExit as t:
+        return ["trap", int(t.va), int(t.level), int(t.node_pfn), int(t.index)]
+    except er.OutOfRange:
+        return ["oor"]
+    except struct.error:
+        return ["struct"]
+
+
+def image_bytes(mem) -> bytes:
+    """Whole host image as bytes (works for both implementations)."""
+    return mem.read(0, mem.size_bytes)
+
+
+def sparse_pages(raw: bytes):
+    arr = np.frombuffer(raw, dtype=np.uint8).reshape(-1, PAGE)
+    nz = np.flatnonzero(arr.any(axis=1))
+    return nz.astype(np.uint32), arr[nz].copy()
+
+
+def sha(raw: bytes) -> str:
+    return hashlib.sha256(raw).hexdigest()
+
+
+# ---- scenario "spec": the spec's known answers (test_memvirt.py:111-128)
+
+def spec_build(mv, be, er):
+    mem = mv.PhysMem(64 * PAGE)
+    alloc = mv.FrameAllocator(mem, 16, 32)
+    root = mv.PageTableRoot(mv.TableKind.GUEST, alloc.alloc())
+    ed = mv.TableEditor(mem, root, alloc.alloc)
+    for page in range(8):
+        ed.map(page * PAGE, page)
+    mem2 = mv.PhysMem(64 * PAGE)
+    # hand-built chain: gva page 5 -> gpa page 9 (root 1, mid 2, leaf 3)
+    mem2.write_word(1, 0, (2 << 12) | 0x3)
+    mem2.write_word(2, 0, (3 << 12) | 0x3)
+    mem2.write_word(3, 5, (9 << 12) | 0x3)
+    return dict(mem=mem, root=root, mem2=mem2, root2=mv.PageTableRoot(mv.TableKind.GUEST, 1))
+
+
+def spec_query(w, mv, be, er):
+    out = []
+    out.append(outcome(lambda: mv.walk_guest(0x0000_3004, w["root"], w["mem"]), er))
+    out.append(outcome(lambda: mv.walk_guest(0x0000_5010, w["root2"], w["mem2"]), er))
+    out.append(outcome(lambda: mv.walk_guest(0x0020_0000, w["root2"], w["mem2"]), er))
+    out.append(outcome(lambda: mv.walk_guest(0x0000_6000, w["root2"], w["mem2"]), er))
+    out.append(outcome(lambda: mv.walk_guest(0xDEAD_B000, mv.PageTableRoot(mv.TableKind.GUEST, 9),
+                                             w["mem2"]), er))
+    return out
+
+
+# ---- scenario "walks": shadow + TDP guests, driver maps, corrupted entries
+
+def walks_build(mv, be, er):
+    memv = mv.MemoryVirtualizer()
+    g0 = memv.add_guest(0, "shadow")
+    g1 = memv.add_guest(1, "tdp")
+    p0 = memv.create_process(g0)
+    p1 = memv.create_process(g1)
+    rng = random.Random(1304)
+    for sp in (p0, p1):
+        memv.map_region(sp, BUF, 40)
+        memv.map_region(sp, BUF + 40 * PAGE, 30)        # extends existing nodes
+        order = list(range(64))
+        rng.shuffle(order)
+        for pg in order:
+            memv.map_process_page(sp, 0x3000_0000 + pg * PAGE)
+        memv.map_region(sp, 0x4020_0000 - 3 * PAGE, 9)  # crosses a mid boundary
+    dev = memv.host_alloc.alloc()
+    memv.host_mem.write(dev * PAGE, b"\xD5" * 64)
+    memv.map_page_into_guest(p0, 0x5000_0000, dev << 12, "shadow")
+    memv.map_page_into_guest(p1, 0x5000_0000, dev << 12, "tdp")
+    sh = mv.TableEditor(memv.host_mem, p0.shadow_root, memv.host_alloc.alloc)
+    sh.set_leaf_state(BUF + 3 * PAGE, mv.EntryState.TRAPPING)
+    sh.set_leaf_state(BUF + 5 * PAGE, mv.EntryState.NOT_PRESENT)
+    gp1 = mv.TableEditor(g1.mem, p1.guest_root, g1.os_alloc.alloc)
+    gp1.set_leaf_state(BUF + 7 * PAGE, mv.EntryState.NOT_PRESENT)
+    # guest PTE whose gpa lies beyond the 16 MiB slot: TDP-stage fault
+    gp1.map(0x6000_0000, (32 << 20) >> 12)
+    # guest PTE whose gpa is inside the slot but beyond... page 0x800 of the slot
+    gp1.map(0x6000_1000, 0x800)
+    # shadow top entry 2 pointing at a node far past the image: struct.error
+    memv.host_mem.write_word(p0.shadow_root.root_pfn, 2, (0xF_FFFF << 12) | 0x3)
+    # a trapping top-level entry in a second shadow process
+    p2 = memv.create_process(g0)
+    memv.map_region(p2, BUF, 4)
+    memv.host_mem.write_word(p2.shadow_root.root_pfn, 0,
+                             memv.host_mem.read_word(p2.shadow_root.root_pfn, 0) | 0x4)
+    hybrid = mv.HybridTopLevel(memv.host_mem, memv.host_alloc)
+    hroot = hybrid.build(p0.shadow_root, memv.host_kernel_root)
+    return dict(memv=memv, g0=g0, g1=g1, p0=p0, p1=p1, p2=p2, hroot=hroot, dev=dev)
+
+
+def walk_vas(seed: int = 77, n_random: int = 120) -> list[int]:
+    rng = random.Random(seed)
+    vas = [BUF + i * PAGE + rng.randrange(PAGE) for i in range(80)]
+    vas += [0x3000_0000 + i * PAGE + rng.randrange(PAGE) for i in range(0, 70, 3)]
+    vas += [0x4020_0000 + i * PAGE - 3 * PAGE + 5 for i in range(10)]
+    vas += [0x5000_0000, 0x5000_0FFF, 0x6000_0010, 0x6000_1234, 0x7000_0000, 0x8000_0000, 0x8123_4567,
+            0xC000_0000, 0xC000_0000 + 63 * PAGE + 7, 0xC004_0000, 0xFFFF_FFFF, 0]
+    vas += [(1 << 32) | (BUF + 9 * PAGE + 1), (7 << 40) | (BUF + 11 * PAGE)]
+    vas += [rng.randrange(1 << 32) for _ in range(n_random)]
+    return vas
+
+
+def walks_query(w, mv, be, er):
+    memv, p0, p1, p2 = w["memv"], w["p0"], w["p1"], w["p2"]
+    g0, g1 = w["g0"], w["g1"]
+    host = memv.host_mem
+    vas = walk_vas()
+    res = {}
+    res["walk_shadow"] = [outcome(lambda: mv.walk(host, p0.shadow_root.root_pfn, va), er) for va in vas]
+    res["walk_shadow_p2"] = [outcome(lambda: mv.walk(host, p2.shadow_root.root_pfn, va), er) for va in vas[:40]]
+    res["walk_guest0"] = [outcome(lambda: mv.walk_guest(va, p0.guest_root, g0.mem), er) for va in vas]
+    res["walk_guest1"] = [outcome(lambda: mv.walk_guest(va, p1.guest_root, g1.mem), er) for va in vas]
+    gpas = [v & 0x3FF_FFFF for v in vas] + [16 << 20, (16 << 20) - 1, 1 << 33]
+    res["walk_tdp"] = [outcome(lambda: mv.walk(host, g1.tdp_root.root_pfn, gpa), er) for gpa in gpas]
+    res["hybrid"] = [outcome(lambda: mv.resolve_hybrid(va, w["hroot"], host), er) for va in vas]
+    for name, sp in (("p0", p0), ("p1", p1)):
+        unc = memv.translator(sp, use_cache=False)
+        res[f"translate_{name}"] = [outcome(lambda: unc.translate(va), er) for va in vas]
+        cache = mv.TranslationCache()
+        tr = memv.translator(sp, cache)
+        seq = vas[:60] + vas[:60] + [BUF + (i % 12) * PAGE + i for i in range(200)]
+        res[f"cached_{name}"] = [outcome(lambda: tr.translate(va), er) for va in seq]
+        res[f"cached_{name}_state"] = [cache.hits, cache.misses, [list(e) for e in cache.entries()]]
+    res["gpa_to_hpa"] = [outcome(lambda: memv.gpa_to_hpa(g, 1), er) for g in gpas[:40]]
+    return res
+
+
+# ---- scenario "copies": user-buffer copies through every translator kind
+
+def copies_build(mv, be, er):
+    memv = mv.MemoryVirtualizer()
+    g0 = memv.add_guest(0, "shadow")
+    g1 = memv.add_guest(1, "tdp")
+    p0 = memv.create_process(g0)
+    p1 = memv.create_process(g1)
+    for sp in (p0, p1):
+        memv.map_region(sp, BUF, 24)
+        memv.map_region(sp, 0x3000_0000, 3)   # 4th page unmapped
+    sh = mv.TableEditor(memv.host_mem, p0.shadow_root, memv.host_alloc.alloc)
+    sh.set_leaf_state(BUF + 10 * PAGE, mv.EntryState.TRAPPING)
+    r0 = be.GuestProcessRecord(_Guest(0, "shadow"), p0, memv)
+    r1 = be.GuestProcessRecord(_Guest(1, "tdp"), p1, memv)
+    return dict(memv=memv, p0=p0, p1=p1, r0=r0, r1=r1)
+
+
+COPY_CASES = [  # (gva, length)
+    (BUF, 3 * PAGE), (BUF + 0x800, 12 * 1024), (BUF + 0x123, 5000), (BUF + 4095, 2), (BUF, 0),
+    (BUF + 20 * PAGE + 100, 6 * PAGE), (0x3000_0000 + 17, 4 * PAGE), (BUF + 9 * PAGE, 3 * PAGE),
+    (BUF + 2 * PAGE + 1, 1), (0x7000_0000, 100), (BUF + 12 * PAGE + 3, 4 * PAGE + 9),
+]
+
+
+def _payload(n: int, seed: int) -> bytes:
+    return random.Random(seed).randbytes(n)
+
+
+def copies_query(w, mv, be, er):
+    memv, p0, p1 = w["memv"], w["p0"], w["p1"]
+    res = {}
+    for name, sp in (("p0", p0), ("p1", p1)):
+        for cached in (False, True):
+            cache = mv.TranslationCache()
+            tr = memv.translator(sp, cache, use_cache=cached)
+            rows = []
+            for i, (gva, n) in enumerate(COPY_CASES):
+                data = _payload(n, 1000 + i)
+                rows.append(outcome(lambda: mv.copy_user_buffer("to_guest", gva, n, data, translator=tr,
+                                                                host_mem=memv.host_mem), er))
+                back = bytearray(n)
+                o = outcome(lambda: mv.copy_user_buffer("from_guest", gva, n, back, translator=tr,
+                                                        host_mem=memv.host_mem), er)
+                rows.append(o + [sha(bytes(back))])
+            rows.append([cache.hits, cache.misses, [list(e) for e in cache.entries()]])
+            res[f"{name}_{'cached' if cached else 'uncached'}"] = rows
+    # access classes: software (cached) and hardware (hybrid + shim) HAS
+    for name, rec in (("sw0", w["r0"]), ("sw1", w["r1"])):
+        acc = be.SoftwareHasAccess(rec, memv)
+        rows = []
+        for i, (gva, n) in enumerate(COPY_CASES[:8]):
+            data = _payload(n, 2000 + i)
+            rows.append(outcome(lambda: acc.copy_to_user(gva, data), er))
+            rows.append(outcome(lambda: int.from_bytes(hashlib.sha256(acc.copy_from_user(gva, n)).digest()[:8],
+                                                       "little"), er))
+        rows.append([rec.translation_cache.hits, rec.translation_cache.misses])
+        res[name] = rows
+    acc = be.HardwareHasAccess(w["r0"], memv)
+    rows = []
+    for i, (gva, n) in enumerate(COPY_CASES):
+        data = _payload(n, 3000 + i)
+        rows.append(outcome(lambda: acc.copy_to_user(gva, data), er))
+        rows.append(outcome(lambda: int.from_bytes(hashlib.sha256(acc.copy_from_user(gva, n)).digest()[:8],
+                                                   "little"), er))
+    rows.append([w["r0"].hw_translations])
+    res["hw0"] = rows
+    res["image_sha"] = sha(image_bytes(memv.host_mem))
+    return res
+
+
+# ---- scenario "c01": acceptance criterion 1 (test_acceptance.py:90-127)
+
+def c01_build(mv, be, er):
+    rng = random.Random(101)
+    memv = mv.MemoryVirtualizer()
+    guest = memv.add_guest(0, "shadow")
+    space = memv.create_process(guest)
+    ed = mv.TableEditor(guest.mem, space.guest_root, guest.os_alloc.alloc)
+    pages = rng.sample(range(mv.KERNEL_BASE // PAGE), 1500)
+    for page in pages:
+        ed.map(page * PAGE, rng.randrange(guest.mem.n_pages))
+    samples = [page * PAGE + rng.randrange(PAGE) for page in rng.choices(pages, k=5000)]
+    samples += [rng.randrange(2 ** 32) for _ in range(5000)]
+    return dict(memv=memv, guest=guest, space=space, samples=samples)
+
+
+def c01_query(w, mv, be, er):
+    return [outcome(lambda: mv.walk_guest(va, w["space"].guest_root, w["guest"].mem), er) for va in w["samples"]]
+
+
+# ---- scenario "c03": hybrid merge (test_acceptance.py:184-224), first trials
+
+def c03_build(mv, be, er, trials: int = 4):
+    rng = random.Random(303)
+    worlds = []
+    for _ in range(trials):
+        memv = mv.MemoryVirtualizer()
+        memv.add_guest(0, "shadow")
+        space = memv.create_process(memv.guest_memory(0))
+        se = mv.TableEditor(memv.host_mem, space.shadow_root, memv.host_alloc.alloc)
+        user = rng.sample(range(mv.KERNEL_BASE // PAGE), 30)
+        trapping = set(rng.sample(user, 5))
+        for page in user:
+            st = mv.EntryState.TRAPPING if page in trapping else mv.EntryState.PRESENT
+            se.map(page * PAGE, memv.host_alloc.alloc(), state=st)
+        host_root = mv.PageTableRoot(mv.TableKind.HOST, memv.host_alloc.alloc())
+        he = mv.TableEditor(memv.host_mem, host_root, memv.host_alloc.alloc)
+        kernel = rng.sample(range(mv.KERNEL_BASE // PAGE, 2 ** 20), 30)
+        for page in kernel:
+            he.map(page * PAGE, memv.host_alloc.alloc())
+        hybrid = mv.HybridTopLevel(memv.host_mem, memv.host_alloc).build(space.shadow_root, host_root)
+        vas = [p * PAGE + rng.randrange(PAGE) for p in rng.choices(user + kernel, k=600)]
+        vas += [rng.randrange(2 ** 32) for _ in range(450)]
+        worlds.append(dict(memv=memv, space=space, host_root=host_root, hybrid=hybrid, vas=vas))
+    return worlds
+
+
+def c03_query(worlds, mv, be, er):
+    out = []
+    for w in worlds:
+        out.append([outcome(lambda: mv.resolve_hybrid(va, w["hybrid"], w["memv"].host_mem), er) for va in w["vas"]])
+    return out
+
+
+# ---- scenario "fifo": cache law traces (test_memvirt.py:509-521; c02)
+
+def fifo_traces():
+    rng = random.Random(42)
+    traces = []
+    for _ in range(200):
+        traces.append([rng.randrange(16) for _ in range(rng.randrange(5, 60))])
+    rng = random.Random(202)
+    for _ in range(300):
+        traces.append([rng.randrange(18) for _ in range(rng.randrange(3, 50))])
+    return traces
+
+
+def fifo_query(mv):
+    out = []
+    for tr in fifo_traces():
+        c = mv.TranslationCache()
+        for key in tr:
+            if c.lookup(key) is None:
+                c.insert(key, key * 3 + 1)
+        out.append([c.hits, c.misses, [list(e) for e in c.entries()]])
+    return out
+
+
+# ---- C1 (BASELINE config 1, reference geometry): full-size table build
+
+C1_HOST = 128 << 20
+C1_GUEST = 96 << 20
+C1_GVA = 0x1000_0000
+C1_PAGES = 16384
+
+
+def c1_build(mv, be, er, mode: str):
+    memv = mv.MemoryVirtualizer(host_bytes=C1_HOST)
+    guest = memv.add_guest(0, mode, C1_GUEST)
+    space = memv.create_process(guest)
+    order = list(range(C1_PAGES))
+    random.Random(1304).shuffle(order)
+    if hasattr(memv, "map_pages"):
+        memv.map_pages(space, [C1_GVA + p * PAGE for p in order])
+    else:
+        for p in order:
+            memv.map_process_page(space, C1_GVA + p * PAGE)
+    return dict(memv=memv, guest=guest, space=space)
+
+
+def c1_vas(n: int = 1_000_000) -> np.ndarray:
+    rng = random.Random(3771)
+    return np.array([C1_GVA + rng.randrange(64 << 20) for _ in range(n)], dtype=np.uint64)

@@ -1,0 +1,183 @@
+"""Host-side control plane vs the reference: byte-identical memory images.
+
+Table construction (allocators, TableEditor, MemoryVirtualizer, the bulk
+mapper, the hybrid merge) runs on the host mirror without a GPU; every
+scenario's build phase must leave exactly the bytes the reference left
+(golden SHA-256 over the whole host image).  CPU only.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import random
+
+import numpy as np
+import pytest
+
+import scenarios as S
+from conftest import load_json, status_outcome
+from oracle import oracle as O
+from paper_1304_3771_b200 import errors as er
+from paper_1304_3771_b200 import has as be
+from paper_1304_3771_b200 import memvirt as mv
+
+
+def sha_of(mem) -> str:
+    return S.sha(S.image_bytes(mem))
+
+
+def test_spec_build():
+    w = S.spec_build(mv, be, er)
+    g = load_json("spec.json")
+    assert sha_of(w["mem"]) == g["mem_sha"]
+    assert sha_of(w["mem2"]) == g["mem2_sha"]
+
+
+def test_walks_build_bytes():
+    w = S.walks_build(mv, be, er)
+    assert sha_of(w["memv"].host_mem) == load_json("walks.json")["build_sha"]
+
+
+def test_copies_build_bytes():
+    w = S.copies_build(mv, be, er)
+    assert sha_of(w["memv"].host_mem) == load_json("copies.json")["build_sha"]
+
+
+def test_c01_build_bytes():
+    w = S.c01_build(mv, be, er)
+    assert sha_of(w["memv"].host_mem) == load_json("c01.json")["image_sha"]
+
+
+def test_c03_build_bytes():
+    worlds = S.c03_build(mv, be, er)
+    for i, w in enumerate(worlds):
+        assert sha_of(w["memv"].host_mem) == load_json(f"c03_{i}.json")["image_sha"]
+
+
+@pytest.mark.parametrize("mode", ["shadow", "tdp"])
+def test_c1_bulk_build_and_oracle(mode):
+    """Full-size BASELINE config 1 (16,384 shuffled pages) built by the
+    vectorised mapper is byte-identical to the reference's per-page loop, and
+    the oracle on it reproduces the reference's translations."""
+    w = S.c1_build(mv, be, er, mode)
+    g = load_json(f"c1_{mode}.json")
+    raw = S.image_bytes(w["memv"].host_mem)
+    assert S.sha(raw) == g["image_sha"]
+    img = np.frombuffer(raw, dtype=np.uint8)
+    if mode == "shadow":
+        sp = O.space(0, g["shadow_root"])
+    else:
+        sp = O.space(g["guest_base"], g["guest_root"], g["tdp_root"], 2)
+    vas = S.c1_vas(g["n_vas"])
+    v, s, a = O.translate(img, sp, vas, threads=0)
+    got = [status_outcome(int(s[i]), int(v[i]), int(a[i]), int(vas[i])) for i in range(len(vas))]
+    assert got == g["expected"]
+
+
+def test_fifo_law_traces():
+    assert S.fifo_query(mv) == load_json("fifo.json")["expected"]
+
+
+def test_codec_roundtrip_and_precedence():
+    for state in mv.EntryState:
+        for w in (False, True):
+            e = mv.PageTableEntry(state, 0xABCDE, w)
+            assert mv.decode_entry(mv.encode_entry(e)) == e
+    assert mv.decode_entry(0x5).state is mv.EntryState.TRAPPING   # T wins over P
+    assert mv.decode_entry(0x2).state is mv.EntryState.NOT_PRESENT
+    assert mv.split_va((1 << 32) | 0x4020_1234) == mv.split_va(0x4020_1234)
+
+
+def test_physmem_windows_and_bounds():
+    host = mv.PhysMem(8 * 4096)
+    win = mv.PhysMem(2 * 4096, backing=host.backing, base=4 * 4096)
+    win.write(8, b"\xAA\xBB")
+    assert host.read(4 * 4096 + 8, 2) == b"\xAA\xBB"
+    with pytest.raises(er.OutOfRange):
+        win.read(2 * 4096 - 1, 2)
+    with pytest.raises(ValueError):
+        mv.PhysMem(4097)
+    assert len(host.dump_hex(0).splitlines()) == 128
+
+
+def test_allocator_fifo_order_with_frees():
+    mem = mv.PhysMem(64 * 4096)
+    a = mv.FrameAllocator(mem, 4, 6)
+    first = [a.alloc() for _ in range(3)]
+    a.free(first[1])
+    rest = [a.alloc() for _ in range(4)]
+    assert first == [4, 5, 6] and rest == [7, 8, 9, 5]
+    with pytest.raises(er.PoolExhausted):
+        a.alloc()
+
+
+def test_alloc_zeroes_reused_frames():
+    mem = mv.PhysMem(16 * 4096)
+    a = mv.FrameAllocator(mem, 1, 2)
+    p = a.alloc()
+    mem.write(p * 4096, b"\x77" * 4096)
+    a.free(p)
+    a.alloc()
+    q = a.alloc()
+    assert q == p and mem.read(p * 4096, 4096) == bytes(4096)
+
+
+def test_bulk_mapper_matches_loop_on_random_pages():
+    """Vectorised map_pages == per-page map_process_page, on random page
+    sets with pre-existing nodes, for both memory modes."""
+    for mode in ("shadow", "tdp"):
+        for seed in range(3):
+            rng = random.Random(seed)
+            worlds = []
+            for bulk in (False, True):
+                memv = mv.MemoryVirtualizer()
+                g = memv.add_guest(0, mode)
+                sp = memv.create_process(g)
+                memv.map_process_page(sp, 0x2000_0000)
+                pages = rng.sample(range(0x40000, 0x40000 + 6000), 700) if not bulk else pages
+                gvas = [p * 4096 for p in pages]
+                if bulk:
+                    memv.map_pages(sp, gvas)
+                else:
+                    for gva in gvas:
+                        memv.map_process_page(sp, gva)
+                worlds.append(sha_of(memv.host_mem))
+            assert worlds[0] == worlds[1]
+
+
+def test_bulk_mapper_falls_back_on_conflicts():
+    memv = mv.MemoryVirtualizer()
+    g = memv.add_guest(0, "shadow")
+    sp = memv.create_process(g)
+    memv.map_region(sp, 0x2000_0000, 4)
+    with pytest.raises(er.AlreadyMapped):
+        memv.map_region(sp, 0x2000_0000 - 2 * 4096, 4)   # overlaps page 0
+    # the first two pages of the failing region were mapped before the error
+    ed = mv.TableEditor(g.mem, sp.guest_root, g.os_alloc.alloc)
+    assert ed.is_mapped(0x2000_0000 - 4096) and ed.is_mapped(0x2000_0000 - 2 * 4096)
+
+
+def test_hybrid_rebuild_reuses_root():
+    memv = mv.MemoryVirtualizer()
+    g = memv.add_guest(0, "shadow")
+    sp = memv.create_process(g)
+    memv.map_region(sp, 0x2000_0000, 2)
+    h = mv.HybridTopLevel(memv.host_mem, memv.host_alloc)
+    r1 = h.build(sp.shadow_root, memv.host_kernel_root)
+    assert h.build(sp.shadow_root, memv.host_kernel_root) is r1
+    memv.map_region(sp, 0x8000_0000, 1)
+    r2 = h.build(sp.shadow_root, memv.host_kernel_root)
+    assert r2 is r1
+    assert memv.host_mem.read_word(r1.root_pfn, 2) == memv.host_mem.read_word(sp.shadow_root.root_pfn, 2)
+    with pytest.raises(er.TdpUnsupported):
+        t = memv.add_guest(1, "tdp")
+        h.build(t.tdp_root, memv.host_kernel_root)
+
+
+def test_has_records_without_gpu():
+    memv = mv.MemoryVirtualizer()
+    g = memv.add_guest(0, "tdp")
+    sp = memv.create_process(g)
+    rec = be.GuestProcessRecord(S._Guest(0, "tdp"), sp, memv)
+    with pytest.raises(er.TdpUnsupported):
+        be.HardwareHasAccess(rec, memv)

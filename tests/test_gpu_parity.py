@@ -1,0 +1,252 @@
+"""Data-plane parity on the GPU: this package's CUDA path vs the reference.
+
+Two anchors:
+* the golden fixtures recorded from the reference itself (every outcome of
+  the scripted scenarios, including exceptions, cache counters and the
+  final image digest);
+* the C oracle (pinned to the same fixtures by tests/test_oracle.py) at the
+  BASELINE config sizes, compared lane by lane and byte by byte.
+All results must be bit-exact.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import random
+
+import numpy as np
+import pytest
+import torch
+
+import scenarios as S
+from conftest import load_json, status_outcome
+from oracle import oracle as O
+from paper_1304_3771_b200 import _native as N
+from paper_1304_3771_b200 import dataplane as dp
+from paper_1304_3771_b200 import errors as er
+from paper_1304_3771_b200 import has as be
+from paper_1304_3771_b200 import memvirt as mv
+
+pytestmark = pytest.mark.gpu
+
+
+def test_spec_known_answers(cuda):
+    w = S.spec_build(mv, be, er)
+    assert S.spec_query(w, mv, be, er) == load_json("spec.json")["expected"]
+
+
+def test_walks_scenario(cuda):
+    w = S.walks_build(mv, be, er)
+    got = S.walks_query(w, mv, be, er)
+    exp = load_json("walks.json")["expected"]
+    for key in exp:
+        assert got[key] == exp[key], key
+
+
+def test_copies_scenario(cuda):
+    w = S.copies_build(mv, be, er)
+    got = S.copies_query(w, mv, be, er)
+    exp = load_json("copies.json")["expected"]
+    for key in exp:
+        assert got[key] == exp[key], key
+
+
+def test_c01_single_and_batch(cuda):
+    w = S.c01_build(mv, be, er)
+    g = load_json("c01.json")
+    assert S.c01_query(w, mv, be, er) == g["expected"]
+    # the same 10,000 addresses as one device batch
+    space = dp.Space(w["guest"].mem.base, w["space"].guest_root.root_pfn)
+    plan = dp.TranslatePlan([space], [(0, len(w["samples"]), 0)])
+    vas = torch.tensor(np.array(w["samples"], dtype=np.uint64).view(np.int64), device="cuda")
+    v, s, a = dp.translate_lanes(w["memv"].host_mem.backing, plan, vas)
+    v = v.cpu().numpy().view(np.uint64)
+    s = s.cpu().numpy().view(np.uint32)
+    a = a.cpu().numpy().view(np.uint64)
+    got = [status_outcome(int(s[i]), int(v[i]), int(a[i]), w["samples"][i]) for i in range(len(s))]
+    assert got == g["expected"]
+
+
+def test_c03_hybrid(cuda):
+    worlds = S.c03_build(mv, be, er)
+    exp = [load_json(f"c03_{i}.json")["expected"] for i in range(len(worlds))]
+    assert S.c03_query(worlds, mv, be, er) == exp
+
+
+@pytest.fixture(scope="module", params=["shadow", "tdp"])
+def c1(request, cuda):
+    w = S.c1_build(mv, be, er, request.param)
+    g = load_json(f"c1_{request.param}.json")
+    host = w["memv"].host_mem
+    raw = np.frombuffer(S.image_bytes(host), dtype=np.uint8).copy()
+    assert hashlib.sha256(raw.tobytes()).hexdigest() == g["image_sha"]
+    tr = w["memv"].translator(w["space"], use_cache=False)
+    sp = tr.device_space
+    osp = O.space(sp.s1_base, sp.s1_root_pfn, sp.s2_root_pfn, sp.mode)
+    return dict(w=w, g=g, raw=raw, tr=tr, osp=osp, mode=request.param)
+
+
+def test_c1_translate_1m_vs_oracle_and_reference(c1):
+    vas = S.c1_vas()
+    hpa, st, aux = c1["tr"].translate_batch(vas)
+    v, s, a = O.translate(c1["raw"], c1["osp"], vas, threads=0)
+    assert np.array_equal(st, s)
+    assert np.array_equal(hpa, v)
+    assert np.array_equal(aux, a)
+    n = c1["g"]["n_vas"]
+    got = [status_outcome(int(st[i]), int(hpa[i]), int(aux[i]), int(vas[i])) for i in range(n)]
+    assert got == c1["g"]["expected"]
+
+
+def test_c1_translate_cached_fifo_replay(c1):
+    w = c1["w"]
+    vas = S.c1_vas(200_000)
+    # mix in a looped 8-page phase so hits and evictions both happen
+    loop = np.array([S.C1_GVA + (i % 8) * 4096 + i % 4096 for i in range(20_000)], dtype=np.uint64)
+    vas = np.concatenate([vas[:100_000], loop, vas[100_000:]])
+    cache = mv.TranslationCache()
+    tr = w["memv"].translator(w["space"], cache)
+    hpa, st, aux = tr.translate_batch(vas)
+    ocache = O.new_cache()
+    v, s, a = O.translate_cached(c1["raw"], c1["osp"], vas, ocache)
+    assert np.array_equal(st, s) and np.array_equal(hpa, v)
+    entries, hits, misses = O.cache_state(ocache)
+    assert (cache.hits, cache.misses) == (hits, misses)
+    assert cache.entries() == entries
+
+
+def _c1_copy(c1, gva, length, *, cached: bool, direction: str):
+    w = c1["w"]
+    data = np.frombuffer(random.Random(3771).randbytes(length), dtype=np.uint8)
+    img_ref = c1["raw"].copy()
+    cache = mv.TranslationCache()
+    tr = w["memv"].translator(w["space"], cache, use_cache=cached)
+    host = w["memv"].host_mem
+    before = np.frombuffer(S.image_bytes(host), dtype=np.uint8).copy()
+    if direction == "to_guest":
+        n = mv.copy_user_buffer("to_guest", gva, length, data.tobytes(), translator=tr, host_mem=host)
+        oc = O.new_cache() if cached else None
+        res = O.copy(before, O.space(*[int(x) for x in c1["osp"]]).reshape(1, 4),
+                     np.array([[gva, length, 0, 0]], np.uint64), data.copy(), 0,
+                     caches=oc, op_cache=[0] if cached else None)
+        assert n == length and int(res[0, 0]) == length
+        after = np.frombuffer(S.image_bytes(host), dtype=np.uint8)
+        assert np.array_equal(after, before)
+        if cached:
+            entries, hits, misses = O.cache_state(oc)
+            assert (cache.hits, cache.misses, cache.entries()) == (hits, misses, entries)
+    else:
+        back = bytearray(length)
+        n = mv.copy_user_buffer("from_guest", gva, length, back, translator=tr, host_mem=host)
+        out = np.zeros(length, np.uint8)
+        O.copy(before, O.space(*[int(x) for x in c1["osp"]]).reshape(1, 4),
+               np.array([[gva, length, 0, 0]], np.uint64), out, 1)
+        assert n == length and bytes(back) == out.tobytes()
+    del img_ref
+
+
+@pytest.mark.parametrize("cached", [False, True])
+def test_c1_copy_to_user_64mib(c1, cached):
+    _c1_copy(c1, S.C1_GVA, 64 << 20, cached=cached, direction="to_guest")
+    _c1_copy(c1, S.C1_GVA + 0x800, (64 << 20) - 4096, cached=cached, direction="to_guest")
+
+
+def test_c1_copy_from_user_64mib(c1):
+    _c1_copy(c1, S.C1_GVA + 0x123, (64 << 20) - 8192, cached=False, direction="from_guest")
+
+
+def _corrupt(memv, space, mode, seed=1304):
+    """C4: 20% of leaf PTEs NOT_PRESENT, 10% TRAPPING (shadow only)."""
+    rng = random.Random(seed)
+    if mode == "shadow":
+        ed = mv.TableEditor(memv.host_mem, space.shadow_root, memv.host_alloc.alloc)
+    else:
+        g = space.guest
+        ed = mv.TableEditor(g.mem, space.guest_root, g.os_alloc.alloc)
+    for p in range(S.C1_PAGES):
+        r = rng.random()
+        va = S.C1_GVA + p * 4096
+        if r < 0.2:
+            ed.set_leaf_state(va, mv.EntryState.NOT_PRESENT)
+        elif r < 0.3 and mode == "shadow":
+            ed.set_leaf_state(va, mv.EntryState.TRAPPING)
+
+
+@pytest.mark.parametrize("mode", ["shadow", "tdp"])
+def test_c4_fault_heavy_translate_and_copy(cuda, mode):
+    w = S.c1_build(mv, be, er, mode)
+    memv, space = w["memv"], w["space"]
+    _corrupt(memv, space, mode)
+    if mode == "tdp":
+        # guest PTEs pointing past the slot: TDP-stage faults
+        ed = mv.TableEditor(space.guest.mem, space.guest_root, space.guest.os_alloc.alloc)
+        for p in range(0, S.C1_PAGES, 97):
+            ed.map(S.C1_GVA + p * 4096, (200 << 20) >> 12, replace=True)
+    tr = memv.translator(space, use_cache=False)
+    sp = tr.device_space
+    osp = O.space(sp.s1_base, sp.s1_root_pfn, sp.s2_root_pfn, sp.mode)
+    rng = random.Random(4)
+    vas = np.array([S.C1_GVA + rng.randrange(64 << 20) if rng.random() < 0.9 else rng.randrange(1 << 32)
+                    for _ in range(300_000)], dtype=np.uint64)
+    raw = np.frombuffer(S.image_bytes(memv.host_mem), dtype=np.uint8).copy()
+    hpa, st, aux = tr.translate_batch(vas)
+    v, s, a = O.translate(raw, osp, vas, threads=0)
+    assert np.array_equal(st, s) and np.array_equal(hpa, v) and np.array_equal(aux, a)
+    kinds = set((s & 0xFF0).tolist())
+    assert 0x010 in kinds and (0x040 in kinds if mode == "shadow" else 0x020 in kinds)
+    # a batch of copies that stop at the first bad page, with bytes_copied
+    rec = be.GuestProcessRecord(S._Guest(0, mode), space, memv)
+    acc = be.SoftwareHasAccess(rec, memv)
+    gvas = [S.C1_GVA + rng.randrange(60 << 20) for _ in range(64)]
+    lens = [rng.randrange(1, 5 * 4096) for _ in gvas]
+    # disjoint destinations: sort and space them
+    gvas = [S.C1_GVA + i * (1 << 20) + rng.randrange(4096) for i in range(64)]
+    src = np.frombuffer(random.Random(5).randbytes(sum(lens)), dtype=np.uint8)
+    outs = acc.copy_to_user_batch(gvas, lens, src.tobytes())
+    ops = dp.page_spans  # noqa: F841 (keep import used)
+    offs = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.uint64)
+    orows = np.stack([np.array(gvas, np.uint64), np.array(lens, np.uint64), offs, np.zeros(64, np.uint64)], 1)
+    oc = O.new_cache()
+    res = O.copy(raw, osp.reshape(1, 4), orows, src.copy(), 0, caches=oc, op_cache=[0] * 64)
+    after = np.frombuffer(S.image_bytes(memv.host_mem), dtype=np.uint8)
+    assert np.array_equal(after, raw)
+    for o, r in zip(outs, res):
+        st_o = int(r[3]) & 0xFFFFFFFF
+        if st_o == 0:
+            assert o == int(r[1 - 1])
+        else:
+            assert isinstance(o, Exception)
+            if (st_o & 0xFF0) in (0x010, 0x020):
+                assert isinstance(o, er.PageFault) and o.bytes_copied == int(r[0])
+            elif (st_o & 0xFF0) == 0x040:
+                assert isinstance(o, er.TrapExit)
+    entries, hits, misses = O.cache_state(oc)
+    assert (rec.translation_cache.hits, rec.translation_cache.misses) == (hits, misses)
+
+
+def test_overlapping_batch_is_last_writer_wins(cuda):
+    memv = mv.MemoryVirtualizer()
+    g = memv.add_guest(0, "shadow")
+    sp = memv.create_process(g)
+    memv.map_region(sp, S.BUF, 16)
+    rec = be.GuestProcessRecord(S._Guest(0, "shadow"), sp, memv)
+    acc = be.SoftwareHasAccess(rec, memv)
+    rng = random.Random(9)
+    gvas = [S.BUF + rng.randrange(8 * 4096) for _ in range(40)]
+    lens = [rng.randrange(64, 4096) for _ in gvas]
+    src = np.frombuffer(random.Random(10).randbytes(sum(lens)), dtype=np.uint8)
+    raw = np.frombuffer(S.image_bytes(memv.host_mem), dtype=np.uint8).copy()
+    outs = acc.copy_to_user_batch(gvas, lens, src.tobytes())
+    assert outs == lens
+    offs = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.uint64)
+    orows = np.stack([np.array(gvas, np.uint64), np.array(lens, np.uint64), offs, np.zeros(40, np.uint64)], 1)
+    tr = rec.translator
+    s = tr.device_space
+    O.copy(raw, O.space(s.s1_base, s.s1_root_pfn).reshape(1, 4), orows, src.copy(), 0)
+    assert np.array_equal(np.frombuffer(S.image_bytes(memv.host_mem), dtype=np.uint8), raw)
+
+
+def test_lanes_api_rejects_missing_gpu_never_falls_back(cuda):
+    # the data plane is the CUDA library: it must be the thing loaded
+    lib = N.lib()
+    assert lib.pv_abi_version() == N.ABI_VERSION
