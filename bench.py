@@ -1,0 +1,589 @@
+"""Benchmark of the HAS data plane on B200 (BASELINE.json metric).
+
+Step = one pass of the hot path over one batch of the workload:
+  * translate: every owned guest's random-VA batch, one pv_translate launch
+    over all owned processes (uncached software translation, the walk
+    ProcessTranslator._resolve_page performs; memvirt.py:596-601);
+  * copy: every owned guest's copy_to_user op batch through the hybrid
+    (hardware HAS) translator: pv_copy_plan + pv_copy_stamp + pv_copy_exec
+    (copy_user_buffer semantics, memvirt.py:604-628).
+Workload C5 (default, BASELINE configs[4]): 8 shadow guests x 8 GiB, per
+guest 16 M random VAs + 1 GiB of 4 MiB copy ops; guest g runs on rank
+g mod N (no collective on the data path; "strong" scaling: fixed total work).
+
+Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+        [--workload c5|c1]
+Prints ONE JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "translations/sec and forwarded-copy GB/s (% HBM roofline) at 1/2/4/8 B200 vs CPU ref"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=["c5", "c1"], default="c5")
+    ap.add_argument("--scale", type=int, default=1, help="shrink C5 by this factor (testing only)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-vas", type=int, default=16 << 20)
+    ap.add_argument("--cpu-sample-bytes", type=int, default=1 << 30)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:  # noqa: BLE001
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:  # noqa: BLE001
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            if len(r) >= 9:
+                for name, v in zip(names, r[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# ---- workload setup ---------------------------------------------------------------
+
+class Workload:
+    """Device-resident inputs of this rank's share of the workload."""
+
+    def __init__(self, name: str, rank: int, world: int, scale: int):
+        import torch
+
+        from paper_1304_3771_b200 import dataplane as dp
+        from paper_1304_3771_b200 import workloads as W
+
+        self.name = name
+        t0 = time.time()
+        if name == "c5":
+            cfg = W.C5Config() if scale == 1 else W.C5Config().scaled(scale)
+            self.cfg = cfg
+            wd = W.build_c5(cfg)
+            self.world = wd
+            self.memv = wd.memv
+            owned = [g for g in range(cfg.guests) if g % world == rank]
+            self.owned = owned
+            t_spaces, bounds, vas_parts, self.proc_vas = [], [], [], []
+            lane = 0
+            for g in owned:
+                for p, v in enumerate(W.c5_vas(cfg, g)):
+                    t_spaces.append(W.c5_shadow_space(wd, g, p))
+                    bounds.append((lane, lane + len(v), len(t_spaces) - 1))
+                    vas_parts.append(v)
+                    self.proc_vas.append((g, p, v))
+                    lane += len(v)
+            self.n_vas = lane
+            self.total_vas = cfg.guests * cfg.vas_per_guest
+            c_spaces, rows = [], []
+            self.proc_ops = []
+            buf_off = 0
+            for g in owned:
+                for p, ops in enumerate(W.c5_ops(cfg, g)):
+                    c_spaces.append(W.c5_hybrid_space(wd, g, p))
+                    si = len(c_spaces) - 1
+                    offs = buf_off + np.arange(len(ops), dtype=np.uint64) * np.uint64(cfg.op_bytes)
+                    rows.append(np.stack([ops[:, 0], ops[:, 1], offs, np.full(len(ops), si, np.uint64)], 1))
+                    self.proc_ops.append((g, p, ops, offs))
+                    buf_off += int(ops[:, 1].sum())
+            self.copy_bytes = buf_off
+            self.total_copy_bytes = cfg.guests * cfg.copy_bytes_per_guest
+            ops_all = np.concatenate(rows)
+        else:
+            memv, guest, space = W.build_c1("shadow")
+            self.memv = memv
+            self.owned = [0]
+            tr = memv.translator(space, use_cache=False)
+            t_spaces = [tr.device_space]
+            v = W.c1_vas().astype(np.uint32)
+            vas_parts = [v]
+            bounds = [(0, len(v), 0)]
+            self.n_vas = self.total_vas = len(v)
+            self.proc_vas = [(0, 0, v)]
+            c_spaces = [tr.device_space]
+            n = 64 << 20
+            ops_all = np.array([[W.C1_GVA, n, 0, 0]], dtype=np.uint64)
+            self.proc_ops = [(0, 0, ops_all[:, :2], np.zeros(1, np.uint64))]
+            self.copy_bytes = self.total_copy_bytes = n
+            self.c1_space = space
+        self.build_s = time.time() - t0
+        self.image = self.memv.host_mem.backing
+        self.image.device()  # allocate + push tables
+        self.vas = torch.from_numpy(np.concatenate(vas_parts).view(np.int32)).to("cuda")
+        self.tplan = dp.TranslatePlan(t_spaces, bounds)
+        n = self.n_vas
+        self.out = (torch.empty(n, dtype=torch.int64, device="cuda"), torch.empty(n, dtype=torch.int32, device="cuda"),
+                    torch.zeros(n, dtype=torch.int64, device="cuda"))
+        self.cplan = dp.CopyPlan(c_spaces, ops_all)
+        g = torch.Generator(device="cuda")
+        g.manual_seed(1304 + rank)
+        self.src = torch.randint(0, 256, (max(self.copy_bytes, 1),), dtype=torch.uint8, device="cuda", generator=g)
+        torch.cuda.synchronize()
+
+
+def run_ours(args, rank, world, local):
+    import torch
+    import torch.distributed as tdist
+
+    from paper_1304_3771_b200 import _native as N
+    from paper_1304_3771_b200 import dataplane as dp
+
+    torch.cuda.set_device(local)
+    wl = Workload(args.workload, rank, world, args.scale)
+    lib = N.lib()
+    img = wl.image
+    dev = img.device()
+    plan = wl.cplan
+    stream = torch.cuda.current_stream()
+    s = stream.cuda_stream
+    owner, _ = dp._owner_map(img)
+
+    def step(ev):
+        ev[0].record(stream)
+        dp.translate_lanes(img, wl.tplan, wl.vas, out=wl.out)
+        ev[1].record(stream)
+        plan.first_bad.fill_(-1)
+        plan.results.zero_()
+        plan.conflict.zero_()
+        ev[2].record(stream)
+        N.check(lib.pv_copy_plan(dev.data_ptr(), img.nbytes, plan.spaces.data_ptr(), plan.ops.data_ptr(),
+                                 plan.n_ops, plan.page_off.data_ptr(), plan.n_pages, N.TO_GUEST,
+                                 plan.page_hpa.data_ptr(), plan.page_status.data_ptr(), plan.page_aux.data_ptr(),
+                                 plan.first_bad.data_ptr(), None, 0, None, s), "plan")
+        img._epoch += 1
+        N.check(lib.pv_copy_stamp(plan.page_off.data_ptr(), plan.n_ops, plan.n_pages, plan.page_hpa.data_ptr(),
+                                  plan.first_bad.data_ptr(), owner.data_ptr(), img.npages, img._epoch,
+                                  plan.conflict.data_ptr(), s), "stamp")
+        ev[3].record(stream)
+        N.check(lib.pv_copy_exec(dev.data_ptr(), img.nbytes, plan.ops.data_ptr(), plan.n_ops,
+                                 plan.page_off.data_ptr(), plan.n_pages, N.TO_GUEST, plan.page_hpa.data_ptr(),
+                                 plan.page_status.data_ptr(), plan.page_aux.data_ptr(), plan.first_bad.data_ptr(),
+                                 wl.src.data_ptr(), wl.src.numel(), plan.results.data_ptr(),
+                                 img.dirty_map().data_ptr(), plan.conflict.data_ptr(), s), "exec")
+        ev[4].record(stream)
+        img.note_device_write()
+
+    def barrier():
+        if world > 1:
+            tdist.barrier()
+
+    for _ in range(args.warmup):
+        step([torch.cuda.Event(enable_timing=True) for _ in range(5)])
+    torch.cuda.synchronize()
+    # correctness of the timed configuration: no conflicts, every op complete
+    assert int(plan.conflict.item()) == 0, "conflicting destinations in the bench batch"
+    res = plan.results.cpu().numpy().view(np.uint64)
+    assert (res[:, 3] & 0xFFFFFFFF == 0).all() and (res[:, 0] == plan.host_ops[:, 1]).all()
+    st = wl.out[1]
+    n_faults = int((st != 0).sum().item())
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    barrier()
+    torch.cuda.synchronize()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for k in range(args.steps):
+        step(evs[k])
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    total_ms = t_start.elapsed_time(t_end)
+    tr_ms = sum(e[0].elapsed_time(e[1]) for e in evs)
+    plan_ms = sum(e[2].elapsed_time(e[3]) for e in evs)
+    exec_ms = sum(e[3].elapsed_time(e[4]) for e in evs)
+    copy_ms = sum(e[1].elapsed_time(e[4]) for e in evs)
+    local_t = torch.tensor([total_ms, tr_ms, copy_ms, exec_ms, plan_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        tdist.all_reduce(local_t, op=tdist.ReduceOp.MAX)
+    total_ms, tr_ms, copy_ms, exec_ms, plan_ms = local_t.tolist()
+    K = args.steps
+    trans_per_s = wl.total_vas * K / (tr_ms / 1e3) if world > 0 else 0.0
+    copy_gbs = wl.total_copy_bytes * K / (copy_ms / 1e3) / 1e9
+
+    # e2e through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(wl, args, world)
+
+    peak, peak_kind = peaks()
+    exec_achieved = 2 * wl.copy_bytes * K / (exec_ms / 1e3) / 1e9
+    walk_bytes = 16 * wl.n_vas  # u32 VA in + u64 hpa + u32 status out
+    walk_achieved = walk_bytes * K / (tr_ms / 1e3) / 1e9
+    traffic = load_traffic(args.workload)
+    line = {
+        "metric": METRIC,
+        "value": trans_per_s,
+        "unit": "translations/s",
+        "n_gpus": world,
+        "steps": K,
+        "warmup": args.warmup,
+        "ms_per_step": total_ms / K,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "u64 (integer walk) / u8 (payload)",
+        "data": "synthetic",
+        "config": config_of(wl, world),
+        "copy": {"value": copy_gbs, "unit": "GB/s", "payload_bytes_per_step": wl.total_copy_bytes,
+                 "ms_per_step": copy_ms / K, "exec_ms_per_step": exec_ms / K,
+                 "plan_stamp_ms_per_step": plan_ms / K},
+        "translate_ms_per_step": tr_ms / K,
+        "roofline": {"bound": "hbm", "kernel": "pv_copy_exec (exec_kernel)", "achieved": exec_achieved,
+                     "peak": peak, "unit": "GB/s", "frac": exec_achieved / peak, "peak_source": peak_kind,
+                     "traffic": traffic.get("exec"),
+                     "algorithmic_bytes_per_launch": 2 * wl.copy_bytes},
+        "roofline_walk": {"bound": "hbm", "kernel": "pv_translate (translate_kernel)", "achieved": walk_achieved,
+                          "peak": peak, "unit": "GB/s", "frac": walk_achieved / peak,
+                          "traffic": traffic.get("translate"), "algorithmic_bytes_per_launch": walk_bytes,
+                          "note": "16 B/translation (u32 VA in, u64 hpa + u32 status out); leaf-PTE gathers "
+                                  "are extra traffic"},
+        "faulting_lanes": n_faults,
+        "gpu_launches": 4 * K,
+        "clocks": clk,
+        "e2e": e2e,
+        "build_s": wl.build_s,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(wl, args)
+    return line
+
+
+def run_e2e(wl, args, world):
+    """Same step through the public API (ProcessTranslator.translate_batch,
+    HardwareHasAccess.copy_to_user_batch) with pinned host buffers: H2D of
+    the VAs and payload, D2H of the translations and per-op results are
+    inside the timed region."""
+    import torch
+    import torch.distributed as tdist
+
+    from paper_1304_3771_b200 import has
+    from paper_1304_3771_b200 import workloads as W
+
+    memv = wl.memv
+    host_vas = [(torch.from_numpy(v.view(np.int32)).pin_memory(), g, p) for g, p, v in wl.proc_vas]
+    if wl.name == "c5":
+        translators = {(g, p): memv.translator(wl.world.spaces[g][p], use_cache=False)
+                       for g, p, _ in wl.proc_vas}
+        recs = {}
+        for g, p, ops, offs in wl.proc_ops:
+            rec = has.GuestProcessRecord(_FakeGuest(g), wl.world.spaces[g][p], memv)
+            rec.hybrid = _Prebuilt(wl.world.hybrid_roots[g][p])
+            recs[(g, p)] = has.HardwareHasAccess(rec, memv)
+    else:
+        translators = {(0, 0): memv.translator(wl.c1_space, use_cache=False)}
+        rec = has.GuestProcessRecord(_FakeGuest(0), wl.c1_space, memv)
+        recs = {(0, 0): has.HardwareHasAccess(rec, memv)}
+    payload = [(torch.empty(int(ops[:, 1].sum()), dtype=torch.uint8).pin_memory(), g, p, ops)
+               for g, p, ops, offs in wl.proc_ops]
+    for t, *_ in payload:
+        t.random_(0, 256)
+
+    h2d = sum(t.numel() * 4 for t, _, _ in host_vas) + sum(t.numel() for t, *_ in payload)
+    d2h = sum(t.numel() * 20 for t, _, _ in host_vas) + sum(len(ops) * 32 for *_, ops in payload)
+
+    def one_step():
+        t0 = time.perf_counter()
+        for t, g, p in host_vas:
+            translators[(g, p)].translate_batch(t)
+        t1 = time.perf_counter()
+        for t, g, p, ops in payload:
+            outs = recs[(g, p)].copy_to_user_batch(ops[:, 0], ops[:, 1], t)
+            assert all(isinstance(o, int) for o in outs)
+        torch.cuda.synchronize()
+        return t1 - t0, time.perf_counter() - t1
+
+    one_step()  # warm (pinned pools, plans)
+    if world > 1:
+        tdist.barrier()
+    torch.cuda.synchronize()
+    tr_s = cp_s = 0.0
+    steps = max(1, min(args.steps, 3))
+    for _ in range(steps):
+        a, b = one_step()
+        tr_s += a
+        cp_s += b
+    tt = torch.tensor([tr_s, cp_s], dtype=torch.float64, device="cuda")
+    if world > 1:
+        tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
+    tr_s, cp_s = tt.tolist()
+    return {"value": wl.total_vas * steps / tr_s, "unit": "translations/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "copy": {"value": wl.total_copy_bytes * steps / cp_s / 1e9, "unit": "GB/s"},
+            "steps": steps, "api": "ProcessTranslator.translate_batch + HardwareHasAccess.copy_to_user_batch"}
+
+
+class _FakeGuest:
+    """GuestProcessRecord reads .id and .mem_mode (backend.py:267-286)."""
+
+    def __init__(self, gid):
+        self.id = gid
+        self.mem_mode = "shadow"
+
+
+class _Prebuilt:
+    """A HybridTopLevel that already holds the world's merged root."""
+
+    def __init__(self, root):
+        self.root = root
+
+    def build(self, shadow_root, host_root):
+        return self.root
+
+
+def load_traffic(workload: str) -> dict:
+    path = os.path.join(ROOT, "profiles", f"traffic_{workload}.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:  # noqa: BLE001
+        return {}
+
+
+def config_of(wl, world):
+    if wl.name == "c5":
+        c = wl.cfg
+        return {"workload": "C5: 8 shadow guests x 8 GiB, 3 processes each, per guest 16M random-VA "
+                            "translations + 1 GiB copy_to_user in 4 MiB ops (hybrid/hardware HAS)",
+                "guests": c.guests, "guest_bytes": c.guest_bytes, "vas_per_guest": c.vas_per_guest,
+                "copy_bytes_per_guest": c.copy_bytes_per_guest, "op_bytes": c.op_bytes,
+                "geometry": "reference 3-level 2/9/9/12", "sharding": f"guest g -> rank g mod {world}",
+                "parallelism": f"guest-sharded x{world}, no collective",
+                "l2": "inputs larger than L2 (512 MiB VAs, 8 GiB payload per step)",
+                "scale": 1 if wl.cfg.guest_bytes == 8 << 30 else "reduced"}
+    return {"workload": "C1: 1 shadow guest, 16384 shuffled pages, 1M random-VA translations + 64 MiB "
+                        "copy_to_user", "geometry": "reference 3-level 2/9/9/12",
+            "l2": "inputs smaller than L2 (not flushed)"}
+
+
+# ---- CPU baseline / reference arm ---------------------------------------------------
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:  # noqa: BLE001
+        return os.cpu_count() or 1
+
+
+def cpu_sample(memv, proc_vas, proc_ops, n_vas: int, n_bytes: int, threads: int):
+    """Time the oracle port (oracle/pvoracle.c, test infrastructure) on a
+    bounded sample: the first ``n_vas`` translations and ``n_bytes`` of copy
+    ops of this workload.  Returns (translations/s, copy GB/s, sample)."""
+    sys.path.insert(0, ROOT)
+    from oracle import oracle as O
+
+    # the host mirror holds every table byte (tables are written host-side)
+    img = memv.host_mem.backing.host
+    # translations: first processes' VAs (shadow walks)
+    done = 0
+    t_tr = 0.0
+    for sp, vas in proc_vas:
+        take = vas[: max(0, n_vas - done)]
+        if len(take) == 0:
+            break
+        t0 = time.perf_counter()
+        O.translate(img, sp, take.astype(np.uint64), threads=threads)
+        t_tr += time.perf_counter() - t0
+        done += len(take)
+    copied = 0
+    t_cp = 0.0
+    for sp, ops in proc_ops:
+        room = n_bytes - copied
+        if room <= 0:
+            break
+        k = max(1, min(len(ops), room // max(int(ops[0, 1]), 1)))
+        sel = ops[:k]
+        rows = np.stack([sel[:, 0], sel[:, 1], np.concatenate([[0], np.cumsum(sel[:-1, 1])]).astype(np.uint64),
+                         np.zeros(k, np.uint64)], 1).astype(np.uint64)
+        buf = np.random.default_rng(0).integers(0, 256, int(sel[:, 1].sum()), dtype=np.uint8)
+        t0 = time.perf_counter()
+        O.copy(img, sp.reshape(1, 4), rows, buf, 0, threads=threads)
+        t_cp += time.perf_counter() - t0
+        copied += int(sel[:, 1].sum())
+    return done / t_tr, copied / t_cp / 1e9, f"{done} translations + {copied} bytes of copy_to_user ops"
+
+
+def _oracle_inputs(wl):
+    from oracle import oracle as O
+
+    proc_vas, proc_ops = [], []
+    if wl.name == "c5":
+        for g, p, v in wl.proc_vas:
+            sp = wl.world.spaces[g][p].shadow_root.root_pfn
+            proc_vas.append((O.space(0, sp), v))
+        for g, p, ops, offs in wl.proc_ops:
+            proc_ops.append((O.space(0, wl.world.hybrid_roots[g][p].root_pfn), ops))
+    else:
+        sp = O.space(0, wl.c1_space.shadow_root.root_pfn)
+        proc_vas.append((sp, wl.proc_vas[0][2]))
+        proc_ops.append((sp, wl.proc_ops[0][2]))
+    return proc_vas, proc_ops
+
+
+def cpu_baseline(wl, args):
+    threads = cpu_threads()
+    proc_vas, proc_ops = _oracle_inputs(wl)
+    tps, gbs, sample = cpu_sample(wl.memv, proc_vas, proc_ops, args.cpu_sample_vas, args.cpu_sample_bytes, threads)
+    return {"value": tps, "unit": "translations/s", "cores": threads, "kind": "port", "sample": sample,
+            "copy": {"value": gbs, "unit": "GB/s"},
+            "note": "oracle/pvoracle.c (C restatement of memvirt.py walk/copy_user_buffer, OpenMP); the "
+                    "reference itself is pure Python and cannot run on the GPU box"}
+
+
+class _HostOnlyWorkload:
+    """The reference arm's world: host tables only, no device."""
+
+    def __init__(self, name, scale):
+        from paper_1304_3771_b200 import workloads as W
+
+        self.name = name
+        if name == "c5":
+            cfg = W.C5Config() if scale == 1 else W.C5Config().scaled(scale)
+            self.cfg = cfg
+            self.world = W.build_c5(cfg)
+            self.memv = self.world.memv
+            self.proc_vas = [(g, p, v) for g in range(cfg.guests) for p, v in enumerate(W.c5_vas(cfg, g))]
+            self.proc_ops = [(g, p, ops, None) for g in range(cfg.guests) for p, ops in enumerate(W.c5_ops(cfg, g))]
+            self.total_vas = cfg.guests * cfg.vas_per_guest
+        else:
+            memv, guest, space = W.build_c1("shadow")
+            self.memv, self.c1_space = memv, space
+            v = W.c1_vas().astype(np.uint32)
+            self.proc_vas = [(0, 0, v)]
+            self.proc_ops = [(0, 0, np.array([[W.C1_GVA, 64 << 20]], np.uint64), None)]
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    wl = _HostOnlyWorkload(args.workload, args.scale)
+    threads = cpu_threads()
+    proc_vas, proc_ops = _oracle_inputs(wl)
+    for _ in range(max(args.warmup, 0)):
+        cpu_sample(wl.memv, proc_vas, proc_ops, min(args.cpu_sample_vas, 1 << 20), 64 << 20, threads)
+    vals, gbs = [], []
+    for _ in range(args.steps):
+        tps, g, sample = cpu_sample(wl.memv, proc_vas, proc_ops, args.cpu_sample_vas // 4, args.cpu_sample_bytes // 4,
+                                    threads)
+        vals.append(tps)
+        gbs.append(g)
+    v = statistics.median(vals)
+    return {
+        "metric": METRIC, "value": v, "unit": "translations/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic", "impl": "reference",
+        "config": config_of(wl, world) if args.workload == "c5" else {"workload": "C1"},
+        "copy": {"value": statistics.median(gbs), "unit": "GB/s"},
+        "cpu_baseline": {"value": v, "unit": "translations/s", "cores": threads, "kind": "port",
+                         "sample": sample + " per step"},
+        "e2e": {"value": v, "unit": "translations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.gpus != world and world != 1:
+        args.gpus = world
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+
+        if args.impl == "ours":
+            torch.cuda.set_device(local)
+            tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            tdist.init_process_group("gloo")
+    if args.impl == "reference":
+        line = run_reference(args, rank, world)
+    else:
+        line = run_ours(args, rank, world, local)
+    if rank == 0 and line is not None:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as tdist
+
+        tdist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -55,7 +55,10 @@ def _i64(values) -> np.ndarray:
 def _to_dev(arr: np.ndarray, stream=None):
     import torch
 
-    t = torch.from_numpy(np.ascontiguousarray(arr))
+    arr = np.ascontiguousarray(arr)
+    if not arr.flags.writeable:
+        arr = arr.copy()
+    t = torch.from_numpy(arr)
     if t.numel() * t.element_size() >= 1 << 16:
         t = t.pin_memory()
     return t.to("cuda", non_blocking=True)

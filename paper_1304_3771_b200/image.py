@@ -37,6 +37,18 @@ PAGE_SHIFT = 12
 _STAGE_PAGES = 65536
 
 
+def _zeroed_host(nbytes: int) -> np.ndarray:
+    """Zero-filled host mirror.  Large images are anonymous MAP_NORESERVE
+    mappings: untouched pages cost neither RAM nor commit charge."""
+    if nbytes < (1 << 30):
+        return np.zeros(nbytes, dtype=np.uint8)
+    import mmap
+
+    flags = mmap.MAP_PRIVATE | mmap.MAP_ANONYMOUS | getattr(mmap, "MAP_NORESERVE", 0x4000)
+    mm = mmap.mmap(-1, nbytes, flags=flags, prot=mmap.PROT_READ | mmap.PROT_WRITE)
+    return np.frombuffer(mm, dtype=np.uint8)
+
+
 class MemoryImage:
     """One physical memory (the reference's host ``bytearray``)."""
 
@@ -45,7 +57,7 @@ class MemoryImage:
             raise ValueError("memory size must be a multiple of the page size")
         self.nbytes = nbytes
         self.npages = nbytes // PAGE_SIZE
-        self.host = np.zeros(nbytes, dtype=np.uint8) if host is None else host
+        self.host = _zeroed_host(nbytes) if host is None else host
         self._host_dirty = np.zeros(self.npages, dtype=np.bool_)
         self._host_dirty_any = False
         # pages that may hold non-zero bytes (host or device side); frames

@@ -843,8 +843,14 @@ def translate_batch(translator: ProcessTranslator, gvas, *, use_cache: bool | No
     import torch
 
     on_device = isinstance(gvas, torch.Tensor) and gvas.is_cuda
+    host_tensor = isinstance(gvas, torch.Tensor) and not gvas.is_cuda
     if on_device:
         vas = gvas if gvas.dtype in (torch.int64, torch.int32) else gvas.to(torch.int64)
+    elif host_tensor:
+        # (pinned) host tensor in, pinned host tensors out: async copies on
+        # the current stream, one synchronisation at the end
+        src = gvas if gvas.dtype in (torch.int64, torch.int32) else gvas.to(torch.int64)
+        vas = src.to("cuda", non_blocking=True)
     else:
         host = np.ascontiguousarray(np.asarray(gvas, dtype=np.uint64)).view(np.int64)
         vas = dp._to_dev(host)
@@ -860,6 +866,14 @@ def translate_batch(translator: ProcessTranslator, gvas, *, use_cache: bool | No
         dp.unpack_fifo(fifo.cpu().numpy(), [translator.cache])
     if on_device:
         return value, status, aux
+    if host_tensor:
+        outs = []
+        for t in (value, status, aux):
+            h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+            h.copy_(t, non_blocking=True)
+            outs.append(h)
+        torch.cuda.current_stream().synchronize()
+        return tuple(outs)
     return (value.cpu().numpy().view(np.uint64), status.cpu().numpy().view(np.uint32),
             aux.cpu().numpy().view(np.uint64))
 
