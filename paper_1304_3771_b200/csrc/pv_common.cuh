@@ -32,6 +32,31 @@ __device__ __forceinline__ uint64_t ld_word(const uint8_t* image, uint64_t base,
   return __ldg(reinterpret_cast<const unsigned long long*>(image + base + (pfn << kPageShift)) + idx);
 }
 
+// L2 cache-policy descriptors: streamed data (VAs, results, payload) is
+// evict-first so it does not push the page tables out of the 126 MB L2;
+// page-table gathers are evict-last.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t ld_u64_hint(const void* p, uint64_t pol) {
+  unsigned long long v;
+  asm("ld.global.nc.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_u64_stream(void* p, uint64_t v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_u32_stream(void* p, uint32_t v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
+}
+
 // Classify one entry word at `level`.  Returns PV_ST_OK and advances *node,
 // or a status word (fault / trap) for the walk's stage.
 __device__ __forceinline__ uint32_t classify(uint64_t w, uint32_t level, uint32_t index, uint32_t stage2,

@@ -97,16 +97,16 @@ stamp_kernel(const uint64_t* __restrict__ page_off, uint64_t n_ops, uint64_t n_p
 
 // ---- warp copy of one chunk (<= 4096 bytes) -------------------------------
 
-__device__ __forceinline__ uint4 ld_v4_stream(const uint4* p) {
+__device__ __forceinline__ uint4 ld_v4_stream(const uint4* p, uint64_t pol) {
   uint4 r;
-  asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
       : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-      : "l"(p));
+      : "l"(p), "l"(pol));
   return r;
 }
-__device__ __forceinline__ void st_v4_stream(uint4* p, const uint4& v) {
-  asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
-               "r"(v.w)
+__device__ __forceinline__ void st_v4_stream(uint4* p, const uint4& v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol)
                : "memory");
 }
 
@@ -117,7 +117,7 @@ __device__ __forceinline__ void warp_copy_bytes(uint8_t* __restrict__ d, const u
 
 // Copy n bytes (n <= 4096) from s to d with the whole warp.
 __device__ __forceinline__ void warp_copy(uint8_t* __restrict__ d, const uint8_t* __restrict__ s, uint32_t n,
-                                          uint32_t lane) {
+                                          uint32_t lane, uint64_t pol) {
   const uintptr_t da = reinterpret_cast<uintptr_t>(d), sa = reinterpret_cast<uintptr_t>(s);
   if (((da ^ sa) & 15) == 0) {
     const uint32_t head = min(n, (uint32_t)((16 - (da & 15)) & 15));
@@ -129,12 +129,12 @@ __device__ __forceinline__ void warp_copy(uint8_t* __restrict__ d, const uint8_t
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const uint32_t i = lane + 32 * j;
-      if (i < nv) r[j] = ld_v4_stream(sv + i);
+      if (i < nv) r[j] = ld_v4_stream(sv + i, pol);
     }
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const uint32_t i = lane + 32 * j;
-      if (i < nv) st_v4_stream(dv + i, r[j]);
+      if (i < nv) st_v4_stream(dv + i, r[j], pol);
     }
     const uint32_t done = head + (nv << 4), tail = n - done;
     if (lane < tail) d[done + lane] = s[done + lane];
@@ -184,6 +184,7 @@ exec_kernel(uint8_t* __restrict__ image, uint64_t image_bytes, const pv_op* __re
             const uint32_t* __restrict__ abort_flag) {
   // A conflicted batch (stamp pass) is left untouched for the host to re-plan.
   if (abort_flag != nullptr && *abort_flag != 0) return;
+  const uint64_t pol = policy_evict_first();
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -228,10 +229,10 @@ exec_kernel(uint8_t* __restrict__ image, uint64_t image_bytes, const pv_op* __re
       const uint32_t chunk = (uint32_t)min(o.len - done, kPageSize - (cur & kPageMask));
       uint8_t* bp = buf + o.buf_off + done;
       if (direction == PV_TO_GUEST) {
-        warp_copy(image + hpa, bp, chunk, lane);
+        warp_copy(image + hpa, bp, chunk, lane, pol);
         if (dirty != nullptr && lane == 0) dirty[hpa >> kPageShift] = 1;
       } else {
-        warp_copy(bp, image + hpa, chunk, lane);
+        warp_copy(bp, image + hpa, chunk, lane, pol);
       }
     }
   }

@@ -5,15 +5,22 @@
 // ProcessTranslator resolve (memvirt.py:596-601) and resolve_hybrid
 // (memvirt.py:677-682).
 //
-// B200 design.  A CTA owns a contiguous run of 2048-lane chunks of one
-// segment (one address space).  On entering a space it stages the space's
-// top-level words and every present mid-level node (<= 4 x 4 KiB per stage)
-// in shared memory, so the two upper levels of every walk are shared-memory
-// lookups and each stage costs exactly one dependent global load: the leaf
-// PTE (L1-allocating, since leaf tables are small and reused across lanes).
-// Each thread walks 8 lanes at once (8 independent leaf loads in flight),
-// VAs stream in with L1::no_allocate loads and results stream out with
-// evict-first stores.
+// B200 design.  A CTA owns a contiguous run of 2048-lane chunks (mostly of
+// one segment = one address space).  On entering a space it stages the two
+// upper levels of each walk stage in shared memory as 4-byte codes, one per
+// mid-level entry of every present top entry (4 x 512 codes = 8 KiB per
+// stage):
+//     bits 0-1  kind: 0 not present (fault at level 2), 1 present,
+//               2 trapping (trap at level 2), 3 the walk already stopped at
+//               level 1 / 2 (status precomputed per top entry)
+//     bit  2    the leaf node lies past the image (struct.error at level 3)
+//     bits 3-31 leaf-node pfn
+// so resolving the two upper levels of a lane is ONE 4-byte shared-memory
+// read, and every stage costs exactly one dependent global load: the leaf
+// PTE.  Each thread walks 8 lanes at once with predicated (branch-free) code
+// (8 independent leaf loads in flight) and prefetches the next chunk's VAs
+// before gathering the current chunk's leaves; VAs stream in with
+// L1::no_allocate loads and results stream out with evict-first stores.
 #include "pv_common.cuh"
 
 namespace pv {
@@ -21,123 +28,133 @@ namespace pv {
 constexpr int kTpb = 256;
 constexpr int kVpt = 8;
 constexpr uint64_t kChunk = (uint64_t)kTpb * kVpt;  // lanes per chunk
+constexpr uint32_t kCodeStop = 3u;
 
-struct StageSmem {
-  uint64_t root;          // root pfn
-  uint64_t lim;           // node limit of the window
-  uint64_t base;          // window base
-  uint64_t top_word[4];
-  uint32_t top_status[4]; // PV_ST_OK if the mid node is staged, else final status
-  uint64_t top_node[4];   // trap node (root) for level-1 traps / mid node pfn
+struct Stage {
+  uint64_t base;          // window base (bytes)
+  uint64_t lim;           // node limit of the window (pages)
+  uint64_t top_node[4];   // root (level-1 traps) / mid node pfn (level-2 traps)
+  uint32_t top_status[4]; // status when the walk stops at level 1 or 2 (code kind 3)
 };
 
-__device__ __forceinline__ uint64_t ld_stream_va(const void* vas, uint64_t i, bool va32) {
+__device__ __forceinline__ uint64_t ld_stream_va(const void* vas, uint64_t i, bool va32, uint64_t pol) {
   if (va32) {
     uint32_t v;
-    asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"((const uint32_t*)vas + i));
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+        : "=r"(v)
+        : "l"((const uint32_t*)vas + i), "l"(pol));
     return v;
   }
   unsigned long long v;
-  asm("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(v) : "l"((const uint64_t*)vas + i));
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u64 %0, [%1], %2;"
+      : "=l"(v)
+      : "l"((const uint64_t*)vas + i), "l"(pol));
   return v;
 }
 
-// Stage one walk stage: top words and present mid nodes.  Called by all
-// threads of the CTA; ends with __syncthreads().
-__device__ void stage_space(const uint8_t* __restrict__ image, uint64_t image_bytes, uint64_t base,
-                            uint64_t root, uint32_t stage2, StageSmem& s, uint64_t* mid /*[4][512]*/) {
+// Stage the upper two levels of one walk stage (all threads; ends with a
+// barrier).  Requires image_bytes < 2^41 so leaf pfns fit 29 bits.
+__device__ void stage_codes(const uint8_t* __restrict__ image, uint64_t image_bytes, uint64_t base, uint64_t root,
+                            uint32_t stage2, Stage& s, uint32_t* codes /*[4*512]*/) {
   const uint32_t tid = threadIdx.x;
-  if (tid == 0) {
-    s.root = root;
-    s.base = base;
-    s.lim = node_limit(image_bytes, base);
-  }
+  const uint64_t lim = node_limit(image_bytes, base);
   if (tid < 4) {
-    const uint64_t lim = node_limit(image_bytes, base);
+    uint32_t st;
+    uint64_t node = 0;
     if (root >= lim) {
-      s.top_word[tid] = 0;
-      s.top_status[tid] = (stage2 ? PV_ST_NODE_OOR2 : PV_ST_NODE_OOR) | 1u;
-      s.top_node[tid] = 0;
+      st = (stage2 ? PV_ST_NODE_OOR2 : PV_ST_NODE_OOR) | 1u;
     } else {
       const uint64_t w = ld_word(image, base, root, tid);
-      s.top_word[tid] = w;
       if (w & kFlagTrapping) {
-        s.top_status[tid] = (stage2 ? PV_ST_TRAP2 : PV_ST_TRAP) | 1u | (tid << 16);
-        s.top_node[tid] = root;
+        st = (stage2 ? PV_ST_TRAP2 : PV_ST_TRAP) | 1u | (tid << 16);
+        node = root;
       } else if (!(w & kFlagPresent)) {
-        s.top_status[tid] = (stage2 ? PV_ST_FAULT2 : PV_ST_FAULT) | 1u;
-        s.top_node[tid] = 0;
-      } else if ((w >> kPageShift) >= lim) {
-        s.top_status[tid] = (stage2 ? PV_ST_NODE_OOR2 : PV_ST_NODE_OOR) | 2u;
-        s.top_node[tid] = w >> kPageShift;
+        st = (stage2 ? PV_ST_FAULT2 : PV_ST_FAULT) | 1u;
       } else {
-        s.top_status[tid] = PV_ST_OK;
-        s.top_node[tid] = w >> kPageShift;
+        node = w >> kPageShift;
+        st = node >= lim ? ((stage2 ? PV_ST_NODE_OOR2 : PV_ST_NODE_OOR) | 2u) : PV_ST_OK;
       }
+    }
+    s.top_status[tid] = st;
+    s.top_node[tid] = node;
+    if (tid == 0) {
+      s.base = base;
+      s.lim = lim;
     }
   }
   __syncthreads();
-  // 4 nodes x 4 KiB, 16 B per thread per step.
-#pragma unroll
-  for (int t = 0; t < 4; ++t) {
-    if (s.top_status[t] != PV_ST_OK) continue;
-    const uint4* src = reinterpret_cast<const uint4*>(image + base + (s.top_node[t] << kPageShift));
-    uint4* dst = reinterpret_cast<uint4*>(mid + t * 512);
-    for (uint32_t i = tid; i < 256; i += kTpb) dst[i] = __ldg(src + i);
+  for (uint32_t i = tid; i < 4 * 512; i += kTpb) {
+    const uint32_t t = i >> 9;
+    uint32_t code = kCodeStop;
+    if (s.top_status[t] == PV_ST_OK) {
+      const uint64_t w = ld_word(image, base, s.top_node[t], i & 511);
+      const uint64_t leaf = w >> kPageShift;
+      if (w & kFlagTrapping) code = 2u;
+      else if (!(w & kFlagPresent)) code = 0u;
+      else code = 1u | (leaf >= lim ? 4u : ((uint32_t)leaf << 3));
+    }
+    codes[i] = code;
   }
   __syncthreads();
 }
 
-// Upper two levels from shared memory.  Returns PV_ST_OK with *leaf_node set
-// (already bounds-checked), or a final status with *value.
-__device__ __forceinline__ uint32_t walk_upper(const StageSmem& s, const uint64_t* mid, uint64_t va,
-                                               uint32_t stage2, uint64_t* leaf_node, uint64_t* value) {
-  const uint32_t t = top_index(va);
-  const uint32_t ts = s.top_status[t];
-  if (ts != PV_ST_OK) {
-    *value = (PV_ST_KIND(ts) == PV_ST_TRAP || PV_ST_KIND(ts) == PV_ST_TRAP2) ? s.top_node[t] : va;
-    return ts;
-  }
-  const uint32_t m = mid_index(va);
-  const uint64_t w = mid[t * 512 + m];
-  if (w & kFlagTrapping) {
-    *value = s.top_node[t];
-    return (stage2 ? PV_ST_TRAP2 : PV_ST_TRAP) | 2u | (m << 16);
-  }
-  if (!(w & kFlagPresent)) {
-    *value = va;
-    return (stage2 ? PV_ST_FAULT2 : PV_ST_FAULT) | 2u;
-  }
-  const uint64_t node = w >> kPageShift;
-  if (node >= s.lim) {
-    *value = va;
-    return (stage2 ? PV_ST_NODE_OOR2 : PV_ST_NODE_OOR) | 3u;
-  }
-  *leaf_node = node;
+// Upper two levels of one stage for one lane from the code table.  `x` is
+// the address walked (va, or gpa in the TDP stage).  Returns PV_ST_OK when
+// the leaf PTE must be read (leaf node in *code_out >> 3), else the status.
+template <bool kStage2>
+__device__ __forceinline__ uint32_t upper(const Stage& s, const uint32_t* codes, uint64_t x, uint32_t* code_out) {
+  const uint32_t t = top_index(x), m = mid_index(x);
+  const uint32_t code = codes[(t << 9) | m];
+  *code_out = code;
+  const uint32_t kind = code & 3u;
+  const uint32_t st_present = (code & 4u) ? ((kStage2 ? PV_ST_NODE_OOR2 : PV_ST_NODE_OOR) | 3u) : PV_ST_OK;
+  const uint32_t st_np = (kStage2 ? PV_ST_FAULT2 : PV_ST_FAULT) | 2u;
+  const uint32_t st_trap = (kStage2 ? PV_ST_TRAP2 : PV_ST_TRAP) | 2u | (m << 16);
+  return kind == 1u ? st_present : kind == 0u ? st_np : kind == 2u ? st_trap : s.top_status[t];
+}
+
+template <bool kStage2>
+__device__ __forceinline__ uint32_t leaf_status(uint64_t w, uint32_t st, uint64_t x) {
+  if (st != PV_ST_OK) return st;
+  if (w & kFlagTrapping) return (kStage2 ? PV_ST_TRAP2 : PV_ST_TRAP) | 3u | (leaf_index(x) << 16);
+  if (!(w & kFlagPresent)) return (kStage2 ? PV_ST_FAULT2 : PV_ST_FAULT) | 3u;
   return PV_ST_OK;
 }
 
+// Node pfn a trap reports: level 3 -> the leaf node, level 1/2 -> top_node.
+__device__ __forceinline__ uint64_t trap_node(const Stage& s, uint32_t st, uint32_t code, uint64_t x) {
+  return PV_ST_LEVEL(st) == 3u ? (uint64_t)(code >> 3) : s.top_node[top_index(x)];
+}
+
+__device__ __forceinline__ uint64_t leaf_word(const uint8_t* image, const Stage& s, uint32_t code, uint64_t x,
+                                              uint64_t pol) {
+  return ld_u64_hint(reinterpret_cast<const unsigned long long*>(image + s.base + ((uint64_t)(code >> 3) << kPageShift)) +
+                         leaf_index(x),
+                     pol);
+}
+
 template <bool kTwo, bool kVa32, bool kPfn>
-__global__ void __launch_bounds__(kTpb)
+__global__ void __launch_bounds__(kTpb, 3)
 translate_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const pv_space* __restrict__ spaces,
                  const pv_seg* __restrict__ segs, uint32_t n_segs, uint64_t n_chunks, const void* __restrict__ vas,
                  uint64_t* __restrict__ out_value, uint32_t* __restrict__ out_status, uint64_t* __restrict__ out_aux) {
-  extern __shared__ __align__(16) uint64_t smem_mid[];  // [kTwo ? 2 : 1][4][512]
-  __shared__ StageSmem st1, st2;
-  uint64_t* mid1 = smem_mid;
-  uint64_t* mid2 = smem_mid + 4 * 512;
+  __shared__ __align__(16) uint32_t codes1[4 * 512];
+  __shared__ __align__(16) uint32_t codes2[kTwo ? 4 * 512 : 1];
+  __shared__ Stage st1, st2;
 
   const uint64_t c_begin = (n_chunks * blockIdx.x) / gridDim.x;
   const uint64_t c_end = (n_chunks * (blockIdx.x + 1)) / gridDim.x;
-  // Every thread tracks the segment and the staged space in registers; the
-  // values are CTA-uniform, so the staging branch is uniform too.
+  // Segment and staged space live in registers; they are CTA-uniform, so
+  // every branch on them is uniform.
   pv_seg seg;
   seg.begin = seg.end = seg.chunk0 = 0;
+  seg.space = 0xFFFFFFFFu;
   uint64_t seg_chunks = 0;
   uint32_t staged_space = 0xFFFFFFFFu;
   bool two = false;
+  const uint64_t pol_stream = policy_evict_first(), pol_table = policy_evict_last();
 
-  for (uint64_t c = c_begin; c < c_end; ++c) {
+  auto find_seg = [&](uint64_t c) {
     if (c < seg.chunk0 || c >= seg.chunk0 + seg_chunks) {
       uint32_t lo = 0, hi = n_segs;
       while (hi - lo > 1) {
@@ -147,88 +164,87 @@ translate_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const 
       seg = segs[lo];
       seg_chunks = (seg.end - seg.begin + kChunk - 1) / kChunk;
     }
+  };
+  auto load_vas = [&](uint64_t c, uint64_t (&va)[kVpt]) {
+    const uint64_t lane0 = seg.begin + (c - seg.chunk0) * kChunk;
+#pragma unroll
+    for (int j = 0; j < kVpt; ++j) {
+      const uint64_t i = lane0 + (uint64_t)j * kTpb + threadIdx.x;
+      va[j] = i < seg.end ? ld_stream_va(vas, i, kVa32, pol_stream) : 0;
+    }
+  };
+
+  uint64_t va[kVpt], nva[kVpt];
+  bool have_next = false;
+  for (uint64_t c = c_begin; c < c_end; ++c) {
+    find_seg(c);
     if (seg.space != staged_space) {
       const pv_space sp = spaces[seg.space];
       staged_space = seg.space;
       two = kTwo && sp.mode == PV_TWO_STAGE;
       __syncthreads();  // everyone is done with the previous staging
-      stage_space(image, image_bytes, sp.s1_base, sp.s1_root_pfn, 0, st1, mid1);
-      if (two) stage_space(image, image_bytes, 0, sp.s2_root_pfn, 1, st2, mid2);
+      stage_codes(image, image_bytes, sp.s1_base, sp.s1_root_pfn, 0, st1, codes1);
+      if (two) stage_codes(image, image_bytes, 0, sp.s2_root_pfn, 1, st2, codes2);
+    }
+    if (have_next) {
+#pragma unroll
+      for (int j = 0; j < kVpt; ++j) va[j] = nva[j];
+    } else {
+      load_vas(c, va);
     }
     const uint64_t lane0 = seg.begin + (c - seg.chunk0) * kChunk;
+    const uint64_t seg_end = seg.end;
+    // Prefetch the next chunk's VAs when it is in the same segment.
+    have_next = c + 1 < c_end && c + 1 < seg.chunk0 + seg_chunks;
+    if (have_next) load_vas(c + 1, nva);
 
-    uint64_t va[kVpt], node[kVpt], val[kVpt], aux[kVpt];
-    uint32_t status[kVpt];
-    bool live[kVpt];
-#pragma unroll
-    for (int j = 0; j < kVpt; ++j) {
-      const uint64_t i = lane0 + (uint64_t)j * kTpb + threadIdx.x;
-      live[j] = i < seg.end;
-      va[j] = live[j] ? ld_stream_va(vas, i, kVa32) : 0;
-      aux[j] = 0;
-    }
-    // Stage 1: upper levels from smem.
-#pragma unroll
-    for (int j = 0; j < kVpt; ++j) status[j] = walk_upper(st1, mid1, va[j], 0, &node[j], &val[j]);
-    // Stage 1 leaf: one independent global load per lane.
+    uint32_t st[kVpt], code[kVpt];
     uint64_t w[kVpt];
 #pragma unroll
-    for (int j = 0; j < kVpt; ++j)
-      w[j] = (live[j] && status[j] == PV_ST_OK) ? ld_word(image, st1.base, node[j], leaf_index(va[j])) : 0;
+    for (int j = 0; j < kVpt; ++j) st[j] = upper<false>(st1, codes1, va[j], &code[j]);
+#pragma unroll
+    for (int j = 0; j < kVpt; ++j) w[j] = st[j] == PV_ST_OK ? leaf_word(image, st1, code[j], va[j], pol_table) : 0;
+    uint64_t val[kVpt], aux[kVpt];
 #pragma unroll
     for (int j = 0; j < kVpt; ++j) {
-      if (status[j] != PV_ST_OK) continue;
-      const uint32_t li = leaf_index(va[j]);
-      if (w[j] & kFlagTrapping) {
-        status[j] = PV_ST_TRAP | 3u | (li << 16);
-        val[j] = node[j];
-      } else if (!(w[j] & kFlagPresent)) {
-        status[j] = PV_ST_FAULT | 3u;
-        val[j] = va[j];
-      } else {
-        val[j] = w[j] >> kPageShift;  // leaf target pfn
-      }
+      st[j] = leaf_status<false>(w[j], st[j], va[j]);
+      const uint32_t k = PV_ST_KIND(st[j]);
+      val[j] = k == PV_ST_OK ? (w[j] >> kPageShift) : k == PV_ST_TRAP ? trap_node(st1, st[j], code[j], va[j]) : va[j];
+      aux[j] = 0;
     }
     if (kTwo && two) {
       uint64_t gpa[kVpt];
 #pragma unroll
       for (int j = 0; j < kVpt; ++j) {
         gpa[j] = (val[j] << kPageShift) | (va[j] & kPageMask);
-        if (status[j] == PV_ST_OK) status[j] = walk_upper(st2, mid2, gpa[j], 1, &node[j], &val[j]) | 0x80000000u;
+        if (st[j] == PV_ST_OK) st[j] = upper<true>(st2, codes2, gpa[j], &code[j]) | 0x80000000u;
       }
 #pragma unroll
-      for (int j = 0; j < kVpt; ++j)
-        w[j] = (live[j] && status[j] == 0x80000000u) ? ld_word(image, 0, node[j], leaf_index(gpa[j])) : 0;
+      for (int j = 0; j < kVpt; ++j) w[j] = st[j] == 0x80000000u ? leaf_word(image, st2, code[j], gpa[j], pol_table) : 0;
 #pragma unroll
       for (int j = 0; j < kVpt; ++j) {
-        if (!(status[j] & 0x80000000u)) continue;
-        status[j] &= 0x7FFFFFFFu;
-        if (status[j] != PV_ST_OK) {
-          if (PV_ST_KIND(status[j]) == PV_ST_TRAP2) aux[j] = gpa[j];
-          continue;
-        }
-        const uint32_t li = leaf_index(gpa[j]);
-        if (w[j] & kFlagTrapping) {
-          status[j] = PV_ST_TRAP2 | 3u | (li << 16);
-          val[j] = node[j];
-          aux[j] = gpa[j];
-        } else if (!(w[j] & kFlagPresent)) {
-          status[j] = PV_ST_FAULT2 | 3u;
-          val[j] = gpa[j];
-        } else {
+        if (!(st[j] & 0x80000000u)) continue;
+        st[j] = leaf_status<true>(w[j], st[j] & 0x7FFFFFFFu, gpa[j]);
+        const uint32_t k = PV_ST_KIND(st[j]);
+        if (k == PV_ST_OK) {
           val[j] = w[j] >> kPageShift;
+        } else if (k == PV_ST_TRAP2) {
+          val[j] = trap_node(st2, st[j], code[j], gpa[j]);
+          aux[j] = gpa[j];
+        } else {
+          val[j] = gpa[j];
         }
       }
     }
 #pragma unroll
     for (int j = 0; j < kVpt; ++j) {
-      if (!live[j]) continue;
       const uint64_t i = lane0 + (uint64_t)j * kTpb + threadIdx.x;
+      if (i >= seg_end) continue;
       uint64_t v = val[j];
-      if (!kPfn && status[j] == PV_ST_OK) v = (v << kPageShift) | (va[j] & kPageMask);
-      __stcs(reinterpret_cast<unsigned long long*>(out_value) + i, (unsigned long long)v);
-      __stcs(out_status + i, status[j]);
-      if (out_aux != nullptr && PV_ST_KIND(status[j]) == PV_ST_TRAP2) out_aux[i] = aux[j];
+      if (!kPfn && st[j] == PV_ST_OK) v = (v << kPageShift) | (va[j] & kPageMask);
+      st_u64_stream(out_value + i, v, pol_stream);
+      st_u32_stream(out_status + i, st[j], pol_stream);
+      if (kTwo && out_aux != nullptr && PV_ST_KIND(st[j]) == PV_ST_TRAP2) out_aux[i] = aux[j];
     }
   }
 }
@@ -237,19 +253,19 @@ template <bool kTwo, bool kVa32, bool kPfn>
 static cudaError_t launch_t(const uint8_t* image, uint64_t image_bytes, const pv_space* spaces, const pv_seg* segs,
                             uint32_t n_segs, uint64_t n_chunks, const void* vas, uint64_t* out_value,
                             uint32_t* out_status, uint64_t* out_aux, cudaStream_t stream) {
-  const size_t smem = (kTwo ? 2 : 1) * 4 * 512 * sizeof(uint64_t);
   auto k = translate_kernel<kTwo, kVa32, kPfn>;
-  uint64_t grid = resident_grid((const void*)k, kTpb, smem);
+  uint64_t grid = resident_grid((const void*)k, kTpb, 0);
   if (grid > n_chunks) grid = n_chunks;
   if (grid == 0) return cudaSuccess;
-  k<<<(unsigned)grid, kTpb, smem, stream>>>(image, image_bytes, spaces, segs, n_segs, n_chunks, vas, out_value,
-                                            out_status, out_aux);
+  k<<<(unsigned)grid, kTpb, 0, stream>>>(image, image_bytes, spaces, segs, n_segs, n_chunks, vas, out_value,
+                                         out_status, out_aux);
   return cudaGetLastError();
 }
 
 cudaError_t launch_translate(const uint8_t* image, uint64_t image_bytes, const pv_space* spaces, const pv_seg* segs,
                              uint32_t n_segs, uint64_t n_chunks, const void* vas, uint32_t flags, bool two_stage,
                              uint64_t* out_value, uint32_t* out_status, uint64_t* out_aux, cudaStream_t stream) {
+  if (image_bytes >= (1ull << 41)) return cudaErrorInvalidValue;  // leaf pfns must fit the 29-bit codes
   const bool va32 = flags & PV_VA32, pfn = flags & PV_OUT_PFN;
 #define PV_DISPATCH(T, V, P)                                                                                    \
   if (two_stage == T && va32 == V && pfn == P)                                                                  \
