@@ -245,12 +245,6 @@ def run_ours(args, rank, world, local):
     for _ in range(args.warmup):
         step([torch.cuda.Event(enable_timing=True) for _ in range(5)])
     torch.cuda.synchronize()
-    # correctness of the timed configuration: no conflicts, every op complete
-    assert int(plan.conflict.item()) == 0, "conflicting destinations in the bench batch"
-    res = plan.results.cpu().numpy().view(np.uint64)
-    assert (res[:, 3] & 0xFFFFFFFF == 0).all() and (res[:, 0] == plan.host_ops[:, 1]).all()
-    st = wl.out[1]
-    n_faults = int((st != 0).sum().item())
 
     clocks = ClockSampler(local)
     clocks.start()
@@ -267,6 +261,11 @@ def run_ours(args, rank, world, local):
     torch.cuda.synchronize()
     barrier()
     clk = clocks.stop()
+    # correctness of the timed configuration: no conflicts, every op complete
+    assert int(plan.conflict.item()) == 0, "conflicting destinations in the bench batch"
+    res = plan.results.cpu().numpy().view(np.uint64)
+    assert (res[:, 3] & 0xFFFFFFFF == 0).all() and (res[:, 0] == plan.host_ops[:, 1]).all()
+    n_faults = int((wl.out[1] != 0).sum().item())
     total_ms = t_start.elapsed_time(t_end)
     tr_ms = sum(e[0].elapsed_time(e[1]) for e in evs)
     plan_ms = sum(e[2].elapsed_time(e[3]) for e in evs)
