@@ -101,6 +101,34 @@ typedef struct pv_seg {
   uint32_t reserved;
 } pv_seg;
 
+/* ---- leaf index ------------------------------------------------------------
+ * A derived, L2-resident 4-byte copy of the leaf-level page-table nodes a
+ * batch walks (the reference's 8-byte leaf PTEs of a large world do not fit
+ * the 126 MB L2).  Slot s caches image page slot_page[s] (absolute page
+ * number) as 512 codes:  bits 0-1 state (0 not present, 1 present,
+ * 2 trapping, 3 escape: read the raw PTE), bits 2-31 target pfn (present).
+ * slot_of[page] maps an image page to its slot (0xFFFFFFFF = not indexed).
+ * It is a cache keyed by page contents: pv_index_encode must re-run for a
+ * slot whenever its page changes (the host runtime does this for host writes
+ * and, via the device dirty map, for device writes).  Walks that reach a
+ * page that is not indexed read the raw PTE, so results never depend on
+ * what is indexed.
+ */
+typedef struct pv_index {
+  const uint32_t* slot_of;    /* device, one per image page                  */
+  const uint32_t* leaf_codes; /* device, 512 per slot                        */
+  const uint64_t* slot_page;  /* device, absolute image page of each slot    */
+  uint64_t n_slots;
+} pv_index;
+
+/* (Re)build leaf codes.  slots (device, may be NULL): encode slots[i] for
+ * i < n; NULL: encode slots first_slot .. first_slot+n-1.  dirty (device,
+ * one byte per image page, may be NULL): only slots whose page is marked. */
+int pv_index_encode(const uint8_t* image, uint64_t image_bytes,
+                    const uint64_t* slot_page, const uint64_t* slots,
+                    uint64_t first_slot, uint64_t n, uint32_t* leaf_codes,
+                    const uint8_t* dirty, void* stream);
+
 /* ---- translate flags ---------------------------------------------------- */
 #define PV_VA32 0x1u    /* vas is uint32_t[] (else uint64_t[])             */
 #define PV_OUT_PFN 0x2u /* value = leaf pfn (walk); else address with the
@@ -155,11 +183,14 @@ const char* pv_status_name(uint32_t status);
  * _resolve_page (memvirt.py:585-601) and resolve_hybrid (memvirt.py:677-682).
  * spaces / segs / vas / out_* are device pointers.  out_aux may be NULL
  * (then TDP-stage trap gpas are not reported).  Lanes not covered by any
- * segment are not written.
+ * segment are not written.  index (HOST pointer to a struct of device
+ * pointers, may be NULL): leaf index consulted instead of the raw leaf PTEs
+ * for indexed leaf nodes.
  */
 int pv_translate(const uint8_t* image, uint64_t image_bytes,
                  const pv_space* spaces, const pv_seg* segs, uint32_t n_segs,
                  uint64_t n_chunks, const void* vas, uint32_t flags,
+                 const pv_index* index,
                  uint64_t* out_value, uint32_t* out_status, uint64_t* out_aux,
                  void* stream);
 

@@ -56,7 +56,7 @@ FIFO_WORDS = 2 * FIFO_MAX + 4  # pv_fifo
 EXPORTS = (
     "pv_abi_version", "pv_translate_chunk", "pv_status_name", "pv_translate",
     "pv_fifo_replay", "pv_copy_plan", "pv_copy_stamp", "pv_copy_exec",
-    "pv_copy_fifo_replay", "pv_scatter_pages", "pv_gather_pages", "pv_stream_sync",
+    "pv_copy_fifo_replay", "pv_scatter_pages", "pv_gather_pages", "pv_stream_sync", "pv_index_encode",
 )
 
 _u64 = ctypes.c_uint64
@@ -67,7 +67,8 @@ _SIGNATURES = {
     "pv_abi_version": (ctypes.c_int, []),
     "pv_translate_chunk": (_u64, []),
     "pv_status_name": (ctypes.c_char_p, [_u32]),
-    "pv_translate": (ctypes.c_int, [_p, _u64, _p, _p, _u32, _u64, _p, _u32, _p, _p, _p, _p]),
+    "pv_translate": (ctypes.c_int, [_p, _u64, _p, _p, _u32, _u64, _p, _u32, _p, _p, _p, _p, _p]),
+    "pv_index_encode": (ctypes.c_int, [_p, _u64, _p, _p, _u64, _u64, _p, _p, _p]),
     "pv_fifo_replay": (ctypes.c_int, [_p, _u32, _p, _p, _u32, _p, _p, _p, _p]),
     "pv_copy_plan": (ctypes.c_int, [_p, _u64, _p, _p, _u64, _p, _u64, _u32, _p, _p, _p, _p, _p, _u32, _p, _p]),
     "pv_copy_stamp": (ctypes.c_int, [_p, _u64, _u64, _p, _p, _p, _u64, _u32, _p, _p]),

@@ -9,7 +9,10 @@
 
 namespace pv {
 cudaError_t launch_translate(const uint8_t*, uint64_t, const pv_space*, const pv_seg*, uint32_t, uint64_t,
-                             const void*, uint32_t, bool, uint64_t*, uint32_t*, uint64_t*, cudaStream_t);
+                             const void*, uint32_t, bool, const pv_index*, uint64_t*, uint32_t*, uint64_t*,
+                             cudaStream_t);
+cudaError_t launch_index_encode(const uint8_t*, uint64_t, const uint64_t*, const uint64_t*, uint64_t, uint64_t,
+                                uint32_t*, const uint8_t*, cudaStream_t);
 uint64_t translate_chunk();
 cudaError_t launch_copy_plan(const uint8_t*, uint64_t, const pv_space*, const pv_op*, uint64_t, const uint64_t*,
                              uint64_t, uint64_t*, uint32_t*, uint64_t*, uint64_t*, cudaStream_t);
@@ -94,15 +97,24 @@ const char* pv_status_name(uint32_t status) {
 }
 
 int pv_translate(const uint8_t* image, uint64_t image_bytes, const pv_space* spaces, const pv_seg* segs,
-                 uint32_t n_segs, uint64_t n_chunks, const void* vas, uint32_t flags, uint64_t* out_value,
-                 uint32_t* out_status, uint64_t* out_aux, void* stream) {
+                 uint32_t n_segs, uint64_t n_chunks, const void* vas, uint32_t flags, const pv_index* index,
+                 uint64_t* out_value, uint32_t* out_status, uint64_t* out_aux, void* stream) {
   if (n_chunks == 0) return PV_SUCCESS;
   if (!image || !spaces || !segs || !vas || !out_value || !out_status || n_segs == 0) return PV_EINVAL;
   if (image_bytes % kPageSize) return PV_EINVAL;
   if (flags & ~(uint32_t)(PV_VA32 | PV_OUT_PFN | PV_HAS_TWO_STAGE)) return PV_EINVAL;
   const bool two = flags & PV_HAS_TWO_STAGE;
-  return rc(launch_translate(image, image_bytes, spaces, segs, n_segs, n_chunks, vas, flags & 0x3u, two, out_value,
-                             out_status, out_aux, (cudaStream_t)stream));
+  if (index != nullptr && (!index->slot_of || !index->leaf_codes || !index->slot_page)) return PV_EINVAL;
+  return rc(launch_translate(image, image_bytes, spaces, segs, n_segs, n_chunks, vas, flags & 0x3u, two, index,
+                             out_value, out_status, out_aux, (cudaStream_t)stream));
+}
+
+int pv_index_encode(const uint8_t* image, uint64_t image_bytes, const uint64_t* slot_page, const uint64_t* slots,
+                    uint64_t first_slot, uint64_t n, uint32_t* leaf_codes, const uint8_t* dirty, void* stream) {
+  if (n == 0) return PV_SUCCESS;
+  if (!image || !slot_page || !leaf_codes || image_bytes % kPageSize) return PV_EINVAL;
+  return rc(launch_index_encode(image, image_bytes, slot_page, slots, first_slot, n, leaf_codes, dirty,
+                                (cudaStream_t)stream));
 }
 
 int pv_fifo_replay(const void* vas, uint32_t flags, const uint64_t* lane_idx, const uint64_t* proc_off,

@@ -14,10 +14,12 @@
 //               2 trapping (trap at level 2), 3 the walk already stopped at
 //               level 1 / 2 (status precomputed per top entry)
 //     bit  2    the leaf node lies past the image (struct.error at level 3)
-//     bits 3-31 leaf-node pfn
+//     bit  3    the leaf node is in the leaf index (pv.h pv_index)
+//     bits 4-31 leaf-index slot (bit 3 set) or leaf-node pfn
 // so resolving the two upper levels of a lane is ONE 4-byte shared-memory
-// read, and every stage costs exactly one dependent global load: the leaf
-// PTE.  Each thread walks 8 lanes at once with predicated (branch-free) code
+// read, and every stage costs exactly one dependent global load: a 4-byte
+// leaf-index code (L2-resident: half the bytes of the reference's 8-byte
+// PTEs) or, for leaf nodes outside the index, the raw leaf PTE.  Each thread walks 8 lanes at once with predicated (branch-free) code
 // (8 independent leaf loads in flight) and prefetches the next chunk's VAs
 // before gathering the current chunk's leaves; VAs stream in with
 // L1::no_allocate loads and results stream out with evict-first stores.
@@ -29,6 +31,9 @@ constexpr int kTpb = 256;
 constexpr int kVpt = 8;
 constexpr uint64_t kChunk = (uint64_t)kTpb * kVpt;  // lanes per chunk
 constexpr uint32_t kCodeStop = 3u;
+constexpr uint32_t kCodeOor = 4u;      // leaf node past the image
+constexpr uint32_t kCodeIndexed = 8u;  // payload is a leaf-index slot, not a pfn
+constexpr uint32_t kNoSlot = 0xFFFFFFFFu;
 
 struct Stage {
   uint64_t base;          // window base (bytes)
@@ -55,7 +60,8 @@ __device__ __forceinline__ uint64_t ld_stream_va(const void* vas, uint64_t i, bo
 // Stage the upper two levels of one walk stage (all threads; ends with a
 // barrier).  Requires image_bytes < 2^41 so leaf pfns fit 29 bits.
 __device__ void stage_codes(const uint8_t* __restrict__ image, uint64_t image_bytes, uint64_t base, uint64_t root,
-                            uint32_t stage2, Stage& s, uint32_t* codes /*[4*512]*/) {
+                            uint32_t stage2, Stage& s, uint32_t* codes /*[4*512]*/,
+                            const uint32_t* __restrict__ slot_of) {
   const uint32_t tid = threadIdx.x;
   const uint64_t lim = node_limit(image_bytes, base);
   if (tid < 4) {
@@ -89,9 +95,16 @@ __device__ void stage_codes(const uint8_t* __restrict__ image, uint64_t image_by
     if (s.top_status[t] == PV_ST_OK) {
       const uint64_t w = ld_word(image, base, s.top_node[t], i & 511);
       const uint64_t leaf = w >> kPageShift;
-      if (w & kFlagTrapping) code = 2u;
-      else if (!(w & kFlagPresent)) code = 0u;
-      else code = 1u | (leaf >= lim ? 4u : ((uint32_t)leaf << 3));
+      if (w & kFlagTrapping) {
+        code = 2u;
+      } else if (!(w & kFlagPresent)) {
+        code = 0u;
+      } else if (leaf >= lim) {
+        code = 1u | kCodeOor;
+      } else {
+        const uint32_t slot = slot_of != nullptr ? slot_of[(base >> kPageShift) + leaf] : kNoSlot;
+        code = slot != kNoSlot ? (1u | kCodeIndexed | (slot << 4)) : (1u | ((uint32_t)leaf << 4));
+      }
     }
     codes[i] = code;
   }
@@ -107,7 +120,7 @@ __device__ __forceinline__ uint32_t upper(const Stage& s, const uint32_t* codes,
   const uint32_t code = codes[(t << 9) | m];
   *code_out = code;
   const uint32_t kind = code & 3u;
-  const uint32_t st_present = (code & 4u) ? ((kStage2 ? PV_ST_NODE_OOR2 : PV_ST_NODE_OOR) | 3u) : PV_ST_OK;
+  const uint32_t st_present = (code & kCodeOor) ? ((kStage2 ? PV_ST_NODE_OOR2 : PV_ST_NODE_OOR) | 3u) : PV_ST_OK;
   const uint32_t st_np = (kStage2 ? PV_ST_FAULT2 : PV_ST_FAULT) | 2u;
   const uint32_t st_trap = (kStage2 ? PV_ST_TRAP2 : PV_ST_TRAP) | 2u | (m << 16);
   return kind == 1u ? st_present : kind == 0u ? st_np : kind == 2u ? st_trap : s.top_status[t];
@@ -121,22 +134,50 @@ __device__ __forceinline__ uint32_t leaf_status(uint64_t w, uint32_t st, uint64_
   return PV_ST_OK;
 }
 
-// Node pfn a trap reports: level 3 -> the leaf node, level 1/2 -> top_node.
-__device__ __forceinline__ uint64_t trap_node(const Stage& s, uint32_t st, uint32_t code, uint64_t x) {
-  return PV_ST_LEVEL(st) == 3u ? (uint64_t)(code >> 3) : s.top_node[top_index(x)];
+// Window-relative pfn of the leaf node a staged code points at.
+__device__ __forceinline__ uint64_t leaf_node_pfn(const Stage& s, uint32_t code,
+                                                  const uint64_t* __restrict__ slot_page) {
+  return (code & kCodeIndexed) ? slot_page[code >> 4] - (s.base >> kPageShift) : (uint64_t)(code >> 4);
 }
 
-__device__ __forceinline__ uint64_t leaf_word(const uint8_t* image, const Stage& s, uint32_t code, uint64_t x,
-                                              uint64_t pol) {
-  return ld_u64_hint(reinterpret_cast<const unsigned long long*>(image + s.base + ((uint64_t)(code >> 3) << kPageShift)) +
+// Node pfn a trap reports: level 3 -> the leaf node, level 1/2 -> top_node.
+__device__ __forceinline__ uint64_t trap_node(const Stage& s, uint32_t st, uint32_t code, uint64_t x,
+                                              const uint64_t* __restrict__ slot_page) {
+  return PV_ST_LEVEL(st) == 3u ? leaf_node_pfn(s, code, slot_page) : s.top_node[top_index(x)];
+}
+
+__device__ __forceinline__ uint64_t raw_leaf(const uint8_t* image, const Stage& s, uint64_t node, uint64_t x,
+                                             uint64_t pol) {
+  return ld_u64_hint(reinterpret_cast<const unsigned long long*>(image + s.base + (node << kPageShift)) +
                          leaf_index(x),
                      pol);
+}
+
+// Leaf PTE word of a lane whose upper levels resolved: from the leaf index
+// (decoded back into an equivalent word) or the raw table.
+__device__ __forceinline__ uint64_t leaf_word(const uint8_t* image, const Stage& s, uint32_t code, uint64_t x,
+                                              const uint32_t* __restrict__ leaf_codes,
+                                              const uint64_t* __restrict__ slot_page, uint64_t pol) {
+  if (code & kCodeIndexed) {
+    uint32_t lc;
+    asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;"
+        : "=r"(lc)
+        : "l"(leaf_codes + ((uint64_t)(code >> 4) << 9) + leaf_index(x)), "l"(pol));
+    const uint32_t k = lc & 3u;
+    if (k == 1u) return ((uint64_t)(lc >> 2) << kPageShift) | kFlagPresent;
+    if (k == 0u) return 0;
+    if (k == 2u) return kFlagTrapping;
+    return raw_leaf(image, s, leaf_node_pfn(s, code, slot_page), x, pol);  // escape
+  }
+  return raw_leaf(image, s, code >> 4, x, pol);
 }
 
 template <bool kTwo, bool kVa32, bool kPfn>
 __global__ void __launch_bounds__(kTpb, 3)
 translate_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const pv_space* __restrict__ spaces,
                  const pv_seg* __restrict__ segs, uint32_t n_segs, uint64_t n_chunks, const void* __restrict__ vas,
+                 const uint32_t* __restrict__ slot_of, const uint32_t* __restrict__ leaf_codes,
+                 const uint64_t* __restrict__ slot_page,
                  uint64_t* __restrict__ out_value, uint32_t* __restrict__ out_status, uint64_t* __restrict__ out_aux) {
   __shared__ __align__(16) uint32_t codes1[4 * 512];
   __shared__ __align__(16) uint32_t codes2[kTwo ? 4 * 512 : 1];
@@ -183,8 +224,8 @@ translate_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const 
       staged_space = seg.space;
       two = kTwo && sp.mode == PV_TWO_STAGE;
       __syncthreads();  // everyone is done with the previous staging
-      stage_codes(image, image_bytes, sp.s1_base, sp.s1_root_pfn, 0, st1, codes1);
-      if (two) stage_codes(image, image_bytes, 0, sp.s2_root_pfn, 1, st2, codes2);
+      stage_codes(image, image_bytes, sp.s1_base, sp.s1_root_pfn, 0, st1, codes1, slot_of);
+      if (two) stage_codes(image, image_bytes, 0, sp.s2_root_pfn, 1, st2, codes2, slot_of);
     }
     if (have_next) {
 #pragma unroll
@@ -203,13 +244,13 @@ translate_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const 
 #pragma unroll
     for (int j = 0; j < kVpt; ++j) st[j] = upper<false>(st1, codes1, va[j], &code[j]);
 #pragma unroll
-    for (int j = 0; j < kVpt; ++j) w[j] = st[j] == PV_ST_OK ? leaf_word(image, st1, code[j], va[j], pol_table) : 0;
+    for (int j = 0; j < kVpt; ++j) w[j] = st[j] == PV_ST_OK ? leaf_word(image, st1, code[j], va[j], leaf_codes, slot_page, pol_table) : 0;
     uint64_t val[kVpt], aux[kVpt];
 #pragma unroll
     for (int j = 0; j < kVpt; ++j) {
       st[j] = leaf_status<false>(w[j], st[j], va[j]);
       const uint32_t k = PV_ST_KIND(st[j]);
-      val[j] = k == PV_ST_OK ? (w[j] >> kPageShift) : k == PV_ST_TRAP ? trap_node(st1, st[j], code[j], va[j]) : va[j];
+      val[j] = k == PV_ST_OK ? (w[j] >> kPageShift) : k == PV_ST_TRAP ? trap_node(st1, st[j], code[j], va[j], slot_page) : va[j];
       aux[j] = 0;
     }
     if (kTwo && two) {
@@ -220,7 +261,7 @@ translate_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const 
         if (st[j] == PV_ST_OK) st[j] = upper<true>(st2, codes2, gpa[j], &code[j]) | 0x80000000u;
       }
 #pragma unroll
-      for (int j = 0; j < kVpt; ++j) w[j] = st[j] == 0x80000000u ? leaf_word(image, st2, code[j], gpa[j], pol_table) : 0;
+      for (int j = 0; j < kVpt; ++j) w[j] = st[j] == 0x80000000u ? leaf_word(image, st2, code[j], gpa[j], leaf_codes, slot_page, pol_table) : 0;
 #pragma unroll
       for (int j = 0; j < kVpt; ++j) {
         if (!(st[j] & 0x80000000u)) continue;
@@ -229,7 +270,7 @@ translate_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const 
         if (k == PV_ST_OK) {
           val[j] = w[j] >> kPageShift;
         } else if (k == PV_ST_TRAP2) {
-          val[j] = trap_node(st2, st[j], code[j], gpa[j]);
+          val[j] = trap_node(st2, st[j], code[j], gpa[j], slot_page);
           aux[j] = gpa[j];
         } else {
           val[j] = gpa[j];
@@ -251,26 +292,30 @@ translate_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const 
 
 template <bool kTwo, bool kVa32, bool kPfn>
 static cudaError_t launch_t(const uint8_t* image, uint64_t image_bytes, const pv_space* spaces, const pv_seg* segs,
-                            uint32_t n_segs, uint64_t n_chunks, const void* vas, uint64_t* out_value,
-                            uint32_t* out_status, uint64_t* out_aux, cudaStream_t stream) {
+                            uint32_t n_segs, uint64_t n_chunks, const void* vas, const pv_index* idx,
+                            uint64_t* out_value, uint32_t* out_status, uint64_t* out_aux, cudaStream_t stream) {
   auto k = translate_kernel<kTwo, kVa32, kPfn>;
   uint64_t grid = resident_grid((const void*)k, kTpb, 0);
   if (grid > n_chunks) grid = n_chunks;
   if (grid == 0) return cudaSuccess;
-  k<<<(unsigned)grid, kTpb, 0, stream>>>(image, image_bytes, spaces, segs, n_segs, n_chunks, vas, out_value,
-                                         out_status, out_aux);
+  const uint32_t* slot_of = idx != nullptr ? idx->slot_of : nullptr;
+  const uint32_t* leaf_codes = idx != nullptr ? idx->leaf_codes : nullptr;
+  const uint64_t* slot_page = idx != nullptr ? idx->slot_page : nullptr;
+  k<<<(unsigned)grid, kTpb, 0, stream>>>(image, image_bytes, spaces, segs, n_segs, n_chunks, vas, slot_of,
+                                         leaf_codes, slot_page, out_value, out_status, out_aux);
   return cudaGetLastError();
 }
 
 cudaError_t launch_translate(const uint8_t* image, uint64_t image_bytes, const pv_space* spaces, const pv_seg* segs,
                              uint32_t n_segs, uint64_t n_chunks, const void* vas, uint32_t flags, bool two_stage,
-                             uint64_t* out_value, uint32_t* out_status, uint64_t* out_aux, cudaStream_t stream) {
-  if (image_bytes >= (1ull << 41)) return cudaErrorInvalidValue;  // leaf pfns must fit the 29-bit codes
+                             const pv_index* idx, uint64_t* out_value, uint32_t* out_status, uint64_t* out_aux,
+                             cudaStream_t stream) {
+  if (image_bytes >= (1ull << 40)) return cudaErrorInvalidValue;  // leaf pfns / slots must fit 28-bit codes
   const bool va32 = flags & PV_VA32, pfn = flags & PV_OUT_PFN;
 #define PV_DISPATCH(T, V, P)                                                                                    \
   if (two_stage == T && va32 == V && pfn == P)                                                                  \
-    return launch_t<T, V, P>(image, image_bytes, spaces, segs, n_segs, n_chunks, vas, out_value, out_status, \
-                             out_aux, stream);
+    return launch_t<T, V, P>(image, image_bytes, spaces, segs, n_segs, n_chunks, vas, idx, out_value, \
+                             out_status, out_aux, stream);
   PV_DISPATCH(false, false, false)
   PV_DISPATCH(false, false, true)
   PV_DISPATCH(false, true, false)

@@ -19,6 +19,8 @@ Status words are decoded back into the reference's exceptions by
 
 from __future__ import annotations
 
+import ctypes
+import os
 import struct
 import threading
 from dataclasses import dataclass
@@ -135,7 +137,7 @@ def translate_one(image, space: Space, va: int, *, out_pfn: bool = False) -> tup
     one.dev.copy_(one.host, non_blocking=True)
     base = one.dev.data_ptr()
     flags = (N.OUT_PFN if out_pfn else 0) | (N.HAS_TWO_STAGE if space.mode == N.TWO_STAGE else 0)
-    N.check(lib.pv_translate(dev_img.data_ptr(), image.nbytes, base, base + 32, 1, 1, base + 64, flags,
+    N.check(lib.pv_translate(dev_img.data_ptr(), image.nbytes, base, base + 32, 1, 1, base + 64, flags, None,
                              base + 72, base + 88, base + 80, s.cuda_stream), "pv_translate")
     one.out.copy_(one.dev[9:13], non_blocking=True)
     s.synchronize()
@@ -159,16 +161,154 @@ def build_segments(bounds: list[tuple[int, int, int]]) -> np.ndarray:
     return np.array(rows, dtype=np.uint64).reshape(-1, 4), c0
 
 
-class TranslatePlan:
-    """Device-resident descriptors of a translate batch (reusable)."""
+class PvIndex(ctypes.Structure):
+    """pv_index (include/pv.h)."""
 
-    def __init__(self, spaces: list[Space], bounds: list[tuple[int, int, int]]):
+    _fields_ = [("slot_of", ctypes.c_void_p), ("leaf_codes", ctypes.c_void_p), ("slot_page", ctypes.c_void_p),
+                ("n_slots", ctypes.c_uint64)]
+
+
+NO_SLOT = 0xFFFFFFFF
+
+
+class LeafIndex:
+    """The leaf index of one MemoryImage (pv.h ``pv_index``): 4-byte codes of
+    the leaf-level table nodes that translate batches walk, L2-resident where
+    the reference's 8-byte PTEs are not.  A cache keyed by page contents:
+
+    * :meth:`ensure` indexes the leaf nodes reachable from some spaces (host
+      scan of their top and mid levels, then one encode launch);
+    * host writes to an indexed page re-encode its slot when the image pushes
+      them (:meth:`on_push`);
+    * device writes are caught through the image's device dirty map before
+      the map is cleared or the next translate launch (:meth:`sync_device_writes`).
+    Leaf nodes that are not indexed are walked through the raw PTEs, so the
+    index can only change speed, never results.
+    """
+
+    def __init__(self, image):
+        import torch
+
+        self.image = image
+        self.slot_of_host = np.full(image.npages, NO_SLOT, dtype=np.uint32)
+        self.pages = np.zeros(0, dtype=np.int64)
+        self.slot_of = torch.full((image.npages,), -1, dtype=torch.int32, device="cuda")
+        self.slot_page = torch.zeros(1, dtype=torch.int64, device="cuda")
+        self.codes = torch.zeros(512, dtype=torch.int32, device="cuda")
+        self.seen_dev_epoch = image.dev_write_epoch
+        self._abi = PvIndex()
+
+    @property
+    def n_slots(self) -> int:
+        return len(self.pages)
+
+    def leaf_pages(self, spaces: list["Space"]) -> np.ndarray:
+        """Absolute image pages of every leaf node the spaces can reach."""
+        img = self.image
+        host = img.host_for_read()
+        words = host[: img.nbytes - img.nbytes % 8].view(np.uint64)
+        out = []
+        for sp in spaces:
+            stages = [(sp.s1_base, sp.s1_root_pfn)]
+            if sp.mode == N.TWO_STAGE:
+                stages.append((0, sp.s2_root_pfn))
+            for base, root in stages:
+                if base % PAGE_SIZE:
+                    continue
+                lim = (img.nbytes - base) // PAGE_SIZE if base < img.nbytes else 0
+                if root >= lim:
+                    continue
+                top = words[(base + root * PAGE_SIZE) // 8:(base + root * PAGE_SIZE) // 8 + 4]
+                for w in top.tolist():
+                    if w & 4 or not w & 1 or (w >> PAGE_SHIFT) >= lim:
+                        continue
+                    at = (base + (w >> PAGE_SHIFT) * PAGE_SIZE) // 8
+                    mids = words[at:at + 512]
+                    ok = ((mids & np.uint64(5)) == np.uint64(1))
+                    leaf = (mids[ok] >> np.uint64(PAGE_SHIFT)).astype(np.uint64)
+                    leaf = leaf[leaf < np.uint64(lim)].astype(np.int64)
+                    out.append(leaf + base // PAGE_SIZE)
+        return np.unique(np.concatenate(out)) if out else np.zeros(0, dtype=np.int64)
+
+    def ensure(self, spaces: list["Space"]) -> None:
+        import torch
+
+        dev = self.image.device()
+        pages = self.leaf_pages(spaces)
+        new = pages[self.slot_of_host[pages] == NO_SLOT]
+        if len(new) == 0:
+            return
+        first = self.n_slots
+        slots = np.arange(first, first + len(new), dtype=np.int64)
+        self.slot_of_host[new] = slots.astype(np.uint32)
+        self.pages = np.concatenate([self.pages, new])
+        slot_page = torch.from_numpy(self.pages.copy()).to("cuda")
+        codes = torch.empty(self.n_slots * 512, dtype=torch.int32, device="cuda")
+        if first:
+            codes[: first * 512].copy_(self.codes[: first * 512])
+        self.slot_page, self.codes = slot_page, codes
+        self.slot_of[torch.from_numpy(new).to("cuda")] = torch.from_numpy(slots.astype(np.int32)).to("cuda")
+        self._encode(dev, None, first, len(new), None)
+
+    def _encode(self, dev, slots, first, n, dirty) -> None:
+        lib = N.lib()
+        N.check(lib.pv_index_encode(dev.data_ptr(), self.image.nbytes, self.slot_page.data_ptr(),
+                                    None if slots is None else slots.data_ptr(), first, n, self.codes.data_ptr(),
+                                    None if dirty is None else dirty.data_ptr(), _stream().cuda_stream),
+                "pv_index_encode")
+
+    def on_push(self, pages: np.ndarray, dev) -> None:
+        """Host wrote these pages (now in HBM): re-encode indexed ones."""
+        s = self.slot_of_host[pages]
+        s = s[s != NO_SLOT].astype(np.int64)
+        if len(s):
+            import torch
+
+            self._encode(dev, torch.from_numpy(s).to("cuda"), 0, len(s), None)
+
+    def sync_device_writes(self) -> None:
+        """Re-encode indexed pages the device wrote since the last sync."""
+        img = self.image
+        if self.seen_dev_epoch != img.dev_write_epoch and self.n_slots and img.on_device:
+            self._encode(img._dev, None, 0, self.n_slots, img.dirty_map())
+        self.seen_dev_epoch = img.dev_write_epoch
+
+    def abi(self) -> PvIndex:
+        self._abi.slot_of = self.slot_of.data_ptr()
+        self._abi.leaf_codes = self.codes.data_ptr()
+        self._abi.slot_page = self.slot_page.data_ptr()
+        self._abi.n_slots = self.n_slots
+        return self._abi
+
+
+def leaf_index(image) -> LeafIndex:
+    if image.leaf_index is None:
+        image.device()
+        image.leaf_index = LeafIndex(image)
+    return image.leaf_index
+
+
+class TranslatePlan:
+    """Device-resident descriptors of a translate batch (reusable).
+
+    ``image`` (optional) indexes the leaf nodes the spaces reach (pv.h leaf
+    index) so the walks gather 4-byte L2-resident codes; ``use_index=False``
+    walks the raw 8-byte PTEs only."""
+
+    def __init__(self, spaces: list[Space], bounds: list[tuple[int, int, int]], *, image=None,
+                 use_index: bool = True):
         segs, n_chunks = build_segments(bounds)
+        self.host_spaces = list(spaces)
         self.spaces = _to_dev(_i64([sp.words() for sp in spaces]).reshape(-1, 4))
         self.segs = _to_dev(segs.view(np.int64))
         self.n_segs = len(segs)
         self.n_chunks = n_chunks
         self.two = any(sp.mode == N.TWO_STAGE for sp in spaces)
+        self.use_index = use_index and os.environ.get("PV_LEAF_INDEX", "1") != "0"
+        self._indexed = False
+        if image is not None and self.use_index:
+            leaf_index(image).ensure(self.host_spaces)
+            self._indexed = True
 
 
 def translate_lanes(image, plan: TranslatePlan, vas, *, out_pfn: bool = False, out=None):
@@ -192,8 +332,16 @@ def translate_lanes(image, plan: TranslatePlan, vas, *, out_pfn: bool = False, o
     flags = (N.VA32 if vas.dtype == torch.int32 else 0) | (N.OUT_PFN if out_pfn else 0)
     if plan.two:
         flags |= N.HAS_TWO_STAGE
+    idx = None
+    if plan.use_index:
+        li = leaf_index(image)
+        if not plan._indexed:
+            li.ensure(plan.host_spaces)
+            plan._indexed = True
+        li.sync_device_writes()
+        idx = ctypes.byref(li.abi())
     N.check(lib.pv_translate(dev_img.data_ptr(), image.nbytes, plan.spaces.data_ptr(), plan.segs.data_ptr(),
-                             plan.n_segs, plan.n_chunks, vas.data_ptr(), flags, value.data_ptr(),
+                             plan.n_segs, plan.n_chunks, vas.data_ptr(), flags, idx, value.data_ptr(),
                              status.data_ptr(), aux.data_ptr(), _stream().cuda_stream), "pv_translate")
     return value, status, aux
 

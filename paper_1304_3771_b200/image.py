@@ -67,6 +67,8 @@ class MemoryImage:
         self._dev = None          # torch.uint8 [nbytes]
         self._dev_dirty = None    # torch.uint8 [npages]
         self._dev_dirty_any = False
+        self.dev_write_epoch = 0  # bumped by every device write (leaf-index coherence)
+        self.leaf_index = None    # dataplane.LeafIndex, created on first indexed translate
         self._lock = threading.RLock()
 
     @classmethod
@@ -138,6 +140,7 @@ class MemoryImage:
 
     def note_device_write(self) -> None:
         self._dev_dirty_any = True
+        self.dev_write_epoch += 1
 
     def push(self) -> None:
         """Scatter host-dirty pages into HBM."""
@@ -159,6 +162,8 @@ class MemoryImage:
                 _native.check(lib.pv_scatter_pages(self._dev.data_ptr(), self.nbytes, pfns.data_ptr(),
                                                    len(idx), src.data_ptr(), stream.cuda_stream),
                               "pv_scatter_pages")
+                if self.leaf_index is not None:
+                    self.leaf_index.on_push(idx, self._dev)
                 stream.synchronize()  # staging buffers are freed at scope exit
             self._host_dirty[:] = False
             self._host_dirty_any = False
@@ -173,6 +178,8 @@ class MemoryImage:
                 return
             lib = _native.lib()
             stream = torch.cuda.current_stream()
+            if self.leaf_index is not None:
+                self.leaf_index.sync_device_writes()  # before the dirty map is cleared
             dmap = self._dev_dirty.cpu().numpy()
             pages = np.flatnonzero(dmap)
             host2d = self.host.reshape(self.npages, PAGE_SIZE)

@@ -38,13 +38,14 @@ def test_library_exports_every_symbol():
 def test_argument_validation_needs_no_gpu():
     lib = N.load()
     # NULL buffers are rejected before any CUDA call
-    assert lib.pv_translate(None, 4096, None, None, 1, 1, None, 0, None, None, None, None) == N.EINVAL
+    assert lib.pv_translate(None, 4096, None, None, 1, 1, None, 0, None, None, None, None, None) == N.EINVAL
     assert lib.pv_copy_plan(None, 4096, None, None, 1, None, 1, 0, None, None, None, None, None, 0, None,
                             None) == N.EINVAL
     # bad image size / flags
     assert lib.pv_translate(ctypes.c_void_p(8), 4095, ctypes.c_void_p(8), ctypes.c_void_p(8), 1, 1,
-                            ctypes.c_void_p(8), 0, ctypes.c_void_p(8), ctypes.c_void_p(8), None,
+                            ctypes.c_void_p(8), 0, None, ctypes.c_void_p(8), ctypes.c_void_p(8), None,
                             None) == N.EINVAL
+    assert lib.pv_index_encode(None, 4096, None, None, 0, 1, None, None, None) == N.EINVAL
 
 
 def test_compute_entry_points_fail_loudly_without_gpu():

@@ -250,3 +250,62 @@ def test_lanes_api_rejects_missing_gpu_never_falls_back(cuda):
     # the data plane is the CUDA library: it must be the thing loaded
     lib = N.lib()
     assert lib.pv_abi_version() == N.ABI_VERSION
+
+
+def _oracle_of(memv, tr, vas):
+    raw = np.frombuffer(S.image_bytes(memv.host_mem), dtype=np.uint8).copy()
+    sp = tr.device_space
+    return O.translate(raw, O.space(sp.s1_base, sp.s1_root_pfn, sp.s2_root_pfn, sp.mode), vas, threads=0)
+
+
+@pytest.mark.parametrize("mode", ["shadow", "tdp"])
+def test_leaf_index_coherent_with_host_and_device_writes(cuda, mode):
+    """The leaf index is a cache: host edits of indexed leaf nodes, device
+    copies that land inside a leaf node, and index on/off all agree with the
+    oracle on the current tables."""
+    memv = mv.MemoryVirtualizer()
+    g = memv.add_guest(0, mode)
+    sp = memv.create_process(g)
+    memv.map_region(sp, S.BUF, 600)  # two leaf nodes
+    tr = memv.translator(sp, use_cache=False)
+    rng = random.Random(12)
+    vas = np.array([S.BUF + rng.randrange(700 * 4096) for _ in range(50_000)], dtype=np.uint64)
+
+    def check():
+        hpa, st, aux = tr.translate_batch(vas)
+        v, s, a = _oracle_of(memv, tr, vas)
+        assert np.array_equal(st, s) and np.array_equal(hpa, v)
+        space = tr.device_space
+        plan = dp.TranslatePlan([space], [(0, len(vas), 0)], use_index=False)
+        d = torch.tensor(vas.view(np.int64), device="cuda")
+        v2, s2, _ = dp.translate_lanes(memv.host_mem.backing, plan, d)
+        assert np.array_equal(s2.cpu().numpy().view(np.uint32), s)
+        assert np.array_equal(v2.cpu().numpy().view(np.uint64), v)
+
+    check()
+    # host edit of an indexed leaf node
+    if mode == "shadow":
+        ed = mv.TableEditor(memv.host_mem, sp.shadow_root, memv.host_alloc.alloc)
+        ed.set_leaf_state(S.BUF + 7 * 4096, mv.EntryState.TRAPPING)
+    else:
+        ed = mv.TableEditor(g.mem, sp.guest_root, g.os_alloc.alloc)
+    ed.set_leaf_state(S.BUF + 9 * 4096, mv.EntryState.NOT_PRESENT)
+    ed.map(S.BUF + 11 * 4096, 0x7FFF_FFFF, replace=True)  # pfn beyond 2^30 -> escape code
+    check()
+    # a device copy that writes into a leaf node page (shadow: the shadow leaf;
+    # tdp: the guest's own leaf node, reached through a driver mapping)
+    if mode == "shadow":
+        leaf_page = memv.host_mem.read_word(memv.host_mem.read_word(sp.shadow_root.root_pfn, 0) >> 12,
+                                            (S.BUF >> 21) & 0x1FF) >> 12
+        hpa = leaf_page << 12
+    else:
+        top = g.mem.read_word(sp.guest_root.root_pfn, 0) >> 12
+        leaf_page = g.mem.read_word(top, (S.BUF >> 21) & 0x1FF) >> 12
+        hpa = g.base_hpa + (leaf_page << 12)
+    memv.map_page_into_guest(sp, 0x5000_0000, hpa, mode)
+    words = np.array([(0x1234 + i) << 12 | (1 if i % 3 else 4 if mode == "shadow" else 0) for i in range(64)],
+                     dtype=np.uint64)
+    n = mv.copy_user_buffer("to_guest", 0x5000_0000 + 8 * 32, 64 * 8, words.tobytes(), translator=tr,
+                            host_mem=memv.host_mem)
+    assert n == 512
+    check()
