@@ -23,6 +23,8 @@
 // (8 independent leaf loads in flight) and prefetches the next chunk's VAs
 // before gathering the current chunk's leaves; VAs stream in with
 // L1::no_allocate loads and results stream out with evict-first stores.
+#include <type_traits>
+
 #include "pv_common.cuh"
 
 namespace pv {
@@ -173,7 +175,7 @@ __device__ __forceinline__ uint64_t leaf_word(const uint8_t* image, const Stage&
 }
 
 template <bool kTwo, bool kVa32, bool kPfn>
-__global__ void __launch_bounds__(kTpb, 3)
+__global__ void __launch_bounds__(kTpb, kTwo ? 3 : 4)
 translate_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const pv_space* __restrict__ spaces,
                  const pv_seg* __restrict__ segs, uint32_t n_segs, uint64_t n_chunks, const void* __restrict__ vas,
                  const uint32_t* __restrict__ slot_of, const uint32_t* __restrict__ leaf_codes,
@@ -206,16 +208,17 @@ translate_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const 
       seg_chunks = (seg.end - seg.begin + kChunk - 1) / kChunk;
     }
   };
-  auto load_vas = [&](uint64_t c, uint64_t (&va)[kVpt]) {
+  using VaT = typename std::conditional<kVa32, uint32_t, uint64_t>::type;
+  auto load_vas = [&](uint64_t c, VaT (&va)[kVpt]) {
     const uint64_t lane0 = seg.begin + (c - seg.chunk0) * kChunk;
 #pragma unroll
     for (int j = 0; j < kVpt; ++j) {
       const uint64_t i = lane0 + (uint64_t)j * kTpb + threadIdx.x;
-      va[j] = i < seg.end ? ld_stream_va(vas, i, kVa32, pol_stream) : 0;
+      va[j] = i < seg.end ? (VaT)ld_stream_va(vas, i, kVa32, pol_stream) : 0;
     }
   };
 
-  uint64_t va[kVpt], nva[kVpt];
+  VaT va[kVpt], nva[kVpt];
   bool have_next = false;
   for (uint64_t c = c_begin; c < c_end; ++c) {
     find_seg(c);
