@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--workload", choices=["c5", "c1"], default="c5")
     ap.add_argument("--scale", type=int, default=1, help="shrink C5 by this factor (testing only)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--gather", action="store_true", help="return every guest's translations to rank 0 after "
+                    "timing (point-to-point over NCCL = NVLink peer copies) and report its time")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-vas", type=int, default=16 << 20)
     ap.add_argument("--cpu-sample-bytes", type=int, default=1 << 30)
@@ -127,6 +129,7 @@ class Workload:
         import torch
 
         from paper_1304_3771_b200 import dataplane as dp
+        from paper_1304_3771_b200 import shard
         from paper_1304_3771_b200 import workloads as W
 
         self.name = name
@@ -137,7 +140,7 @@ class Workload:
             wd = W.build_c5(cfg)
             self.world = wd
             self.memv = wd.memv
-            owned = [g for g in range(cfg.guests) if g % world == rank]
+            owned = shard.owned_guests(cfg.guests, rank, world)
             self.owned = owned
             t_spaces, bounds, vas_parts, self.proc_vas = [], [], [], []
             lane = 0
@@ -271,10 +274,11 @@ def run_ours(args, rank, world, local):
     plan_ms = sum(e[2].elapsed_time(e[3]) for e in evs)
     exec_ms = sum(e[3].elapsed_time(e[4]) for e in evs)
     copy_ms = sum(e[1].elapsed_time(e[4]) for e in evs)
-    local_t = torch.tensor([total_ms, tr_ms, copy_ms, exec_ms, plan_ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        tdist.all_reduce(local_t, op=tdist.ReduceOp.MAX)
-    total_ms, tr_ms, copy_ms, exec_ms, plan_ms = local_t.tolist()
+    from paper_1304_3771_b200 import shard
+
+    total_ms, tr_ms, copy_ms, exec_ms, plan_ms = shard.max_over_ranks(
+        [total_ms, tr_ms, copy_ms, exec_ms, plan_ms], world, device="cuda")
+    gather = gather_results(wl, rank, world) if (args.gather and wl.name == "c5") else None
     K = args.steps
     trans_per_s = wl.total_vas * K / (tr_ms / 1e3) if world > 0 else 0.0
     copy_gbs = wl.total_copy_bytes * K / (copy_ms / 1e3) / 1e9
@@ -317,6 +321,7 @@ def run_ours(args, rank, world, local):
                           "note": "16 B/translation (u32 VA in, u64 hpa + u32 status out); leaf-PTE gathers "
                                   "are extra traffic"},
         "faulting_lanes": n_faults,
+        "gather_to_rank0": gather,
         "gpu_launches": 4 * K,
         "clocks": clk,
         "e2e": e2e,
@@ -325,6 +330,38 @@ def run_ours(args, rank, world, local):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(wl, args)
     return line
+
+
+def gather_results(wl, rank, world):
+    """Return each owned guest's translation results to rank 0 (timed
+    separately from the step: it is result delivery, not the data plane)."""
+    import torch
+
+    from paper_1304_3771_b200 import shard
+
+    cfg = wl.cfg
+    value, status, _ = wl.out
+    per_guest, lane = {}, 0
+    for g in shard.owned_guests(cfg.guests, rank, world):
+        n = cfg.vas_per_guest
+        per_guest[g] = {"value": value[lane:lane + n], "status": status[lane:lane + n]}
+        lane += n
+
+    def like(g):
+        return {"value": torch.empty(cfg.vas_per_guest, dtype=torch.int64, device="cuda"),
+                "status": torch.empty(cfg.vas_per_guest, dtype=torch.int32, device="cuda")}
+
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    got = shard.gather_to_rank0(per_guest, cfg.guests, rank, world, like)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    (dt,) = shard.max_over_ranks([dt], world, device="cuda")
+    nbytes = cfg.guests * cfg.vas_per_guest * 12
+    ok = None
+    if rank == 0:
+        ok = sorted(got) == list(range(cfg.guests))
+    return {"ms": dt * 1e3, "bytes": nbytes, "remote_bytes": nbytes * (world - 1) // world, "complete": ok}
 
 
 def run_e2e(wl, args, world):
