@@ -395,7 +395,7 @@ def run_e2e(wl, args, world):
         t.random_(0, 256)
 
     h2d = sum(t.numel() * 4 for t, _, _ in host_vas) + sum(t.numel() for t, *_ in payload)
-    d2h = sum(t.numel() * 20 for t, _, _ in host_vas) + sum(len(ops) * 32 for *_, ops in payload)
+    d2h = sum(t.numel() * 12 for t, _, _ in host_vas) + sum(len(ops) * 32 for *_, ops in payload)
 
     def one_step():
         t0 = time.perf_counter()

@@ -202,32 +202,44 @@ class LeafIndex:
     def n_slots(self) -> int:
         return len(self.pages)
 
+    def _device_pages(self, pages: list[int]) -> np.ndarray:
+        """Whole pages read from HBM (always current: host writes are pushed
+        first), so scanning tables never pulls the device's data writes back."""
+        import torch
+
+        if not pages:
+            return np.zeros((0, PAGE_SIZE // 8), dtype=np.uint64)
+        dev = self.image.device()
+        pfns = torch.tensor(np.asarray(pages, dtype=np.int64), device="cuda")
+        dst = torch.empty(len(pages) * PAGE_SIZE, dtype=torch.uint8, device="cuda")
+        N.check(N.lib().pv_gather_pages(dev.data_ptr(), self.image.nbytes, pfns.data_ptr(), len(pages),
+                                        dst.data_ptr(), _stream().cuda_stream), "pv_gather_pages")
+        return dst.cpu().numpy().view(np.uint64).reshape(len(pages), PAGE_SIZE // 8)
+
     def leaf_pages(self, spaces: list["Space"]) -> np.ndarray:
         """Absolute image pages of every leaf node the spaces can reach."""
-        img = self.image
-        host = img.host_for_read()
-        words = host[: img.nbytes - img.nbytes % 8].view(np.uint64)
-        out = []
+        nbytes = self.image.nbytes
+        stages = []
         for sp in spaces:
-            stages = [(sp.s1_base, sp.s1_root_pfn)]
+            stages.append((sp.s1_base, sp.s1_root_pfn))
             if sp.mode == N.TWO_STAGE:
                 stages.append((0, sp.s2_root_pfn))
-            for base, root in stages:
-                if base % PAGE_SIZE:
-                    continue
-                lim = (img.nbytes - base) // PAGE_SIZE if base < img.nbytes else 0
-                if root >= lim:
-                    continue
-                top = words[(base + root * PAGE_SIZE) // 8:(base + root * PAGE_SIZE) // 8 + 4]
-                for w in top.tolist():
-                    if w & 4 or not w & 1 or (w >> PAGE_SHIFT) >= lim:
-                        continue
-                    at = (base + (w >> PAGE_SHIFT) * PAGE_SIZE) // 8
-                    mids = words[at:at + 512]
-                    ok = ((mids & np.uint64(5)) == np.uint64(1))
-                    leaf = (mids[ok] >> np.uint64(PAGE_SHIFT)).astype(np.uint64)
-                    leaf = leaf[leaf < np.uint64(lim)].astype(np.int64)
-                    out.append(leaf + base // PAGE_SIZE)
+        stages = [(b, r) for b, r in dict.fromkeys(stages)
+                  if b % PAGE_SIZE == 0 and b < nbytes and r < (nbytes - b) // PAGE_SIZE]
+        roots = self._device_pages([b // PAGE_SIZE + r for b, r in stages])
+        mids = []  # (absolute mid page, window base)
+        for (base, _), words in zip(stages, roots):
+            lim = (nbytes - base) // PAGE_SIZE
+            for w in words[:4].tolist():
+                if not (w & 4 or not w & 1 or (w >> PAGE_SHIFT) >= lim):
+                    mids.append((base // PAGE_SIZE + (w >> PAGE_SHIFT), base))
+        mids = list(dict.fromkeys(mids))
+        out = []
+        for (_, base), words in zip(mids, self._device_pages([m for m, _ in mids])):
+            lim = np.uint64((nbytes - base) // PAGE_SIZE)
+            ok = (words & np.uint64(5)) == np.uint64(1)
+            leaf = words[ok] >> np.uint64(PAGE_SHIFT)
+            out.append(leaf[leaf < lim].astype(np.int64) + base // PAGE_SIZE)
         return np.unique(np.concatenate(out)) if out else np.zeros(0, dtype=np.int64)
 
     def ensure(self, spaces: list["Space"]) -> None:
@@ -343,6 +355,59 @@ def translate_lanes(image, plan: TranslatePlan, vas, *, out_pfn: bool = False, o
     N.check(lib.pv_translate(dev_img.data_ptr(), image.nbytes, plan.spaces.data_ptr(), plan.segs.data_ptr(),
                              plan.n_segs, plan.n_chunks, vas.data_ptr(), flags, idx, value.data_ptr(),
                              status.data_ptr(), aux.data_ptr(), _stream().cuda_stream), "pv_translate")
+    return value, status, aux
+
+
+def translate_host_pipelined(image, space: Space, host_vas, chunk: int = 1 << 22):
+    """Translate a (pinned) host tensor of VAs; results come back as pinned
+    host tensors.  Chunks overlap: H2D of chunk i+1 and D2H of chunk i-1 run
+    on side streams while chunk i translates.  ``aux`` only travels for
+    two-stage spaces (one-stage walks never produce a TDP-stage trap)."""
+    import torch
+
+    n = host_vas.numel()
+    dtype = host_vas.dtype if host_vas.dtype in (torch.int32, torch.int64) else torch.int64
+    src = host_vas if host_vas.dtype == dtype else host_vas.to(dtype)
+    if not src.is_pinned():
+        src = src.pin_memory()
+    value = torch.empty(n, dtype=torch.int64, pin_memory=True)
+    status = torch.empty(n, dtype=torch.int32, pin_memory=True)
+    two = space.mode == N.TWO_STAGE
+    aux = torch.empty(n, dtype=torch.int64, pin_memory=True) if two else torch.zeros(n, dtype=torch.int64)
+    if n == 0:
+        return value, status, aux
+    compute = torch.cuda.current_stream()
+    h2d, d2h = torch.cuda.Stream(), torch.cuda.Stream()
+    plans = {}
+    bufs = []
+    for b in range(2):
+        bufs.append((torch.empty(chunk, dtype=dtype, device="cuda"), torch.empty(chunk, dtype=torch.int64, device="cuda"),
+                     torch.empty(chunk, dtype=torch.int32, device="cuda"), torch.zeros(chunk, dtype=torch.int64, device="cuda"),
+                     torch.cuda.Event(), torch.cuda.Event(), torch.cuda.Event()))
+    for i, start in enumerate(range(0, n, chunk)):
+        m = min(chunk, n - start)
+        d_vas, d_val, d_st, d_aux, ev_in, ev_done, ev_out = bufs[i % 2]
+        if i >= 2:
+            h2d.wait_event(ev_out)  # buffers of chunk i-2 fully drained
+        with torch.cuda.stream(h2d):
+            d_vas[:m].copy_(src[start:start + m], non_blocking=True)
+            ev_in.record(h2d)
+        compute.wait_event(ev_in)
+        if m not in plans:
+            plans[m] = TranslatePlan([space], [(0, m, 0)], image=image)
+        if two:
+            d_aux[:m].zero_()
+        translate_lanes(image, plans[m], d_vas[:m], out=(d_val[:m], d_st[:m], d_aux[:m]))
+        ev_done.record(compute)
+        d2h.wait_event(ev_done)
+        with torch.cuda.stream(d2h):
+            value[start:start + m].copy_(d_val[:m], non_blocking=True)
+            status[start:start + m].copy_(d_st[:m], non_blocking=True)
+            if two:
+                aux[start:start + m].copy_(d_aux[:m], non_blocking=True)
+            ev_out.record(d2h)
+    d2h.synchronize()
+    compute.synchronize()
     return value, status, aux
 
 

@@ -844,6 +844,10 @@ def translate_batch(translator: ProcessTranslator, gvas, *, use_cache: bool | No
 
     on_device = isinstance(gvas, torch.Tensor) and gvas.is_cuda
     host_tensor = isinstance(gvas, torch.Tensor) and not gvas.is_cuda
+    cache_on = translator.use_cache if use_cache is None else use_cache
+    if host_tensor and not cache_on:
+        # host in / host out: chunked H2D | translate | D2H pipeline
+        return dp.translate_host_pipelined(translator.image, translator.device_space, gvas)
     if on_device:
         vas = gvas if gvas.dtype in (torch.int64, torch.int32) else gvas.to(torch.int64)
     elif host_tensor:
@@ -857,7 +861,6 @@ def translate_batch(translator: ProcessTranslator, gvas, *, use_cache: bool | No
     n = vas.numel()
     plan = dp.TranslatePlan([translator.device_space], [(0, n, 0)])
     value, status, aux = dp.translate_lanes(translator.image, plan, vas)
-    cache_on = translator.use_cache if use_cache is None else use_cache
     if cache_on and n:
         fifo = dp._to_dev(dp.pack_fifo([translator.cache]))
         lane_idx = torch.arange(n, dtype=torch.int64, device="cuda")

@@ -309,3 +309,21 @@ def test_leaf_index_coherent_with_host_and_device_writes(cuda, mode):
                             host_mem=memv.host_mem)
     assert n == 512
     check()
+
+
+@pytest.mark.parametrize("mode", ["shadow", "tdp"])
+def test_host_pipelined_translate_equals_device_path(cuda, mode):
+    memv = mv.MemoryVirtualizer()
+    g = memv.add_guest(0, mode)
+    sp = memv.create_process(g)
+    memv.map_region(sp, S.BUF, 300)
+    tr = memv.translator(sp, use_cache=False)
+    rng = np.random.default_rng(3)
+    vas = (S.BUF + rng.integers(0, 400 * 4096, 25_000)).astype(np.uint32)
+    v, s, a = dp.translate_host_pipelined(memv.host_mem.backing, tr.device_space,
+                                          torch.from_numpy(vas.view(np.int32)), chunk=4096)
+    hv, hs, ha = tr.translate_batch(vas.astype(np.uint64))
+    assert np.array_equal(v.numpy().view(np.uint64), hv)
+    assert np.array_equal(s.numpy().view(np.uint32), hs)
+    assert np.array_equal(a.numpy().view(np.uint64), ha)
+    assert (hs != 0).any() and (hs == 0).any()
