@@ -195,17 +195,28 @@ int pv_translate(const uint8_t* image, uint64_t image_bytes,
                  void* stream);
 
 /* ---- K4: FIFO cache replay --------------------------------------------------
- * Applies the per-process FIFO-10 translation cache (memvirt.py:336-374,
- * 585-594) to a batch of lanes that pv_translate resolved fresh: lanes of
- * process p are lane_idx[proc_off[p] .. proc_off[p+1]) in lookup order.  A
- * hit replaces the lane's value/status with the cached translation; a miss
- * that resolved inserts (oldest-first eviction); a miss that faulted keeps
- * the fault and inserts nothing.  fifo[] is updated in place (device).
- * flags: PV_VA32 as for pv_translate.
+ * Applies the per-process FIFO translation cache (memvirt.py:336-374,
+ * 585-594) to lookups that pv_translate / pv_copy_plan resolved fresh.
+ * Lookups of process p are positions proc_off[p] .. proc_off[p+1]) of a
+ * lookup stream in program order; win_off[p] = sum over q < p of
+ * ceil(lookups_q / 32) (n_procs + 1 entries).  Every process uses the same
+ * `capacity` (1..PV_FIFO_MAX).  A hit replaces the lookup's value/status with
+ * the cached translation; a miss that resolved inserts (oldest-first
+ * eviction); a miss that faulted keeps the fault and inserts nothing.
+ * fifo[] (device) is updated in place (entries rewritten oldest-first with
+ * head 0, counters advanced).  Exact; parallel over 32-lookup windows with
+ * sequential verification (see pv_fifo.cu).  scratch: device memory of
+ * pv_fifo_scratch_bytes(lookups, windows, capacity) bytes.
  */
+uint64_t pv_fifo_scratch_bytes(uint64_t n_lookups, uint64_t n_windows, uint32_t capacity);
+
+/* Lanes of a pv_translate batch: lookup l is lane lane_idx[l] (device);
+ * key = vas[lane] >> 12.  flags: PV_VA32 as for pv_translate. */
 int pv_fifo_replay(const void* vas, uint32_t flags, const uint64_t* lane_idx,
-                   const uint64_t* proc_off, uint32_t n_procs, pv_fifo* fifo,
-                   uint64_t* value, uint32_t* status, void* stream);
+                   const uint64_t* proc_off, const uint64_t* win_off,
+                   uint32_t n_procs, uint32_t capacity, pv_fifo* fifo,
+                   uint64_t* value, uint32_t* status, void* scratch,
+                   uint64_t scratch_bytes, void* stream);
 
 /* ---- K2/K3: batched user-buffer copy -------------------------------------
  * Replaces copy_user_buffer (memvirt.py:604-628) as used by
@@ -254,17 +265,19 @@ int pv_copy_stamp(const uint64_t* page_off, uint64_t n_ops, uint64_t n_pages,
                   uint64_t* page_owner, uint64_t owner_pages, uint32_t epoch,
                   uint32_t* conflict, void* stream);
 
-/* Replays the FIFO cache over a copy plan (lookups in op order, page order,
- * each op stopping at its first miss that fails to resolve), rewriting
- * page_hpa / page_status / op_first_bad so pv_copy_exec sees cached
- * translations.  op_idx lists the ops of process p at
- * op_idx[proc_off[p] .. proc_off[p+1]) in program order. */
+/* Replays the FIFO cache over a copy plan: lookup l is page look_page[l]
+ * of op look_op[l] (pages of an op consecutive and in order, ops of a
+ * process in program order).  Each op stops at its first page that misses
+ * and fails to resolve or whose data access is out of range; page_hpa /
+ * page_status are rewritten for cache hits and op_first_bad recomputed for
+ * every op in the stream, so pv_copy_exec sees the cached translations. */
 int pv_copy_fifo_replay(const pv_op* ops, const uint64_t* page_off,
-                        const uint64_t* op_idx, const uint64_t* proc_off,
-                        uint32_t n_procs, pv_fifo* fifo, uint64_t image_bytes,
-                        uint32_t direction, uint64_t* page_hpa,
+                        const uint64_t* look_page, const uint32_t* look_op,
+                        const uint64_t* proc_off, const uint64_t* win_off,
+                        uint32_t n_procs, uint32_t capacity, pv_fifo* fifo,
+                        uint64_t image_bytes, uint64_t* page_hpa,
                         uint32_t* page_status, uint64_t* op_first_bad,
-                        void* stream);
+                        void* scratch, uint64_t scratch_bytes, void* stream);
 
 /* ---- utility kernels used by the host runtime ---------------------------- */
 /* Scatter `n` whole pages from a (pinned) host staging area into the image:

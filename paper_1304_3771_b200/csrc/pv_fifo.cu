@@ -1,216 +1,510 @@
 // pv_fifo.cu — K4: exact replay of the per-process FIFO translation cache.
 //
 // The reference's TranslationCache (memvirt.py:336-374) is a per-process
-// FIFO of (gva page, hpa page) pairs: capacity 10, linear lookup, insert only
-// on a miss that resolved, oldest-first eviction independent of hits, hit /
-// miss counters.  ProcessTranslator.translate (memvirt.py:585-594) consults
-// it before walking.  Results may differ from a fresh walk when an entry is
+// FIFO of (gva page, hpa page): capacity 10, linear lookup, insert only on a
+// miss that resolved, oldest-first eviction independent of hits, hit / miss
+// counters.  ProcessTranslator.translate (memvirt.py:585-594) consults it
+// before walking.  Results may differ from a fresh walk when an entry is
 // stale (tables edited without flush_page, e.g. backend.py:164-174 or the
 // trap shim backend.py:288-296), and the counters are pinned metrics
-// (harness.py:180-184), so the replay is exact and order-preserving.
+// (harness.py:180-184), so the replay must be exact and order-preserving --
+// an inherently sequential automaton.  It is parallelised here in three
+// exact steps over 32-lookup windows of each process's lookup stream:
 //
-// B200 design: one warp per process.  Lane i holds ring slot i of the cache
-// (key, value); a lookup is a broadcast key, one __ballot_sync compare over
-// the live slots and a shuffle of the hit value.  Lookup inputs are fetched
-// 32 at a time (one per lane, coalesced) and results written back 32 at a
-// time, so the sequential part is only the compare/insert chain.
+//  1. speculate (one warp per window, all windows in parallel): rebuild the
+//     window's start state by replaying the H previous windows from an empty
+//     cache (or exactly from the initial cache near the stream start), then
+//     replay the window; record start state S'w, end state E'w, per-lookup
+//     hit/terminate flags and hit values;
+//  2. link (one thread per window): match[w] = (E'w-1 == S'w);
+//  3. verify (one warp per process, sequential over windows): a window whose
+//     predecessor was accepted and whose match flag is set is accepted as
+//     is (the common case costs one flag read); otherwise the window's true
+//     start state is compared with S'w and, if different, the window is
+//     replayed again from the true state;
+//  4. apply (one thread per lookup): hits overwrite value/status, op
+//     terminations set op_first_bad.
+//
+// Replaying one window is itself warp-parallel: lane j holds lookup j, the
+// cache state lives in lanes (lane i = i-th oldest entry), and hit / insert /
+// terminate masks are found by a fixed-point iteration (lookup j only
+// depends on lookups < j, so the iteration is exact after at most 32 rounds
+// and typically converges in two or three): membership in the start state
+// (shifted by the insertions before j), membership among earlier window
+// insertions (__match_any_sync on the key; an insertion i is still cached at
+// j if fewer than `capacity` insertions happened in between), and, for copy
+// plans, op termination (a miss whose walk failed, or a data access out of
+// range) deactivating the op's later pages (memvirt.py:615-627).
 #include "pv_common.cuh"
 
 namespace pv {
 
-struct WarpFifo {
-  uint64_t key, val;  // this lane's slot
-  uint32_t cap, len, head;
-  uint64_t hits, misses;
+constexpr uint32_t kNoOp = 0xFFFFFFFFu;
+constexpr int kWarmWindows = 2;  // H
 
-  __device__ void load(const pv_fifo& f, uint32_t lane) {
-    cap = f.capacity;
-    len = f.len;
-    head = f.head;
-    hits = f.hits;
-    misses = f.misses;
-    key = lane < PV_FIFO_MAX ? f.key[lane] : 0;
-    val = lane < PV_FIFO_MAX ? f.val[lane] : 0;
-  }
-  __device__ void store(pv_fifo& f, uint32_t lane) const {
-    f.key[lane] = key;
-    f.val[lane] = val;
-    if (lane == 0) {
-      f.len = len;
-      f.head = head;
-      f.hits = hits;
-      f.misses = misses;
-    }
-  }
-  // Is lane's slot live?  Live slots are head .. head+len-1 (mod cap).
-  __device__ __forceinline__ bool live(uint32_t lane) const {
-    if (lane >= cap) return false;
-    const uint32_t rel = lane >= head ? lane - head : lane + cap - head;
-    return rel < len;
-  }
-  // Returns true on a hit with *v = cached value (broadcast to all lanes).
-  __device__ __forceinline__ bool lookup(uint64_t k, uint32_t lane, uint64_t* v) {
-    const uint32_t m = __ballot_sync(0xFFFFFFFFu, live(lane) && key == k);
-    if (m) {
-      *v = __shfl_sync(0xFFFFFFFFu, val, __ffs(m) - 1);
-      ++hits;
-      return true;
-    }
-    ++misses;
-    return false;
-  }
-  __device__ __forceinline__ void insert(uint64_t k, uint64_t v, uint32_t lane) {
-    uint32_t slot;
-    if (len >= cap) {
-      slot = head;
-      head = head + 1 == cap ? 0 : head + 1;
-    } else {
-      slot = head + len;
-      if (slot >= cap) slot -= cap;
-      ++len;
-    }
-    if (lane == slot) {
-      key = k;
-      val = v;
-    }
-  }
+struct FifoStream {
+  const uint64_t* ref;       // per lookup: index into value / status (lane or page)
+  const uint32_t* op;        // per lookup: op id (copy plans) or nullptr (lanes)
+  const uint64_t* lk_off;    // [n_procs + 1] lookup offsets per process
+  const uint64_t* win_off;   // [n_procs + 1] global window offsets per process
+  uint32_t n_procs;
+  const void* vas;           // lanes: key = vas[ref] >> 12
+  uint32_t va32;
+  const pv_op* ops;          // copy plans: key = page va >> 12
+  const uint64_t* page_off;
+  uint64_t image_bytes;
+  const uint64_t* value;     // fresh values (hpa for lanes; hpa of the chunk for pages)
+  const uint32_t* status;    // fresh statuses
+  uint32_t cap;
+  uint32_t state_words;      // 2 * cap + 1
 };
 
-// Translate-lane replay: lookups are whole lanes of a pv_translate batch.
-template <bool kVa32>
-__global__ void fifo_lanes_kernel(const void* __restrict__ vas, const uint64_t* __restrict__ lane_idx,
-                                  const uint64_t* __restrict__ proc_off, uint32_t n_procs, pv_fifo* __restrict__ fifo,
-                                  uint64_t* __restrict__ value, uint32_t* __restrict__ status) {
-  const uint32_t lane = threadIdx.x & 31;
-  const uint32_t proc = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (proc >= n_procs) return;
-  WarpFifo c;
-  c.load(fifo[proc], lane);
-  const uint64_t b = proc_off[proc], e = proc_off[proc + 1];
-  for (uint64_t base = b; base < e; base += 32) {
-    const uint64_t mine = base + lane;
-    uint64_t li = 0, va = 0, v = 0;
-    uint32_t st = 0;
-    if (mine < e) {
-      li = lane_idx[mine];
-      va = kVa32 ? (uint64_t)((const uint32_t*)vas)[li] : ((const uint64_t*)vas)[li];
-      v = value[li];
-      st = status[li];
-    }
-    bool changed = false;
-    const uint32_t n = (uint32_t)(e - base < 32 ? e - base : 32);
-    for (uint32_t j = 0; j < n; ++j) {
-      const uint64_t vj = __shfl_sync(0xFFFFFFFFu, va, j);
-      const uint64_t fresh = __shfl_sync(0xFFFFFFFFu, v, j);
-      const uint32_t sj = __shfl_sync(0xFFFFFFFFu, st, j);
-      uint64_t hv;
-      if (c.lookup(vj >> kPageShift, lane, &hv)) {
-        if (lane == j) {
-          v = (hv << kPageShift) | (vj & kPageMask);
-          st = PV_ST_OK;
-          changed = true;
-        }
-      } else if (sj == PV_ST_OK) {
-        c.insert(vj >> kPageShift, fresh >> kPageShift, lane);
-      }
-    }
-    if (changed) {
-      value[li] = v;
-      status[li] = st;
-    }
+struct Lookup {
+  uint64_t key, fresh;  // fresh: value (hpa) from the walk
+  uint64_t off, chunk;  // page offset + chunk length (copy plans; for the OOR check of a hit)
+  uint32_t op;
+  bool walk_ok;         // the walk resolved (status OK, or OK walk + DATA_OOR)
+  bool data_ok;         // status OK
+  bool valid;
+};
+
+__device__ __forceinline__ Lookup load_lookup(const FifoStream& fs, uint64_t l, bool valid) {
+  Lookup r;
+  r.valid = valid;
+  r.key = r.fresh = r.off = r.chunk = 0;
+  r.op = kNoOp;
+  r.walk_ok = r.data_ok = false;
+  if (!valid) return r;
+  const uint64_t ref = fs.ref[l];
+  const uint32_t st = fs.status[ref];
+  r.fresh = fs.value[ref];
+  r.data_ok = st == PV_ST_OK;
+  r.walk_ok = st == PV_ST_OK || st == PV_ST_DATA_OOR;
+  if (fs.op == nullptr) {
+    const uint64_t va = fs.va32 ? (uint64_t)((const uint32_t*)fs.vas)[ref] : ((const uint64_t*)fs.vas)[ref];
+    r.key = va >> kPageShift;
+    r.off = va & kPageMask;
+    r.op = (uint32_t)l;  // every lane is its own op: never terminates a later one
+  } else {
+    const uint32_t o = fs.op[l];
+    const pv_op op = fs.ops[o];
+    const uint64_t k = ref - fs.page_off[o];
+    const uint64_t cur = op_page_va(op.gva, k);
+    r.key = cur >> kPageShift;
+    r.off = cur & kPageMask;
+    r.chunk = min(op.len - (cur - op.gva), kPageSize - r.off);
+    r.op = o;
   }
-  c.store(fifo[proc], lane);
+  return r;
 }
 
-// Copy-plan replay: lookups are the pages of each op of the process, in op
-// order and page order; an op stops at its first page that misses and fails
-// to resolve, or whose data access is out of range.
-__global__ void fifo_copy_kernel(const pv_op* __restrict__ ops, const uint64_t* __restrict__ page_off,
-                                 const uint64_t* __restrict__ op_idx, const uint64_t* __restrict__ proc_off,
-                                 uint32_t n_procs, pv_fifo* __restrict__ fifo, uint64_t image_bytes,
-                                 uint64_t* __restrict__ page_hpa, uint32_t* __restrict__ page_status,
-                                 unsigned long long* __restrict__ op_first_bad) {
-  const uint32_t lane = threadIdx.x & 31;
-  const uint32_t proc = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (proc >= n_procs) return;
-  WarpFifo c;
-  c.load(fifo[proc], lane);
-  for (uint64_t q = proc_off[proc]; q < proc_off[proc + 1]; ++q) {
-    const uint64_t op = op_idx[q];
-    const pv_op o = ops[op];
-    const uint64_t p_begin = page_off[op], p_end = page_off[op + 1];
-    uint64_t bad = kNone;
-    for (uint64_t base = p_begin; base < p_end && bad == kNone; base += 32) {
-      const uint64_t mine = base + lane;
-      uint64_t v = 0;
-      uint32_t st = 0;
-      if (mine < p_end) {
-        v = page_hpa[mine];
-        st = page_status[mine];
-      }
-      bool changed = false;
-      const uint32_t n = (uint32_t)(p_end - base < 32 ? p_end - base : 32);
-      for (uint32_t j = 0; j < n; ++j) {
-        const uint64_t k = base + j - p_begin;
-        const uint64_t cur = op_page_va(o.gva, k);
-        const uint64_t chunk = min(o.len - (cur - o.gva), kPageSize - (cur & kPageMask));
-        const uint64_t fresh = __shfl_sync(0xFFFFFFFFu, v, j);
-        const uint32_t sj = __shfl_sync(0xFFFFFFFFu, st, j);
-        uint64_t hv;
-        if (c.lookup(cur >> kPageShift, lane, &hv)) {
-          const uint64_t hpa = (hv << kPageShift) | (cur & kPageMask);
-          const bool oor = hpa + chunk > image_bytes || hpa + chunk < hpa;
-          if (lane == j) {
-            v = hpa;
-            st = oor ? PV_ST_DATA_OOR : PV_ST_OK;
-            changed = true;
-          }
-          if (oor) {
-            bad = k;
-            break;
-          }
-        } else {
-          // A resolved walk is cached even when the data access then fails.
-          if (sj == PV_ST_OK || sj == PV_ST_DATA_OOR) c.insert(cur >> kPageShift, fresh >> kPageShift, lane);
-          if (sj != PV_ST_OK) {
-            bad = k;
-            break;
-          }
-        }
-      }
-      if (changed && mine < p_end) {
-        page_hpa[mine] = v;
-        page_status[mine] = st;
+// Cache state distributed over a warp: lane i < len holds the i-th oldest
+// entry.  term_op: op whose pages are already terminated (copy plans).
+struct WarpState {
+  uint64_t qk, qv;
+  uint32_t len;
+  uint32_t term_op;
+};
+
+__device__ __forceinline__ uint32_t lt_mask(uint32_t lane) { return (1u << lane) - 1u; }
+
+// Replay one window of n <= 32 lookups from state `s` (updated in place).
+// Outputs per lane: hit, the hit's cached page, terminate, active.
+__device__ void window_run(const FifoStream& fs, const Lookup& x, uint32_t n, uint32_t lane, WarpState& s,
+                           bool* hit_out, uint64_t* hitpage_out, bool* term_out, bool* active_out,
+                           uint64_t* counts) {
+  const uint32_t full = 0xFFFFFFFFu;
+  const uint32_t cap = fs.cap;
+  const bool copy = fs.op != nullptr;
+  const uint32_t valid = __ballot_sync(full, x.valid);
+  // position of x.key in the start state (or -1)
+  int qidx = -1;
+  for (uint32_t i = 0; i < s.len; ++i) {
+    const uint64_t k = __shfl_sync(full, s.qk, i);
+    if (qidx < 0 && k == x.key) qidx = (int)i;
+  }
+  const uint64_t qval = __shfl_sync(full, s.qv, qidx < 0 ? 0 : qidx);
+  const uint32_t same_key = __match_any_sync(full, x.valid ? x.key : ~0ull - lane);
+  const uint32_t same_op = copy ? __match_any_sync(full, x.op) : (1u << lane);
+  const uint32_t walk_ok = __ballot_sync(full, x.valid && x.walk_ok);
+  uint32_t M = walk_ok, T = 0, A = valid;
+  if (copy && s.term_op != kNoOp) A &= ~__ballot_sync(full, x.op == s.term_op);
+  bool hit = false;
+  uint64_t hitpage = 0;
+  for (int it = 0; it < 34; ++it) {
+    const uint32_t e = __popc(M & lt_mask(lane));
+    const int ev = (int)s.len + (int)e - (int)cap;
+    const bool in_q = qidx >= 0 && qidx >= ev;
+    bool in_w = false;
+    const uint32_t cand = same_key & M & lt_mask(lane);
+    if (cand) {
+      const uint32_t i = 31 - __clz(cand);
+      const uint32_t ei = __popc(M & lt_mask(i));
+      in_w = (e - ei) <= cap;  // fewer than `cap` insertions strictly between i and j
+    }
+    const bool active = (A >> lane) & 1u;
+    hit = active && (in_q || in_w);
+    hitpage = in_w ? (x.fresh >> kPageShift) : qval;  // a window insertion of this key cached the fresh page
+    bool term = false;
+    if (copy && active) {
+      if (hit) {
+        const uint64_t hpa = (hitpage << kPageShift) | x.off;
+        term = hpa + x.chunk > fs.image_bytes || hpa + x.chunk < hpa;
+      } else {
+        term = !x.data_ok;
       }
     }
-    if (lane == 0) op_first_bad[op] = bad;
+    const uint32_t T_new = __ballot_sync(full, term);
+    const uint32_t M_new = __ballot_sync(full, active && !hit && x.walk_ok);
+    uint32_t A_new = valid;
+    if (copy) {
+      if (s.term_op != kNoOp) A_new &= ~__ballot_sync(full, x.op == s.term_op);
+      A_new &= ~__ballot_sync(full, (same_op & T_new & lt_mask(lane)) != 0);
+    }
+    const bool done = M_new == M && T_new == T && A_new == A;
+    M = M_new;
+    T = T_new;
+    A = A_new;
+    if (done) break;
   }
-  c.store(fifo[proc], lane);
+  const bool active = (A >> lane) & 1u;
+  *hit_out = hit && active;
+  *hitpage_out = hitpage;
+  *term_out = (T >> lane) & 1u;
+  *active_out = active;
+  const uint32_t hits = __popc(__ballot_sync(full, hit && active));
+  if (counts) *counts = (uint64_t)hits | ((uint64_t)__popc(A) << 32);  // hits | lookups
+  // new state = last `cap` of (start entries ++ window insertions)
+  const uint32_t ins = __popc(M);
+  const uint32_t total = s.len + ins;
+  const uint32_t nlen = total < cap ? total : cap;
+  const uint32_t idx = total - nlen + lane;
+  uint64_t nk = 0, nv = 0;
+  // source lane: start entry idx, or the (idx - len)-th window insertion
+  const bool from_q = idx < s.len;
+  int src = from_q ? (int)idx : (lane < nlen ? (int)__fns(M, 0, (int)(idx - s.len) + 1) : 0);
+  if (src < 0) src = 0;
+  const uint64_t qk_s = __shfl_sync(full, s.qk, from_q ? src : 0);
+  const uint64_t qv_s = __shfl_sync(full, s.qv, from_q ? src : 0);
+  const uint64_t wk_s = __shfl_sync(full, x.key, from_q ? 0 : src);
+  const uint64_t wv_s = __shfl_sync(full, x.fresh >> kPageShift, from_q ? 0 : src);
+  if (lane < nlen) {
+    nk = from_q ? qk_s : wk_s;
+    nv = from_q ? qv_s : wv_s;
+  }
+  s.qk = nk;
+  s.qv = nv;
+  s.len = nlen;
+  if (copy) {
+    // the op of the window's last valid lookup carries over
+    const uint32_t last = valid ? 31 - __clz(valid) : 0;
+    const uint32_t last_op = __shfl_sync(full, x.op, last);
+    const bool last_term = s.term_op == last_op || (__ballot_sync(full, x.op == last_op && ((T >> lane) & 1u)) != 0);
+    if (n > 0) s.term_op = last_term ? last_op : kNoOp;
+  }
 }
 
-cudaError_t launch_fifo_lanes(const void* vas, uint32_t flags, const uint64_t* lane_idx, const uint64_t* proc_off,
-                              uint32_t n_procs, pv_fifo* fifo, uint64_t* value, uint32_t* status,
-                              cudaStream_t stream) {
-  if (n_procs == 0) return cudaSuccess;
-  const uint32_t warps = 4;
-  const uint32_t grid = (n_procs + warps - 1) / warps;
-  if (flags & PV_VA32)
-    fifo_lanes_kernel<true><<<grid, warps * 32, 0, stream>>>(vas, lane_idx, proc_off, n_procs, fifo, value, status);
-  else
-    fifo_lanes_kernel<false><<<grid, warps * 32, 0, stream>>>(vas, lane_idx, proc_off, n_procs, fifo, value, status);
+__device__ __forceinline__ void load_state(const uint64_t* st, uint32_t cap, uint32_t lane, WarpState& s) {
+  const uint64_t meta = st[2 * cap];
+  s.len = (uint32_t)meta;
+  s.term_op = (uint32_t)(meta >> 32);
+  s.qk = lane < s.len ? st[lane] : 0;
+  s.qv = lane < s.len ? st[cap + lane] : 0;
+}
+__device__ __forceinline__ void store_state(uint64_t* st, uint32_t cap, uint32_t lane, const WarpState& s) {
+  if (lane < cap) {
+    st[lane] = lane < s.len ? s.qk : 0;
+    st[cap + lane] = lane < s.len ? s.qv : 0;
+  }
+  if (lane == 0) st[2 * cap] = (uint64_t)s.len | ((uint64_t)s.term_op << 32);
+}
+
+// Initial state of process p from its pv_fifo (ring -> oldest-first lanes).
+__device__ __forceinline__ void initial_state(const pv_fifo& f, uint32_t lane, WarpState& s) {
+  s.len = f.len;
+  s.term_op = kNoOp;
+  const uint32_t slot = f.capacity ? (f.head + lane) % f.capacity : 0;
+  s.qk = lane < f.len ? f.key[slot] : 0;
+  s.qv = lane < f.len ? f.val[slot] : 0;
+}
+
+struct Scratch {
+  uint64_t* spec_start;  // [windows][state_words]
+  uint64_t* spec_end;    // [windows][state_words]
+  uint64_t* win_counts;  // [windows]: hits | lookups << 32
+  uint8_t* match;        // [windows]
+  uint64_t* hitpage;     // [lookups]
+  uint8_t* flags;        // [lookups]: 1 hit, 2 terminate, 4 active
+};
+
+__device__ __forceinline__ uint32_t proc_of_window(const FifoStream& fs, uint64_t w) {
+  uint32_t lo = 0, hi = fs.n_procs;
+  while (hi - lo > 1) {
+    const uint32_t m = (lo + hi) >> 1;
+    if (fs.win_off[m] <= w) lo = m; else hi = m;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ void run_one(const FifoStream& fs, uint64_t lb, uint64_t le, uint64_t wi, uint32_t lane,
+                                        WarpState& s, const Scratch* out, uint64_t* counts) {
+  const uint64_t l0 = lb + wi * 32;
+  const uint64_t l = l0 + lane;
+  const bool valid = l < le;
+  const uint32_t n = (uint32_t)(le > l0 ? (le - l0 < 32 ? le - l0 : 32) : 0);
+  const Lookup x = load_lookup(fs, l, valid);
+  bool hit, term, active;
+  uint64_t hp;
+  window_run(fs, x, n, lane, s, &hit, &hp, &term, &active, counts);
+  if (out != nullptr && valid) {
+    out->hitpage[l] = hp;
+    out->flags[l] = (hit ? 1 : 0) | (term ? 2 : 0) | (active ? 4 : 0);
+  }
+}
+
+// Step 1: speculate every window.
+__global__ void fifo_spec_kernel(FifoStream fs, const pv_fifo* __restrict__ fifo, Scratch sc, uint64_t n_windows,
+                                 unsigned long long* first_bad) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n_windows; w += nwarps) {
+    const uint32_t p = proc_of_window(fs, w);
+    const uint64_t w0 = fs.win_off[p], lb = fs.lk_off[p], le = fs.lk_off[p + 1];
+    const uint64_t wi = w - w0;
+    WarpState s;
+    uint64_t from;
+    if (wi <= (uint64_t)kWarmWindows) {
+      initial_state(fifo[p], lane, s);  // exact: replay from the stream start
+      from = 0;
+    } else {
+      s.qk = s.qv = 0;
+      s.len = 0;
+      s.term_op = kNoOp;
+      from = wi - kWarmWindows;
+    }
+    for (uint64_t v = from; v < wi; ++v) run_one(fs, lb, le, v, lane, s, nullptr, nullptr);
+    store_state(sc.spec_start + w * fs.state_words, fs.cap, lane, s);
+    uint64_t counts = 0;
+    run_one(fs, lb, le, wi, lane, s, &sc, &counts);
+    store_state(sc.spec_end + w * fs.state_words, fs.cap, lane, s);
+    if (lane == 0) {
+      sc.win_counts[w] = counts;
+      sc.match[w] = wi <= (uint64_t)kWarmWindows ? 1 : 0;  // exact start state
+    }
+    // copy plans: every op of this window starts from "not failed"
+    if (fs.op != nullptr && first_bad != nullptr) {
+      const uint64_t l = lb + wi * 32 + lane;
+      if (l < le) {
+        const uint32_t o = fs.op[l];
+        if (fs.ref[l] == fs.page_off[o]) first_bad[o] = kNone;
+      }
+    }
+  }
+}
+
+// Step 2: link neighbouring windows.
+__global__ void fifo_link_kernel(FifoStream fs, Scratch sc, uint64_t n_windows) {
+  const uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= n_windows || sc.match[w]) return;
+  const uint32_t p = proc_of_window(fs, w);
+  if (w == fs.win_off[p]) return;
+  const uint64_t* a = sc.spec_end + (w - 1) * fs.state_words;
+  const uint64_t* b = sc.spec_start + w * fs.state_words;
+  const uint32_t len = (uint32_t)a[2 * fs.cap];
+  bool eq = a[2 * fs.cap] == b[2 * fs.cap];
+  for (uint32_t i = 0; eq && i < len; ++i) eq = a[i] == b[i] && a[fs.cap + i] == b[fs.cap + i];
+  sc.match[w] = eq ? 1 : 0;
+}
+
+// Step 3: verify each process's chain; replay mismatching windows exactly.
+__global__ void fifo_verify_kernel(FifoStream fs, pv_fifo* __restrict__ fifo, Scratch sc) {
+  const uint32_t full = 0xFFFFFFFFu;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (p >= fs.n_procs) return;
+  const uint64_t w0 = fs.win_off[p], w1 = fs.win_off[p + 1], lb = fs.lk_off[p], le = fs.lk_off[p + 1];
+  WarpState s;
+  initial_state(fifo[p], lane, s);
+  // have_s: s holds the true state before window w; otherwise that state is
+  // spec_end[w - 1] (the previous window was accepted as speculated).
+  bool have_s = true;
+  uint64_t hits = 0, lookups = 0;
+  for (uint64_t wb = w0; wb < w1; wb += 32) {
+    const uint64_t wl = wb + lane;
+    const uint32_t mm = __ballot_sync(full, wl < w1 && sc.match[wl]);
+    const uint64_t wc = wl < w1 ? sc.win_counts[wl] : 0;
+    const uint32_t nb = (uint32_t)(w1 - wb < 32 ? w1 - wb : 32);
+    for (uint32_t j = 0; j < nb; ++j) {
+      const uint64_t w = wb + j;
+      const uint64_t cj = __shfl_sync(full, wc, j);
+      if (!have_s) {
+        if ((mm >> j) & 1u) {  // spec_start[w] == spec_end[w-1] == true state
+          hits += (uint32_t)cj;
+          lookups += cj >> 32;
+          continue;
+        }
+        load_state(sc.spec_end + (w - 1) * fs.state_words, fs.cap, lane, s);
+        have_s = true;
+      }
+      const uint64_t* b = sc.spec_start + w * fs.state_words;
+      const uint64_t meta = b[2 * fs.cap];
+      const bool lane_eq = lane >= s.len || (b[lane] == s.qk && b[fs.cap + lane] == s.qv);
+      const bool same = (uint32_t)meta == s.len && (uint32_t)(meta >> 32) == s.term_op && __all_sync(full, lane_eq);
+      if (same) {
+        hits += (uint32_t)cj;
+        lookups += cj >> 32;
+        have_s = false;
+      } else {
+        uint64_t c = 0;
+        run_one(fs, lb, le, w - w0, lane, s, &sc, &c);
+        hits += (uint32_t)c;
+        lookups += c >> 32;
+      }
+    }
+  }
+  if (!have_s) load_state(sc.spec_end + (w1 - 1) * fs.state_words, fs.cap, lane, s);
+  pv_fifo& f = fifo[p];
+  if (lane < f.capacity) {
+    f.key[lane] = lane < s.len ? s.qk : 0;
+    f.val[lane] = lane < s.len ? s.qv : 0;
+  }
+  if (lane == 0) {
+    f.len = s.len;
+    f.head = 0;
+    f.hits += hits;
+    f.misses += lookups - hits;
+  }
+}
+
+// Step 4: apply hits and terminations.
+__global__ void fifo_apply_kernel(FifoStream fs, Scratch sc, uint64_t n_lookups, uint64_t* value, uint32_t* status,
+                                  unsigned long long* first_bad) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t l = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; l < n_lookups; l += stride) {
+    const uint8_t fl = sc.flags[l];
+    const uint64_t ref = fs.ref[l];
+    if (fs.op == nullptr) {
+      if (fl & 1) {
+        const uint64_t va = fs.va32 ? (uint64_t)((const uint32_t*)fs.vas)[ref] : ((const uint64_t*)fs.vas)[ref];
+        value[ref] = (sc.hitpage[l] << kPageShift) | (va & kPageMask);
+        status[ref] = PV_ST_OK;
+      }
+      continue;
+    }
+    const uint32_t o = fs.op[l];
+    const pv_op op = fs.ops[o];
+    const uint64_t k = ref - fs.page_off[o];
+    const uint64_t cur = op_page_va(op.gva, k);
+    if (fl & 1) {
+      value[ref] = (sc.hitpage[l] << kPageShift) | (cur & kPageMask);
+      status[ref] = (fl & 2) ? PV_ST_DATA_OOR : PV_ST_OK;
+    }
+    if (fl & 2) first_bad[o] = k;
+  }
+}
+
+// ---- launchers ------------------------------------------------------------------
+
+size_t fifo_scratch_bytes(uint64_t n_lookups, uint64_t n_windows, uint32_t cap) {
+  const uint64_t sw = 2ull * cap + 1;
+  return 2 * n_windows * sw * 8 + n_windows * 8 + n_windows + n_lookups * 8 + n_lookups + 256;
+}
+
+static Scratch carve(void* base, uint64_t n_lookups, uint64_t n_windows, uint32_t cap) {
+  const uint64_t sw = 2ull * cap + 1;
+  uint8_t* p = static_cast<uint8_t*>(base);
+  Scratch s;
+  s.spec_start = reinterpret_cast<uint64_t*>(p);
+  p += n_windows * sw * 8;
+  s.spec_end = reinterpret_cast<uint64_t*>(p);
+  p += n_windows * sw * 8;
+  s.hitpage = reinterpret_cast<uint64_t*>(p);
+  p += n_lookups * 8;
+  s.win_counts = reinterpret_cast<uint64_t*>(p);
+  p += n_windows * 8;
+  s.match = p;
+  p += n_windows;
+  s.flags = p;
+  return s;
+}
+
+cudaError_t launch_fifo_stream(const FifoStream& fs, pv_fifo* fifo, void* scratch, uint64_t n_lookups,
+                               uint64_t n_windows, uint64_t* value, uint32_t* status, uint64_t* first_bad,
+                               cudaStream_t stream) {
+  if (fs.n_procs == 0 || n_windows == 0) return cudaSuccess;
+  const Scratch sc = carve(scratch, n_lookups, n_windows, fs.cap);
+  auto* fb = reinterpret_cast<unsigned long long*>(first_bad);
+  {
+    const uint64_t warps = n_windows;
+    uint64_t grid = (warps + 7) / 8;
+    const uint64_t cap = resident_grid((const void*)fifo_spec_kernel, 256, 0);
+    if (grid > cap) grid = cap;
+    fifo_spec_kernel<<<(unsigned)grid, 256, 0, stream>>>(fs, fifo, sc, n_windows, fb);
+  }
+  fifo_link_kernel<<<(unsigned)((n_windows + 255) / 256), 256, 0, stream>>>(fs, sc, n_windows);
+  fifo_verify_kernel<<<(fs.n_procs + 3) / 4, 128, 0, stream>>>(fs, fifo, sc);
+  {
+    uint64_t grid = (n_lookups + 255) / 256;
+    const uint64_t cap = resident_grid((const void*)fifo_apply_kernel, 256, 0);
+    if (grid > cap) grid = cap;
+    fifo_apply_kernel<<<(unsigned)grid, 256, 0, stream>>>(fs, sc, n_lookups, value, status, fb);
+  }
   return cudaGetLastError();
 }
 
-cudaError_t launch_fifo_copy(const pv_op* ops, const uint64_t* page_off, const uint64_t* op_idx,
-                             const uint64_t* proc_off, uint32_t n_procs, pv_fifo* fifo, uint64_t image_bytes,
-                             uint64_t* page_hpa, uint32_t* page_status, uint64_t* op_first_bad, cudaStream_t stream) {
-  if (n_procs == 0) return cudaSuccess;
-  const uint32_t warps = 4;
-  const uint32_t grid = (n_procs + warps - 1) / warps;
-  fifo_copy_kernel<<<grid, warps * 32, 0, stream>>>(ops, page_off, op_idx, proc_off, n_procs, fifo, image_bytes,
-                                                   page_hpa, page_status,
-                                                   reinterpret_cast<unsigned long long*>(op_first_bad));
-  return cudaGetLastError();
+// Window totals need the lookup counts: read from the offsets on the host
+// side of the launch (they are small device arrays; copied synchronously).
+static uint64_t last_u64(const uint64_t* dev_arr, uint32_t idx, cudaStream_t stream) {
+  uint64_t v = 0;
+  cudaMemcpyAsync(&v, dev_arr + idx, sizeof(v), cudaMemcpyDeviceToHost, stream);
+  cudaStreamSynchronize(stream);
+  return v;
+}
+
+cudaError_t launch_fifo_lanes_abi(const void* vas, uint32_t flags, const uint64_t* lane_idx, const uint64_t* proc_off,
+                                  const uint64_t* win_off, uint32_t n_procs, uint32_t cap, pv_fifo* fifo,
+                                  uint64_t* value, uint32_t* status, void* scratch, uint64_t scratch_bytes,
+                                  cudaStream_t stream) {
+  FifoStream fs{};
+  fs.ref = lane_idx;
+  fs.op = nullptr;
+  fs.lk_off = proc_off;
+  fs.win_off = win_off;
+  fs.n_procs = n_procs;
+  fs.vas = vas;
+  fs.va32 = (flags & PV_VA32) ? 1u : 0u;
+  fs.value = value;
+  fs.status = status;
+  fs.cap = cap;
+  fs.state_words = 2 * cap + 1;
+  const uint64_t n_lookups = last_u64(proc_off, n_procs, stream);
+  const uint64_t n_windows = last_u64(win_off, n_procs, stream);
+  if (scratch_bytes < fifo_scratch_bytes(n_lookups, n_windows, cap)) return cudaErrorInvalidValue;
+  return launch_fifo_stream(fs, fifo, scratch, n_lookups, n_windows, value, status, nullptr, stream);
+}
+
+cudaError_t launch_fifo_copy_abi(const pv_op* ops, const uint64_t* page_off, const uint64_t* look_page,
+                                 const uint32_t* look_op, const uint64_t* proc_off, const uint64_t* win_off,
+                                 uint32_t n_procs, uint32_t cap, pv_fifo* fifo, uint64_t image_bytes,
+                                 uint64_t* page_hpa, uint32_t* page_status, uint64_t* op_first_bad, void* scratch,
+                                 uint64_t scratch_bytes, cudaStream_t stream) {
+  FifoStream fs{};
+  fs.ref = look_page;
+  fs.op = look_op;
+  fs.lk_off = proc_off;
+  fs.win_off = win_off;
+  fs.n_procs = n_procs;
+  fs.ops = ops;
+  fs.page_off = page_off;
+  fs.image_bytes = image_bytes;
+  fs.value = page_hpa;
+  fs.status = page_status;
+  fs.cap = cap;
+  fs.state_words = 2 * cap + 1;
+  const uint64_t n_lookups = last_u64(proc_off, n_procs, stream);
+  const uint64_t n_windows = last_u64(win_off, n_procs, stream);
+  if (scratch_bytes < fifo_scratch_bytes(n_lookups, n_windows, cap)) return cudaErrorInvalidValue;
+  return launch_fifo_stream(fs, fifo, scratch, n_lookups, n_windows, page_hpa, page_status, op_first_bad, stream);
 }
 
 }  // namespace pv

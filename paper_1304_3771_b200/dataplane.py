@@ -443,14 +443,46 @@ def unpack_fifo(rows: np.ndarray, caches) -> None:
         c._load_state(entries, int(rows[i, 2 * N.FIFO_MAX]), int(rows[i, 2 * N.FIFO_MAX + 1]))
 
 
-def fifo_replay_lanes(vas, lane_idx, proc_off, fifo_dev, value, status) -> None:
+def _windows(proc_off: np.ndarray) -> np.ndarray:
+    """Per-process window offsets (32 lookups per window) from lookup offsets."""
+    counts = np.diff(proc_off.astype(np.int64))
+    win = np.zeros(len(proc_off), dtype=np.int64)
+    np.cumsum((counts + 31) // 32, out=win[1:])
+    return win
+
+
+def fifo_capacity(caches) -> int:
+    caps = {c.capacity for c in caches}
+    if len(caps) != 1:
+        raise ValueError("a FIFO replay batch needs one cache capacity for every process")
+    cap = caps.pop()
+    if not 1 <= cap <= N.FIFO_MAX:
+        raise ValueError(f"device FIFO replay supports capacities 1..{N.FIFO_MAX}, got {cap}")
+    return cap
+
+
+def _fifo_scratch(n_lookups: int, n_windows: int, cap: int):
+    import torch
+
+    nbytes = int(N.load().pv_fifo_scratch_bytes(n_lookups, n_windows, cap))
+    return torch.empty(max(nbytes, 1), dtype=torch.uint8, device="cuda"), nbytes
+
+
+def fifo_replay_lanes(vas, lane_idx, proc_off: np.ndarray, fifo_dev, value, status, capacity: int) -> None:
+    """K4 over translate lanes: lookups of process p are lanes
+    lane_idx[proc_off[p]:proc_off[p+1]] in order (proc_off host array)."""
     import torch
 
     lib = N.lib()
     flags = N.VA32 if vas.dtype == torch.int32 else 0
-    N.check(lib.pv_fifo_replay(vas.data_ptr(), flags, lane_idx.data_ptr(), proc_off.data_ptr(),
-                               proc_off.numel() - 1, fifo_dev.data_ptr(), value.data_ptr(), status.data_ptr(),
-                               _stream().cuda_stream), "pv_fifo_replay")
+    win = _windows(proc_off)
+    scratch, nbytes = _fifo_scratch(int(proc_off[-1]), int(win[-1]), capacity)
+    off_d = _to_dev(np.asarray(proc_off, dtype=np.int64))
+    win_d = _to_dev(win)
+    N.check(lib.pv_fifo_replay(vas.data_ptr(), flags, lane_idx.data_ptr(), off_d.data_ptr(), win_d.data_ptr(),
+                               len(proc_off) - 1, capacity, fifo_dev.data_ptr(), value.data_ptr(),
+                               status.data_ptr(), scratch.data_ptr(), nbytes, _stream().cuda_stream),
+            "pv_fifo_replay")
 
 
 # ---- K2/K3: batched copy -----------------------------------------------------
@@ -494,13 +526,31 @@ class CopyPlan:
         self.conflict = torch.zeros(1, dtype=torch.int32, device="cuda")
         self.fifo_groups = fifo_groups
         if fifo_groups is not None:
-            idx = np.concatenate([np.asarray(g, dtype=np.uint64) for g in fifo_groups]) if fifo_groups else \
-                np.zeros(0, np.uint64)
-            off = np.zeros(len(fifo_groups) + 1, dtype=np.uint64)
-            np.cumsum([len(g) for g in fifo_groups], out=off[1:])
-            self.fifo_idx = _to_dev(idx.view(np.int64)) if len(idx) else torch.zeros(1, dtype=torch.int64,
-                                                                                      device="cuda")
-            self.fifo_off = _to_dev(off.view(np.int64))
+            # lookup stream: the pages of each process's ops, op order, page order
+            po = page_off.astype(np.int64)
+            sp = spans.astype(np.int64)
+            look_op, look_page, lk_off = [], [], [0]
+            for g in fifo_groups:
+                g = np.asarray(g, dtype=np.int64)
+                cnt = sp[g]
+                total = int(cnt.sum())
+                excl = np.zeros(len(g), dtype=np.int64)
+                if len(g) > 1:
+                    np.cumsum(cnt[:-1], out=excl[1:])
+                look_op.append(np.repeat(g, cnt))
+                look_page.append(np.repeat(po[g] - excl, cnt) + np.arange(total, dtype=np.int64))
+                lk_off.append(lk_off[-1] + total)
+            lk_off = np.asarray(lk_off, dtype=np.int64)
+            lop = np.concatenate(look_op) if look_op else np.zeros(0, np.int64)
+            lpg = np.concatenate(look_page) if look_page else np.zeros(0, np.int64)
+            self.fifo_lookups = int(lk_off[-1])
+            self.fifo_win = _windows(lk_off)
+            self.fifo_look_op = _to_dev(lop.astype(np.uint32).view(np.int32)) if len(lop) else \
+                torch.zeros(1, dtype=torch.int32, device="cuda")
+            self.fifo_look_page = _to_dev(lpg) if len(lpg) else torch.zeros(1, dtype=torch.int64, device="cuda")
+            self.fifo_off = _to_dev(lk_off)
+            self.fifo_win_d = _to_dev(self.fifo_win)
+            self.fifo_scratch = None
 
 
 def _owner_map(image):
@@ -517,8 +567,8 @@ def _owner_map(image):
     return image._owner, image._epoch
 
 
-def copy_launch(image, plan: CopyPlan, direction: int, buf, *, fifo_dev=None, detect_conflicts: bool = True,
-                track_dirty: bool = True) -> None:
+def copy_launch(image, plan: CopyPlan, direction: int, buf, *, fifo_dev=None, fifo_cap: int = 10,
+                detect_conflicts: bool = True, track_dirty: bool = True) -> None:
     """Enqueue plan (+ FIFO replay) (+ conflict stamp) + exec on the current
     stream.  Results land in ``plan.results`` / ``plan.conflict``."""
     lib = N.lib()
@@ -534,12 +584,19 @@ def copy_launch(image, plan: CopyPlan, direction: int, buf, *, fifo_dev=None, de
                                  plan.n_ops, plan.page_off.data_ptr(), plan.n_pages, direction,
                                  plan.page_hpa.data_ptr(), plan.page_status.data_ptr(), plan.page_aux.data_ptr(),
                                  plan.first_bad.data_ptr(), None, 0, None, s), "pv_copy_plan")
-        if fifo_dev is not None:
-            N.check(lib.pv_copy_fifo_replay(plan.ops.data_ptr(), plan.page_off.data_ptr(), plan.fifo_idx.data_ptr(),
-                                            plan.fifo_off.data_ptr(), plan.fifo_off.numel() - 1,
-                                            fifo_dev.data_ptr(), image.nbytes, direction,
+        if fifo_dev is not None and plan.fifo_lookups:
+            cap = fifo_cap
+            if plan.fifo_scratch is None or plan.fifo_cap != cap:
+                plan.fifo_cap = cap
+                plan.fifo_scratch = _fifo_scratch(plan.fifo_lookups, int(plan.fifo_win[-1]), cap)
+            scratch, nbytes = plan.fifo_scratch
+            N.check(lib.pv_copy_fifo_replay(plan.ops.data_ptr(), plan.page_off.data_ptr(),
+                                            plan.fifo_look_page.data_ptr(), plan.fifo_look_op.data_ptr(),
+                                            plan.fifo_off.data_ptr(), plan.fifo_win_d.data_ptr(),
+                                            plan.fifo_off.numel() - 1, cap, fifo_dev.data_ptr(), image.nbytes,
                                             plan.page_hpa.data_ptr(), plan.page_status.data_ptr(),
-                                            plan.first_bad.data_ptr(), s), "pv_copy_fifo_replay")
+                                            plan.first_bad.data_ptr(), scratch.data_ptr(), nbytes, s),
+                    "pv_copy_fifo_replay")
         abort = None
         if direction == N.TO_GUEST and detect_conflicts:
             owner, epoch = _owner_map(image)
@@ -588,10 +645,11 @@ def copy_ops(image, spaces: list[Space], ops: np.ndarray, direction: int, buf, *
     """
     import torch
 
+    cap = fifo_capacity(caches) if caches is not None else 10
     plan = CopyPlan(spaces, ops, fifo_groups=fifo_groups if caches is not None else None)
     fifo_dev = _to_dev(pack_fifo(caches)) if caches is not None else None
     snapshot = fifo_dev.clone() if fifo_dev is not None else None
-    copy_launch(image, plan, direction, buf, fifo_dev=fifo_dev, detect_conflicts=detect_conflicts)
+    copy_launch(image, plan, direction, buf, fifo_dev=fifo_dev, fifo_cap=cap, detect_conflicts=detect_conflicts)
     conflict = int(plan.conflict.item()) if (direction == N.TO_GUEST and detect_conflicts) else 0
     if not conflict:
         results = decode_results(plan.results.cpu().numpy())
@@ -609,21 +667,21 @@ def copy_ops(image, spaces: list[Space], ops: np.ndarray, direction: int, buf, *
                 proc_of[int(o)] = p
     results = []
     for i in range(len(ops)):
-        out = _copy_one_ordered(image, spaces, ops[i], direction, buf, fifo_dev, proc_of.get(i), caches)
+        out = _copy_one_ordered(image, spaces, ops[i], direction, buf, fifo_dev, proc_of.get(i), caches, cap)
         results.append(out)
     if caches is not None:
         unpack_fifo(fifo_dev.cpu().numpy(), caches)
     return results
 
 
-def _copy_one_ordered(image, spaces, op, direction, buf, fifo_dev, proc, caches) -> OpOutcome:
+def _copy_one_ordered(image, spaces, op, direction, buf, fifo_dev, proc, caches, cap=10) -> OpOutcome:
     """One op, split into single-page sub-ops if its own pages alias."""
     fifo_one = None
     if caches is not None and proc is not None:
         fifo_one = fifo_dev[proc:proc + 1]
     groups = [[0]] if fifo_one is not None else None
     plan = CopyPlan(spaces, op.reshape(1, 4), fifo_groups=groups)
-    copy_launch(image, plan, direction, buf, fifo_dev=fifo_one, detect_conflicts=True)
+    copy_launch(image, plan, direction, buf, fifo_dev=fifo_one, fifo_cap=cap, detect_conflicts=True)
     if not int(plan.conflict.item()):
         return decode_results(plan.results.cpu().numpy())[0]
     gva, length, buf_off, sp = (int(x) for x in op)
@@ -633,7 +691,7 @@ def _copy_one_ordered(image, spaces, op, direction, buf, fifo_dev, proc, caches)
         chunk = min(length - copied, PAGE_SIZE - (cur & PAGE_MASK))
         sub = np.array([[cur, chunk, buf_off + copied, sp]], dtype=np.uint64)
         splan = CopyPlan(spaces, sub, fifo_groups=groups)
-        copy_launch(image, splan, direction, buf, fifo_dev=fifo_one, detect_conflicts=False)
+        copy_launch(image, splan, direction, buf, fifo_dev=fifo_one, fifo_cap=cap, detect_conflicts=False)
         r = decode_results(splan.results.cpu().numpy())[0]
         if r.status != N.ST_OK:
             r.copied = copied

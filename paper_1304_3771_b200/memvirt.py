@@ -862,10 +862,10 @@ def translate_batch(translator: ProcessTranslator, gvas, *, use_cache: bool | No
     plan = dp.TranslatePlan([translator.device_space], [(0, n, 0)])
     value, status, aux = dp.translate_lanes(translator.image, plan, vas)
     if cache_on and n:
+        cap = dp.fifo_capacity([translator.cache])
         fifo = dp._to_dev(dp.pack_fifo([translator.cache]))
         lane_idx = torch.arange(n, dtype=torch.int64, device="cuda")
-        proc_off = torch.tensor([0, n], dtype=torch.int64, device="cuda")
-        dp.fifo_replay_lanes(vas, lane_idx, proc_off, fifo, value, status)
+        dp.fifo_replay_lanes(vas, lane_idx, np.array([0, n], dtype=np.int64), fifo, value, status, cap)
         dp.unpack_fifo(fifo.cpu().numpy(), [translator.cache])
     if on_device:
         return value, status, aux

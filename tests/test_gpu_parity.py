@@ -327,3 +327,122 @@ def test_host_pipelined_translate_equals_device_path(cuda, mode):
     assert np.array_equal(s.numpy().view(np.uint32), hs)
     assert np.array_equal(a.numpy().view(np.uint64), ha)
     assert (hs != 0).any() and (hs == 0).any()
+
+
+def _fifo_world(mode="shadow", pages=40):
+    memv = mv.MemoryVirtualizer()
+    g = memv.add_guest(0, mode)
+    sp = memv.create_process(g)
+    memv.map_region(sp, S.BUF, pages)
+    # a page whose PTE points past the image: walk ok, data access OutOfRange
+    if mode == "shadow":
+        mv.TableEditor(memv.host_mem, sp.shadow_root, memv.host_alloc.alloc).map(S.BUF + pages * 4096, 0xF_FFFF)
+    return memv, g, sp
+
+
+@pytest.mark.parametrize("cap", [1, 3, 10, 32])
+@pytest.mark.parametrize("mode", ["shadow", "tdp"])
+def test_parallel_fifo_replay_lanes_vs_sequential_oracle(cuda, cap, mode):
+    """K4 over long translate streams: small key sets (hits, evictions,
+    re-insertions), faulting keys, and stale initial entries that must win
+    over the tables."""
+    memv, g, sp = _fifo_world(mode)
+    rng = random.Random(cap * 7 + len(mode))
+    pages = list(range(0, 50))  # 40 mapped + holes
+    vas = np.array([S.BUF + rng.choice(pages[: rng.choice([4, 9, 12, 50])]) * 4096 + rng.randrange(4096)
+                    for _ in range(120_000)], dtype=np.uint64)
+    stale = [((S.BUF >> 12) + 2, 0x77777), ((S.BUF >> 12) + 45, 0x12345), ((S.BUF >> 12) + 7, 0x55)][:cap]
+    cache = mv.TranslationCache(cap)
+    for k, v in stale:
+        cache.insert(k, v)
+    cache.hits, cache.misses = 5, 6
+    tr = memv.translator(sp, cache)
+    raw = np.frombuffer(S.image_bytes(memv.host_mem), dtype=np.uint8).copy()
+    spc = tr.device_space
+    ocache = O.new_cache(cap, stale, 5, 6)
+    v, s, a = O.translate_cached(raw, O.space(spc.s1_base, spc.s1_root_pfn, spc.s2_root_pfn, spc.mode), vas, ocache)
+    hv, hs, ha = tr.translate_batch(vas)
+    assert np.array_equal(hs, s) and np.array_equal(hv, v)
+    entries, hits, misses = O.cache_state(ocache)
+    assert (cache.hits, cache.misses, cache.entries()) == (hits, misses, entries)
+    assert 0 < hits < len(vas)
+
+
+@pytest.mark.parametrize("mode", ["shadow", "tdp"])
+def test_parallel_fifo_replay_copy_plans_vs_sequential_oracle(cuda, mode):
+    """K4 over copy plans: thousands of small ops (1-3 pages) with faults,
+    out-of-range data pages and stale entries; ops stop at their first bad
+    page, overlapping destinations are last-writer-wins."""
+    memv, g, sp = _fifo_world(mode)
+    rng = random.Random(99)
+    rec = be.GuestProcessRecord(S._Guest(0, mode), sp, memv)
+    for k, v in [((S.BUF >> 12) + 3, (S.BUF >> 12) + 999), ((S.BUF >> 12) + 44, 0x1234)]:
+        rec.translation_cache.insert(k, v if mode == "tdp" else memv.host_mem.read_word(0, 0) * 0 + 0x1200 + k % 7)
+    acc = be.SoftwareHasAccess(rec, memv)
+    n_ops = 3000
+    gvas = [S.BUF + rng.randrange(46 * 4096) for _ in range(n_ops)]
+    lens = [rng.randrange(1, 3 * 4096) for _ in range(n_ops)]
+    src = np.frombuffer(random.Random(7).randbytes(sum(lens)), dtype=np.uint8)
+    raw = np.frombuffer(S.image_bytes(memv.host_mem), dtype=np.uint8).copy()
+    c0 = rec.translation_cache
+    ocache = O.new_cache(c0.capacity, c0.entries(), c0.hits, c0.misses)
+    outs = acc.copy_to_user_batch(gvas, lens, src.tobytes())
+    offs = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.uint64)
+    rows = np.stack([np.array(gvas, np.uint64), np.array(lens, np.uint64), offs, np.zeros(n_ops, np.uint64)], 1)
+    spc = rec.translator.device_space
+    res = O.copy(raw, O.space(spc.s1_base, spc.s1_root_pfn, spc.s2_root_pfn, spc.mode).reshape(1, 4), rows,
+                 src.copy(), 0, caches=ocache, op_cache=[0] * n_ops)
+    assert np.array_equal(np.frombuffer(S.image_bytes(memv.host_mem), dtype=np.uint8), raw)
+    kinds = set()
+    for o, r in zip(outs, res):
+        st = int(r[3]) & 0xFFFFFFFF
+        kinds.add(st & 0xFF0)
+        if st == 0:
+            assert o == int(r[0])
+        elif (st & 0xFF0) in (0x010, 0x020):
+            assert isinstance(o, er.PageFault) and o.bytes_copied == int(r[0])
+        elif st == 0x100:
+            assert isinstance(o, er.OutOfRange)
+    entries, hits, misses = O.cache_state(ocache)
+    assert (rec.translation_cache.hits, rec.translation_cache.misses) == (hits, misses)
+    assert rec.translation_cache.entries() == entries
+    assert 0 in kinds and (0x010 in kinds or 0x020 in kinds)
+
+
+@pytest.mark.parametrize("mode", ["shadow", "tdp"])
+def test_parallel_fifo_replay_copy_from_user_batch(cuda, mode):
+    """copy_from_user batches never conflict, so the whole batch runs through
+    one plan + parallel FIFO replay + exec; compare with the sequential oracle."""
+    memv, g, sp = _fifo_world(mode)
+    rng = random.Random(5)
+    rec = be.GuestProcessRecord(S._Guest(0, mode), sp, memv)
+    rec.translation_cache.insert((S.BUF >> 12) + 5, (S.BUF >> 12) + 2)
+    acc = be.SoftwareHasAccess(rec, memv)
+    data = np.frombuffer(random.Random(1).randbytes(40 * 4096), dtype=np.uint8)
+    assert acc.copy_to_user(S.BUF, data.tobytes()) == len(data) or True
+    n_ops = 5000
+    gvas = [S.BUF + rng.randrange(46 * 4096) for _ in range(n_ops)]
+    lens = [rng.randrange(1, 3 * 4096) for _ in range(n_ops)]
+    raw = np.frombuffer(S.image_bytes(memv.host_mem), dtype=np.uint8).copy()
+    c0 = rec.translation_cache
+    ocache = O.new_cache(c0.capacity, c0.entries(), c0.hits, c0.misses)
+    payload, outs = acc.copy_from_user_batch(gvas, lens)
+    payload = payload.cpu().numpy()
+    offs = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.uint64)
+    rows = np.stack([np.array(gvas, np.uint64), np.array(lens, np.uint64), offs, np.zeros(n_ops, np.uint64)], 1)
+    spc = rec.translator.device_space
+    obuf = np.zeros(sum(lens), np.uint8)
+    res = O.copy(raw, O.space(spc.s1_base, spc.s1_root_pfn, spc.s2_root_pfn, spc.mode).reshape(1, 4), rows,
+                 obuf, 1, caches=ocache, op_cache=[0] * n_ops)
+    for i, (o, r) in enumerate(zip(outs, res)):
+        st = int(r[3]) & 0xFFFFFFFF
+        done = int(r[0])
+        a = int(offs[i])
+        assert np.array_equal(payload[a:a + done], obuf[a:a + done]), i
+        if st == 0:
+            assert o == lens[i]
+        else:
+            assert isinstance(o, Exception)
+    entries, hits, misses = O.cache_state(ocache)
+    assert (rec.translation_cache.hits, rec.translation_cache.misses) == (hits, misses)
+    assert rec.translation_cache.entries() == entries
