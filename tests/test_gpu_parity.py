@@ -416,10 +416,13 @@ def test_parallel_fifo_replay_copy_from_user_batch(cuda, mode):
     memv, g, sp = _fifo_world(mode)
     rng = random.Random(5)
     rec = be.GuestProcessRecord(S._Guest(0, mode), sp, memv)
-    rec.translation_cache.insert((S.BUF >> 12) + 5, (S.BUF >> 12) + 2)
     acc = be.SoftwareHasAccess(rec, memv)
     data = np.frombuffer(random.Random(1).randbytes(40 * 4096), dtype=np.uint8)
-    assert acc.copy_to_user(S.BUF, data.tobytes()) == len(data) or True
+    assert acc.copy_to_user(S.BUF, data.tobytes()) == len(data)
+    # a stale entry: page 5 -> the frame of page 2 (valid memory, wrong page)
+    stale = memv.translator(sp, use_cache=False).translate(S.BUF + 2 * 4096) >> 12
+    rec.translation_cache.flush_page((S.BUF >> 12) + 5)
+    rec.translation_cache.insert((S.BUF >> 12) + 5, stale)
     n_ops = 5000
     gvas = [S.BUF + rng.randrange(46 * 4096) for _ in range(n_ops)]
     lens = [rng.randrange(1, 3 * 4096) for _ in range(n_ops)]
