@@ -279,6 +279,22 @@ int pv_copy_fifo_replay(const pv_op* ops, const uint64_t* page_off,
                         uint32_t* page_status, uint64_t* op_first_bad,
                         void* scratch, uint64_t scratch_bytes, void* stream);
 
+/* Ordered execution of a PV_TO_GUEST batch whose chunks share destination
+ * pages (the stamp pass reported a conflict): runs after pv_copy_plan (and
+ * pv_copy_fifo_replay) instead of pv_copy_exec and gives exactly the bytes
+ * the reference's sequential copy_user_buffer calls leave (last writer wins
+ * in op order, pages of an op in order); fills results[] like pv_copy_exec.
+ * Chunks are grouped by destination page with a stable radix sort and each
+ * page is rebuilt in shared memory by one CTA.  scratch: device memory of
+ * pv_copy_ordered_scratch_bytes(n_pages, image_bytes) bytes. */
+uint64_t pv_copy_ordered_scratch_bytes(uint64_t n_pages, uint64_t image_bytes);
+int pv_copy_ordered(uint8_t* image, uint64_t image_bytes, const pv_op* ops,
+                    uint64_t n_ops, const uint64_t* page_off, uint64_t n_pages,
+                    const uint64_t* page_hpa, const uint32_t* page_status,
+                    const uint64_t* page_aux, const uint64_t* op_first_bad,
+                    const uint8_t* buf, pv_op_result* results, uint8_t* dirty,
+                    void* scratch, uint64_t scratch_bytes, void* stream);
+
 /* ---- utility kernels used by the host runtime ---------------------------- */
 /* Scatter `n` whole pages from a (pinned) host staging area into the image:
  * page i of src goes to image page pfns[i].  pfns device, src device. */

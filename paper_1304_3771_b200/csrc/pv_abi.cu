@@ -22,6 +22,10 @@ cudaError_t launch_copy_exec(uint8_t*, uint64_t, const pv_op*, uint64_t, const u
                              const uint64_t*, const uint32_t*, const uint64_t*, const uint64_t*, uint8_t*,
                              pv_op_result*, uint8_t*, const uint32_t*, cudaStream_t);
 size_t fifo_scratch_bytes(uint64_t, uint64_t, uint32_t);
+size_t ordered_scratch_bytes(uint64_t, uint64_t);
+cudaError_t launch_copy_ordered(uint8_t*, uint64_t, const pv_op*, uint64_t, const uint64_t*, uint64_t, const uint64_t*,
+                                const uint32_t*, const uint64_t*, const uint64_t*, const uint8_t*, pv_op_result*,
+                                uint8_t*, void*, uint64_t, cudaStream_t);
 cudaError_t launch_fifo_lanes_abi(const void*, uint32_t, const uint64_t*, const uint64_t*, const uint64_t*, uint32_t,
                                   uint32_t, pv_fifo*, uint64_t*, uint32_t*, void*, uint64_t, cudaStream_t);
 cudaError_t launch_fifo_copy_abi(const pv_op*, const uint64_t*, const uint64_t*, const uint32_t*, const uint64_t*,
@@ -188,6 +192,22 @@ int pv_copy_fifo_replay(const pv_op* ops, const uint64_t* page_off, const uint64
   return rc(launch_fifo_copy_abi(ops, page_off, look_page, look_op, proc_off, win_off, n_procs, capacity, fifo,
                                  image_bytes, page_hpa, page_status, op_first_bad, scratch, scratch_bytes,
                                  (cudaStream_t)stream));
+}
+
+uint64_t pv_copy_ordered_scratch_bytes(uint64_t n_pages, uint64_t image_bytes) {
+  return ordered_scratch_bytes(n_pages, image_bytes >> kPageShift);
+}
+
+int pv_copy_ordered(uint8_t* image, uint64_t image_bytes, const pv_op* ops, uint64_t n_ops, const uint64_t* page_off,
+                    uint64_t n_pages, const uint64_t* page_hpa, const uint32_t* page_status,
+                    const uint64_t* page_aux, const uint64_t* op_first_bad, const uint8_t* buf,
+                    pv_op_result* results, uint8_t* dirty, void* scratch, uint64_t scratch_bytes, void* stream) {
+  if (n_ops == 0) return PV_SUCCESS;
+  if (!image || !ops || !page_off || !page_hpa || !page_status || !op_first_bad || !buf || !results || !scratch)
+    return PV_EINVAL;
+  if (image_bytes % kPageSize) return PV_EINVAL;
+  return rc(launch_copy_ordered(image, image_bytes, ops, n_ops, page_off, n_pages, page_hpa, page_status, page_aux,
+                                op_first_bad, buf, results, dirty, scratch, scratch_bytes, (cudaStream_t)stream));
 }
 
 int pv_scatter_pages(uint8_t* image, uint64_t image_bytes, const uint64_t* pfns, uint64_t n, const uint8_t* src,

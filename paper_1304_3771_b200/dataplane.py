@@ -634,68 +634,42 @@ def decode_results(res: np.ndarray) -> list[OpOutcome]:
     return out
 
 
+def copy_ordered(image, plan: CopyPlan, buf) -> None:
+    """Ordered execution of a planned to_guest batch whose chunks share
+    destination pages (pv_copy_ordered): exact last-writer-wins."""
+    import torch
+
+    lib = N.lib()
+    dev_img = image.device()
+    nbytes = int(lib.pv_copy_ordered_scratch_bytes(plan.n_pages, image.nbytes))
+    scratch = torch.empty(max(nbytes, 1), dtype=torch.uint8, device="cuda")
+    N.check(lib.pv_copy_ordered(dev_img.data_ptr(), image.nbytes, plan.ops.data_ptr(), plan.n_ops,
+                                plan.page_off.data_ptr(), plan.n_pages, plan.page_hpa.data_ptr(),
+                                plan.page_status.data_ptr(), plan.page_aux.data_ptr(), plan.first_bad.data_ptr(),
+                                buf.data_ptr(), plan.results.data_ptr(), image.dirty_map().data_ptr(),
+                                scratch.data_ptr(), nbytes, _stream().cuda_stream), "pv_copy_ordered")
+    image.note_device_write()
+
+
 def copy_ops(image, spaces: list[Space], ops: np.ndarray, direction: int, buf, *, caches=None, fifo_groups=None,
              detect_conflicts: bool = True) -> list[OpOutcome]:
     """Run a batch of copies with the reference's sequential semantics.
 
     ``caches`` (with ``fifo_groups``) are host TranslationCache objects whose
     state is replayed on the device and written back.  When the stamp pass
-    finds two pages of the batch writing one hpa page, the batch is re-run
-    one op at a time (in order), which reproduces last-writer-wins exactly.
+    finds two chunks of a to_guest batch writing one hpa page, the exec kernel
+    stands down and the batch runs through the ordered path
+    (:func:`copy_ordered`), which reproduces last-writer-wins exactly.
     """
-    import torch
-
     cap = fifo_capacity(caches) if caches is not None else 10
     plan = CopyPlan(spaces, ops, fifo_groups=fifo_groups if caches is not None else None)
     fifo_dev = _to_dev(pack_fifo(caches)) if caches is not None else None
-    snapshot = fifo_dev.clone() if fifo_dev is not None else None
     copy_launch(image, plan, direction, buf, fifo_dev=fifo_dev, fifo_cap=cap, detect_conflicts=detect_conflicts)
-    conflict = int(plan.conflict.item()) if (direction == N.TO_GUEST and detect_conflicts) else 0
-    if not conflict:
-        results = decode_results(plan.results.cpu().numpy())
-        if caches is not None:
-            unpack_fifo(fifo_dev.cpu().numpy(), caches)
-        return results
-    # Ordered re-run: one op (and, for ops whose own pages alias, one page) at
-    # a time.  The FIFO state restarts from the pre-batch snapshot.
-    fifo_dev = snapshot
-    ops = np.ascontiguousarray(ops, dtype=np.uint64).reshape(-1, 4)
-    proc_of = {}
-    if caches is not None:
-        for p, group in enumerate(fifo_groups):
-            for o in group:
-                proc_of[int(o)] = p
-    results = []
-    for i in range(len(ops)):
-        out = _copy_one_ordered(image, spaces, ops[i], direction, buf, fifo_dev, proc_of.get(i), caches, cap)
-        results.append(out)
+    if direction == N.TO_GUEST and detect_conflicts and int(plan.conflict.item()):
+        copy_ordered(image, plan, buf)
+    results = decode_results(plan.results.cpu().numpy())
     if caches is not None:
         unpack_fifo(fifo_dev.cpu().numpy(), caches)
     return results
 
 
-def _copy_one_ordered(image, spaces, op, direction, buf, fifo_dev, proc, caches, cap=10) -> OpOutcome:
-    """One op, split into single-page sub-ops if its own pages alias."""
-    fifo_one = None
-    if caches is not None and proc is not None:
-        fifo_one = fifo_dev[proc:proc + 1]
-    groups = [[0]] if fifo_one is not None else None
-    plan = CopyPlan(spaces, op.reshape(1, 4), fifo_groups=groups)
-    copy_launch(image, plan, direction, buf, fifo_dev=fifo_one, fifo_cap=cap, detect_conflicts=True)
-    if not int(plan.conflict.item()):
-        return decode_results(plan.results.cpu().numpy())[0]
-    gva, length, buf_off, sp = (int(x) for x in op)
-    copied = 0
-    while copied < length:
-        cur = gva + copied
-        chunk = min(length - copied, PAGE_SIZE - (cur & PAGE_MASK))
-        sub = np.array([[cur, chunk, buf_off + copied, sp]], dtype=np.uint64)
-        splan = CopyPlan(spaces, sub, fifo_groups=groups)
-        copy_launch(image, splan, direction, buf, fifo_dev=fifo_one, fifo_cap=cap, detect_conflicts=False)
-        r = decode_results(splan.results.cpu().numpy())[0]
-        if r.status != N.ST_OK:
-            r.copied = copied
-            r.fail_page = (cur >> PAGE_SHIFT) - (gva >> PAGE_SHIFT)
-            return r
-        copied += chunk
-    return OpOutcome(N.ST_OK, length, 0, 0, 0)

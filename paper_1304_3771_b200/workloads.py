@@ -153,3 +153,49 @@ def c5_ops(cfg: C5Config, guest: int) -> list[np.ndarray]:
         lens = np.full(per[p], cfg.op_bytes, dtype=np.uint64)
         out.append(np.stack([gvas, lens], axis=1))
     return out
+
+
+# ---- C2 ----------------------------------------------------------------------------
+
+C2_ARENA_GVA = 0x2000_0000
+C2_ARENA_PAGES = 256
+C2_PROCS = 8
+
+
+def build_c2(n_procs: int = C2_PROCS):
+    """One TDP guest, ``n_procs`` processes each with a 256-page arena at
+    0x2000_0000."""
+    memv = mv.MemoryVirtualizer()
+    guest = memv.add_guest(0, "tdp")
+    spaces = []
+    for _ in range(n_procs):
+        sp = memv.create_process(guest)
+        memv.map_region(sp, C2_ARENA_GVA, C2_ARENA_PAGES)
+        spaces.append(sp)
+    return memv, guest, spaces
+
+
+def c2_trace(n_ops: int, n_procs: int = C2_PROCS, seed: int = 3771):
+    """IOCTL_SNAPSHOT trace: op i runs in process i % n_procs with
+    arg_len = randint(64, 4096) at arg_gva = arena + randrange(1 MiB - 4096).
+    Returns (proc, gva, len) arrays in program order."""
+    rng = np.random.default_rng(seed)
+    lens = rng.integers(64, 4097, size=n_ops, dtype=np.int64)
+    gvas = C2_ARENA_GVA + rng.integers(0, (1 << 20) - 4096, size=n_ops, dtype=np.int64)
+    procs = np.arange(n_ops, dtype=np.int64) % n_procs
+    return procs, gvas, lens
+
+
+def snapshot_blob(n: int) -> np.ndarray:
+    """The EventDevice IOCTL_SNAPSHOT result blob (devices.py:162-166)."""
+    return ((np.arange(n, dtype=np.int64) * 7 + 3) & 0xFF).astype(np.uint8)
+
+
+def c2_payload(lens: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+    """Per-op blobs laid out back to back: (buffer, offsets)."""
+    offs = np.zeros(len(lens), dtype=np.int64)
+    if len(lens) > 1:
+        np.cumsum(lens[:-1], out=offs[1:])
+    total = int(lens.sum())
+    pos = np.arange(total, dtype=np.int64) - np.repeat(offs, lens)
+    return ((pos * 7 + 3) & 0xFF).astype(np.uint8), offs

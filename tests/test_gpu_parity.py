@@ -449,3 +449,31 @@ def test_parallel_fifo_replay_copy_from_user_batch(cuda, mode):
     entries, hits, misses = O.cache_state(ocache)
     assert (rec.translation_cache.hits, rec.translation_cache.misses) == (hits, misses)
     assert rec.translation_cache.entries() == entries
+
+
+def test_c2_ioctl_trace_ordered_fifo_batch(cuda):
+    """BASELINE config 2 (scaled to 80k ops): IOCTL_SNAPSHOT blobs staged
+    with copy_to_user into 8 processes' 1 MiB arenas of a TDP guest through
+    the software HAS (FIFO-cached translators), heavily overlapping ->
+    last-writer-wins.  One device batch (plan + parallel FIFO replay + ordered
+    apply) must leave the bytes and cache counters of the sequential oracle."""
+    from paper_1304_3771_b200 import workloads as W
+
+    memv, guest, spaces = W.build_c2()
+    procs, gvas, lens = W.c2_trace(80_000)
+    buf, offs = W.c2_payload(lens)
+    trs = [memv.translator(sp, mv.TranslationCache()) for sp in spaces]
+    dspaces = [t.device_space for t in trs]
+    rows = np.stack([gvas, lens, offs, procs], 1).astype(np.uint64)
+    groups = [np.flatnonzero(procs == p) for p in range(len(spaces))]
+    raw = np.frombuffer(S.image_bytes(memv.host_mem), dtype=np.uint8).copy()
+    outs = dp.copy_ops(memv.host_mem.backing, dspaces, rows, N.TO_GUEST, torch.from_numpy(buf).cuda(),
+                       caches=[t.cache for t in trs], fifo_groups=groups)
+    assert all(o.status == 0 and o.copied == int(n) for o, n in zip(outs, lens))
+    ocaches = np.stack([O.new_cache() for _ in spaces])
+    ospaces = np.stack([O.space(s.s1_base, s.s1_root_pfn, s.s2_root_pfn, s.mode) for s in dspaces])
+    O.copy(raw, ospaces, rows, buf.copy(), 0, caches=ocaches, op_cache=procs.astype(np.int32))
+    assert np.array_equal(np.frombuffer(S.image_bytes(memv.host_mem), dtype=np.uint8), raw)
+    for t, oc in zip(trs, ocaches):
+        entries, hits, misses = O.cache_state(oc)
+        assert (t.cache.hits, t.cache.misses, t.cache.entries()) == (hits, misses, entries)
