@@ -9,9 +9,9 @@
 // destination page: it stages the page in shared memory, applies every chunk
 // of that page in order (all source bytes really move; the successive
 // overwrites land in SMEM instead of HBM, the way a write-back cache would
-// absorb them), and writes the page back once.  Source bytes of the next
-// chunk are prefetched into registers while the current one is applied, so
-// the per-chunk barrier only orders the shared-memory writes.
+// absorb them), and writes the page back once.  Chunk payloads stream in
+// through a cp.async ring ahead of the ordered applies, so the per-chunk
+// barrier only orders the shared-memory writes.
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_run_length_encode.cuh>
 #include <cub/device/device_scan.cuh>
@@ -23,71 +23,112 @@ namespace pv {
 constexpr int kOrdTpb = 256;
 constexpr uint32_t kDeadKey = 0xFFFFFFFFu;
 
-// keys[p] = destination page of live page p, else kDeadKey; vals[p] = p.
+// keys[p] = destination page of live page p, else kDeadKey; vals[p] = p;
+// page_op[p] = the op page p belongs to.
 __global__ void ordered_keys_kernel(const uint64_t* __restrict__ page_off, uint64_t n_ops, uint64_t n_pages,
                                     const uint64_t* __restrict__ page_hpa, const unsigned long long* __restrict__ first_bad,
-                                    uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+                                    uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                                    uint32_t* __restrict__ page_op) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n_pages; p += stride) {
     const uint64_t op = upper_search(page_off, 0, n_ops, p);
     const uint64_t k = p - page_off[op];
     keys[p] = k < first_bad[op] ? (uint32_t)(page_hpa[p] >> kPageShift) : kDeadKey;
     vals[p] = (uint32_t)p;
+    page_op[p] = (uint32_t)op;
   }
 }
 
-// One CTA per destination page segment.
+constexpr int kRing = 4;                       // chunks in flight per CTA
+constexpr uint32_t kSlot = kPageSize + 32;     // aligned superset of a <= 4 KiB chunk
+constexpr uint32_t kBatch = kOrdTpb;           // chunk descriptors resolved per round
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// One CTA per destination page: stage the page in SMEM, then apply its
+// chunks in order.  Chunk descriptors are resolved 256 at a time (one per
+// thread, independent loads); chunk payloads stream in with 16-byte
+// cp.async (LDGSTS) into a 4-deep SMEM ring, so global-memory latency
+// overlaps the ordered SMEM applies.  The buffer must be readable up to the
+// next 16-byte boundary after each chunk (true of any 512-byte-granular
+// device allocation).
 __global__ void __launch_bounds__(kOrdTpb)
-ordered_apply_kernel(uint8_t* __restrict__ image, const pv_op* __restrict__ ops, uint64_t n_ops,
-                     const uint64_t* __restrict__ page_off, const uint64_t* __restrict__ page_hpa,
+ordered_apply_kernel(uint8_t* __restrict__ image, const pv_op* __restrict__ ops, const uint64_t* __restrict__ page_off,
+                     const uint64_t* __restrict__ page_hpa, const uint32_t* __restrict__ page_op,
                      const uint32_t* __restrict__ sorted_pages, const uint32_t* __restrict__ seg_key,
                      const uint32_t* __restrict__ seg_len, const uint32_t* __restrict__ seg_start,
-                     const uint32_t* __restrict__ n_segs_dev, const uint8_t* __restrict__ buf, uint8_t* __restrict__ dirty) {
+                     const uint32_t* __restrict__ n_segs_dev, const uint8_t* __restrict__ buf,
+                     uint8_t* __restrict__ dirty) {
   __shared__ __align__(16) uint8_t page[kPageSize];
+  __shared__ __align__(16) uint8_t ring[kRing][kSlot];
+  __shared__ uint64_t d_src[kBatch];   // 16-byte aligned source start
+  __shared__ uint32_t d_meta[kBatch];  // shift (4 bits) | off (12 bits) << 4 | len (13 bits) << 16
   const uint32_t n_segs = *n_segs_dev;
+  const uint32_t t = threadIdx.x;
   for (uint32_t s = blockIdx.x; s < n_segs; s += gridDim.x) {
     const uint32_t key = seg_key[s];
     if (key == kDeadKey) continue;
     const uint64_t dst = (uint64_t)key << kPageShift;
-    // stage the destination page
-    reinterpret_cast<uint4*>(page)[threadIdx.x] = reinterpret_cast<const uint4*>(image + dst)[threadIdx.x];
+    reinterpret_cast<uint4*>(page)[t] = reinterpret_cast<const uint4*>(image + dst)[t];
     const uint32_t b = seg_start[s], n = seg_len[s];
-    // per chunk: thread t moves bytes [16t, 16t+16) of the chunk
-    uint8_t nxt[16];
-    uint32_t nxt_off = 0, nxt_len = 0;
-    auto fetch = [&](uint32_t c, uint8_t (&v)[16], uint32_t& off, uint32_t& len) {
-      const uint64_t p = sorted_pages[b + c];
-      const uint64_t op = upper_search(page_off, 0, n_ops, p);
-      const pv_op o = ops[op];
-      const uint64_t k = p - page_off[op];
-      const uint64_t cur = op_page_va(o.gva, k);
-      const uint64_t done = cur - o.gva;
-      len = (uint32_t)min(o.len - done, kPageSize - (cur & kPageMask));
-      off = (uint32_t)(page_hpa[p] & kPageMask);
-      const uint8_t* src = buf + o.buf_off + done;
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const uint32_t x = threadIdx.x * 16 + i;
-        v[i] = x < len ? src[x] : 0;
-      }
-    };
-    if (n) fetch(0, nxt, nxt_off, nxt_len);
-    __syncthreads();
-    for (uint32_t c = 0; c < n; ++c) {
-      uint8_t v[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] = nxt[i];
-      const uint32_t off = nxt_off, len = nxt_len;
-      if (c + 1 < n) fetch(c + 1, nxt, nxt_off, nxt_len);
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const uint32_t x = threadIdx.x * 16 + i;
-        if (x < len) page[off + x] = v[i];
+    for (uint32_t base = 0; base < n; base += kBatch) {
+      const uint32_t m = min(kBatch, n - base);
+      __syncthreads();  // previous round's descriptors / ring slots are free
+      if (t < m) {
+        const uint32_t p = sorted_pages[b + base + t];
+        const uint32_t op = page_op[p];
+        const pv_op o = ops[op];
+        const uint64_t k = p - page_off[op];
+        const uint64_t cur = op_page_va(o.gva, k);
+        const uint64_t done = cur - o.gva;
+        const uint32_t len = (uint32_t)min(o.len - done, kPageSize - (cur & kPageMask));
+        const uint32_t off = (uint32_t)(page_hpa[p] & kPageMask);
+        const uint64_t src = reinterpret_cast<uint64_t>(buf + o.buf_off + done);
+        d_src[t] = src & ~15ull;
+        d_meta[t] = (uint32_t)(src & 15) | (off << 4) | (len << 16);
       }
       __syncthreads();
+      auto issue = [&](uint32_t c) {
+        const uint32_t meta = d_meta[c];
+        const uint32_t shift = meta & 15, len = meta >> 16;
+        const uint32_t blocks = (shift + len + 15) >> 4;  // <= 257
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(d_src[c]);
+        uint8_t* slot = ring[c % kRing];
+        for (uint32_t i = t; i < blocks; i += kOrdTpb) cp_async16(slot + 16 * i, src + 16 * i);
+      };
+#pragma unroll
+      for (int c = 0; c < kRing - 1; ++c) {
+        if ((uint32_t)c < m) issue(c);
+        cp_async_commit();
+      }
+      for (uint32_t c = 0; c < m; ++c) {
+        if (c + kRing - 1 < m) issue(c + kRing - 1);
+        cp_async_commit();
+        cp_async_wait<kRing - 1>();  // chunk c's group (this thread's part) landed
+        __syncthreads();             // ... and every thread's part
+        const uint32_t meta = d_meta[c];
+        const uint32_t shift = meta & 15, off = (meta >> 4) & 0xFFF, len = meta >> 16;
+        const uint8_t* slot = ring[c % kRing] + shift;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const uint32_t x = t * 16 + i;
+          if (x < len) page[off + x] = slot[x];
+        }
+        __syncthreads();  // chunk c applied before c+1; its slot may be refilled
+      }
+      cp_async_wait<0>();
     }
-    reinterpret_cast<uint4*>(image + dst)[threadIdx.x] = reinterpret_cast<const uint4*>(page)[threadIdx.x];
-    if (dirty != nullptr && threadIdx.x == 0) dirty[key] = 1;
+    __syncthreads();
+    reinterpret_cast<uint4*>(image + dst)[t] = reinterpret_cast<const uint4*>(page)[t];
+    if (dirty != nullptr && t == 0) dirty[key] = 1;
     __syncthreads();
   }
 }
@@ -121,7 +162,7 @@ __global__ void ordered_results_kernel(const pv_op* __restrict__ ops, uint64_t n
 }
 
 struct OrderedScratch {
-  uint32_t *keys_in, *vals_in, *keys_out, *vals_out, *seg_key, *seg_len, *seg_start, *n_segs;
+  uint32_t *keys_in, *vals_in, *keys_out, *vals_out, *seg_key, *seg_len, *seg_start, *page_op, *n_segs;
   void* cub_tmp;
   size_t cub_bytes;
 };
@@ -142,13 +183,14 @@ static int bits_for(uint64_t) {
 
 size_t ordered_scratch_bytes(uint64_t n_pages, uint64_t image_pages) {
   const uint64_t arr = ((n_pages + 1) * 4 + 255) / 256 * 256;
-  return 7 * arr + 256 + cub_need(n_pages, bits_for(image_pages)) + 256;
+  return 8 * arr + 256 + cub_need(n_pages, bits_for(image_pages)) + 256;
 }
 
 static OrderedScratch carve(void* base, uint64_t n, size_t cub_bytes) {
   uint8_t* p = static_cast<uint8_t*>(base);
   OrderedScratch s;
-  uint32_t** arrs[] = {&s.keys_in, &s.vals_in, &s.keys_out, &s.vals_out, &s.seg_key, &s.seg_len, &s.seg_start};
+  uint32_t** arrs[] = {&s.keys_in, &s.vals_in, &s.keys_out, &s.vals_out, &s.seg_key, &s.seg_len, &s.seg_start,
+                       &s.page_op};
   for (auto a : arrs) {
     *a = reinterpret_cast<uint32_t*>(p);
     p += ((n + 1) * 4 + 255) / 256 * 256;
@@ -182,7 +224,7 @@ cudaError_t launch_copy_ordered(uint8_t* image, uint64_t image_bytes, const pv_o
   if (grid > 4096) grid = 4096;
   ordered_keys_kernel<<<(unsigned)grid, 256, 0, stream>>>(page_off, n_ops, n_pages, page_hpa,
                                                           reinterpret_cast<const unsigned long long*>(op_first_bad),
-                                                          s.keys_in, s.vals_in);
+                                                          s.keys_in, s.vals_in, s.page_op);
   size_t tb = s.cub_bytes;
   cudaError_t e = cub::DeviceRadixSort::SortPairs(s.cub_tmp, tb, s.keys_in, s.keys_out, s.vals_in, s.vals_out,
                                                   (int)n_pages, 0, end_bit, stream);
@@ -196,7 +238,7 @@ cudaError_t launch_copy_ordered(uint8_t* image, uint64_t image_bytes, const pv_o
   if (e != cudaSuccess) return e;
   uint64_t g2 = resident_grid((const void*)ordered_apply_kernel, kOrdTpb, 0);
   if (g2 > n_pages) g2 = n_pages;
-  ordered_apply_kernel<<<(unsigned)g2, kOrdTpb, 0, stream>>>(image, ops, n_ops, page_off, page_hpa, s.vals_out,
+  ordered_apply_kernel<<<(unsigned)g2, kOrdTpb, 0, stream>>>(image, ops, page_off, page_hpa, s.page_op, s.vals_out,
                                                              s.seg_key, s.seg_len, s.seg_start, s.n_segs, buf, dirty);
   return cudaGetLastError();
 }
