@@ -39,8 +39,9 @@ __global__ void ordered_keys_kernel(const uint64_t* __restrict__ page_off, uint6
   }
 }
 
-constexpr int kRing = 4;                       // chunks in flight per CTA
-constexpr uint32_t kSlot = kPageSize + 32;     // aligned superset of a <= 4 KiB chunk
+constexpr int kRing = 8;                       // chunks in flight per CTA
+constexpr uint32_t kSlotPad = 16;              // headroom so word reads at offset -3.. stay in the slot
+constexpr uint32_t kSlot = kSlotPad + kPageSize + 32;  // aligned superset of a <= 4 KiB chunk
 constexpr uint32_t kBatch = kOrdTpb;           // chunk descriptors resolved per round
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -101,7 +102,7 @@ ordered_apply_kernel(uint8_t* __restrict__ image, const pv_op* __restrict__ ops,
         const uint32_t shift = meta & 15, len = meta >> 16;
         const uint32_t blocks = (shift + len + 15) >> 4;  // <= 257
         const uint8_t* src = reinterpret_cast<const uint8_t*>(d_src[c]);
-        uint8_t* slot = ring[c % kRing];
+        uint8_t* slot = ring[c % kRing] + kSlotPad;
         for (uint32_t i = t; i < blocks; i += kOrdTpb) cp_async16(slot + 16 * i, src + 16 * i);
       };
 #pragma unroll
@@ -116,11 +117,24 @@ ordered_apply_kernel(uint8_t* __restrict__ image, const pv_op* __restrict__ ops,
         __syncthreads();             // ... and every thread's part
         const uint32_t meta = d_meta[c];
         const uint32_t shift = meta & 15, off = (meta >> 4) & 0xFFF, len = meta >> 16;
-        const uint8_t* slot = ring[c % kRing] + shift;
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const uint32_t x = t * 16 + i;
-          if (x < len) page[off + x] = slot[x];
+        // destination-aligned 4-byte words; each word is owned by one thread
+        // (no read-modify-write races), the source is realigned with a funnel
+        // shift from two aligned slot words; conflict-free SMEM banks.
+        const uint32_t* slot32 = reinterpret_cast<const uint32_t*>(ring[c % kRing]);
+        uint32_t* page32 = reinterpret_cast<uint32_t*>(page);
+        const uint32_t w_first = off >> 2, w_last = (off + len - 1) >> 2;
+        for (uint32_t w = w_first + t; w <= w_last; w += kOrdTpb) {
+          const int32_t s0 = (int32_t)(kSlotPad + shift + 4 * w) - (int32_t)off;  // slot byte of word byte 0
+          const uint32_t lo = slot32[s0 >> 2], hi = slot32[(s0 >> 2) + 1];
+          const uint32_t v = __funnelshift_r(lo, hi, (s0 & 3) * 8);
+          const uint32_t b0 = 4 * w < off ? off - 4 * w : 0;                      // first byte of the word in chunk
+          const uint32_t b1 = 4 * w + 4 > off + len ? off + len - 4 * w : 4;      // one past the last
+          if (b0 == 0 && b1 == 4) {
+            page32[w] = v;
+          } else {
+            const uint32_t m = (b1 == 4 ? 0xFFFFFFFFu : ((1u << (8 * b1)) - 1u)) & ~((1u << (8 * b0)) - 1u);
+            page32[w] = (page32[w] & ~m) | (v & m);
+          }
         }
         __syncthreads();  // chunk c applied before c+1; its slot may be refilled
       }
