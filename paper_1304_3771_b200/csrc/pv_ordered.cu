@@ -57,7 +57,7 @@ __device__ __forceinline__ void cp_async_wait() {
 // One CTA per destination page: stage the page in SMEM, then apply its
 // chunks in order.  Chunk descriptors are resolved 256 at a time (one per
 // thread, independent loads); chunk payloads stream in with 16-byte
-// cp.async (LDGSTS) into a 4-deep SMEM ring, so global-memory latency
+// cp.async (LDGSTS) into an 8-deep SMEM ring, so global-memory latency
 // overlaps the ordered SMEM applies.  The buffer must be readable up to the
 // next 16-byte boundary after each chunk (true of any 512-byte-granular
 // device allocation).
