@@ -295,6 +295,23 @@ int pv_copy_ordered(uint8_t* image, uint64_t image_bytes, const pv_op* ops,
                     const uint8_t* buf, pv_op_result* results, uint8_t* dirty,
                     void* scratch, uint64_t scratch_bytes, void* stream);
 
+/* ---- result-page codec ------------------------------
+ * Batched resultpage.encode + the backend's host_mem.write of the record
+ * (resultpage.py:44-51, backend.py:352-355): record r is header[9*r ..
+ * 9*r+8] = {status, flags, values[6], blob_len} followed by blob_len bytes
+ * of blob_buf at blob_off[r], written at image offset page_hpa[r].  At most
+ * one record per page per batch.  status[r]: PV_ST_OK, PV_ST_DATA_OOR
+ * (record past the image: OutOfRange), PV_ST_CONFLICT (blob_len > 4060:
+ * the codec's ValueError).  dirty as for pv_copy_exec. */
+int pv_result_encode(uint8_t* image, uint64_t image_bytes, const uint64_t* page_hpa,
+                     const uint32_t* header, const uint8_t* blob_buf,
+                     const uint64_t* blob_off, uint64_t n, uint32_t* status,
+                     uint8_t* dirty, void* stream);
+/* Batched resultpage.decode of the header words (resultpage.py:54-61);
+ * blobs stay in the image at page_hpa[r] + 36. */
+int pv_result_decode(const uint8_t* image, uint64_t image_bytes, const uint64_t* page_hpa,
+                     uint64_t n, uint32_t* header, uint32_t* status, void* stream);
+
 /* ---- utility kernels used by the host runtime ---------------------------- */
 /* Scatter `n` whole pages from a (pinned) host staging area into the image:
  * page i of src goes to image page pfns[i].  pfns device, src device. */

@@ -57,7 +57,8 @@ EXPORTS = (
     "pv_abi_version", "pv_translate_chunk", "pv_status_name", "pv_translate",
     "pv_fifo_replay", "pv_copy_plan", "pv_copy_stamp", "pv_copy_exec",
     "pv_copy_fifo_replay", "pv_scatter_pages", "pv_gather_pages", "pv_stream_sync", "pv_index_encode",
-    "pv_fifo_scratch_bytes", "pv_copy_ordered_scratch_bytes", "pv_copy_ordered",
+    "pv_fifo_scratch_bytes", "pv_copy_ordered_scratch_bytes", "pv_copy_ordered", "pv_result_encode",
+    "pv_result_decode",
 )
 
 _u64 = ctypes.c_uint64
@@ -73,6 +74,8 @@ _SIGNATURES = {
     "pv_fifo_replay": (ctypes.c_int, [_p, _u32, _p, _p, _p, _u32, _u32, _p, _p, _p, _p, _u64, _p]),
     "pv_fifo_scratch_bytes": (_u64, [_u64, _u64, _u32]),
     "pv_copy_ordered_scratch_bytes": (_u64, [_u64, _u64]),
+    "pv_result_encode": (ctypes.c_int, [_p, _u64, _p, _p, _p, _p, _u64, _p, _p, _p]),
+    "pv_result_decode": (ctypes.c_int, [_p, _u64, _p, _u64, _p, _p, _p]),
     "pv_copy_ordered": (ctypes.c_int, [_p, _u64, _p, _u64, _p, _u64, _p, _p, _p, _p, _p, _p, _p, _p, _u64, _p]),
     "pv_copy_plan": (ctypes.c_int, [_p, _u64, _p, _p, _u64, _p, _u64, _u32, _p, _p, _p, _p, _p, _u32, _p, _p]),
     "pv_copy_stamp": (ctypes.c_int, [_p, _u64, _u64, _p, _p, _p, _u64, _u32, _p, _p]),

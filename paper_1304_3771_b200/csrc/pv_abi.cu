@@ -23,6 +23,10 @@ cudaError_t launch_copy_exec(uint8_t*, uint64_t, const pv_op*, uint64_t, const u
                              pv_op_result*, uint8_t*, const uint32_t*, cudaStream_t);
 size_t fifo_scratch_bytes(uint64_t, uint64_t, uint32_t);
 size_t ordered_scratch_bytes(uint64_t, uint64_t);
+cudaError_t launch_result_encode(uint8_t*, uint64_t, const uint64_t*, const uint32_t*, const uint8_t*, const uint64_t*,
+                                 uint64_t, uint32_t*, uint8_t*, cudaStream_t);
+cudaError_t launch_result_decode(const uint8_t*, uint64_t, const uint64_t*, uint64_t, uint32_t*, uint32_t*,
+                                 cudaStream_t);
 cudaError_t launch_copy_ordered(uint8_t*, uint64_t, const pv_op*, uint64_t, const uint64_t*, uint64_t, const uint64_t*,
                                 const uint32_t*, const uint64_t*, const uint64_t*, const uint8_t*, pv_op_result*,
                                 uint8_t*, void*, uint64_t, cudaStream_t);
@@ -208,6 +212,22 @@ int pv_copy_ordered(uint8_t* image, uint64_t image_bytes, const pv_op* ops, uint
   if (image_bytes % kPageSize) return PV_EINVAL;
   return rc(launch_copy_ordered(image, image_bytes, ops, n_ops, page_off, n_pages, page_hpa, page_status, page_aux,
                                 op_first_bad, buf, results, dirty, scratch, scratch_bytes, (cudaStream_t)stream));
+}
+
+int pv_result_encode(uint8_t* image, uint64_t image_bytes, const uint64_t* page_hpa, const uint32_t* header,
+                     const uint8_t* blob_buf, const uint64_t* blob_off, uint64_t n, uint32_t* status, uint8_t* dirty,
+                     void* stream) {
+  if (n == 0) return PV_SUCCESS;
+  if (!image || !page_hpa || !header || !blob_off || !status) return PV_EINVAL;
+  return rc(launch_result_encode(image, image_bytes, page_hpa, header, blob_buf, blob_off, n, status, dirty,
+                                 (cudaStream_t)stream));
+}
+
+int pv_result_decode(const uint8_t* image, uint64_t image_bytes, const uint64_t* page_hpa, uint64_t n,
+                     uint32_t* header, uint32_t* status, void* stream) {
+  if (n == 0) return PV_SUCCESS;
+  if (!image || !page_hpa || !header || !status) return PV_EINVAL;
+  return rc(launch_result_decode(image, image_bytes, page_hpa, n, header, status, (cudaStream_t)stream));
 }
 
 int pv_scatter_pages(uint8_t* image, uint64_t image_bytes, const uint64_t* pfns, uint64_t n, const uint8_t* src,

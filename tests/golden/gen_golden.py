@@ -32,6 +32,12 @@ def load_reference(src: str):
     return memvirt, backend, errors
 
 
+def load_resultpage():
+    from devfsim import resultpage  # noqa: E402
+
+    return resultpage
+
+
 def save_image(name: str, mem, extra: dict, meta: dict) -> None:
     raw = S.image_bytes(mem)
     pages, data = S.sparse_pages(raw)
@@ -98,6 +104,8 @@ def main(src: str) -> None:
         )
         with open(os.path.join(HERE, f"c1_{mode}.json"), "w") as f:
             json.dump(meta, f)
+    with open(os.path.join(HERE, "resultpage.json"), "w") as f:
+        json.dump({"expected": S.resultpage_query(load_resultpage())}, f)
     print("golden fixtures written to", HERE)
 
 

@@ -345,3 +345,31 @@ def c1_build(mv, be, er, mode: str):
 def c1_vas(n: int = 1_000_000) -> np.ndarray:
     rng = random.Random(3771)
     return np.array([C1_GVA + rng.randrange(64 << 20) for _ in range(n)], dtype=np.uint64)
+
+
+# ---- scenario "resultpage": record codec (resultpage.py:44-61)
+
+def resultpage_records():
+    rng = random.Random(4060)
+    recs = [(0, (), None, False), (14, (4096,), None, False), (0, (1, 2, 3, 4, 5, 6, 7), b"", False),
+            (0, (9,), b"\x01\x02\x03", False), (3, (0xFFFFFFFF, 1), bytes(range(256)) * 15, True),
+            (0, (len(b"x" * 4060),), b"x" * 4060, False)]
+    for _ in range(20):
+        n = rng.randrange(0, 4061)
+        recs.append((rng.randrange(16), tuple(rng.randrange(1 << 32) for _ in range(rng.randrange(0, 7))),
+                     rng.randbytes(n) if rng.random() < 0.8 else None, rng.random() < 0.3))
+    return recs
+
+
+def resultpage_query(rp):
+    out = []
+    for status, values, blob, staged in resultpage_records():
+        enc = rp.encode(status, values, blob, staged)
+        d = rp.decode(enc + bytes(64))
+        out.append([enc.hex(), d.status, list(d.values), d.blob.hex() if d.blob is not None else None, d.staged])
+    try:
+        rp.encode(0, (), b"z" * 4061)
+        out.append("no error")
+    except ValueError:
+        out.append("ValueError")
+    return out

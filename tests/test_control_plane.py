@@ -181,3 +181,10 @@ def test_has_records_without_gpu():
     rec = be.GuestProcessRecord(S._Guest(0, "tdp"), sp, memv)
     with pytest.raises(er.TdpUnsupported):
         be.HardwareHasAccess(rec, memv)
+
+
+def test_resultpage_codec_matches_reference():
+    from paper_1304_3771_b200 import resultpage as rp
+
+    assert S.resultpage_query(rp) == load_json("resultpage.json")["expected"]
+    assert rp.HEADER_BYTES == 36 and rp.BLOB_CAPACITY == 4060

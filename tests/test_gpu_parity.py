@@ -477,3 +477,51 @@ def test_c2_ioctl_trace_ordered_fifo_batch(cuda):
     for t, oc in zip(trs, ocaches):
         entries, hits, misses = O.cache_state(oc)
         assert (t.cache.hits, t.cache.misses, t.cache.entries()) == (hits, misses, entries)
+
+
+def test_resultpage_encode_decode_deliver_batch(cuda):
+    """a batch of result records encoded into result pages
+    on the device is byte-identical to the reference codec, decodes back, and
+    the inline blobs delivered with guest_write semantics (uncached, prefix
+    then fault with bytes_copied 0, last writer wins) match the oracle."""
+    from paper_1304_3771_b200 import resultpage as rp
+    from paper_1304_3771_b200 import workloads as W
+
+    memv, guest, spaces = W.build_c2(4)
+    recs = S.resultpage_records()
+    rng = random.Random(8)
+    # one result page per record: reserved-looking frames high in the slot
+    gpas = [(guest.mem.n_pages - 200 + i) << 12 for i in range(len(recs))]
+    hpas = [memv.gpa_to_hpa(g, 0) for g in gpas]
+    errs = rp.encode_batch(memv.host_mem, hpas, recs)
+    assert all(e is None for e in errs)
+    for hpa, r in zip(hpas, recs):
+        enc = rp.encode(*r)
+        assert memv.host_mem.read(hpa, len(enc)) == enc
+    dec = rp.decode_batch(memv.host_mem, hpas)
+    assert dec == [rp.decode(rp.encode(*r)) for r in recs]
+    # delivery into the processes' arenas (overlapping), some unmapped targets
+    procs = [rng.randrange(4) for _ in recs]
+    gvas = [0 if rng.random() < 0.1 else (W.C2_ARENA_GVA + rng.randrange(W.C2_ARENA_PAGES * 4096 + 8192))
+            for _ in recs]
+    raw = np.frombuffer(S.image_bytes(memv.host_mem), dtype=np.uint8).copy()
+    out = rp.deliver_batch(memv, [spaces[p] for p in procs], hpas, gvas)
+    # oracle: guest_write one record after another
+    for i, (status, values, blob, staged) in enumerate(recs):
+        if not blob or staged or gvas[i] == 0:
+            assert out[i] is None
+            continue
+        tr = memv.translator(spaces[procs[i]], use_cache=False).device_space
+        osp = O.space(tr.s1_base, tr.s1_root_pfn, tr.s2_root_pfn, tr.mode).reshape(1, 4)
+        res = O.copy(raw, osp, np.array([[gvas[i], len(blob), 0, 0]], np.uint64),
+                     np.frombuffer(blob, dtype=np.uint8).copy(), 0)
+        st = int(res[0, 3]) & 0xFFFFFFFF
+        if st == 0:
+            assert out[i] is None
+        else:
+            assert isinstance(out[i], er.PageFault) and out[i].bytes_copied == 0
+    assert np.array_equal(np.frombuffer(S.image_bytes(memv.host_mem), dtype=np.uint8), raw)
+    assert any(isinstance(o, er.PageFault) for o in out)
+    # codec errors
+    errs = rp.encode_batch(memv.host_mem, [hpas[0]], [(0, (), b"z" * 4061, False)])
+    assert isinstance(errs[0], ValueError)
