@@ -504,6 +504,10 @@ def test_resultpage_encode_decode_deliver_batch(cuda):
     procs = [rng.randrange(4) for _ in recs]
     gvas = [0 if rng.random() < 0.1 else (W.C2_ARENA_GVA + rng.randrange(W.C2_ARENA_PAGES * 4096 + 8192))
             for _ in recs]
+    arena_end = W.C2_ARENA_GVA + W.C2_ARENA_PAGES * 4096
+    for i, r in enumerate(recs):  # blobs that run off the arena: fault after a written prefix
+        if r[2] and len(r[2]) > 64 and not r[3] and i % 3 == 0:
+            gvas[i] = arena_end - 40
     raw = np.frombuffer(S.image_bytes(memv.host_mem), dtype=np.uint8).copy()
     out = rp.deliver_batch(memv, [spaces[p] for p in procs], hpas, gvas)
     # oracle: guest_write one record after another
