@@ -529,3 +529,50 @@ def test_resultpage_encode_decode_deliver_batch(cuda):
     # codec errors
     errs = rp.encode_batch(memv.host_mem, [hpas[0]], [(0, (), b"z" * 4061, False)])
     assert isinstance(errs[0], ValueError)
+
+
+@pytest.mark.parametrize("va32", [False, True])
+@pytest.mark.parametrize("out_pfn", [False, True])
+def test_mixed_space_batch_segments_and_lane_formats(cuda, va32, out_pfn):
+    """One pv_translate launch over shadow, TDP, hybrid and guest-window
+    spaces in ragged segments (including empty ones and segments that end
+    mid-chunk), u32 or u64 VAs (u64 with bits >= 32 set: aliasing), address
+    or pfn output -- lane by lane against the oracle, with and without the
+    leaf index."""
+    w = S.walks_build(mv, be, er)
+    memv, p0, p1, g1 = w["memv"], w["p0"], w["p1"], w["g1"]
+    spaces = [memv.translator(p0, use_cache=False).device_space,
+              memv.translator(p1, use_cache=False).device_space,
+              dp.Space(0, w["hroot"].root_pfn),
+              dp.Space(g1.mem.base, p1.guest_root.root_pfn)]
+    rng = random.Random(va32 * 2 + out_pfn)
+    sizes = [5000, 0, 2048, 1, 7777, 2047, 4096, 300]
+    bounds, lane = [], 0
+    vas = []
+    for i, n in enumerate(sizes):
+        bounds.append((lane, lane + n, i % len(spaces)))
+        for _ in range(n):
+            va = rng.choice(S.walk_vas()) if rng.random() < 0.5 else S.BUF + rng.randrange(80 * 4096)
+            if not va32 and rng.random() < 0.2:
+                va |= rng.randrange(1, 1 << 20) << 32
+            vas.append(va & 0xFFFFFFFF if va32 else va)
+        lane += n
+    vas = np.array(vas, dtype=np.uint64)
+    raw = np.frombuffer(S.image_bytes(memv.host_mem), dtype=np.uint8).copy()
+    exp_v = np.zeros(len(vas), np.uint64)
+    exp_s = np.zeros(len(vas), np.uint32)
+    exp_a = np.zeros(len(vas), np.uint64)
+    for b, e, si in bounds:
+        if e > b:
+            s = spaces[si]
+            v, st, a = O.translate(raw, O.space(s.s1_base, s.s1_root_pfn, s.s2_root_pfn, s.mode), vas[b:e],
+                                   want_pfn=out_pfn, threads=0)
+            exp_v[b:e], exp_s[b:e], exp_a[b:e] = v, st, a
+    d = torch.tensor(vas.astype(np.uint32).view(np.int32) if va32 else vas.view(np.int64), device="cuda")
+    for use_index in (True, False):
+        plan = dp.TranslatePlan(spaces, bounds, use_index=use_index)
+        v, s, a = dp.translate_lanes(memv.host_mem.backing, plan, d, out_pfn=out_pfn)
+        assert np.array_equal(s.cpu().numpy().view(np.uint32), exp_s)
+        assert np.array_equal(v.cpu().numpy().view(np.uint64), exp_v)
+        assert np.array_equal(a.cpu().numpy().view(np.uint64), exp_a)
+    assert len(set((exp_s & 0xFF0).tolist())) >= 4
