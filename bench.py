@@ -216,6 +216,7 @@ def run_ours(args, rank, world, local):
     stream = torch.cuda.current_stream()
     s = stream.cuda_stream
     owner, _ = dp._owner_map(img)
+    hint = N.COPY_ALIGNED16 if plan.aligned16(wl.src.data_ptr()) else 0
 
     def step(ev):
         ev[0].record(stream)
@@ -235,7 +236,7 @@ def run_ours(args, rank, world, local):
                                   plan.conflict.data_ptr(), s), "stamp")
         ev[3].record(stream)
         N.check(lib.pv_copy_exec(dev.data_ptr(), img.nbytes, plan.ops.data_ptr(), plan.n_ops,
-                                 plan.page_off.data_ptr(), plan.n_pages, N.TO_GUEST, plan.page_hpa.data_ptr(),
+                                 plan.page_off.data_ptr(), plan.n_pages, N.TO_GUEST | hint, plan.page_hpa.data_ptr(),
                                  plan.page_status.data_ptr(), plan.page_aux.data_ptr(), plan.first_bad.data_ptr(),
                                  wl.src.data_ptr(), wl.src.numel(), plan.results.data_ptr(),
                                  img.dirty_map().data_ptr(), plan.conflict.data_ptr(), s), "exec")

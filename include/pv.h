@@ -169,6 +169,11 @@ typedef struct pv_fifo {
 
 #define PV_TO_GUEST 0u   /* copy_to_user  : buffer -> guest pages           */
 #define PV_FROM_GUEST 1u /* copy_from_user: guest pages -> buffer           */
+/* pv_copy_exec direction hint (or-ed in): for every op,
+ * (gva - (buf + buf_off)) % 16 == 0, so every chunk moves with 16-byte
+ * vectors (a lighter kernel with twice the resident warps).  Chunks that do
+ * not satisfy it are still copied correctly, byte-wise. */
+#define PV_COPY_ALIGNED16 0x100u
 
 /* ---- library ------------------------------------------------------------ */
 int pv_abi_version(void);

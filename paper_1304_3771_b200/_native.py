@@ -43,6 +43,7 @@ HAS_TWO_STAGE = 0x80000000
 
 TO_GUEST = 0
 FROM_GUEST = 1
+COPY_ALIGNED16 = 0x100
 
 FIFO_MAX = 32
 # struct sizes in 8-byte words (all structs are u64-aligned)

@@ -179,7 +179,8 @@ int pv_copy_exec(uint8_t* image, uint64_t image_bytes, const pv_op* ops, uint64_
   if (n_pages == 0) return PV_SUCCESS;
   if (!image || !ops || !page_off || !page_hpa || !page_status || !op_first_bad || !buf || !results)
     return PV_EINVAL;
-  if (direction != PV_TO_GUEST && direction != PV_FROM_GUEST) return PV_EINVAL;
+  if ((direction & ~PV_COPY_ALIGNED16) != PV_TO_GUEST && (direction & ~PV_COPY_ALIGNED16) != PV_FROM_GUEST)
+    return PV_EINVAL;
   return rc(launch_copy_exec(image, image_bytes, ops, n_ops, page_off, n_pages, direction, page_hpa, page_status,
                              page_aux, op_first_bad, buf, results, dirty, abort_flag, (cudaStream_t)stream));
 }

@@ -175,7 +175,38 @@ __device__ __forceinline__ void warp_copy(uint8_t* __restrict__ d, const uint8_t
   if (lane < tail) d[done + lane] = s[done + lane];
 }
 
-__global__ void __launch_bounds__(kExecTpb, 2)
+// Copy with 16-byte vectors only, for chunks whose source and destination
+// agree modulo 16 (the host proves it per batch: (gva - src) mod 16 is an op
+// constant); a chunk that does not qualify still copies correctly byte-wise.
+__device__ __forceinline__ void warp_copy_aligned(uint8_t* __restrict__ d, const uint8_t* __restrict__ s, uint32_t n,
+                                                  uint32_t lane, uint64_t pol) {
+  const uintptr_t da = reinterpret_cast<uintptr_t>(d), sa = reinterpret_cast<uintptr_t>(s);
+  if (((da ^ sa) & 15) != 0) {
+    warp_copy_bytes(d, s, n, lane);
+    return;
+  }
+  const uint32_t head = min(n, (uint32_t)((16 - (da & 15)) & 15));
+  if (lane < head) d[lane] = s[lane];
+  const uint32_t nv = (n - head) >> 4;
+  const uint4* sv = reinterpret_cast<const uint4*>(s + head);
+  uint4* dv = reinterpret_cast<uint4*>(d + head);
+  uint4 r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint32_t i = lane + 32 * j;
+    if (i < nv) r[j] = ld_v4_stream(sv + i, pol);
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint32_t i = lane + 32 * j;
+    if (i < nv) st_v4_stream(dv + i, r[j], pol);
+  }
+  const uint32_t done = head + (nv << 4), tail = n - done;
+  if (lane < tail) d[done + lane] = s[done + lane];
+}
+
+template <bool kAligned>
+__global__ void __launch_bounds__(kExecTpb, kAligned ? 4 : 2)
 exec_kernel(uint8_t* __restrict__ image, uint64_t image_bytes, const pv_op* __restrict__ ops, uint64_t n_ops,
             const uint64_t* __restrict__ page_off, uint64_t n_pages, uint32_t direction,
             const uint64_t* __restrict__ page_hpa, const uint32_t* __restrict__ page_status,
@@ -228,12 +259,11 @@ exec_kernel(uint8_t* __restrict__ image, uint64_t image_bytes, const pv_op* __re
       const uint64_t hpa = page_hpa[p];
       const uint32_t chunk = (uint32_t)min(o.len - done, kPageSize - (cur & kPageMask));
       uint8_t* bp = buf + o.buf_off + done;
-      if (direction == PV_TO_GUEST) {
-        warp_copy(image + hpa, bp, chunk, lane, pol);
-        if (dirty != nullptr && lane == 0) dirty[hpa >> kPageShift] = 1;
-      } else {
-        warp_copy(bp, image + hpa, chunk, lane, pol);
-      }
+      uint8_t* dst = direction == PV_TO_GUEST ? image + hpa : bp;
+      const uint8_t* src = direction == PV_TO_GUEST ? bp : image + hpa;
+      if (kAligned) warp_copy_aligned(dst, src, chunk, lane, pol);
+      else warp_copy(dst, src, chunk, lane, pol);
+      if (direction == PV_TO_GUEST && dirty != nullptr && lane == 0) dirty[hpa >> kPageShift] = 1;
     }
   }
 }
@@ -272,14 +302,17 @@ cudaError_t launch_copy_exec(uint8_t* image, uint64_t image_bytes, const pv_op* 
                              uint8_t* buf, pv_op_result* results, uint8_t* dirty, const uint32_t* abort_flag,
                              cudaStream_t stream) {
   if (n_pages == 0) return cudaSuccess;
+  const bool aligned = direction & PV_COPY_ALIGNED16;
+  direction &= ~PV_COPY_ALIGNED16;
+  auto k = aligned ? exec_kernel<true> : exec_kernel<false>;
   const uint64_t warps = (n_pages + kExecPpw - 1) / kExecPpw;
   uint64_t grid = (warps + kExecWarps - 1) / kExecWarps;
-  const uint64_t cap = resident_grid((const void*)exec_kernel, kExecTpb, 0);
+  const uint64_t cap = resident_grid((const void*)k, kExecTpb, 0);
   if (grid > cap) grid = cap;
-  exec_kernel<<<(unsigned)grid, kExecTpb, 0, stream>>>(image, image_bytes, ops, n_ops, page_off, n_pages, direction,
-                                                       page_hpa, page_status, page_aux,
-                                                       reinterpret_cast<const unsigned long long*>(op_first_bad), buf,
-                                                       results, dirty, abort_flag);
+  k<<<(unsigned)grid, kExecTpb, 0, stream>>>(image, image_bytes, ops, n_ops, page_off, n_pages, direction, page_hpa,
+                                             page_status, page_aux,
+                                             reinterpret_cast<const unsigned long long*>(op_first_bad), buf, results,
+                                             dirty, abort_flag);
   return cudaGetLastError();
 }
 

@@ -553,6 +553,19 @@ class CopyPlan:
             self.fifo_scratch = None
 
 
+def _aligned16(plan: "CopyPlan", buf_ptr: int) -> bool:
+    """(gva - (buf + buf_off)) % 16 == 0 for every op (host check, cached)."""
+    key = buf_ptr % 16
+    cache = plan.__dict__.setdefault("_aligned_cache", {})
+    if key not in cache:
+        o = plan.host_ops
+        cache[key] = bool(len(o) == 0 or (((o[:, 0] - o[:, 2] - np.uint64(key)) % np.uint64(16)) == 0).all())
+    return cache[key]
+
+
+CopyPlan.aligned16 = lambda self, buf_ptr: _aligned16(self, buf_ptr)
+
+
 def _owner_map(image):
     """Per-image conflict stamp map (one u64 per page) and epoch counter."""
     import torch
@@ -605,8 +618,9 @@ def copy_launch(image, plan: CopyPlan, direction: int, buf, *, fifo_dev=None, fi
                                       plan.conflict.data_ptr(), s), "pv_copy_stamp")
             abort = plan.conflict.data_ptr()
         dirty = image.dirty_map().data_ptr() if (direction == N.TO_GUEST and track_dirty) else None
+        hint = N.COPY_ALIGNED16 if plan.aligned16(buf.data_ptr()) else 0
         N.check(lib.pv_copy_exec(dev_img.data_ptr(), image.nbytes, plan.ops.data_ptr(), plan.n_ops,
-                                 plan.page_off.data_ptr(), plan.n_pages, direction, plan.page_hpa.data_ptr(),
+                                 plan.page_off.data_ptr(), plan.n_pages, direction | hint, plan.page_hpa.data_ptr(),
                                  plan.page_status.data_ptr(), plan.page_aux.data_ptr(), plan.first_bad.data_ptr(),
                                  buf.data_ptr(), buf.numel(), plan.results.data_ptr(), dirty, abort, s),
                 "pv_copy_exec")
