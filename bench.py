@@ -683,7 +683,7 @@ def run_reference(args, rank, world):
     threads = cpu_threads()
     proc_vas, proc_ops = _oracle_inputs(wl)
     for _ in range(max(args.warmup, 0)):
-        cpu_sample(wl.memv, proc_vas, proc_ops, min(args.cpu_sample_vas, 1 << 20), 64 << 20, threads)
+        cpu_sample(wl.memv, proc_vas, proc_ops, args.cpu_sample_vas // 4, args.cpu_sample_bytes // 4, threads)
     vals, gbs = [], []
     for _ in range(args.steps):
         tps, g, sample = cpu_sample(wl.memv, proc_vas, proc_ops, args.cpu_sample_vas // 4, args.cpu_sample_bytes // 4,
