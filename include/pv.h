@@ -82,6 +82,14 @@ extern "C" {
  */
 #define PV_ONE_STAGE 1u
 #define PV_TWO_STAGE 2u
+/* Extension (BASELINE config 3; no reference semantics, parity pinned only
+ * by the oracle restatement): a single-stage 4-level table over 48-bit VAs
+ * (9/9/9/9/12; VA bits >= 48 ignored) whose level-3 entries may map 2 MiB
+ * pages (PV_FLAG_PS).  Same entry codec otherwise (T before P, W ignored);
+ * a 2 MiB leaf translates to (pfn << 12) + (va & 0x1FFFFF).  Fault / trap
+ * levels run 1..4. */
+#define PV_ONE_STAGE_4L 3u
+#define PV_FLAG_PS 0x80u
 
 typedef struct pv_space {
   uint64_t s1_base;     /* byte base of the stage-1 memory window          */
@@ -133,6 +141,8 @@ int pv_index_encode(const uint8_t* image, uint64_t image_bytes,
 #define PV_VA32 0x1u    /* vas is uint32_t[] (else uint64_t[])             */
 #define PV_OUT_PFN 0x2u /* value = leaf pfn (walk); else address with the
                            page offset of the va (translate / resolve)     */
+#define PV_HAS_4L 0x40000000u        /* some space of the batch is
+                           PV_ONE_STAGE_4L (selects the generic kernel)    */
 #define PV_HAS_TWO_STAGE 0x80000000u /* some space of the batch is
                            PV_TWO_STAGE (selects the two-stage kernel)     */
 

@@ -30,7 +30,7 @@ def build() -> str:
 def lib():
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB):
+        if not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(os.path.join(HERE, "pvoracle.c")):
             build()
         l = ctypes.CDLL(LIB)
         l.orc_walk.restype = ctypes.c_uint32

@@ -83,13 +83,49 @@ uint32_t orc_walk(const uint8_t* img, uint64_t img_bytes, uint64_t base, uint64_
   return ST_OK;
 }
 
+/* Extension geometry (mode 3, BASELINE config 3; NOT a reference semantic,
+ * so this restatement is the only anchor -- "parity unpinned"): 4 levels of
+ * 512 entries over 48-bit VAs, the reference's entry codec (T before P, W
+ * ignored), and a 2 MiB leaf at level 3 when bit 0x80 (PS) is set.  Returns
+ * the 4 KiB frame of va. */
+uint32_t orc_walk4(const uint8_t* img, uint64_t img_bytes, uint64_t base, uint64_t root, uint64_t va,
+                   uint64_t* out) {
+  uint64_t node = root;
+  for (uint32_t level = 1; level <= 4; ++level) {
+    const uint32_t index = (uint32_t)((va >> (12 + 9 * (4 - level))) & 0x1FFu);
+    if (base >= img_bytes || node >= (img_bytes - base) / PG) return ST_NODE_OOR | level;
+    const uint64_t w = rd64(img, base + node * PG + (uint64_t)index * 8u);
+    if (w & 0x4u) {
+      *out = node;
+      return ST_TRAP | level | (index << 16);
+    }
+    if (!(w & 0x1u)) return ST_FAULT | level;
+    if (level == 3 && (w & 0x80u)) {
+      *out = (w >> 12) + ((va >> 12) & 0x1FFu);
+      return ST_OK;
+    }
+    node = w >> 12;
+  }
+  *out = node;
+  return ST_OK;
+}
+
 /* One uncached translation; value/aux follow the pv.h conventions.
  * want_pfn: return the leaf pfn (walk) instead of the address. */
 uint32_t orc_translate1(const uint8_t* img, uint64_t img_bytes, const orc_space* sp, uint64_t va, int want_pfn,
                         uint64_t* value, uint64_t* aux) {
   uint64_t r = 0;
-  uint32_t st = orc_walk(img, img_bytes, sp->s1_base, sp->s1_root, va, 0, &r);
   *aux = 0;
+  if (sp->mode == 3) {
+    const uint32_t st4 = orc_walk4(img, img_bytes, sp->s1_base, sp->s1_root, va, &r);
+    if (st4 != ST_OK) {
+      *value = ((st4 & 0xFF0u) == ST_TRAP) ? r : va;
+      return st4;
+    }
+    *value = want_pfn ? r : ((r << 12) | (va & 0xFFFu));
+    return ST_OK;
+  }
+  uint32_t st = orc_walk(img, img_bytes, sp->s1_base, sp->s1_root, va, 0, &r);
   if (st != ST_OK) {
     *value = ((st & 0xFF0u) == ST_TRAP) ? r : va;
     return st;

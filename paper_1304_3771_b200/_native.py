@@ -36,10 +36,13 @@ ST_CONFLICT = 0x400
 
 ONE_STAGE = 1
 TWO_STAGE = 2
+ONE_STAGE_4L = 3  # extension geometry (BASELINE config 3)
+FLAG_PS = 0x80
 
 VA32 = 0x1
 OUT_PFN = 0x2
 HAS_TWO_STAGE = 0x80000000
+HAS_4L = 0x40000000
 
 TO_GUEST = 0
 FROM_GUEST = 1

@@ -112,10 +112,11 @@ int pv_translate(const uint8_t* image, uint64_t image_bytes, const pv_space* spa
   if (n_chunks == 0) return PV_SUCCESS;
   if (!image || !spaces || !segs || !vas || !out_value || !out_status || n_segs == 0) return PV_EINVAL;
   if (image_bytes % kPageSize) return PV_EINVAL;
-  if (flags & ~(uint32_t)(PV_VA32 | PV_OUT_PFN | PV_HAS_TWO_STAGE)) return PV_EINVAL;
+  if (flags & ~(uint32_t)(PV_VA32 | PV_OUT_PFN | PV_HAS_TWO_STAGE | PV_HAS_4L)) return PV_EINVAL;
   const bool two = flags & PV_HAS_TWO_STAGE;
   if (index != nullptr && (!index->slot_of || !index->leaf_codes || !index->slot_page)) return PV_EINVAL;
-  return rc(launch_translate(image, image_bytes, spaces, segs, n_segs, n_chunks, vas, flags & 0x3u, two, index,
+  return rc(launch_translate(image, image_bytes, spaces, segs, n_segs, n_chunks, vas,
+                             flags & (PV_VA32 | PV_OUT_PFN | PV_HAS_4L), two, index,
                              out_value, out_status, out_aux, (cudaStream_t)stream));
 }
 

@@ -92,6 +92,34 @@ __device__ __forceinline__ uint32_t walk_global(const uint8_t* __restrict__ imag
   return PV_ST_OK;
 }
 
+// Extension geometry PV_ONE_STAGE_4L: 4 levels of 512 entries over 48-bit
+// VAs, 2 MiB leaves at level 3 (PV_FLAG_PS).  Returns the 4 KiB frame of
+// va (for a 2 MiB leaf: its pfn + va's 4 KiB index inside it).
+__device__ __forceinline__ uint32_t walk4_global(const uint8_t* __restrict__ image, uint64_t image_bytes,
+                                                 uint64_t base, uint64_t root, uint64_t va, uint64_t* out) {
+  const uint64_t lim = node_limit(image_bytes, base);
+  const uint32_t idx[4] = {(uint32_t)(va >> 39) & 511u, (uint32_t)(va >> 30) & 511u, (uint32_t)(va >> 21) & 511u,
+                           (uint32_t)(va >> 12) & 511u};
+  uint64_t node = root;
+#pragma unroll
+  for (uint32_t l = 0; l < 4; ++l) {
+    if (node >= lim) return PV_ST_NODE_OOR | (l + 1);
+    const uint64_t w = ld_word(image, base, node, idx[l]);
+    if (w & kFlagTrapping) {
+      *out = node;
+      return PV_ST_TRAP | (l + 1) | (idx[l] << 16);
+    }
+    if (!(w & kFlagPresent)) return PV_ST_FAULT | (l + 1);
+    if (l == 2 && (w & PV_FLAG_PS)) {
+      *out = (w >> kPageShift) + idx[3];
+      return PV_ST_OK;
+    }
+    node = w >> kPageShift;
+  }
+  *out = node;
+  return PV_ST_OK;
+}
+
 // Translate `va` through a space with global-memory walks.  On success
 // *value = leaf pfn of the final stage.  On failure *value / *aux follow the
 // pv.h status conventions (va or gpa for faults, node pfn for traps).
@@ -99,6 +127,11 @@ __device__ __forceinline__ uint32_t translate_global(const uint8_t* __restrict__
                                                      const pv_space& sp, uint64_t va, uint64_t* value,
                                                      uint64_t* aux) {
   uint64_t r = 0;
+  if (sp.mode == PV_ONE_STAGE_4L) {
+    const uint32_t st4 = walk4_global(image, image_bytes, sp.s1_base, sp.s1_root_pfn, va, &r);
+    *value = (st4 == PV_ST_OK || PV_ST_KIND(st4) == PV_ST_TRAP) ? r : va;
+    return st4;
+  }
   uint32_t st = walk_global(image, image_bytes, sp.s1_base, sp.s1_root_pfn, va, 0, &r);
   if (st != PV_ST_OK) {
     *value = (PV_ST_KIND(st) == PV_ST_TRAP) ? r : va;

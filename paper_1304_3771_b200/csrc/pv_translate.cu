@@ -293,6 +293,52 @@ translate_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const 
   }
 }
 
+// Generic form for batches that contain extension-geometry spaces
+// (PV_ONE_STAGE_4L): every lane walks through L1/L2-cached global loads
+// (translate_global), 8 lanes per thread.
+template <bool kVa32, bool kPfn>
+__global__ void __launch_bounds__(kTpb)
+translate_generic_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes,
+                         const pv_space* __restrict__ spaces, const pv_seg* __restrict__ segs, uint32_t n_segs,
+                         uint64_t n_chunks, const void* __restrict__ vas, uint64_t* __restrict__ out_value,
+                         uint32_t* __restrict__ out_status, uint64_t* __restrict__ out_aux) {
+  for (uint64_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+    uint32_t lo = 0, hi = n_segs;
+    while (hi - lo > 1) {
+      const uint32_t m = (lo + hi) >> 1;
+      if (segs[m].chunk0 <= c) lo = m; else hi = m;
+    }
+    const pv_seg seg = segs[lo];
+    const pv_space sp = spaces[seg.space];
+    const uint64_t lane0 = seg.begin + (c - seg.chunk0) * kChunk;
+#pragma unroll
+    for (int j = 0; j < kVpt; ++j) {
+      const uint64_t i = lane0 + (uint64_t)j * kTpb + threadIdx.x;
+      if (i >= seg.end) continue;
+      const uint64_t va = kVa32 ? (uint64_t)((const uint32_t*)vas)[i] : ((const uint64_t*)vas)[i];
+      uint64_t v = 0, a = 0;
+      const uint32_t st = translate_global(image, image_bytes, sp, va, &v, &a);
+      if (!kPfn && st == PV_ST_OK) v = (v << kPageShift) | (va & kPageMask);
+      out_value[i] = v;
+      out_status[i] = st;
+      if (out_aux != nullptr && PV_ST_KIND(st) == PV_ST_TRAP2) out_aux[i] = a;
+    }
+  }
+}
+
+template <bool kVa32, bool kPfn>
+static cudaError_t launch_generic(const uint8_t* image, uint64_t image_bytes, const pv_space* spaces,
+                                  const pv_seg* segs, uint32_t n_segs, uint64_t n_chunks, const void* vas,
+                                  uint64_t* out_value, uint32_t* out_status, uint64_t* out_aux, cudaStream_t stream) {
+  auto k = translate_generic_kernel<kVa32, kPfn>;
+  uint64_t grid = resident_grid((const void*)k, kTpb, 0);
+  if (grid > n_chunks) grid = n_chunks;
+  if (grid == 0) return cudaSuccess;
+  k<<<(unsigned)grid, kTpb, 0, stream>>>(image, image_bytes, spaces, segs, n_segs, n_chunks, vas, out_value,
+                                         out_status, out_aux);
+  return cudaGetLastError();
+}
+
 template <bool kTwo, bool kVa32, bool kPfn>
 static cudaError_t launch_t(const uint8_t* image, uint64_t image_bytes, const pv_space* spaces, const pv_seg* segs,
                             uint32_t n_segs, uint64_t n_chunks, const void* vas, const pv_index* idx,
@@ -313,8 +359,18 @@ cudaError_t launch_translate(const uint8_t* image, uint64_t image_bytes, const p
                              uint32_t n_segs, uint64_t n_chunks, const void* vas, uint32_t flags, bool two_stage,
                              const pv_index* idx, uint64_t* out_value, uint32_t* out_status, uint64_t* out_aux,
                              cudaStream_t stream) {
-  if (image_bytes >= (1ull << 40)) return cudaErrorInvalidValue;  // leaf pfns / slots must fit 28-bit codes
   const bool va32 = flags & PV_VA32, pfn = flags & PV_OUT_PFN;
+  if (flags & PV_HAS_4L) {
+    if (va32) return pfn ? launch_generic<true, true>(image, image_bytes, spaces, segs, n_segs, n_chunks, vas,
+                                                      out_value, out_status, out_aux, stream)
+                         : launch_generic<true, false>(image, image_bytes, spaces, segs, n_segs, n_chunks, vas,
+                                                       out_value, out_status, out_aux, stream);
+    return pfn ? launch_generic<false, true>(image, image_bytes, spaces, segs, n_segs, n_chunks, vas, out_value,
+                                             out_status, out_aux, stream)
+               : launch_generic<false, false>(image, image_bytes, spaces, segs, n_segs, n_chunks, vas, out_value,
+                                              out_status, out_aux, stream);
+  }
+  if (image_bytes >= (1ull << 40)) return cudaErrorInvalidValue;  // leaf pfns / slots must fit 28-bit codes
 #define PV_DISPATCH(T, V, P)                                                                                    \
   if (two_stage == T && va32 == V && pfn == P)                                                                  \
     return launch_t<T, V, P>(image, image_bytes, spaces, segs, n_segs, n_chunks, vas, idx, out_value, \

@@ -136,7 +136,8 @@ def translate_one(image, space: Space, va: int, *, out_pfn: bool = False) -> tup
     s = _stream()
     one.dev.copy_(one.host, non_blocking=True)
     base = one.dev.data_ptr()
-    flags = (N.OUT_PFN if out_pfn else 0) | (N.HAS_TWO_STAGE if space.mode == N.TWO_STAGE else 0)
+    flags = (N.OUT_PFN if out_pfn else 0) | (N.HAS_TWO_STAGE if space.mode == N.TWO_STAGE else 0) | \
+        (N.HAS_4L if space.mode == N.ONE_STAGE_4L else 0)
     N.check(lib.pv_translate(dev_img.data_ptr(), image.nbytes, base, base + 32, 1, 1, base + 64, flags, None,
                              base + 72, base + 88, base + 80, s.cuda_stream), "pv_translate")
     one.out.copy_(one.dev[9:13], non_blocking=True)
@@ -316,7 +317,8 @@ class TranslatePlan:
         self.n_segs = len(segs)
         self.n_chunks = n_chunks
         self.two = any(sp.mode == N.TWO_STAGE for sp in spaces)
-        self.use_index = use_index and os.environ.get("PV_LEAF_INDEX", "1") != "0"
+        self.four = any(sp.mode == N.ONE_STAGE_4L for sp in spaces)
+        self.use_index = use_index and not self.four and os.environ.get("PV_LEAF_INDEX", "1") != "0"
         self._indexed = False
         if image is not None and self.use_index:
             leaf_index(image).ensure(self.host_spaces)
@@ -344,6 +346,8 @@ def translate_lanes(image, plan: TranslatePlan, vas, *, out_pfn: bool = False, o
     flags = (N.VA32 if vas.dtype == torch.int32 else 0) | (N.OUT_PFN if out_pfn else 0)
     if plan.two:
         flags |= N.HAS_TWO_STAGE
+    if plan.four:
+        flags |= N.HAS_4L
     idx = None
     if plan.use_index:
         li = leaf_index(image)

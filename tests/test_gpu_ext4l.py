@@ -1,0 +1,82 @@
+"""GPU: extension geometry (BASELINE config 3, 16 GiB mixed 4 KiB / 2 MiB
+mmap, 4-level tables) -- device walker and copier vs the C restatement
+(parity unpinned by the reference, see tests/test_ext4l.py)."""
+
+from __future__ import annotations
+
+import random
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import status_outcome
+from oracle import oracle as O
+from paper_1304_3771_b200 import _native as N
+from paper_1304_3771_b200 import dataplane as dp
+from paper_1304_3771_b200 import errors as er
+from paper_1304_3771_b200 import ext4l as X
+
+pytestmark = pytest.mark.gpu
+
+
+def _check(mem, t, vas, *, out_pfn=False):
+    raw = mem.backing.host_for_read()
+    sp = t.space
+    plan = dp.TranslatePlan([sp], [(0, len(vas), 0)])
+    v, s, a = dp.translate_lanes(mem.backing, plan, torch.tensor(vas.view(np.int64), device="cuda"),
+                                 out_pfn=out_pfn)
+    ov, os_, oa = O.translate(raw, O.space(sp.s1_base, sp.s1_root_pfn, 0, N.ONE_STAGE_4L), vas, want_pfn=out_pfn,
+                              threads=0)
+    assert np.array_equal(s.cpu().numpy().view(np.uint32), os_)
+    assert np.array_equal(v.cpu().numpy().view(np.uint64), ov)
+    return os_
+
+
+def test_c3_16gib_sequential_and_strided(cuda):
+    mem, t = X.build_c3()
+    seq = X.c3_sequential()
+    st = _check(mem, t, seq)
+    assert (st == 0).all() and len(seq) == 4_194_304
+    st = _check(mem, t, X.c3_strided(), out_pfn=True)
+    assert (st == 0).all()
+
+
+def test_4l_faults_traps_and_aliasing(cuda):
+    region = 256 << 20
+    mem, t = X.build_c3(region)
+    rng = random.Random(44)
+    # corrupt entries at every level
+    t.set_entry(X.C3_VA + 3 * X.LARGE, 3, 0)                               # PD entry not present
+    t.set_entry(X.C3_VA + 5 * X.LARGE + 7 * 4096, 4, (1234 << 12) | 0x4)   # PT entry trapping
+    t.set_entry(X.C3_VA + 9 * X.LARGE + 9 * 4096, 4, 0)                    # PT hole
+    t.set_entry(X.C3_VA + 12 * X.LARGE, 3, (0xFFFFFF << 12) | 0x1)          # PT node past the image
+    t.set_entry(X.C3_VA + (1 << 30) + 5, 2, 0x4)                          # PDPT entry trapping
+    t.map_2m(X.C3_VA + region + (4 << 20), 0x200)                           # a lone 2 MiB page
+    vas = [X.C3_VA + rng.randrange(region + (8 << 20)) for _ in range(200_000)]
+    vas += [X.C3_VA + (1 << 30) + rng.randrange(1 << 20) for _ in range(100)]
+    vas += [(rng.randrange(1, 1 << 16) << 48) | (X.C3_VA + rng.randrange(region)) for _ in range(1000)]  # alias
+    vas += [rng.randrange(1 << 48) for _ in range(1000)]
+    st = _check(mem, t, np.array(vas, dtype=np.uint64))
+    kinds = {int(x) & 0xFF0 for x in st}
+    assert {0x000, 0x010, 0x040, 0x080} <= kinds
+    levels = {int(x) & 0xF for x in st if int(x) & 0xFF0 == 0x010}
+    assert {1, 3, 4} <= levels
+
+
+def test_4l_copy_roundtrip_across_page_sizes(cuda):
+    region = 64 << 20
+    mem, t = X.build_c3(region)
+    raw = mem.backing.host_for_read().copy()
+    gva = X.C3_VA + X.LARGE - 1000          # spans a 2 MiB leaf into a 4 KiB region
+    n = 3 * X.LARGE + 777
+    data = np.frombuffer(random.Random(1).randbytes(n), dtype=np.uint8)
+    ops = np.array([[gva, n, 0, 0]], np.uint64)
+    out = dp.copy_ops(mem.backing, [t.space], ops, N.TO_GUEST, torch.from_numpy(data.copy()).cuda())[0]
+    assert out.status == 0 and out.copied == n
+    sp = t.space
+    O.copy(raw, O.space(sp.s1_base, sp.s1_root_pfn, 0, N.ONE_STAGE_4L).reshape(1, 4), ops, data.copy(), 0)
+    assert np.array_equal(mem.backing.host_for_read(), raw)
+    assert X.walk4(mem, t.root, gva) == X.walk4(mem, t.root, gva - 5)
+    with pytest.raises(er.PageFault):
+        X.walk4(mem, t.root, X.C3_VA + region + 4096)
