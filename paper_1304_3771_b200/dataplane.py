@@ -197,6 +197,7 @@ class LeafIndex:
         self.slot_page = torch.zeros(1, dtype=torch.int64, device="cuda")
         self.codes = torch.zeros(512, dtype=torch.int32, device="cuda")
         self.seen_dev_epoch = image.dev_write_epoch
+        self._scanned: dict = {}  # space -> image.host_epoch of its last scan
         self._abi = PvIndex()
 
     @property
@@ -244,10 +245,20 @@ class LeafIndex:
         return np.unique(np.concatenate(out)) if out else np.zeros(0, dtype=np.int64)
 
     def ensure(self, spaces: list["Space"]) -> None:
+        """Index the leaf nodes ``spaces`` reach.  A space is rescanned only
+        after host writes changed the image (tables are edited host-side;
+        a structural change the scan misses only costs speed: unindexed leaf
+        nodes are walked raw)."""
         import torch
 
         dev = self.image.device()
-        pages = self.leaf_pages(spaces)
+        epoch = self.image.host_epoch
+        todo = [sp for sp in spaces if self._scanned.get(sp) != epoch]
+        if not todo:
+            return
+        for sp in todo:
+            self._scanned[sp] = epoch
+        pages = self.leaf_pages(todo)
         new = pages[self.slot_of_host[pages] == NO_SLOT]
         if len(new) == 0:
             return
@@ -364,32 +375,51 @@ def translate_lanes(image, plan: TranslatePlan, vas, *, out_pfn: bool = False, o
 
 def translate_host_pipelined(image, space: Space, host_vas, chunk: int = 1 << 22):
     """Translate a (pinned) host tensor of VAs; results come back as pinned
-    host tensors.  Chunks overlap: H2D of chunk i+1 and D2H of chunk i-1 run
-    on side streams while chunk i translates.  ``aux`` only travels for
+    host tensors (see :func:`translate_host_many`)."""
+    return translate_host_many(image, [(space, host_vas)], chunk=chunk)[0]
+
+
+def translate_host_many(image, jobs, chunk: int = 1 << 22):
+    """Translate several host VA tensors (``jobs = [(space, vas), ...]``) in
+    one pipeline: chunks of every job stream through two device buffer sets,
+    H2D of chunk i+1 and D2H of chunk i-1 run on side streams while chunk i
+    translates, one synchronisation at the end.  Returns per job pinned
+    ``(value int64, status int32, aux int64)``; ``aux`` only travels for
     two-stage spaces (one-stage walks never produce a TDP-stage trap)."""
     import torch
 
-    n = host_vas.numel()
-    dtype = host_vas.dtype if host_vas.dtype in (torch.int32, torch.int64) else torch.int64
-    src = host_vas if host_vas.dtype == dtype else host_vas.to(dtype)
-    if not src.is_pinned():
-        src = src.pin_memory()
-    value = torch.empty(n, dtype=torch.int64, pin_memory=True)
-    status = torch.empty(n, dtype=torch.int32, pin_memory=True)
-    two = space.mode == N.TWO_STAGE
-    aux = torch.empty(n, dtype=torch.int64, pin_memory=True) if two else torch.zeros(n, dtype=torch.int64)
-    if n == 0:
-        return value, status, aux
+    outs, work = [], []
+    dtype = torch.int32
+    srcs = []
+    for space, host_vas in jobs:
+        if host_vas.dtype not in (torch.int32, torch.int64):
+            host_vas = host_vas.to(torch.int64)
+        if host_vas.dtype == torch.int64:
+            dtype = torch.int64
+        srcs.append((space, host_vas))
+    for space, host_vas in srcs:
+        src = host_vas if host_vas.dtype == dtype else host_vas.to(dtype)
+        if not src.is_pinned():
+            src = src.pin_memory()
+        n = src.numel()
+        two = space.mode == N.TWO_STAGE
+        value = torch.empty(n, dtype=torch.int64, pin_memory=True)
+        status = torch.empty(n, dtype=torch.int32, pin_memory=True)
+        aux = torch.empty(n, dtype=torch.int64, pin_memory=True) if two else torch.zeros(n, dtype=torch.int64)
+        outs.append((value, status, aux))
+        for start in range(0, n, chunk):
+            work.append((space, two, src, value, status, aux, start, min(chunk, n - start)))
+    if not work:
+        return outs
     compute = torch.cuda.current_stream()
     h2d, d2h = torch.cuda.Stream(), torch.cuda.Stream()
     plans = {}
     bufs = []
-    for b in range(2):
+    for _ in range(2):
         bufs.append((torch.empty(chunk, dtype=dtype, device="cuda"), torch.empty(chunk, dtype=torch.int64, device="cuda"),
                      torch.empty(chunk, dtype=torch.int32, device="cuda"), torch.zeros(chunk, dtype=torch.int64, device="cuda"),
                      torch.cuda.Event(), torch.cuda.Event(), torch.cuda.Event()))
-    for i, start in enumerate(range(0, n, chunk)):
-        m = min(chunk, n - start)
+    for i, (space, two, src, value, status, aux, start, m) in enumerate(work):
         d_vas, d_val, d_st, d_aux, ev_in, ev_done, ev_out = bufs[i % 2]
         if i >= 2:
             h2d.wait_event(ev_out)  # buffers of chunk i-2 fully drained
@@ -397,11 +427,11 @@ def translate_host_pipelined(image, space: Space, host_vas, chunk: int = 1 << 22
             d_vas[:m].copy_(src[start:start + m], non_blocking=True)
             ev_in.record(h2d)
         compute.wait_event(ev_in)
-        if m not in plans:
-            plans[m] = TranslatePlan([space], [(0, m, 0)], image=image)
+        if (space, m) not in plans:
+            plans[(space, m)] = TranslatePlan([space], [(0, m, 0)], image=image)
         if two:
             d_aux[:m].zero_()
-        translate_lanes(image, plans[m], d_vas[:m], out=(d_val[:m], d_st[:m], d_aux[:m]))
+        translate_lanes(image, plans[(space, m)], d_vas[:m], out=(d_val[:m], d_st[:m], d_aux[:m]))
         ev_done.record(compute)
         d2h.wait_event(ev_done)
         with torch.cuda.stream(d2h):
@@ -412,7 +442,7 @@ def translate_host_pipelined(image, space: Space, host_vas, chunk: int = 1 << 22
             ev_out.record(d2h)
     d2h.synchronize()
     compute.synchronize()
-    return value, status, aux
+    return outs
 
 
 # ---- K4: FIFO cache state packing -------------------------------------------

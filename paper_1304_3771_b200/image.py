@@ -68,6 +68,7 @@ class MemoryImage:
         self._dev_dirty = None    # torch.uint8 [npages]
         self._dev_dirty_any = False
         self.dev_write_epoch = 0  # bumped by every device write (leaf-index coherence)
+        self.host_epoch = 0       # bumped by every push of host writes into HBM
         self.leaf_index = None    # dataplane.LeafIndex, created on first indexed translate
         self._lock = threading.RLock()
 
@@ -167,6 +168,7 @@ class MemoryImage:
                 stream.synchronize()  # staging buffers are freed at scope exit
             self._host_dirty[:] = False
             self._host_dirty_any = False
+            self.host_epoch += 1
 
     def pull(self) -> None:
         """Gather device-written pages back into the host mirror."""

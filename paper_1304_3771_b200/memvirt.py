@@ -881,6 +881,29 @@ def translate_batch(translator: ProcessTranslator, gvas, *, use_cache: bool | No
             aux.cpu().numpy().view(np.uint64))
 
 
+def translate_many(pairs, *, chunk: int = 1 << 22):
+    """``translate_batch`` for several uncached translators at once, host
+    tensors in and out: ``pairs = [(translator, host_vas), ...]`` -> one
+    pipelined H2D / translate / D2H stream over every pair (they must share
+    one physical memory).  Returns ``[(hpa, status, aux), ...]`` as pinned
+    host tensors."""
+    import torch
+
+    if not pairs:
+        return []
+    image = pairs[0][0].image
+    jobs = []
+    for tr, vas in pairs:
+        if tr.use_cache:
+            raise ValueError("translate_many runs uncached translators (the FIFO cache needs translate_batch)")
+        if tr.image is not image:
+            raise ValueError("translate_many needs translators of one physical memory")
+        if not isinstance(vas, torch.Tensor):
+            vas = torch.from_numpy(np.ascontiguousarray(np.asarray(vas, dtype=np.uint64)).view(np.int64))
+        jobs.append((tr.device_space, vas))
+    return dp.translate_host_many(image, jobs, chunk=chunk)
+
+
 def lane_error(status: int, value: int, aux: int, va: int, image_bytes: int) -> Exception | None:
     """The exception a translate_batch lane stands for (None if OK)."""
     try:
