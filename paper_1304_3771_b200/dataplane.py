@@ -405,7 +405,9 @@ def translate_host_many(image, jobs, chunk: int = 1 << 22):
         two = space.mode == N.TWO_STAGE
         value = torch.empty(n, dtype=torch.int64, pin_memory=True)
         status = torch.empty(n, dtype=torch.int32, pin_memory=True)
-        aux = torch.empty(n, dtype=torch.int64, pin_memory=True) if two else torch.zeros(n, dtype=torch.int64)
+        # one-stage walks never produce a TDP-stage trap: aux is identically 0
+        aux = torch.empty(n, dtype=torch.int64, pin_memory=True) if two else \
+            torch.zeros(1, dtype=torch.int64).expand(n)
         outs.append((value, status, aux))
         for start in range(0, n, chunk):
             work.append((space, two, src, value, status, aux, start, min(chunk, n - start)))
