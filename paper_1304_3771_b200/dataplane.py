@@ -373,13 +373,13 @@ def translate_lanes(image, plan: TranslatePlan, vas, *, out_pfn: bool = False, o
     return value, status, aux
 
 
-def translate_host_pipelined(image, space: Space, host_vas, chunk: int = 1 << 22):
+def translate_host_pipelined(image, space: Space, host_vas, chunk: int = 1 << 23):
     """Translate a (pinned) host tensor of VAs; results come back as pinned
     host tensors (see :func:`translate_host_many`)."""
     return translate_host_many(image, [(space, host_vas)], chunk=chunk)[0]
 
 
-def translate_host_many(image, jobs, chunk: int = 1 << 22):
+def translate_host_many(image, jobs, chunk: int = 1 << 23):
     """Translate several host VA tensors (``jobs = [(space, vas), ...]``) in
     one pipeline: chunks of every job stream through two device buffer sets,
     H2D of chunk i+1 and D2H of chunk i-1 run on side streams while chunk i

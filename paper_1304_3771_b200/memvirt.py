@@ -881,7 +881,7 @@ def translate_batch(translator: ProcessTranslator, gvas, *, use_cache: bool | No
             aux.cpu().numpy().view(np.uint64))
 
 
-def translate_many(pairs, *, chunk: int = 1 << 22):
+def translate_many(pairs, *, chunk: int = 1 << 23):
     """``translate_batch`` for several uncached translators at once, host
     tensors in and out: ``pairs = [(translator, host_vas), ...]`` -> one
     pipelined H2D / translate / D2H stream over every pair (they must share
