@@ -216,7 +216,8 @@ def run_ours(args, rank, world, local):
     stream = torch.cuda.current_stream()
     s = stream.cuda_stream
     owner, _ = dp._owner_map(img)
-    hint = N.COPY_ALIGNED16 if plan.aligned16(wl.src.data_ptr()) else 0
+    hint = N.COPY_ALIGNED16 if (os.environ.get("PV_EXEC_ALIGNED") == "1" and plan.aligned16(wl.src.data_ptr())) \
+        else 0
 
     def step(ev):
         ev[0].record(stream)

@@ -654,7 +654,10 @@ def copy_launch(image, plan: CopyPlan, direction: int, buf, *, fifo_dev=None, fi
                                       plan.conflict.data_ptr(), s), "pv_copy_stamp")
             abort = plan.conflict.data_ptr()
         dirty = image.dirty_map().data_ptr() if (direction == N.TO_GUEST and track_dirty) else None
-        hint = N.COPY_ALIGNED16 if plan.aligned16(buf.data_ptr()) else 0
+        # the 16-byte-only exec variant measured ~1 % slower than the generic
+        # one on B200 (scripts/exp_exec.py); opt in with PV_EXEC_ALIGNED=1
+        hint = N.COPY_ALIGNED16 if (os.environ.get("PV_EXEC_ALIGNED") == "1" and plan.aligned16(buf.data_ptr())) \
+            else 0
         N.check(lib.pv_copy_exec(dev_img.data_ptr(), image.nbytes, plan.ops.data_ptr(), plan.n_ops,
                                  plan.page_off.data_ptr(), plan.n_pages, direction | hint, plan.page_hpa.data_ptr(),
                                  plan.page_status.data_ptr(), plan.page_aux.data_ptr(), plan.first_bad.data_ptr(),
