@@ -23,6 +23,7 @@
 // (8 independent leaf loads in flight) and prefetches the next chunk's VAs
 // before gathering the current chunk's leaves; VAs stream in with
 // L1::no_allocate loads and results stream out with evict-first stores.
+#include <cstdlib>
 #include <type_traits>
 
 #include "pv_common.cuh"
@@ -91,7 +92,7 @@ __device__ void stage_codes(const uint8_t* __restrict__ image, uint64_t image_by
     }
   }
   __syncthreads();
-  for (uint32_t i = tid; i < 4 * 512; i += kTpb) {
+  for (uint32_t i = tid; i < 4 * 512; i += blockDim.x) {
     const uint32_t t = i >> 9;
     uint32_t code = kCodeStop;
     if (s.top_status[t] == PV_ST_OK) {
@@ -174,13 +175,14 @@ __device__ __forceinline__ uint64_t leaf_word(const uint8_t* image, const Stage&
   return raw_leaf(image, s, code >> 4, x, pol);
 }
 
-template <bool kTwo, bool kVa32, bool kPfn>
-__global__ void __launch_bounds__(kTpb, kTwo ? 3 : 4)
+template <bool kTwo, bool kVa32, bool kPfn, int TPB = kTpb, int MINB = (kTwo ? 3 : 4)>
+__global__ void __launch_bounds__(TPB, MINB)
 translate_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const pv_space* __restrict__ spaces,
                  const pv_seg* __restrict__ segs, uint32_t n_segs, uint64_t n_chunks, const void* __restrict__ vas,
                  const uint32_t* __restrict__ slot_of, const uint32_t* __restrict__ leaf_codes,
                  const uint64_t* __restrict__ slot_page,
                  uint64_t* __restrict__ out_value, uint32_t* __restrict__ out_status, uint64_t* __restrict__ out_aux) {
+  constexpr int VPT = (int)(kChunk / TPB);
   __shared__ __align__(16) uint32_t codes1[4 * 512];
   __shared__ __align__(16) uint32_t codes2[kTwo ? 4 * 512 : 1];
   __shared__ Stage st1, st2;
@@ -209,16 +211,16 @@ translate_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const 
     }
   };
   using VaT = typename std::conditional<kVa32, uint32_t, uint64_t>::type;
-  auto load_vas = [&](uint64_t c, VaT (&va)[kVpt]) {
+  auto load_vas = [&](uint64_t c, VaT (&va)[VPT]) {
     const uint64_t lane0 = seg.begin + (c - seg.chunk0) * kChunk;
 #pragma unroll
-    for (int j = 0; j < kVpt; ++j) {
-      const uint64_t i = lane0 + (uint64_t)j * kTpb + threadIdx.x;
+    for (int j = 0; j < VPT; ++j) {
+      const uint64_t i = lane0 + (uint64_t)j * TPB + threadIdx.x;
       va[j] = i < seg.end ? (VaT)ld_stream_va(vas, i, kVa32, pol_stream) : 0;
     }
   };
 
-  VaT va[kVpt], nva[kVpt];
+  VaT va[VPT], nva[VPT];
   bool have_next = false;
   for (uint64_t c = c_begin; c < c_end; ++c) {
     find_seg(c);
@@ -232,7 +234,7 @@ translate_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const 
     }
     if (have_next) {
 #pragma unroll
-      for (int j = 0; j < kVpt; ++j) va[j] = nva[j];
+      for (int j = 0; j < VPT; ++j) va[j] = nva[j];
     } else {
       load_vas(c, va);
     }
@@ -242,31 +244,31 @@ translate_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const 
     have_next = c + 1 < c_end && c + 1 < seg.chunk0 + seg_chunks;
     if (have_next) load_vas(c + 1, nva);
 
-    uint32_t st[kVpt], code[kVpt];
-    uint64_t w[kVpt];
+    uint32_t st[VPT], code[VPT];
+    uint64_t w[VPT];
 #pragma unroll
-    for (int j = 0; j < kVpt; ++j) st[j] = upper<false>(st1, codes1, va[j], &code[j]);
+    for (int j = 0; j < VPT; ++j) st[j] = upper<false>(st1, codes1, va[j], &code[j]);
 #pragma unroll
-    for (int j = 0; j < kVpt; ++j) w[j] = st[j] == PV_ST_OK ? leaf_word(image, st1, code[j], va[j], leaf_codes, slot_page, pol_table) : 0;
-    uint64_t val[kVpt], aux[kVpt];
+    for (int j = 0; j < VPT; ++j) w[j] = st[j] == PV_ST_OK ? leaf_word(image, st1, code[j], va[j], leaf_codes, slot_page, pol_table) : 0;
+    uint64_t val[VPT], aux[VPT];
 #pragma unroll
-    for (int j = 0; j < kVpt; ++j) {
+    for (int j = 0; j < VPT; ++j) {
       st[j] = leaf_status<false>(w[j], st[j], va[j]);
       const uint32_t k = PV_ST_KIND(st[j]);
       val[j] = k == PV_ST_OK ? (w[j] >> kPageShift) : k == PV_ST_TRAP ? trap_node(st1, st[j], code[j], va[j], slot_page) : va[j];
       aux[j] = 0;
     }
     if (kTwo && two) {
-      uint64_t gpa[kVpt];
+      uint64_t gpa[VPT];
 #pragma unroll
-      for (int j = 0; j < kVpt; ++j) {
+      for (int j = 0; j < VPT; ++j) {
         gpa[j] = (val[j] << kPageShift) | (va[j] & kPageMask);
         if (st[j] == PV_ST_OK) st[j] = upper<true>(st2, codes2, gpa[j], &code[j]) | 0x80000000u;
       }
 #pragma unroll
-      for (int j = 0; j < kVpt; ++j) w[j] = st[j] == 0x80000000u ? leaf_word(image, st2, code[j], gpa[j], leaf_codes, slot_page, pol_table) : 0;
+      for (int j = 0; j < VPT; ++j) w[j] = st[j] == 0x80000000u ? leaf_word(image, st2, code[j], gpa[j], leaf_codes, slot_page, pol_table) : 0;
 #pragma unroll
-      for (int j = 0; j < kVpt; ++j) {
+      for (int j = 0; j < VPT; ++j) {
         if (!(st[j] & 0x80000000u)) continue;
         st[j] = leaf_status<true>(w[j], st[j] & 0x7FFFFFFFu, gpa[j]);
         const uint32_t k = PV_ST_KIND(st[j]);
@@ -281,8 +283,8 @@ translate_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const 
       }
     }
 #pragma unroll
-    for (int j = 0; j < kVpt; ++j) {
-      const uint64_t i = lane0 + (uint64_t)j * kTpb + threadIdx.x;
+    for (int j = 0; j < VPT; ++j) {
+      const uint64_t i = lane0 + (uint64_t)j * TPB + threadIdx.x;
       if (i >= seg_end) continue;
       uint64_t v = val[j];
       if (!kPfn && st[j] == PV_ST_OK) v = (v << kPageShift) | (va[j] & kPageMask);
@@ -344,14 +346,24 @@ static cudaError_t launch_t(const uint8_t* image, uint64_t image_bytes, const pv
                             uint32_t n_segs, uint64_t n_chunks, const void* vas, const pv_index* idx,
                             uint64_t* out_value, uint32_t* out_status, uint64_t* out_aux, cudaStream_t stream) {
   auto k = translate_kernel<kTwo, kVa32, kPfn>;
-  uint64_t grid = resident_grid((const void*)k, kTpb, 0);
+  int tpb = kTpb;
+  if (!kTwo) {
+    // one-stage walks: 512-thread CTAs x 4 lanes (2 CTAs/SM) measured best on
+    // the C5 walk (1.03 vs 1.05 ms at 256 x 8); tuning hook PV_TRANSLATE_TPB
+    static const char* env = getenv("PV_TRANSLATE_TPB");
+    const int want = env ? atoi(env) : 512;
+    if (want == 512) { k = translate_kernel<kTwo, kVa32, kPfn, 512, 2>; tpb = 512; }
+    if (want == 1024) { k = translate_kernel<kTwo, kVa32, kPfn, 1024, 1>; tpb = 1024; }
+    if (want == 128) { k = translate_kernel<kTwo, kVa32, kPfn, 128, 8>; tpb = 128; }
+  }
+  uint64_t grid = resident_grid((const void*)k, tpb, 0);
   if (grid > n_chunks) grid = n_chunks;
   if (grid == 0) return cudaSuccess;
   const uint32_t* slot_of = idx != nullptr ? idx->slot_of : nullptr;
   const uint32_t* leaf_codes = idx != nullptr ? idx->leaf_codes : nullptr;
   const uint64_t* slot_page = idx != nullptr ? idx->slot_page : nullptr;
-  k<<<(unsigned)grid, kTpb, 0, stream>>>(image, image_bytes, spaces, segs, n_segs, n_chunks, vas, slot_of,
-                                         leaf_codes, slot_page, out_value, out_status, out_aux);
+  k<<<(unsigned)grid, tpb, 0, stream>>>(image, image_bytes, spaces, segs, n_segs, n_chunks, vas, slot_of,
+                                        leaf_codes, slot_page, out_value, out_status, out_aux);
   return cudaGetLastError();
 }
 
