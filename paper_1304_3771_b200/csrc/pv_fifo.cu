@@ -329,23 +329,38 @@ __global__ void fifo_verify_kernel(FifoStream fs, pv_fifo* __restrict__ fifo, Sc
   // spec_end[w - 1] (the previous window was accepted as speculated).
   bool have_s = true;
   uint64_t hits = 0, lookups = 0;
+  // the next block's link flags and counts are fetched one block ahead
+  uint8_t nx_m = (w0 + lane < w1) ? sc.match[w0 + lane] : 0;
+  uint64_t nx_c = (w0 + lane < w1) ? sc.win_counts[w0 + lane] : 0;
   for (uint64_t wb = w0; wb < w1; wb += 32) {
-    const uint64_t wl = wb + lane;
-    const uint32_t mm = __ballot_sync(full, wl < w1 && sc.match[wl]);
-    const uint64_t wc = wl < w1 ? sc.win_counts[wl] : 0;
+    const uint32_t mm = __ballot_sync(full, nx_m != 0);
+    const uint64_t wc = nx_c;
+    {
+      const uint64_t nl = wb + 32 + lane;
+      nx_m = nl < w1 ? sc.match[nl] : 0;
+      nx_c = nl < w1 ? sc.win_counts[nl] : 0;
+    }
+    // per-window hits | lookups packed in 16-bit halves for warp sums (<= 32 each)
+    const uint32_t wc16 = (uint32_t)(wc & 0xFFFF) | ((uint32_t)((wc >> 32) & 0xFFFF) << 16);
     const uint32_t nb = (uint32_t)(w1 - wb < 32 ? w1 - wb : 32);
-    for (uint32_t j = 0; j < nb; ++j) {
-      const uint64_t w = wb + j;
-      const uint64_t cj = __shfl_sync(full, wc, j);
+    uint32_t j = 0;
+    while (j < nb) {
       if (!have_s) {
-        if ((mm >> j) & 1u) {  // spec_start[w] == spec_end[w-1] == true state
-          hits += (uint32_t)cj;
-          lookups += cj >> 32;
-          continue;
+        // accept the whole run of linked windows j .. z-1 at once
+        const uint32_t rest = ~mm & (nb == 32 ? 0xFFFFFFFFu : ((1u << nb) - 1u)) & ~((1u << j) - 1u);
+        const uint32_t z = rest ? __ffs(rest) - 1 : nb;
+        if (z > j) {
+          const uint32_t sum = __reduce_add_sync(full, (lane >= j && lane < z) ? wc16 : 0u);
+          hits += sum & 0xFFFF;
+          lookups += sum >> 16;
+          j = z;
         }
-        load_state(sc.spec_end + (w - 1) * fs.state_words, fs.cap, lane, s);
+        if (j >= nb) break;
+        load_state(sc.spec_end + (wb + j - 1) * fs.state_words, fs.cap, lane, s);
         have_s = true;
       }
+      const uint64_t w = wb + j;
+      const uint64_t cj = __shfl_sync(full, wc, j);
       const uint64_t* b = sc.spec_start + w * fs.state_words;
       const uint64_t meta = b[2 * fs.cap];
       const bool lane_eq = lane >= s.len || (b[lane] == s.qk && b[fs.cap + lane] == s.qv);
@@ -360,6 +375,7 @@ __global__ void fifo_verify_kernel(FifoStream fs, pv_fifo* __restrict__ fifo, Sc
         hits += (uint32_t)c;
         lookups += c >> 32;
       }
+      ++j;
     }
   }
   if (!have_s) load_state(sc.spec_end + (w1 - 1) * fs.state_words, fs.cap, lane, s);
