@@ -339,6 +339,16 @@ int pv_gather_pages(const uint8_t* image, uint64_t image_bytes,
 /* Synchronises `stream` and reports the first CUDA error seen (0 if none). */
 int pv_stream_sync(void* stream);
 
+/* ---- measurement hook ------------------------------------------------------ */
+/* pv_timing(1) resets and starts recording a CUDA event pair around every
+ * launch of the library's dominant kernels (on the stream they are launched
+ * on); pv_timing(0) stops.  pv_timing_ms(kernel, &launches) synchronises the
+ * recorded events and returns the summed milliseconds of the named kernel
+ * ("ordered_apply") since the last reset.  Not a reference interface: bench.py
+ * uses it for the roofline's per-launch duration. */
+int pv_timing(int enable);
+double pv_timing_ms(const char* kernel, uint64_t* launches);
+
 #ifdef __cplusplus
 }
 #endif

@@ -62,7 +62,7 @@ EXPORTS = (
     "pv_fifo_replay", "pv_copy_plan", "pv_copy_stamp", "pv_copy_exec",
     "pv_copy_fifo_replay", "pv_scatter_pages", "pv_gather_pages", "pv_stream_sync", "pv_index_encode",
     "pv_fifo_scratch_bytes", "pv_copy_ordered_scratch_bytes", "pv_copy_ordered", "pv_result_encode",
-    "pv_result_decode",
+    "pv_result_decode", "pv_timing", "pv_timing_ms",
 )
 
 _u64 = ctypes.c_uint64
@@ -89,6 +89,8 @@ _SIGNATURES = {
     "pv_scatter_pages": (ctypes.c_int, [_p, _u64, _p, _u64, _p, _p]),
     "pv_gather_pages": (ctypes.c_int, [_p, _u64, _p, _u64, _p, _p]),
     "pv_stream_sync": (ctypes.c_int, [_p]),
+    "pv_timing": (ctypes.c_int, [ctypes.c_int]),
+    "pv_timing_ms": (ctypes.c_double, [ctypes.c_char_p, _p]),
 }
 
 _lock = threading.Lock()

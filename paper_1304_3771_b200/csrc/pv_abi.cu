@@ -3,6 +3,8 @@
 // Thin validation + launch layer: no allocation of user-visible memory, no
 // exceptions across the boundary, CUDA errors returned as PV_ECUDA - err.
 #include <mutex>
+#include <string>
+#include <vector>
 #include <unordered_map>
 
 #include "pv_common.cuh"
@@ -35,6 +37,61 @@ cudaError_t launch_fifo_lanes_abi(const void*, uint32_t, const uint64_t*, const 
 cudaError_t launch_fifo_copy_abi(const pv_op*, const uint64_t*, const uint64_t*, const uint32_t*, const uint64_t*,
                                  const uint64_t*, uint32_t, uint32_t, pv_fifo*, uint64_t, uint64_t*, uint32_t*,
                                  uint64_t*, void*, uint64_t, cudaStream_t);
+
+namespace {
+struct TimedLaunch {
+  std::string name;
+  cudaEvent_t ev[2];
+};
+std::mutex timing_mu;
+bool timing_on = false;
+std::vector<TimedLaunch> timing_log;
+}  // namespace
+
+cudaError_t timing_enable(bool on) {
+  std::lock_guard<std::mutex> g(timing_mu);
+  for (auto& t : timing_log) {
+    cudaEventDestroy(t.ev[0]);
+    cudaEventDestroy(t.ev[1]);
+  }
+  timing_log.clear();
+  timing_on = on;
+  return cudaSuccess;
+}
+
+void* timing_begin(const char* name, cudaStream_t stream) {
+  std::lock_guard<std::mutex> g(timing_mu);
+  if (!timing_on) return nullptr;
+  TimedLaunch t{name, {nullptr, nullptr}};
+  if (cudaEventCreate(&t.ev[0]) != cudaSuccess || cudaEventCreate(&t.ev[1]) != cudaSuccess) return nullptr;
+  cudaEventRecord(t.ev[0], stream);
+  timing_log.push_back(t);
+  return reinterpret_cast<void*>(timing_log.size());
+}
+
+void timing_end(void* token, cudaStream_t stream) {
+  if (token == nullptr) return;
+  std::lock_guard<std::mutex> g(timing_mu);
+  const size_t i = reinterpret_cast<size_t>(token) - 1;
+  if (i < timing_log.size()) cudaEventRecord(timing_log[i].ev[1], stream);
+}
+
+double timing_ms(const char* name, uint64_t* launches) {
+  std::lock_guard<std::mutex> g(timing_mu);
+  double ms = 0;
+  uint64_t n = 0;
+  for (auto& t : timing_log) {
+    if (name != nullptr && t.name != name) continue;
+    float f = 0;
+    cudaEventSynchronize(t.ev[1]);
+    if (cudaEventElapsedTime(&f, t.ev[0], t.ev[1]) == cudaSuccess) {
+      ms += f;
+      ++n;
+    }
+  }
+  if (launches != nullptr) *launches = n;
+  return ms;
+}
 
 uint64_t resident_grid(const void* func, int tpb, size_t smem) {
   static std::mutex mu;
@@ -249,6 +306,10 @@ int pv_gather_pages(const uint8_t* image, uint64_t image_bytes, const uint64_t* 
   gather_pages_kernel<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(image, image_bytes / kPageSize, pfns, n, dst);
   return rc(cudaGetLastError());
 }
+
+int pv_timing(int enable) { return rc(timing_enable(enable != 0)); }
+
+double pv_timing_ms(const char* kernel, uint64_t* launches) { return timing_ms(kernel, launches); }
 
 int pv_stream_sync(void* stream) {
   cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);

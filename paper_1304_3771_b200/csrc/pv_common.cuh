@@ -12,6 +12,10 @@
 
 namespace pv {
 
+// Measurement hook (pv_timing): event pair around a named launch when enabled.
+void* timing_begin(const char* name, cudaStream_t stream);
+void timing_end(void* token, cudaStream_t stream);
+
 constexpr uint32_t kPageShift = 12;
 constexpr uint64_t kPageSize = 4096;
 constexpr uint64_t kPageMask = kPageSize - 1;

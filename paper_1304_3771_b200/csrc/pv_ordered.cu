@@ -3,15 +3,17 @@
 // reference's sequential copy_user_buffer calls, memvirt.py:604-628).
 //
 // B200 design: every live chunk (page k of op o with k < first_bad[o]) is
-// keyed by its destination hpa page; a stable radix sort (CUB, 32-bit keys,
-// only the bits the image needs) groups chunks by page while preserving the
-// global chunk order (= op order, then page order); one CTA then owns one
-// destination page: it stages the page in shared memory, applies every chunk
-// of that page in order (all source bytes really move; the successive
-// overwrites land in SMEM instead of HBM, the way a write-back cache would
-// absorb them), and writes the page back once.  Chunk payloads stream in
-// through a cp.async ring ahead of the ordered applies, so the per-chunk
-// barrier only orders the shared-memory writes.
+// keyed by its destination hpa page; a stable radix sort (CUB, only the bits
+// the image needs) groups chunks by page while preserving the global chunk
+// order (= op order, then page order), and a gather lays the 16-byte chunk
+// descriptors out in that order.  One WARP then owns one destination page:
+// it stages the page in shared memory, streams the page's chunk payloads in
+// with TMA bulk copies (cp.async.bulk issued by one lane, completion counted
+// on a per-slot mbarrier) into a circular byte ring up to kK chunks ahead, and applies the chunks in order with 16-byte realigned
+// shared-memory writes.  All source bytes really move (HBM -> SMEM); the
+// successive overwrites land in SMEM instead of HBM, the way a write-back
+// cache would absorb them, and the page is written back once.  The pipeline
+// is warp-private: no CTA-wide barriers on the per-chunk path.
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_run_length_encode.cuh>
 #include <cub/device/device_scan.cuh>
@@ -20,130 +22,234 @@
 
 namespace pv {
 
-constexpr int kOrdTpb = 256;
-constexpr uint32_t kDeadKey = 0xFFFFFFFFu;
+// A chunk descriptor: the 16-byte aligned source start, and
+// meta = shift (4 bits) | dst offset in page (12 bits) << 4 | len (13 bits) << 16.
+struct __align__(16) ChunkDesc {
+  uint64_t src;
+  uint32_t meta;
+  uint32_t pad;
+};
 
-// keys[p] = destination page of live page p, else kDeadKey; vals[p] = p;
-// page_op[p] = the op page p belongs to.
-__global__ void ordered_keys_kernel(const uint64_t* __restrict__ page_off, uint64_t n_ops, uint64_t n_pages,
-                                    const uint64_t* __restrict__ page_hpa, const unsigned long long* __restrict__ first_bad,
-                                    uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
-                                    uint32_t* __restrict__ page_op) {
+// One thread per op: keys[p] = destination page of live page p (else the
+// dead key, which sorts last), vals[p] = p, desc[p] = p's chunk descriptor.
+__global__ void ordered_keys_kernel(const pv_op* __restrict__ ops, uint64_t n_ops, const uint64_t* __restrict__ page_off,
+                                    const uint64_t* __restrict__ page_hpa,
+                                    const unsigned long long* __restrict__ first_bad, const uint8_t* __restrict__ buf,
+                                    uint32_t dead_key, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                                    ChunkDesc* __restrict__ desc) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n_pages; p += stride) {
-    const uint64_t op = upper_search(page_off, 0, n_ops, p);
-    const uint64_t k = p - page_off[op];
-    keys[p] = k < first_bad[op] ? (uint32_t)(page_hpa[p] >> kPageShift) : kDeadKey;
-    vals[p] = (uint32_t)p;
-    page_op[p] = (uint32_t)op;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_ops; i += stride) {
+    const pv_op o = ops[i];
+    const uint64_t p0 = page_off[i], p1 = page_off[i + 1];
+    const uint64_t bad = first_bad[i];
+    for (uint64_t p = p0; p < p1; ++p) {
+      const uint64_t k = p - p0;
+      const uint64_t hpa = page_hpa[p];
+      const bool live = k < bad;
+      keys[p] = live ? (uint32_t)(hpa >> kPageShift) : dead_key;
+      vals[p] = (uint32_t)p;
+      const uint64_t cur = op_page_va(o.gva, k);
+      const uint64_t done = cur - o.gva;
+      const uint32_t len = live ? (uint32_t)min(o.len - done, kPageSize - (cur & kPageMask)) : 0;
+      const uint64_t src = reinterpret_cast<uint64_t>(buf + o.buf_off + done);
+      ChunkDesc d;
+      d.src = src & ~15ull;
+      d.meta = (uint32_t)(src & 15) | ((uint32_t)(hpa & kPageMask) << 4) | (len << 16);
+      d.pad = 0;
+      desc[p] = d;
+    }
   }
 }
 
-constexpr int kRing = 8;                       // chunks in flight per CTA
-constexpr uint32_t kSlotPad = 16;              // headroom so word reads at offset -3.. stay in the slot
-constexpr uint32_t kSlot = kSlotPad + kPageSize + 32;  // aligned superset of a <= 4 KiB chunk
-constexpr uint32_t kBatch = kOrdTpb;           // chunk descriptors resolved per round
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+// desc_sorted[i] = desc[sorted_pages[i]].
+__global__ void ordered_gather_kernel(const uint32_t* __restrict__ sorted_pages, uint64_t n,
+                                      const ChunkDesc* __restrict__ desc, ChunkDesc* __restrict__ out) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = desc[sorted_pages[i]];
 }
 
-// One CTA per destination page: stage the page in SMEM, then apply its
-// chunks in order.  Chunk descriptors are resolved 256 at a time (one per
-// thread, independent loads); chunk payloads stream in with 16-byte
-// cp.async (LDGSTS) into an 8-deep SMEM ring, so global-memory latency
-// overlaps the ordered SMEM applies.  The buffer must be readable up to the
-// next 16-byte boundary after each chunk (true of any 512-byte-granular
-// device allocation).
-__global__ void __launch_bounds__(kOrdTpb)
-ordered_apply_kernel(uint8_t* __restrict__ image, const pv_op* __restrict__ ops, const uint64_t* __restrict__ page_off,
-                     const uint64_t* __restrict__ page_hpa, const uint32_t* __restrict__ page_op,
-                     const uint32_t* __restrict__ sorted_pages, const uint32_t* __restrict__ seg_key,
-                     const uint32_t* __restrict__ seg_len, const uint32_t* __restrict__ seg_start,
-                     const uint32_t* __restrict__ n_segs_dev, const uint8_t* __restrict__ buf,
-                     uint8_t* __restrict__ dirty) {
-  __shared__ __align__(16) uint8_t page[kPageSize];
-  __shared__ __align__(16) uint8_t ring[kRing][kSlot];
-  __shared__ uint64_t d_src[kBatch];   // 16-byte aligned source start
-  __shared__ uint32_t d_meta[kBatch];  // shift (4 bits) | off (12 bits) << 4 | len (13 bits) << 16
+// ---- warp-per-page apply ------------------------------------------------------------
+
+constexpr int kApWarps = 4;                    // warps (pages in flight) per CTA
+constexpr int kK = 16;                         // chunks in flight per warp (mbarrier slots)
+constexpr uint32_t kRB = 8192;                 // circular byte ring per warp (power of two)
+constexpr uint32_t kRB16 = kRB / 16;
+
+struct __align__(16) WarpSmem {
+  uint8_t page[kPageSize];
+  uint8_t ring[kRB];
+  uint64_t mbar[kK];
+  uint32_t meta[kK];
+};
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, uint64_t src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
+      : "memory");
+}
+
+// Apply one chunk: dest bytes [off, off + len) of the page <- ring bytes
+// starting at ring byte `v0` (circular), realigned 16 bytes at a time.  D is
+// the (warp-uniform) word part of the realignment, so the word selection is
+// static: a whole destination block is two 16-byte SMEM loads, four funnel
+// shifts and one 16-byte SMEM store.  The (at most two) partial edge blocks
+// are merged by lanes 0 and 1 with byte masks from the `low` table
+// (low[x] = the low x bytes of 16 set), once per chunk.
+template <int D>
+__device__ __forceinline__ uint4 realign(const uint4* ring16, int32_t j, int32_t dq, uint32_t sb) {
+  const uint4 U = ring16[(uint32_t)(j + dq) & (kRB16 - 1)];
+  const uint4 V = ring16[(uint32_t)(j + dq + 1) & (kRB16 - 1)];
+  uint32_t y0, y1, y2, y3, y4;
+  if constexpr (D == 0) { y0 = U.x; y1 = U.y; y2 = U.z; y3 = U.w; y4 = V.x; }
+  if constexpr (D == 1) { y0 = U.y; y1 = U.z; y2 = U.w; y3 = V.x; y4 = V.y; }
+  if constexpr (D == 2) { y0 = U.z; y1 = U.w; y2 = V.x; y3 = V.y; y4 = V.z; }
+  if constexpr (D == 3) { y0 = U.w; y1 = V.x; y2 = V.y; y3 = V.z; y4 = V.w; }
+  uint4 out;
+  out.x = __funnelshift_r(y0, y1, sb);
+  out.y = __funnelshift_r(y1, y2, sb);
+  out.z = __funnelshift_r(y2, y3, sb);
+  out.w = __funnelshift_r(y3, y4, sb);
+  return out;
+}
+
+template <int D>
+__device__ __forceinline__ void apply_chunk(WarpSmem& W, const uint4* __restrict__ low, uint32_t lane, int32_t off,
+                                            int32_t len, int32_t dq, uint32_t sb) {
+  const uint4* ring16 = reinterpret_cast<const uint4*>(W.ring);
+  uint4* page16 = reinterpret_cast<uint4*>(W.page);
+  const int32_t end = off + len;
+  const int32_t jf0 = (off + 15) >> 4, jf1 = end >> 4;  // whole blocks [jf0, jf1)
+  for (int32_t j = jf0 + (int32_t)lane; j < jf1; j += 32) page16[j] = realign<D>(ring16, j, dq, sb);
+  // partial blocks: the head block (off not 16-aligned, or the chunk inside one block) and the tail block
+  const int32_t jh = off >> 4, jt = (end - 1) >> 4;
+  const bool head = (off & 15) != 0 || (jh == jt && (end & 15) != 0);
+  const bool tail = (end & 15) != 0 && jt != jh;
+  if ((lane == 0 && head) || (lane == 1 && tail)) {
+    const int32_t j = lane == 0 ? jh : jt;
+    const int32_t lo = max(off - 16 * j, 0), hi = min(end - 16 * j, 16);
+    const uint4 v = realign<D>(ring16, j, dq, sb);
+    const uint4 old = page16[j], mh = low[hi], ml = low[lo];
+    uint4 out;
+    out.x = (old.x & ~(mh.x & ~ml.x)) | (v.x & mh.x & ~ml.x);
+    out.y = (old.y & ~(mh.y & ~ml.y)) | (v.y & mh.y & ~ml.y);
+    out.z = (old.z & ~(mh.z & ~ml.z)) | (v.z & mh.z & ~ml.z);
+    out.w = (old.w & ~(mh.w & ~ml.w)) | (v.w & mh.w & ~ml.w);
+    page16[j] = out;
+  }
+}
+
+__global__ void __launch_bounds__(kApWarps * 32)
+ordered_apply_kernel(uint8_t* __restrict__ image, const ChunkDesc* __restrict__ desc,
+                     const uint32_t* __restrict__ seg_key, const uint32_t* __restrict__ seg_len,
+                     const uint32_t* __restrict__ seg_start, const uint32_t* __restrict__ n_segs_dev,
+                     uint32_t dead_key, uint8_t* __restrict__ dirty) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  WarpSmem& W = reinterpret_cast<WarpSmem*>(smem_raw)[warp];
+  __shared__ uint4 low[17];
+  if (threadIdx.x < 17) {
+    const uint32_t x = threadIdx.x;
+    auto lw = [](uint32_t n) { return n >= 4 ? 0xFFFFFFFFu : ((1u << (8 * n)) - 1u); };
+    low[x] = make_uint4(lw(x), lw(x > 4 ? x - 4 : 0), lw(x > 8 ? x - 8 : 0), lw(x > 12 ? x - 12 : 0));
+  }
+  __syncthreads();
+  if (lane == 0) {
+    for (int k = 0; k < kK; ++k) mbar_init(&W.mbar[k], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const uint64_t pol = policy_evict_first();
   const uint32_t n_segs = *n_segs_dev;
-  const uint32_t t = threadIdx.x;
-  for (uint32_t s = blockIdx.x; s < n_segs; s += gridDim.x) {
+  uint32_t gi = 0, ga = 0;  // chunks issued / applied by this warp (slot = g % kK, phase = (g / kK) & 1)
+  for (uint32_t s = blockIdx.x * kApWarps + warp; s < n_segs; s += gridDim.x * kApWarps) {
     const uint32_t key = seg_key[s];
-    if (key == kDeadKey) continue;
+    if (key == dead_key) continue;
     const uint64_t dst = (uint64_t)key << kPageShift;
-    reinterpret_cast<uint4*>(page)[t] = reinterpret_cast<const uint4*>(image + dst)[t];
     const uint32_t b = seg_start[s], n = seg_len[s];
-    for (uint32_t base = 0; base < n; base += kBatch) {
-      const uint32_t m = min(kBatch, n - base);
-      __syncthreads();  // previous round's descriptors / ring slots are free
-      if (t < m) {
-        const uint32_t p = sorted_pages[b + base + t];
-        const uint32_t op = page_op[p];
-        const pv_op o = ops[op];
-        const uint64_t k = p - page_off[op];
-        const uint64_t cur = op_page_va(o.gva, k);
-        const uint64_t done = cur - o.gva;
-        const uint32_t len = (uint32_t)min(o.len - done, kPageSize - (cur & kPageMask));
-        const uint32_t off = (uint32_t)(page_hpa[p] & kPageMask);
-        const uint64_t src = reinterpret_cast<uint64_t>(buf + o.buf_off + done);
-        d_src[t] = src & ~15ull;
-        d_meta[t] = (uint32_t)(src & 15) | (off << 4) | (len << 16);
-      }
-      __syncthreads();
-      auto issue = [&](uint32_t c) {
-        const uint32_t meta = d_meta[c];
-        const uint32_t shift = meta & 15, len = meta >> 16;
-        const uint32_t blocks = (shift + len + 15) >> 4;  // <= 257
-        const uint8_t* src = reinterpret_cast<const uint8_t*>(d_src[c]);
-        uint8_t* slot = ring[c % kRing] + kSlotPad;
-        for (uint32_t i = t; i < blocks; i += kOrdTpb) cp_async16(slot + 16 * i, src + 16 * i);
-      };
+    // chunk descriptors, 32 at a time in registers (lane j holds chunk cb + j), next batch prefetched
+    ChunkDesc cur{0, 0, 0}, nxt{0, 0, 0};
+    if (lane < n) cur = desc[b + lane];
+    if (32 + lane < n) nxt = desc[b + 32 + lane];
 #pragma unroll
-      for (int c = 0; c < kRing - 1; ++c) {
-        if ((uint32_t)c < m) issue(c);
-        cp_async_commit();
-      }
-      for (uint32_t c = 0; c < m; ++c) {
-        if (c + kRing - 1 < m) issue(c + kRing - 1);
-        cp_async_commit();
-        cp_async_wait<kRing - 1>();  // chunk c's group (this thread's part) landed
-        __syncthreads();             // ... and every thread's part
-        const uint32_t meta = d_meta[c];
-        const uint32_t shift = meta & 15, off = (meta >> 4) & 0xFFF, len = meta >> 16;
-        // destination-aligned 4-byte words; each word is owned by one thread
-        // (no read-modify-write races), the source is realigned with a funnel
-        // shift from two aligned slot words; conflict-free SMEM banks.
-        const uint32_t* slot32 = reinterpret_cast<const uint32_t*>(ring[c % kRing]);
-        uint32_t* page32 = reinterpret_cast<uint32_t*>(page);
-        const uint32_t w_first = off >> 2, w_last = (off + len - 1) >> 2;
-        for (uint32_t w = w_first + t; w <= w_last; w += kOrdTpb) {
-          const int32_t s0 = (int32_t)(kSlotPad + shift + 4 * w) - (int32_t)off;  // slot byte of word byte 0
-          const uint32_t lo = slot32[s0 >> 2], hi = slot32[(s0 >> 2) + 1];
-          const uint32_t v = __funnelshift_r(lo, hi, (s0 & 3) * 8);
-          const uint32_t b0 = 4 * w < off ? off - 4 * w : 0;                      // first byte of the word in chunk
-          const uint32_t b1 = 4 * w + 4 > off + len ? off + len - 4 * w : 4;      // one past the last
-          if (b0 == 0 && b1 == 4) {
-            page32[w] = v;
-          } else {
-            const uint32_t m = (b1 == 4 ? 0xFFFFFFFFu : ((1u << (8 * b1)) - 1u)) & ~((1u << (8 * b0)) - 1u);
-            page32[w] = (page32[w] & ~m) | (v & m);
-          }
+    for (int k = 0; k < 8; ++k)
+      reinterpret_cast<uint4*>(W.page)[lane + 32 * k] = reinterpret_cast<const uint4*>(image + dst)[lane + 32 * k];
+    // ring bytes in use: virtual [vtail, vhead), chunks packed back to back (circular)
+    uint32_t cb = 0, i = 0, a = 0, vhead = 0, vtail = 0;
+    __syncwarp();
+    while (a < n) {
+      // issue ahead: bounded by kK slots and the byte ring
+      while (i < n && i - a < (uint32_t)kK) {
+        if (i == cb + 32) {
+          cur = nxt;
+          cb += 32;
+          nxt = cb + 32 + lane < n ? desc[b + cb + 32 + lane] : ChunkDesc{0, 0, 0};
         }
-        __syncthreads();  // chunk c applied before c+1; its slot may be refilled
+        const uint32_t meta = __shfl_sync(0xFFFFFFFFu, cur.meta, i - cb);
+        const uint32_t span = (((meta & 15) + (meta >> 16) + 15) >> 4) << 4;
+        if (vhead + span - vtail > kRB) break;
+        const uint64_t src = ((uint64_t)__shfl_sync(0xFFFFFFFFu, (uint32_t)(cur.src >> 32), i - cb) << 32) |
+                             __shfl_sync(0xFFFFFFFFu, (uint32_t)cur.src, i - cb);
+        const uint32_t slot = gi % kK;
+        if (lane == 0) {
+          W.meta[slot] = meta;
+          const uint32_t p = vhead % kRB;
+          const uint32_t first = span < kRB - p ? span : kRB - p;  // split at the ring's end
+          mbar_expect_tx(&W.mbar[slot], span);
+          bulk_g2s(W.ring + p, src, first, &W.mbar[slot], pol);
+          if (first < span) bulk_g2s(W.ring, src + first, span - first, &W.mbar[slot], pol);
+        }
+        vhead += span;
+        ++i;
+        ++gi;
       }
-      cp_async_wait<0>();
+      __syncwarp();
+      // apply chunk a
+      const uint32_t slot = ga % kK;
+      mbar_wait(&W.mbar[slot], (ga / kK) & 1);
+      const uint32_t meta = W.meta[slot];
+      const uint32_t shift = meta & 15, len = meta >> 16;
+      const int32_t off = (int32_t)((meta >> 4) & 0xFFF);
+      // dest byte 16j + x  <->  ring byte 16j + delta + x
+      const int32_t delta = (int32_t)(vtail % kRB + shift) - off;
+      const int32_t dq = delta >> 4;
+      const uint32_t dr = (uint32_t)delta & 15, sb = (dr & 3) * 8;
+      switch (dr >> 2) {
+        case 0: apply_chunk<0>(W, low, lane, off, (int32_t)len, dq, sb); break;
+        case 1: apply_chunk<1>(W, low, lane, off, (int32_t)len, dq, sb); break;
+        case 2: apply_chunk<2>(W, low, lane, off, (int32_t)len, dq, sb); break;
+        default: apply_chunk<3>(W, low, lane, off, (int32_t)len, dq, sb); break;
+      }
+      vtail += ((shift + len + 15) >> 4) << 4;
+      __syncwarp();  // chunk a applied before a+1; its ring bytes and slot may be reissued
+      ++a;
+      ++ga;
     }
-    __syncthreads();
-    reinterpret_cast<uint4*>(image + dst)[t] = reinterpret_cast<const uint4*>(page)[t];
-    if (dirty != nullptr && t == 0) dirty[key] = 1;
-    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      reinterpret_cast<uint4*>(image + dst)[lane + 32 * k] = reinterpret_cast<const uint4*>(W.page)[lane + 32 * k];
+    if (dirty != nullptr && lane == 0) dirty[key] = 1;
+    __syncwarp();
   }
 }
 
@@ -176,7 +282,8 @@ __global__ void ordered_results_kernel(const pv_op* __restrict__ ops, uint64_t n
 }
 
 struct OrderedScratch {
-  uint32_t *keys_in, *vals_in, *keys_out, *vals_out, *seg_key, *seg_len, *seg_start, *page_op, *n_segs;
+  uint32_t *keys_in, *vals_in, *keys_out, *vals_out, *seg_key, *seg_len, *seg_start, *n_segs;
+  ChunkDesc *desc, *desc_sorted;
   void* cub_tmp;
   size_t cub_bytes;
 };
@@ -191,24 +298,33 @@ static size_t cub_need(uint64_t n, int end_bit) {
   return std::max(a, std::max(b, c));
 }
 
-static int bits_for(uint64_t) {
-  return 32;  // dead keys (0xFFFFFFFF) must sort last: sort on every bit
+// Keys are destination page numbers < image_pages and the dead key is
+// image_pages itself, so sorting the low bits_for(image_pages) bits suffices.
+static int bits_for(uint64_t image_pages) {
+  int b = 1;
+  while (b < 32 && (image_pages >> b) != 0) ++b;
+  return b;
 }
 
+static uint64_t arr_bytes(uint64_t n, uint64_t elt) { return ((n + 1) * elt + 255) / 256 * 256; }
+
 size_t ordered_scratch_bytes(uint64_t n_pages, uint64_t image_pages) {
-  const uint64_t arr = ((n_pages + 1) * 4 + 255) / 256 * 256;
-  return 8 * arr + 256 + cub_need(n_pages, bits_for(image_pages)) + 256;
+  return 7 * arr_bytes(n_pages, 4) + 2 * arr_bytes(n_pages, sizeof(ChunkDesc)) + 256 +
+         cub_need(n_pages, bits_for(image_pages)) + 256;
 }
 
 static OrderedScratch carve(void* base, uint64_t n, size_t cub_bytes) {
   uint8_t* p = static_cast<uint8_t*>(base);
   OrderedScratch s;
-  uint32_t** arrs[] = {&s.keys_in, &s.vals_in, &s.keys_out, &s.vals_out, &s.seg_key, &s.seg_len, &s.seg_start,
-                       &s.page_op};
+  uint32_t** arrs[] = {&s.keys_in, &s.vals_in, &s.keys_out, &s.vals_out, &s.seg_key, &s.seg_len, &s.seg_start};
   for (auto a : arrs) {
     *a = reinterpret_cast<uint32_t*>(p);
-    p += ((n + 1) * 4 + 255) / 256 * 256;
+    p += arr_bytes(n, 4);
   }
+  s.desc = reinterpret_cast<ChunkDesc*>(p);
+  p += arr_bytes(n, sizeof(ChunkDesc));
+  s.desc_sorted = reinterpret_cast<ChunkDesc*>(p);
+  p += arr_bytes(n, sizeof(ChunkDesc));
   s.n_segs = reinterpret_cast<uint32_t*>(p);
   p += 256;
   s.cub_tmp = p;
@@ -229,20 +345,29 @@ cudaError_t launch_copy_ordered(uint8_t* image, uint64_t image_bytes, const pv_o
         reinterpret_cast<const unsigned long long*>(op_first_bad), results);
   }
   if (n_pages == 0) return cudaGetLastError();
-  if (n_pages >= 0xFFFFFFFFull || (image_bytes >> kPageShift) >= 0xFFFFFFFFull) return cudaErrorInvalidValue;
-  const int end_bit = bits_for(image_bytes >> kPageShift);
+  const uint64_t image_pages = image_bytes >> kPageShift;
+  if (n_pages >= 0xFFFFFFFFull || image_pages >= 0xFFFFFFFFull) return cudaErrorInvalidValue;
+  const uint32_t dead_key = (uint32_t)image_pages;
+  const int end_bit = bits_for(image_pages);
   const size_t need = cub_need(n_pages, end_bit);
-  if (scratch_bytes < ordered_scratch_bytes(n_pages, image_bytes >> kPageShift)) return cudaErrorInvalidValue;
+  if (scratch_bytes < ordered_scratch_bytes(n_pages, image_pages)) return cudaErrorInvalidValue;
   OrderedScratch s = carve(scratch, n_pages, need);
-  uint64_t grid = (n_pages + 255) / 256;
-  if (grid > 4096) grid = 4096;
-  ordered_keys_kernel<<<(unsigned)grid, 256, 0, stream>>>(page_off, n_ops, n_pages, page_hpa,
-                                                          reinterpret_cast<const unsigned long long*>(op_first_bad),
-                                                          s.keys_in, s.vals_in, s.page_op);
+  {
+    uint64_t g = (n_ops + 255) / 256;
+    if (g > 8192) g = 8192;
+    ordered_keys_kernel<<<(unsigned)g, 256, 0, stream>>>(ops, n_ops, page_off, page_hpa,
+                                                         reinterpret_cast<const unsigned long long*>(op_first_bad),
+                                                         buf, dead_key, s.keys_in, s.vals_in, s.desc);
+  }
   size_t tb = s.cub_bytes;
   cudaError_t e = cub::DeviceRadixSort::SortPairs(s.cub_tmp, tb, s.keys_in, s.keys_out, s.vals_in, s.vals_out,
                                                   (int)n_pages, 0, end_bit, stream);
   if (e != cudaSuccess) return e;
+  {
+    uint64_t g = (n_pages + 255) / 256;
+    if (g > 8192) g = 8192;
+    ordered_gather_kernel<<<(unsigned)g, 256, 0, stream>>>(s.vals_out, n_pages, s.desc, s.desc_sorted);
+  }
   tb = s.cub_bytes;
   e = cub::DeviceRunLengthEncode::Encode(s.cub_tmp, tb, s.keys_out, s.seg_key, s.seg_len, s.n_segs, (int)n_pages,
                                          stream);
@@ -250,10 +375,20 @@ cudaError_t launch_copy_ordered(uint8_t* image, uint64_t image_bytes, const pv_o
   tb = s.cub_bytes;
   e = cub::DeviceScan::ExclusiveSum(s.cub_tmp, tb, s.seg_len, s.seg_start, (int)n_pages, stream);
   if (e != cudaSuccess) return e;
-  uint64_t g2 = resident_grid((const void*)ordered_apply_kernel, kOrdTpb, 0);
-  if (g2 > n_pages) g2 = n_pages;
-  ordered_apply_kernel<<<(unsigned)g2, kOrdTpb, 0, stream>>>(image, ops, page_off, page_hpa, s.page_op, s.vals_out,
-                                                             s.seg_key, s.seg_len, s.seg_start, s.n_segs, buf, dirty);
+  constexpr size_t smem = sizeof(WarpSmem) * kApWarps;
+  static bool attr_set = false;
+  if (!attr_set) {
+    e = cudaFuncSetAttribute(ordered_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  uint64_t g2 = resident_grid((const void*)ordered_apply_kernel, kApWarps * 32, smem);
+  const uint64_t want = (n_pages + kApWarps - 1) / kApWarps;
+  if (g2 > want) g2 = want;
+  void* tk = timing_begin("ordered_apply", stream);
+  ordered_apply_kernel<<<(unsigned)g2, kApWarps * 32, smem, stream>>>(image, s.desc_sorted, s.seg_key, s.seg_len,
+                                                                      s.seg_start, s.n_segs, dead_key, dirty);
+  timing_end(tk, stream);
   return cudaGetLastError();
 }
 

@@ -479,6 +479,46 @@ def test_c2_ioctl_trace_ordered_fifo_batch(cuda):
         assert (t.cache.hits, t.cache.misses, t.cache.entries()) == (hits, misses, entries)
 
 
+@pytest.mark.parametrize("seed", [0, 1])
+def test_ordered_apply_stress_faults_hot_pages_unaligned(cuda, seed):
+    """The ordered (last-writer-wins) path on its corner cases: thousands of
+    chunks on a few hot pages (deep per-page streams), every source/destination
+    byte alignment, multi-page ops, ops that fault part-way (prefix written,
+    later pages dead), zero-length ops and overlapping source ranges -- bytes
+    and per-op results equal the sequential oracle."""
+    from paper_1304_3771_b200 import workloads as W
+
+    memv, guest, spaces = W.build_c2(3)
+    trs = [memv.translator(sp, use_cache=False) for sp in spaces]
+    dspaces = [t.device_space for t in trs]
+    rng = np.random.default_rng(seed)
+    arena = W.C2_ARENA_GVA
+    arena_bytes = W.C2_ARENA_PAGES * 4096
+    n = 12_000
+    kind = rng.integers(0, 10, n)
+    gva = np.where(kind < 5, arena + rng.integers(0, 4 * 4096, n),                 # 4 hot pages
+                   arena + rng.integers(0, arena_bytes, n))
+    ln = np.where(kind < 5, rng.integers(1, 4097, n), rng.integers(0, 3 * 4096 + 77, n))
+    tail = kind == 9                                                                   # run off the arena
+    gva[tail] = arena + arena_bytes - rng.integers(1, 6000, int(tail.sum()))
+    ln[tail] = rng.integers(1, 9000, int(tail.sum()))
+    gva[kind == 8] = 0x4000_0000 + rng.integers(0, 1 << 20, int((kind == 8).sum()))  # unmapped: faults at once
+    ln[rng.random(n) < 0.01] = 0
+    buf_bytes = 1 << 22
+    boff = rng.integers(0, buf_bytes - 3 * 4096 - 100, n)
+    buf = rng.integers(0, 256, buf_bytes, dtype=np.uint8)
+    proc = rng.integers(0, len(spaces), n)
+    rows = np.stack([gva, ln, boff, proc], 1).astype(np.uint64)
+    raw = np.frombuffer(S.image_bytes(memv.host_mem), dtype=np.uint8).copy()
+    outs = dp.copy_ops(memv.host_mem.backing, dspaces, rows, N.TO_GUEST, torch.from_numpy(buf).cuda())
+    ospaces = np.stack([O.space(s.s1_base, s.s1_root_pfn, s.s2_root_pfn, s.mode) for s in dspaces])
+    ores = O.copy(raw, ospaces, rows, buf.copy(), 0)
+    assert np.array_equal(np.frombuffer(S.image_bytes(memv.host_mem), dtype=np.uint8), raw)
+    got = np.array([[o.copied, o.value, o.aux, o.status | (o.fail_page << 32)] for o in outs], np.uint64)
+    assert np.array_equal(got, ores)
+    assert {o.status for o in outs} != {0}
+
+
 def test_resultpage_encode_decode_deliver_batch(cuda):
     """a batch of result records encoded into result pages
     on the device is byte-identical to the reference codec, decodes back, and
