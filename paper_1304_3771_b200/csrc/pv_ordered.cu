@@ -71,16 +71,18 @@ __global__ void ordered_gather_kernel(const uint32_t* __restrict__ sorted_pages,
 
 // ---- warp-per-page apply ------------------------------------------------------------
 
-constexpr int kApWarps = 4;                    // warps (pages in flight) per CTA
-constexpr int kK = 16;                         // chunks in flight per warp (mbarrier slots)
-constexpr uint32_t kRB = 8192;                 // circular byte ring per warp (power of two)
+constexpr int kApPages = 4;                    // page slots (producer + consumer warp each) per CTA
+constexpr int kK = 16;                         // chunks in flight per page slot (mbarrier pairs)
+constexpr uint32_t kRB = 8192;                 // circular byte ring per page slot (power of two)
 constexpr uint32_t kRB16 = kRB / 16;
 
-struct __align__(16) WarpSmem {
+struct __align__(16) PageSmem {
   uint8_t page[kPageSize];
   uint8_t ring[kRB];
-  uint64_t mbar[kK];
+  uint64_t full[kK];
+  uint64_t empty[kK];
   uint32_t meta[kK];
+  uint32_t vstart[kK];
 };
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -134,7 +136,7 @@ __device__ __forceinline__ uint4 realign(const uint4* ring16, int32_t j, int32_t
 }
 
 template <int D>
-__device__ __forceinline__ void apply_chunk(WarpSmem& W, const uint4* __restrict__ low, uint32_t lane, int32_t off,
+__device__ __forceinline__ void apply_chunk(PageSmem& W, const uint4* __restrict__ low, uint32_t lane, int32_t off,
                                             int32_t len, int32_t dq, uint32_t sb) {
   const uint4* ring16 = reinterpret_cast<const uint4*>(W.ring);
   uint4* page16 = reinterpret_cast<uint4*>(W.page);
@@ -159,95 +161,124 @@ __device__ __forceinline__ void apply_chunk(WarpSmem& W, const uint4* __restrict
   }
 }
 
-__global__ void __launch_bounds__(kApWarps * 32)
+// One page slot per producer/consumer warp pair.  The producer warp walks
+// the page's chunk descriptors and keeps the ring full (TMA bulk copies,
+// completion on full[slot]); the consumer warp stages the destination page,
+// applies chunk after chunk in order and releases each ring slot on
+// empty[slot].  Ring bytes are packed back to back in virtual byte order;
+// before reusing bytes the producer waits for the release of the newest
+// chunk that still occupies them (releases are in order).
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+
+__device__ __forceinline__ void produce(PageSmem& P, const ChunkDesc* __restrict__ desc, uint32_t b, uint32_t n,
+                                        uint32_t lane, uint64_t pol, uint32_t& G, uint32_t& vhead, uint32_t& hptr,
+                                        int64_t& released) {
+  ChunkDesc cur{0, 0, 0}, nxt{0, 0, 0};
+  if (lane < n) cur = desc[b + lane];
+  if (32 + lane < n) nxt = desc[b + 32 + lane];
+  uint32_t cb = 0;
+  for (uint32_t k = 0; k < n; ++k, ++G) {
+    if (k == cb + 32) {
+      cur = nxt;
+      cb += 32;
+      nxt = cb + 32 + lane < n ? desc[b + cb + 32 + lane] : ChunkDesc{0, 0, 0};
+    }
+    const uint32_t meta = __shfl_sync(0xFFFFFFFFu, cur.meta, k - cb);
+    const uint64_t src = ((uint64_t)__shfl_sync(0xFFFFFFFFu, (uint32_t)(cur.src >> 32), k - cb) << 32) |
+                         __shfl_sync(0xFFFFFFFFu, (uint32_t)cur.src, k - cb);
+    const uint32_t span = (((meta & 15) + (meta >> 16) + 15) >> 4) << 4;
+    const uint32_t ve = vhead + span;
+    // chunk G reuses slot G % kK (last held by chunk G - kK) and the ring
+    // bytes of every chunk whose virtual start is below ve - kRB
+    if (G >= (uint32_t)kK && hptr < G - kK + 1) hptr = G - kK + 1;
+    while (hptr < G && (int32_t)(P.vstart[hptr % kK] - (ve - kRB)) < 0) ++hptr;
+    int64_t r = (int64_t)hptr - 1;
+    if (G >= (uint32_t)kK && (int64_t)(G - kK) > r) r = G - kK;
+    if (r > released) {
+      mbar_wait(&P.empty[r % kK], (uint32_t)(r / kK) & 1);
+      released = r;
+    }
+    const uint32_t slot = G % kK;
+    P.vstart[slot] = vhead;  // producer-private history (every lane stores the same value)
+    if (lane == 0) {
+      P.meta[slot] = meta;
+      const uint32_t p = vhead % kRB;
+      const uint32_t first = span < kRB - p ? span : kRB - p;  // split at the ring's end
+      mbar_expect_tx(&P.full[slot], span);
+      if (span != 0) bulk_g2s(P.ring + p, src, first, &P.full[slot], pol);
+      if (first < span) bulk_g2s(P.ring, src + first, span - first, &P.full[slot], pol);
+    }
+    vhead = ve;
+  }
+}
+
+__global__ void __launch_bounds__(kApPages * 64)
 ordered_apply_kernel(uint8_t* __restrict__ image, const ChunkDesc* __restrict__ desc,
                      const uint32_t* __restrict__ seg_key, const uint32_t* __restrict__ seg_len,
                      const uint32_t* __restrict__ seg_start, const uint32_t* __restrict__ n_segs_dev,
                      uint32_t dead_key, uint8_t* __restrict__ dirty) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  WarpSmem& W = reinterpret_cast<WarpSmem*>(smem_raw)[warp];
+  const uint32_t pslot = warp >> 1;
+  const bool producer = (warp & 1) == 0;
+  PageSmem& P = reinterpret_cast<PageSmem*>(smem_raw)[pslot];
   __shared__ uint4 low[17];
   if (threadIdx.x < 17) {
     const uint32_t x = threadIdx.x;
     auto lw = [](uint32_t n) { return n >= 4 ? 0xFFFFFFFFu : ((1u << (8 * n)) - 1u); };
     low[x] = make_uint4(lw(x), lw(x > 4 ? x - 4 : 0), lw(x > 8 ? x - 8 : 0), lw(x > 12 ? x - 12 : 0));
   }
-  __syncthreads();
-  if (lane == 0) {
-    for (int k = 0; k < kK; ++k) mbar_init(&W.mbar[k], 1);
+  if (producer && lane == 0) {
+    for (int k = 0; k < kK; ++k) {
+      mbar_init(&P.full[k], 1);
+      mbar_init(&P.empty[k], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  __syncwarp();
+  __syncthreads();
   const uint64_t pol = policy_evict_first();
   const uint32_t n_segs = *n_segs_dev;
-  uint32_t gi = 0, ga = 0;  // chunks issued / applied by this warp (slot = g % kK, phase = (g / kK) & 1)
-  for (uint32_t s = blockIdx.x * kApWarps + warp; s < n_segs; s += gridDim.x * kApWarps) {
+  uint32_t G = 0, vhead = 0, hptr = 0;  // chunks so far / virtual ring bytes so far (both roles)
+  int64_t released = -1;                 // producer: newest chunk known released
+  for (uint32_t s = blockIdx.x * kApPages + pslot; s < n_segs; s += gridDim.x * kApPages) {
     const uint32_t key = seg_key[s];
     if (key == dead_key) continue;
-    const uint64_t dst = (uint64_t)key << kPageShift;
     const uint32_t b = seg_start[s], n = seg_len[s];
-    // chunk descriptors, 32 at a time in registers (lane j holds chunk cb + j), next batch prefetched
-    ChunkDesc cur{0, 0, 0}, nxt{0, 0, 0};
-    if (lane < n) cur = desc[b + lane];
-    if (32 + lane < n) nxt = desc[b + 32 + lane];
+    if (producer) {
+      produce(P, desc, b, n, lane, pol, G, vhead, hptr, released);
+      continue;
+    }
+    const uint64_t dst = (uint64_t)key << kPageShift;
 #pragma unroll
     for (int k = 0; k < 8; ++k)
-      reinterpret_cast<uint4*>(W.page)[lane + 32 * k] = reinterpret_cast<const uint4*>(image + dst)[lane + 32 * k];
-    // ring bytes in use: virtual [vtail, vhead), chunks packed back to back (circular)
-    uint32_t cb = 0, i = 0, a = 0, vhead = 0, vtail = 0;
+      reinterpret_cast<uint4*>(P.page)[lane + 32 * k] = reinterpret_cast<const uint4*>(image + dst)[lane + 32 * k];
     __syncwarp();
-    while (a < n) {
-      // issue ahead: bounded by kK slots and the byte ring
-      while (i < n && i - a < (uint32_t)kK) {
-        if (i == cb + 32) {
-          cur = nxt;
-          cb += 32;
-          nxt = cb + 32 + lane < n ? desc[b + cb + 32 + lane] : ChunkDesc{0, 0, 0};
-        }
-        const uint32_t meta = __shfl_sync(0xFFFFFFFFu, cur.meta, i - cb);
-        const uint32_t span = (((meta & 15) + (meta >> 16) + 15) >> 4) << 4;
-        if (vhead + span - vtail > kRB) break;
-        const uint64_t src = ((uint64_t)__shfl_sync(0xFFFFFFFFu, (uint32_t)(cur.src >> 32), i - cb) << 32) |
-                             __shfl_sync(0xFFFFFFFFu, (uint32_t)cur.src, i - cb);
-        const uint32_t slot = gi % kK;
-        if (lane == 0) {
-          W.meta[slot] = meta;
-          const uint32_t p = vhead % kRB;
-          const uint32_t first = span < kRB - p ? span : kRB - p;  // split at the ring's end
-          mbar_expect_tx(&W.mbar[slot], span);
-          bulk_g2s(W.ring + p, src, first, &W.mbar[slot], pol);
-          if (first < span) bulk_g2s(W.ring, src + first, span - first, &W.mbar[slot], pol);
-        }
-        vhead += span;
-        ++i;
-        ++gi;
-      }
-      __syncwarp();
-      // apply chunk a
-      const uint32_t slot = ga % kK;
-      mbar_wait(&W.mbar[slot], (ga / kK) & 1);
-      const uint32_t meta = W.meta[slot];
+    for (uint32_t k = 0; k < n; ++k, ++G) {
+      const uint32_t slot = G % kK;
+      mbar_wait(&P.full[slot], (G / kK) & 1);
+      const uint32_t meta = P.meta[slot];
       const uint32_t shift = meta & 15, len = meta >> 16;
       const int32_t off = (int32_t)((meta >> 4) & 0xFFF);
       // dest byte 16j + x  <->  ring byte 16j + delta + x
-      const int32_t delta = (int32_t)(vtail % kRB + shift) - off;
+      const int32_t delta = (int32_t)(vhead % kRB + shift) - off;
       const int32_t dq = delta >> 4;
       const uint32_t dr = (uint32_t)delta & 15, sb = (dr & 3) * 8;
       switch (dr >> 2) {
-        case 0: apply_chunk<0>(W, low, lane, off, (int32_t)len, dq, sb); break;
-        case 1: apply_chunk<1>(W, low, lane, off, (int32_t)len, dq, sb); break;
-        case 2: apply_chunk<2>(W, low, lane, off, (int32_t)len, dq, sb); break;
-        default: apply_chunk<3>(W, low, lane, off, (int32_t)len, dq, sb); break;
+        case 0: apply_chunk<0>(P, low, lane, off, (int32_t)len, dq, sb); break;
+        case 1: apply_chunk<1>(P, low, lane, off, (int32_t)len, dq, sb); break;
+        case 2: apply_chunk<2>(P, low, lane, off, (int32_t)len, dq, sb); break;
+        default: apply_chunk<3>(P, low, lane, off, (int32_t)len, dq, sb); break;
       }
-      vtail += ((shift + len + 15) >> 4) << 4;
-      __syncwarp();  // chunk a applied before a+1; its ring bytes and slot may be reissued
-      ++a;
-      ++ga;
+      vhead += ((shift + len + 15) >> 4) << 4;
+      __syncwarp();  // every lane's ring reads and page writes of chunk k are done
+      if (lane == 0) mbar_arrive(&P.empty[slot]);
     }
+    __syncwarp();
 #pragma unroll
     for (int k = 0; k < 8; ++k)
-      reinterpret_cast<uint4*>(image + dst)[lane + 32 * k] = reinterpret_cast<const uint4*>(W.page)[lane + 32 * k];
+      reinterpret_cast<uint4*>(image + dst)[lane + 32 * k] = reinterpret_cast<const uint4*>(P.page)[lane + 32 * k];
     if (dirty != nullptr && lane == 0) dirty[key] = 1;
     __syncwarp();
   }
@@ -375,18 +406,18 @@ cudaError_t launch_copy_ordered(uint8_t* image, uint64_t image_bytes, const pv_o
   tb = s.cub_bytes;
   e = cub::DeviceScan::ExclusiveSum(s.cub_tmp, tb, s.seg_len, s.seg_start, (int)n_pages, stream);
   if (e != cudaSuccess) return e;
-  constexpr size_t smem = sizeof(WarpSmem) * kApWarps;
+  constexpr size_t smem = sizeof(PageSmem) * kApPages;
   static bool attr_set = false;
   if (!attr_set) {
     e = cudaFuncSetAttribute(ordered_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  uint64_t g2 = resident_grid((const void*)ordered_apply_kernel, kApWarps * 32, smem);
-  const uint64_t want = (n_pages + kApWarps - 1) / kApWarps;
+  uint64_t g2 = resident_grid((const void*)ordered_apply_kernel, kApPages * 64, smem);
+  const uint64_t want = (n_pages + kApPages - 1) / kApPages;
   if (g2 > want) g2 = want;
   void* tk = timing_begin("ordered_apply", stream);
-  ordered_apply_kernel<<<(unsigned)g2, kApWarps * 32, smem, stream>>>(image, s.desc_sorted, s.seg_key, s.seg_len,
+  ordered_apply_kernel<<<(unsigned)g2, kApPages * 64, smem, stream>>>(image, s.desc_sorted, s.seg_key, s.seg_len,
                                                                       s.seg_start, s.n_segs, dead_key, dirty);
   timing_end(tk, stream);
   return cudaGetLastError();
