@@ -475,8 +475,8 @@ def run_c2(args, rank, world, local):
         "copy": {"value": payload * K / (total_ms / 1e3) / 1e9, "unit": "GB/s (payload)"},
         "plan_fifo_ms_per_step": plan_ms / K, "ordered_apply_ms_per_step": apply_ms / K,
         "roofline": {"bound": "hbm", "kernel": "ordered_apply_kernel", "achieved": ach, "peak": peak,
-                     "unit": "GB/s", "frac": ach / peak, "peak_source": peak_kind, "traffic": None,
-                     "launch_ms": per_launch_ms, "alg_bytes_per_launch": alg_bytes,
+                     "unit": "GB/s", "frac": ach / peak, "peak_source": peak_kind,
+                     "traffic": load_traffic("c2").get("ordered_apply"), "launch_ms": per_launch_ms, "alg_bytes_per_launch": alg_bytes,
                      "note": "payload bytes read once + each destination page staged and written back once, "
                              "over the apply kernel's event-timed launch duration (pv_timing)"},
         "gpu_launches": 10 * K, "gpu_launches_note": "plan, 4 FIFO-replay steps, stamp, exec (stands down), "
