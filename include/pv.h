@@ -310,6 +310,41 @@ int pv_copy_ordered(uint8_t* image, uint64_t image_bytes, const pv_op* ops,
                     const uint8_t* buf, pv_op_result* results, uint8_t* dirty,
                     void* scratch, uint64_t scratch_bytes, void* stream);
 
+/* ---- trap shim on the device -----------------------
+ * The default hypervisor shim of the hybrid resolver (backend.py:117-128,
+ * 288-296; resolve_hybrid_with_fixup, memvirt.py:685-696) for a planned copy
+ * batch over hybrid spaces: run after pv_copy_plan, before the stamp / exec.
+ * shims[s] (device, one per space of the batch) names the guest process
+ * behind hybrid space s; guest_bytes == 0 disables the shim for that space.
+ *
+ * Every trapped page whose shim the device can run exactly is resolved: a
+ * leaf-level trap whose shadow descend (TableEditor._descend, memvirt.py:
+ * 282-298) ends on the trapping slot, whose guest walk succeeds and whose
+ * gpa lies inside the slot.  Per slot, the earliest such page in (op, page)
+ * order writes word = (hpa >> 12) << 12 | P | W into the image (dirty set for
+ * the node page); the page then re-walks the hybrid table (the retry) and
+ * gets an ordinary translation.  op_first_bad is recomputed.  Every other
+ * trap keeps its PV_ST_TRAP status; the first op whose first failure is such
+ * a trap is the cut -- shims of pages after it are not applied (their traps
+ * stand), so the host can finish that op with its own shim and re-plan the
+ * rest in order.  n_written (device u64, may be NULL) is incremented by the
+ * number of table words written.  scratch: device memory of pv_copy_shim_scratch_bytes
+ * (n_pages) bytes, zero-filled before its first use; every call leaves it
+ * zero-filled again. */
+typedef struct pv_shim {
+  uint64_t guest_base;      /* byte base of the guest slot (gpa 0)                */
+  uint64_t guest_bytes;     /* slot size: gpa_to_hpa bound (memvirt.py:491-497)   */
+  uint64_t guest_root_pfn;  /* the process's guest table root (window relative)  */
+  uint64_t shadow_root_pfn; /* the process's shadow table root (host memory)     */
+} pv_shim;
+
+uint64_t pv_copy_shim_scratch_bytes(uint64_t n_pages);
+int pv_copy_shim(uint8_t* image, uint64_t image_bytes, const pv_space* spaces, const pv_shim* shims,
+                 const pv_op* ops, uint64_t n_ops, const uint64_t* page_off, uint64_t n_pages,
+                 uint64_t* page_hpa, uint32_t* page_status, uint64_t* op_first_bad,
+                 uint8_t* dirty, uint64_t* n_written, void* scratch, uint64_t scratch_bytes,
+                 void* stream);
+
 /* ---- result-page codec ------------------------------
  * Batched resultpage.encode + the backend's host_mem.write of the record
  * (resultpage.py:44-51, backend.py:352-355): record r is header[9*r ..

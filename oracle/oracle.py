@@ -43,6 +43,8 @@ def lib():
         l.orc_translate_cached.argtypes = [_p, _u64, _p, _p, _u64, _p, _p, _p, _p]
         l.orc_copy.restype = None
         l.orc_copy.argtypes = [_p, _u64, _p, _p, _u64, _p, ctypes.c_int, _p, _p, _p, ctypes.c_int]
+        l.orc_copy_hybrid.restype = _u64
+        l.orc_copy_hybrid.argtypes = [_p, _u64, _p, _p, _p, _u64, _p, ctypes.c_int, _p, _p]
         _lib = l
     return _lib
 
@@ -112,3 +114,20 @@ def copy(img: np.ndarray, spaces: np.ndarray, ops: np.ndarray, buf: np.ndarray, 
     lib().orc_copy(_ptr(img), img.nbytes, _ptr(spaces), _ptr(ops), len(ops), _ptr(buf), direction, cptr, optr,
                    _ptr(res), threads)
     return res
+
+
+ST_SHIM_HOST = 0x800
+
+
+def copy_hybrid(img: np.ndarray, spaces: np.ndarray, shims: np.ndarray, ops: np.ndarray, buf: np.ndarray,
+                direction: int):
+    """Hybrid-resolver copies with the default trap shim, in order (rows as
+    :func:`copy`).  Returns (results, cut op index or len(ops), translations)."""
+    spaces = np.ascontiguousarray(spaces, dtype=np.uint64).reshape(-1, 4)
+    shims = np.ascontiguousarray(shims, dtype=np.uint64).reshape(-1, 4)
+    ops = np.ascontiguousarray(ops, dtype=np.uint64).reshape(-1, 4)
+    res = np.zeros((len(ops), 4), np.uint64)
+    count = np.zeros(1, np.uint64)
+    cut = lib().orc_copy_hybrid(_ptr(img), img.nbytes, _ptr(spaces), _ptr(shims), _ptr(ops), len(ops), _ptr(buf),
+                                direction, _ptr(res), _ptr(count))
+    return res, int(cut), int(count[0])

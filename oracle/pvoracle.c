@@ -21,6 +21,13 @@
  *                                            prefix on fault, bytes_copied)
  *                       memvirt.py:156-168   PhysMem read/write bounds ->
  *                                            OutOfRange
+ *   orc_copy_hybrid     memvirt.py:685-696   resolve_hybrid_with_fixup with
+ *                       backend.py:288-296   the default trap shim (walk_guest,
+ *                       memvirt.py:491-497   gpa_to_hpa, TableEditor.map
+ *                       memvirt.py:282-313   replace=True) inside
+ *                                            copy_user_buffer; shims that
+ *                                            would allocate a node or raise
+ *                                            stop the batch (ST_SHIM_HOST)
  * Status words use the same encoding as include/pv.h so results compare
  * directly; the encoding is defined there, the semantics here.
  * Parity of this file against the reference itself is pinned by
@@ -280,6 +287,112 @@ void orc_copy(uint8_t* img, uint64_t img_bytes, const orc_space* spaces, const u
     orc_fifo* c = (caches && op_cache && op_cache[i] >= 0) ? &caches[op_cache[i]] : 0;
     orc_copy1(img, img_bytes, &spaces[o[3] & 0xFFFFFFFFu], o[0], o[1], buf + o[2], direction, c, &results[i]);
   }
+}
+
+/* ---- hybrid copies with the default trap shim ------------------------- */
+#define ST_SHIM_HOST 0x800u /* the shim would allocate, raise or diverge: not restated */
+
+typedef struct {
+  uint64_t guest_base, guest_bytes, guest_root, shadow_root;
+} orc_shim; /* same layout as pv_shim */
+
+/* backend.py:288-296 for a trap at `va`: 0 and the word written, or
+ * ST_SHIM_HOST.  The shadow descend follows every entry that is not
+ * NOT_PRESENT (memvirt.py:282-298); a NOT_PRESENT upper entry would allocate. */
+static uint32_t shim_once(uint8_t* img, uint64_t img_bytes, const orc_shim* sh, uint64_t va) {
+  const uint64_t page_va = va & ~0xFFFull;
+  uint64_t gpfn = 0;
+  if (orc_walk(img, img_bytes, sh->guest_base, sh->guest_root, page_va, 0, &gpfn) != ST_OK) return ST_SHIM_HOST;
+  const uint64_t gpa = gpfn << 12;
+  if (gpa >= sh->guest_bytes) return ST_SHIM_HOST; /* gpa_to_hpa: OutOfRange */
+  const uint64_t lim = img_bytes / PG;
+  uint64_t node = sh->shadow_root;
+  const uint32_t idx[3] = {(uint32_t)((page_va >> 30) & 3u), (uint32_t)((page_va >> 21) & 0x1FFu),
+                           (uint32_t)((page_va >> 12) & 0x1FFu)};
+  for (int l = 0; l < 2; ++l) {
+    if (node >= lim) return ST_SHIM_HOST;
+    const uint64_t w = rd64(img, node * PG + (uint64_t)idx[l] * 8u);
+    if (!(w & 0x5u)) return ST_SHIM_HOST;
+    node = w >> 12;
+  }
+  if (node >= lim) return ST_SHIM_HOST;
+  const uint64_t hpa = sh->guest_base + gpa;
+  const uint64_t word = ((hpa >> 12) << 12) | 0x3u; /* PRESENT | writable */
+  memcpy(img + node * PG + (uint64_t)idx[2] * 8u, &word, 8);
+  return ST_OK;
+}
+
+/* copy_user_buffer through _HybridResolver (backend.py:117-128): each page
+ * resolves through the hybrid root (spaces[op].s1_root, host memory); a trap
+ * runs the shim once and retries; a second trap is TrapFixupFailed
+ * (status ST_TRAP | ST_SHIM_HOST here).  Ops run in order.  Returns the index
+ * of the first op whose shim is outside the restated subset (that op's
+ * status carries ST_SHIM_HOST and nothing after it ran), or n_ops.
+ * *translations counts translate() calls (hw_translations). */
+uint64_t orc_copy_hybrid(uint8_t* img, uint64_t img_bytes, const orc_space* spaces, const orc_shim* shims,
+                         const uint64_t* ops, uint64_t n_ops, uint8_t* buf, int direction, orc_result* results,
+                         uint64_t* translations) {
+  for (uint64_t i = 0; i < n_ops; ++i) {
+    const uint64_t* o = ops + 4 * i;
+    const orc_space* sp = &spaces[o[3] & 0xFFFFFFFFu];
+    const orc_shim* sh = &shims[o[3] & 0xFFFFFFFFu];
+    const uint64_t gva = o[0], len = o[1];
+    uint8_t* b = buf + o[2];
+    orc_result* res = &results[i];
+    uint64_t copied = 0, page = 0;
+    memset(res, 0, sizeof(*res));
+    while (copied < len) {
+      const uint64_t cur = gva + copied;
+      uint64_t chunk = PG - (cur & 0xFFFu);
+      if (chunk > len - copied) chunk = len - copied;
+      uint64_t hpa = 0, a = 0;
+      ++*translations;
+      uint32_t st = orc_translate1(img, img_bytes, sp, cur, 0, &hpa, &a);
+      if ((st & 0xFF0u) == ST_TRAP) {
+        if (sh->guest_bytes == 0 || shim_once(img, img_bytes, sh, cur) != ST_OK) {
+          res->copied = copied;
+          res->value = hpa;
+          res->status = st | ST_SHIM_HOST;
+          res->fail_page = (uint32_t)page;
+          return i;
+        }
+        st = orc_translate1(img, img_bytes, sp, cur, 0, &hpa, &a);
+        if ((st & 0xFF0u) == ST_TRAP) { /* TrapFixupFailed */
+          res->copied = copied;
+          res->value = hpa;
+          res->status = st | ST_SHIM_HOST;
+          res->fail_page = (uint32_t)page;
+          return i;
+        }
+      }
+      if (st != ST_OK) {
+        res->copied = copied;
+        res->value = hpa;
+        res->aux = a;
+        res->status = st;
+        res->fail_page = (uint32_t)page;
+        break;
+      }
+      if (hpa + chunk > img_bytes || hpa + chunk < hpa) {
+        res->copied = copied;
+        res->value = hpa;
+        res->status = ST_DATA_OOR;
+        res->fail_page = (uint32_t)page;
+        break;
+      }
+      if (direction == 0)
+        memcpy(img + hpa, b + copied, chunk);
+      else
+        memcpy(b + copied, img + hpa, chunk);
+      copied += chunk;
+      ++page;
+    }
+    if (copied == len) {
+      res->copied = copied;
+      res->status = ST_OK;
+    }
+  }
+  return n_ops;
 }
 
 int orc_abi_version(void) { return 1; }

@@ -52,6 +52,7 @@ FIFO_MAX = 32
 # struct sizes in 8-byte words (all structs are u64-aligned)
 SPACE_WORDS = 4    # pv_space
 SEG_WORDS = 4      # pv_seg
+SHIM_WORDS = 4     # pv_shim
 OP_WORDS = 4       # pv_op
 RESULT_WORDS = 4   # pv_op_result
 FIFO_WORDS = 2 * FIFO_MAX + 4  # pv_fifo
@@ -62,7 +63,7 @@ EXPORTS = (
     "pv_fifo_replay", "pv_copy_plan", "pv_copy_stamp", "pv_copy_exec",
     "pv_copy_fifo_replay", "pv_scatter_pages", "pv_gather_pages", "pv_stream_sync", "pv_index_encode",
     "pv_fifo_scratch_bytes", "pv_copy_ordered_scratch_bytes", "pv_copy_ordered", "pv_result_encode",
-    "pv_result_decode", "pv_timing", "pv_timing_ms",
+    "pv_result_decode", "pv_timing", "pv_timing_ms", "pv_copy_shim_scratch_bytes", "pv_copy_shim",
 )
 
 _u64 = ctypes.c_uint64
@@ -78,6 +79,8 @@ _SIGNATURES = {
     "pv_fifo_replay": (ctypes.c_int, [_p, _u32, _p, _p, _p, _u32, _u32, _p, _p, _p, _p, _u64, _p]),
     "pv_fifo_scratch_bytes": (_u64, [_u64, _u64, _u32]),
     "pv_copy_ordered_scratch_bytes": (_u64, [_u64, _u64]),
+    "pv_copy_shim_scratch_bytes": (_u64, [_u64]),
+    "pv_copy_shim": (ctypes.c_int, [_p, _u64, _p, _p, _p, _u64, _p, _u64, _p, _p, _p, _p, _p, _p, _u64, _p]),
     "pv_result_encode": (ctypes.c_int, [_p, _u64, _p, _p, _p, _p, _u64, _p, _p, _p]),
     "pv_result_decode": (ctypes.c_int, [_p, _u64, _p, _u64, _p, _p, _p]),
     "pv_copy_ordered": (ctypes.c_int, [_p, _u64, _p, _u64, _p, _u64, _p, _p, _p, _p, _p, _p, _p, _p, _u64, _p]),

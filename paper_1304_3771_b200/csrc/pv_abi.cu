@@ -24,6 +24,10 @@ cudaError_t launch_copy_exec(uint8_t*, uint64_t, const pv_op*, uint64_t, const u
                              const uint64_t*, const uint32_t*, const uint64_t*, const uint64_t*, uint8_t*,
                              pv_op_result*, uint8_t*, const uint32_t*, cudaStream_t);
 size_t fifo_scratch_bytes(uint64_t, uint64_t, uint32_t);
+size_t shim_scratch_bytes(uint64_t);
+cudaError_t launch_copy_shim(uint8_t*, uint64_t, const pv_space*, const pv_shim*, const pv_op*, uint64_t,
+                             const uint64_t*, uint64_t, uint64_t*, uint32_t*, uint64_t*, uint8_t*, uint64_t*,
+                             void*, cudaStream_t);
 size_t ordered_scratch_bytes(uint64_t, uint64_t);
 cudaError_t launch_result_encode(uint8_t*, uint64_t, const uint64_t*, const uint32_t*, const uint8_t*, const uint64_t*,
                                  uint64_t, uint32_t*, uint8_t*, cudaStream_t);
@@ -255,6 +259,21 @@ int pv_copy_fifo_replay(const pv_op* ops, const uint64_t* page_off, const uint64
   return rc(launch_fifo_copy_abi(ops, page_off, look_page, look_op, proc_off, win_off, n_procs, capacity, fifo,
                                  image_bytes, page_hpa, page_status, op_first_bad, scratch, scratch_bytes,
                                  (cudaStream_t)stream));
+}
+
+uint64_t pv_copy_shim_scratch_bytes(uint64_t n_pages) { return shim_scratch_bytes(n_pages); }
+
+int pv_copy_shim(uint8_t* image, uint64_t image_bytes, const pv_space* spaces, const pv_shim* shims, const pv_op* ops,
+                 uint64_t n_ops, const uint64_t* page_off, uint64_t n_pages, uint64_t* page_hpa,
+                 uint32_t* page_status, uint64_t* op_first_bad, uint8_t* dirty, uint64_t* n_written,
+                 void* scratch, uint64_t scratch_bytes, void* stream) {
+  if (n_pages == 0) return PV_SUCCESS;
+  if (!image || !spaces || !shims || !ops || !page_off || !page_hpa || !page_status || !op_first_bad || !scratch ||
+      n_ops == 0)
+    return PV_EINVAL;
+  if (image_bytes % kPageSize || scratch_bytes < shim_scratch_bytes(n_pages)) return PV_EINVAL;
+  return rc(launch_copy_shim(image, image_bytes, spaces, shims, ops, n_ops, page_off, n_pages, page_hpa, page_status,
+                             op_first_bad, dirty, n_written, scratch, (cudaStream_t)stream));
 }
 
 uint64_t pv_copy_ordered_scratch_bytes(uint64_t n_pages, uint64_t image_bytes) {

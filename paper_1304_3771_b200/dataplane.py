@@ -49,6 +49,23 @@ class Space:
         return [self.s1_base, self.s1_root_pfn, self.s2_root_pfn, self.mode]
 
 
+@dataclass(frozen=True)
+class Shim:
+    """The default trap shim of one hybrid space (pv_shim): the guest
+    process whose shadow leaves it re-syncs (backend.py:288-296)."""
+
+    guest_base: int
+    guest_bytes: int
+    guest_root_pfn: int
+    shadow_root_pfn: int
+
+    def words(self) -> list[int]:
+        return [self.guest_base, self.guest_bytes, self.guest_root_pfn, self.shadow_root_pfn]
+
+
+NO_SHIM = Shim(0, 0, 0, 0)
+
+
 def _i64(values) -> np.ndarray:
     """uint64 bit patterns as an int64 array (torch has no uint64 math)."""
     return np.asarray(values, dtype=np.uint64).view(np.int64)
@@ -536,10 +553,12 @@ def page_spans(gva: np.ndarray, length: np.ndarray) -> np.ndarray:
 class CopyPlan:
     """Device-resident descriptors of a copy batch (reusable across runs)."""
 
-    def __init__(self, spaces: list[Space], ops: np.ndarray, *, fifo_groups=None):
+    def __init__(self, spaces: list[Space], ops: np.ndarray, *, fifo_groups=None, shims=None):
         """``ops``: uint64 rows (gva, len, buf_off, space).  ``fifo_groups``:
         optional list of lists of op indices, one per process whose
-        TranslationCache applies (program order)."""
+        TranslationCache applies (program order).  ``shims``: optional
+        :class:`Shim` (or None) per space -- the hybrid resolver's trap shim
+        runs on the device for those spaces (pv_copy_shim)."""
         import torch
 
         ops = np.ascontiguousarray(ops, dtype=np.uint64).reshape(-1, 4)
@@ -560,6 +579,10 @@ class CopyPlan:
         self.first_bad = torch.empty(max(self.n_ops, 1), dtype=torch.int64, device="cuda")
         self.results = torch.empty((max(self.n_ops, 1), 4), dtype=torch.int64, device="cuda")
         self.conflict = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self.shims = None
+        if shims is not None and any(sh is not None for sh in shims):
+            self.shims = _to_dev(_i64([(sh or NO_SHIM).words() for sh in shims]).reshape(-1, 4))
+            self.shim_written = torch.zeros(1, dtype=torch.int64, device="cuda")
         self.fifo_groups = fifo_groups
         if fifo_groups is not None:
             # lookup stream: the pages of each process's ops, op order, page order
@@ -616,6 +639,19 @@ def _owner_map(image):
     return image._owner, image._epoch
 
 
+def _shim_scratch(image, n_pages: int):
+    """Per-image zero-filled scratch of pv_copy_shim (grown on demand; every
+    call leaves it zero-filled)."""
+    import torch
+
+    need = int(N.lib().pv_copy_shim_scratch_bytes(n_pages))
+    cur = getattr(image, "_shim_scratch", None)
+    if cur is None or cur.numel() < need:
+        cur = torch.zeros(need, dtype=torch.uint8, device="cuda")
+        image._shim_scratch = cur
+    return cur
+
+
 def copy_launch(image, plan: CopyPlan, direction: int, buf, *, fifo_dev=None, fifo_cap: int = 10,
                 detect_conflicts: bool = True, track_dirty: bool = True) -> None:
     """Enqueue plan (+ FIFO replay) (+ conflict stamp) + exec on the current
@@ -633,6 +669,13 @@ def copy_launch(image, plan: CopyPlan, direction: int, buf, *, fifo_dev=None, fi
                                  plan.n_ops, plan.page_off.data_ptr(), plan.n_pages, direction,
                                  plan.page_hpa.data_ptr(), plan.page_status.data_ptr(), plan.page_aux.data_ptr(),
                                  plan.first_bad.data_ptr(), None, 0, None, s), "pv_copy_plan")
+        if plan.shims is not None:
+            scratch = _shim_scratch(image, plan.n_pages)
+            N.check(lib.pv_copy_shim(dev_img.data_ptr(), image.nbytes, plan.spaces.data_ptr(), plan.shims.data_ptr(),
+                                     plan.ops.data_ptr(), plan.n_ops, plan.page_off.data_ptr(), plan.n_pages,
+                                     plan.page_hpa.data_ptr(), plan.page_status.data_ptr(), plan.first_bad.data_ptr(),
+                                     image.dirty_map().data_ptr(), plan.shim_written.data_ptr(), scratch.data_ptr(),
+                                     scratch.numel(), s), "pv_copy_shim")
         if fifo_dev is not None and plan.fifo_lookups:
             cap = fifo_cap
             if plan.fifo_scratch is None or plan.fifo_cap != cap:
@@ -705,7 +748,7 @@ def copy_ordered(image, plan: CopyPlan, buf) -> None:
 
 
 def copy_ops(image, spaces: list[Space], ops: np.ndarray, direction: int, buf, *, caches=None, fifo_groups=None,
-             detect_conflicts: bool = True) -> list[OpOutcome]:
+             detect_conflicts: bool = True, shims=None) -> list[OpOutcome]:
     """Run a batch of copies with the reference's sequential semantics.
 
     ``caches`` (with ``fifo_groups``) are host TranslationCache objects whose
@@ -715,12 +758,14 @@ def copy_ops(image, spaces: list[Space], ops: np.ndarray, direction: int, buf, *
     (:func:`copy_ordered`), which reproduces last-writer-wins exactly.
     """
     cap = fifo_capacity(caches) if caches is not None else 10
-    plan = CopyPlan(spaces, ops, fifo_groups=fifo_groups if caches is not None else None)
+    plan = CopyPlan(spaces, ops, fifo_groups=fifo_groups if caches is not None else None, shims=shims)
     fifo_dev = _to_dev(pack_fifo(caches)) if caches is not None else None
     copy_launch(image, plan, direction, buf, fifo_dev=fifo_dev, fifo_cap=cap, detect_conflicts=detect_conflicts)
     if direction == N.TO_GUEST and detect_conflicts and int(plan.conflict.item()):
         copy_ordered(image, plan, buf)
     results = decode_results(plan.results.cpu().numpy())
+    if plan.shims is not None and int(plan.shim_written.item()):
+        image.note_device_write()  # the shim rewrote shadow leaves
     if caches is not None:
         unpack_fifo(fifo_dev.cpu().numpy(), caches)
     return results

@@ -120,14 +120,16 @@ class _BatchMixin:
         if not hasattr(tr, "_on_trap"):
             outs = dp.copy_ops(image, [space], rows, direction, buf, caches=caches, fifo_groups=groups)
             return [_decode_outcome(o, r, image.nbytes) for o, r in zip(outs, rows)]
-        # Hybrid resolver: a trap changes the shadow table for every later
-        # page, so the batch is cut at the first trapped op, which finishes
-        # through the per-op shim loop, and the rest is re-planned.
+        # Hybrid resolver: the device runs the default shim for every trap it
+        # can resolve exactly (pv_copy_shim).  Any other trap changes the
+        # shadow table for every later page on the host, so the batch is cut
+        # at that op, which finishes through the per-op shim loop, and the
+        # rest is re-planned.
         results = []
         start = 0
         while start < len(rows):
             part = rows[start:]
-            outs = dp.copy_ops(image, [space], part, direction, buf)
+            outs = dp.copy_ops(image, [space], part, direction, buf, shims=[tr.device_shim])
             cut = next((i for i, o in enumerate(outs) if dp.kind(o.status) in (N.ST_TRAP, N.ST_TRAP2)), None)
             upto = len(outs) if cut is None else cut
             for o, r in zip(outs[:upto], part[:upto]):
@@ -250,6 +252,17 @@ class _HybridResolver:
     @property
     def device_space(self) -> dp.Space:
         return dp.Space(self._memv.host_mem.base, self._record.active_hybrid.root_pfn, 0, N.ONE_STAGE)
+
+    @property
+    def device_shim(self):
+        """The default shim as the device runs it (pv_copy_shim), or None when
+        the record's shim was replaced (then traps go to the host per op)."""
+        rec = self._record
+        if "trap_shim" in rec.__dict__ or type(rec).trap_shim is not GuestProcessRecord.trap_shim:
+            return None
+        space, memv = rec.space, self._memv
+        base = memv.guest_base_offset(rec.guest_id)
+        return dp.Shim(base, space.guest.mem.size_bytes, space.guest_root.root_pfn, space.shadow_root.root_pfn)
 
     def _count(self, n: int) -> None:
         self._record.hw_translations += n

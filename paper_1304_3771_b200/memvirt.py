@@ -962,7 +962,8 @@ def _copy_device(direction, gva, length, buf, translator, host_mem, space, first
         cur_op[0, 0] = (gva + done) & dp.U64
         cur_op[0, 1] = length - done
         cur_op[0, 2] = done
-        out = dp.copy_ops(image, [space], cur_op, d, buf, caches=caches, fifo_groups=groups)[0]
+        out = dp.copy_ops(image, [space], cur_op, d, buf, caches=caches, fifo_groups=groups,
+                          shims=[getattr(translator, "device_shim", None)])[0]
         count = getattr(translator, "_count", None)
         if out.status == N.ST_OK:
             if count is not None:

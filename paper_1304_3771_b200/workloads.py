@@ -128,6 +128,12 @@ def c5_hybrid_space(world: C5World, g: int, p: int) -> dp.Space:
     return dp.Space(0, world.hybrid_roots[g][p].root_pfn)
 
 
+def c5_shim(world: C5World, g: int, p: int) -> dp.Shim:
+    """The default trap shim of process p of guest g (backend.py:288-296)."""
+    sp = world.spaces[g][p]
+    return dp.Shim(sp.guest.base_hpa, sp.guest.mem.size_bytes, sp.guest_root.root_pfn, sp.shadow_root.root_pfn)
+
+
 def c5_vas(cfg: C5Config, guest: int) -> list[np.ndarray]:
     """Per process of ``guest``: uniform random u32 VAs over its mapped region."""
     rng = np.random.default_rng(cfg.seed * 1000 + guest)

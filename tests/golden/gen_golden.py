@@ -104,6 +104,13 @@ def main(src: str) -> None:
         )
         with open(os.path.join(HERE, f"c1_{mode}.json"), "w") as f:
             json.dump(meta, f)
+    w = S.shim_build(mv, be, er)
+    build_sha = S.sha(S.image_bytes(w["memv"].host_mem))
+    res = S.shim_query(w, mv, be, er)
+    with open(os.path.join(HERE, "shim.json"), "w") as f:
+        json.dump(dict(res, build_sha=build_sha, shadow_root=w["p0"].shadow_root.root_pfn,
+                       guest_root=w["p0"].guest_root.root_pfn, guest_base=w["g0"].base_hpa,
+                       guest_bytes=w["g0"].mem.size_bytes, hybrid_root=w["rec"].active_hybrid.root_pfn), f)
     with open(os.path.join(HERE, "resultpage.json"), "w") as f:
         json.dump({"expected": S.resultpage_query(load_resultpage())}, f)
     print("golden fixtures written to", HERE)

@@ -373,3 +373,76 @@ def resultpage_query(rp):
     except ValueError:
         out.append("ValueError")
     return out
+
+
+# ---- scenario "shim": the hybrid resolver's default trap shim (backend.py:117-128,
+# 288-296; memvirt.py:685-696) over every kind of trapping shadow entry
+
+ALIAS = 0x2C00_0000   # its shadow mid entry is made to share BUF's leaf node
+NOGUEST = 0x3000_0000  # shadow-only trapping leaf: the shim's guest walk faults
+MIDTRAP = 0x2800_0000  # trapping shadow mid entry: the retry traps again
+
+
+def shim_build(mv, be, er):
+    memv = mv.MemoryVirtualizer()
+    g0 = memv.add_guest(0, "shadow")
+    p0 = memv.create_process(g0)
+    memv.map_region(p0, BUF, 64)
+    memv.map_region(p0, ALIAS, 64)
+    memv.map_region(p0, MIDTRAP, 4)
+    host = memv.host_mem
+    sh = mv.TableEditor(host, p0.shadow_root, memv.host_alloc.alloc)
+    for k in (3, 4, 5, 17, 30, 31, 32, 40, 50, 60):
+        sh.set_leaf_state(BUF + k * PAGE, mv.EntryState.TRAPPING)
+    # ALIAS's shadow mid entry -> BUF's leaf node (two paths to one slot)
+    top = host.read_word(p0.shadow_root.root_pfn, 0)
+    mid_node = top >> 12
+    host.write_word(mid_node, (ALIAS >> 21) & 0x1FF, host.read_word(mid_node, (BUF >> 21) & 0x1FF))
+    # a shadow-only trapping leaf (no guest mapping behind it)
+    sh.map(NOGUEST, 0x1234, state=mv.EntryState.TRAPPING)
+    # a trapping mid entry
+    host.write_word(mid_node, (MIDTRAP >> 21) & 0x1FF, host.read_word(mid_node, (MIDTRAP >> 21) & 0x1FF) | 0x4)
+    # BUF page 40: the guest maps it past the slot (gpa_to_hpa: OutOfRange)
+    gm = g0.mem
+    groot = p0.guest_root.root_pfn
+    gmid = gm.read_word(groot, 0) >> 12
+    gleaf = gm.read_word(gmid, (BUF >> 21) & 0x1FF) >> 12
+    gm.write_word(gleaf, 40, ((g0.mem.size_bytes >> 12) + 7) << 12 | 0x3)
+    rec = be.GuestProcessRecord(_Guest(0, "shadow"), p0, memv)
+    return dict(memv=memv, p0=p0, g0=g0, rec=rec)
+
+
+SHIM_OPS = [  # (direction, gva, length)
+    ("to", ALIAS + 5 * PAGE + 7, 100),      # first reach of the shared slot: fixed from ALIAS's guest page
+    ("to", BUF + 2 * PAGE + 100, 4 * PAGE),  # 3, 4 simple traps; 5 reads ALIAS's fix
+    ("from", BUF + 3 * PAGE, 2 * PAGE + 9),
+    ("to", BUF + 16 * PAGE, 3 * PAGE),
+    ("to", NOGUEST + 8, 64),                # shim: walk_guest faults -> PageFault(page va)
+    ("to", BUF + 29 * PAGE + 5, 5 * PAGE),
+    ("to", MIDTRAP + PAGE, 100),            # retry traps at level 2 -> TrapFixupFailed
+    ("to", BUF + 39 * PAGE, 2 * PAGE),      # shim: gpa past the slot -> OutOfRange
+    ("to", BUF + 50 * PAGE - 10, 20),
+    ("from", BUF + 49 * PAGE, 3 * PAGE),
+    ("to", BUF + 70 * PAGE, 10),            # not present
+    ("to", BUF + 5 * PAGE, 10),
+    ("to", BUF + 59 * PAGE + 1, 2 * PAGE),  # 60 trap, 61 ok
+    ("from", ALIAS + 4 * PAGE, 3 * PAGE),
+]
+
+
+def shim_payload(i: int, n: int) -> bytes:
+    return _payload(n, 5000 + i)
+
+
+def shim_query(w, mv, be, er):
+    memv, rec = w["memv"], w["rec"]
+    acc = be.HardwareHasAccess(rec, memv)
+    rows = []
+    for i, (d, gva, n) in enumerate(SHIM_OPS):
+        if d == "to":
+            data = shim_payload(i, n)
+            rows.append(outcome(lambda: acc.copy_to_user(gva, data), er))
+        else:
+            rows.append(outcome(lambda: int.from_bytes(hashlib.sha256(acc.copy_from_user(gva, n)).digest()[:8],
+                                                       "little"), er))
+    return dict(rows=rows, hw_translations=rec.hw_translations, image_sha=sha(image_bytes(memv.host_mem)))

@@ -188,3 +188,46 @@ def test_resultpage_codec_matches_reference():
 
     assert S.resultpage_query(rp) == load_json("resultpage.json")["expected"]
     assert rp.HEADER_BYTES == 36 and rp.BLOB_CAPACITY == 4060
+
+
+def _shim_oracle_rows(w, ops):
+    """Run ops through the oracle's hybrid copy with the default shim; rows in
+    the scenario's outcome format, up to the first op outside the restated
+    subset (returned as the cut)."""
+    import hashlib as hl
+
+    memv, rec = w["memv"], w["rec"]
+    img = np.frombuffer(memv.host_mem.read(0, memv.host_mem.size_bytes), dtype=np.uint8).copy()
+    sp = O.space(0, rec.active_hybrid.root_pfn)
+    g0, p0 = w["g0"], w["p0"]
+    shim = np.array([g0.base_hpa, g0.mem.size_bytes, p0.guest_root.root_pfn, p0.shadow_root.root_pfn], np.uint64)
+    rows, total = [], 0
+    for i, (d, gva, n) in enumerate(ops):
+        buf = np.frombuffer(S.shim_payload(i, n), dtype=np.uint8).copy() if d == "to" else np.zeros(n, np.uint8)
+        op = np.array([[gva, n, 0, 0]], np.uint64)
+        res, cut, cnt = O.copy_hybrid(img, sp, shim, op, buf if n else np.zeros(1, np.uint8), 0 if d == "to" else 1)
+        total += cnt
+        if cut == 0:
+            return rows, i, img, total
+        st = int(res[0, 3]) & 0xFFFFFFFF
+        if st == 0:
+            rows.append(["ok", n if d == "to" else
+                         int.from_bytes(hl.sha256(buf.tobytes()).digest()[:8], "little")])
+        else:
+            rows.append(status_outcome(st, int(res[0, 1]), int(res[0, 2]), 0)[:3] + [int(res[0, 0])])
+    return rows, len(ops), img, total
+
+
+def test_shim_build_bytes_and_oracle():
+    """The shim scenario's world is byte-identical to the reference's, and the
+    oracle's restatement of the default trap shim gives the reference's
+    outcomes for every op it covers (simple leaf traps, a slot reached through
+    two shadow paths); it stops at the first shim that would raise."""
+    w = S.shim_build(mv, be, er)
+    g = load_json("shim.json")
+    assert sha_of(w["memv"].host_mem) == g["build_sha"]
+    be.HardwareHasAccess(w["rec"], w["memv"])  # activates the hybrid root
+    assert w["rec"].active_hybrid.root_pfn == g["hybrid_root"]
+    rows, cut, _, _ = _shim_oracle_rows(w, S.SHIM_OPS)
+    assert cut == 4  # NOGUEST: the shim's guest walk faults (host-side)
+    assert rows == g["rows"][:cut]
