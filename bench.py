@@ -139,7 +139,7 @@ class Workload:
         if name == "c5":
             cfg = W.C5Config() if scale == 1 else W.C5Config().scaled(scale)
             self.cfg = cfg
-            wd = W.build_c5(cfg)
+            wd = W.build_c5(cfg, device=True)  # tables built in HBM (pv_map_*)
             self.world = wd
             self.memv = wd.memv
             owned = shard.owned_guests(cfg.guests, rank, world)

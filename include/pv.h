@@ -345,6 +345,44 @@ int pv_copy_shim(uint8_t* image, uint64_t image_bytes, const pv_space* spaces, c
                  uint8_t* dirty, uint64_t* n_written, void* scratch, uint64_t scratch_bytes,
                  void* stream);
 
+/* ---- batched table construction --------------------
+ * n calls of TableEditor(mem, root, alloc).map(vas[i], target_i) in order
+ * (memvirt.py:270-313) on the image window at byte `base` (host memory: 0;
+ * a guest memory: its slot base), node frames drawn from a FIFO frame
+ * allocator (memvirt.py:191-213); with data_first, every page first draws its
+ * own data frame from the same allocator and maps it (map_process_page /
+ * map_region, memvirt.py:508-526: frame order per page [data][mid?][leaf?]).
+ *
+ * pv_map_plan: need[i] (device u8) = bit 0 "page i allocates the mid node of
+ * its top entry", bit 1 "page i allocates the leaf node of its (top, mid)
+ * entry".  *bad (device u64; the caller sets it to all-ones) is lowered to
+ * the first page the batch cannot build exactly -- its leaf entry is not
+ * NOT_PRESENT (AlreadyMapped), an existing node lies past the image
+ * (struct.error), or it repeats the (top, mid, leaf) slot of an earlier page
+ * -- in which case the caller runs the reference's per-page loop instead.
+ * vas (device u64) must be page aligned.  scratch: pv_map_scratch_bytes().
+ *
+ * pv_map_commit: frames (device u64, n_frames) = the allocator's frames in
+ * allocation order, frame_off[i] (device u64) = exclusive prefix sum over
+ * pages of (data_first + popcount(need[i])).  Frames j with hot[j] != 0
+ * (device u8, may be NULL) or whose page is marked in dirty are zeroed
+ * (FrameAllocator.alloc zeroes; never-written frames are already zero).  The
+ * leaf entry of page i becomes (target << 12) | leaf_flags with target =
+ * frames[frame_off[i]] + target_add (data_first; the data frame is also
+ * stored to out_data[i] when out_data != NULL) or targets[i] + target_add;
+ * new nodes are installed PRESENT | writable.  dirty (device, one byte per
+ * image page, may be NULL) is set for every page written. */
+uint64_t pv_map_scratch_bytes(void);
+int pv_map_plan(const uint8_t* image, uint64_t image_bytes, uint64_t base, uint64_t root_pfn,
+                const uint64_t* vas, uint64_t n, uint8_t* need, uint64_t* bad,
+                void* scratch, void* stream);
+int pv_map_commit(uint8_t* image, uint64_t image_bytes, uint64_t base, uint64_t root_pfn,
+                  const uint64_t* vas, uint64_t n, const uint8_t* need,
+                  const uint64_t* frames, uint64_t n_frames, const uint64_t* frame_off,
+                  const uint8_t* hot, uint32_t data_first, const uint64_t* targets,
+                  uint64_t target_add, uint64_t leaf_flags, uint64_t* out_data,
+                  uint8_t* dirty, void* stream);
+
 /* ---- result-page codec ------------------------------
  * Batched resultpage.encode + the backend's host_mem.write of the record
  * (resultpage.py:44-51, backend.py:352-355): record r is header[9*r ..

@@ -64,6 +64,7 @@ EXPORTS = (
     "pv_copy_fifo_replay", "pv_scatter_pages", "pv_gather_pages", "pv_stream_sync", "pv_index_encode",
     "pv_fifo_scratch_bytes", "pv_copy_ordered_scratch_bytes", "pv_copy_ordered", "pv_result_encode",
     "pv_result_decode", "pv_timing", "pv_timing_ms", "pv_copy_shim_scratch_bytes", "pv_copy_shim",
+    "pv_map_scratch_bytes", "pv_map_plan", "pv_map_commit",
 )
 
 _u64 = ctypes.c_uint64
@@ -80,6 +81,10 @@ _SIGNATURES = {
     "pv_fifo_scratch_bytes": (_u64, [_u64, _u64, _u32]),
     "pv_copy_ordered_scratch_bytes": (_u64, [_u64, _u64]),
     "pv_copy_shim_scratch_bytes": (_u64, [_u64]),
+    "pv_map_scratch_bytes": (_u64, []),
+    "pv_map_plan": (ctypes.c_int, [_p, _u64, _u64, _u64, _p, _u64, _p, _p, _p, _p]),
+    "pv_map_commit": (ctypes.c_int, [_p, _u64, _u64, _u64, _p, _u64, _p, _p, _u64, _p, _p, _u32, _p, _u64, _u64, _p,
+                                     _p, _p]),
     "pv_copy_shim": (ctypes.c_int, [_p, _u64, _p, _p, _p, _u64, _p, _u64, _p, _p, _p, _p, _p, _p, _u64, _p]),
     "pv_result_encode": (ctypes.c_int, [_p, _u64, _p, _p, _p, _p, _u64, _p, _p, _p]),
     "pv_result_decode": (ctypes.c_int, [_p, _u64, _p, _u64, _p, _p, _p]),

@@ -25,6 +25,12 @@ cudaError_t launch_copy_exec(uint8_t*, uint64_t, const pv_op*, uint64_t, const u
                              pv_op_result*, uint8_t*, const uint32_t*, cudaStream_t);
 size_t fifo_scratch_bytes(uint64_t, uint64_t, uint32_t);
 size_t shim_scratch_bytes(uint64_t);
+size_t map_scratch_bytes();
+cudaError_t launch_map_plan(const uint8_t*, uint64_t, uint64_t, uint64_t, const uint64_t*, uint64_t, uint8_t*,
+                            uint64_t*, void*, cudaStream_t);
+cudaError_t launch_map_commit(uint8_t*, uint64_t, uint64_t, uint64_t, const uint64_t*, uint64_t, const uint8_t*,
+                              const uint64_t*, uint64_t, const uint64_t*, const uint8_t*, uint32_t, const uint64_t*,
+                              uint64_t, uint64_t, uint64_t*, uint8_t*, cudaStream_t);
 cudaError_t launch_copy_shim(uint8_t*, uint64_t, const pv_space*, const pv_shim*, const pv_op*, uint64_t,
                              const uint64_t*, uint64_t, uint64_t*, uint32_t*, uint64_t*, uint8_t*, uint64_t*,
                              void*, cudaStream_t);
@@ -274,6 +280,29 @@ int pv_copy_shim(uint8_t* image, uint64_t image_bytes, const pv_space* spaces, c
   if (image_bytes % kPageSize || scratch_bytes < shim_scratch_bytes(n_pages)) return PV_EINVAL;
   return rc(launch_copy_shim(image, image_bytes, spaces, shims, ops, n_ops, page_off, n_pages, page_hpa, page_status,
                              op_first_bad, dirty, n_written, scratch, (cudaStream_t)stream));
+}
+
+uint64_t pv_map_scratch_bytes(void) { return map_scratch_bytes(); }
+
+int pv_map_plan(const uint8_t* image, uint64_t image_bytes, uint64_t base, uint64_t root_pfn, const uint64_t* vas,
+                uint64_t n, uint8_t* need, uint64_t* bad, void* scratch, void* stream) {
+  if (n == 0) return PV_SUCCESS;
+  if (!image || !vas || !need || !bad || !scratch || image_bytes % kPageSize || base % kPageSize) return PV_EINVAL;
+  if (n >= 0xFFFFFFFFull) return PV_EINVAL;
+  return rc(launch_map_plan(image, image_bytes, base, root_pfn, vas, n, need, bad, scratch, (cudaStream_t)stream));
+}
+
+int pv_map_commit(uint8_t* image, uint64_t image_bytes, uint64_t base, uint64_t root_pfn, const uint64_t* vas,
+                  uint64_t n, const uint8_t* need, const uint64_t* frames, uint64_t n_frames,
+                  const uint64_t* frame_off, const uint8_t* hot, uint32_t data_first, const uint64_t* targets,
+                  uint64_t target_add, uint64_t leaf_flags, uint64_t* out_data, uint8_t* dirty, void* stream) {
+  if (n == 0) return PV_SUCCESS;
+  if (!image || !vas || !need || !frame_off || image_bytes % kPageSize || base % kPageSize) return PV_EINVAL;
+  if (n_frames && !frames) return PV_EINVAL;
+  if (!data_first && !targets) return PV_EINVAL;
+  return rc(launch_map_commit(image, image_bytes, base, root_pfn, vas, n, need, frames, n_frames, frame_off, hot,
+                              data_first ? 1u : 0u, targets, target_add, leaf_flags, out_data, dirty,
+                              (cudaStream_t)stream));
 }
 
 uint64_t pv_copy_ordered_scratch_bytes(uint64_t n_pages, uint64_t image_bytes) {

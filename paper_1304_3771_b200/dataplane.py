@@ -771,3 +771,64 @@ def copy_ops(image, spaces: list[Space], ops: np.ndarray, direction: int, buf, *
     return results
 
 
+
+
+# ---- batched table construction (pv_map_plan / pv_map_commit) ------------------
+
+def _map_scratch(image):
+    import torch
+
+    if getattr(image, "_map_scratch", None) is None:
+        image._map_scratch = torch.empty(int(N.lib().pv_map_scratch_bytes()), dtype=torch.uint8, device="cuda")
+    return image._map_scratch
+
+
+class TableBuild:
+    """One table of a batched map on the device: the plan of ``vas`` (device
+    int64 tensor, page aligned) over the window at byte ``base`` with root
+    ``root_pfn`` (pv_map_plan).  ``need`` / ``bad`` / ``count`` stay on the
+    device until :meth:`stats` reads them."""
+
+    def __init__(self, image, base: int, root_pfn: int, vas):
+        import torch
+
+        lib = N.lib()
+        self.image, self.base, self.root, self.vas = image, base, root_pfn, vas
+        n = vas.numel()
+        dev = image.device()
+        self.need = torch.empty(n, dtype=torch.uint8, device="cuda")
+        self.bad = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+        N.check(lib.pv_map_plan(dev.data_ptr(), image.nbytes, base, root_pfn, vas.data_ptr(), n,
+                                self.need.data_ptr(), self.bad.data_ptr(), _map_scratch(image).data_ptr(),
+                                _stream().cuda_stream), "pv_map_plan")
+        self.nodes = (self.need & 1).to(torch.int64) + (self.need >> 1).to(torch.int64)
+
+    def summary(self):
+        """Device scalars (bad page or -1, node frames needed) for one sync."""
+        import torch
+
+        return torch.stack([self.bad[0], self.nodes.sum()])
+
+    def commit(self, frames: np.ndarray, *, data_first: bool, targets=None, target_add: int = 0,
+               leaf_flags: int = 0x3, out_data=None) -> None:
+        """Write the table given the frames drawn from the allocator (in
+        allocation order)."""
+        import torch
+
+        lib = N.lib()
+        image = self.image
+        dev = image.device()
+        per = self.nodes + (1 if data_first else 0)
+        frame_off = torch.cumsum(per, 0) - per
+        fr = _to_dev(frames.astype(np.int64)) if len(frames) else None
+        pages = (self.base >> PAGE_SHIFT) + frames
+        hot = image._maybe_nonzero[pages] if len(frames) else np.zeros(0, bool)
+        hot_d = _to_dev(hot.astype(np.uint8)) if hot.any() else None
+        N.check(lib.pv_map_commit(dev.data_ptr(), image.nbytes, self.base, self.root, self.vas.data_ptr(),
+                                  self.vas.numel(), self.need.data_ptr(), None if fr is None else fr.data_ptr(),
+                                  len(frames), frame_off.data_ptr(), None if hot_d is None else hot_d.data_ptr(),
+                                  1 if data_first else 0, None if targets is None else targets.data_ptr(), target_add,
+                                  leaf_flags, None if out_data is None else out_data.data_ptr(),
+                                  image.dirty_map().data_ptr(), _stream().cuda_stream), "pv_map_commit")
+        image.note_device_write()
+        image.host_epoch += 1  # table structure changed: leaf-index scans must look again

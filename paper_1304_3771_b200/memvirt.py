@@ -709,10 +709,68 @@ class MemoryVirtualizer:
                                  use_cache=use_cache)
 
 
+# Batches of at least this many pages are built on the device when the image
+# already lives there (pv_map_plan / pv_map_commit); smaller ones stay on the
+# host mirror.  PV_DEVICE_MAP=0 disables the device builder.
+DEVICE_MAP_MIN = 4096
+
+
+def _device_map_ok(mem: PhysMem, n: int) -> bool:
+    import os
+
+    return mem.backing.on_device and n >= DEVICE_MAP_MIN and os.environ.get("PV_DEVICE_MAP", "1") != "0"
+
+
+def _device_map(mem: PhysMem, root: PageTableRoot, alloc: FrameAllocator, vas: np.ndarray,
+                targets: np.ndarray, leaf_flags: int) -> bool:
+    """_bulk_map on the device; False (nothing changed) when the batch is not
+    exactly buildable there."""
+    tb = dp.TableBuild(mem.backing, mem.base, root.root_pfn, dp._to_dev(vas.astype(np.int64)))
+    bad, cnt = (int(x) for x in tb.summary().cpu().tolist())
+    if bad != -1 or cnt > alloc.free_count:
+        return False
+    tb.commit(alloc._take(cnt), data_first=False, targets=dp._to_dev(np.asarray(targets, dtype=np.int64)),
+              leaf_flags=leaf_flags)
+    return True
+
+
+def _device_process_map(memv: "MemoryVirtualizer", space: "ProcessSpace", gvas: np.ndarray) -> bool:
+    """map_process_page over ``gvas`` on the device (guest table with
+    data-first frames, then the shadow table); False when not applicable."""
+    import torch
+
+    guest = space.guest
+    vas = dp._to_dev(gvas.astype(np.int64))
+    gt = dp.TableBuild(guest.mem.backing, guest.mem.base, space.guest_root.root_pfn, vas)
+    parts = [gt.summary()]
+    st = None
+    if space.shadow_root is not None:
+        st = dp.TableBuild(memv.host_mem.backing, memv.host_mem.base, space.shadow_root.root_pfn, vas)
+        parts.append(st.summary())
+    stats = torch.cat(parts).cpu().tolist()
+    if any(int(b) != -1 for b in stats[0::2]):
+        return False
+    n = len(gvas)
+    if n + int(stats[1]) > guest.os_alloc.free_count:
+        return False
+    if st is not None and int(stats[3]) > memv.host_alloc.free_count:
+        return False
+    data = torch.empty(n, dtype=torch.int64, device="cuda")
+    gt.commit(guest.os_alloc._take(n + int(stats[1])), data_first=True, leaf_flags=FLAG_PRESENT | FLAG_WRITABLE,
+              out_data=data)
+    if st is not None:
+        st.commit(memv.host_alloc._take(int(stats[3])), data_first=False, targets=data,
+                  target_add=guest.base_hpa >> PAGE_SHIFT, leaf_flags=FLAG_PRESENT | FLAG_WRITABLE)
+    return True
+
+
 def _bulk_map(mem: PhysMem, root: PageTableRoot, alloc: FrameAllocator, vas: np.ndarray,
               targets: np.ndarray, leaf_flags: int) -> None:
     """TableEditor(mem, root, alloc.alloc).map(va, target) for each pair in
     order, vectorised (node frames are the only allocations)."""
+    if _device_map_ok(mem, len(vas)) and not (vas & PAGE_MASK).any() and \
+            _device_map(mem, root, alloc, vas, targets, leaf_flags):
+        return
     bm = _BulkMapper(mem, root.root_pfn, vas)
     if not _distinct_pages(vas) or not bm.plan():
         editor = TableEditor(mem, root, alloc.alloc)
@@ -748,7 +806,11 @@ def _split_node_frames(new_mid: np.ndarray, new_leaf: np.ndarray, frames: np.nda
 
 def _bulk_process_map(memv: MemoryVirtualizer, space: ProcessSpace, gvas: np.ndarray) -> bool:
     """Vectorised map_process_page over ``gvas``; False if not applicable."""
-    if not _distinct_pages(gvas) or (gvas & PAGE_MASK).any() or (gvas < 0).any():
+    if (gvas & PAGE_MASK).any() or (gvas < 0).any():
+        return False
+    if _device_map_ok(space.guest.mem, len(gvas)):
+        return _device_process_map(memv, space, gvas)
+    if not _distinct_pages(gvas):
         return False
     guest = space.guest
     gm = _BulkMapper(guest.mem, space.guest_root.root_pfn, gvas)

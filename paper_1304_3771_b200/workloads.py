@@ -97,11 +97,15 @@ class C5World:
     hybrid_roots: list = field(default_factory=list)  # [guest][proc] PageTableRoot
 
 
-def build_c5(cfg: C5Config) -> C5World:
+def build_c5(cfg: C5Config, device: bool = False) -> C5World:
     """The whole 8-guest world (every rank builds the same image, so hpas are
-    identical across ranks; a rank only touches its own guests' pages)."""
+    identical across ranks; a rank only touches its own guests' pages).
+    ``device``: allocate the HBM image first so the tables are built there
+    (pv_map_plan / pv_map_commit) instead of on the host mirror."""
     cls = type("C5Virtualizer", (mv.MemoryVirtualizer,), {"HOST_PRIVATE_BYTES": cfg.host_private})
     memv = cls(host_bytes=cfg.host_private + cfg.guests * cfg.guest_bytes)
+    if device:
+        memv.host_mem.backing.device()
     world = C5World(cfg, memv)
     for g in range(cfg.guests):
         guest = memv.add_guest(g, "shadow", cfg.guest_bytes)
