@@ -332,7 +332,8 @@ def run_ours(args, rank, world, local):
                           "peak": peak, "unit": "GB/s", "frac": walk_achieved / peak,
                           "traffic": traffic.get("translate"), "algorithmic_bytes_per_launch": walk_bytes,
                           "note": "16 B/translation (u32 VA in, u64 hpa + u32 status out); leaf-PTE gathers "
-                                  "are extra traffic"},
+                                  "are extra traffic",
+                          "gather_sol": walker_sol(wl.n_vas * K / (tr_ms / 1e3))},
         "faulting_lanes": n_faults,
         "gather_to_rank0": gather,
         "gpu_launches": (4 + (8 if wl.cplan.shims is not None else 0)) * K,
@@ -635,6 +636,18 @@ class _Prebuilt:
 
     def build(self, shadow_root, host_root):
         return self.root
+
+
+def walker_sol(lanes_per_s: float):
+    """The walker against the measured speed of light of its access pattern
+    (random 4-byte gathers + 16 B/lane stream; profiles/walker_sol.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "walker_sol.json")) as f:
+            sol = json.load(f)
+    except Exception:  # noqa: BLE001
+        return None
+    return {"achieved": lanes_per_s, "probe": sol["lanes_per_s"], "unit": "lanes/s",
+            "frac": lanes_per_s / sol["lanes_per_s"], "source": "profiles/walker_sol.json"}
 
 
 def load_traffic(workload: str) -> dict:

@@ -25,20 +25,32 @@ __device__ __forceinline__ uint32_t ld32(const uint32_t* p, uint64_t pol) {
   return v;
 }
 
-template <int MODE>
+// MODE 0: 4 B out; 1: walker-shaped 12 B out; 2: stream only.
+// SMEM: resolve the upper levels through an 8 KiB shared-memory code table
+// first (the walker's staged codes), L lanes per thread.
+template <int MODE, bool SMEM, int L>
 __global__ void __launch_bounds__(512, 2) k(const uint32_t* __restrict__ idx, const uint32_t* __restrict__ tab,
                                             uint32_t mask, uint64_t n, uint64_t* __restrict__ o64,
                                             uint32_t* __restrict__ o32) {
+  __shared__ uint32_t codes[2048];
+  if (SMEM) {
+    for (int i = threadIdx.x; i < 2048; i += blockDim.x) codes[i] = ((uint32_t)i * 2654435761u) | 1u;
+    __syncthreads();
+  }
   const uint64_t pf = pol_first(), pl = pol_last();
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * 8;
-  for (uint64_t base = ((uint64_t)blockIdx.x * blockDim.x) * 8 + threadIdx.x; base < n; base += stride) {
-    uint32_t v[8], r[8];
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * L;
+  for (uint64_t base = ((uint64_t)blockIdx.x * blockDim.x) * L + threadIdx.x; base < n; base += stride) {
+    uint32_t v[L], r[L];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) v[j] = ld32(idx + base + j * blockDim.x, pf);
+    for (int j = 0; j < L; ++j) v[j] = ld32(idx + base + j * blockDim.x, pf);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) r[j] = MODE == 2 ? v[j] : ld32(tab + (v[j] & mask), pl);
+    for (int j = 0; j < L; ++j) {
+      uint32_t a = v[j] & mask;
+      if (SMEM) a = (codes[(v[j] >> 9) & 2047] ^ v[j]) & mask;  // dependent, still uniform over the table
+      r[j] = MODE == 2 ? v[j] : ld32(tab + a, pl);
+    }
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < L; ++j) {
       const uint64_t i = base + j * blockDim.x;
       if (MODE == 0) {
         o32[i] = r[j];
@@ -70,23 +82,33 @@ int main() {
   cudaMemset(tab, 1, tab_words * 4);
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  const char* names[3] = {"gather, 4 B out", "gather, walker-shaped 12 B out", "stream only, 16 B/lane"};
-  for (int mode = 0; mode < 3; ++mode) {
-    auto fn = mode == 0 ? k<0> : mode == 1 ? k<1> : k<2>;
+  struct Case {
+    const char* name;
+    void (*fn)(const uint32_t*, const uint32_t*, uint32_t, uint64_t, uint64_t*, uint32_t*);
+  };
+  const Case cases[] = {
+      {"gather, 4 B out, 8/thr", k<0, false, 8>},
+      {"gather, walker 12 B out, 8/thr", k<1, false, 8>},
+      {"stream only, 16 B/lane, 8/thr", k<2, false, 8>},
+      {"gather+smem codes, walker, 8/thr", k<1, true, 8>},
+      {"gather, walker, 4/thr", k<1, false, 4>},
+      {"gather+smem codes, walker, 4/thr", k<1, true, 4>},
+  };
+  for (const Case& c : cases) {
     for (int grid_mul = 2; grid_mul <= 4; grid_mul += 2) {
       cudaEvent_t a, b;
       cudaEventCreate(&a);
       cudaEventCreate(&b);
-      for (int w = 0; w < 3; ++w) fn<<<sms * grid_mul, 512>>>(idx, tab, (uint32_t)tab_words - 1, n, o64, o32);
+      for (int w = 0; w < 3; ++w) c.fn<<<sms * grid_mul, 512>>>(idx, tab, (uint32_t)tab_words - 1, n, o64, o32);
       cudaEventRecord(a);
       const int reps = 10;
-      for (int r = 0; r < reps; ++r) fn<<<sms * grid_mul, 512>>>(idx, tab, (uint32_t)tab_words - 1, n, o64, o32);
+      for (int r = 0; r < reps; ++r) c.fn<<<sms * grid_mul, 512>>>(idx, tab, (uint32_t)tab_words - 1, n, o64, o32);
       cudaEventRecord(b);
       cudaEventSynchronize(b);
       float ms = 0;
       cudaEventElapsedTime(&ms, a, b);
       ms /= reps;
-      printf("%-34s grid %3dx%d: %.3f ms  %.1f G lanes/s\n", names[mode], sms * grid_mul, 512, ms, n / ms / 1e6);
+      printf("%-36s grid %3dx%d: %.3f ms  %.1f G lanes/s\n", c.name, sms * grid_mul, 512, ms, n / ms / 1e6);
     }
   }
   printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
