@@ -35,8 +35,10 @@ C1_GVA = 0x1000_0000
 C1_PAGES = 16384
 
 
-def build_c1(mode: str = "shadow"):
+def build_c1(mode: str = "shadow", device: bool = False):
     memv = mv.MemoryVirtualizer(host_bytes=C1_HOST)
+    if device:
+        memv.host_mem.backing.device()  # tables built in HBM
     guest = memv.add_guest(0, mode, C1_GUEST)
     space = memv.create_process(guest)
     order = list(range(C1_PAGES))
