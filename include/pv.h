@@ -383,6 +383,61 @@ int pv_map_commit(uint8_t* image, uint64_t image_bytes, uint64_t base, uint64_t 
                   uint64_t target_add, uint64_t leaf_flags, uint64_t* out_data,
                   uint8_t* dirty, void* stream);
 
+/* ---- hypercall frame codec ---------------------------
+ * The forwarding wire format (hypercall.py): a FileOp is PV_FOP_WORDS u64
+ * words {kind, device_id, handle, gva, length, offset, flags, cmd, arg_gva,
+ * arg_len, prot, event_mask, timeout_ms, pid, access, vma_start, vma_length}
+ * (hypercall.py:62-79, field order); a frame is one opcode, six 32-bit slots,
+ * the issuing vCPU and the virtual CR3 (HypercallFrame, :92-101). */
+#define PV_FOP_WORDS 17
+typedef struct pv_frame {
+  uint32_t opcode;      /* FileOpKind, or 0x7F = continuation                 */
+  uint32_t args[6];     /* the six argument slots                              */
+  uint32_t vcpu;
+  uint64_t virtual_cr3;
+} pv_frame;
+
+/* per-op / per-frame outcome */
+#define PV_FRAME_OK 0u               /* packed / identified / op decoded here    */
+#define PV_FRAME_PENDING 1u          /* page-fault first frame still waiting     */
+#define PV_FRAME_CONSUMED 2u         /* first frame completed by a later frame   */
+#define PV_FRAME_UNPACKABLE 3u       /* Unpackable: layout word >= 2^32; bits
+                                        8-15 = FileOp field index (pack)          */
+#define PV_FRAME_BAD_KIND 4u         /* not a FileOpKind (ValueError)            */
+#define PV_FRAME_ORPHAN 5u           /* Unpackable: continuation without a first */
+#define PV_FRAME_DUP_FIRST 6u        /* Unpackable: second first-frame           */
+#define PV_FRAME_UNKNOWN_VCPU 7u     /* UnknownVcpu (identify)                   */
+#define PV_FRAME_UNKNOWN_PROCESS 8u  /* UnknownProcess (identify)                */
+
+/* pack (hypercall.py:125-137) for n ops (device, n x PV_FOP_WORDS u64):
+ * op i writes its frames at frames[frame_off[i]] (frame_off = exclusive scan
+ * of 2 for PAGE_FAULT, else 1); vcpu / cr3 / tag are per-op device u64
+ * arrays (tag: page faults only).  status[i] (device u32) per op; a failing
+ * op writes no frame. */
+int pv_frame_pack(const uint64_t* ops, uint64_t n, const uint64_t* vcpu, const uint64_t* cr3,
+                  const uint64_t* tag, const uint64_t* frame_off, pv_frame* frames,
+                  uint32_t* status, void* stream);
+/* VcpuRegistry.identify (hypercall.py:178-211) per frame: vcpu_guest[v]
+ * (device i32, n_vcpus entries, -1 = unregistered) and the registry of
+ * processes sorted by (reg_guest, reg_cr3) (device u64 arrays, n_reg
+ * entries).  record[i] = index of the frame's process in the registry;
+ * status[i] = PV_FRAME_OK / UNKNOWN_VCPU / UNKNOWN_PROCESS. */
+int pv_frame_identify(const pv_frame* frames, uint64_t n, const int32_t* vcpu_guest,
+                      uint32_t n_vcpus, const uint64_t* reg_guest, const uint64_t* reg_cr3,
+                      uint32_t n_reg, uint32_t* record, uint32_t* status, void* stream);
+/* FrameAssembler.feed (hypercall.py:155-175) over a batch in frame order,
+ * after pv_frame_identify (frames whose status is not PV_FRAME_OK are
+ * skipped, as the reference raises before feeding them).  Frame i that
+ * completes an operation gets PV_FRAME_OK and the op at ops_out[i *
+ * PV_FOP_WORDS]; pending frames are keyed by (record, tag).  Equal to
+ * feeding the frames one by one, each error caught.  SYNCHRONISES `stream`
+ * once (the size of the pairing set).  scratch: device memory of
+ * pv_frame_assemble_scratch_bytes(n) bytes. */
+uint64_t pv_frame_assemble_scratch_bytes(uint64_t n);
+int pv_frame_assemble(const pv_frame* frames, uint64_t n, const uint32_t* record,
+                      uint64_t* ops_out, uint32_t* status, void* scratch,
+                      uint64_t scratch_bytes, void* stream);
+
 /* ---- result-page codec ------------------------------
  * Batched resultpage.encode + the backend's host_mem.write of the record
  * (resultpage.py:44-51, backend.py:352-355): record r is header[9*r ..

@@ -48,6 +48,11 @@ TO_GUEST = 0
 FROM_GUEST = 1
 COPY_ALIGNED16 = 0x100
 
+FOP_WORDS = 17     # FileOp words (kind + 16 fields), pv.h PV_FOP_WORDS
+FRAME_BYTES = 40   # sizeof(pv_frame)
+FRAME_OK, FRAME_PENDING, FRAME_CONSUMED, FRAME_UNPACKABLE, FRAME_BAD_KIND = 0, 1, 2, 3, 4
+FRAME_ORPHAN, FRAME_DUP_FIRST, FRAME_UNKNOWN_VCPU, FRAME_UNKNOWN_PROCESS = 5, 6, 7, 8
+
 FIFO_MAX = 32
 # struct sizes in 8-byte words (all structs are u64-aligned)
 SPACE_WORDS = 4    # pv_space
@@ -65,6 +70,7 @@ EXPORTS = (
     "pv_fifo_scratch_bytes", "pv_copy_ordered_scratch_bytes", "pv_copy_ordered", "pv_result_encode",
     "pv_result_decode", "pv_timing", "pv_timing_ms", "pv_copy_shim_scratch_bytes", "pv_copy_shim",
     "pv_map_scratch_bytes", "pv_map_plan", "pv_map_commit",
+    "pv_frame_pack", "pv_frame_identify", "pv_frame_assemble_scratch_bytes", "pv_frame_assemble",
 )
 
 _u64 = ctypes.c_uint64
@@ -82,6 +88,10 @@ _SIGNATURES = {
     "pv_copy_ordered_scratch_bytes": (_u64, [_u64, _u64]),
     "pv_copy_shim_scratch_bytes": (_u64, [_u64]),
     "pv_map_scratch_bytes": (_u64, []),
+    "pv_frame_pack": (ctypes.c_int, [_p, _u64, _p, _p, _p, _p, _p, _p, _p]),
+    "pv_frame_identify": (ctypes.c_int, [_p, _u64, _p, _u32, _p, _p, _u32, _p, _p, _p]),
+    "pv_frame_assemble_scratch_bytes": (_u64, [_u64]),
+    "pv_frame_assemble": (ctypes.c_int, [_p, _u64, _p, _p, _p, _p, _u64, _p]),
     "pv_map_plan": (ctypes.c_int, [_p, _u64, _u64, _u64, _p, _u64, _p, _p, _p, _p]),
     "pv_map_commit": (ctypes.c_int, [_p, _u64, _u64, _u64, _p, _u64, _p, _p, _u64, _p, _p, _u32, _p, _u64, _u64, _p,
                                      _p, _p]),

@@ -26,6 +26,13 @@ cudaError_t launch_copy_exec(uint8_t*, uint64_t, const pv_op*, uint64_t, const u
 size_t fifo_scratch_bytes(uint64_t, uint64_t, uint32_t);
 size_t shim_scratch_bytes(uint64_t);
 size_t map_scratch_bytes();
+size_t frame_scratch_bytes(uint64_t);
+cudaError_t launch_frame_pack(const uint64_t*, uint64_t, const uint64_t*, const uint64_t*, const uint64_t*,
+                              const uint64_t*, pv_frame*, uint32_t*, cudaStream_t);
+cudaError_t launch_frame_identify(const pv_frame*, uint64_t, const int32_t*, uint32_t, const uint64_t*,
+                                  const uint64_t*, uint32_t, uint32_t*, uint32_t*, cudaStream_t);
+cudaError_t launch_frame_assemble(const pv_frame*, uint64_t, const uint32_t*, uint64_t*, uint32_t*, void*, uint64_t,
+                                  cudaStream_t);
 cudaError_t launch_map_plan(const uint8_t*, uint64_t, uint64_t, uint64_t, const uint64_t*, uint64_t, uint8_t*,
                             uint64_t*, void*, cudaStream_t);
 cudaError_t launch_map_commit(uint8_t*, uint64_t, uint64_t, uint64_t, const uint64_t*, uint64_t, const uint8_t*,
@@ -280,6 +287,33 @@ int pv_copy_shim(uint8_t* image, uint64_t image_bytes, const pv_space* spaces, c
   if (image_bytes % kPageSize || scratch_bytes < shim_scratch_bytes(n_pages)) return PV_EINVAL;
   return rc(launch_copy_shim(image, image_bytes, spaces, shims, ops, n_ops, page_off, n_pages, page_hpa, page_status,
                              op_first_bad, dirty, n_written, scratch, (cudaStream_t)stream));
+}
+
+int pv_frame_pack(const uint64_t* ops, uint64_t n, const uint64_t* vcpu, const uint64_t* cr3, const uint64_t* tag,
+                  const uint64_t* frame_off, pv_frame* frames, uint32_t* status, void* stream) {
+  if (n == 0) return PV_SUCCESS;
+  if (!ops || !vcpu || !cr3 || !tag || !frame_off || !frames || !status) return PV_EINVAL;
+  return rc(launch_frame_pack(ops, n, vcpu, cr3, tag, frame_off, frames, status, (cudaStream_t)stream));
+}
+
+int pv_frame_identify(const pv_frame* frames, uint64_t n, const int32_t* vcpu_guest, uint32_t n_vcpus,
+                      const uint64_t* reg_guest, const uint64_t* reg_cr3, uint32_t n_reg, uint32_t* record,
+                      uint32_t* status, void* stream) {
+  if (n == 0) return PV_SUCCESS;
+  if (!frames || !record || !status || (n_vcpus && !vcpu_guest) || (n_reg && (!reg_guest || !reg_cr3)))
+    return PV_EINVAL;
+  return rc(launch_frame_identify(frames, n, vcpu_guest, n_vcpus, reg_guest, reg_cr3, n_reg, record, status,
+                                  (cudaStream_t)stream));
+}
+
+uint64_t pv_frame_assemble_scratch_bytes(uint64_t n) { return frame_scratch_bytes(n); }
+
+int pv_frame_assemble(const pv_frame* frames, uint64_t n, const uint32_t* record, uint64_t* ops_out, uint32_t* status,
+                      void* scratch, uint64_t scratch_bytes, void* stream) {
+  if (n == 0) return PV_SUCCESS;
+  if (!frames || !record || !ops_out || !status || !scratch || n >= 0xFFFFFFFFull) return PV_EINVAL;
+  if (scratch_bytes < frame_scratch_bytes(n)) return PV_EINVAL;
+  return rc(launch_frame_assemble(frames, n, record, ops_out, status, scratch, scratch_bytes, (cudaStream_t)stream));
 }
 
 uint64_t pv_map_scratch_bytes(void) { return map_scratch_bytes(); }

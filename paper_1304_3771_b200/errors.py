@@ -64,3 +64,15 @@ class NativeUnavailable(RuntimeError):
     Raised by every data-plane entry point instead of falling back to a CPU
     path: the product has no CPU fallback.
     """
+
+
+class UnknownVcpu(SimError):
+    """Hypercall frame carries a vCPU id not registered to any guest (errors.py:64-65)."""
+
+
+class Unpackable(SimError):
+    """A file operation cannot be framed or a frame sequence is malformed (errors.py:68-69)."""
+
+
+class UnknownProcess(SimError):
+    """A frame's virtual CR3 matches no process of its guest (errors.py:80-81)."""

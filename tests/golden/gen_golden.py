@@ -111,6 +111,11 @@ def main(src: str) -> None:
         json.dump(dict(res, build_sha=build_sha, shadow_root=w["p0"].shadow_root.root_pfn,
                        guest_root=w["p0"].guest_root.root_pfn, guest_base=w["g0"].base_hpa,
                        guest_bytes=w["g0"].mem.size_bytes, hybrid_root=w["rec"].active_hybrid.root_pfn), f)
+    from devfsim import hypercall as hc  # noqa: E402
+
+    with open(os.path.join(HERE, "frames.json"), "w") as f:
+        json.dump({"pack": S.frames_pack_query(hc), "feed": S.frames_feed_query(hc),
+                   "identify": S.frames_identify_query(hc)}, f)
     with open(os.path.join(HERE, "resultpage.json"), "w") as f:
         json.dump({"expected": S.resultpage_query(load_resultpage())}, f)
     print("golden fixtures written to", HERE)

@@ -446,3 +446,113 @@ def shim_query(w, mv, be, er):
             rows.append(outcome(lambda: int.from_bytes(hashlib.sha256(acc.copy_from_user(gva, n)).digest()[:8],
                                                        "little"), er))
     return dict(rows=rows, hw_translations=rec.hw_translations, image_sha=sha(image_bytes(memv.host_mem)))
+
+
+# ---- scenario "frames": hypercall framing (hypercall.py:110-211)
+
+def frames_ops(hc, n: int = 600, seed: int = 808):
+    """Random ops of every kind with random 32-bit words, plus ops whose
+    layout words do not fit (unpackable) and page faults with large tags."""
+    rng = random.Random(seed)
+    kinds = list(hc.FileOpKind)
+    ops = []
+    for i in range(n):
+        kind = rng.choice(kinds)
+        vals = {f: rng.randrange(2 ** 32) for f in hc.ARG_LAYOUT[kind]}
+        if i % 37 == 5:
+            vals[rng.choice(hc.ARG_LAYOUT[kind])] = 2 ** 32 + rng.randrange(1000)
+        ops.append(hc.FileOp(kind=kind, **vals))
+    return ops
+
+
+def op_outcome(op):
+    if op is None:
+        return None
+    return [int(op.kind)] + [int(getattr(op, f)) for f in ("device_id", "handle", "gva", "length", "offset", "flags",
+                                                               "cmd", "arg_gva", "arg_len", "prot", "event_mask",
+                                                               "timeout_ms", "pid", "access", "vma_start",
+                                                               "vma_length")]
+
+
+def frame_outcome(f):
+    return [int(f.opcode), [int(a) for a in f.args], int(f.vcpu), int(f.virtual_cr3)]
+
+
+def exc_name(e) -> str:
+    return type(e).__name__
+
+
+def frames_pack_query(hc):
+    out = []
+    for i, op in enumerate(frames_ops(hc)):
+        try:
+            out.append([frame_outcome(f) for f in hc.pack(op, vcpu=i % 4, virtual_cr3=0x40 + (i % 3),
+                                                          tag=(i * 2654435761) & 0x1_FFFF_FFFF)])
+        except Exception as e:  # noqa: BLE001
+            out.append(["err", exc_name(e)])
+    return out
+
+
+def frames_stream(hc, seed: int = 909, n_ops: int = 400):
+    """An interleaved frame stream of several (guest, process) sources with
+    page faults split across other traffic, reused tags, orphan
+    continuations, duplicate first frames and bad opcodes."""
+    rng = random.Random(seed)
+    srcs = [(0, 1), (0, 2), (1, 1), (1, 7)]
+    queue = {s: [] for s in srcs}
+    stream = []
+    for i, op in enumerate(frames_ops(hc, n_ops, seed)):
+        s = srcs[i % len(srcs)]
+        try:
+            fr = hc.pack(op, vcpu=s[0], virtual_cr3=0x100 * (s[1] + 1), tag=rng.randrange(6))
+        except Exception:  # noqa: BLE001
+            continue
+        queue[s].extend(fr)
+        while any(queue.values()) and rng.random() < 0.6:
+            q = rng.choice([x for x in srcs if queue[x]])
+            stream.append((queue[q].pop(0), q))
+        r = rng.random()
+        if r < 0.03:
+            stream.append((hc.HypercallFrame(hc.OPCODE_CONTINUATION, (rng.randrange(6), 1, 2, 0, 0, 0), 0, 0),
+                           rng.choice(srcs)))
+        elif r < 0.05:
+            stream.append((hc.HypercallFrame(int(hc.FileOpKind.PAGE_FAULT), (rng.randrange(6), 9, 9, 9, 9, 9), 0, 0),
+                           rng.choice(srcs)))
+        elif r < 0.06:
+            stream.append((hc.HypercallFrame(rng.choice([0, 10, 0x7E]), (0,) * 6, 0, 0), rng.choice(srcs)))
+    for q in srcs:
+        stream.extend((f, q) for f in queue[q])
+    return stream
+
+
+def frames_feed_query(hc):
+    asm = hc.FrameAssembler()
+    out = []
+    for f, (g, p) in frames_stream(hc):
+        try:
+            out.append(op_outcome(asm.feed(f, g, p)))
+        except Exception as e:  # noqa: BLE001
+            out.append(["err", exc_name(e)])
+    return out
+
+
+def frames_registry(hc):
+    reg = hc.VcpuRegistry()
+    for v, g in ((0, 0), (1, 0), (2, 1), (5, 1)):
+        reg.register_vcpu(v, g)
+    for g, cr3, pid in ((0, 0x100, 11), (0, 0x200, 12), (1, 0x100, 21), (1, 0x800, 22)):
+        reg.register_process(g, cr3, pid)
+    return reg
+
+
+def frames_identify_query(hc):
+    reg = frames_registry(hc)
+    out = []
+    for vcpu in range(7):
+        for cr3 in (0x100, 0x200, 0x800, 0x999):
+            f = hc.HypercallFrame(int(hc.FileOpKind.POLL), (0,) * 6, vcpu, cr3)
+            try:
+                out.append(list(reg.identify(f)))
+            except Exception as e:  # noqa: BLE001
+                out.append(["err", exc_name(e)])
+    return out
