@@ -431,23 +431,46 @@ def run_c2(args, rank, world, local):
     plan = dp.CopyPlan([t.device_space for t in trs], rows, fifo_groups=groups)
     fifo0 = dp.pack_fifo([t.cache for t in trs])
     fifo = dp._to_dev(fifo0)
+    # the forwarding leg (frontend pack -> backend identify + reassemble,
+    # hypercall.py:125-211): the trace as IOCTL FileOps, one vCPU per process
+    from paper_1304_3771_b200 import hypercall as hc
+
+    reg = hc.VcpuRegistry()
+    for p, sp in enumerate(spaces):
+        reg.register_vcpu(p, guest.guest_id)
+        reg.register_process(guest.guest_id, sp.cr3, sp.pid)
+    fops = np.zeros((len(gvas), N.FOP_WORDS), dtype=np.uint64)
+    fops[:, 0] = int(hc.FileOpKind.IOCTL)
+    fops[:, 1 + hc._FIELD_INDEX["handle"]] = 3
+    fops[:, 1 + hc._FIELD_INDEX["cmd"]] = W.IOCTL_SNAPSHOT
+    fops[:, 1 + hc._FIELD_INDEX["arg_gva"]] = gvas
+    fops[:, 1 + hc._FIELD_INDEX["arg_len"]] = lens
+    t64 = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.uint64).view(np.int64)).cuda()  # noqa: E731
+    fops_d, vcpu_d = t64(fops), t64(procs)
+    cr3_d = t64(np.array([spaces[p].cr3 for p in range(len(spaces))], dtype=np.uint64)[procs])
+    tag_d = torch.zeros_like(vcpu_d)
+    tables = reg.device_tables()
+    fwd = {}
     build_s = time.time() - t0
     stream = torch.cuda.current_stream()
 
     def step(ev):
         ev[0].record(stream)
-        dp.copy_launch(img, plan, N.TO_GUEST, buf, fifo_dev=fifo, fifo_cap=10)
+        frames, _, _ = hc.pack_device(fops_d, vcpu_d, cr3_d, tag_d, n_frames=len(gvas))
+        fwd["ops"], fwd["status"], fwd["record"], _ = hc.dispatch_device(frames, reg, tables)
         ev[1].record(stream)
-        dp.copy_ordered(img, plan, buf)
+        dp.copy_launch(img, plan, N.TO_GUEST, buf, fifo_dev=fifo, fifo_cap=10)
         ev[2].record(stream)
+        dp.copy_ordered(img, plan, buf)
+        ev[3].record(stream)
 
     for _ in range(args.warmup):
-        step([torch.cuda.Event(enable_timing=True) for _ in range(3)])
+        step([torch.cuda.Event(enable_timing=True) for _ in range(4)])
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     if world > 1:
         import torch.distributed as tdist
 
@@ -462,12 +485,20 @@ def run_c2(args, rank, world, local):
     n_apply = ctypes.c_uint64(0)
     kern_ms = lib.pv_timing_ms(b"ordered_apply", ctypes.byref(n_apply))
     lib.pv_timing(0)
-    plan_ms = sum(e[0].elapsed_time(e[1]) for e in evs)
-    apply_ms = sum(e[1].elapsed_time(e[2]) for e in evs)
-    total_ms, plan_ms, apply_ms, kern_ms = shard.max_over_ranks([plan_ms + apply_ms, plan_ms, apply_ms, kern_ms],
-                                                                world, device="cuda")
+    fwd_ms = sum(e[0].elapsed_time(e[1]) for e in evs)
+    plan_ms = sum(e[1].elapsed_time(e[2]) for e in evs)
+    apply_ms = sum(e[2].elapsed_time(e[3]) for e in evs)
+    total_ms, fwd_ms, plan_ms, apply_ms, kern_ms = shard.max_over_ranks(
+        [fwd_ms + plan_ms + apply_ms, fwd_ms, plan_ms, apply_ms, kern_ms], world, device="cuda")
     res = plan.results.cpu().numpy().view(np.uint64)
     assert (res[:, 3] & 0xFFFFFFFF == 0).all(), "C2 ops must all succeed"
+    # the reassembled ops are the trace: arg_gva / arg_len / issuing process
+    got = fwd["ops"].cpu().numpy().view(np.uint64)
+    assert (fwd["status"].cpu().numpy() == 0).all()
+    assert np.array_equal(got, fops)
+    recs = tables[5]
+    rec_pid = np.array([pid for _, pid in recs])[fwd["record"].cpu().numpy()]
+    assert np.array_equal(rec_pid, np.array([sp.pid for sp in spaces])[procs])
     K = args.steps
     payload = int(W.c2_trace(args.c2_ops)[2].sum())
     peak, peak_kind = peaks()
@@ -481,17 +512,20 @@ def run_c2(args, rank, world, local):
         "metric": METRIC, "value": args.c2_ops * K / (total_ms / 1e3), "unit": "ioctls/s", "n_gpus": world,
         "steps": K, "warmup": args.warmup, "ms_per_step": total_ms / K, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "u64 (integer walk) / u8 (payload)", "data": "synthetic",
-        "config": {"workload": f"C2: {args.c2_ops} IOCTL_SNAPSHOT ops (64 B-4 KiB blobs) staged by copy_to_user "
-                               "into 8 processes' 1 MiB arenas of one TDP guest, software HAS (FIFO-10)",
+        "config": {"workload": f"C2: {args.c2_ops} IOCTL_SNAPSHOT ops forwarded as hypercall frames (frontend "
+                               "pack, backend identify + reassemble) and their 64 B-4 KiB blobs staged by "
+                               "copy_to_user into 8 processes' 1 MiB arenas of one TDP guest, software HAS (FIFO-10)",
                    "parallelism": f"process-sharded x{world}"},
         "copy": {"value": payload * K / (total_ms / 1e3) / 1e9, "unit": "GB/s (payload)"},
-        "plan_fifo_ms_per_step": plan_ms / K, "ordered_apply_ms_per_step": apply_ms / K,
+        "forward_ms_per_step": fwd_ms / K, "plan_fifo_ms_per_step": plan_ms / K,
+        "ordered_apply_ms_per_step": apply_ms / K,
         "roofline": {"bound": "hbm", "kernel": "ordered_apply_kernel", "achieved": ach, "peak": peak,
                      "unit": "GB/s", "frac": ach / peak, "peak_source": peak_kind,
                      "traffic": load_traffic("c2").get("ordered_apply"), "launch_ms": per_launch_ms, "alg_bytes_per_launch": alg_bytes,
                      "note": "payload bytes read once + each destination page staged and written back once, "
                              "over the apply kernel's event-timed launch duration (pv_timing)"},
-        "gpu_launches": 10 * K, "gpu_launches_note": "plan, 4 FIFO-replay steps, stamp, exec (stands down), "
+        "gpu_launches": 14 * K, "gpu_launches_note": "frame pack, identify, classify (+ CUB select), plan, 4 FIFO-replay "
+                                                     "steps, stamp, exec (stands down), "
                                                      "results, keys, apply per step + CUB sort/RLE/scan kernels",
         "clocks": clk, "build_s": build_s,
     }

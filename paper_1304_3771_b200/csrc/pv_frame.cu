@@ -29,7 +29,6 @@
 
 namespace pv {
 
-constexpr uint32_t kSlots = 6;
 constexpr uint32_t kCont = 0x7F;
 constexpr uint32_t kPageFault = 7;
 constexpr int kFrTpb = 256;
@@ -61,21 +60,31 @@ __global__ void __launch_bounds__(kFrTpb)
 frame_pack_kernel(const uint64_t* __restrict__ ops, uint64_t n, const uint64_t* __restrict__ vcpu,
                   const uint64_t* __restrict__ cr3, const uint64_t* __restrict__ tag,
                   const uint64_t* __restrict__ frame_off, pv_frame* __restrict__ frames, uint32_t* __restrict__ status) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const uint64_t* op = ops + i * PV_FOP_WORDS;
+  __shared__ uint64_t rows[kFrTpb * PV_FOP_WORDS];  // the tile's op rows, loaded with coalesced words
+  const uint64_t n_tiles = (n + kFrTpb - 1) / kFrTpb;
+  for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const uint64_t i0 = tile * kFrTpb, i = i0 + threadIdx.x;
+    const uint64_t words = (min((uint64_t)kFrTpb, n - i0)) * PV_FOP_WORDS;
+    const uint64_t* src = ops + i0 * PV_FOP_WORDS;
+    __syncthreads();
+    for (uint64_t w = threadIdx.x; w < words; w += kFrTpb) rows[w] = src[w];
+    __syncthreads();
+    if (i >= n) continue;
+    const uint64_t* op = rows + threadIdx.x * PV_FOP_WORDS;
     const uint32_t kind = (uint32_t)op[0];
     uint32_t st = PV_FRAME_OK;
     uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    uint32_t nw = 0;
-    if (kind < 1 || kind > 9) {
+    if (kind < 1 || kind > 9 || op[0] > 9) {
       st = PV_FRAME_BAD_KIND;
     } else {
-      nw = layout_len(kind);
-      for (uint32_t k = 0; k < nw; ++k) {
-        const uint64_t v = op[1 + kLayout[kind][k]];
+      // the layout's words, in layout order (unrolled over the 7 slots so w stays in registers)
+#pragma unroll
+      for (uint32_t k = 0; k < 7; ++k) {
+        const int f = kLayout[kind][k];
+        if (f < 0) break;
+        const uint64_t v = op[1 + f];
         if (v > 0xFFFFFFFFull) {  // `0 <= value <= WORD_MASK` (hypercall.py:114-116)
-          st = PV_FRAME_UNPACKABLE | ((uint32_t)kLayout[kind][k] << 8);
+          st = PV_FRAME_UNPACKABLE | ((uint32_t)f << 8);
           break;
         }
         w[k] = (uint32_t)v;
@@ -83,7 +92,7 @@ frame_pack_kernel(const uint64_t* __restrict__ ops, uint64_t n, const uint64_t* 
     }
     status[i] = st;
     if (st != PV_FRAME_OK) continue;
-    pv_frame* f = frames + frame_off[i];
+    pv_frame* fo = frames + frame_off[i];
     const uint32_t vc = (uint32_t)vcpu[i];
     const uint64_t c3 = cr3[i];
     if (kind == kPageFault) {
@@ -92,21 +101,30 @@ frame_pack_kernel(const uint64_t* __restrict__ ops, uint64_t n, const uint64_t* 
       a.opcode = kind;
       b.opcode = kCont;
       a.args[0] = b.args[0] = t;
-      for (uint32_t k = 0; k < kSlots - 1; ++k) a.args[1 + k] = w[k];
+      a.args[1] = w[0];
+      a.args[2] = w[1];
+      a.args[3] = w[2];
+      a.args[4] = w[3];
+      a.args[5] = w[4];
       b.args[1] = w[5];
       b.args[2] = w[6];
       b.args[3] = b.args[4] = b.args[5] = 0;
       a.vcpu = b.vcpu = vc;
       a.virtual_cr3 = b.virtual_cr3 = c3;
-      f[0] = a;
-      f[1] = b;
+      fo[0] = a;
+      fo[1] = b;
     } else {
       pv_frame a;
       a.opcode = kind;
-      for (uint32_t k = 0; k < kSlots; ++k) a.args[k] = w[k];
+      a.args[0] = w[0];
+      a.args[1] = w[1];
+      a.args[2] = w[2];
+      a.args[3] = w[3];
+      a.args[4] = w[4];
+      a.args[5] = w[5];
       a.vcpu = vc;
       a.virtual_cr3 = c3;
-      f[0] = a;
+      fo[0] = a;
     }
   }
 }
@@ -137,33 +155,69 @@ frame_identify_kernel(const pv_frame* __restrict__ frames, uint64_t n, const int
   }
 }
 
+// kInv[kind][field] = position of FileOp field `field` in the kind's layout
+// (-1: not carried), the inverse of kLayout.
+__constant__ int8_t kInv[10][16] = {
+    {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1},
+    {0, -1, -1, -1, -1, 1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1},  // OPEN
+    {-1, 0, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1}, // RELEASE
+    {-1, 0, 1, 2, 3, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1},    // READ
+    {-1, 0, 1, 2, 3, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1},    // WRITE
+    {-1, 0, 4, -1, -1, 5, 1, 2, 3, -1, -1, -1, -1, -1, -1, -1},      // IOCTL
+    {-1, 0, 1, 2, 4, 5, -1, -1, -1, 3, -1, -1, -1, -1, -1, -1},      // MMAP
+    {-1, 0, 1, -1, 5, 6, -1, -1, -1, -1, -1, -1, -1, 2, 3, 4},       // PAGE_FAULT
+    {-1, 0, -1, -1, -1, -1, -1, -1, -1, -1, 1, 2, -1, -1, -1, -1},   // POLL
+    {-1, 0, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, 1, -1, -1, -1},      // NOTIFY_SUBSCRIBE
+};
+
+// One FileOp row {kind, 16 fields} from the kind's layout words w0..w6,
+// built in registers (selects, no indexed register arrays) and stored once.
+__device__ __forceinline__ void store_op(uint64_t* __restrict__ row, uint32_t kind, uint32_t w0, uint32_t w1,
+                                         uint32_t w2, uint32_t w3, uint32_t w4, uint32_t w5, uint32_t w6) {
+  row[0] = kind;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int p = kInv[kind][j];
+    const uint32_t v = p == 0 ? w0 : p == 1 ? w1 : p == 2 ? w2 : p == 3 ? w3 : p == 4 ? w4 : p == 5 ? w5 :
+                       p == 6 ? w6 : 0u;
+    row[1 + j] = v;
+  }
+}
+
 // Per frame: decode single-frame operations, flag page-fault first /
-// continuation frames for the pairing pass.
+// continuation frames for the pairing pass.  A CTA builds the 136-byte op
+// rows of 256 consecutive frames in shared memory and stores them as
+// coalesced 8-byte words (row stores straight from registers would scatter
+// every warp store over 32 rows).
 __global__ void __launch_bounds__(kFrTpb)
 frame_classify_kernel(const pv_frame* __restrict__ frames, uint64_t n, const uint32_t* __restrict__ record,
                       uint64_t* __restrict__ ops_out, uint32_t* __restrict__ status, uint8_t* __restrict__ pair_flag,
                       uint64_t* __restrict__ keys, uint32_t* __restrict__ iota) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    pair_flag[i] = 0;
-    iota[i] = (uint32_t)i;
-    if (status[i] != PV_FRAME_OK) continue;  // identify failed: the reference raises before feed
-    const pv_frame f = frames[i];
-    if (f.opcode == kCont || f.opcode == kPageFault) {
-      pair_flag[i] = 1;
-      keys[i] = ((uint64_t)record[i] << 32) | f.args[0];
-      continue;
+  __shared__ uint64_t rows[kFrTpb * PV_FOP_WORDS];
+  const uint64_t n_tiles = (n + kFrTpb - 1) / kFrTpb;
+  for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const uint64_t i0 = tile * kFrTpb, i = i0 + threadIdx.x;
+    if (i < n) {
+      pair_flag[i] = 0;
+      iota[i] = (uint32_t)i;
+      if (status[i] == PV_FRAME_OK) {  // identify failed: the reference raises before feed
+        const pv_frame f = frames[i];
+        if (f.opcode == kCont || f.opcode == kPageFault) {
+          pair_flag[i] = 1;
+          keys[i] = ((uint64_t)record[i] << 32) | f.args[0];
+        } else if (f.opcode < 1 || f.opcode > 9) {  // FileOpKind(opcode): ValueError
+          status[i] = PV_FRAME_BAD_KIND;
+        } else {
+          store_op(rows + threadIdx.x * PV_FOP_WORDS, f.opcode, f.args[0], f.args[1], f.args[2], f.args[3],
+                   f.args[4], f.args[5], 0);
+        }
+      }
     }
-    if (f.opcode < 1 || f.opcode > 9) {  // FileOpKind(opcode): ValueError
-      status[i] = PV_FRAME_BAD_KIND;
-      continue;
-    }
-    uint64_t* op = ops_out + i * PV_FOP_WORDS;
-    for (uint32_t k = 0; k < PV_FOP_WORDS; ++k) op[k] = 0;
-    op[0] = f.opcode;
-    const uint32_t nw = layout_len(f.opcode);
-    for (uint32_t k = 0; k < nw; ++k) op[1 + kLayout[f.opcode][k]] = f.args[k];
-    status[i] = PV_FRAME_OK;
+    __syncthreads();
+    const uint64_t words = (min((uint64_t)kFrTpb, n - i0)) * PV_FOP_WORDS;
+    uint64_t* dst = ops_out + i0 * PV_FOP_WORDS;
+    for (uint64_t w = threadIdx.x; w < words; w += kFrTpb) dst[w] = rows[w];  // rows of other frames: undefined
+    __syncthreads();
   }
 }
 
@@ -195,13 +249,9 @@ frame_pair_kernel(const pv_frame* __restrict__ frames, const uint64_t* __restric
         continue;
       }
       const pv_frame h = frames[pending];
-      uint64_t* op = ops_out + (uint64_t)i * PV_FOP_WORDS;
-      for (uint32_t k = 0; k < PV_FOP_WORDS; ++k) op[k] = 0;
-      op[0] = kPageFault;
       // words = head.args[1:] + frame.args[1 : 1 + n_tail]
-      for (uint32_t k = 0; k < 5; ++k) op[1 + kLayout[kPageFault][k]] = h.args[1 + k];
-      op[1 + kLayout[kPageFault][5]] = f.args[1];
-      op[1 + kLayout[kPageFault][6]] = f.args[2];
+      store_op(ops_out + (uint64_t)i * PV_FOP_WORDS, kPageFault, h.args[1], h.args[2], h.args[3], h.args[4],
+               h.args[5], f.args[1], f.args[2]);
       status[pending] = PV_FRAME_CONSUMED;
       status[i] = PV_FRAME_OK;
       pending = 0xFFFFFFFFu;

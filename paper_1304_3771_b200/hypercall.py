@@ -209,17 +209,33 @@ def _frame_error(status: int, ops_row=None):
     return RuntimeError(f"frame status {status:#x}")
 
 
-def pack_device(ops, vcpu, cr3, tags):
+_SCRATCH: dict = {}
+
+
+def _cached(name: str, nbytes: int):
+    """Per-size device scratch reused across calls on the current stream."""
+    import torch
+
+    t = _SCRATCH.get(name)
+    if t is None or t.numel() < nbytes:
+        t = torch.empty(max(nbytes, 1), dtype=torch.uint8, device="cuda")
+        _SCRATCH[name] = t
+    return t
+
+
+def pack_device(ops, vcpu, cr3, tags, *, n_frames: int | None = None):
     """pv_frame_pack over device arrays (ops: int64 [n, PV_FOP_WORDS];
     vcpu / cr3 / tags: int64 [n]).  Returns (frames uint8 [m*40],
-    frame_off int64 [n], status int32 [n]) on the device."""
+    frame_off int64 [n], status int32 [n]) on the device.  ``n_frames``
+    (n + the number of page faults) saves a device sync when the caller
+    knows it.  Frame slots of ops whose status is not OK are undefined."""
     import torch
 
     n = ops.shape[0]
     per = 1 + (ops[:, 0] == int(FileOpKind.PAGE_FAULT)).to(torch.int64)
     frame_off = torch.cumsum(per, 0) - per
-    m = int(frame_off[-1].item() + per[-1].item()) if n else 0
-    frames = torch.zeros(max(m, 1) * N.FRAME_BYTES, dtype=torch.uint8, device="cuda")
+    m = n_frames if n_frames is not None else (int(frame_off[-1].item() + per[-1].item()) if n else 0)
+    frames = torch.empty(max(m, 1) * N.FRAME_BYTES, dtype=torch.uint8, device="cuda")
     status = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
     if n:
         N.check(N.lib().pv_frame_pack(ops.data_ptr(), n, vcpu.data_ptr(), cr3.data_ptr(), tags.data_ptr(),
@@ -260,15 +276,16 @@ def pack_batch(ops, *, vcpu, virtual_cr3, tags=None):
 def assemble_device(frames, record, status):
     """pv_frame_assemble over device arrays (frames uint8 [m*40], record /
     status int32 [m]; status holds the identify outcome).  Returns ops
-    int64 [m, PV_FOP_WORDS]; status is updated in place."""
+    int64 [m, PV_FOP_WORDS] (rows of frames whose status is not OK are
+    undefined); status is updated in place."""
     import torch
 
     m = frames.numel() // N.FRAME_BYTES
-    ops = torch.zeros((max(m, 1), N.FOP_WORDS), dtype=torch.int64, device="cuda")
+    ops = torch.empty((max(m, 1), N.FOP_WORDS), dtype=torch.int64, device="cuda")
     if m:
         lib = N.lib()
         nbytes = int(lib.pv_frame_assemble_scratch_bytes(m))
-        scratch = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        scratch = _cached("assemble", nbytes)
         N.check(lib.pv_frame_assemble(frames.data_ptr(), m, record.data_ptr(), ops.data_ptr(), status.data_ptr(),
                                       scratch.data_ptr(), nbytes, _stream()), "pv_frame_assemble")
     return ops[:m]

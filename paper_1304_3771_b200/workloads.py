@@ -198,6 +198,9 @@ def c2_trace(n_ops: int, n_procs: int = C2_PROCS, seed: int = 3771):
     return procs, gvas, lens
 
 
+IOCTL_SNAPSHOT = 0x5A4E  # devices.py:35
+
+
 def snapshot_blob(n: int) -> np.ndarray:
     """The EventDevice IOCTL_SNAPSHOT result blob (devices.py:162-166)."""
     return ((np.arange(n, dtype=np.int64) * 7 + 3) & 0xFF).astype(np.uint8)
