@@ -6,19 +6,27 @@
 // keyed by its destination hpa page; a stable radix sort (CUB, only the bits
 // the image needs) groups chunks by page while preserving the global chunk
 // order (= op order, then page order), and a gather lays the 16-byte chunk
-// descriptors out in that order.  One WARP then owns one destination page:
-// it stages the page in shared memory, streams the page's chunk payloads in
-// with TMA bulk copies (cp.async.bulk issued by one lane, completion counted
-// on a per-slot mbarrier) into a circular byte ring up to kK chunks ahead, and applies the chunks in order with 16-byte realigned
-// shared-memory writes.  All source bytes really move (HBM -> SMEM); the
-// successive overwrites land in SMEM instead of HBM, the way a write-back
-// cache would absorb them, and the page is written back once.  The pipeline
-// is warp-private: no CTA-wide barriers on the per-chunk path.
+// descriptors out in that order.  A producer/consumer WARP PAIR then owns one
+// destination page: the consumer stages the page in shared memory; the
+// producer streams the page's chunk payloads in with TMA bulk copies
+// (cp.async.bulk issued by one lane, completion counted on a per-slot
+// mbarrier) into a circular byte ring, up to kK chunks ahead, LAST CHUNK
+// FIRST; the consumer lets each byte take the value of the first arrival that
+// covers it (a per-block coverage map skips bytes a later writer already
+// set), which is exactly the state the in-order copies leave.  All source
+// bytes really move (HBM -> SMEM); the overwritten ones are simply never
+// copied on from SMEM, the way a write-back cache would absorb them, and the
+// page is written back once.  The pipeline is warp-private: no CTA-wide
+// barriers on the per-chunk path.
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_run_length_encode.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include "pv_common.cuh"
+
+#ifndef PV_ORDERED_BACKOFF_NS
+#define PV_ORDERED_BACKOFF_NS 64
+#endif
 
 namespace pv {
 
@@ -71,14 +79,29 @@ __global__ void ordered_gather_kernel(const uint32_t* __restrict__ sorted_pages,
 
 // ---- warp-per-page apply ------------------------------------------------------------
 
-constexpr int kApPages = 4;                    // page slots (producer + consumer warp each) per CTA
-constexpr int kK = 16;                         // chunks in flight per page slot (mbarrier pairs)
-constexpr uint32_t kRB = 8192;                 // circular byte ring per page slot (power of two)
+#ifndef PV_AP_PAGES
+#define PV_AP_PAGES 4
+#endif
+#ifndef PV_AP_RING
+#define PV_AP_RING 8192
+#endif
+#ifndef PV_AP_K
+#define PV_AP_K 16
+#endif
+#ifndef PV_AP_WINDOW
+#define PV_AP_WINDOW 6144  // measured: 3.66 ms vs 6.56 ms at the full ring (C2), see DESIGN.md
+#endif
+constexpr int kApPages = PV_AP_PAGES;                    // page slots (producer + consumer warp each) per CTA
+constexpr int kK = PV_AP_K;                         // chunks in flight per page slot (mbarrier pairs)
+constexpr uint32_t kRB = PV_AP_RING;                 // circular byte ring per page slot (power of two)
 constexpr uint32_t kRB16 = kRB / 16;
+constexpr uint32_t kWin = PV_AP_WINDOW;  // ring bytes a slot keeps in flight (<= kRB)
+static_assert(kRB >= kPageSize + 32 && kWin <= kRB, "a chunk span (<= 4112 bytes) must fit the ring");
 
 struct __align__(16) PageSmem {
   uint8_t page[kPageSize];
   uint8_t ring[kRB];
+  uint16_t cov[kPageSize / 16];  // bytes of each 16-byte block already final (bit x = byte x)
   uint64_t full[kK];
   uint64_t empty[kK];
   uint32_t meta[kK];
@@ -103,6 +126,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
   } while (!ok);
 }
+// Producer-side wait for a ring slot: back off between polls so the spinning
+// warp does not take issue slots from the consumer it is waiting for.
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+      : "=r"(ok)
+      : "r"(smem_addr(bar)), "r"(parity)
+      : "memory");
+  while (!ok) {
+    __nanosleep(PV_ORDERED_BACKOFF_NS);
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
+  }
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, uint64_t src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
@@ -111,13 +152,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, uint64_t src, uint32_t bytes
       : "memory");
 }
 
-// Apply one chunk: dest bytes [off, off + len) of the page <- ring bytes
-// starting at ring byte `v0` (circular), realigned 16 bytes at a time.  D is
-// the (warp-uniform) word part of the realignment, so the word selection is
-// static: a whole destination block is two 16-byte SMEM loads, four funnel
-// shifts and one 16-byte SMEM store.  The (at most two) partial edge blocks
-// are merged by lanes 0 and 1 with byte masks from the `low` table
-// (low[x] = the low x bytes of 16 set), once per chunk.
+// Destination block j of a chunk from the ring, realigned: D is the
+// (warp-uniform) word part of the realignment, so the word selection is
+// static -- two 16-byte SMEM loads and four funnel shifts.
 template <int D>
 __device__ __forceinline__ uint4 realign(const uint4* ring16, int32_t j, int32_t dq, uint32_t sb) {
   const uint4 U = ring16[(uint32_t)(j + dq) & (kRB16 - 1)];
@@ -135,30 +172,44 @@ __device__ __forceinline__ uint4 realign(const uint4* ring16, int32_t j, int32_t
   return out;
 }
 
+// Byte mask of the set bits of a nibble (bit b -> byte b), no table.
+__device__ __forceinline__ uint32_t nibble_bytes(uint32_t x) { return ((x * 0x00204081u) & 0x01010101u) * 0xFFu; }
+
+// Apply one chunk LAST-FIRST: the page's chunks arrive in reverse program
+// order, so a byte takes the value of the first chunk (in arrival order) that
+// covers it and later arrivals only fill bytes no later writer has covered --
+// the same final bytes as applying every chunk in order.  cov[] tracks the
+// final bytes per 16-byte block; blocks already final are skipped.  Returns
+// the number of blocks this lane made fully final.
 template <int D>
-__device__ __forceinline__ void apply_chunk(PageSmem& W, const uint4* __restrict__ low, uint32_t lane, int32_t off,
-                                            int32_t len, int32_t dq, uint32_t sb) {
+__device__ __forceinline__ uint32_t apply_chunk_rev(PageSmem& W, uint32_t lane, int32_t off, int32_t len, int32_t dq,
+                                                    uint32_t sb) {
   const uint4* ring16 = reinterpret_cast<const uint4*>(W.ring);
   uint4* page16 = reinterpret_cast<uint4*>(W.page);
   const int32_t end = off + len;
-  const int32_t jf0 = (off + 15) >> 4, jf1 = end >> 4;  // whole blocks [jf0, jf1)
-  for (int32_t j = jf0 + (int32_t)lane; j < jf1; j += 32) page16[j] = realign<D>(ring16, j, dq, sb);
-  // partial blocks: the head block (off not 16-aligned, or the chunk inside one block) and the tail block
   const int32_t jh = off >> 4, jt = (end - 1) >> 4;
-  const bool head = (off & 15) != 0 || (jh == jt && (end & 15) != 0);
-  const bool tail = (end & 15) != 0 && jt != jh;
-  if ((lane == 0 && head) || (lane == 1 && tail)) {
-    const int32_t j = lane == 0 ? jh : jt;
+  uint32_t made_full = 0;
+  for (int32_t j = jh + (int32_t)lane; j <= jt; j += 32) {
     const int32_t lo = max(off - 16 * j, 0), hi = min(end - 16 * j, 16);
+    const uint32_t rmask = (0xFFFFu >> (16 - hi)) & (0xFFFFu << lo);
+    const uint32_t c = W.cov[j];
+    const uint32_t need = rmask & ~c;
+    if (need == 0) continue;
     const uint4 v = realign<D>(ring16, j, dq, sb);
-    const uint4 old = page16[j], mh = low[hi], ml = low[lo];
-    uint4 out;
-    out.x = (old.x & ~(mh.x & ~ml.x)) | (v.x & mh.x & ~ml.x);
-    out.y = (old.y & ~(mh.y & ~ml.y)) | (v.y & mh.y & ~ml.y);
-    out.z = (old.z & ~(mh.z & ~ml.z)) | (v.z & mh.z & ~ml.z);
-    out.w = (old.w & ~(mh.w & ~ml.w)) | (v.w & mh.w & ~ml.w);
-    page16[j] = out;
+    if (need == 0xFFFFu) {
+      page16[j] = v;
+    } else {
+      const uint32_t m0 = nibble_bytes(need & 15), m1 = nibble_bytes((need >> 4) & 15),
+                     m2 = nibble_bytes((need >> 8) & 15), m3 = nibble_bytes(need >> 12);
+      const uint4 old = page16[j];
+      page16[j] = make_uint4((old.x & ~m0) | (v.x & m0), (old.y & ~m1) | (v.y & m1), (old.z & ~m2) | (v.z & m2),
+                             (old.w & ~m3) | (v.w & m3));
+    }
+    const uint32_t nc = c | rmask;
+    W.cov[j] = (uint16_t)nc;
+    made_full += nc == 0xFFFFu;
   }
+  return made_full;
 }
 
 // One page slot per producer/consumer warp pair.  The producer warp walks
@@ -175,15 +226,17 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 __device__ __forceinline__ void produce(PageSmem& P, const ChunkDesc* __restrict__ desc, uint32_t b, uint32_t n,
                                         uint32_t lane, uint64_t pol, uint32_t& G, uint32_t& vhead, uint32_t& hptr,
                                         int64_t& released) {
+  // chunks go into the ring last-first (k-th issued = chunk n-1-k of the page)
+  const ChunkDesc* rdesc = desc + b + n - 1;
   ChunkDesc cur{0, 0, 0}, nxt{0, 0, 0};
-  if (lane < n) cur = desc[b + lane];
-  if (32 + lane < n) nxt = desc[b + 32 + lane];
+  if (lane < n) cur = *(rdesc - lane);
+  if (32 + lane < n) nxt = *(rdesc - (32 + lane));
   uint32_t cb = 0;
   for (uint32_t k = 0; k < n; ++k, ++G) {
     if (k == cb + 32) {
       cur = nxt;
       cb += 32;
-      nxt = cb + 32 + lane < n ? desc[b + cb + 32 + lane] : ChunkDesc{0, 0, 0};
+      nxt = cb + 32 + lane < n ? *(rdesc - (cb + 32 + lane)) : ChunkDesc{0, 0, 0};
     }
     const uint32_t meta = __shfl_sync(0xFFFFFFFFu, cur.meta, k - cb);
     const uint64_t src = ((uint64_t)__shfl_sync(0xFFFFFFFFu, (uint32_t)(cur.src >> 32), k - cb) << 32) |
@@ -193,11 +246,11 @@ __device__ __forceinline__ void produce(PageSmem& P, const ChunkDesc* __restrict
     // chunk G reuses slot G % kK (last held by chunk G - kK) and the ring
     // bytes of every chunk whose virtual start is below ve - kRB
     if (G >= (uint32_t)kK && hptr < G - kK + 1) hptr = G - kK + 1;
-    while (hptr < G && (int32_t)(P.vstart[hptr % kK] - (ve - kRB)) < 0) ++hptr;
+    while (hptr < G && (int32_t)(P.vstart[hptr % kK] - (ve - kWin)) < 0) ++hptr;
     int64_t r = (int64_t)hptr - 1;
     if (G >= (uint32_t)kK && (int64_t)(G - kK) > r) r = G - kK;
     if (r > released) {
-      mbar_wait(&P.empty[r % kK], (uint32_t)(r / kK) & 1);
+      mbar_wait_backoff(&P.empty[r % kK], (uint32_t)(r / kK) & 1);
       released = r;
     }
     const uint32_t slot = G % kK;
@@ -224,12 +277,6 @@ ordered_apply_kernel(uint8_t* __restrict__ image, const ChunkDesc* __restrict__ 
   const uint32_t pslot = warp >> 1;
   const bool producer = (warp & 1) == 0;
   PageSmem& P = reinterpret_cast<PageSmem*>(smem_raw)[pslot];
-  __shared__ uint4 low[17];
-  if (threadIdx.x < 17) {
-    const uint32_t x = threadIdx.x;
-    auto lw = [](uint32_t n) { return n >= 4 ? 0xFFFFFFFFu : ((1u << (8 * n)) - 1u); };
-    low[x] = make_uint4(lw(x), lw(x > 4 ? x - 4 : 0), lw(x > 8 ? x - 8 : 0), lw(x > 12 ? x - 12 : 0));
-  }
   if (producer && lane == 0) {
     for (int k = 0; k < kK; ++k) {
       mbar_init(&P.full[k], 1);
@@ -254,22 +301,28 @@ ordered_apply_kernel(uint8_t* __restrict__ image, const ChunkDesc* __restrict__ 
 #pragma unroll
     for (int k = 0; k < 8; ++k)
       reinterpret_cast<uint4*>(P.page)[lane + 32 * k] = reinterpret_cast<const uint4*>(image + dst)[lane + 32 * k];
+    reinterpret_cast<uint4*>(P.cov)[lane] = make_uint4(0, 0, 0, 0);
+    uint32_t open_blocks = kPageSize / 16;  // blocks not yet final (warp-uniform)
     __syncwarp();
     for (uint32_t k = 0; k < n; ++k, ++G) {
       const uint32_t slot = G % kK;
       mbar_wait(&P.full[slot], (G / kK) & 1);
       const uint32_t meta = P.meta[slot];
       const uint32_t shift = meta & 15, len = meta >> 16;
-      const int32_t off = (int32_t)((meta >> 4) & 0xFFF);
-      // dest byte 16j + x  <->  ring byte 16j + delta + x
-      const int32_t delta = (int32_t)(vhead % kRB + shift) - off;
-      const int32_t dq = delta >> 4;
-      const uint32_t dr = (uint32_t)delta & 15, sb = (dr & 3) * 8;
-      switch (dr >> 2) {
-        case 0: apply_chunk<0>(P, low, lane, off, (int32_t)len, dq, sb); break;
-        case 1: apply_chunk<1>(P, low, lane, off, (int32_t)len, dq, sb); break;
-        case 2: apply_chunk<2>(P, low, lane, off, (int32_t)len, dq, sb); break;
-        default: apply_chunk<3>(P, low, lane, off, (int32_t)len, dq, sb); break;
+      if (open_blocks != 0 && len != 0) {
+        const int32_t off = (int32_t)((meta >> 4) & 0xFFF);
+        // dest byte 16j + x  <->  ring byte 16j + delta + x
+        const int32_t delta = (int32_t)(vhead % kRB + shift) - off;
+        const int32_t dq = delta >> 4;
+        const uint32_t dr = (uint32_t)delta & 15, sb = (dr & 3) * 8;
+        uint32_t full = 0;
+        switch (dr >> 2) {
+          case 0: full = apply_chunk_rev<0>(P, lane, off, (int32_t)len, dq, sb); break;
+          case 1: full = apply_chunk_rev<1>(P, lane, off, (int32_t)len, dq, sb); break;
+          case 2: full = apply_chunk_rev<2>(P, lane, off, (int32_t)len, dq, sb); break;
+          default: full = apply_chunk_rev<3>(P, lane, off, (int32_t)len, dq, sb); break;
+        }
+        open_blocks -= __reduce_add_sync(0xFFFFFFFFu, full);
       }
       vhead += ((shift + len + 15) >> 4) << 4;
       __syncwarp();  // every lane's ring reads and page writes of chunk k are done
