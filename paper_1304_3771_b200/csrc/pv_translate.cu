@@ -244,6 +244,48 @@ translate_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const 
     have_next = c + 1 < c_end && c + 1 < seg.chunk0 + seg_chunks;
     if (have_next) load_vas(c + 1, nva);
 
+    // Fast path (one-stage walks): when every lane of this thread resolves
+    // its upper levels to an indexed, in-image leaf node and its leaf code is
+    // PRESENT, the translation is (code >> 2) << 12 | offset and the status
+    // OK -- no status logic, no branches per lane.  Anything else (faults,
+    // traps, escapes, unindexed nodes, two-stage spaces) takes the general
+    // path below, which re-reads the same (now L1-resident) codes.
+    if (!(kTwo && two) && leaf_codes != nullptr) {
+      uint32_t fc[VPT];
+      bool simple = true;
+#pragma unroll
+      for (int j = 0; j < VPT; ++j) {
+        fc[j] = codes1[(top_index(va[j]) << 9) | mid_index(va[j])];
+        const bool valid = lane0 + (uint64_t)j * TPB + threadIdx.x < seg_end;
+        simple &= !valid || (fc[j] & 0xFu) == (1u | kCodeIndexed);
+      }
+      if (simple) {
+        uint32_t lc[VPT];
+#pragma unroll
+        for (int j = 0; j < VPT; ++j) {
+          const bool valid = lane0 + (uint64_t)j * TPB + threadIdx.x < seg_end;
+          lc[j] = 1u;
+          if (valid)
+            asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;"
+                : "=r"(lc[j])
+                : "l"(leaf_codes + ((uint64_t)(fc[j] >> 4) << 9) + leaf_index(va[j])), "l"(pol_table));
+        }
+        bool present = true;
+#pragma unroll
+        for (int j = 0; j < VPT; ++j) present &= (lc[j] & 3u) == 1u;
+        if (present) {
+#pragma unroll
+          for (int j = 0; j < VPT; ++j) {
+            const uint64_t i = lane0 + (uint64_t)j * TPB + threadIdx.x;
+            if (i >= seg_end) continue;
+            const uint64_t pfn = lc[j] >> 2;
+            st_u64_stream(out_value + i, kPfn ? pfn : ((pfn << kPageShift) | (va[j] & kPageMask)), pol_stream);
+            st_u32_stream(out_status + i, PV_ST_OK, pol_stream);
+          }
+          continue;
+        }
+      }
+    }
     uint32_t st[VPT], code[VPT];
     uint64_t w[VPT];
 #pragma unroll
