@@ -40,7 +40,10 @@
 namespace pv {
 
 constexpr uint32_t kNoOp = 0xFFFFFFFFu;
-constexpr int kWarmWindows = 2;  // H
+#ifndef PV_FIFO_WARM
+#define PV_FIFO_WARM 1
+#endif
+constexpr int kWarmWindows = PV_FIFO_WARM;  // H
 
 struct FifoStream {
   const uint64_t* ref;       // per lookup: index into value / status (lane or page)
@@ -233,6 +236,9 @@ struct Scratch {
   uint64_t* spec_end;    // [windows][state_words]
   uint64_t* win_counts;  // [windows]: hits | lookups << 32
   uint8_t* match;        // [windows]
+  uint64_t* block;       // [windows], at each 32-window block start of a process: bit 63 all
+                         // windows of the block link to their predecessor; bits 0-31 the
+                         // block's hits | lookups << 16
   uint64_t* hitpage;     // [lookups]
   uint8_t* flags;        // [lookups]: 1 hit, 2 terminate, 4 active
 };
@@ -316,6 +322,26 @@ __global__ void fifo_link_kernel(FifoStream fs, Scratch sc, uint64_t n_windows) 
   sc.match[w] = eq ? 1 : 0;
 }
 
+// Step 2b: per 32-window block of each process (aligned to the process's
+// first window): do all its windows link, and its hit / lookup sums.
+__global__ void fifo_block_kernel(FifoStream fs, Scratch sc, uint64_t n_windows) {
+  const uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= n_windows) return;
+  const uint32_t p = proc_of_window(fs, w);
+  const uint64_t w0 = fs.win_off[p], w1 = fs.win_off[p + 1];
+  if ((w - w0) & 31) return;
+  const uint64_t e = w + 32 < w1 ? w + 32 : w1;
+  bool all = true;
+  uint32_t hits = 0, looks = 0;
+  for (uint64_t v = w; v < e; ++v) {
+    all &= sc.match[v] != 0;
+    const uint64_t c = sc.win_counts[v];
+    hits += (uint32_t)c;
+    looks += (uint32_t)(c >> 32);
+  }
+  sc.block[w] = ((uint64_t)all << 63) | hits | ((uint64_t)looks << 16);
+}
+
 // Step 3: verify each process's chain; replay mismatching windows exactly.
 __global__ void fifo_verify_kernel(FifoStream fs, pv_fifo* __restrict__ fifo, Scratch sc) {
   const uint32_t full = 0xFFFFFFFFu;
@@ -329,17 +355,23 @@ __global__ void fifo_verify_kernel(FifoStream fs, pv_fifo* __restrict__ fifo, Sc
   // spec_end[w - 1] (the previous window was accepted as speculated).
   bool have_s = true;
   uint64_t hits = 0, lookups = 0;
-  // the next block's link flags and counts are fetched one block ahead
-  uint8_t nx_m = (w0 + lane < w1) ? sc.match[w0 + lane] : 0;
-  uint64_t nx_c = (w0 + lane < w1) ? sc.win_counts[w0 + lane] : 0;
-  for (uint64_t wb = w0; wb < w1; wb += 32) {
-    const uint32_t mm = __ballot_sync(full, nx_m != 0);
-    const uint64_t wc = nx_c;
-    {
-      const uint64_t nl = wb + 32 + lane;
-      nx_m = nl < w1 ? sc.match[nl] : 0;
-      nx_c = nl < w1 ? sc.win_counts[nl] : 0;
+  // block summaries, 32 blocks (1024 windows) per warp load, one group ahead
+  const uint64_t n_blocks = (w1 - w0 + 31) >> 5;
+  uint64_t grp = lane < n_blocks ? sc.block[w0 + 32ull * lane] : 0;
+  for (uint64_t kb = 0; kb < n_blocks; kb += 32) {
+    const uint64_t cur_grp = grp;
+    grp = kb + 32 + lane < n_blocks ? sc.block[w0 + 32ull * (kb + 32 + lane)] : 0;
+    const uint32_t nq = (uint32_t)(n_blocks - kb < 32 ? n_blocks - kb : 32);
+    for (uint32_t q = 0; q < nq; ++q) {
+    const uint64_t wb = w0 + 32ull * (kb + q);
+    const uint64_t rec = __shfl_sync(full, cur_grp, q);
+    if (!have_s && (rec >> 63)) {  // every window links: accepted as speculated
+      hits += rec & 0xFFFF;
+      lookups += (rec >> 16) & 0xFFFF;
+      continue;
     }
+    const uint32_t mm = __ballot_sync(full, wb + lane < w1 && sc.match[wb + lane] != 0);
+    const uint64_t wc = wb + lane < w1 ? sc.win_counts[wb + lane] : 0;
     // per-window hits | lookups packed in 16-bit halves for warp sums (<= 32 each)
     const uint32_t wc16 = (uint32_t)(wc & 0xFFFF) | ((uint32_t)((wc >> 32) & 0xFFFF) << 16);
     const uint32_t nb = (uint32_t)(w1 - wb < 32 ? w1 - wb : 32);
@@ -376,6 +408,7 @@ __global__ void fifo_verify_kernel(FifoStream fs, pv_fifo* __restrict__ fifo, Sc
         lookups += c >> 32;
       }
       ++j;
+    }
     }
   }
   if (!have_s) load_state(sc.spec_end + (w1 - 1) * fs.state_words, fs.cap, lane, s);
@@ -423,7 +456,7 @@ __global__ void fifo_apply_kernel(FifoStream fs, Scratch sc, uint64_t n_lookups,
 
 size_t fifo_scratch_bytes(uint64_t n_lookups, uint64_t n_windows, uint32_t cap) {
   const uint64_t sw = 2ull * cap + 1;
-  return 2 * n_windows * sw * 8 + n_windows * 8 + n_windows + n_lookups * 8 + n_lookups + 256;
+  return 2 * n_windows * sw * 8 + 2 * n_windows * 8 + n_windows + n_lookups * 8 + n_lookups + 256;
 }
 
 static Scratch carve(void* base, uint64_t n_lookups, uint64_t n_windows, uint32_t cap) {
@@ -437,6 +470,8 @@ static Scratch carve(void* base, uint64_t n_lookups, uint64_t n_windows, uint32_
   s.hitpage = reinterpret_cast<uint64_t*>(p);
   p += n_lookups * 8;
   s.win_counts = reinterpret_cast<uint64_t*>(p);
+  p += n_windows * 8;
+  s.block = reinterpret_cast<uint64_t*>(p);
   p += n_windows * 8;
   s.match = p;
   p += n_windows;
@@ -458,6 +493,7 @@ cudaError_t launch_fifo_stream(const FifoStream& fs, pv_fifo* fifo, void* scratc
     fifo_spec_kernel<<<(unsigned)grid, 256, 0, stream>>>(fs, fifo, sc, n_windows, fb);
   }
   fifo_link_kernel<<<(unsigned)((n_windows + 255) / 256), 256, 0, stream>>>(fs, sc, n_windows);
+  fifo_block_kernel<<<(unsigned)((n_windows + 255) / 256), 256, 0, stream>>>(fs, sc, n_windows);
   fifo_verify_kernel<<<(fs.n_procs + 3) / 4, 128, 0, stream>>>(fs, fifo, sc);
   {
     uint64_t grid = (n_lookups + 255) / 256;

@@ -8,7 +8,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"
   --log-file gpurun_out/${tag}_launches_c5.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline \
   > gpurun_out/${tag}_launch_c5.json 2> gpurun_out/${tag}_launch_c5.err
 echo "c5 launch list rc=$?"
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"^(plan|stamp|exec|fifo|ordered|Device|shim)" -c 60 --csv \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name-base demangled -k regex:"pv::|CUB_" -c 60 --csv \
   --log-file gpurun_out/${tag}_launches_c2.csv python bench.py --workload c2 --steps 2 --warmup 1 \
   > gpurun_out/${tag}_launch_c2.json 2> gpurun_out/${tag}_launch_c2.err
 echo "c2 launch list rc=$?"
