@@ -76,6 +76,9 @@ stamp_kernel(const uint64_t* __restrict__ page_off, uint64_t n_ops, uint64_t n_p
              unsigned long long* __restrict__ owner, uint64_t owner_pages, uint32_t epoch, uint32_t* conflict) {
   const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t * kPlanPpt < n_pages; t += nthreads) {
+    // one detected conflict decides the batch (the exec kernel stands down):
+    // stop stamping, so heavily overlapping batches do not serialise on atomics
+    if (*reinterpret_cast<volatile const uint32_t*>(conflict)) return;
     const uint64_t p0 = t * kPlanPpt;
     uint64_t op = upper_search(page_off, 0, n_ops, p0);
     uint64_t op_end = __ldg(page_off + op + 1);
@@ -89,6 +92,11 @@ stamp_kernel(const uint64_t* __restrict__ page_off, uint64_t n_ops, uint64_t n_p
       const uint64_t hp = page_hpa[p] >> kPageShift;
       if (hp >= owner_pages) continue;
       const unsigned long long mine = ((unsigned long long)epoch << 40) | (p + 1);
+      const unsigned long long seen = *reinterpret_cast<volatile const unsigned long long*>(owner + hp);
+      if ((seen >> 40) == epoch && seen != mine) {  // already stamped by another chunk of this batch
+        atomicOr(conflict, 1u);
+        return;
+      }
       const unsigned long long old = atomicMax(owner + hp, mine);
       if ((old >> 40) == epoch && old != mine) atomicOr(conflict, 1u);
     }
