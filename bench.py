@@ -336,9 +336,9 @@ def run_ours(args, rank, world, local):
                           "gather_sol": walker_sol(wl.n_vas * K / (tr_ms / 1e3))},
         "faulting_lanes": n_faults,
         "gather_to_rank0": gather,
-        "gpu_launches": (4 + (8 if wl.cplan.shims is not None else 0)) * K,
-        "gpu_launches_note": "translate, plan, stamp, exec per step (+ 8 trap-shim passes for hybrid copies: "
-                             "eval, reset, firstbad, cut, claim, apply, rewalk, cleanup; empty when nothing traps)",
+        "gpu_launches": (4 + (2 if wl.cplan.shims is not None else 0)) * K,
+        "gpu_launches_note": "translate, plan, stamp, exec per step (+ the trap shim for hybrid copies: "
+                             "eval + one cooperative resolve kernel that returns at once when nothing traps)",
         "clocks": clk,
         "e2e": e2e,
         "build_s": wl.build_s,
@@ -707,7 +707,7 @@ def run_c4(args, rank, world, local):
         "roofline": {"bound": "hbm", "kernel": "translate_kernel", "achieved": walk_ach, "peak": peak,
                      "unit": "GB/s", "frac": walk_ach / peak, "peak_source": peak_kind,
                      "note": "16 B/translation; 1 M lanes fit L2, so this line is latency-bound, not HBM-bound"},
-        "gpu_launches": 14 * K, "gpu_launches_note": "translate, plan, 8 shim passes, stamp, exec per step",
+        "gpu_launches": 7 * K, "gpu_launches_note": "translate, plan, shim eval + cooperative resolve, stamp, exec per step (+ leaf-index re-encode)",
         "clocks": clk, "build_s": build_s,
     }
 

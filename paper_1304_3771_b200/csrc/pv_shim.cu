@@ -29,9 +29,11 @@
 //   rewalk  : reached simple traps re-walk the hybrid table (the retry) and
 //             become ordinary translations; unreached ones get their trap
 //             status back and re-enter the first-failure minimum.
-// Every kernel after eval returns at once when eval found nothing, so a
-// trap-free batch pays a handful of empty launches.  The scratch area is left
+// The passes after eval run as one cooperative kernel that returns at once
+// when eval found nothing, so a trap-free batch pays two launches.  The scratch area is left
 // zeroed after each call (the claim table cleans up after itself).
+#include <cooperative_groups.h>
+
 #include "pv_common.cuh"
 
 namespace pv {
@@ -140,37 +142,40 @@ shim_eval_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const 
   }
 }
 
-// First failing page per op, simple traps excluded (or, after the rewalk,
-// pages whose status changed).  Only lowers op_first_bad; `reset` first
-// clears the ops that hold a listed page.
-__global__ void __launch_bounds__(kShimTpb)
-shim_reset_kernel(ShimScratch sc, unsigned long long* __restrict__ op_first_bad) {
-  const uint64_t n = *sc.count;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-    op_first_bad[sc.list_op[i]] = kNone;
+// The passes after eval, in ONE cooperative launch (grid-wide barriers
+// between them): a trap-free batch costs one more launch, not seven.
+namespace cg = cooperative_groups;
+
+__device__ __forceinline__ uint64_t find_slot(const ShimScratch& sc, uint64_t key) {
+  uint64_t h = hash_slot(key) & sc.mask;
+  while (sc.keys[h] != key) h = (h + 1) & sc.mask;
+  return h;
 }
 
 __global__ void __launch_bounds__(kShimTpb)
-shim_firstbad_kernel(ShimScratch sc, const uint64_t* __restrict__ page_off, uint64_t n_ops, uint64_t n_pages,
-                     const uint32_t* __restrict__ page_status, unsigned long long* __restrict__ op_first_bad) {
-  if (*sc.count == 0) return;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n_pages; p += stride) {
+shim_resolve_kernel(ShimScratch sc, uint8_t* __restrict__ image, uint64_t image_bytes,
+                    const pv_space* __restrict__ spaces, const pv_op* __restrict__ ops, uint64_t n_ops,
+                    const uint64_t* __restrict__ page_off, uint64_t n_pages, uint64_t* __restrict__ page_hpa,
+                    uint32_t* __restrict__ page_status, unsigned long long* __restrict__ op_first_bad,
+                    uint8_t* __restrict__ dirty, unsigned long long* __restrict__ n_written) {
+  const uint64_t n = *sc.count;
+  if (n == 0) return;  // uniform across the grid: nothing trapped simply
+  cg::grid_group grid = cg::this_grid();
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
+  // 1. the first failing page of every op holding a simple trap is recomputed
+  for (uint64_t i = tid; i < n; i += nthr) op_first_bad[sc.list_op[i]] = kNone;
+  grid.sync();
+  for (uint64_t p = tid; p < n_pages; p += nthr) {
     const uint32_t st = page_status[p];
     if (st == PV_ST_OK || (st & kShimmed)) continue;
     uint64_t op, k;
     op_of(page_off, n_ops, p, &op, &k);
     atomicMin(op_first_bad + op, (unsigned long long)k);
   }
-}
-
-__global__ void __launch_bounds__(kShimTpb)
-shim_cut_kernel(ShimScratch sc, const uint64_t* __restrict__ page_off, uint64_t n_ops, uint64_t n_pages,
-                const uint32_t* __restrict__ page_status, const unsigned long long* __restrict__ op_first_bad) {
-  if (*sc.count == 0) return;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n_pages; p += stride) {
+  grid.sync();
+  // 2. the cut: the first op whose first failure is a trap the device cannot fix
+  for (uint64_t p = tid; p < n_pages; p += nthr) {
     const uint32_t st = page_status[p];
     const uint32_t kd = PV_ST_KIND(st);
     if ((kd != PV_ST_TRAP && kd != PV_ST_TRAP2) || (st & kShimmed)) continue;
@@ -178,15 +183,10 @@ shim_cut_kernel(ShimScratch sc, const uint64_t* __restrict__ page_off, uint64_t 
     op_of(page_off, n_ops, p, &op, &k);
     if (op_first_bad[op] == k) atomicMax(sc.cut, ~(unsigned long long)op);
   }
-}
-
-__global__ void __launch_bounds__(kShimTpb)
-shim_claim_kernel(ShimScratch sc, const uint64_t* __restrict__ page_off, const uint64_t* __restrict__ page_hpa,
-                  const uint32_t* __restrict__ page_status, const unsigned long long* __restrict__ op_first_bad) {
-  const uint64_t n = *sc.count;
+  grid.sync();
+  // 3. claim: per slot, the earliest reached page wins
   const unsigned long long cut = ~*sc.cut;  // kNone when no op is cut
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+  for (uint64_t i = tid; i < n; i += nthr) {
     const uint64_t p = sc.list_p[i], op = sc.list_op[i];
     const uint64_t k = p - __ldg(page_off + op);
     if (op > cut || k >= op_first_bad[op]) continue;  // never reached in program order
@@ -200,21 +200,9 @@ shim_claim_kernel(ShimScratch sc, const uint64_t* __restrict__ page_off, const u
     }
     atomicMax(sc.vals + h, ~(unsigned long long)p);
   }
-}
-
-__device__ __forceinline__ uint64_t find_slot(const ShimScratch& sc, uint64_t key) {
-  uint64_t h = hash_slot(key) & sc.mask;
-  while (sc.keys[h] != key) h = (h + 1) & sc.mask;
-  return h;
-}
-
-__global__ void __launch_bounds__(kShimTpb)
-shim_apply_kernel(ShimScratch sc, uint8_t* __restrict__ image, const uint64_t* __restrict__ page_hpa,
-                  const uint32_t* __restrict__ page_status, uint8_t* __restrict__ dirty,
-                  unsigned long long* __restrict__ n_written) {
-  const uint64_t n = *sc.count;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+  grid.sync();
+  // 4. winners write their word
+  for (uint64_t i = tid; i < n; i += nthr) {
     const uint64_t tagged = sc.list_p[i];
     if (!(tagged >> 63)) continue;
     const uint64_t p = tagged & ~(3ull << 62);
@@ -229,21 +217,19 @@ shim_apply_kernel(ShimScratch sc, uint8_t* __restrict__ image, const uint64_t* _
     if (dirty != nullptr) dirty[node] = 1;
     if (n_written != nullptr) atomicAdd(n_written, 1ull);
   }
-}
-
-__global__ void __launch_bounds__(kShimTpb)
-shim_rewalk_kernel(ShimScratch sc, const uint8_t* __restrict__ image, uint64_t image_bytes,
-                   const pv_space* __restrict__ spaces, const pv_op* __restrict__ ops,
-                   const uint64_t* __restrict__ page_off, uint64_t* __restrict__ page_hpa,
-                   uint32_t* __restrict__ page_status, unsigned long long* __restrict__ op_first_bad) {
-  const uint64_t n = *sc.count;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+  grid.sync();
+  // 5. the retry walk of every reached page; unreached ones get their trap
+  //    status back; winners clear their claim-table entry
+  for (uint64_t i = tid; i < n; i += nthr) {
     const uint64_t tagged = sc.list_p[i];
     const uint64_t p = tagged & ~(3ull << 62), op = sc.list_op[i];
     const uint64_t k = p - __ldg(page_off + op);
+    if ((tagged >> 62) & 1) {
+      const uint64_t h = sc.list_w[i];
+      sc.keys[h] = 0;
+      sc.vals[h] = 0;
+    }
     if (!(tagged >> 63)) {
-      // not reached: the trap stands (the host re-plans this op)
       page_status[p] &= ~kShimmed;
       atomicMin(op_first_bad + op, (unsigned long long)k);
       continue;
@@ -262,17 +248,10 @@ shim_rewalk_kernel(ShimScratch sc, const uint8_t* __restrict__ image, uint64_t i
     page_status[p] = st;
     if (st != PV_ST_OK) atomicMin(op_first_bad + op, (unsigned long long)k);
   }
-}
-
-__global__ void __launch_bounds__(kShimTpb)
-shim_cleanup_kernel(ShimScratch sc) {
-  const uint64_t n = *sc.count;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    if (!((sc.list_p[i] >> 62) & 1)) continue;
-    const uint64_t h = sc.list_w[i];  // the winner's table index (stored by apply)
-    sc.keys[h] = 0;
-    sc.vals[h] = 0;
+  grid.sync();
+  if (tid == 0) {  // leave the scratch zero-filled
+    *sc.count = 0;
+    *sc.cut = 0;
   }
 }
 
@@ -290,21 +269,16 @@ cudaError_t launch_copy_shim(uint8_t* image, uint64_t image_bytes, const pv_spac
     return (unsigned)(g ? g : 1);
   };
   const unsigned gp = grid_for((const void*)shim_eval_kernel, n_pages);
-  const unsigned gl = grid_for((const void*)shim_claim_kernel, n_pages);
   shim_eval_kernel<<<gp, kShimTpb, 0, stream>>>(image, image_bytes, ops, n_ops, page_off, n_pages, shims, page_hpa,
                                                  page_status, sc);
-  shim_reset_kernel<<<gl, kShimTpb, 0, stream>>>(sc, fb);
-  shim_firstbad_kernel<<<gp, kShimTpb, 0, stream>>>(sc, page_off, n_ops, n_pages, page_status, fb);
-  shim_cut_kernel<<<gp, kShimTpb, 0, stream>>>(sc, page_off, n_ops, n_pages, page_status, fb);
-  shim_claim_kernel<<<gl, kShimTpb, 0, stream>>>(sc, page_off, page_hpa, page_status, fb);
-  shim_apply_kernel<<<gl, kShimTpb, 0, stream>>>(sc, image, page_hpa, page_status, dirty,
-                                                 reinterpret_cast<unsigned long long*>(n_written));
-  shim_rewalk_kernel<<<gl, kShimTpb, 0, stream>>>(sc, image, image_bytes, spaces, ops, page_off, page_hpa,
-                                                   page_status, fb);
-  shim_cleanup_kernel<<<gl, kShimTpb, 0, stream>>>(sc);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  return cudaMemsetAsync(scratch, 0, 16, stream);  // count and cut
+  // every CTA of a cooperative launch must be resident at once
+  unsigned gr = (unsigned)resident_grid((const void*)shim_resolve_kernel, kShimTpb, 0);
+  unsigned long long* nw = reinterpret_cast<unsigned long long*>(n_written);
+  void* args[] = {&sc, &image, &image_bytes, &spaces, &ops, &n_ops, &page_off, &n_pages,
+                  &page_hpa, &page_status, &fb, &dirty, &nw};
+  return cudaLaunchCooperativeKernel((const void*)shim_resolve_kernel, dim3(gr), dim3(kShimTpb), args, 0, stream);
 }
 
 }  // namespace pv
