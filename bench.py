@@ -58,6 +58,8 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("PV_BENCH_SHARED_DEVICE") == "1":
+        local = 0  # testing only: every rank on cuda:0 (exercises the N>1 path on a one-GPU box, over gloo)
     return rank, world, local
 
 
@@ -326,11 +328,12 @@ def run_ours(args, rank, world, local):
         "translate_ms_per_step": tr_ms / K,
         "roofline": {"bound": "hbm", "kernel": "pv_copy_exec (exec_kernel)", "achieved": exec_achieved,
                      "peak": peak, "unit": "GB/s", "frac": exec_achieved / peak, "peak_source": peak_kind,
-                     "traffic": traffic.get("exec"),
+                     "traffic": traffic_for(traffic, "exec", 2 * wl.copy_bytes),
                      "algorithmic_bytes_per_launch": 2 * wl.copy_bytes},
         "roofline_walk": {"bound": "hbm", "kernel": "pv_translate (translate_kernel)", "achieved": walk_achieved,
                           "peak": peak, "unit": "GB/s", "frac": walk_achieved / peak,
-                          "traffic": traffic.get("translate"), "algorithmic_bytes_per_launch": walk_bytes,
+                          "traffic": traffic_for(traffic, "translate", walk_bytes),
+                          "algorithmic_bytes_per_launch": walk_bytes,
                           "note": "16 B/translation (u32 VA in, u64 hpa + u32 status out); leaf-PTE gathers "
                                   "are extra traffic",
                           "gather_sol": walker_sol(wl.n_vas * K / (tr_ms / 1e3))},
@@ -521,7 +524,7 @@ def run_c2(args, rank, world, local):
         "ordered_apply_ms_per_step": apply_ms / K,
         "roofline": {"bound": "hbm", "kernel": "ordered_apply_kernel", "achieved": ach, "peak": peak,
                      "unit": "GB/s", "frac": ach / peak, "peak_source": peak_kind,
-                     "traffic": load_traffic("c2").get("ordered_apply"), "launch_ms": per_launch_ms, "alg_bytes_per_launch": alg_bytes,
+                     "traffic": traffic_for(load_traffic("c2"), "ordered_apply", alg_bytes), "launch_ms": per_launch_ms, "alg_bytes_per_launch": alg_bytes,
                      "note": "payload bytes read once + each destination page staged and written back once, "
                              "over the apply kernel's event-timed launch duration (pv_timing)"},
         "gpu_launches": 14 * K, "gpu_launches_note": "frame pack, identify, classify (+ CUB select), plan, 4 FIFO-replay "
@@ -767,10 +770,9 @@ def run_e2e(wl, args, world):
         a, b = one_step()
         tr_s += a
         cp_s += b
-    tt = torch.tensor([tr_s, cp_s], dtype=torch.float64, device="cuda")
-    if world > 1:
-        tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
-    tr_s, cp_s = tt.tolist()
+    from paper_1304_3771_b200 import shard
+
+    tr_s, cp_s = shard.max_over_ranks([tr_s, cp_s], world, device="cuda")
     return {"value": wl.total_vas * steps / tr_s, "unit": "translations/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "copy": {"value": wl.total_copy_bytes * steps / cp_s / 1e9, "unit": "GB/s"},
@@ -817,6 +819,17 @@ def load_traffic(workload: str) -> dict:
         return {}
 
 
+def traffic_for(traffic: dict, kernel: str, alg_bytes: int):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture,
+    scaled to this run's per-launch algorithmic bytes (the capture is the
+    N=1 full-size step; a rank at N>1 launches over a 1/N share)."""
+    t = traffic.get(kernel)
+    a = traffic.get("alg_bytes", {}).get(kernel)
+    if t is None or not a:
+        return t
+    return int(round(t * alg_bytes / a))
+
+
 def config_of(wl, world):
     if wl.name == "c5":
         c = wl.cfg
@@ -826,7 +839,8 @@ def config_of(wl, world):
                 "copy_bytes_per_guest": c.copy_bytes_per_guest, "op_bytes": c.op_bytes,
                 "geometry": "reference 3-level 2/9/9/12", "sharding": f"guest g -> rank g mod {world}",
                 "parallelism": f"guest-sharded x{world}, no collective",
-                "l2": "inputs larger than L2 (512 MiB VAs, 8 GiB payload per step)",
+                "l2": f"inputs larger than L2 ({c.guests * c.vas_per_guest * 4 >> 20} MiB VAs, "
+                      f"{c.guests * c.copy_bytes_per_guest >> 20} MiB payload per step, whole job)",
                 "scale": 1 if wl.cfg.guest_bytes == 8 << 30 else "reduced"}
     return {"workload": "C1: 1 shadow guest, 16384 shuffled pages, 1M random-VA translations + 64 MiB "
                         "copy_to_user", "geometry": "reference 3-level 2/9/9/12",
@@ -966,7 +980,7 @@ def main():
         import torch
         import torch.distributed as tdist
 
-        if args.impl == "ours":
+        if args.impl == "ours" and os.environ.get("PV_BENCH_SHARED_DEVICE") != "1":
             torch.cuda.set_device(local)
             tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:

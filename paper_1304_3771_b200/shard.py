@@ -43,6 +43,7 @@ def gather_to_rank0(results: dict[int, dict], n_guests: int, rank: int, world: i
 
     if world == 1:
         return dict(results)
+    host = _host_backend()  # gloo: stage device tensors through host memory
     out: dict[int, dict] = {}
     for g in range(n_guests):
         src = owner_of(g, world)
@@ -52,16 +53,30 @@ def gather_to_rank0(results: dict[int, dict], n_guests: int, rank: int, world: i
                 continue
             buf = like(g)
             for key in sorted(buf):
-                dist.recv(buf[key], src=src)
+                if host and buf[key].is_cuda:
+                    tmp = buf[key].cpu()
+                    dist.recv(tmp, src=src)
+                    buf[key].copy_(tmp)
+                else:
+                    dist.recv(buf[key], src=src)
             out[g] = buf
         elif rank == src:
             for key in sorted(results[g]):
-                dist.send(results[g][key].contiguous(), dst=0)
+                t = results[g][key].contiguous()
+                dist.send(t.cpu() if host else t, dst=0)
     return out if rank == 0 else None
 
 
+def _host_backend() -> bool:
+    """True when the process group cannot move device tensors (gloo)."""
+    import torch.distributed as dist
+
+    return dist.get_backend() != "nccl"
+
+
 def max_over_ranks(values: Iterable[float], world: int, device=None) -> list[float]:
-    """Element-wise max over ranks (the bench's timing rule)."""
+    """Element-wise max over ranks (the bench's timing rule).  ``device`` is
+    where the reduction tensor lives under NCCL; gloo reduces on the host."""
     import torch
 
     vals = list(values)
@@ -69,6 +84,6 @@ def max_over_ranks(values: Iterable[float], world: int, device=None) -> list[flo
         return vals
     import torch.distributed as dist
 
-    t = torch.tensor(vals, dtype=torch.float64, device=device)
+    t = torch.tensor(vals, dtype=torch.float64, device=None if _host_backend() else device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return t.tolist()

@@ -105,3 +105,29 @@ def test_c5_scaled_bench_world_sharded(cuda):
     ospaces = np.stack([O.space(s.s1_base, s.s1_root_pfn) for s in c_spaces])
     O.copy(raw, ospaces, rows, src.cpu().numpy(), 0, threads=0)
     assert np.array_equal(_raw(memv), raw)
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_one_device(cuda, tmp_path):
+    """bench.py's N>1 path (torchrun, guest sharding, barrier, max over
+    ranks, per-guest results returned to rank 0) on a one-GPU box: both ranks
+    share cuda:0 and talk over gloo (PV_BENCH_SHARED_DEVICE=1)."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PV_BENCH_SHARED_DEVICE="1", MASTER_ADDR="127.0.0.1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29541", os.path.join(root, "bench.py"),
+           "--gpus", "2", "--steps", "2", "--warmup", "3", "--scale", "8", "--gather", "--no-e2e",
+           "--no-cpu-baseline"]
+    p = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, p.stdout  # rank 0 prints exactly one line
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["value"] > 0 and line["faulting_lanes"] == 0
+    assert line["gather_to_rank0"]["complete"] is True
+    assert line["config"]["sharding"] == "guest g -> rank g mod 2"
