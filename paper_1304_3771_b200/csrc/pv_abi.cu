@@ -131,6 +131,25 @@ uint64_t resident_grid(const void* func, int tpb, size_t smem) {
   return g;
 }
 
+cudaError_t stream_scratch(void** p, size_t bytes, cudaStream_t stream) {
+  static std::mutex mu;
+  static bool configured[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64) {
+    std::lock_guard<std::mutex> g(mu);
+    if (!configured[dev]) {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = 256ull << 20;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      }
+      configured[dev] = true;
+    }
+  }
+  return cudaMallocAsync(p, bytes < 256 ? 256 : bytes, stream);
+}
+
 __global__ void scatter_pages_kernel(uint8_t* __restrict__ image, uint64_t image_pages,
                                      const uint64_t* __restrict__ pfns, uint64_t n, const uint8_t* __restrict__ src) {
   for (uint64_t i = blockIdx.x; i < n; i += gridDim.x) {

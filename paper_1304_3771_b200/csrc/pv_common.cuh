@@ -184,4 +184,10 @@ __device__ __forceinline__ uint64_t upper_search(const uint64_t* __restrict__ of
 // function and device; defined in pv_abi.cu).
 uint64_t resident_grid(const void* func, int tpb, size_t smem);
 
+// Stream-ordered device scratch for one call (cudaMallocAsync from the
+// device's default pool, which is told once to keep up to 256 MiB cached so
+// repeated calls do not go back to the driver); release with cudaFreeAsync
+// on the same stream.
+cudaError_t stream_scratch(void** p, size_t bytes, cudaStream_t stream);
+
 }  // namespace pv

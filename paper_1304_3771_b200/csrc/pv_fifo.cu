@@ -241,6 +241,7 @@ struct Scratch {
                          // block's hits | lookups << 16
   uint64_t* hitpage;     // [lookups]
   uint8_t* flags;        // [lookups]: 1 hit, 2 terminate, 4 active
+  uint64_t* run_off;     // [procs + 1]: first kRun-window run of each process
 };
 
 __device__ __forceinline__ uint32_t proc_of_window(const FifoStream& fs, uint64_t w) {
@@ -268,44 +269,106 @@ __device__ __forceinline__ void run_one(const FifoStream& fs, uint64_t lb, uint6
   }
 }
 
-// Step 1: speculate every window.
-__global__ void fifo_spec_kernel(FifoStream fs, const pv_fifo* __restrict__ fifo, Scratch sc, uint64_t n_windows,
-                                 unsigned long long* first_bad) {
+// Step 1: speculate every window.  One warp per run of kRun consecutive
+// windows of a process: the run's start state is rebuilt by replaying the
+// kWarmWindows windows before it (exactly, from the initial cache, near the
+// stream start), then its windows are replayed back to back, so every window
+// after the first starts from its predecessor's speculated end state (its
+// link flag is set here) and the warm-up is paid once per run, not per window.
+#ifndef PV_FIFO_RUN
+#define PV_FIFO_RUN 8
+#endif
+constexpr uint32_t kRun = PV_FIFO_RUN;
+
+// Run order.  Processes' lookup streams interleave in the plan (their pages
+// alternate in op order), so the r-th runs of all processes read the same
+// region of the plan arrays: runs are scheduled process-minor (run k of
+// process 0, 1, ..., then run k + 1 ...) so those sectors are fetched from
+// HBM once and hit in L2 for the other processes, instead of once per process
+// (8x the traffic at C2).  run_off[n_procs + 1] = max runs per process; the
+// interleaved order is used when it wastes at most half the slots (balanced
+// streams), else the process-major order run_off describes.
+__device__ __forceinline__ bool run_of_slot(const uint64_t* run_off, uint32_t n_procs, bool interleave, uint64_t r,
+                                            uint32_t* p_out, uint64_t* k_out) {
+  if (interleave) {
+    const uint32_t p = (uint32_t)(r % n_procs);
+    const uint64_t k = r / n_procs;
+    *p_out = p;
+    *k_out = k;
+    return k < run_off[p + 1] - run_off[p];
+  }
+  uint32_t lo = 0, hi = n_procs;
+  while (hi - lo > 1) {
+    const uint32_t m = (lo + hi) >> 1;
+    if (run_off[m] <= r) lo = m; else hi = m;
+  }
+  *p_out = lo;
+  *k_out = r - run_off[lo];
+  return r < run_off[n_procs];
+}
+
+__global__ void fifo_spec_kernel(FifoStream fs, const pv_fifo* __restrict__ fifo, Scratch sc, uint64_t n_slots_max,
+                                 const uint64_t* __restrict__ run_off, unsigned long long* first_bad) {
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n_windows; w += nwarps) {
-    const uint32_t p = proc_of_window(fs, w);
-    const uint64_t w0 = fs.win_off[p], lb = fs.lk_off[p], le = fs.lk_off[p + 1];
-    const uint64_t wi = w - w0;
+  const uint64_t total_runs = run_off[fs.n_procs], max_runs = run_off[fs.n_procs + 1];
+  const bool interleave = max_runs * fs.n_procs <= 2 * total_runs;
+  uint64_t n_slots = interleave ? max_runs * fs.n_procs : total_runs;
+  if (n_slots > n_slots_max) n_slots = n_slots_max;
+  for (uint64_t r = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n_slots; r += nwarps) {
+    uint32_t p;
+    uint64_t k;
+    if (!run_of_slot(run_off, fs.n_procs, interleave, r, &p, &k)) continue;
+    const uint64_t w0 = fs.win_off[p], nw = fs.win_off[p + 1] - w0, lb = fs.lk_off[p], le = fs.lk_off[p + 1];
+    const uint64_t wi0 = k * kRun;
+    const uint64_t wi1 = wi0 + kRun < nw ? wi0 + kRun : nw;
     WarpState s;
     uint64_t from;
-    if (wi <= (uint64_t)kWarmWindows) {
+    const bool exact = wi0 <= (uint64_t)kWarmWindows;
+    if (exact) {
       initial_state(fifo[p], lane, s);  // exact: replay from the stream start
       from = 0;
     } else {
       s.qk = s.qv = 0;
       s.len = 0;
       s.term_op = kNoOp;
-      from = wi - kWarmWindows;
+      from = wi0 - kWarmWindows;
     }
-    for (uint64_t v = from; v < wi; ++v) run_one(fs, lb, le, v, lane, s, nullptr, nullptr);
-    store_state(sc.spec_start + w * fs.state_words, fs.cap, lane, s);
-    uint64_t counts = 0;
-    run_one(fs, lb, le, wi, lane, s, &sc, &counts);
-    store_state(sc.spec_end + w * fs.state_words, fs.cap, lane, s);
-    if (lane == 0) {
-      sc.win_counts[w] = counts;
-      sc.match[w] = wi <= (uint64_t)kWarmWindows ? 1 : 0;  // exact start state
-    }
-    // copy plans: every op of this window starts from "not failed"
-    if (fs.op != nullptr && first_bad != nullptr) {
-      const uint64_t l = lb + wi * 32 + lane;
-      if (l < le) {
-        const uint32_t o = fs.op[l];
-        if (fs.ref[l] == fs.page_off[o]) first_bad[o] = kNone;
+    for (uint64_t v = from; v < wi0; ++v) run_one(fs, lb, le, v, lane, s, nullptr, nullptr);
+    for (uint64_t wi = wi0; wi < wi1; ++wi) {
+      const uint64_t w = w0 + wi;
+      store_state(sc.spec_start + w * fs.state_words, fs.cap, lane, s);
+      uint64_t counts = 0;
+      run_one(fs, lb, le, wi, lane, s, &sc, &counts);
+      store_state(sc.spec_end + w * fs.state_words, fs.cap, lane, s);
+      if (lane == 0) {
+        sc.win_counts[w] = counts;
+        sc.match[w] = (exact || wi > wi0) ? 1 : 0;  // exact start state, or linked inside the run
+      }
+      // copy plans: every op of this window starts from "not failed"
+      if (fs.op != nullptr && first_bad != nullptr) {
+        const uint64_t l = lb + wi * 32 + lane;
+        if (l < le) {
+          const uint32_t o = fs.op[l];
+          if (fs.ref[l] == fs.page_off[o]) first_bad[o] = kNone;
+        }
       }
     }
   }
+}
+
+// run_off[p] = number of kRun-window runs before process p (one thread).
+// run_off[n_procs + 1] = the most runs of any process (one thread).
+__global__ void fifo_runs_kernel(FifoStream fs, uint64_t* run_off) {
+  uint64_t acc = 0, most = 0;
+  for (uint32_t p = 0; p < fs.n_procs; ++p) {
+    run_off[p] = acc;
+    const uint64_t n = (fs.win_off[p + 1] - fs.win_off[p] + kRun - 1) / kRun;
+    acc += n;
+    most = n > most ? n : most;
+  }
+  run_off[fs.n_procs] = acc;
+  run_off[fs.n_procs + 1] = most;
 }
 
 // Step 2: link neighbouring windows.
@@ -425,44 +488,68 @@ __global__ void fifo_verify_kernel(FifoStream fs, pv_fifo* __restrict__ fifo, Sc
   }
 }
 
-// Step 4: apply hits and terminations.
-__global__ void fifo_apply_kernel(FifoStream fs, Scratch sc, uint64_t n_lookups, uint64_t* value, uint32_t* status,
-                                  unsigned long long* first_bad) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t l = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; l < n_lookups; l += stride) {
-    const uint8_t fl = sc.flags[l];
-    const uint64_t ref = fs.ref[l];
-    if (fs.op == nullptr) {
-      if (fl & 1) {
-        const uint64_t va = fs.va32 ? (uint64_t)((const uint32_t*)fs.vas)[ref] : ((const uint64_t*)fs.vas)[ref];
-        value[ref] = (sc.hitpage[l] << kPageShift) | (va & kPageMask);
-        status[ref] = PV_ST_OK;
-      }
-      continue;
-    }
-    const uint32_t o = fs.op[l];
-    const pv_op op = fs.ops[o];
-    const uint64_t k = ref - fs.page_off[o];
-    const uint64_t cur = op_page_va(op.gva, k);
-    if (fl & 1) {
-      value[ref] = (sc.hitpage[l] << kPageShift) | (cur & kPageMask);
-      status[ref] = (fl & 2) ? PV_ST_DATA_OOR : PV_ST_OK;
-    }
-    if (fl & 2) first_bad[o] = k;
+// Step 4: apply hits and terminations (one warp per run of kRun windows, in
+// the speculation's run order so the scattered page writes of all processes
+// land in the same plan region at the same time).
+__device__ __forceinline__ void apply_one(const FifoStream& fs, const Scratch& sc, uint64_t l, uint64_t* value,
+                                          uint32_t* status, unsigned long long* first_bad) {
+  const uint8_t fl = sc.flags[l];
+  if (!(fl & 3)) return;
+  const uint64_t ref = fs.ref[l];
+  if (fs.op == nullptr) {
+    const uint64_t va = fs.va32 ? (uint64_t)((const uint32_t*)fs.vas)[ref] : ((const uint64_t*)fs.vas)[ref];
+    value[ref] = (sc.hitpage[l] << kPageShift) | (va & kPageMask);
+    status[ref] = PV_ST_OK;
+    return;
+  }
+  const uint32_t o = fs.op[l];
+  const pv_op op = fs.ops[o];
+  const uint64_t k = ref - fs.page_off[o];
+  const uint64_t cur = op_page_va(op.gva, k);
+  if (fl & 1) {
+    value[ref] = (sc.hitpage[l] << kPageShift) | (cur & kPageMask);
+    status[ref] = (fl & 2) ? PV_ST_DATA_OOR : PV_ST_OK;
+  }
+  if (fl & 2) first_bad[o] = k;
+}
+
+__global__ void fifo_apply_kernel(FifoStream fs, Scratch sc, uint64_t n_slots_max, const uint64_t* __restrict__ run_off,
+                                  uint64_t* value, uint32_t* status, unsigned long long* first_bad) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t total_runs = run_off[fs.n_procs], max_runs = run_off[fs.n_procs + 1];
+  const bool interleave = max_runs * fs.n_procs <= 2 * total_runs;
+  uint64_t n_slots = interleave ? max_runs * fs.n_procs : total_runs;
+  if (n_slots > n_slots_max) n_slots = n_slots_max;
+  for (uint64_t r = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n_slots; r += nwarps) {
+    uint32_t p;
+    uint64_t k;
+    if (!run_of_slot(run_off, fs.n_procs, interleave, r, &p, &k)) continue;
+    const uint64_t lb = fs.lk_off[p], le = fs.lk_off[p + 1];
+    const uint64_t l0 = lb + k * kRun * 32;
+    const uint64_t l1 = l0 + kRun * 32 < le ? l0 + kRun * 32 : le;
+    for (uint64_t l = l0 + lane; l < l1; l += 32) apply_one(fs, sc, l, value, status, first_bad);
   }
 }
 
 // ---- launchers ------------------------------------------------------------------
 
+// The run offsets ([procs + 1] u64) sit at the front: a process without
+// windows adds no run but still needs an offset, so they are sized by a
+// generous 64 Ki processes (the ABI caller does not pass the process count).
+constexpr uint64_t kMaxProcsScratch = 1ull << 16;
 size_t fifo_scratch_bytes(uint64_t n_lookups, uint64_t n_windows, uint32_t cap) {
   const uint64_t sw = 2ull * cap + 1;
-  return 2 * n_windows * sw * 8 + 2 * n_windows * 8 + n_windows + n_lookups * 8 + n_lookups + 256;
+  return (kMaxProcsScratch + 2) * 8 + 2 * n_windows * sw * 8 + 2 * n_windows * 8 + n_windows + n_lookups * 8 +
+         n_lookups + 256;
 }
 
 static Scratch carve(void* base, uint64_t n_lookups, uint64_t n_windows, uint32_t cap) {
   const uint64_t sw = 2ull * cap + 1;
   uint8_t* p = static_cast<uint8_t*>(base);
   Scratch s;
+  s.run_off = reinterpret_cast<uint64_t*>(p);
+  p += (kMaxProcsScratch + 2) * 8;
   s.spec_start = reinterpret_cast<uint64_t*>(p);
   p += n_windows * sw * 8;
   s.spec_end = reinterpret_cast<uint64_t*>(p);
@@ -483,23 +570,31 @@ cudaError_t launch_fifo_stream(const FifoStream& fs, pv_fifo* fifo, void* scratc
                                uint64_t n_windows, uint64_t* value, uint32_t* status, uint64_t* first_bad,
                                cudaStream_t stream) {
   if (fs.n_procs == 0 || n_windows == 0) return cudaSuccess;
+  if (fs.n_procs > kMaxProcsScratch) return cudaErrorInvalidValue;
   const Scratch sc = carve(scratch, n_lookups, n_windows, fs.cap);
   auto* fb = reinterpret_cast<unsigned long long*>(first_bad);
   {
-    const uint64_t warps = n_windows;
-    uint64_t grid = (warps + 7) / 8;
+    uint64_t* run_off = sc.run_off;
+    fifo_runs_kernel<<<1, 1, 0, stream>>>(fs, run_off);
+    // every process contributes ceil(nw / kRun) runs <= nw / kRun + 1; the
+    // interleaved order uses at most 2x the runs (the kernel clamps)
+    const uint64_t runs_max = 2 * (n_windows / kRun + fs.n_procs);
+    uint64_t grid = (runs_max / 2 + 7) / 8;
     const uint64_t cap = resident_grid((const void*)fifo_spec_kernel, 256, 0);
     if (grid > cap) grid = cap;
-    fifo_spec_kernel<<<(unsigned)grid, 256, 0, stream>>>(fs, fifo, sc, n_windows, fb);
+    if (grid == 0) grid = 1;
+    fifo_spec_kernel<<<(unsigned)grid, 256, 0, stream>>>(fs, fifo, sc, runs_max, run_off, fb);
   }
   fifo_link_kernel<<<(unsigned)((n_windows + 255) / 256), 256, 0, stream>>>(fs, sc, n_windows);
   fifo_block_kernel<<<(unsigned)((n_windows + 255) / 256), 256, 0, stream>>>(fs, sc, n_windows);
   fifo_verify_kernel<<<(fs.n_procs + 3) / 4, 128, 0, stream>>>(fs, fifo, sc);
   {
-    uint64_t grid = (n_lookups + 255) / 256;
+    const uint64_t runs_max = 2 * (n_windows / kRun + fs.n_procs);
+    uint64_t grid = (runs_max / 2 + 7) / 8;
     const uint64_t cap = resident_grid((const void*)fifo_apply_kernel, 256, 0);
     if (grid > cap) grid = cap;
-    fifo_apply_kernel<<<(unsigned)grid, 256, 0, stream>>>(fs, sc, n_lookups, value, status, fb);
+    if (grid == 0) grid = 1;
+    fifo_apply_kernel<<<(unsigned)grid, 256, 0, stream>>>(fs, sc, runs_max, sc.run_off, value, status, fb);
   }
   return cudaGetLastError();
 }

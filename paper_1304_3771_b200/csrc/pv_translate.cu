@@ -5,11 +5,16 @@
 // ProcessTranslator resolve (memvirt.py:596-601) and resolve_hybrid
 // (memvirt.py:677-682).
 //
-// B200 design.  A CTA owns a contiguous run of 2048-lane chunks (mostly of
-// one segment = one address space).  On entering a space it stages the two
-// upper levels of each walk stage in shared memory as 4-byte codes, one per
-// mid-level entry of every present top entry (4 x 512 codes = 8 KiB per
-// stage):
+// B200 design.  CTAs take 2048-lane chunks in grid-stride order, so at any
+// moment the whole GPU walks one narrow band of the lane array -- one or two
+// address spaces -- and the random leaf gathers hit a few MiB of leaf index
+// that stays L2-resident (contiguous per-CTA ranges kept every space's index,
+// 65 MB at C5, live at once and re-fetched ~10 % of the gathers from HBM).
+// A pre-pass (stage_table_kernel, one CTA per segment) resolves the two
+// upper levels of each walk stage into 4-byte codes, one per mid-level entry
+// of every present top entry (4 x 512 codes = 8 KiB per stage); a CTA
+// entering a segment copies that table into shared memory with 512 16-byte
+// loads instead of re-walking the upper levels:
 //     bits 0-1  kind: 0 not present (fault at level 2), 1 present,
 //               2 trapping (trap at level 2), 3 the walk already stopped at
 //               level 1 / 2 (status precomputed per top entry)
@@ -114,6 +119,39 @@ __device__ void stage_codes(const uint8_t* __restrict__ image, uint64_t image_by
   __syncthreads();
 }
 
+// Per-segment stage tables, computed once per launch: for segment i,
+// codes[(2 i + k) * 2048 ...] and stages[2 i + k] of walk stage k (k = 1 only
+// for two-stage spaces).
+constexpr uint32_t kStageCodes = 4 * 512;
+
+__global__ void __launch_bounds__(256)
+stage_table_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const pv_space* __restrict__ spaces,
+                   const pv_seg* __restrict__ segs, bool kTwoAllowed, const uint32_t* __restrict__ slot_of,
+                   uint32_t* __restrict__ codes_out, Stage* __restrict__ stages_out) {
+  __shared__ __align__(16) uint32_t codes[kStageCodes];
+  __shared__ Stage st;
+  const uint32_t i = blockIdx.x;
+  const pv_space sp = spaces[segs[i].space];
+  const bool two = kTwoAllowed && sp.mode == PV_TWO_STAGE;
+  for (uint32_t k = 0; k < (two ? 2u : 1u); ++k) {
+    if (k == 0) stage_codes(image, image_bytes, sp.s1_base, sp.s1_root_pfn, 0, st, codes, slot_of);
+    else stage_codes(image, image_bytes, 0, sp.s2_root_pfn, 1, st, codes, slot_of);
+    uint4* dst = reinterpret_cast<uint4*>(codes_out + (2ull * i + k) * kStageCodes);
+    for (uint32_t j = threadIdx.x; j < kStageCodes / 4; j += blockDim.x) dst[j] = reinterpret_cast<const uint4*>(codes)[j];
+    if (threadIdx.x == 0) stages_out[2 * i + k] = st;
+    __syncthreads();
+  }
+}
+
+// Copy a segment's stage table into shared memory (all threads; CTA-uniform
+// call site; the caller brackets it with barriers).
+__device__ __forceinline__ void load_stage(const uint32_t* __restrict__ g_codes, const Stage* __restrict__ g_stages,
+                                           uint64_t t, uint32_t* codes, Stage& st) {
+  const uint4* src = reinterpret_cast<const uint4*>(g_codes + t * kStageCodes);
+  for (uint32_t j = threadIdx.x; j < kStageCodes / 4; j += blockDim.x) reinterpret_cast<uint4*>(codes)[j] = src[j];
+  if (threadIdx.x == 0) st = g_stages[t];
+}
+
 // Upper two levels of one stage for one lane from the code table.  `x` is
 // the address walked (va, or gpa in the TDP stage).  Returns PV_ST_OK when
 // the leaf PTE must be read (leaf node in *code_out >> 3), else the status.
@@ -179,23 +217,21 @@ template <bool kTwo, bool kVa32, bool kPfn, int TPB = kTpb, int MINB = (kTwo ? 3
 __global__ void __launch_bounds__(TPB, MINB)
 translate_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const pv_space* __restrict__ spaces,
                  const pv_seg* __restrict__ segs, uint32_t n_segs, uint64_t n_chunks, const void* __restrict__ vas,
-                 const uint32_t* __restrict__ slot_of, const uint32_t* __restrict__ leaf_codes,
-                 const uint64_t* __restrict__ slot_page,
+                 const uint32_t* __restrict__ g_codes, const Stage* __restrict__ g_stages,
+                 const uint32_t* __restrict__ leaf_codes, const uint64_t* __restrict__ slot_page,
                  uint64_t* __restrict__ out_value, uint32_t* __restrict__ out_status, uint64_t* __restrict__ out_aux) {
   constexpr int VPT = (int)(kChunk / TPB);
   __shared__ __align__(16) uint32_t codes1[4 * 512];
   __shared__ __align__(16) uint32_t codes2[kTwo ? 4 * 512 : 1];
   __shared__ Stage st1, st2;
 
-  const uint64_t c_begin = (n_chunks * blockIdx.x) / gridDim.x;
-  const uint64_t c_end = (n_chunks * (blockIdx.x + 1)) / gridDim.x;
-  // Segment and staged space live in registers; they are CTA-uniform, so
+  // Segment and staged segment live in registers; they are CTA-uniform, so
   // every branch on them is uniform.
   pv_seg seg;
   seg.begin = seg.end = seg.chunk0 = 0;
   seg.space = 0xFFFFFFFFu;
   uint64_t seg_chunks = 0;
-  uint32_t staged_space = 0xFFFFFFFFu;
+  uint32_t seg_idx = 0xFFFFFFFFu, staged_seg = 0xFFFFFFFFu;
   bool two = false;
   const uint64_t pol_stream = policy_evict_first(), pol_table = policy_evict_last();
 
@@ -207,6 +243,7 @@ translate_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const 
         if (segs[m].chunk0 <= c) lo = m; else hi = m;
       }
       seg = segs[lo];
+      seg_idx = lo;
       seg_chunks = (seg.end - seg.begin + kChunk - 1) / kChunk;
     }
   };
@@ -222,15 +259,15 @@ translate_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const 
 
   VaT va[VPT], nva[VPT];
   bool have_next = false;
-  for (uint64_t c = c_begin; c < c_end; ++c) {
+  for (uint64_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
     find_seg(c);
-    if (seg.space != staged_space) {
-      const pv_space sp = spaces[seg.space];
-      staged_space = seg.space;
-      two = kTwo && sp.mode == PV_TWO_STAGE;
-      __syncthreads();  // everyone is done with the previous staging
-      stage_codes(image, image_bytes, sp.s1_base, sp.s1_root_pfn, 0, st1, codes1, slot_of);
-      if (two) stage_codes(image, image_bytes, 0, sp.s2_root_pfn, 1, st2, codes2, slot_of);
+    if (seg_idx != staged_seg) {
+      staged_seg = seg_idx;
+      two = kTwo && spaces[seg.space].mode == PV_TWO_STAGE;
+      __syncthreads();  // everyone is done with the previous table
+      load_stage(g_codes, g_stages, 2ull * seg_idx, codes1, st1);
+      if (two) load_stage(g_codes, g_stages, 2ull * seg_idx + 1, codes2, st2);
+      __syncthreads();
     }
     if (have_next) {
 #pragma unroll
@@ -241,8 +278,9 @@ translate_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const 
     const uint64_t lane0 = seg.begin + (c - seg.chunk0) * kChunk;
     const uint64_t seg_end = seg.end;
     // Prefetch the next chunk's VAs when it is in the same segment.
-    have_next = c + 1 < c_end && c + 1 < seg.chunk0 + seg_chunks;
-    if (have_next) load_vas(c + 1, nva);
+    const uint64_t cn = c + gridDim.x;
+    have_next = cn < n_chunks && cn < seg.chunk0 + seg_chunks;
+    if (have_next) load_vas(cn, nva);
 
     // Fast path (one-stage walks): when every lane of this thread resolves
     // its upper levels to an indexed, in-image leaf node and its leaf code is
@@ -404,9 +442,20 @@ static cudaError_t launch_t(const uint8_t* image, uint64_t image_bytes, const pv
   const uint32_t* slot_of = idx != nullptr ? idx->slot_of : nullptr;
   const uint32_t* leaf_codes = idx != nullptr ? idx->leaf_codes : nullptr;
   const uint64_t* slot_page = idx != nullptr ? idx->slot_page : nullptr;
-  k<<<(unsigned)grid, tpb, 0, stream>>>(image, image_bytes, spaces, segs, n_segs, n_chunks, vas, slot_of,
+  // per-segment stage tables: stream-ordered scratch (per call, so calls on
+  // distinct streams never share it)
+  const size_t codes_bytes = 2ull * n_segs * kStageCodes * sizeof(uint32_t);
+  void* tab = nullptr;
+  cudaError_t e = stream_scratch(&tab, codes_bytes + 2ull * n_segs * sizeof(Stage), stream);
+  if (e != cudaSuccess) return e;
+  uint32_t* g_codes = static_cast<uint32_t*>(tab);
+  Stage* g_stages = reinterpret_cast<Stage*>(static_cast<uint8_t*>(tab) + codes_bytes);
+  stage_table_kernel<<<n_segs, 256, 0, stream>>>(image, image_bytes, spaces, segs, kTwo, slot_of, g_codes, g_stages);
+  k<<<(unsigned)grid, tpb, 0, stream>>>(image, image_bytes, spaces, segs, n_segs, n_chunks, vas, g_codes, g_stages,
                                         leaf_codes, slot_page, out_value, out_status, out_aux);
-  return cudaGetLastError();
+  e = cudaGetLastError();
+  cudaFreeAsync(tab, stream);
+  return e;
 }
 
 cudaError_t launch_translate(const uint8_t* image, uint64_t image_bytes, const pv_space* spaces, const pv_seg* segs,
