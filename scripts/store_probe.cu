@@ -1,0 +1,112 @@
+// Probe (not part of the product): does routing the walker's 12 B/lane of
+// results through shared memory + TMA bulk stores (cp.async.bulk.global.
+// shared::cta) relieve the L1->XBAR request port that bounds the walk
+// (ncu: l1tex__m_l1tex2xbar_req_cycles_active ~86 %)?  Each warp owns 128
+// consecutive lanes per step: u32 index in, one random 4-byte gather from a
+// 2 MiB table, u64 + u32 out.  Mode 0 stores from registers (the walker
+// today); mode 1 stages the warp's 1 KiB + 512 B of results in shared memory
+// and one lane bulk-stores them.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o scripts/store_probe.bin scripts/store_probe.cu
+#include <cstdint>
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ uint32_t ld_idx(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(512, 2) k(const uint32_t* __restrict__ idx, const uint32_t* __restrict__ tab,
+                                            uint32_t mask, uint64_t n, uint64_t* __restrict__ o64,
+                                            uint32_t* __restrict__ o32) {
+  constexpr int L = 4;
+  __shared__ __align__(128) uint64_t s64[2][16][128];
+  __shared__ __align__(128) uint32_t s32[2][16][128];
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t nwarps = (uint64_t)gridDim.x * 16;
+  int buf = 0;
+  for (uint64_t wb = ((uint64_t)blockIdx.x * 16 + warp) * 128; wb < n; wb += nwarps * 128) {
+    uint32_t v[L], r[L];
+#pragma unroll
+    for (int j = 0; j < L; ++j) v[j] = ld_idx(idx + wb + j * 32 + lane);
+#pragma unroll
+    for (int j = 0; j < L; ++j) r[j] = __ldg(tab + (v[j] & mask));
+    if (MODE == 0) {
+#pragma unroll
+      for (int j = 0; j < L; ++j) {
+        const uint64_t i = wb + j * 32 + lane;
+        o64[i] = ((uint64_t)r[j] << 12) | (v[j] & 0xFFF);
+        o32[i] = r[j] & 3;
+      }
+    } else {
+      // the buffer written two steps ago must have been read out by its bulk store
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < L; ++j) {
+        s64[buf][warp][j * 32 + lane] = ((uint64_t)r[j] << 12) | (v[j] & 0xFFF);
+        s32[buf][warp][j * 32 + lane] = r[j] & 3;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        const uint32_t a64 = (uint32_t)__cvta_generic_to_shared(&s64[buf][warp][0]);
+        const uint32_t a32 = (uint32_t)__cvta_generic_to_shared(&s32[buf][warp][0]);
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 1024;" ::"l"(o64 + wb), "r"(a64)
+                     : "memory");
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 512;" ::"l"(o32 + wb), "r"(a32)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+      buf ^= 1;
+    }
+  }
+  if (MODE == 1 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+int main() {
+  const uint64_t n = 128ull << 20;
+  const uint32_t words = 1u << 19;  // 2 MiB
+  uint32_t *idx, *tab, *o32;
+  uint64_t* o64;
+  cudaMalloc(&idx, n * 4);
+  cudaMalloc(&tab, (uint64_t)words * 4);
+  cudaMalloc(&o32, n * 4);
+  cudaMalloc(&o64, n * 8);
+  uint32_t* h = (uint32_t*)malloc(n * 4);
+  uint64_t s = 88172645463325252ull;
+  for (uint64_t i = 0; i < n; ++i) {
+    s ^= s << 13; s ^= s >> 7; s ^= s << 17;
+    h[i] = (uint32_t)s;
+  }
+  cudaMemcpy(idx, h, n * 4, cudaMemcpyHostToDevice);
+  cudaMemset(tab, 1, (uint64_t)words * 4);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  void (*fns[2])(const uint32_t*, const uint32_t*, uint32_t, uint64_t, uint64_t*, uint32_t*) = {k<0>, k<1>};
+  const char* names[2] = {"register stores", "smem + bulk stores"};
+  uint64_t* check = (uint64_t*)malloc(1 << 20);
+  for (int m = 0; m < 2; ++m) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaMemset(o64, 0, n * 8);
+    for (int w = 0; w < 3; ++w) fns[m]<<<sms * 2, 512>>>(idx, tab, words - 1, n, o64, o32);
+    cudaEventRecord(a);
+    const int reps = 10;
+    for (int r = 0; r < reps; ++r) fns[m]<<<sms * 2, 512>>>(idx, tab, words - 1, n, o64, o32);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    ms /= reps;
+    cudaMemcpy(check, o64 + (n - 131072), 1 << 20, cudaMemcpyDeviceToHost);
+    uint64_t bad = 0;
+    for (int i = 0; i < 131072; ++i) bad += check[i] != ((0x01010101ull << 12) | (h[n - 131072 + i] & 0xFFF));
+    printf("%-22s %.3f ms  %.1f G lanes/s  mismatches %llu  [%s]\n", names[m], ms, n / ms / 1e6,
+           (unsigned long long)bad, cudaGetErrorString(cudaGetLastError()));
+  }
+  return 0;
+}
