@@ -54,6 +54,15 @@ def parse():
     return ap.parse_args()
 
 
+def _pg() -> bool:
+    """A process group exists (torchrun); PV_BENCH_EMULATE=1 runs one rank's
+    share of an N-rank job alone (RANK / WORLD_SIZE set by hand, no group):
+    per-rank timing estimates on a one-GPU box, no max over ranks."""
+    import torch.distributed as tdist
+
+    return tdist.is_available() and tdist.is_initialized()
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -257,7 +266,7 @@ def run_ours(args, rank, world, local):
         img.note_device_write()
 
     def barrier():
-        if world > 1:
+        if world > 1 and tdist.is_initialized():
             tdist.barrier()
 
     for _ in range(args.warmup):
@@ -474,7 +483,7 @@ def run_c2(args, rank, world, local):
     clocks.start()
     time.sleep(0.3)
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
-    if world > 1:
+    if world > 1 and _pg():
         import torch.distributed as tdist
 
         tdist.barrier()
@@ -669,7 +678,7 @@ def run_c4(args, rank, world, local):
     clocks.start()
     time.sleep(0.3)
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
-    if world > 1:
+    if world > 1 and _pg():
         import torch.distributed as tdist
 
         tdist.barrier()
@@ -761,7 +770,7 @@ def run_e2e(wl, args, world):
         return t1 - t0, time.perf_counter() - t1
 
     one_step()  # warm (pinned pools, plans)
-    if world > 1:
+    if world > 1 and _pg():
         tdist.barrier()
     torch.cuda.synchronize()
     tr_s = cp_s = 0.0
@@ -976,7 +985,7 @@ def main():
     rank, world, local = dist_env()
     if args.gpus != world and world != 1:
         args.gpus = world
-    if world > 1:
+    if world > 1 and os.environ.get("PV_BENCH_EMULATE") != "1":
         import torch
         import torch.distributed as tdist
 
@@ -992,7 +1001,7 @@ def main():
         line = runner(args, rank, world, local)
     if rank == 0 and line is not None:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if world > 1 and _pg():
         import torch.distributed as tdist
 
         tdist.destroy_process_group()

@@ -66,10 +66,11 @@ __device__ __forceinline__ uint64_t ld_stream_va(const void* vas, uint64_t i, bo
 }
 
 // Stage the upper two levels of one walk stage (all threads; ends with a
-// barrier).  Requires image_bytes < 2^41 so leaf pfns fit 29 bits.
+// barrier): the Stage record and the 512 codes of top entry `t`, written to
+// codes[t * 512 ...].  Requires image_bytes < 2^41 so leaf pfns fit 29 bits.
 __device__ void stage_codes(const uint8_t* __restrict__ image, uint64_t image_bytes, uint64_t base, uint64_t root,
                             uint32_t stage2, Stage& s, uint32_t* codes /*[4*512]*/,
-                            const uint32_t* __restrict__ slot_of) {
+                            const uint32_t* __restrict__ slot_of, uint32_t t_sel) {
   const uint32_t tid = threadIdx.x;
   const uint64_t lim = node_limit(image_bytes, base);
   if (tid < 4) {
@@ -97,7 +98,7 @@ __device__ void stage_codes(const uint8_t* __restrict__ image, uint64_t image_by
     }
   }
   __syncthreads();
-  for (uint32_t i = tid; i < 4 * 512; i += blockDim.x) {
+  for (uint32_t i = t_sel * 512 + tid; i < (t_sel + 1) * 512; i += blockDim.x) {
     const uint32_t t = i >> 9;
     uint32_t code = kCodeStop;
     if (s.top_status[t] == PV_ST_OK) {
@@ -124,23 +125,22 @@ __device__ void stage_codes(const uint8_t* __restrict__ image, uint64_t image_by
 // for two-stage spaces).
 constexpr uint32_t kStageCodes = 4 * 512;
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(512)
 stage_table_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const pv_space* __restrict__ spaces,
                    const pv_seg* __restrict__ segs, bool kTwoAllowed, const uint32_t* __restrict__ slot_of,
                    uint32_t* __restrict__ codes_out, Stage* __restrict__ stages_out) {
+  // grid (n_segs, 4 top entries, 2 stages): 512 codes per CTA, one per thread
   __shared__ __align__(16) uint32_t codes[kStageCodes];
   __shared__ Stage st;
-  const uint32_t i = blockIdx.x;
+  const uint32_t i = blockIdx.x, t = blockIdx.y, k = blockIdx.z;
   const pv_space sp = spaces[segs[i].space];
   const bool two = kTwoAllowed && sp.mode == PV_TWO_STAGE;
-  for (uint32_t k = 0; k < (two ? 2u : 1u); ++k) {
-    if (k == 0) stage_codes(image, image_bytes, sp.s1_base, sp.s1_root_pfn, 0, st, codes, slot_of);
-    else stage_codes(image, image_bytes, 0, sp.s2_root_pfn, 1, st, codes, slot_of);
-    uint4* dst = reinterpret_cast<uint4*>(codes_out + (2ull * i + k) * kStageCodes);
-    for (uint32_t j = threadIdx.x; j < kStageCodes / 4; j += blockDim.x) dst[j] = reinterpret_cast<const uint4*>(codes)[j];
-    if (threadIdx.x == 0) stages_out[2 * i + k] = st;
-    __syncthreads();
-  }
+  if (k == 1 && !two) return;
+  if (k == 0) stage_codes(image, image_bytes, sp.s1_base, sp.s1_root_pfn, 0, st, codes, slot_of, t);
+  else stage_codes(image, image_bytes, 0, sp.s2_root_pfn, 1, st, codes, slot_of, t);
+  uint4* dst = reinterpret_cast<uint4*>(codes_out + (2ull * i + k) * kStageCodes + t * 512);
+  for (uint32_t j = threadIdx.x; j < 512 / 4; j += blockDim.x) dst[j] = reinterpret_cast<const uint4*>(codes + t * 512)[j];
+  if (threadIdx.x == 0 && t == 0) stages_out[2 * i + k] = st;
 }
 
 // Copy a segment's stage table into shared memory (all threads; CTA-uniform
@@ -450,7 +450,8 @@ static cudaError_t launch_t(const uint8_t* image, uint64_t image_bytes, const pv
   if (e != cudaSuccess) return e;
   uint32_t* g_codes = static_cast<uint32_t*>(tab);
   Stage* g_stages = reinterpret_cast<Stage*>(static_cast<uint8_t*>(tab) + codes_bytes);
-  stage_table_kernel<<<n_segs, 256, 0, stream>>>(image, image_bytes, spaces, segs, kTwo, slot_of, g_codes, g_stages);
+  stage_table_kernel<<<dim3(n_segs, 4, kTwo ? 2 : 1), 512, 0, stream>>>(image, image_bytes, spaces, segs, kTwo,
+                                                                         slot_of, g_codes, g_stages);
   k<<<(unsigned)grid, tpb, 0, stream>>>(image, image_bytes, spaces, segs, n_segs, n_chunks, vas, g_codes, g_stages,
                                         leaf_codes, slot_page, out_value, out_status, out_aux);
   e = cudaGetLastError();

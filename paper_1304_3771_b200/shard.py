@@ -80,9 +80,10 @@ def max_over_ranks(values: Iterable[float], world: int, device=None) -> list[flo
     import torch
 
     vals = list(values)
-    if world == 1:
-        return vals
     import torch.distributed as dist
+
+    if world == 1 or not dist.is_initialized():  # one rank, or one rank's share run alone
+        return vals
 
     t = torch.tensor(vals, dtype=torch.float64, device=None if _host_backend() else device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
