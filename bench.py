@@ -231,8 +231,7 @@ def run_ours(args, rank, world, local):
     s = stream.cuda_stream
     owner, _ = dp._owner_map(img)
     shim_scratch = dp._shim_scratch(img, plan.n_pages) if plan.shims is not None else None
-    hint = N.COPY_ALIGNED16 if (os.environ.get("PV_EXEC_ALIGNED") == "1" and plan.aligned16(wl.src.data_ptr())) \
-        else 0
+    hint = dp.exec_hint(plan, wl.src.data_ptr())
 
     def step(ev):
         ev[0].record(stream)

@@ -625,6 +625,13 @@ def _aligned16(plan: "CopyPlan", buf_ptr: int) -> bool:
 CopyPlan.aligned16 = lambda self, buf_ptr: _aligned16(self, buf_ptr)
 
 
+def exec_hint(plan: "CopyPlan", buf_ptr: int) -> int:
+    """pv_copy_exec flag selecting the TMA bulk path (host-proven alignment)."""
+    if os.environ.get("PV_EXEC_LSU") == "1":
+        return 0
+    return N.COPY_ALIGNED16 if plan.aligned16(buf_ptr) else 0
+
+
 def _owner_map(image):
     """Per-image conflict stamp map (one u64 per page) and epoch counter."""
     import torch
@@ -697,10 +704,10 @@ def copy_launch(image, plan: CopyPlan, direction: int, buf, *, fifo_dev=None, fi
                                       plan.conflict.data_ptr(), s), "pv_copy_stamp")
             abort = plan.conflict.data_ptr()
         dirty = image.dirty_map().data_ptr() if (direction == N.TO_GUEST and track_dirty) else None
-        # the 16-byte-only exec variant measured ~1 % slower than the generic
-        # one on B200 (scripts/exp_exec.py); opt in with PV_EXEC_ALIGNED=1
-        hint = N.COPY_ALIGNED16 if (os.environ.get("PV_EXEC_ALIGNED") == "1" and plan.aligned16(buf.data_ptr())) \
-            else 0
+        # batches whose buffer and guest pages are 16-byte co-aligned move
+        # through the TMA bulk exec (pv_copy.cu exec_bulk_kernel); the LSU exec
+        # takes the rest (PV_EXEC_LSU=1 forces it, for A/B runs)
+        hint = exec_hint(plan, buf.data_ptr())
         N.check(lib.pv_copy_exec(dev_img.data_ptr(), image.nbytes, plan.ops.data_ptr(), plan.n_ops,
                                  plan.page_off.data_ptr(), plan.n_pages, direction | hint, plan.page_hpa.data_ptr(),
                                  plan.page_status.data_ptr(), plan.page_aux.data_ptr(), plan.first_bad.data_ptr(),

@@ -616,3 +616,48 @@ def test_mixed_space_batch_segments_and_lane_formats(cuda, va32, out_pfn):
         assert np.array_equal(v.cpu().numpy().view(np.uint64), exp_v)
         assert np.array_equal(a.cpu().numpy().view(np.uint64), exp_a)
     assert len(set((exp_s & 0xFF0).tolist())) >= 4
+
+
+@pytest.mark.parametrize("mode", ["shadow", "tdp"])
+def test_tma_bulk_exec_coaligned_batches_vs_oracle(cuda, mode):
+    """The TMA bulk exec (pv_copy.cu exec_bulk_kernel) runs when the host
+    proves every op's buffer and guest address co-aligned mod 16: random
+    heads (< 16 B through the LSU), 16-byte middles through TMA, random
+    tails, ops over 1-6 pages, faulting pages mid-op, both directions,
+    against the sequential oracle byte for byte."""
+    w = S.c1_build(mv, be, er, mode)
+    memv, space = w["memv"], w["space"]
+    _corrupt(memv, space, mode)
+    tr = memv.translator(space, use_cache=False)
+    sp = tr.device_space
+    osp = O.space(sp.s1_base, sp.s1_root_pfn, sp.s2_root_pfn, sp.mode).reshape(1, 4)
+    img = memv.host_mem.backing
+    rng = random.Random(31 + len(mode))
+    n_ops = 700
+    res_mod = [rng.randrange(16) for _ in range(n_ops)]
+    gv = [S.C1_GVA + i * (96 << 10) + 16 * rng.randrange(256) + res_mod[i] for i in range(n_ops)]
+    ln = [rng.choice([rng.randrange(1, 64), rng.randrange(1, 6 * 4096), 4096, 3 * 4096]) for _ in range(n_ops)]
+    boff, off = [], 0
+    for i in range(n_ops):
+        off = (off + 15) // 16 * 16 + res_mod[i]  # buffer offset congruent to the gva mod 16
+        boff.append(off)
+        off += ln[i]
+    rows = np.stack([np.array(gv, np.uint64), np.array(ln, np.uint64), np.array(boff, np.uint64),
+                     np.zeros(n_ops, np.uint64)], 1)
+    plan = dp.CopyPlan([sp], rows)
+    for direction in (N.TO_GUEST, N.FROM_GUEST):
+        raw = np.frombuffer(S.image_bytes(memv.host_mem), dtype=np.uint8).copy()
+        src_h = np.frombuffer(random.Random(direction).randbytes(off + 64), dtype=np.uint8).copy()
+        buf = torch.from_numpy(src_h.copy()).cuda()
+        assert dp.exec_hint(plan, buf.data_ptr()) == N.COPY_ALIGNED16  # the bulk path is the one under test
+        dp.copy_launch(img, plan, direction, buf)
+        got = plan.results.cpu().numpy().view(np.uint64)
+        want = O.copy(raw, osp, rows, src_h, direction)
+        assert np.array_equal(got[:, 0], want[:, 0]) and np.array_equal(got[:, 3], want[:, 3])
+        if direction == N.TO_GUEST:
+            assert int(plan.conflict.item()) == 0
+            assert np.array_equal(np.frombuffer(S.image_bytes(memv.host_mem), dtype=np.uint8), raw)
+        else:
+            assert np.array_equal(buf.cpu().numpy(), src_h)
+        kinds = set((want[:, 3] & 0xFF0).tolist())
+        assert 0 in kinds and len(kinds) > 1  # complete ops and faulting ops both present
