@@ -66,11 +66,11 @@ __device__ __forceinline__ uint64_t ld_stream_va(const void* vas, uint64_t i, bo
 }
 
 // Stage the upper two levels of one walk stage (all threads; ends with a
-// barrier): the Stage record and the 512 codes of top entry `t`, written to
-// codes[t * 512 ...].  Requires image_bytes < 2^41 so leaf pfns fit 29 bits.
+// barrier): the Stage record and the 512 codes of each top entry t_sel ..
+// t_sel + t_cnt - 1, written to codes[t * 512 ...].  Requires image_bytes < 2^41 so leaf pfns fit 29 bits.
 __device__ void stage_codes(const uint8_t* __restrict__ image, uint64_t image_bytes, uint64_t base, uint64_t root,
                             uint32_t stage2, Stage& s, uint32_t* codes /*[4*512]*/,
-                            const uint32_t* __restrict__ slot_of, uint32_t t_sel) {
+                            const uint32_t* __restrict__ slot_of, uint32_t t_sel, uint32_t t_cnt) {
   const uint32_t tid = threadIdx.x;
   const uint64_t lim = node_limit(image_bytes, base);
   if (tid < 4) {
@@ -98,7 +98,7 @@ __device__ void stage_codes(const uint8_t* __restrict__ image, uint64_t image_by
     }
   }
   __syncthreads();
-  for (uint32_t i = t_sel * 512 + tid; i < (t_sel + 1) * 512; i += blockDim.x) {
+  for (uint32_t i = t_sel * 512 + tid; i < (t_sel + t_cnt) * 512; i += blockDim.x) {
     const uint32_t t = i >> 9;
     uint32_t code = kCodeStop;
     if (s.top_status[t] == PV_ST_OK) {
@@ -136,8 +136,8 @@ stage_table_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, cons
   const pv_space sp = spaces[segs[i].space];
   const bool two = kTwoAllowed && sp.mode == PV_TWO_STAGE;
   if (k == 1 && !two) return;
-  if (k == 0) stage_codes(image, image_bytes, sp.s1_base, sp.s1_root_pfn, 0, st, codes, slot_of, t);
-  else stage_codes(image, image_bytes, 0, sp.s2_root_pfn, 1, st, codes, slot_of, t);
+  if (k == 0) stage_codes(image, image_bytes, sp.s1_base, sp.s1_root_pfn, 0, st, codes, slot_of, t, 1);
+  else stage_codes(image, image_bytes, 0, sp.s2_root_pfn, 1, st, codes, slot_of, t, 1);
   uint4* dst = reinterpret_cast<uint4*>(codes_out + (2ull * i + k) * kStageCodes + t * 512);
   for (uint32_t j = threadIdx.x; j < 512 / 4; j += blockDim.x) dst[j] = reinterpret_cast<const uint4*>(codes + t * 512)[j];
   if (threadIdx.x == 0 && t == 0) stages_out[2 * i + k] = st;
@@ -218,7 +218,8 @@ __global__ void __launch_bounds__(TPB, MINB)
 translate_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const pv_space* __restrict__ spaces,
                  const pv_seg* __restrict__ segs, uint32_t n_segs, uint64_t n_chunks, const void* __restrict__ vas,
                  const uint32_t* __restrict__ g_codes, const Stage* __restrict__ g_stages,
-                 const uint32_t* __restrict__ leaf_codes, const uint64_t* __restrict__ slot_page,
+                 const uint32_t* __restrict__ slot_of, const uint32_t* __restrict__ leaf_codes,
+                 const uint64_t* __restrict__ slot_page,
                  uint64_t* __restrict__ out_value, uint32_t* __restrict__ out_status, uint64_t* __restrict__ out_aux) {
   constexpr int VPT = (int)(kChunk / TPB);
   __shared__ __align__(16) uint32_t codes1[4 * 512];
@@ -259,14 +260,27 @@ translate_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const 
 
   VaT va[VPT], nva[VPT];
   bool have_next = false;
-  for (uint64_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+  // Large batches (stage tables precomputed, g_codes != nullptr): grid-stride
+  // chunk order.  Small batches (a few chunks per CTA): contiguous chunk
+  // ranges and in-kernel staging -- no pre-pass launch, no scratch.
+  const bool pre = g_codes != nullptr;
+  const uint64_t c_first = pre ? blockIdx.x : (n_chunks * blockIdx.x) / gridDim.x;
+  const uint64_t c_last = pre ? n_chunks : (n_chunks * (blockIdx.x + 1)) / gridDim.x;
+  const uint64_t c_step = pre ? gridDim.x : 1;
+  for (uint64_t c = c_first; c < c_last; c += c_step) {
     find_seg(c);
     if (seg_idx != staged_seg) {
       staged_seg = seg_idx;
-      two = kTwo && spaces[seg.space].mode == PV_TWO_STAGE;
+      const pv_space sp = spaces[seg.space];
+      two = kTwo && sp.mode == PV_TWO_STAGE;
       __syncthreads();  // everyone is done with the previous table
-      load_stage(g_codes, g_stages, 2ull * seg_idx, codes1, st1);
-      if (two) load_stage(g_codes, g_stages, 2ull * seg_idx + 1, codes2, st2);
+      if (pre) {
+        load_stage(g_codes, g_stages, 2ull * seg_idx, codes1, st1);
+        if (two) load_stage(g_codes, g_stages, 2ull * seg_idx + 1, codes2, st2);
+      } else {
+        stage_codes(image, image_bytes, sp.s1_base, sp.s1_root_pfn, 0, st1, codes1, slot_of, 0, 4);
+        if (two) stage_codes(image, image_bytes, 0, sp.s2_root_pfn, 1, st2, codes2, slot_of, 0, 4);
+      }
       __syncthreads();
     }
     if (have_next) {
@@ -278,8 +292,8 @@ translate_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const 
     const uint64_t lane0 = seg.begin + (c - seg.chunk0) * kChunk;
     const uint64_t seg_end = seg.end;
     // Prefetch the next chunk's VAs when it is in the same segment.
-    const uint64_t cn = c + gridDim.x;
-    have_next = cn < n_chunks && cn < seg.chunk0 + seg_chunks;
+    const uint64_t cn = c + c_step;
+    have_next = cn < c_last && cn < seg.chunk0 + seg_chunks;
     if (have_next) load_vas(cn, nva);
 
     // Fast path (one-stage walks): when every lane of this thread resolves
@@ -425,23 +439,22 @@ template <bool kTwo, bool kVa32, bool kPfn>
 static cudaError_t launch_t(const uint8_t* image, uint64_t image_bytes, const pv_space* spaces, const pv_seg* segs,
                             uint32_t n_segs, uint64_t n_chunks, const void* vas, const pv_index* idx,
                             uint64_t* out_value, uint32_t* out_status, uint64_t* out_aux, cudaStream_t stream) {
-  auto k = translate_kernel<kTwo, kVa32, kPfn>;
-  int tpb = kTpb;
-  if (!kTwo) {
-    // one-stage walks: 512-thread CTAs x 4 lanes (2 CTAs/SM) measured best on
-    // the C5 walk (1.03 vs 1.05 ms at 256 x 8); tuning hook PV_TRANSLATE_TPB
-    static const char* env = getenv("PV_TRANSLATE_TPB");
-    const int want = env ? atoi(env) : 512;
-    if (want == 512) { k = translate_kernel<kTwo, kVa32, kPfn, 512, 2>; tpb = 512; }
-    if (want == 1024) { k = translate_kernel<kTwo, kVa32, kPfn, 1024, 1>; tpb = 1024; }
-    if (want == 128) { k = translate_kernel<kTwo, kVa32, kPfn, 128, 8>; tpb = 128; }
-  }
+  // one-stage walks: 512-thread CTAs x 4 lanes (2 CTAs/SM) measured best on
+  // C5 (scripts/ab_walk.sh: 0.848 ms vs 0.858 at 1024 x 2 and 0.923 at 128 x 16)
+  auto k = kTwo ? translate_kernel<kTwo, kVa32, kPfn> : translate_kernel<kTwo, kVa32, kPfn, 512, 2>;
+  const int tpb = kTwo ? kTpb : 512;
   uint64_t grid = resident_grid((const void*)k, tpb, 0);
   if (grid > n_chunks) grid = n_chunks;
   if (grid == 0) return cudaSuccess;
   const uint32_t* slot_of = idx != nullptr ? idx->slot_of : nullptr;
   const uint32_t* leaf_codes = idx != nullptr ? idx->leaf_codes : nullptr;
   const uint64_t* slot_page = idx != nullptr ? idx->slot_page : nullptr;
+  if (n_chunks < 8 * grid) {
+    // few chunks per CTA: each CTA stages its (usually one) segment itself
+    k<<<(unsigned)grid, tpb, 0, stream>>>(image, image_bytes, spaces, segs, n_segs, n_chunks, vas, nullptr, nullptr,
+                                          slot_of, leaf_codes, slot_page, out_value, out_status, out_aux);
+    return cudaGetLastError();
+  }
   // per-segment stage tables: stream-ordered scratch (per call, so calls on
   // distinct streams never share it)
   const size_t codes_bytes = 2ull * n_segs * kStageCodes * sizeof(uint32_t);
@@ -453,7 +466,7 @@ static cudaError_t launch_t(const uint8_t* image, uint64_t image_bytes, const pv
   stage_table_kernel<<<dim3(n_segs, 4, kTwo ? 2 : 1), 512, 0, stream>>>(image, image_bytes, spaces, segs, kTwo,
                                                                          slot_of, g_codes, g_stages);
   k<<<(unsigned)grid, tpb, 0, stream>>>(image, image_bytes, spaces, segs, n_segs, n_chunks, vas, g_codes, g_stages,
-                                        leaf_codes, slot_page, out_value, out_status, out_aux);
+                                        slot_of, leaf_codes, slot_page, out_value, out_status, out_aux);
   e = cudaGetLastError();
   cudaFreeAsync(tab, stream);
   return e;

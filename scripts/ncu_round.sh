@@ -4,7 +4,7 @@
 # 2. one `--set full` capture of each dominant kernel at full size (DRAM bytes -> roofline traffic).
 tag=${1:-prof}
 mkdir -p gpurun_out
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"^(translate|plan|stamp|exec|shim)" -c 16 --csv \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"^(translate|stage|plan|stamp|exec|shim)" -c 16 --csv \
   --log-file gpurun_out/${tag}_launches_c5.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline \
   > gpurun_out/${tag}_launch_c5.json 2> gpurun_out/${tag}_launch_c5.err
 echo "c5 launch list rc=$?"
@@ -13,7 +13,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --kernel-n
   > gpurun_out/${tag}_launch_c2.json 2> gpurun_out/${tag}_launch_c2.err
 echo "c2 launch list rc=$?"
 timeout 1200 ncu --set full --clock-control none --import-source on \
-  -k regex:"translate_kernel|exec_kernel" -c 2 -o gpurun_out/${tag}_c5_full \
+  -k regex:"translate_kernel|exec_bulk_kernel|exec_kernel" -c 2 -o gpurun_out/${tag}_c5_full \
   python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/${tag}_c5_full.log 2>&1
 echo "c5 full rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on \
