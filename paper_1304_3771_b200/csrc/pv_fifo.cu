@@ -307,7 +307,10 @@ __device__ __forceinline__ bool run_of_slot(const uint64_t* run_off, uint32_t n_
   return r < run_off[n_procs];
 }
 
-__global__ void fifo_spec_kernel(FifoStream fs, const pv_fifo* __restrict__ fifo, Scratch sc, uint64_t n_slots_max,
+#ifndef PV_FIFO_SPEC_MINB
+#define PV_FIFO_SPEC_MINB 4
+#endif
+__global__ void __launch_bounds__(256, PV_FIFO_SPEC_MINB) fifo_spec_kernel(FifoStream fs, const pv_fifo* __restrict__ fifo, Scratch sc, uint64_t n_slots_max,
                                  const uint64_t* __restrict__ run_off, unsigned long long* first_bad) {
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;

@@ -38,18 +38,42 @@ struct __align__(16) ChunkDesc {
   uint32_t pad;
 };
 
-// One thread per op: keys[p] = destination page of live page p (else the
-// dead key, which sorts last), vals[p] = p, desc[p] = p's chunk descriptor.
+__device__ __forceinline__ void write_result(const pv_op& o, uint64_t p0, uint64_t p1, uint64_t bad,
+                                             const uint64_t* __restrict__ page_hpa,
+                                             const uint32_t* __restrict__ page_status,
+                                             const uint64_t* __restrict__ page_aux, pv_op_result* __restrict__ out) {
+  pv_op_result r;
+  if (bad == kNone || p1 == p0) {
+    r.copied = o.len;
+    r.value = r.aux = 0;
+    r.status = PV_ST_OK;
+    r.fail_page = 0;
+  } else {
+    const uint64_t p = p0 + bad;
+    r.copied = op_page_va(o.gva, bad) - o.gva;
+    r.value = page_hpa[p];
+    r.aux = page_aux != nullptr ? page_aux[p] : 0;
+    r.status = page_status[p];
+    r.fail_page = (uint32_t)bad;
+  }
+  *out = r;
+}
+
+// One thread per op: the op's result (copied prefix / first failure), and
+// per page keys[p] = destination page of live page p (else the dead key,
+// which sorts last), vals[p] = p, desc[p] = p's chunk descriptor.
 __global__ void ordered_keys_kernel(const pv_op* __restrict__ ops, uint64_t n_ops, const uint64_t* __restrict__ page_off,
-                                    const uint64_t* __restrict__ page_hpa,
+                                    const uint64_t* __restrict__ page_hpa, const uint32_t* __restrict__ page_status,
+                                    const uint64_t* __restrict__ page_aux,
                                     const unsigned long long* __restrict__ first_bad, const uint8_t* __restrict__ buf,
                                     uint32_t dead_key, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
-                                    ChunkDesc* __restrict__ desc) {
+                                    ChunkDesc* __restrict__ desc, pv_op_result* __restrict__ results) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_ops; i += stride) {
     const pv_op o = ops[i];
     const uint64_t p0 = page_off[i], p1 = page_off[i + 1];
     const uint64_t bad = first_bad[i];
+    write_result(o, p0, p1, bad, page_hpa, page_status, page_aux, results + i);
     for (uint64_t p = p0; p < p1; ++p) {
       const uint64_t k = p - p0;
       const uint64_t hpa = page_hpa[p];
@@ -338,31 +362,15 @@ ordered_apply_kernel(uint8_t* __restrict__ image, const ChunkDesc* __restrict__ 
 }
 
 // Per-op results (the exec kernel's result rule, for ops run in order).
+// Results only (a batch without pages: nothing to sort or apply).
 __global__ void ordered_results_kernel(const pv_op* __restrict__ ops, uint64_t n_ops,
                                        const uint64_t* __restrict__ page_off, const uint64_t* __restrict__ page_hpa,
                                        const uint32_t* __restrict__ page_status, const uint64_t* __restrict__ page_aux,
                                        const unsigned long long* __restrict__ first_bad,
                                        pv_op_result* __restrict__ results) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_ops; i += stride) {
-    const pv_op o = ops[i];
-    const uint64_t bad = first_bad[i];
-    pv_op_result r;
-    if (bad == kNone || page_off[i + 1] == page_off[i]) {
-      r.copied = o.len;
-      r.value = r.aux = 0;
-      r.status = PV_ST_OK;
-      r.fail_page = 0;
-    } else {
-      const uint64_t p = page_off[i] + bad;
-      r.copied = op_page_va(o.gva, bad) - o.gva;
-      r.value = page_hpa[p];
-      r.aux = page_aux != nullptr ? page_aux[p] : 0;
-      r.status = page_status[p];
-      r.fail_page = (uint32_t)bad;
-    }
-    results[i] = r;
-  }
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_ops; i += stride)
+    write_result(ops[i], page_off[i], page_off[i + 1], first_bad[i], page_hpa, page_status, page_aux, results + i);
 }
 
 struct OrderedScratch {
@@ -421,14 +429,14 @@ cudaError_t launch_copy_ordered(uint8_t* image, uint64_t image_bytes, const pv_o
                                 const uint32_t* page_status, const uint64_t* page_aux, const uint64_t* op_first_bad,
                                 const uint8_t* buf, pv_op_result* results, uint8_t* dirty, void* scratch,
                                 uint64_t scratch_bytes, cudaStream_t stream) {
-  {
+  if (n_pages == 0) {
     uint64_t g = (n_ops + 255) / 256;
     if (g > 4096) g = 4096;
     if (g) ordered_results_kernel<<<(unsigned)g, 256, 0, stream>>>(
         ops, n_ops, page_off, page_hpa, page_status, page_aux,
         reinterpret_cast<const unsigned long long*>(op_first_bad), results);
+    return cudaGetLastError();
   }
-  if (n_pages == 0) return cudaGetLastError();
   const uint64_t image_pages = image_bytes >> kPageShift;
   if (n_pages >= 0xFFFFFFFFull || image_pages >= 0xFFFFFFFFull) return cudaErrorInvalidValue;
   const uint32_t dead_key = (uint32_t)image_pages;
@@ -439,9 +447,9 @@ cudaError_t launch_copy_ordered(uint8_t* image, uint64_t image_bytes, const pv_o
   {
     uint64_t g = (n_ops + 255) / 256;
     if (g > 8192) g = 8192;
-    ordered_keys_kernel<<<(unsigned)g, 256, 0, stream>>>(ops, n_ops, page_off, page_hpa,
+    ordered_keys_kernel<<<(unsigned)g, 256, 0, stream>>>(ops, n_ops, page_off, page_hpa, page_status, page_aux,
                                                          reinterpret_cast<const unsigned long long*>(op_first_bad),
-                                                         buf, dead_key, s.keys_in, s.vals_in, s.desc);
+                                                         buf, dead_key, s.keys_in, s.vals_in, s.desc, results);
   }
   size_t tb = s.cub_bytes;
   cudaError_t e = cub::DeviceRadixSort::SortPairs(s.cub_tmp, tb, s.keys_in, s.keys_out, s.vals_in, s.vals_out,
