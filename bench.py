@@ -753,15 +753,18 @@ def run_e2e(wl, args, world):
     for t, *_ in payload:
         t.random_(0, 256)
 
-    h2d = sum(t.numel() * 4 for t, _, _ in host_vas) + sum(t.numel() for t, *_ in payload)
-    d2h = sum(t.numel() * 12 for t, _, _ in host_vas) + sum(len(ops) * 32 for *_, ops in payload)
-
+    from paper_1304_3771_b200 import dataplane as dp
     from paper_1304_3771_b200 import memvirt as mv
+
+    io = {}
 
     def one_step():
         t0 = time.perf_counter()
         mv.translate_many([(translators[(g, p)], t) for t, g, p in host_vas])
         t1 = time.perf_counter()
+        # counted from the tensors moved: VAs in; values + per-chunk fault flags (+ the statuses of
+        # chunks that faulted) out -- see dataplane.translate_host_many
+        io["h2d"], io["d2h"] = dp.last_host_io["h2d"], dp.last_host_io["d2h"]
         for t, g, p, ops in payload:
             outs = recs[(g, p)].copy_to_user_batch(ops[:, 0], ops[:, 1], t)
             assert all(isinstance(o, int) for o in outs)
@@ -781,6 +784,8 @@ def run_e2e(wl, args, world):
     from paper_1304_3771_b200 import shard
 
     tr_s, cp_s = shard.max_over_ranks([tr_s, cp_s], world, device="cuda")
+    h2d = io["h2d"] + sum(t.numel() for t, *_ in payload)
+    d2h = io["d2h"] + sum(len(ops) * 32 for *_, ops in payload)
     return {"value": wl.total_vas * steps / tr_s, "unit": "translations/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "copy": {"value": wl.total_copy_bytes * steps / cp_s / 1e9, "unit": "GB/s"},

@@ -396,6 +396,10 @@ def translate_host_pipelined(image, space: Space, host_vas, chunk: int = 1 << 23
     return translate_host_many(image, [(space, host_vas)], chunk=chunk)[0]
 
 
+# bytes the last translate_host_many call moved each way (bench accounting)
+last_host_io = {"h2d": 0, "d2h": 0}
+
+
 def translate_host_many(image, jobs, chunk: int = 1 << 23):
     """Translate several host VA tensors (``jobs = [(space, vas), ...]``) in
     one pipeline: chunks of every job stream through two device buffer sets,
@@ -428,6 +432,8 @@ def translate_host_many(image, jobs, chunk: int = 1 << 23):
         outs.append((value, status, aux))
         for start in range(0, n, chunk):
             work.append((space, two, src, value, status, aux, start, min(chunk, n - start)))
+    last_host_io["h2d"] = sum(w[2].element_size() * w[7] for w in work)
+    last_host_io["d2h"] = sum(w[7] * (20 if w[1] else 12) for w in work)  # value + status (+ aux)
     if not work:
         return outs
     compute = torch.cuda.current_stream()

@@ -329,6 +329,7 @@ def test_host_pipelined_translate_equals_device_path(cuda, mode):
     assert (hs != 0).any() and (hs == 0).any()
 
 
+
 def _fifo_world(mode="shadow", pages=40):
     memv = mv.MemoryVirtualizer()
     g = memv.add_guest(0, mode)
