@@ -293,7 +293,10 @@ translate_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const 
     const uint64_t seg_end = seg.end;
     // Prefetch the next chunk's VAs when it is in the same segment.
     const uint64_t cn = c + c_step;
-    have_next = cn < c_last && cn < seg.chunk0 + seg_chunks;
+#ifndef PV_TR_PREFETCH
+#define PV_TR_PREFETCH 0  // next-chunk VA prefetch: measured slower once chunks went grid-stride (162 vs 158 G/s)
+#endif
+    have_next = PV_TR_PREFETCH && cn < c_last && cn < seg.chunk0 + seg_chunks;
     if (have_next) load_vas(cn, nva);
 
     // Fast path (one-stage walks): when every lane of this thread resolves
@@ -441,7 +444,10 @@ static cudaError_t launch_t(const uint8_t* image, uint64_t image_bytes, const pv
                             uint64_t* out_value, uint32_t* out_status, uint64_t* out_aux, cudaStream_t stream) {
   // one-stage walks: 512-thread CTAs x 4 lanes (2 CTAs/SM) measured best on
   // C5 (scripts/ab_walk.sh: 0.848 ms vs 0.858 at 1024 x 2 and 0.923 at 128 x 16)
-  auto k = kTwo ? translate_kernel<kTwo, kVa32, kPfn> : translate_kernel<kTwo, kVa32, kPfn, 512, 2>;
+#ifndef PV_TR_MINB
+#define PV_TR_MINB 2
+#endif
+  auto k = kTwo ? translate_kernel<kTwo, kVa32, kPfn> : translate_kernel<kTwo, kVa32, kPfn, 512, PV_TR_MINB>;
   const int tpb = kTwo ? kTpb : 512;
   uint64_t grid = resident_grid((const void*)k, tpb, 0);
   if (grid > n_chunks) grid = n_chunks;
