@@ -180,9 +180,11 @@ typedef struct pv_fifo {
 #define PV_TO_GUEST 0u   /* copy_to_user  : buffer -> guest pages           */
 #define PV_FROM_GUEST 1u /* copy_from_user: guest pages -> buffer           */
 /* pv_copy_exec direction hint (or-ed in): for every op,
- * (gva - (buf + buf_off)) % 16 == 0, so every chunk moves with 16-byte
- * vectors (a lighter kernel with twice the resident warps).  Chunks that do
- * not satisfy it are still copied correctly, byte-wise. */
+ * (gva - (buf + buf_off)) % 16 == 0, so every chunk's 16-byte-aligned middle
+ * moves through the Tensor Memory Accelerator (cp.async.bulk global -> shared
+ * -> global, a 6-stage ring per warp) and only its < 16-byte head / tail
+ * through the LSU.  Chunks that do not satisfy it are still copied correctly,
+ * through the LSU. */
 #define PV_COPY_ALIGNED16 0x100u
 
 /* ---- library ------------------------------------------------------------ */
@@ -221,7 +223,8 @@ int pv_translate(const uint8_t* image, uint64_t image_bytes,
  * fifo[] (device) is updated in place (entries rewritten oldest-first with
  * head 0, counters advanced).  Exact; parallel over 32-lookup windows with
  * sequential verification (see pv_fifo.cu).  scratch: device memory of
- * pv_fifo_scratch_bytes(lookups, windows, capacity) bytes.
+ * pv_fifo_scratch_bytes(lookups, windows, capacity) bytes.  At most 65536
+ * processes per call (PV_EINVAL / CUDA invalid-value beyond).
  */
 uint64_t pv_fifo_scratch_bytes(uint64_t n_lookups, uint64_t n_windows, uint32_t capacity);
 
