@@ -347,9 +347,12 @@ def run_ours(args, rank, world, local):
                           "gather_sol": walker_sol(wl.n_vas * K / (tr_ms / 1e3))},
         "faulting_lanes": n_faults,
         "gather_to_rank0": gather,
-        "gpu_launches": (4 + (2 if wl.cplan.shims is not None else 0)) * K,
-        "gpu_launches_note": "translate, plan, stamp, exec per step (+ the trap shim for hybrid copies: "
-                             "eval + one cooperative resolve kernel that returns at once when nothing traps)",
+        "gpu_launches": (4 + (1 if wl.n_vas >= 8 * 296 * 2048 else 0) + 1
+                         + (2 if wl.cplan.shims is not None else 0)) * K,
+        "gpu_launches_note": "per step: stage-table pre-pass (batches of >= 8 chunks per CTA), translate, "
+                             "leaf-index re-encode of pages the previous step's copies dirtied, plan, stamp, "
+                             "exec (TMA bulk path), + the hybrid trap shim (eval + one cooperative resolve kernel "
+                             "that returns at once when nothing traps); 3 torch fills not counted",
         "clocks": clk,
         "e2e": e2e,
         "build_s": wl.build_s,
@@ -535,9 +538,10 @@ def run_c2(args, rank, world, local):
                      "traffic": traffic_for(load_traffic("c2"), "ordered_apply", alg_bytes), "launch_ms": per_launch_ms, "alg_bytes_per_launch": alg_bytes,
                      "note": "payload bytes read once + each destination page staged and written back once, "
                              "over the apply kernel's event-timed launch duration (pv_timing)"},
-        "gpu_launches": 14 * K, "gpu_launches_note": "frame pack, identify, classify (+ CUB select), plan, 4 FIFO-replay "
-                                                     "steps, stamp, exec (stands down), "
-                                                     "results, keys, apply per step + CUB sort/RLE/scan kernels",
+        "gpu_launches": 15 * K, "gpu_launches_note": "per step: frame pack, identify, classify, plan, 6 FIFO-replay "
+                                                     "kernels (runs, spec, link, block, verify, apply), stamp, exec "
+                                                     "(stands down), ordered keys (+ results), gather, apply; CUB "
+                                                     "select / radix sort / RLE / scan kernels not counted",
         "clocks": clk, "build_s": build_s,
     }
 
