@@ -13,10 +13,13 @@
 //   plan  : one thread per 4 pages walks each page (L1-cached upper levels,
 //           one dependent load per level) and records the op's first failing
 //           page with a u64 atomicMin;
-//   exec  : one warp per page chunk moves up to 4 KiB with 16-byte vector
-//           loads/stores (8 x 16 B in flight per lane, all loads issued
-//           before the stores), realigning with funnel shifts when source and
-//           destination disagree modulo 4, byte loops only for heads/tails.
+//   exec  : batches whose buffer and guest addresses agree modulo 16 (the
+//           host proves it) move through TMA bulk copies (exec_bulk_kernel);
+//           the rest: one warp per page chunk moves up to 4 KiB with 16-byte
+//           vector loads/stores (8 x 16 B in flight per lane, all loads
+//           issued before the stores), realigning with funnel shifts when
+//           source and destination disagree modulo 4, byte loops only for
+//           heads/tails.
 // A separate stamp pass detects two pages of one to_guest batch landing on
 // the same hpa page (order-dependent last-writer-wins), which the host then
 // re-plans sequentially.
@@ -183,38 +186,7 @@ __device__ __forceinline__ void warp_copy(uint8_t* __restrict__ d, const uint8_t
   if (lane < tail) d[done + lane] = s[done + lane];
 }
 
-// Copy with 16-byte vectors only, for chunks whose source and destination
-// agree modulo 16 (the host proves it per batch: (gva - src) mod 16 is an op
-// constant); a chunk that does not qualify still copies correctly byte-wise.
-__device__ __forceinline__ void warp_copy_aligned(uint8_t* __restrict__ d, const uint8_t* __restrict__ s, uint32_t n,
-                                                  uint32_t lane, uint64_t pol) {
-  const uintptr_t da = reinterpret_cast<uintptr_t>(d), sa = reinterpret_cast<uintptr_t>(s);
-  if (((da ^ sa) & 15) != 0) {
-    warp_copy_bytes(d, s, n, lane);
-    return;
-  }
-  const uint32_t head = min(n, (uint32_t)((16 - (da & 15)) & 15));
-  if (lane < head) d[lane] = s[lane];
-  const uint32_t nv = (n - head) >> 4;
-  const uint4* sv = reinterpret_cast<const uint4*>(s + head);
-  uint4* dv = reinterpret_cast<uint4*>(d + head);
-  uint4 r[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const uint32_t i = lane + 32 * j;
-    if (i < nv) r[j] = ld_v4_stream(sv + i, pol);
-  }
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const uint32_t i = lane + 32 * j;
-    if (i < nv) st_v4_stream(dv + i, r[j], pol);
-  }
-  const uint32_t done = head + (nv << 4), tail = n - done;
-  if (lane < tail) d[done + lane] = s[done + lane];
-}
-
-template <bool kAligned>
-__global__ void __launch_bounds__(kExecTpb, kAligned ? 4 : 2)
+__global__ void __launch_bounds__(kExecTpb, 2)
 exec_kernel(uint8_t* __restrict__ image, uint64_t image_bytes, const pv_op* __restrict__ ops, uint64_t n_ops,
             const uint64_t* __restrict__ page_off, uint64_t n_pages, uint32_t direction,
             const uint64_t* __restrict__ page_hpa, const uint32_t* __restrict__ page_status,
@@ -269,8 +241,7 @@ exec_kernel(uint8_t* __restrict__ image, uint64_t image_bytes, const pv_op* __re
       uint8_t* bp = buf + o.buf_off + done;
       uint8_t* dst = direction == PV_TO_GUEST ? image + hpa : bp;
       const uint8_t* src = direction == PV_TO_GUEST ? bp : image + hpa;
-      if (kAligned) warp_copy_aligned(dst, src, chunk, lane, pol);
-      else warp_copy(dst, src, chunk, lane, pol);
+      warp_copy(dst, src, chunk, lane, pol);
       if (direction == PV_TO_GUEST && dirty != nullptr && lane == 0) dirty[hpa >> kPageShift] = 1;
     }
   }
@@ -496,7 +467,7 @@ cudaError_t launch_copy_exec(uint8_t* image, uint64_t image_bytes, const pv_op* 
         reinterpret_cast<const unsigned long long*>(op_first_bad), buf, results, dirty, abort_flag);
     return cudaGetLastError();
   }
-  auto k = exec_kernel<false>;
+  auto k = exec_kernel;
   const uint64_t warps = (n_pages + kExecPpw - 1) / kExecPpw;
   uint64_t grid = (warps + kExecWarps - 1) / kExecWarps;
   const uint64_t cap = resident_grid((const void*)k, kExecTpb, 0);
