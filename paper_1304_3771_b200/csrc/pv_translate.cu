@@ -395,8 +395,14 @@ translate_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const 
 // Generic form for batches that contain extension-geometry spaces
 // (PV_ONE_STAGE_4L): every lane walks through L1/L2-cached global loads
 // (translate_global), 8 lanes per thread.
+#ifndef PV_GEN_TPB
+#define PV_GEN_TPB 256
+#endif
+constexpr int kGenTpb = PV_GEN_TPB;
+constexpr int kGenVpt = (int)(kChunk / kGenTpb);
+
 template <bool kVa32, bool kPfn>
-__global__ void __launch_bounds__(kTpb)
+__global__ void __launch_bounds__(kGenTpb)
 translate_generic_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes,
                          const pv_space* __restrict__ spaces, const pv_seg* __restrict__ segs, uint32_t n_segs,
                          uint64_t n_chunks, const void* __restrict__ vas, uint64_t* __restrict__ out_value,
@@ -411,8 +417,8 @@ translate_generic_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes
     const pv_space sp = spaces[seg.space];
     const uint64_t lane0 = seg.begin + (c - seg.chunk0) * kChunk;
 #pragma unroll
-    for (int j = 0; j < kVpt; ++j) {
-      const uint64_t i = lane0 + (uint64_t)j * kTpb + threadIdx.x;
+    for (int j = 0; j < kGenVpt; ++j) {
+      const uint64_t i = lane0 + (uint64_t)j * kGenTpb + threadIdx.x;
       if (i >= seg.end) continue;
       const uint64_t va = kVa32 ? (uint64_t)((const uint32_t*)vas)[i] : ((const uint64_t*)vas)[i];
       uint64_t v = 0, a = 0;
@@ -430,10 +436,10 @@ static cudaError_t launch_generic(const uint8_t* image, uint64_t image_bytes, co
                                   const pv_seg* segs, uint32_t n_segs, uint64_t n_chunks, const void* vas,
                                   uint64_t* out_value, uint32_t* out_status, uint64_t* out_aux, cudaStream_t stream) {
   auto k = translate_generic_kernel<kVa32, kPfn>;
-  uint64_t grid = resident_grid((const void*)k, kTpb, 0);
+  uint64_t grid = resident_grid((const void*)k, kGenTpb, 0);
   if (grid > n_chunks) grid = n_chunks;
   if (grid == 0) return cudaSuccess;
-  k<<<(unsigned)grid, kTpb, 0, stream>>>(image, image_bytes, spaces, segs, n_segs, n_chunks, vas, out_value,
+  k<<<(unsigned)grid, kGenTpb, 0, stream>>>(image, image_bytes, spaces, segs, n_segs, n_chunks, vas, out_value,
                                          out_status, out_aux);
   return cudaGetLastError();
 }
