@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--gather", action="store_true", help="return every guest's translations to rank 0 after "
                     "timing (point-to-point over NCCL = NVLink peer copies) and report its time")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch the C5 step phases eagerly instead of "
+                    "replaying CUDA graphs of them")
     ap.add_argument("--cpu-sample-vas", type=int, default=16 << 20)
     ap.add_argument("--cpu-sample-bytes", type=int, default=1 << 30)
     return ap.parse_args()
@@ -233,34 +235,57 @@ def run_ours(args, rank, world, local):
     shim_scratch = dp._shim_scratch(img, plan.n_pages) if plan.shims is not None else None
     hint = dp.exec_hint(plan, wl.src.data_ptr())
 
-    def step(ev):
-        ev[0].record(stream)
+    def phase_translate():
         dp.translate_lanes(img, wl.tplan, wl.vas, out=wl.out)
-        ev[1].record(stream)
+
+    def phase_plan():  # fills + plan + trap shim + conflict stamp
+        cs = torch.cuda.current_stream().cuda_stream
         plan.first_bad.fill_(-1)
         plan.results.zero_()
         plan.conflict.zero_()
-        ev[2].record(stream)
         N.check(lib.pv_copy_plan(dev.data_ptr(), img.nbytes, plan.spaces.data_ptr(), plan.ops.data_ptr(),
                                  plan.n_ops, plan.page_off.data_ptr(), plan.n_pages, N.TO_GUEST,
                                  plan.page_hpa.data_ptr(), plan.page_status.data_ptr(), plan.page_aux.data_ptr(),
-                                 plan.first_bad.data_ptr(), None, 0, None, s), "plan")
+                                 plan.first_bad.data_ptr(), None, 0, None, cs), "plan")
         if plan.shims is not None:  # the hybrid resolver's trap shim (none trap in C5: empty passes)
             N.check(lib.pv_copy_shim(dev.data_ptr(), img.nbytes, plan.spaces.data_ptr(), plan.shims.data_ptr(),
                                      plan.ops.data_ptr(), plan.n_ops, plan.page_off.data_ptr(), plan.n_pages,
                                      plan.page_hpa.data_ptr(), plan.page_status.data_ptr(), plan.first_bad.data_ptr(),
                                      img.dirty_map().data_ptr(), plan.shim_written.data_ptr(), shim_scratch.data_ptr(),
-                                     shim_scratch.numel(), s), "shim")
+                                     shim_scratch.numel(), cs), "shim")
+        # a captured step keeps this epoch: its stamps (epoch, chunk) repeat identically, never a conflict
         img._epoch += 1
         N.check(lib.pv_copy_stamp(plan.page_off.data_ptr(), plan.n_ops, plan.n_pages, plan.page_hpa.data_ptr(),
                                   plan.first_bad.data_ptr(), owner.data_ptr(), img.npages, img._epoch,
-                                  plan.conflict.data_ptr(), s), "stamp")
-        ev[3].record(stream)
+                                  plan.conflict.data_ptr(), cs), "stamp")
+
+    def phase_exec():
+        cs = torch.cuda.current_stream().cuda_stream
         N.check(lib.pv_copy_exec(dev.data_ptr(), img.nbytes, plan.ops.data_ptr(), plan.n_ops,
                                  plan.page_off.data_ptr(), plan.n_pages, N.TO_GUEST | hint, plan.page_hpa.data_ptr(),
                                  plan.page_status.data_ptr(), plan.page_aux.data_ptr(), plan.first_bad.data_ptr(),
                                  wl.src.data_ptr(), wl.src.numel(), plan.results.data_ptr(),
-                                 img.dirty_map().data_ptr(), plan.conflict.data_ptr(), s), "exec")
+                                 img.dirty_map().data_ptr(), plan.conflict.data_ptr(), cs), "exec")
+
+    graphs = None
+
+    def step(ev):
+        ev[0].record(stream)
+        if graphs:
+            graphs[0].replay()
+        else:
+            phase_translate()
+        ev[1].record(stream)
+        ev[2].record(stream)
+        if graphs:
+            graphs[1].replay()
+        else:
+            phase_plan()
+        ev[3].record(stream)
+        if graphs:
+            graphs[2].replay()
+        else:
+            phase_exec()
         ev[4].record(stream)
         img.note_device_write()
 
@@ -271,6 +296,26 @@ def run_ours(args, rank, world, local):
     for _ in range(args.warmup):
         step([torch.cuda.Event(enable_timing=True) for _ in range(5)])
     torch.cuda.synchronize()
+    launch_mode = "eager"
+    if not args.no_graph:
+        # CUDA graphs of the three phases (the kernels and their arguments are identical every step),
+        # replayed between the per-phase events: no per-launch host/driver gaps inside a phase
+        try:
+            gs = [torch.cuda.CUDAGraph() for _ in range(3)]
+            for g, fn in zip(gs, (phase_translate, phase_plan, phase_exec)):
+                with torch.cuda.graph(g):
+                    fn()
+            img.note_device_write()
+            torch.cuda.synchronize()
+            graphs = gs
+            for _ in range(2):
+                step([torch.cuda.Event(enable_timing=True) for _ in range(5)])
+            torch.cuda.synchronize()
+            launch_mode = "cuda_graph"
+        except Exception as exc:  # noqa: BLE001 - eager launches are the same kernels
+            graphs = None
+            launch_mode = f"eager (graph capture failed: {type(exc).__name__}: {str(exc)[:120]})"
+            torch.cuda.synchronize()
 
     clocks = ClockSampler(local)
     clocks.start()
@@ -349,6 +394,7 @@ def run_ours(args, rank, world, local):
         "gather_to_rank0": gather,
         "gpu_launches": (4 + (1 if wl.n_vas >= 8 * 296 * 2048 else 0) + 1
                          + (2 if wl.cplan.shims is not None else 0)) * K,
+        "launch": launch_mode,
         "gpu_launches_note": "per step: stage-table pre-pass (batches of >= 8 chunks per CTA), translate, "
                              "leaf-index re-encode of pages the previous step's copies dirtied, plan, stamp, "
                              "exec (TMA bulk path), + the hybrid trap shim (eval + one cooperative resolve kernel "
