@@ -379,7 +379,9 @@ def run_ours(args, rank, world, local):
                  "ms_per_step": copy_ms / K, "exec_ms_per_step": exec_ms / K,
                  "plan_shim_stamp_ms_per_step": plan_ms / K},
         "translate_ms_per_step": tr_ms / K,
-        "roofline": {"bound": "hbm", "kernel": "pv_copy_exec (exec_kernel)", "achieved": exec_achieved,
+        "roofline": {"bound": "hbm",
+                     "kernel": "pv_copy_exec (" + ("exec_bulk_kernel, TMA" if hint else "exec_kernel, LSU") + ")",
+                     "achieved": exec_achieved,
                      "peak": peak, "unit": "GB/s", "frac": exec_achieved / peak, "peak_source": peak_kind,
                      "traffic": traffic_for(traffic, "exec", 2 * wl.copy_bytes),
                      "algorithmic_bytes_per_launch": 2 * wl.copy_bytes},
