@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define PV_ABI_VERSION 1
+#define PV_ABI_VERSION 2
 
 /* ---- return codes ------------------------------------------------------ */
 #define PV_SUCCESS 0
@@ -224,7 +224,9 @@ int pv_translate(const uint8_t* image, uint64_t image_bytes,
  * head 0, counters advanced).  Exact; parallel over 32-lookup windows with
  * sequential verification (see pv_fifo.cu).  scratch: device memory of
  * pv_fifo_scratch_bytes(lookups, windows, capacity) bytes.  At most 65536
- * processes per call (PV_EINVAL / CUDA invalid-value beyond).
+ * processes per call (PV_EINVAL / CUDA invalid-value beyond).  n_lookups and
+ * n_windows must equal proc_off[n_procs] and win_off[n_procs] (the device
+ * arrays are not read back: the call never synchronises the stream).
  */
 uint64_t pv_fifo_scratch_bytes(uint64_t n_lookups, uint64_t n_windows, uint32_t capacity);
 
@@ -232,7 +234,8 @@ uint64_t pv_fifo_scratch_bytes(uint64_t n_lookups, uint64_t n_windows, uint32_t 
  * key = vas[lane] >> 12.  flags: PV_VA32 as for pv_translate. */
 int pv_fifo_replay(const void* vas, uint32_t flags, const uint64_t* lane_idx,
                    const uint64_t* proc_off, const uint64_t* win_off,
-                   uint32_t n_procs, uint32_t capacity, pv_fifo* fifo,
+                   uint32_t n_procs, uint64_t n_lookups, uint64_t n_windows,
+                   uint32_t capacity, pv_fifo* fifo,
                    uint64_t* value, uint32_t* status, void* scratch,
                    uint64_t scratch_bytes, void* stream);
 
@@ -292,7 +295,8 @@ int pv_copy_stamp(const uint64_t* page_off, uint64_t n_ops, uint64_t n_pages,
 int pv_copy_fifo_replay(const pv_op* ops, const uint64_t* page_off,
                         const uint64_t* look_page, const uint32_t* look_op,
                         const uint64_t* proc_off, const uint64_t* win_off,
-                        uint32_t n_procs, uint32_t capacity, pv_fifo* fifo,
+                        uint32_t n_procs, uint64_t n_lookups, uint64_t n_windows,
+                        uint32_t capacity, pv_fifo* fifo,
                         uint64_t image_bytes, uint64_t* page_hpa,
                         uint32_t* page_status, uint64_t* op_first_bad,
                         void* scratch, uint64_t scratch_bytes, void* stream);

@@ -18,7 +18,7 @@ from .errors import NativeUnavailable
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpv.so")
 
 # ---- constants mirrored from include/pv.h --------------------------------
-ABI_VERSION = 1
+ABI_VERSION = 2
 SUCCESS = 0
 EINVAL = -22
 ENOMEM = -12
@@ -83,7 +83,7 @@ _SIGNATURES = {
     "pv_status_name": (ctypes.c_char_p, [_u32]),
     "pv_translate": (ctypes.c_int, [_p, _u64, _p, _p, _u32, _u64, _p, _u32, _p, _p, _p, _p, _p]),
     "pv_index_encode": (ctypes.c_int, [_p, _u64, _p, _p, _u64, _u64, _p, _p, _p]),
-    "pv_fifo_replay": (ctypes.c_int, [_p, _u32, _p, _p, _p, _u32, _u32, _p, _p, _p, _p, _u64, _p]),
+    "pv_fifo_replay": (ctypes.c_int, [_p, _u32, _p, _p, _p, _u32, _u64, _u64, _u32, _p, _p, _p, _p, _u64, _p]),
     "pv_fifo_scratch_bytes": (_u64, [_u64, _u64, _u32]),
     "pv_copy_ordered_scratch_bytes": (_u64, [_u64, _u64]),
     "pv_copy_shim_scratch_bytes": (_u64, [_u64]),
@@ -102,8 +102,8 @@ _SIGNATURES = {
     "pv_copy_plan": (ctypes.c_int, [_p, _u64, _p, _p, _u64, _p, _u64, _u32, _p, _p, _p, _p, _p, _u32, _p, _p]),
     "pv_copy_stamp": (ctypes.c_int, [_p, _u64, _u64, _p, _p, _p, _u64, _u32, _p, _p]),
     "pv_copy_exec": (ctypes.c_int, [_p, _u64, _p, _u64, _p, _u64, _u32, _p, _p, _p, _p, _p, _u64, _p, _p, _p, _p]),
-    "pv_copy_fifo_replay": (ctypes.c_int, [_p, _p, _p, _p, _p, _p, _u32, _u32, _p, _u64, _p, _p, _p, _p, _u64,
-                                            _p]),
+    "pv_copy_fifo_replay": (ctypes.c_int, [_p, _p, _p, _p, _p, _p, _u32, _u64, _u64, _u32, _p, _u64, _p, _p, _p,
+                                            _p, _u64, _p]),
     "pv_scatter_pages": (ctypes.c_int, [_p, _u64, _p, _u64, _p, _p]),
     "pv_gather_pages": (ctypes.c_int, [_p, _u64, _p, _u64, _p, _p]),
     "pv_stream_sync": (ctypes.c_int, [_p]),

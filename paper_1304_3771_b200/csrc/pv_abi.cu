@@ -50,10 +50,11 @@ cudaError_t launch_copy_ordered(uint8_t*, uint64_t, const pv_op*, uint64_t, cons
                                 const uint32_t*, const uint64_t*, const uint64_t*, const uint8_t*, pv_op_result*,
                                 uint8_t*, void*, uint64_t, cudaStream_t);
 cudaError_t launch_fifo_lanes_abi(const void*, uint32_t, const uint64_t*, const uint64_t*, const uint64_t*, uint32_t,
-                                  uint32_t, pv_fifo*, uint64_t*, uint32_t*, void*, uint64_t, cudaStream_t);
+                                  uint64_t, uint64_t, uint32_t, pv_fifo*, uint64_t*, uint32_t*, void*, uint64_t,
+                                  cudaStream_t);
 cudaError_t launch_fifo_copy_abi(const pv_op*, const uint64_t*, const uint64_t*, const uint32_t*, const uint64_t*,
-                                 const uint64_t*, uint32_t, uint32_t, pv_fifo*, uint64_t, uint64_t*, uint32_t*,
-                                 uint64_t*, void*, uint64_t, cudaStream_t);
+                                 const uint64_t*, uint32_t, uint64_t, uint64_t, uint32_t, pv_fifo*, uint64_t, uint64_t*,
+                                 uint32_t*, uint64_t*, void*, uint64_t, cudaStream_t);
 
 namespace {
 struct TimedLaunch {
@@ -226,13 +227,14 @@ uint64_t pv_fifo_scratch_bytes(uint64_t n_lookups, uint64_t n_windows, uint32_t 
 }
 
 int pv_fifo_replay(const void* vas, uint32_t flags, const uint64_t* lane_idx, const uint64_t* proc_off,
-                   const uint64_t* win_off, uint32_t n_procs, uint32_t capacity, pv_fifo* fifo, uint64_t* value,
-                   uint32_t* status, void* scratch, uint64_t scratch_bytes, void* stream) {
+                   const uint64_t* win_off, uint32_t n_procs, uint64_t n_lookups, uint64_t n_windows,
+                   uint32_t capacity, pv_fifo* fifo, uint64_t* value, uint32_t* status, void* scratch,
+                   uint64_t scratch_bytes, void* stream) {
   if (n_procs == 0) return PV_SUCCESS;
   if (!vas || !lane_idx || !proc_off || !win_off || !fifo || !value || !status || !scratch) return PV_EINVAL;
   if (capacity < 1 || capacity > PV_FIFO_MAX) return PV_EINVAL;
-  return rc(launch_fifo_lanes_abi(vas, flags, lane_idx, proc_off, win_off, n_procs, capacity, fifo, value, status,
-                                  scratch, scratch_bytes, (cudaStream_t)stream));
+  return rc(launch_fifo_lanes_abi(vas, flags, lane_idx, proc_off, win_off, n_procs, n_lookups, n_windows, capacity,
+                                  fifo, value, status, scratch, scratch_bytes, (cudaStream_t)stream));
 }
 
 int pv_copy_plan(const uint8_t* image, uint64_t image_bytes, const pv_space* spaces, const pv_op* ops,
@@ -280,17 +282,18 @@ int pv_copy_exec(uint8_t* image, uint64_t image_bytes, const pv_op* ops, uint64_
 }
 
 int pv_copy_fifo_replay(const pv_op* ops, const uint64_t* page_off, const uint64_t* look_page, const uint32_t* look_op,
-                        const uint64_t* proc_off, const uint64_t* win_off, uint32_t n_procs, uint32_t capacity,
-                        pv_fifo* fifo, uint64_t image_bytes, uint64_t* page_hpa, uint32_t* page_status,
-                        uint64_t* op_first_bad, void* scratch, uint64_t scratch_bytes, void* stream) {
+                        const uint64_t* proc_off, const uint64_t* win_off, uint32_t n_procs, uint64_t n_lookups,
+                        uint64_t n_windows, uint32_t capacity, pv_fifo* fifo, uint64_t image_bytes,
+                        uint64_t* page_hpa, uint32_t* page_status, uint64_t* op_first_bad, void* scratch,
+                        uint64_t scratch_bytes, void* stream) {
   if (n_procs == 0) return PV_SUCCESS;
   if (!ops || !page_off || !look_page || !look_op || !proc_off || !win_off || !fifo || !page_hpa || !page_status ||
       !op_first_bad || !scratch)
     return PV_EINVAL;
   if (capacity < 1 || capacity > PV_FIFO_MAX) return PV_EINVAL;
-  return rc(launch_fifo_copy_abi(ops, page_off, look_page, look_op, proc_off, win_off, n_procs, capacity, fifo,
-                                 image_bytes, page_hpa, page_status, op_first_bad, scratch, scratch_bytes,
-                                 (cudaStream_t)stream));
+  return rc(launch_fifo_copy_abi(ops, page_off, look_page, look_op, proc_off, win_off, n_procs, n_lookups, n_windows,
+                                 capacity, fifo, image_bytes, page_hpa, page_status, op_first_bad, scratch,
+                                 scratch_bytes, (cudaStream_t)stream));
 }
 
 uint64_t pv_copy_shim_scratch_bytes(uint64_t n_pages) { return shim_scratch_bytes(n_pages); }

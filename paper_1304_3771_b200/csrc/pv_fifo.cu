@@ -602,17 +602,11 @@ cudaError_t launch_fifo_stream(const FifoStream& fs, pv_fifo* fifo, void* scratc
   return cudaGetLastError();
 }
 
-// Window totals need the lookup counts: read from the offsets on the host
-// side of the launch (they are small device arrays; copied synchronously).
-static uint64_t last_u64(const uint64_t* dev_arr, uint32_t idx, cudaStream_t stream) {
-  uint64_t v = 0;
-  cudaMemcpyAsync(&v, dev_arr + idx, sizeof(v), cudaMemcpyDeviceToHost, stream);
-  cudaStreamSynchronize(stream);
-  return v;
-}
-
+// n_lookups / n_windows come from the caller (proc_off[n_procs] and
+// win_off[n_procs]): the launch never reads device memory back.
 cudaError_t launch_fifo_lanes_abi(const void* vas, uint32_t flags, const uint64_t* lane_idx, const uint64_t* proc_off,
-                                  const uint64_t* win_off, uint32_t n_procs, uint32_t cap, pv_fifo* fifo,
+                                  const uint64_t* win_off, uint32_t n_procs, uint64_t n_lookups, uint64_t n_windows,
+                                  uint32_t cap, pv_fifo* fifo,
                                   uint64_t* value, uint32_t* status, void* scratch, uint64_t scratch_bytes,
                                   cudaStream_t stream) {
   FifoStream fs{};
@@ -627,15 +621,14 @@ cudaError_t launch_fifo_lanes_abi(const void* vas, uint32_t flags, const uint64_
   fs.status = status;
   fs.cap = cap;
   fs.state_words = 2 * cap + 1;
-  const uint64_t n_lookups = last_u64(proc_off, n_procs, stream);
-  const uint64_t n_windows = last_u64(win_off, n_procs, stream);
   if (scratch_bytes < fifo_scratch_bytes(n_lookups, n_windows, cap)) return cudaErrorInvalidValue;
   return launch_fifo_stream(fs, fifo, scratch, n_lookups, n_windows, value, status, nullptr, stream);
 }
 
 cudaError_t launch_fifo_copy_abi(const pv_op* ops, const uint64_t* page_off, const uint64_t* look_page,
                                  const uint32_t* look_op, const uint64_t* proc_off, const uint64_t* win_off,
-                                 uint32_t n_procs, uint32_t cap, pv_fifo* fifo, uint64_t image_bytes,
+                                 uint32_t n_procs, uint64_t n_lookups, uint64_t n_windows, uint32_t cap, pv_fifo* fifo,
+                                 uint64_t image_bytes,
                                  uint64_t* page_hpa, uint32_t* page_status, uint64_t* op_first_bad, void* scratch,
                                  uint64_t scratch_bytes, cudaStream_t stream) {
   FifoStream fs{};
@@ -651,8 +644,6 @@ cudaError_t launch_fifo_copy_abi(const pv_op* ops, const uint64_t* page_off, con
   fs.status = page_status;
   fs.cap = cap;
   fs.state_words = 2 * cap + 1;
-  const uint64_t n_lookups = last_u64(proc_off, n_procs, stream);
-  const uint64_t n_windows = last_u64(win_off, n_procs, stream);
   if (scratch_bytes < fifo_scratch_bytes(n_lookups, n_windows, cap)) return cudaErrorInvalidValue;
   return launch_fifo_stream(fs, fifo, scratch, n_lookups, n_windows, page_hpa, page_status, op_first_bad, stream);
 }

@@ -539,7 +539,8 @@ def fifo_replay_lanes(vas, lane_idx, proc_off: np.ndarray, fifo_dev, value, stat
     off_d = _to_dev(np.asarray(proc_off, dtype=np.int64))
     win_d = _to_dev(win)
     N.check(lib.pv_fifo_replay(vas.data_ptr(), flags, lane_idx.data_ptr(), off_d.data_ptr(), win_d.data_ptr(),
-                               len(proc_off) - 1, capacity, fifo_dev.data_ptr(), value.data_ptr(),
+                               len(proc_off) - 1, int(proc_off[-1]), int(win[-1]), capacity, fifo_dev.data_ptr(),
+                               value.data_ptr(),
                                status.data_ptr(), scratch.data_ptr(), nbytes, _stream().cuda_stream),
             "pv_fifo_replay")
 
@@ -698,7 +699,8 @@ def copy_launch(image, plan: CopyPlan, direction: int, buf, *, fifo_dev=None, fi
             N.check(lib.pv_copy_fifo_replay(plan.ops.data_ptr(), plan.page_off.data_ptr(),
                                             plan.fifo_look_page.data_ptr(), plan.fifo_look_op.data_ptr(),
                                             plan.fifo_off.data_ptr(), plan.fifo_win_d.data_ptr(),
-                                            plan.fifo_off.numel() - 1, cap, fifo_dev.data_ptr(), image.nbytes,
+                                            plan.fifo_off.numel() - 1, plan.fifo_lookups, int(plan.fifo_win[-1]), cap,
+                                            fifo_dev.data_ptr(), image.nbytes,
                                             plan.page_hpa.data_ptr(), plan.page_status.data_ptr(),
                                             plan.first_bad.data_ptr(), scratch.data_ptr(), nbytes, s),
                     "pv_copy_fifo_replay")

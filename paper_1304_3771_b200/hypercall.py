@@ -232,8 +232,12 @@ def pack_device(ops, vcpu, cr3, tags, *, n_frames: int | None = None):
     import torch
 
     n = ops.shape[0]
-    per = 1 + (ops[:, 0] == int(FileOpKind.PAGE_FAULT)).to(torch.int64)
-    frame_off = torch.cumsum(per, 0) - per
+    if n_frames is not None and n_frames == n:
+        # the caller vouches for one frame per op (no PAGE_FAULT op): frame i is op i's
+        frame_off = torch.arange(n, dtype=torch.int64, device="cuda")
+    else:
+        per = 1 + (ops[:, 0] == int(FileOpKind.PAGE_FAULT)).to(torch.int64)
+        frame_off = torch.cumsum(per, 0) - per
     m = n_frames if n_frames is not None else (int(frame_off[-1].item() + per[-1].item()) if n else 0)
     frames = torch.empty(max(m, 1) * N.FRAME_BYTES, dtype=torch.uint8, device="cuda")
     status = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
