@@ -713,18 +713,49 @@ def run_c4(args, rank, world, local):
                                      saved.data_ptr(), s), "scatter")
         img.note_device_write()
 
-    def step(ev):
-        ev[0].record(stream)
+    def phase_translate():
         dp.translate_lanes(img, tplan, vas, out=out)
-        ev[1].record(stream)
+
+    def phase_copy():
         cplan.shim_written.zero_()
         dp.copy_launch(img, cplan, N.TO_GUEST, src)
+
+    graphs = None
+
+    def step(ev):
+        ev[0].record(stream)
+        graphs[0].replay() if graphs else phase_translate()
+        ev[1].record(stream)
+        graphs[1].replay() if graphs else phase_copy()
         ev[2].record(stream)
+        img.note_device_write()
 
     for _ in range(args.warmup):
         restore()
         step([torch.cuda.Event(enable_timing=True) for _ in range(3)])
     torch.cuda.synchronize()
+    launch_mode = "eager"
+    if not args.no_graph:
+        # the two phases as CUDA graphs (same kernels, same arguments every step; the shim's data-dependent
+        # work -- which slots trap, which page claims them -- is decided on the device each replay)
+        try:
+            restore()
+            gs = [torch.cuda.CUDAGraph() for _ in range(2)]
+            for g, fn in zip(gs, (phase_translate, phase_copy)):
+                with torch.cuda.graph(g):
+                    fn()
+            img.note_device_write()
+            torch.cuda.synchronize()
+            graphs = gs
+            for _ in range(2):
+                restore()
+                step([torch.cuda.Event(enable_timing=True) for _ in range(3)])
+            torch.cuda.synchronize()
+            launch_mode = "cuda_graph"
+        except Exception as exc:  # noqa: BLE001 - eager launches are the same kernels
+            graphs = None
+            launch_mode = f"eager (graph capture failed: {type(exc).__name__}: {str(exc)[:120]})"
+            torch.cuda.synchronize()
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
@@ -770,6 +801,7 @@ def run_c4(args, rank, world, local):
         "roofline": {"bound": "hbm", "kernel": "translate_kernel", "achieved": walk_ach, "peak": peak,
                      "unit": "GB/s", "frac": walk_ach / peak, "peak_source": peak_kind,
                      "note": "16 B/translation; 1 M lanes fit L2, so this line is latency-bound, not HBM-bound"},
+        "launch": launch_mode,
         "gpu_launches": 7 * K, "gpu_launches_note": "translate, plan, shim eval + cooperative resolve, stamp, exec per step (+ leaf-index re-encode)",
         "clocks": clk, "build_s": build_s,
     }
