@@ -16,8 +16,10 @@ import numpy as np
 import pytest
 import torch
 
+import scenarios as S
 from oracle import oracle as O
 from paper_1304_3771_b200 import _native as N
+from paper_1304_3771_b200 import has as be
 from paper_1304_3771_b200 import dataplane as dp
 from paper_1304_3771_b200 import memvirt as mv
 from paper_1304_3771_b200 import shard
@@ -131,3 +133,70 @@ def test_bench_two_ranks_one_device(cuda, tmp_path):
     assert line["n_gpus"] == 2 and line["value"] > 0 and line["faulting_lanes"] == 0
     assert line["gather_to_rank0"]["complete"] is True
     assert line["config"]["sharding"] == "guest g -> rank g mod 2"
+
+
+@pytest.mark.gpu
+def test_graph_replayed_step_equals_eager(cuda):
+    """bench.py replays its step phases as CUDA graphs: a captured translate
+    (large enough for the stage-table pre-pass and its stream-ordered
+    scratch) + hybrid copy batch (device trap shim: cooperative kernel, 10 %
+    trapping leaves) replayed once must leave exactly what the eager launches
+    leave -- lane results, op results and every byte of memory."""
+
+    def world():
+        memv, guest, space = W.build_c1("shadow", device=True)
+        W.corrupt_c4(memv, space, "shadow")
+        rec = be.GuestProcessRecord(S._Guest(0, "shadow"), space, memv)
+        acc = be.HardwareHasAccess(rec, memv)
+        tr = memv.translator(space, use_cache=False)
+        return memv, space, acc, tr
+
+    rng = np.random.default_rng(11)
+    vas_h = (W.C1_GVA + rng.integers(0, 64 << 20, 5 << 20)).astype(np.uint32)
+    n_ops, op_len = 1024, 16 << 10
+    gv = np.uint64(W.C1_GVA) + np.arange(n_ops, dtype=np.uint64) * np.uint64(op_len) + np.uint64(0x40)
+    rows = np.stack([gv, np.full(n_ops, op_len - 0x80, np.uint64), np.arange(n_ops, dtype=np.uint64) * np.uint64(op_len),
+                     np.zeros(n_ops, np.uint64)], 1)
+    src = torch.randint(0, 256, (n_ops * op_len,), dtype=torch.uint8, device="cuda",
+                        generator=torch.Generator(device="cuda").manual_seed(5))
+    outs = []
+    for graphed in (False, True):
+        memv, space, acc, tr = world()
+        img = memv.host_mem.backing
+        vas = torch.from_numpy(vas_h.view(np.int32)).cuda()
+        tplan = dp.TranslatePlan([tr.device_space], [(0, len(vas_h), 0)], image=img)
+        cplan = dp.CopyPlan([acc._resolver.device_space], rows, shims=[acc._resolver.device_shim])
+        out = (torch.empty(len(vas_h), dtype=torch.int64, device="cuda"),
+               torch.empty(len(vas_h), dtype=torch.int32, device="cuda"),
+               torch.zeros(len(vas_h), dtype=torch.int64, device="cuda"))
+        dp.translate_lanes(img, tplan, vas, out=out)  # leaf index built outside any capture
+        dp._shim_scratch(img, cplan.n_pages)
+        dp._owner_map(img)
+        torch.cuda.synchronize()
+
+        def phase_translate():
+            dp.translate_lanes(img, tplan, vas, out=out)
+
+        def phase_copy():
+            cplan.shim_written.zero_()
+            dp.copy_launch(img, cplan, N.TO_GUEST, src)
+
+        if graphed:
+            gs = [torch.cuda.CUDAGraph() for _ in range(2)]
+            for g, fn in zip(gs, (phase_translate, phase_copy)):
+                with torch.cuda.graph(g):
+                    fn()
+            out[0].fill_(-1)
+            for g in gs:
+                g.replay()
+        else:
+            phase_translate()
+            phase_copy()
+        img.note_device_write()
+        torch.cuda.synchronize()
+        outs.append((out[0].cpu().numpy(), out[1].cpu().numpy(), cplan.results.cpu().numpy(),
+                     int(cplan.shim_written.item()), _raw(memv)))
+    (v0, s0, r0, w0, m0), (v1, s1, r1, w1, m1) = outs
+    assert w0 > 0 and w0 == w1  # the shim fixed trapping slots in both
+    assert (s0 != 0).any() and np.array_equal(s0, s1) and np.array_equal(v0, v1)
+    assert np.array_equal(r0, r1) and np.array_equal(m0, m1)
