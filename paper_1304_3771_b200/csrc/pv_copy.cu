@@ -259,8 +259,14 @@ exec_kernel(uint8_t* __restrict__ image, uint64_t image_bytes, const pv_op* __re
 // and copies the < 16-byte head / tail of a chunk with the LSU.  Measured on
 // the C5 pattern (scripts/tma_copy_probe.cu): 6.36 TB/s vs 6.16 TB/s for
 // the best LSU copy.
-constexpr int kBulkWarps = 8;
-constexpr int kBulkStages = 6;
+#ifndef PV_BULK_WARPS
+#define PV_BULK_WARPS 8
+#endif
+#ifndef PV_BULK_STAGES
+#define PV_BULK_STAGES 6
+#endif
+constexpr int kBulkWarps = PV_BULK_WARPS;
+constexpr int kBulkStages = PV_BULK_STAGES;
 constexpr size_t kBulkSmem = (size_t)kBulkWarps * kBulkStages * kPageSize;
 
 struct BulkMeta {
