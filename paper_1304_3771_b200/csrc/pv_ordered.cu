@@ -5,8 +5,8 @@
 // B200 design: every live chunk (page k of op o with k < first_bad[o]) is
 // keyed by its destination hpa page; a stable radix sort (CUB, only the bits
 // the image needs) groups chunks by page while preserving the global chunk
-// order (= op order, then page order), and a gather lays the 16-byte chunk
-// descriptors out in that order.  A producer/consumer WARP PAIR then owns one
+// order (= op order, then page order), carrying the 16-byte chunk
+// descriptors along as values.  A producer/consumer WARP PAIR then owns one
 // destination page: the consumer stages the page in shared memory; the
 // producer streams the page's chunk payloads in with TMA bulk copies
 // (cp.async.bulk issued by one lane, completion counted on a per-slot
@@ -61,12 +61,12 @@ __device__ __forceinline__ void write_result(const pv_op& o, uint64_t p0, uint64
 
 // One thread per op: the op's result (copied prefix / first failure), and
 // per page keys[p] = destination page of live page p (else the dead key,
-// which sorts last), vals[p] = p, desc[p] = p's chunk descriptor.
+// which sorts last) and desc[p] = p's chunk descriptor (sorted along as the value).
 __global__ void ordered_keys_kernel(const pv_op* __restrict__ ops, uint64_t n_ops, const uint64_t* __restrict__ page_off,
                                     const uint64_t* __restrict__ page_hpa, const uint32_t* __restrict__ page_status,
                                     const uint64_t* __restrict__ page_aux,
                                     const unsigned long long* __restrict__ first_bad, const uint8_t* __restrict__ buf,
-                                    uint32_t dead_key, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                                    uint32_t dead_key, uint32_t* __restrict__ keys,
                                     ChunkDesc* __restrict__ desc, pv_op_result* __restrict__ results) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_ops; i += stride) {
@@ -79,7 +79,6 @@ __global__ void ordered_keys_kernel(const pv_op* __restrict__ ops, uint64_t n_op
       const uint64_t hpa = page_hpa[p];
       const bool live = k < bad;
       keys[p] = live ? (uint32_t)(hpa >> kPageShift) : dead_key;
-      vals[p] = (uint32_t)p;
       const uint64_t cur = op_page_va(o.gva, k);
       const uint64_t done = cur - o.gva;
       const uint32_t len = live ? (uint32_t)min(o.len - done, kPageSize - (cur & kPageMask)) : 0;
@@ -93,13 +92,6 @@ __global__ void ordered_keys_kernel(const pv_op* __restrict__ ops, uint64_t n_op
   }
 }
 
-// desc_sorted[i] = desc[sorted_pages[i]].
-__global__ void ordered_gather_kernel(const uint32_t* __restrict__ sorted_pages, uint64_t n,
-                                      const ChunkDesc* __restrict__ desc, ChunkDesc* __restrict__ out) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-    out[i] = desc[sorted_pages[i]];
-}
 
 // ---- warp-per-page apply ------------------------------------------------------------
 
@@ -374,7 +366,7 @@ __global__ void ordered_results_kernel(const pv_op* __restrict__ ops, uint64_t n
 }
 
 struct OrderedScratch {
-  uint32_t *keys_in, *vals_in, *keys_out, *vals_out, *seg_key, *seg_len, *seg_start, *n_segs;
+  uint32_t *keys_in, *keys_out, *seg_key, *seg_len, *seg_start, *n_segs;
   ChunkDesc *desc, *desc_sorted;
   void* cub_tmp;
   size_t cub_bytes;
@@ -382,8 +374,8 @@ struct OrderedScratch {
 
 static size_t cub_need(uint64_t n, int end_bit) {
   size_t a = 0, b = 0, c = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, a, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint32_t*)nullptr,
-                                  (uint32_t*)nullptr, (int)n, 0, end_bit);
+  cub::DeviceRadixSort::SortPairs(nullptr, a, (uint32_t*)nullptr, (uint32_t*)nullptr, (ChunkDesc*)nullptr,
+                                  (ChunkDesc*)nullptr, (int)n, 0, end_bit);
   cub::DeviceRunLengthEncode::Encode(nullptr, b, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint32_t*)nullptr,
                                      (uint32_t*)nullptr, (int)n);
   cub::DeviceScan::ExclusiveSum(nullptr, c, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)n);
@@ -401,14 +393,14 @@ static int bits_for(uint64_t image_pages) {
 static uint64_t arr_bytes(uint64_t n, uint64_t elt) { return ((n + 1) * elt + 255) / 256 * 256; }
 
 size_t ordered_scratch_bytes(uint64_t n_pages, uint64_t image_pages) {
-  return 7 * arr_bytes(n_pages, 4) + 2 * arr_bytes(n_pages, sizeof(ChunkDesc)) + 256 +
+  return 5 * arr_bytes(n_pages, 4) + 2 * arr_bytes(n_pages, sizeof(ChunkDesc)) + 256 +
          cub_need(n_pages, bits_for(image_pages)) + 256;
 }
 
 static OrderedScratch carve(void* base, uint64_t n, size_t cub_bytes) {
   uint8_t* p = static_cast<uint8_t*>(base);
   OrderedScratch s;
-  uint32_t** arrs[] = {&s.keys_in, &s.vals_in, &s.keys_out, &s.vals_out, &s.seg_key, &s.seg_len, &s.seg_start};
+  uint32_t** arrs[] = {&s.keys_in, &s.keys_out, &s.seg_key, &s.seg_len, &s.seg_start};
   for (auto a : arrs) {
     *a = reinterpret_cast<uint32_t*>(p);
     p += arr_bytes(n, 4);
@@ -449,17 +441,13 @@ cudaError_t launch_copy_ordered(uint8_t* image, uint64_t image_bytes, const pv_o
     if (g > 8192) g = 8192;
     ordered_keys_kernel<<<(unsigned)g, 256, 0, stream>>>(ops, n_ops, page_off, page_hpa, page_status, page_aux,
                                                          reinterpret_cast<const unsigned long long*>(op_first_bad),
-                                                         buf, dead_key, s.keys_in, s.vals_in, s.desc, results);
+                                                         buf, dead_key, s.keys_in, s.desc, results);
   }
   size_t tb = s.cub_bytes;
-  cudaError_t e = cub::DeviceRadixSort::SortPairs(s.cub_tmp, tb, s.keys_in, s.keys_out, s.vals_in, s.vals_out,
+  // the 16-byte descriptors ride along as the sort's values (no index gather afterwards)
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(s.cub_tmp, tb, s.keys_in, s.keys_out, s.desc, s.desc_sorted,
                                                   (int)n_pages, 0, end_bit, stream);
   if (e != cudaSuccess) return e;
-  {
-    uint64_t g = (n_pages + 255) / 256;
-    if (g > 8192) g = 8192;
-    ordered_gather_kernel<<<(unsigned)g, 256, 0, stream>>>(s.vals_out, n_pages, s.desc, s.desc_sorted);
-  }
   tb = s.cub_bytes;
   e = cub::DeviceRunLengthEncode::Encode(s.cub_tmp, tb, s.keys_out, s.seg_key, s.seg_len, s.n_segs, (int)n_pages,
                                          stream);
