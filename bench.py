@@ -586,10 +586,10 @@ def run_c2(args, rank, world, local):
                      "traffic": traffic_for(load_traffic("c2"), "ordered_apply", alg_bytes), "launch_ms": per_launch_ms, "alg_bytes_per_launch": alg_bytes,
                      "note": "payload bytes read once + each destination page staged and written back once, "
                              "over the apply kernel's event-timed launch duration (pv_timing)"},
-        "gpu_launches": 15 * K, "gpu_launches_note": "per step: frame pack, identify, classify, plan, 6 FIFO-replay "
+        "gpu_launches": 14 * K, "gpu_launches_note": "per step: frame pack, identify, classify, plan, 6 FIFO-replay "
                                                      "kernels (runs, spec, link, block, verify, apply), stamp, exec "
-                                                     "(stands down), ordered keys (+ results), gather, apply; CUB "
-                                                     "select / radix sort / RLE / scan kernels not counted",
+                                                     "(stands down), ordered keys (+ results), apply; CUB select / "
+                                                     "radix sort / RLE / scan kernels not counted",
         "clocks": clk, "build_s": build_s,
     }
 
