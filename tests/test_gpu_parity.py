@@ -98,6 +98,26 @@ def test_c1_translate_1m_vs_oracle_and_reference(c1):
     assert got == c1["g"]["expected"]
 
 
+def test_c1_translate_6m_stage_table_prepass(c1):
+    """Batches of >= 8 chunks per CTA take the walker's other arm: per-segment
+    stage tables built by the pre-pass (both stages for TDP spaces) and
+    grid-stride chunks -- 6 M lanes (10 % outside the region: faults at
+    every level) over two segments of the same space, against the oracle."""
+    rng = np.random.default_rng(6)
+    n = 6 << 20
+    vas = np.where(rng.random(n) < 0.9, S.C1_GVA + rng.integers(0, 64 << 20, n),
+                   rng.integers(0, 1 << 32, n)).astype(np.uint64)
+    tr = c1["tr"]
+    img = c1["w"]["memv"].host_mem.backing
+    plan = dp.TranslatePlan([tr.device_space], [(0, n // 3, 0), (n // 3, n, 0)], image=img)
+    v, s, a = dp.translate_lanes(img, plan, torch.from_numpy(vas.astype(np.uint32).view(np.int32)).cuda())
+    ov, os_, oa = O.translate(c1["raw"], c1["osp"], vas, threads=0)
+    assert np.array_equal(s.cpu().numpy().view(np.uint32), os_)
+    assert np.array_equal(v.cpu().numpy().view(np.uint64), ov)
+    assert np.array_equal(a.cpu().numpy().view(np.uint64), oa)
+    assert (os_ != 0).any() and (os_ == 0).any()
+
+
 def test_c1_translate_cached_fifo_replay(c1):
     w = c1["w"]
     vas = S.c1_vas(200_000)
