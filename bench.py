@@ -47,7 +47,8 @@ def parse():
     ap.add_argument("--scale", type=int, default=1, help="shrink C5 by this factor (testing only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--gather", action="store_true", help="return every guest's translations to rank 0 after "
-                    "timing (point-to-point over NCCL = NVLink peer copies) and report its time")
+                    "timing (point-to-point over NCCL = NVLink peer copies) and report its time (default at N > 1)")
+    ap.add_argument("--no-gather", action="store_true", help="skip the result return to rank 0 at N > 1")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch the C5 step phases eagerly instead of "
                     "replaying CUDA graphs of them")
@@ -346,7 +347,8 @@ def run_ours(args, rank, world, local):
 
     total_ms, tr_ms, copy_ms, exec_ms, plan_ms = shard.max_over_ranks(
         [total_ms, tr_ms, copy_ms, exec_ms, plan_ms], world, device="cuda")
-    gather = gather_results(wl, rank, world) if (args.gather and wl.name == "c5") else None
+    want_gather = (args.gather or (world > 1 and _pg())) and not args.no_gather
+    gather = gather_results(wl, rank, world) if (want_gather and wl.name == "c5") else None
     K = args.steps
     trans_per_s = wl.total_vas * K / (tr_ms / 1e3) if world > 0 else 0.0
     copy_gbs = wl.total_copy_bytes * K / (copy_ms / 1e3) / 1e9
