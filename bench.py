@@ -386,6 +386,7 @@ def run_ours(args, rank, world, local):
                      "achieved": exec_achieved,
                      "peak": peak, "unit": "GB/s", "frac": exec_achieved / peak, "peak_source": peak_kind,
                      "traffic": traffic_for(traffic, "exec", 2 * wl.copy_bytes),
+                     "frac_of_8tbs_spec": exec_achieved / 8000.0,
                      "algorithmic_bytes_per_launch": 2 * wl.copy_bytes},
         "roofline_walk": {"bound": "hbm", "kernel": "pv_translate (translate_kernel)", "achieved": walk_achieved,
                           "peak": peak, "unit": "GB/s", "frac": walk_achieved / peak,
@@ -393,7 +394,8 @@ def run_ours(args, rank, world, local):
                           "algorithmic_bytes_per_launch": walk_bytes,
                           "note": "16 B/translation (u32 VA in, u64 hpa + u32 status out); leaf-PTE gathers "
                                   "are extra traffic",
-                          "gather_sol": walker_sol(wl.n_vas * K / (tr_ms / 1e3))},
+                          "gather_sol": walker_sol(wl.n_vas * K / (tr_ms / 1e3)),
+                          "ncu": load_json_profile("walker_ncu.json")},
         "faulting_lanes": n_faults,
         "gather_to_rank0": gather,
         "gpu_launches": (4 + (1 if wl.n_vas >= 8 * 296 * 2048 else 0) + 1
@@ -916,6 +918,15 @@ def load_traffic(workload: str) -> dict:
             return json.load(f)
     except Exception:  # noqa: BLE001
         return {}
+
+
+def load_json_profile(name: str):
+    """A committed ncu summary under profiles/ (None when absent)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", name)) as f:
+            return json.load(f)
+    except Exception:  # noqa: BLE001
+        return None
 
 
 def traffic_for(traffic: dict, kernel: str, alg_bytes: int):
