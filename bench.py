@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=["c5", "c1", "c2", "c3", "c4"], default="c5")
     ap.add_argument("--c2-ops", type=int, default=10_000_000)
+    ap.add_argument("--c1-mode", choices=["shadow", "tdp"], default="shadow",
+                    help="C1 translator: shadow table (one stage) or guest table + TDP (two stages)")
     ap.add_argument("--scale", type=int, default=1, help="shrink C5 by this factor (testing only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--gather", action="store_true", help="return every guest's translations to rank 0 after "
@@ -141,7 +143,7 @@ class ClockSampler:
 class Workload:
     """Device-resident inputs of this rank's share of the workload."""
 
-    def __init__(self, name: str, rank: int, world: int, scale: int):
+    def __init__(self, name: str, rank: int, world: int, scale: int, c1_mode: str = "shadow"):
         import torch
 
         from paper_1304_3771_b200 import dataplane as dp
@@ -185,7 +187,8 @@ class Workload:
             self.total_copy_bytes = cfg.guests * cfg.copy_bytes_per_guest
             ops_all = np.concatenate(rows)
         else:
-            memv, guest, space = W.build_c1("shadow")
+            memv, guest, space = W.build_c1(c1_mode)
+            self.c1_mode = c1_mode
             self.memv = memv
             self.owned = [0]
             tr = memv.translator(space, use_cache=False)
@@ -225,7 +228,7 @@ def run_ours(args, rank, world, local):
     from paper_1304_3771_b200 import dataplane as dp
 
     torch.cuda.set_device(local)
-    wl = Workload(args.workload, rank, world, args.scale)
+    wl = Workload(args.workload, rank, world, args.scale, args.c1_mode)
     lib = N.lib()
     img = wl.image
     dev = img.device()
@@ -834,8 +837,10 @@ def run_e2e(wl, args, world):
             recs[(g, p)] = has.HardwareHasAccess(rec, memv)
     else:
         translators = {(0, 0): memv.translator(wl.c1_space, use_cache=False)}
-        rec = has.GuestProcessRecord(_FakeGuest(0), wl.c1_space, memv)
-        recs = {(0, 0): has.HardwareHasAccess(rec, memv)}
+        rec = has.GuestProcessRecord(_FakeGuest(0, wl.c1_mode), wl.c1_space, memv)
+        # hardware HAS needs the shadow table's hybrid root; TDP guests use software HAS (the paper's setup)
+        access = has.HardwareHasAccess if wl.c1_mode == "shadow" else has.SoftwareHasAccess
+        recs = {(0, 0): access(rec, memv)}
     payload = [(torch.empty(int(ops[:, 1].sum()), dtype=torch.uint8).pin_memory(), g, p, ops)
                for g, p, ops, offs in wl.proc_ops]
     for t, *_ in payload:
@@ -884,9 +889,9 @@ def run_e2e(wl, args, world):
 class _FakeGuest:
     """GuestProcessRecord reads .id and .mem_mode (backend.py:267-286)."""
 
-    def __init__(self, gid):
+    def __init__(self, gid, mode: str = "shadow"):
         self.id = gid
-        self.mem_mode = "shadow"
+        self.mem_mode = mode
 
 
 class _Prebuilt:
@@ -952,8 +957,8 @@ def config_of(wl, world):
                 "l2": f"inputs larger than L2 ({c.guests * c.vas_per_guest * 4 >> 20} MiB VAs, "
                       f"{c.guests * c.copy_bytes_per_guest >> 20} MiB payload per step, whole job)",
                 "scale": 1 if wl.cfg.guest_bytes == 8 << 30 else "reduced"}
-    return {"workload": "C1: 1 shadow guest, 16384 shuffled pages, 1M random-VA translations + 64 MiB "
-                        "copy_to_user", "geometry": "reference 3-level 2/9/9/12",
+    return {"workload": f"C1: 1 {wl.c1_mode} guest, 16384 shuffled pages, 1M random-VA translations + 64 MiB "
+                        "copy_to_user", "mode": wl.c1_mode, "geometry": "reference 3-level 2/9/9/12",
             "l2": "inputs smaller than L2 (not flushed)"}
 
 
@@ -1015,7 +1020,8 @@ def _oracle_inputs(wl):
         for g, p, ops, offs in wl.proc_ops:
             proc_ops.append((O.space(0, wl.world.hybrid_roots[g][p].root_pfn), ops))
     else:
-        sp = O.space(0, wl.c1_space.shadow_root.root_pfn)
+        d = wl.memv.translator(wl.c1_space, use_cache=False).device_space  # shadow or guest + TDP tables
+        sp = O.space(d.s1_base, d.s1_root_pfn, d.s2_root_pfn, d.mode)
         proc_vas.append((sp, wl.proc_vas[0][2]))
         proc_ops.append((sp, wl.proc_ops[0][2]))
     return proc_vas, proc_ops
