@@ -346,6 +346,11 @@ def run_ours(args, rank, world, local):
     plan_ms = sum(e[2].elapsed_time(e[3]) for e in evs)
     exec_ms = sum(e[3].elapsed_time(e[4]) for e in evs)
     copy_ms = sum(e[1].elapsed_time(e[4]) for e in evs)
+    # this rank's per-step spread (best and median of the timed steps)
+    tr_steps = sorted(e[0].elapsed_time(e[1]) for e in evs)
+    ex_steps = sorted(e[3].elapsed_time(e[4]) for e in evs)
+    spread = {"translate_ms": {"best": tr_steps[0], "median": statistics.median(tr_steps)},
+              "exec_ms": {"best": ex_steps[0], "median": statistics.median(ex_steps)}, "rank": rank}
     from paper_1304_3771_b200 import shard
 
     total_ms, tr_ms, copy_ms, exec_ms, plan_ms = shard.max_over_ranks(
@@ -384,6 +389,7 @@ def run_ours(args, rank, world, local):
                  "ms_per_step": copy_ms / K, "exec_ms_per_step": exec_ms / K,
                  "plan_shim_stamp_ms_per_step": plan_ms / K},
         "translate_ms_per_step": tr_ms / K,
+        "per_step": spread,
         "roofline": {"bound": "hbm",
                      "kernel": "pv_copy_exec (" + ("exec_bulk_kernel, TMA" if hint else "exec_kernel, LSU") + ")",
                      "achieved": exec_achieved,
