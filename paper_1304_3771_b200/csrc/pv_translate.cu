@@ -453,8 +453,12 @@ static cudaError_t launch_t(const uint8_t* image, uint64_t image_bytes, const pv
 #ifndef PV_TR_MINB
 #define PV_TR_MINB 2
 #endif
-  auto k = kTwo ? translate_kernel<kTwo, kVa32, kPfn> : translate_kernel<kTwo, kVa32, kPfn, 512, PV_TR_MINB>;
-  const int tpb = kTwo ? kTpb : 512;
+#ifndef PV_TR2_TPB
+#define PV_TR2_TPB 512  // two-stage walks: 512 x 4 lanes, 2 CTAs/SM (C1 TDP 37.5 vs 28.2 G/s at 256 x 8)
+#endif
+  auto k = kTwo ? translate_kernel<kTwo, kVa32, kPfn, PV_TR2_TPB, (PV_TR2_TPB == 256 ? 3 : 1024 / PV_TR2_TPB)>
+                : translate_kernel<kTwo, kVa32, kPfn, 512, PV_TR_MINB>;
+  const int tpb = kTwo ? PV_TR2_TPB : 512;
   uint64_t grid = resident_grid((const void*)k, tpb, 0);
   if (grid > n_chunks) grid = n_chunks;
   if (grid == 0) return cudaSuccess;

@@ -6,7 +6,7 @@ orig=$(mktemp); cp paper_1304_3771_b200/libpv.so $orig
 for v in scripts/variants/*.so; do
   cp $v paper_1304_3771_b200/libpv.so
   [ -n "$K" ] && timeout 600 python -m pytest tests -q -x -m gpu -p no:cacheprovider -k "$K" 2>&1 | tail -1
-  timeout 300 python bench.py --workload $W --steps 10 --warmup 3 --no-e2e --no-cpu-baseline 2>/dev/null | python -c "
+  timeout 300 python bench.py --workload $W $BARGS --steps 10 --warmup 3 --no-e2e --no-cpu-baseline 2>/dev/null | python -c "
 import json,sys; d=json.loads(sys.stdin.read())
 c = d.get('copy') if isinstance(d.get('copy'), dict) else {}
 print('$v', 'value', round(d['value']/1e9,2), 'translate_ms', d.get('translate_ms_per_step'), 'exec_ms', c.get('exec_ms_per_step'),
