@@ -667,9 +667,11 @@ def _shim_scratch(image, n_pages: int):
 
 
 def copy_launch(image, plan: CopyPlan, direction: int, buf, *, fifo_dev=None, fifo_cap: int = 10,
-                detect_conflicts: bool = True, track_dirty: bool = True) -> None:
+                detect_conflicts: bool = True, track_dirty: bool = True, buf_ready=None) -> None:
     """Enqueue plan (+ FIFO replay) (+ conflict stamp) + exec on the current
-    stream.  Results land in ``plan.results`` / ``plan.conflict``."""
+    stream.  Results land in ``plan.results`` / ``plan.conflict``.
+    ``buf_ready`` (a CUDA event, optional): the buffer is still arriving on
+    another stream; only the exec waits for it, the plan passes overlap it."""
     lib = N.lib()
     dev_img = image.device()
     s = _stream().cuda_stream
@@ -716,6 +718,8 @@ def copy_launch(image, plan: CopyPlan, direction: int, buf, *, fifo_dev=None, fi
         # through the TMA bulk exec (pv_copy.cu exec_bulk_kernel); the LSU exec
         # takes the rest (PV_EXEC_LSU=1 forces it, for A/B runs)
         hint = exec_hint(plan, buf.data_ptr())
+        if buf_ready is not None:
+            _stream().wait_event(buf_ready)
         N.check(lib.pv_copy_exec(dev_img.data_ptr(), image.nbytes, plan.ops.data_ptr(), plan.n_ops,
                                  plan.page_off.data_ptr(), plan.n_pages, direction | hint, plan.page_hpa.data_ptr(),
                                  plan.page_status.data_ptr(), plan.page_aux.data_ptr(), plan.first_bad.data_ptr(),
@@ -763,7 +767,7 @@ def copy_ordered(image, plan: CopyPlan, buf) -> None:
 
 
 def copy_ops(image, spaces: list[Space], ops: np.ndarray, direction: int, buf, *, caches=None, fifo_groups=None,
-             detect_conflicts: bool = True, shims=None) -> list[OpOutcome]:
+             detect_conflicts: bool = True, shims=None, buf_ready=None) -> list[OpOutcome]:
     """Run a batch of copies with the reference's sequential semantics.
 
     ``caches`` (with ``fifo_groups``) are host TranslationCache objects whose
@@ -775,7 +779,8 @@ def copy_ops(image, spaces: list[Space], ops: np.ndarray, direction: int, buf, *
     cap = fifo_capacity(caches) if caches is not None else 10
     plan = CopyPlan(spaces, ops, fifo_groups=fifo_groups if caches is not None else None, shims=shims)
     fifo_dev = _to_dev(pack_fifo(caches)) if caches is not None else None
-    copy_launch(image, plan, direction, buf, fifo_dev=fifo_dev, fifo_cap=cap, detect_conflicts=detect_conflicts)
+    copy_launch(image, plan, direction, buf, fifo_dev=fifo_dev, fifo_cap=cap, detect_conflicts=detect_conflicts,
+                buf_ready=buf_ready)
     if direction == N.TO_GUEST and detect_conflicts and int(plan.conflict.item()):
         copy_ordered(image, plan, buf)
     results = decode_results(plan.results.cpu().numpy())

@@ -84,6 +84,31 @@ def _as_src_tensor(src):
                       else np.ascontiguousarray(src, dtype=np.uint8))
 
 
+_h2d_stream = None
+
+
+def _src_async(src):
+    """(device tensor, ready event or None).  A pinned host tensor starts its
+    H2D copy on a side stream, so the batch's plan / shim / stamp passes (and
+    the host work building them) overlap the transfer; only the exec waits."""
+    import torch
+
+    global _h2d_stream
+    if isinstance(src, torch.Tensor) and not src.is_cuda and src.is_pinned():
+        if _h2d_stream is None:
+            _h2d_stream = torch.cuda.Stream()
+        side = _h2d_stream
+        side.wait_stream(torch.cuda.current_stream())  # the destination allocation is ordered on the main stream
+        with torch.cuda.stream(side):
+            dev = torch.empty(src.shape, dtype=src.dtype, device="cuda")
+            dev.copy_(src, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(side)
+        dev.record_stream(torch.cuda.current_stream())
+        return dev, ev
+    return _as_src_tensor(src), None
+
+
 def _ops_rows(gvas, lengths, offsets):
     gvas = np.asarray(gvas, dtype=np.uint64)
     lengths = np.asarray(lengths, dtype=np.uint64)
@@ -111,14 +136,15 @@ def _decode_outcome(out: dp.OpOutcome, row, image_bytes: int):
 class _BatchMixin:
     """Batch copies through one translator (``self._batch_translator``)."""
 
-    def _batch(self, direction: int, rows: np.ndarray, buf):
+    def _batch(self, direction: int, rows: np.ndarray, buf, buf_ready=None):
         tr = self._batch_translator()
         image = self._memv.host_mem.backing
         space = tr.device_space
         caches = [tr.cache] if getattr(tr, "use_cache", False) else None
         groups = [list(range(len(rows)))] if caches is not None else None
         if not hasattr(tr, "_on_trap"):
-            outs = dp.copy_ops(image, [space], rows, direction, buf, caches=caches, fifo_groups=groups)
+            outs = dp.copy_ops(image, [space], rows, direction, buf, caches=caches, fifo_groups=groups,
+                               buf_ready=buf_ready)
             return [_decode_outcome(o, r, image.nbytes) for o, r in zip(outs, rows)]
         # Hybrid resolver: the device runs the default shim for every trap it
         # can resolve exactly (pv_copy_shim).  Any other trap changes the
@@ -129,7 +155,7 @@ class _BatchMixin:
         start = 0
         while start < len(rows):
             part = rows[start:]
-            outs = dp.copy_ops(image, [space], part, direction, buf, shims=[tr.device_shim])
+            outs = dp.copy_ops(image, [space], part, direction, buf, shims=[tr.device_shim], buf_ready=buf_ready)
             cut = next((i for i, o in enumerate(outs) if dp.kind(o.status) in (N.ST_TRAP, N.ST_TRAP2)), None)
             upto = len(outs) if cut is None else cut
             for o, r in zip(outs[:upto], part[:upto]):
@@ -175,7 +201,8 @@ class _BatchMixin:
         every i, in order, on the device.  Returns per-op outcomes."""
         self._bump(len(gvas))
         rows = _ops_rows(gvas, lengths, offsets)
-        return self._batch(N.TO_GUEST, rows, _as_src_tensor(src))
+        buf, ready = _src_async(src)
+        return self._batch(N.TO_GUEST, rows, buf, ready)
 
     def copy_from_user_batch(self, gvas, lengths):
         """copy_from_user for every op, in order.  Returns ``(payload,
