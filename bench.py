@@ -196,14 +196,17 @@ class Workload:
             v = W.c1_vas().astype(np.uint32)
             vas_parts = [v]
             bounds = [(0, len(v), 0)]
-            self.n_vas = self.total_vas = len(v)
+            # one guest, one process: at N > 1 every rank runs its own replica of the batch
+            self.n_vas = len(v)
+            self.total_vas = len(v) * world
             self.proc_vas = [(0, 0, v)]
             c_spaces = [tr.device_space]
             c_shims = None
             n = 64 << 20
             ops_all = np.array([[W.C1_GVA, n, 0, 0]], dtype=np.uint64)
             self.proc_ops = [(0, 0, ops_all[:, :2], np.zeros(1, np.uint64))]
-            self.copy_bytes = self.total_copy_bytes = n
+            self.copy_bytes = n
+            self.total_copy_bytes = n * world
             self.c1_space = space
         self.build_s = time.time() - t0
         self.image = self.memv.host_mem.backing
@@ -978,6 +981,7 @@ def config_of(wl, world):
                 "scale": 1 if wl.cfg.guest_bytes == 8 << 30 else "reduced"}
     return {"workload": f"C1: 1 {wl.c1_mode} guest, 16384 shuffled pages, 1M random-VA translations + 64 MiB "
                         "copy_to_user", "mode": wl.c1_mode, "geometry": "reference 3-level 2/9/9/12",
+            "parallelism": f"replicas x{world} (one process: every rank runs the full batch on its own image)",
             "l2": "inputs smaller than L2 (not flushed)"}
 
 
