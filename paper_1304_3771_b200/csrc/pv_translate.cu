@@ -305,7 +305,11 @@ translate_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const 
     // OK -- no status logic, no branches per lane.  Anything else (faults,
     // traps, escapes, unindexed nodes, two-stage spaces) takes the general
     // path below, which re-reads the same (now L1-resident) codes.
-    if (!(kTwo && two) && leaf_codes != nullptr) {
+    // (Two-stage walks take the same path twice: the stage-1 leaf code gives
+    // the gpa, whose TDP upper levels come from codes2 and leaf code from the
+    // index -- a TDP fault or trap anywhere sends the thread to the general
+    // path.)
+    if (leaf_codes != nullptr) {
       uint32_t fc[VPT];
       bool simple = true;
 #pragma unroll
@@ -328,6 +332,32 @@ translate_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const 
         bool present = true;
 #pragma unroll
         for (int j = 0; j < VPT; ++j) present &= (lc[j] & 3u) == 1u;
+        if (present && kTwo && two) {
+          // stage 2 over the gpa: lc[] becomes the TDP leaf code (same shape)
+          uint64_t gpa[VPT];
+          bool simple2 = true;
+#pragma unroll
+          for (int j = 0; j < VPT; ++j) {
+            gpa[j] = ((uint64_t)(lc[j] >> 2) << kPageShift) | (va[j] & kPageMask);
+            fc[j] = codes2[(top_index(gpa[j]) << 9) | mid_index(gpa[j])];
+            const bool valid = lane0 + (uint64_t)j * TPB + threadIdx.x < seg_end;
+            simple2 &= !valid || (fc[j] & 0xFu) == (1u | kCodeIndexed);
+          }
+          present = simple2;
+          if (simple2) {
+#pragma unroll
+            for (int j = 0; j < VPT; ++j) {
+              const bool valid = lane0 + (uint64_t)j * TPB + threadIdx.x < seg_end;
+              lc[j] = 1u;
+              if (valid)
+                asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;"
+                    : "=r"(lc[j])
+                    : "l"(leaf_codes + ((uint64_t)(fc[j] >> 4) << 9) + leaf_index(gpa[j])), "l"(pol_table));
+            }
+#pragma unroll
+            for (int j = 0; j < VPT; ++j) present &= (lc[j] & 3u) == 1u;
+          }
+        }
         if (present) {
 #pragma unroll
           for (int j = 0; j < VPT; ++j) {
