@@ -104,6 +104,22 @@ def main(src: str) -> None:
         )
         with open(os.path.join(HERE, f"c1_{mode}.json"), "w") as f:
             json.dump(meta, f)
+    # BASELINE config 4 tables (corrupted leaves, traps, TDP-stage faults): 100 k VAs per mode,
+    # every outcome folded into one digest (the fixture stays small)
+    c4 = {}
+    for mode in ("shadow", "tdp"):
+        w = S.c1_build(mv, be, er, mode)
+        S.c4_corrupt(mv, w, mode)
+        vas = S.c4_vas()
+        tr = w["memv"].translator(w["space"], use_cache=False)
+        out = [S.outcome(lambda: tr.translate(int(va)), er) for va in vas]
+        kinds = {}
+        for o in out:
+            kinds[o[0]] = kinds.get(o[0], 0) + 1
+        c4[mode] = dict(image_sha=S.sha(S.image_bytes(w["memv"].host_mem)), n_vas=len(vas),
+                        digest=S.digest(out), kinds=kinds, head=out[:50])
+    with open(os.path.join(HERE, "c4_digest.json"), "w") as f:
+        json.dump(c4, f)
     w = S.shim_build(mv, be, er)
     build_sha = S.sha(S.image_bytes(w["memv"].host_mem))
     res = S.shim_query(w, mv, be, er)

@@ -16,6 +16,7 @@ Outcomes are JSON-able lists.
 from __future__ import annotations
 
 import hashlib
+import json
 import random
 import struct
 
@@ -345,6 +346,43 @@ def c1_build(mv, be, er, mode: str):
 def c1_vas(n: int = 1_000_000) -> np.ndarray:
     rng = random.Random(3771)
     return np.array([C1_GVA + rng.randrange(64 << 20) for _ in range(n)], dtype=np.uint64)
+
+
+# ---- scenario "c4_digest": BASELINE config 4 tables, 100 k VAs, pinned by digest
+
+def c4_corrupt(mv, w, mode: str, seed: int = 1304) -> None:
+    """20 % of the C1 leaf PTEs NOT_PRESENT, 10 % TRAPPING (shadow only; the
+    reference's TDP tables cannot trap), on the shadow table or the guest
+    table (TDP); TDP worlds also get guest PTEs past the slot on every 97th
+    page (TDP-stage faults)."""
+    memv, space = w["memv"], w["space"]
+    rng = random.Random(seed)
+    if mode == "shadow":
+        ed = mv.TableEditor(memv.host_mem, space.shadow_root, memv.host_alloc.alloc)
+    else:
+        g = space.guest
+        ed = mv.TableEditor(g.mem, space.guest_root, g.os_alloc.alloc)
+    for p in range(C1_PAGES):
+        r = rng.random()
+        va = C1_GVA + p * PAGE
+        if r < 0.2:
+            ed.set_leaf_state(va, mv.EntryState.NOT_PRESENT)
+        elif r < 0.3 and mode == "shadow":
+            ed.set_leaf_state(va, mv.EntryState.TRAPPING)
+    if mode == "tdp":
+        for p in range(0, C1_PAGES, 97):
+            ed.map(C1_GVA + p * PAGE, (200 << 20) >> 12, replace=True)
+
+
+def c4_vas(n: int = 100_000) -> np.ndarray:
+    """90 % in the C1 region, 10 % uniform over 2^32 (faults at every level)."""
+    rng = random.Random(4404)
+    return np.array([C1_GVA + rng.randrange(64 << 20) if rng.random() < 0.9 else rng.randrange(1 << 32)
+                     for _ in range(n)], dtype=np.uint64)
+
+
+def digest(outcomes) -> str:
+    return hashlib.sha256(json.dumps(outcomes, separators=(",", ":")).encode()).hexdigest()
 
 
 # ---- scenario "resultpage": record codec (resultpage.py:44-61)

@@ -231,3 +231,25 @@ def test_shim_build_bytes_and_oracle():
     rows, cut, _, _ = _shim_oracle_rows(w, S.SHIM_OPS)
     assert cut == 4  # NOGUEST: the shim's guest walk faults (host-side)
     assert rows == g["rows"][:cut]
+
+
+@pytest.mark.parametrize("mode", ["shadow", "tdp"])
+def test_c4_corrupted_tables_oracle_digest(mode):
+    """BASELINE config 4 tables (20 % not-present and, shadow only, 10 %
+    trapping leaves; TDP guest PTEs past the slot) built by this package's
+    control plane equal the reference's byte for byte, and the oracle's
+    outcomes for 100 k VAs (10 % uniform over 2^32) fold into the digest the
+    reference's own translator produced (tests/golden/c4_digest.json)."""
+    g = load_json("c4_digest.json")[mode]
+    w = S.c1_build(mv, be, er, mode)
+    S.c4_corrupt(mv, w, mode)
+    raw = S.image_bytes(w["memv"].host_mem)
+    assert S.sha(raw) == g["image_sha"]
+    tr = w["memv"].translator(w["space"], use_cache=False)
+    sp = tr.device_space
+    vas = S.c4_vas(g["n_vas"])
+    v, s, a = O.translate(np.frombuffer(raw, dtype=np.uint8), O.space(sp.s1_base, sp.s1_root_pfn, sp.s2_root_pfn,
+                                                                      sp.mode), vas, threads=0)
+    got = [status_outcome(int(s[i]), int(v[i]), int(a[i]), int(vas[i])) for i in range(len(vas))]
+    assert got[:50] == g["head"]
+    assert S.digest(got) == g["digest"]

@@ -682,3 +682,20 @@ def test_tma_bulk_exec_coaligned_batches_vs_oracle(cuda, mode):
             assert np.array_equal(buf.cpu().numpy(), src_h)
         kinds = set((want[:, 3] & 0xFF0).tolist())
         assert 0 in kinds and len(kinds) > 1  # complete ops and faulting ops both present
+
+
+@pytest.mark.parametrize("mode", ["shadow", "tdp"])
+def test_c4_device_translate_matches_reference_digest(cuda, mode):
+    """The device's outcomes for 100 k VAs over BASELINE config 4 tables fold
+    into the digest of the REFERENCE's own translator (tests/golden/
+    c4_digest.json, generated from devfsim by tests/golden/gen_golden.py)."""
+    g = load_json("c4_digest.json")[mode]
+    w = S.c1_build(mv, be, er, mode)
+    S.c4_corrupt(mv, w, mode)
+    assert S.sha(S.image_bytes(w["memv"].host_mem)) == g["image_sha"]
+    tr = w["memv"].translator(w["space"], use_cache=False)
+    vas = S.c4_vas(g["n_vas"])
+    hpa, st, aux = tr.translate_batch(vas)
+    got = [status_outcome(int(st[i]), int(hpa[i]), int(aux[i]), int(vas[i])) for i in range(len(vas))]
+    assert got[:50] == g["head"]
+    assert S.digest(got) == g["digest"]
