@@ -120,6 +120,14 @@ def main(src: str) -> None:
                         digest=S.digest(out), kinds=kinds, head=out[:50])
     with open(os.path.join(HERE, "c4_digest.json"), "w") as f:
         json.dump(c4, f)
+    # BASELINE config 2 staging: 20 k overlapping IOCTL_SNAPSHOT blobs through 8 FIFO-cached
+    # software-HAS processes of one TDP guest, in program order
+    w = S.c2_build(mv, be, er)
+    ops = S.c2_ops(20000)
+    out, caches = S.c2_reference_run(w, mv, be, er, ops)
+    with open(os.path.join(HERE, "c2_digest.json"), "w") as f:
+        json.dump(dict(n_ops=len(ops), image_sha=S.sha(S.image_bytes(w["memv"].host_mem)), digest=S.digest(out),
+                       head=out[:50], caches=caches), f)
     w = S.shim_build(mv, be, er)
     build_sha = S.sha(S.image_bytes(w["memv"].host_mem))
     res = S.shim_query(w, mv, be, er)

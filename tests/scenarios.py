@@ -594,3 +594,47 @@ def frames_identify_query(hc):
             except Exception as e:  # noqa: BLE001
                 out.append(["err", exc_name(e)])
     return out
+
+
+# ---- scenario "c2_digest": BASELINE config 2 staging, pinned by digest
+
+C2_ARENA = 0x2000_0000
+C2_PAGES = 256
+C2_PROCS = 8
+
+
+def c2_build(mv, be, er):
+    """One TDP guest, 8 processes with a 256-page arena each."""
+    memv = mv.MemoryVirtualizer()
+    guest = memv.add_guest(0, "tdp")
+    spaces = []
+    for _ in range(C2_PROCS):
+        sp = memv.create_process(guest)
+        memv.map_region(sp, C2_ARENA, C2_PAGES)
+        spaces.append(sp)
+    return dict(memv=memv, guest=guest, spaces=spaces)
+
+
+def c2_ops(n: int, seed: int = 2022):
+    """(proc, gva, len) of an IOCTL_SNAPSHOT trace: op i in process i % 8,
+    len randint(64, 4096) at a random arena offset (overlapping writes)."""
+    rng = random.Random(seed)
+    return [(i % C2_PROCS, C2_ARENA + rng.randrange((1 << 20) - 4096), rng.randint(64, 4096)) for i in range(n)]
+
+
+def snapshot_blob(n: int) -> bytes:
+    """EventDevice IOCTL_SNAPSHOT blob (devices.py:162-166)."""
+    return bytes(((j * 7 + 3) & 0xFF) for j in range(n))
+
+
+def c2_reference_run(w, mv, be, er, ops):
+    """copy_to_user of every op's blob in program order through each process's
+    FIFO-cached software HAS (backend.py:75-114).  Returns (per-op outcome,
+    per-process (hits, misses, entries))."""
+    memv = w["memv"]
+    recs = [be.GuestProcessRecord(_Guest(0, "tdp"), sp, memv) for sp in w["spaces"]]
+    accs = [be.SoftwareHasAccess(r, memv) for r in recs]
+    out = [outcome(lambda: accs[p].copy_to_user(gva, snapshot_blob(ln)), er) for p, gva, ln in ops]
+    caches = [[r.translation_cache.hits, r.translation_cache.misses, [list(e) for e in r.translation_cache.entries()]]
+              for r in recs]
+    return out, caches

@@ -253,3 +253,35 @@ def test_c4_corrupted_tables_oracle_digest(mode):
     got = [status_outcome(int(s[i]), int(v[i]), int(a[i]), int(vas[i])) for i in range(len(vas))]
     assert got[:50] == g["head"]
     assert S.digest(got) == g["digest"]
+
+
+def _c2_rows(ops):
+    """(rows, buffer) of a c2_digest trace: blobs back to back."""
+    rows, blobs, off = [], [], 0
+    for p, gva, ln in ops:
+        rows.append((gva, ln, off, p))
+        blobs.append(S.snapshot_blob(ln))
+        off += ln
+    return np.array(rows, dtype=np.uint64), np.frombuffer(b"".join(blobs), dtype=np.uint8).copy()
+
+
+def test_c2_staging_oracle_digest():
+    """BASELINE config 2 staging (20 k overlapping blobs, 8 FIFO-cached
+    processes of one TDP guest) replayed by the oracle leaves the reference's
+    final memory (SHA-256), per-op outcomes and cache counters/entries."""
+    g = load_json("c2_digest.json")
+    w = S.c2_build(mv, be, er)
+    ops = S.c2_ops(g["n_ops"])
+    rows, buf = _c2_rows(ops)
+    raw = np.frombuffer(S.image_bytes(w["memv"].host_mem), dtype=np.uint8).copy()
+    sps = [w["memv"].translator(sp, use_cache=False).device_space for sp in w["spaces"]]
+    oc = np.ascontiguousarray(np.stack([O.new_cache(10) for _ in sps]))
+    res = O.copy(raw, np.stack([O.space(s.s1_base, s.s1_root_pfn, s.s2_root_pfn, s.mode) for s in sps]), rows, buf, 0,
+                 caches=oc, op_cache=rows[:, 3].astype(np.int32))
+    assert (res[:, 3] == 0).all()
+    got = [["ok", int(r[0])] for r in res]
+    assert got[:50] == g["head"] and S.digest(got) == g["digest"]
+    assert S.sha(raw.tobytes()) == g["image_sha"]
+    for p, (hits, misses, entries) in enumerate(g["caches"]):
+        e, h, m = O.cache_state(oc[p])
+        assert (h, m, [list(x) for x in e]) == (hits, misses, entries)

@@ -699,3 +699,29 @@ def test_c4_device_translate_matches_reference_digest(cuda, mode):
     got = [status_outcome(int(st[i]), int(hpa[i]), int(aux[i]), int(vas[i])) for i in range(len(vas))]
     assert got[:50] == g["head"]
     assert S.digest(got) == g["digest"]
+
+
+def test_c2_staging_device_matches_reference_digest(cuda):
+    """The device copy batch (plan, exact parallel FIFO-10 replay, conflict
+    stamp, ordered last-writer-wins apply) over the c2_digest trace leaves the
+    reference's final memory, outcomes and cache states."""
+    g = load_json("c2_digest.json")
+    w = S.c2_build(mv, be, er)
+    ops = S.c2_ops(g["n_ops"])
+    rows, blobs, off = [], [], 0
+    for p, gva, ln in ops:
+        rows.append((gva, ln, off, p))
+        blobs.append(S.snapshot_blob(ln))
+        off += ln
+    rows = np.array(rows, dtype=np.uint64)
+    buf = torch.from_numpy(np.frombuffer(b"".join(blobs), dtype=np.uint8).copy()).cuda()
+    memv = w["memv"]
+    sps = [memv.translator(sp, use_cache=False).device_space for sp in w["spaces"]]
+    caches = [mv.TranslationCache(10) for _ in sps]
+    groups = [list(range(p, len(ops), S.C2_PROCS)) for p in range(S.C2_PROCS)]
+    outs = dp.copy_ops(memv.host_mem.backing, sps, rows, N.TO_GUEST, buf, caches=caches, fifo_groups=groups)
+    got = [["ok", int(o.copied)] if o.status == 0 else ["status", int(o.status)] for o in outs]
+    assert got[:50] == g["head"] and S.digest(got) == g["digest"]
+    assert S.sha(S.image_bytes(memv.host_mem)) == g["image_sha"]
+    for c, (hits, misses, entries) in zip(caches, g["caches"]):
+        assert (c.hits, c.misses, [list(x) for x in c.entries()]) == (hits, misses, entries)
