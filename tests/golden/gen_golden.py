@@ -128,6 +128,13 @@ def main(src: str) -> None:
     with open(os.path.join(HERE, "c2_digest.json"), "w") as f:
         json.dump(dict(n_ops=len(ops), image_sha=S.sha(S.image_bytes(w["memv"].host_mem)), digest=S.digest(out),
                        head=out[:50], caches=caches), f)
+    c1c = {}
+    for mode in ("shadow", "tdp"):
+        w = S.c1_build(mv, be, er, mode)
+        out, cache = S.c1_copy_reference_run(w, mv, be, er, mode)
+        c1c[mode] = dict(outcomes=out, cache=cache, image_sha=S.sha(S.image_bytes(w["memv"].host_mem)))
+    with open(os.path.join(HERE, "c1_copy_digest.json"), "w") as f:
+        json.dump(c1c, f)
     w = S.shim_build(mv, be, er)
     build_sha = S.sha(S.image_bytes(w["memv"].host_mem))
     res = S.shim_query(w, mv, be, er)

@@ -638,3 +638,23 @@ def c2_reference_run(w, mv, be, er, ops):
     caches = [[r.translation_cache.hits, r.translation_cache.misses, [list(e) for e in r.translation_cache.entries()]]
               for r in recs]
     return out, caches
+
+
+# ---- scenario "c1_copy_digest": BASELINE config 1's 64 MiB copy_to_user
+
+def c1_copy_payload() -> bytes:
+    return random.Random(3771).randbytes(64 << 20)
+
+
+def c1_copy_reference_run(w, mv, be, er, mode: str):
+    """copy_to_user of the 64 MiB payload at the region start, then of its
+    first 64 MiB - 4 KiB at +0x800 (unaligned), through the process's
+    FIFO-cached software HAS; returns the two outcomes and the cache state."""
+    memv = w["memv"]
+    rec = be.GuestProcessRecord(_Guest(0, mode), w["space"], memv)
+    acc = be.SoftwareHasAccess(rec, memv)
+    data = c1_copy_payload()
+    out = [outcome(lambda: acc.copy_to_user(C1_GVA, data), er),
+           outcome(lambda: acc.copy_to_user(C1_GVA + 0x800, data[:(64 << 20) - 4096]), er)]
+    c = rec.translation_cache
+    return out, [c.hits, c.misses, [list(e) for e in c.entries()]]

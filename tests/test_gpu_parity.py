@@ -725,3 +725,23 @@ def test_c2_staging_device_matches_reference_digest(cuda):
     assert S.sha(S.image_bytes(memv.host_mem)) == g["image_sha"]
     for c, (hits, misses, entries) in zip(caches, g["caches"]):
         assert (c.hits, c.misses, [list(x) for x in c.entries()]) == (hits, misses, entries)
+
+
+@pytest.mark.parametrize("mode", ["shadow", "tdp"])
+def test_c1_copy_matches_reference_digest(cuda, mode):
+    """BASELINE config 1's 64 MiB copy_to_user (aligned, then unaligned at
+    +0x800) through the FIFO-cached software HAS on the device leaves the
+    memory, outcomes and cache state the reference leaves
+    (tests/golden/c1_copy_digest.json)."""
+    g = load_json("c1_copy_digest.json")[mode]
+    w = S.c1_build(mv, be, er, mode)
+    memv = w["memv"]
+    rec = be.GuestProcessRecord(S._Guest(0, mode), w["space"], memv)
+    acc = be.SoftwareHasAccess(rec, memv)
+    data = S.c1_copy_payload()
+    out = [S.outcome(lambda: acc.copy_to_user(S.C1_GVA, data), er),
+           S.outcome(lambda: acc.copy_to_user(S.C1_GVA + 0x800, data[:(64 << 20) - 4096]), er)]
+    assert out == g["outcomes"]
+    c = rec.translation_cache
+    assert [c.hits, c.misses, [list(e) for e in c.entries()]] == g["cache"]
+    assert S.sha(S.image_bytes(memv.host_mem)) == g["image_sha"]
