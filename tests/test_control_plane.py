@@ -285,3 +285,22 @@ def test_c2_staging_oracle_digest():
     for p, (hits, misses, entries) in enumerate(g["caches"]):
         e, h, m = O.cache_state(oc[p])
         assert (h, m, [list(x) for x in e]) == (hits, misses, entries)
+
+
+@pytest.mark.parametrize("mode", ["shadow", "tdp"])
+def test_c1_copy_oracle_digest(mode):
+    """The oracle's FIFO-cached copy_user_buffer over BASELINE config 1's
+    64 MiB copies leaves the reference's memory and cache state."""
+    g = load_json("c1_copy_digest.json")[mode]
+    w = S.c1_build(mv, be, er, mode)
+    raw = np.frombuffer(S.image_bytes(w["memv"].host_mem), dtype=np.uint8).copy()
+    sp = w["memv"].translator(w["space"], use_cache=False).device_space
+    data = np.frombuffer(S.c1_copy_payload(), dtype=np.uint8).copy()
+    rows = np.array([[S.C1_GVA, 64 << 20, 0, 0], [S.C1_GVA + 0x800, (64 << 20) - 4096, 0, 0]], np.uint64)
+    oc = O.new_cache(10)
+    res = O.copy(raw, O.space(sp.s1_base, sp.s1_root_pfn, sp.s2_root_pfn, sp.mode).reshape(1, 4), rows, data, 0,
+                 caches=oc, op_cache=[0, 0])
+    assert [["ok", int(r[0])] for r in res] == g["outcomes"]
+    e, h, m = O.cache_state(oc)
+    assert [h, m, [list(x) for x in e]] == g["cache"]
+    assert S.sha(raw.tobytes()) == g["image_sha"]
