@@ -132,6 +132,20 @@ uint64_t resident_grid(const void* func, int tpb, size_t smem) {
   return g;
 }
 
+cudaError_t ensure_dynamic_smem(const void* func, size_t bytes) {
+  static std::mutex mu;
+  static std::unordered_map<uint64_t, size_t> done;  // (func, device) -> bytes set
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t key = (reinterpret_cast<uint64_t>(func) << 8) ^ (uint64_t)dev;
+  std::lock_guard<std::mutex> g(mu);
+  auto it = done.find(key);
+  if (it != done.end() && it->second >= bytes) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) done[key] = bytes;
+  return e;
+}
+
 cudaError_t stream_scratch(void** p, size_t bytes, cudaStream_t stream) {
   static std::mutex mu;
   static bool configured[64] = {};

@@ -190,4 +190,8 @@ uint64_t resident_grid(const void* func, int tpb, size_t smem);
 // on the same stream.
 cudaError_t stream_scratch(void** p, size_t bytes, cudaStream_t stream);
 
+// Raise a kernel's dynamic shared-memory limit once per (kernel, device),
+// thread-safe.
+cudaError_t ensure_dynamic_smem(const void* func, size_t bytes);
+
 }  // namespace pv

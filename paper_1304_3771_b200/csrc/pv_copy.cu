@@ -457,14 +457,8 @@ cudaError_t launch_copy_exec(uint8_t* image, uint64_t image_bytes, const pv_op* 
   direction &= ~PV_COPY_ALIGNED16;
   if (aligned) {
     // host-proven 16-byte co-alignment: the TMA bulk path (1 CTA of 8 warps per SM)
-    static bool attr_set[64] = {};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev < 64 && !attr_set[dev]) {
-      cudaError_t e = cudaFuncSetAttribute(exec_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBulkSmem);
-      if (e != cudaSuccess) return e;
-      attr_set[dev] = true;
-    }
+    const cudaError_t e = ensure_dynamic_smem((const void*)exec_bulk_kernel, kBulkSmem);
+    if (e != cudaSuccess) return e;
     uint64_t grid = resident_grid((const void*)exec_bulk_kernel, kBulkWarps * 32, kBulkSmem);
     const uint64_t want = (n_pages + kBulkWarps - 1) / kBulkWarps;
     if (grid > want) grid = want;

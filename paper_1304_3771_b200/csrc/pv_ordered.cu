@@ -456,12 +456,8 @@ cudaError_t launch_copy_ordered(uint8_t* image, uint64_t image_bytes, const pv_o
   e = cub::DeviceScan::ExclusiveSum(s.cub_tmp, tb, s.seg_len, s.seg_start, (int)n_pages, stream);
   if (e != cudaSuccess) return e;
   constexpr size_t smem = sizeof(PageSmem) * kApPages;
-  static bool attr_set = false;
-  if (!attr_set) {
-    e = cudaFuncSetAttribute(ordered_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  e = ensure_dynamic_smem((const void*)ordered_apply_kernel, smem);
+  if (e != cudaSuccess) return e;
   uint64_t g2 = resident_grid((const void*)ordered_apply_kernel, kApPages * 64, smem);
   const uint64_t want = (n_pages + kApPages - 1) / kApPages;
   if (g2 > want) g2 = want;
