@@ -202,7 +202,10 @@ const char* pv_status_name(uint32_t status);
  * (then TDP-stage trap gpas are not reported).  Lanes not covered by any
  * segment are not written.  index (HOST pointer to a struct of device
  * pointers, may be NULL): leaf index consulted instead of the raw leaf PTEs
- * for indexed leaf nodes.
+ * for indexed leaf nodes.  Batches of at least 8 chunks per resident CTA
+ * build per-segment stage tables in library-internal scratch taken from the
+ * device's default stream-ordered pool (cudaMallocAsync / cudaFreeAsync on
+ * `stream`, 16.5 KiB per segment; the pool keeps up to 256 MiB cached).
  */
 int pv_translate(const uint8_t* image, uint64_t image_bytes,
                  const pv_space* spaces, const pv_seg* segs, uint32_t n_segs,
