@@ -420,6 +420,7 @@ def run_ours(args, rank, world, local):
         "clocks": clk,
         "e2e": e2e,
         "build_s": wl.build_s,
+        "provenance": provenance(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(wl, args)
@@ -980,6 +981,19 @@ def load_traffic(workload: str) -> dict:
             return json.load(f)
     except Exception:  # noqa: BLE001
         return {}
+
+
+def provenance() -> dict:
+    """Which code and which device produced this line."""
+    import torch
+
+    out = {"gpu": torch.cuda.get_device_name(0) if torch.cuda.is_available() else None}
+    try:
+        out["git"] = subprocess.run(["git", "-C", ROOT, "rev-parse", "--short", "HEAD"], capture_output=True,
+                                    text=True, timeout=10).stdout.strip() or None
+    except Exception:  # noqa: BLE001 - the GPU box's snapshot has no .git
+        out["git"] = None
+    return out
 
 
 def load_json_profile(name: str):
