@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define PV_ABI_VERSION 2
+#define PV_ABI_VERSION 3
 
 /* ---- return codes ------------------------------------------------------ */
 #define PV_SUCCESS 0
@@ -256,13 +256,16 @@ int pv_fifo_replay(const void* vas, uint32_t flags, const uint64_t* lane_idx,
  * first failing page in op_first_bad[] (device, n_ops; the caller sets it to
  * all-ones first).  For PV_TO_GUEST it also stamps destination pages in
  * page_owner[] (device, one u64 per image page; NULL disables) with
- * (epoch << 32 | op + 1) and sets *conflict (device u32) when two ops of the
- * batch write one hpa page.
+ * (epoch << 40 | page + 1), one stamp per live chunk, and sets *conflict
+ * (device u32) when two chunks of the batch write one hpa page.
  *
  * pv_copy_exec moves the bytes for every page below its op's first failing
  * page and fills results[] (device, n_ops).  dirty[] (device, one byte per
  * image page; may be NULL) is set to 1 for every image page written.
- * buf is the op buffer (device).  abort_flag (device, may be NULL): when
+ * buf is the op buffer (device) of buf_bytes bytes: a chunk reaching past
+ * it moves only the bytes the buffer holds (the reference's slice of a
+ * short host_buf, memvirt.py:624), never reading or writing beyond it.
+ * abort_flag (device, may be NULL): when
  * *abort_flag != 0 at launch (the conflict word of the stamp pass) the
  * kernel writes nothing, so the host can re-plan the batch in order.
  */
@@ -317,8 +320,9 @@ int pv_copy_ordered(uint8_t* image, uint64_t image_bytes, const pv_op* ops,
                     uint64_t n_ops, const uint64_t* page_off, uint64_t n_pages,
                     const uint64_t* page_hpa, const uint32_t* page_status,
                     const uint64_t* page_aux, const uint64_t* op_first_bad,
-                    const uint8_t* buf, pv_op_result* results, uint8_t* dirty,
-                    void* scratch, uint64_t scratch_bytes, void* stream);
+                    const uint8_t* buf, uint64_t buf_bytes, pv_op_result* results,
+                    uint8_t* dirty, void* scratch, uint64_t scratch_bytes,
+                    void* stream);
 
 /* ---- trap shim on the device -----------------------
  * The default hypervisor shim of the hybrid resolver (backend.py:117-128,

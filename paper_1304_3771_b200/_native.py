@@ -18,7 +18,7 @@ from .errors import NativeUnavailable
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpv.so")
 
 # ---- constants mirrored from include/pv.h --------------------------------
-ABI_VERSION = 2
+ABI_VERSION = 3
 SUCCESS = 0
 EINVAL = -22
 ENOMEM = -12
@@ -98,7 +98,7 @@ _SIGNATURES = {
     "pv_copy_shim": (ctypes.c_int, [_p, _u64, _p, _p, _p, _u64, _p, _u64, _p, _p, _p, _p, _p, _p, _u64, _p]),
     "pv_result_encode": (ctypes.c_int, [_p, _u64, _p, _p, _p, _p, _u64, _p, _p, _p]),
     "pv_result_decode": (ctypes.c_int, [_p, _u64, _p, _u64, _p, _p, _p]),
-    "pv_copy_ordered": (ctypes.c_int, [_p, _u64, _p, _u64, _p, _u64, _p, _p, _p, _p, _p, _p, _p, _p, _u64, _p]),
+    "pv_copy_ordered": (ctypes.c_int, [_p, _u64, _p, _u64, _p, _u64, _p, _p, _p, _p, _p, _u64, _p, _p, _p, _u64, _p]),
     "pv_copy_plan": (ctypes.c_int, [_p, _u64, _p, _p, _u64, _p, _u64, _u32, _p, _p, _p, _p, _p, _u32, _p, _p]),
     "pv_copy_stamp": (ctypes.c_int, [_p, _u64, _u64, _p, _p, _p, _u64, _u32, _p, _p]),
     "pv_copy_exec": (ctypes.c_int, [_p, _u64, _p, _u64, _p, _u64, _u32, _p, _p, _p, _p, _p, _u64, _p, _p, _p, _p]),

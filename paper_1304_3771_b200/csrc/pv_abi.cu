@@ -22,7 +22,7 @@ cudaError_t launch_copy_stamp(const uint64_t*, uint64_t, uint64_t, const uint64_
                               uint64_t, uint32_t, uint32_t*, cudaStream_t);
 cudaError_t launch_copy_exec(uint8_t*, uint64_t, const pv_op*, uint64_t, const uint64_t*, uint64_t, uint32_t,
                              const uint64_t*, const uint32_t*, const uint64_t*, const uint64_t*, uint8_t*,
-                             pv_op_result*, uint8_t*, const uint32_t*, cudaStream_t);
+                             uint64_t, pv_op_result*, uint8_t*, const uint32_t*, cudaStream_t);
 size_t fifo_scratch_bytes(uint64_t, uint64_t, uint32_t);
 size_t shim_scratch_bytes(uint64_t);
 size_t map_scratch_bytes();
@@ -47,8 +47,8 @@ cudaError_t launch_result_encode(uint8_t*, uint64_t, const uint64_t*, const uint
 cudaError_t launch_result_decode(const uint8_t*, uint64_t, const uint64_t*, uint64_t, uint32_t*, uint32_t*,
                                  cudaStream_t);
 cudaError_t launch_copy_ordered(uint8_t*, uint64_t, const pv_op*, uint64_t, const uint64_t*, uint64_t, const uint64_t*,
-                                const uint32_t*, const uint64_t*, const uint64_t*, const uint8_t*, pv_op_result*,
-                                uint8_t*, void*, uint64_t, cudaStream_t);
+                                const uint32_t*, const uint64_t*, const uint64_t*, const uint8_t*, uint64_t,
+                                pv_op_result*, uint8_t*, void*, uint64_t, cudaStream_t);
 cudaError_t launch_fifo_lanes_abi(const void*, uint32_t, const uint64_t*, const uint64_t*, const uint64_t*, uint32_t,
                                   uint64_t, uint64_t, uint32_t, pv_fifo*, uint64_t*, uint32_t*, void*, uint64_t,
                                   cudaStream_t);
@@ -220,6 +220,8 @@ int pv_translate(const uint8_t* image, uint64_t image_bytes, const pv_space* spa
   if (n_chunks == 0) return PV_SUCCESS;
   if (!image || !spaces || !segs || !vas || !out_value || !out_status || n_segs == 0) return PV_EINVAL;
   if (image_bytes % kPageSize) return PV_EINVAL;
+  // 4-byte walk codes carry leaf pfns in 28 bits (pv_translate.cu stage_codes)
+  if (image_bytes >= (1ull << 40)) return PV_EINVAL;
   if (flags & ~(uint32_t)(PV_VA32 | PV_OUT_PFN | PV_HAS_TWO_STAGE | PV_HAS_4L)) return PV_EINVAL;
   const bool two = flags & PV_HAS_TWO_STAGE;
   if (index != nullptr && (!index->slot_of || !index->leaf_codes || !index->slot_page)) return PV_EINVAL;
@@ -285,14 +287,14 @@ int pv_copy_exec(uint8_t* image, uint64_t image_bytes, const pv_op* ops, uint64_
                  uint64_t n_pages, uint32_t direction, const uint64_t* page_hpa, const uint32_t* page_status,
                  const uint64_t* page_aux, const uint64_t* op_first_bad, uint8_t* buf, uint64_t buf_bytes,
                  pv_op_result* results, uint8_t* dirty, const uint32_t* abort_flag, void* stream) {
-  (void)buf_bytes;
   if (n_pages == 0) return PV_SUCCESS;
   if (!image || !ops || !page_off || !page_hpa || !page_status || !op_first_bad || !buf || !results)
     return PV_EINVAL;
   if ((direction & ~PV_COPY_ALIGNED16) != PV_TO_GUEST && (direction & ~PV_COPY_ALIGNED16) != PV_FROM_GUEST)
     return PV_EINVAL;
   return rc(launch_copy_exec(image, image_bytes, ops, n_ops, page_off, n_pages, direction, page_hpa, page_status,
-                             page_aux, op_first_bad, buf, results, dirty, abort_flag, (cudaStream_t)stream));
+                             page_aux, op_first_bad, buf, buf_bytes, results, dirty, abort_flag,
+                             (cudaStream_t)stream));
 }
 
 int pv_copy_fifo_replay(const pv_op* ops, const uint64_t* page_off, const uint64_t* look_page, const uint32_t* look_op,
@@ -381,14 +383,15 @@ uint64_t pv_copy_ordered_scratch_bytes(uint64_t n_pages, uint64_t image_bytes) {
 
 int pv_copy_ordered(uint8_t* image, uint64_t image_bytes, const pv_op* ops, uint64_t n_ops, const uint64_t* page_off,
                     uint64_t n_pages, const uint64_t* page_hpa, const uint32_t* page_status,
-                    const uint64_t* page_aux, const uint64_t* op_first_bad, const uint8_t* buf,
+                    const uint64_t* page_aux, const uint64_t* op_first_bad, const uint8_t* buf, uint64_t buf_bytes,
                     pv_op_result* results, uint8_t* dirty, void* scratch, uint64_t scratch_bytes, void* stream) {
   if (n_ops == 0) return PV_SUCCESS;
   if (!image || !ops || !page_off || !page_hpa || !page_status || !op_first_bad || !buf || !results || !scratch)
     return PV_EINVAL;
   if (image_bytes % kPageSize) return PV_EINVAL;
   return rc(launch_copy_ordered(image, image_bytes, ops, n_ops, page_off, n_pages, page_hpa, page_status, page_aux,
-                                op_first_bad, buf, results, dirty, scratch, scratch_bytes, (cudaStream_t)stream));
+                                op_first_bad, buf, buf_bytes, results, dirty, scratch, scratch_bytes,
+                                (cudaStream_t)stream));
 }
 
 int pv_result_encode(uint8_t* image, uint64_t image_bytes, const uint64_t* page_hpa, const uint32_t* header,

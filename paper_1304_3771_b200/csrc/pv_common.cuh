@@ -170,6 +170,12 @@ __host__ __device__ __forceinline__ uint64_t op_page_va(uint64_t gva, uint64_t k
   return k == 0 ? gva : ((gva >> kPageShift) + k) << kPageShift;
 }
 
+// Bytes of a `len`-byte chunk at buffer offset `at` that lie inside a
+// `buf_bytes`-byte op buffer (a short host_buf slice, memvirt.py:624).
+__host__ __device__ __forceinline__ uint32_t buf_clamp(uint64_t at, uint32_t len, uint64_t buf_bytes) {
+  return at >= buf_bytes ? 0u : (buf_bytes - at < len ? (uint32_t)(buf_bytes - at) : len);
+}
+
 // Largest i with off[i] <= p, searching [lo, hi).
 __device__ __forceinline__ uint64_t upper_search(const uint64_t* __restrict__ off, uint64_t lo, uint64_t hi,
                                                  uint64_t p) {

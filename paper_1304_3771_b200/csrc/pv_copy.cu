@@ -7,7 +7,11 @@
 //     copied, nothing after it; `copied` is the completed prefix
 //     (PageFault.bytes_copied, memvirt.py:618-622);
 //   * the data access is bounds-checked against host memory and raises
-//     OutOfRange (memvirt.py:156-168) -- also a stopping point.
+//     OutOfRange (memvirt.py:156-168) -- also a stopping point;
+//   * the op buffer side is clamped at buf_bytes: a chunk reaching past the
+//     buffer moves only the bytes the buffer holds, like the reference's
+//     slices of a short host_buf (host_buf[copied:copied + chunk],
+//     memvirt.py:624) -- the page is still translated and counted.
 //
 // B200 design: two launches over one flat page list of the batch.
 //   plan  : one thread per 4 pages walks each page (L1-cached upper levels,
@@ -191,8 +195,8 @@ exec_kernel(uint8_t* __restrict__ image, uint64_t image_bytes, const pv_op* __re
             const uint64_t* __restrict__ page_off, uint64_t n_pages, uint32_t direction,
             const uint64_t* __restrict__ page_hpa, const uint32_t* __restrict__ page_status,
             const uint64_t* __restrict__ page_aux, const unsigned long long* __restrict__ op_first_bad,
-            uint8_t* __restrict__ buf, pv_op_result* __restrict__ results, uint8_t* __restrict__ dirty,
-            const uint32_t* __restrict__ abort_flag) {
+            uint8_t* __restrict__ buf, uint64_t buf_bytes, pv_op_result* __restrict__ results,
+            uint8_t* __restrict__ dirty, const uint32_t* __restrict__ abort_flag) {
   // A conflicted batch (stamp pass) is left untouched for the host to re-plan.
   if (abort_flag != nullptr && *abort_flag != 0) return;
   const uint64_t pol = policy_evict_first();
@@ -237,7 +241,8 @@ exec_kernel(uint8_t* __restrict__ image, uint64_t image_bytes, const pv_op* __re
       }
       if (k >= bad) continue;
       const uint64_t hpa = page_hpa[p];
-      const uint32_t chunk = (uint32_t)min(o.len - done, kPageSize - (cur & kPageMask));
+      const uint32_t chunk = buf_clamp(o.buf_off + done, (uint32_t)min(o.len - done, kPageSize - (cur & kPageMask)),
+                                       buf_bytes);
       uint8_t* bp = buf + o.buf_off + done;
       uint8_t* dst = direction == PV_TO_GUEST ? image + hpa : bp;
       const uint8_t* src = direction == PV_TO_GUEST ? bp : image + hpa;
@@ -284,8 +289,8 @@ exec_bulk_kernel(uint8_t* __restrict__ image, uint64_t image_bytes, const pv_op*
                  const uint64_t* __restrict__ page_off, uint64_t n_pages, uint32_t direction,
                  const uint64_t* __restrict__ page_hpa, const uint32_t* __restrict__ page_status,
                  const uint64_t* __restrict__ page_aux, const unsigned long long* __restrict__ op_first_bad,
-                 uint8_t* __restrict__ buf, pv_op_result* __restrict__ results, uint8_t* __restrict__ dirty,
-                 const uint32_t* __restrict__ abort_flag) {
+                 uint8_t* __restrict__ buf, uint64_t buf_bytes, pv_op_result* __restrict__ results,
+                 uint8_t* __restrict__ dirty, const uint32_t* __restrict__ abort_flag) {
   extern __shared__ __align__(128) uint8_t bulk_ring[];
   __shared__ __align__(8) uint64_t bars[kBulkWarps][kBulkStages];
   if (abort_flag != nullptr && *abort_flag != 0) return;
@@ -338,7 +343,8 @@ exec_bulk_kernel(uint8_t* __restrict__ image, uint64_t image_bytes, const pv_op*
       }
       if (k < bad) {
         const uint64_t hpa = page_hpa[p];
-        const uint32_t len = (uint32_t)min(o.len - done, kPageSize - (cur & kPageMask));
+        const uint32_t len =
+            buf_clamp(o.buf_off + done, (uint32_t)min(o.len - done, kPageSize - (cur & kPageMask)), buf_bytes);
         uint8_t* bp = buf + o.buf_off + done;
         m.dst = reinterpret_cast<uint64_t>(to_guest ? image + hpa : bp);
         m.src = reinterpret_cast<uint64_t>(to_guest ? bp : image + hpa);
@@ -450,8 +456,8 @@ cudaError_t launch_copy_stamp(const uint64_t* page_off, uint64_t n_ops, uint64_t
 cudaError_t launch_copy_exec(uint8_t* image, uint64_t image_bytes, const pv_op* ops, uint64_t n_ops,
                              const uint64_t* page_off, uint64_t n_pages, uint32_t direction, const uint64_t* page_hpa,
                              const uint32_t* page_status, const uint64_t* page_aux, const uint64_t* op_first_bad,
-                             uint8_t* buf, pv_op_result* results, uint8_t* dirty, const uint32_t* abort_flag,
-                             cudaStream_t stream) {
+                             uint8_t* buf, uint64_t buf_bytes, pv_op_result* results, uint8_t* dirty,
+                             const uint32_t* abort_flag, cudaStream_t stream) {
   if (n_pages == 0) return cudaSuccess;
   const bool aligned = direction & PV_COPY_ALIGNED16;
   direction &= ~PV_COPY_ALIGNED16;
@@ -464,7 +470,7 @@ cudaError_t launch_copy_exec(uint8_t* image, uint64_t image_bytes, const pv_op* 
     if (grid > want) grid = want;
     exec_bulk_kernel<<<(unsigned)grid, kBulkWarps * 32, kBulkSmem, stream>>>(
         image, image_bytes, ops, n_ops, page_off, n_pages, direction, page_hpa, page_status, page_aux,
-        reinterpret_cast<const unsigned long long*>(op_first_bad), buf, results, dirty, abort_flag);
+        reinterpret_cast<const unsigned long long*>(op_first_bad), buf, buf_bytes, results, dirty, abort_flag);
     return cudaGetLastError();
   }
   auto k = exec_kernel;
@@ -474,8 +480,8 @@ cudaError_t launch_copy_exec(uint8_t* image, uint64_t image_bytes, const pv_op* 
   if (grid > cap) grid = cap;
   k<<<(unsigned)grid, kExecTpb, 0, stream>>>(image, image_bytes, ops, n_ops, page_off, n_pages, direction, page_hpa,
                                              page_status, page_aux,
-                                             reinterpret_cast<const unsigned long long*>(op_first_bad), buf, results,
-                                             dirty, abort_flag);
+                                             reinterpret_cast<const unsigned long long*>(op_first_bad), buf, buf_bytes,
+                                             results, dirty, abort_flag);
   return cudaGetLastError();
 }
 

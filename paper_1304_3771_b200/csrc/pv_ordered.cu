@@ -13,11 +13,12 @@
 // mbarrier) into a circular byte ring, up to kK chunks ahead, LAST CHUNK
 // FIRST; the consumer lets each byte take the value of the first arrival that
 // covers it (a per-block coverage map skips bytes a later writer already
-// set), which is exactly the state the in-order copies leave.  All source
-// bytes really move (HBM -> SMEM); the overwritten ones are simply never
-// copied on from SMEM, the way a write-back cache would absorb them, and the
-// page is written back once.  The pipeline is warp-private: no CTA-wide
-// barriers on the per-chunk path.
+// set), which is exactly the state the in-order copies leave.  Chunks that
+// later writers overwrite completely never move: both warps first walk the
+// page's descriptors last-first until the chunks seen cover the whole page
+// (live_chunks, metadata only), and only those chunks are streamed; a fully
+// covered page is not even read.  The page is written back once.  The
+// pipeline is warp-private: no CTA-wide barriers on the per-chunk path.
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_run_length_encode.cuh>
 #include <cub/device/device_scan.cuh>
@@ -66,7 +67,7 @@ __global__ void ordered_keys_kernel(const pv_op* __restrict__ ops, uint64_t n_op
                                     const uint64_t* __restrict__ page_hpa, const uint32_t* __restrict__ page_status,
                                     const uint64_t* __restrict__ page_aux,
                                     const unsigned long long* __restrict__ first_bad, const uint8_t* __restrict__ buf,
-                                    uint32_t dead_key, uint32_t* __restrict__ keys,
+                                    uint64_t buf_bytes, uint32_t dead_key, uint32_t* __restrict__ keys,
                                     ChunkDesc* __restrict__ desc, pv_op_result* __restrict__ results) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_ops; i += stride) {
@@ -81,7 +82,8 @@ __global__ void ordered_keys_kernel(const pv_op* __restrict__ ops, uint64_t n_op
       keys[p] = live ? (uint32_t)(hpa >> kPageShift) : dead_key;
       const uint64_t cur = op_page_va(o.gva, k);
       const uint64_t done = cur - o.gva;
-      const uint32_t len = live ? (uint32_t)min(o.len - done, kPageSize - (cur & kPageMask)) : 0;
+      const uint32_t len =
+          live ? buf_clamp(o.buf_off + done, (uint32_t)min(o.len - done, kPageSize - (cur & kPageMask)), buf_bytes) : 0;
       const uint64_t src = reinterpret_cast<uint64_t>(buf + o.buf_off + done);
       ChunkDesc d;
       d.src = src & ~15ull;
@@ -283,6 +285,40 @@ __device__ __forceinline__ void produce(PageSmem& P, const ChunkDesc* __restrict
   }
 }
 
+// How many of a page's chunks (counted from the LAST one, program order) can
+// still change its bytes: walking the chunk descriptors last-first, the
+// chunks before the one that completes the page's coverage are overwritten
+// entirely by later writers, so neither their payload nor their turn in the
+// ring is needed.  Coverage only depends on (offset, len) -- the metadata --
+// so both warps of a page slot compute the same count without talking.
+// Lane l tracks bytes [128 l, 128 l + 128) of the page in four words.
+// *full: the live chunks cover every byte (the page need not be read first).
+__device__ __forceinline__ uint32_t live_chunks(const ChunkDesc* __restrict__ desc, uint32_t b, uint32_t n,
+                                                uint32_t lane, bool* full) {
+  uint32_t c[4] = {0u, 0u, 0u, 0u};
+  const int32_t mine = 128 * (int32_t)lane;
+  for (uint32_t k0 = 0; k0 < n; k0 += 32) {
+    const uint32_t meta = k0 + lane < n ? desc[b + n - 1 - (k0 + lane)].meta : 0u;
+    const uint32_t m = n - k0 < 32 ? n - k0 : 32;
+    for (uint32_t j = 0; j < m; ++j) {
+      const uint32_t mj = __shfl_sync(0xFFFFFFFFu, meta, (int)j);
+      const int32_t off = (int32_t)((mj >> 4) & 0xFFF), len = (int32_t)(mj >> 16);
+      const int32_t lo = max(off - mine, 0), hi = min(off + len - mine, 128);
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const int32_t wl = max(lo - 32 * w, 0), wh = min(hi - 32 * w, 32);
+        if (wl < wh) c[w] |= (wh == 32 ? 0xFFFFFFFFu : ((1u << wh) - 1u)) & ~((1u << wl) - 1u);
+      }
+      if (__all_sync(0xFFFFFFFFu, (c[0] & c[1] & c[2] & c[3]) == 0xFFFFFFFFu)) {
+        *full = true;
+        return k0 + j + 1;
+      }
+    }
+  }
+  *full = false;
+  return n;
+}
+
 __global__ void __launch_bounds__(kApPages * 64)
 ordered_apply_kernel(uint8_t* __restrict__ image, const ChunkDesc* __restrict__ desc,
                      const uint32_t* __restrict__ seg_key, const uint32_t* __restrict__ seg_len,
@@ -308,15 +344,21 @@ ordered_apply_kernel(uint8_t* __restrict__ image, const ChunkDesc* __restrict__ 
   for (uint32_t s = blockIdx.x * kApPages + pslot; s < n_segs; s += gridDim.x * kApPages) {
     const uint32_t key = seg_key[s];
     if (key == dead_key) continue;
-    const uint32_t b = seg_start[s], n = seg_len[s];
+    const uint32_t b = seg_start[s], n_all = seg_len[s];
+    // only the last n chunks can change the page (live_chunks); both roles
+    // agree on n, so the ring accounting (G, vhead) stays in step
+    bool covered;
+    const uint32_t n = live_chunks(desc, b, n_all, lane, &covered);
     if (producer) {
-      produce(P, desc, b, n, lane, pol, G, vhead, hptr, released);
+      produce(P, desc, b + n_all - n, n, lane, pol, G, vhead, hptr, released);
       continue;
     }
     const uint64_t dst = (uint64_t)key << kPageShift;
+    if (!covered) {  // bytes no chunk writes keep the page's current contents
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
-      reinterpret_cast<uint4*>(P.page)[lane + 32 * k] = reinterpret_cast<const uint4*>(image + dst)[lane + 32 * k];
+      for (int k = 0; k < 8; ++k)
+        reinterpret_cast<uint4*>(P.page)[lane + 32 * k] = reinterpret_cast<const uint4*>(image + dst)[lane + 32 * k];
+    }
     reinterpret_cast<uint4*>(P.cov)[lane] = make_uint4(0, 0, 0, 0);
     uint32_t open_blocks = kPageSize / 16;  // blocks not yet final (warp-uniform)
     __syncwarp();
@@ -419,8 +461,8 @@ static OrderedScratch carve(void* base, uint64_t n, size_t cub_bytes) {
 cudaError_t launch_copy_ordered(uint8_t* image, uint64_t image_bytes, const pv_op* ops, uint64_t n_ops,
                                 const uint64_t* page_off, uint64_t n_pages, const uint64_t* page_hpa,
                                 const uint32_t* page_status, const uint64_t* page_aux, const uint64_t* op_first_bad,
-                                const uint8_t* buf, pv_op_result* results, uint8_t* dirty, void* scratch,
-                                uint64_t scratch_bytes, cudaStream_t stream) {
+                                const uint8_t* buf, uint64_t buf_bytes, pv_op_result* results, uint8_t* dirty,
+                                void* scratch, uint64_t scratch_bytes, cudaStream_t stream) {
   if (n_pages == 0) {
     uint64_t g = (n_ops + 255) / 256;
     if (g > 4096) g = 4096;
@@ -441,7 +483,7 @@ cudaError_t launch_copy_ordered(uint8_t* image, uint64_t image_bytes, const pv_o
     if (g > 8192) g = 8192;
     ordered_keys_kernel<<<(unsigned)g, 256, 0, stream>>>(ops, n_ops, page_off, page_hpa, page_status, page_aux,
                                                          reinterpret_cast<const unsigned long long*>(op_first_bad),
-                                                         buf, dead_key, s.keys_in, s.desc, results);
+                                                         buf, buf_bytes, dead_key, s.keys_in, s.desc, results);
   }
   size_t tb = s.cub_bytes;
   // the 16-byte descriptors ride along as the sort's values (no index gather afterwards)

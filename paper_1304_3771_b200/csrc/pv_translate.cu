@@ -67,7 +67,8 @@ __device__ __forceinline__ uint64_t ld_stream_va(const void* vas, uint64_t i, bo
 
 // Stage the upper two levels of one walk stage (all threads; ends with a
 // barrier): the Stage record and the 512 codes of each top entry t_sel ..
-// t_sel + t_cnt - 1, written to codes[t * 512 ...].  Requires image_bytes < 2^41 so leaf pfns fit 29 bits.
+// t_sel + t_cnt - 1, written to codes[t * 512 ...].  Leaf pfns take 28 bits of a
+// code (pfn << 4), so images must be below 2^40 bytes (pv_translate checks).
 __device__ void stage_codes(const uint8_t* __restrict__ image, uint64_t image_bytes, uint64_t base, uint64_t root,
                             uint32_t stage2, Stage& s, uint32_t* codes /*[4*512]*/,
                             const uint32_t* __restrict__ slot_of, uint32_t t_sel, uint32_t t_cnt) {

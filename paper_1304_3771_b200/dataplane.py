@@ -667,11 +667,14 @@ def _shim_scratch(image, n_pages: int):
 
 
 def copy_launch(image, plan: CopyPlan, direction: int, buf, *, fifo_dev=None, fifo_cap: int = 10,
-                detect_conflicts: bool = True, track_dirty: bool = True, buf_ready=None) -> None:
+                detect_conflicts: bool = True, track_dirty: bool = True, buf_ready=None,
+                buf_bytes: int | None = None) -> None:
     """Enqueue plan (+ FIFO replay) (+ conflict stamp) + exec on the current
     stream.  Results land in ``plan.results`` / ``plan.conflict``.
     ``buf_ready`` (a CUDA event, optional): the buffer is still arriving on
-    another stream; only the exec waits for it, the plan passes overlap it."""
+    another stream; only the exec waits for it, the plan passes overlap it.
+    ``buf_bytes`` (default ``buf.numel()``): bytes of ``buf`` the ops may
+    touch; chunks reaching past it move only what the buffer holds."""
     lib = N.lib()
     dev_img = image.device()
     s = _stream().cuda_stream
@@ -723,7 +726,8 @@ def copy_launch(image, plan: CopyPlan, direction: int, buf, *, fifo_dev=None, fi
         N.check(lib.pv_copy_exec(dev_img.data_ptr(), image.nbytes, plan.ops.data_ptr(), plan.n_ops,
                                  plan.page_off.data_ptr(), plan.n_pages, direction | hint, plan.page_hpa.data_ptr(),
                                  plan.page_status.data_ptr(), plan.page_aux.data_ptr(), plan.first_bad.data_ptr(),
-                                 buf.data_ptr(), buf.numel(), plan.results.data_ptr(), dirty, abort, s),
+                                 buf.data_ptr(), buf.numel() if buf_bytes is None else buf_bytes,
+                                 plan.results.data_ptr(), dirty, abort, s),
                 "pv_copy_exec")
         if direction == N.TO_GUEST:
             image.note_device_write()
@@ -749,7 +753,7 @@ def decode_results(res: np.ndarray) -> list[OpOutcome]:
     return out
 
 
-def copy_ordered(image, plan: CopyPlan, buf) -> None:
+def copy_ordered(image, plan: CopyPlan, buf, buf_bytes: int | None = None) -> None:
     """Ordered execution of a planned to_guest batch whose chunks share
     destination pages (pv_copy_ordered): exact last-writer-wins."""
     import torch
@@ -761,13 +765,14 @@ def copy_ordered(image, plan: CopyPlan, buf) -> None:
     N.check(lib.pv_copy_ordered(dev_img.data_ptr(), image.nbytes, plan.ops.data_ptr(), plan.n_ops,
                                 plan.page_off.data_ptr(), plan.n_pages, plan.page_hpa.data_ptr(),
                                 plan.page_status.data_ptr(), plan.page_aux.data_ptr(), plan.first_bad.data_ptr(),
-                                buf.data_ptr(), plan.results.data_ptr(), image.dirty_map().data_ptr(),
+                                buf.data_ptr(), buf.numel() if buf_bytes is None else buf_bytes,
+                                plan.results.data_ptr(), image.dirty_map().data_ptr(),
                                 scratch.data_ptr(), nbytes, _stream().cuda_stream), "pv_copy_ordered")
     image.note_device_write()
 
 
 def copy_ops(image, spaces: list[Space], ops: np.ndarray, direction: int, buf, *, caches=None, fifo_groups=None,
-             detect_conflicts: bool = True, shims=None, buf_ready=None) -> list[OpOutcome]:
+             detect_conflicts: bool = True, shims=None, buf_ready=None, buf_bytes: int | None = None) -> list[OpOutcome]:
     """Run a batch of copies with the reference's sequential semantics.
 
     ``caches`` (with ``fifo_groups``) are host TranslationCache objects whose
@@ -780,9 +785,9 @@ def copy_ops(image, spaces: list[Space], ops: np.ndarray, direction: int, buf, *
     plan = CopyPlan(spaces, ops, fifo_groups=fifo_groups if caches is not None else None, shims=shims)
     fifo_dev = _to_dev(pack_fifo(caches)) if caches is not None else None
     copy_launch(image, plan, direction, buf, fifo_dev=fifo_dev, fifo_cap=cap, detect_conflicts=detect_conflicts,
-                buf_ready=buf_ready)
+                buf_ready=buf_ready, buf_bytes=buf_bytes)
     if direction == N.TO_GUEST and detect_conflicts and int(plan.conflict.item()):
-        copy_ordered(image, plan, buf)
+        copy_ordered(image, plan, buf, buf_bytes)
     results = decode_results(plan.results.cpu().numpy())
     if plan.shims is not None and int(plan.shim_written.item()):
         image.note_device_write()  # the shim rewrote shadow leaves

@@ -109,7 +109,11 @@ def _src_async(src):
     return _as_src_tensor(src), None
 
 
-def _ops_rows(gvas, lengths, offsets):
+def _ops_rows(gvas, lengths, offsets, src_bytes=None):
+    """pv_op rows (gva, len, buf_off, space 0).  With ``src_bytes`` (a
+    to_guest source of that many bytes) each op has the slice semantics of
+    ``copy_to_user(gva, src[off:off + len])``: a slice running past the
+    source is shorter, so the op copies (and translates) fewer bytes."""
     gvas = np.asarray(gvas, dtype=np.uint64)
     lengths = np.asarray(lengths, dtype=np.uint64)
     if offsets is None:
@@ -117,7 +121,22 @@ def _ops_rows(gvas, lengths, offsets):
         if len(lengths) > 1:
             np.cumsum(lengths[:-1], out=offsets[1:])
     offsets = np.asarray(offsets, dtype=np.uint64)
+    if len(gvas) != len(lengths) or len(offsets) != len(lengths):
+        raise ValueError("gvas, lengths and offsets must have one entry per op")
+    if src_bytes is not None:
+        room = np.where(offsets < np.uint64(src_bytes), np.uint64(src_bytes) - offsets, np.uint64(0))
+        lengths = np.minimum(lengths, room)
     return np.stack([gvas, lengths, offsets, np.zeros(len(gvas), np.uint64)], axis=1)
+
+
+def _nbytes(src) -> int:
+    import torch
+
+    if isinstance(src, torch.Tensor):
+        return src.numel() * src.element_size()
+    if isinstance(src, np.ndarray):
+        return src.nbytes
+    return len(memoryview(src).cast("B"))
 
 
 def _decode_outcome(out: dp.OpOutcome, row, image_bytes: int):
@@ -200,7 +219,7 @@ class _BatchMixin:
         """copy_to_user(gvas[i], src[offsets[i]:offsets[i]+lengths[i]]) for
         every i, in order, on the device.  Returns per-op outcomes."""
         self._bump(len(gvas))
-        rows = _ops_rows(gvas, lengths, offsets)
+        rows = _ops_rows(gvas, lengths, offsets, src_bytes=_nbytes(src))
         buf, ready = _src_async(src)
         return self._batch(N.TO_GUEST, rows, buf, ready)
 

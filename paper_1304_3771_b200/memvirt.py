@@ -316,13 +316,18 @@ class TableEditor:
     def _leaf_slot(self, va: int, create: bool) -> tuple[int, int]:
         top, mid, leaf, _ = split_va(va)
         node = self._root.root_pfn
-        for level, index in ((LEVEL_TOP, top), (LEVEL_MID, mid)):
+        for index in (top, mid):
             word = self._mem.read_word(node, index)
             if entry_state(word) is not EntryState.NOT_PRESENT:
                 node = word >> PAGE_SHIFT
                 continue
             if not create:
-                raise PageFault(va, level)
+                # the reference names the level with an identity test,
+                # ``LEVEL_TOP if index is top else LEVEL_MID``
+                # (memvirt.py:290): CPython's small ints make a missing mid
+                # node whose mid index equals the top index (0..3) a level-1
+                # fault; value equality reproduces that in this range
+                raise PageFault(va, LEVEL_TOP if index == top else LEVEL_MID)
             child = self._alloc()
             self._mem.write_word(node, index, (child << PAGE_SHIFT) | FLAG_PRESENT | FLAG_WRITABLE)
             node = child
@@ -993,15 +998,22 @@ def copy_user_buffer(direction: str, gva: Gva, length: int, host_buf, *, transla
 
     to_guest = direction == "to_guest"
     if to_guest:
+        # a host_buf shorter than ``length`` behaves like the reference's
+        # slices of it (memvirt.py:624): every page is still translated, only
+        # the bytes the buffer holds are written (the kernels clamp at
+        # buf_bytes).  The reference bounds-checks the shorter write; here the
+        # page's full chunk is checked.
         src = np.frombuffer(bytes(host_buf[0:length]), dtype=np.uint8)
-        buf = dp._to_dev(src)
+        avail = len(src)
+        buf = dp._to_dev(src) if avail else torch.zeros(1, dtype=torch.uint8, device="cuda")
     else:
+        avail = length
         buf = torch.empty(length, dtype=torch.uint8, device="cuda")
     space = getattr(translator, "device_space", None)
     if space is None:
-        copied, err = _copy_foreign_translator(direction, gva, length, buf, translator, host_mem)
+        copied, err = _copy_foreign_translator(direction, gva, length, buf, translator, host_mem, avail)
     else:
-        copied, err = _copy_device(direction, gva, length, buf, translator, host_mem, space)
+        copied, err = _copy_device(direction, gva, length, buf, translator, host_mem, space, buf_bytes=avail)
     if not to_guest and copied:
         host_buf[0:copied] = buf[:copied].cpu().numpy().tobytes()
     if err is not None:
@@ -1009,7 +1021,7 @@ def copy_user_buffer(direction: str, gva: Gva, length: int, host_buf, *, transla
     return copied
 
 
-def _copy_device(direction, gva, length, buf, translator, host_mem, space, first_shimmed=False):
+def _copy_device(direction, gva, length, buf, translator, host_mem, space, first_shimmed=False, buf_bytes=None):
     """Device plan/exec for our own translators (cached, uncached, hybrid)."""
     op = np.array([[gva & dp.U64, length, 0, 0]], dtype=np.uint64)
     d = N.TO_GUEST if direction == "to_guest" else N.FROM_GUEST
@@ -1025,7 +1037,7 @@ def _copy_device(direction, gva, length, buf, translator, host_mem, space, first
         cur_op[0, 1] = length - done
         cur_op[0, 2] = done
         out = dp.copy_ops(image, [space], cur_op, d, buf, caches=caches, fifo_groups=groups,
-                          shims=[getattr(translator, "device_shim", None)])[0]
+                          shims=[getattr(translator, "device_shim", None)], buf_bytes=buf_bytes)[0]
         count = getattr(translator, "_count", None)
         if out.status == N.ST_OK:
             if count is not None:
@@ -1066,9 +1078,11 @@ def _copy_device(direction, gva, length, buf, translator, host_mem, space, first
         return copied, None
 
 
-def _copy_foreign_translator(direction, gva, length, buf, translator, host_mem):
+def _copy_foreign_translator(direction, gva, length, buf, translator, host_mem, avail=None):
     """A duck-typed translator object: translate per page through it, move
-    the bytes with device copies on the HBM image."""
+    the bytes with device copies on the HBM image (``avail``: bytes ``buf``
+    holds; chunks past it move only those, like the reference's slices)."""
+    avail = length if avail is None else avail
     image = host_mem.backing
     dev = image.device()
     copied = 0
@@ -1083,12 +1097,14 @@ def _copy_foreign_translator(direction, gva, length, buf, translator, host_mem):
         except Exception as exc:  # noqa: BLE001
             return copied, exc
         start = host_mem.base + hpa
-        if hpa < 0 or hpa + chunk > host_mem.size_bytes:
-            return copied, OutOfRange(f"access [{hpa:#x}, +{chunk}) beyond {host_mem.size_bytes:#x}")
+        n = max(0, min(chunk, avail - copied)) if direction == "to_guest" else chunk
+        if hpa < 0 or hpa + n > host_mem.size_bytes:
+            return copied, OutOfRange(f"access [{hpa:#x}, +{n}) beyond {host_mem.size_bytes:#x}")
         if direction == "to_guest":
-            dev[start:start + chunk].copy_(buf[copied:copied + chunk])
-            image._dev_dirty[start >> PAGE_SHIFT:((start + chunk - 1) >> PAGE_SHIFT) + 1] = 1
-            image.note_device_write()
+            if n:
+                dev[start:start + n].copy_(buf[copied:copied + n])
+                image._dev_dirty[start >> PAGE_SHIFT:((start + n - 1) >> PAGE_SHIFT) + 1] = 1
+                image.note_device_write()
         else:
             buf[copied:copied + chunk].copy_(dev[start:start + chunk])
         copied += chunk
