@@ -324,6 +324,58 @@ int pv_copy_ordered(uint8_t* image, uint64_t image_bytes, const pv_op* ops,
                     uint8_t* dirty, void* scratch, uint64_t scratch_bytes,
                     void* stream);
 
+/* ---- per-call path (one walk or one small copy per launch) -----------------
+ * The reference's drivers call ctx.mem.copy_to_user / copy_from_user once per
+ * op and ProcessTranslator.translate once per page (devices.py:148, 254, 316;
+ * backend.py:92-104; memvirt.py:585-628).  These entry points serve one such
+ * call in ONE launch with no memcpy: the request travels in the kernel's
+ * parameters (by value), results are written straight into host-mapped
+ * pinned memory (pv_host_alloc) and published last with `seq`, so the caller
+ * can spin on out->seq instead of synchronising the stream.
+ *
+ * pv_walk_one: walk / walk_guest / translate (uncached) / resolve_hybrid of
+ * one address (memvirt.py:244-267, 596-601, 677-682).  flags: PV_OUT_PFN.
+ * out->value / aux / status follow the pv_translate conventions. */
+typedef struct pv_one_result {
+  uint64_t value;
+  uint64_t aux;
+  uint64_t status;
+  uint64_t seq; /* written last (after a system-scope fence) */
+} pv_one_result;
+int pv_walk_one(const uint8_t* image, uint64_t image_bytes, const pv_space* space /* host */,
+                uint64_t va, uint32_t flags, pv_one_result* out, uint64_t seq, void* stream);
+
+/* pv_copy_small: one copy_user_buffer op of at most PV_SMALL_PAGES pages
+ * (memvirt.py:604-628): every page translated (pre_hpa[k] != 0: the caller
+ * resolved page k itself -- a FIFO cache hit -- to byte hpa pre_hpa[k] - 1;
+ * still bounds-checked), the op stops at its first failing
+ * page, the chunks before it move between `buf` (device memory or
+ * host-mapped pinned memory, buf_bytes bytes, clamped like pv_copy_exec) and
+ * the image, dirty[] marks written image pages.  out->page_hpa /
+ * page_status hold every page's translation (for the caller's FIFO inserts). */
+#define PV_SMALL_PAGES 64
+typedef struct pv_small_op {
+  pv_space space;
+  uint64_t gva;
+  uint64_t len;
+  uint32_t direction; /* PV_TO_GUEST / PV_FROM_GUEST */
+  uint32_t reserved;
+  uint64_t pre_hpa[PV_SMALL_PAGES];
+} pv_small_op;
+typedef struct pv_small_result {
+  pv_op_result op;
+  uint64_t page_hpa[PV_SMALL_PAGES];
+  uint32_t page_status[PV_SMALL_PAGES];
+  uint64_t seq; /* written last (after a system-scope fence) */
+} pv_small_result;
+int pv_copy_small(uint8_t* image, uint64_t image_bytes, const pv_small_op* op /* host */, uint8_t* buf,
+                  uint64_t buf_bytes, pv_small_result* out, uint8_t* dirty, uint64_t seq, void* stream);
+
+/* Host-mapped pinned memory (cudaHostAllocMapped | Portable): the device
+ * reads and writes it through the same pointer (UVA). */
+void* pv_host_alloc(uint64_t bytes);
+void pv_host_free(void* p);
+
 /* ---- trap shim on the device -----------------------
  * The default hypervisor shim of the hybrid resolver (backend.py:117-128,
  * 288-296; resolve_hybrid_with_fixup, memvirt.py:685-696) for a planned copy

@@ -71,6 +71,7 @@ EXPORTS = (
     "pv_result_decode", "pv_timing", "pv_timing_ms", "pv_copy_shim_scratch_bytes", "pv_copy_shim",
     "pv_map_scratch_bytes", "pv_map_plan", "pv_map_commit",
     "pv_frame_pack", "pv_frame_identify", "pv_frame_assemble_scratch_bytes", "pv_frame_assemble",
+    "pv_walk_one", "pv_copy_small", "pv_host_alloc", "pv_host_free",
 )
 
 _u64 = ctypes.c_uint64
@@ -109,7 +110,35 @@ _SIGNATURES = {
     "pv_stream_sync": (ctypes.c_int, [_p]),
     "pv_timing": (ctypes.c_int, [ctypes.c_int]),
     "pv_timing_ms": (ctypes.c_double, [ctypes.c_char_p, _p]),
+    "pv_walk_one": (ctypes.c_int, [_p, _u64, _p, _u64, _u32, _p, _u64, _p]),
+    "pv_copy_small": (ctypes.c_int, [_p, _u64, _p, _p, _u64, _p, _p, _u64, _p]),
+    "pv_host_alloc": (_p, [_u64]),
+    "pv_host_free": (None, [_p]),
 }
+
+SMALL_PAGES = 64  # pv.h PV_SMALL_PAGES
+
+
+class PvSpace(ctypes.Structure):
+    _fields_ = [("s1_base", _u64), ("s1_root_pfn", _u64), ("s2_root_pfn", _u64), ("mode", _u64)]
+
+
+class PvOpResult(ctypes.Structure):
+    _fields_ = [("copied", _u64), ("value", _u64), ("aux", _u64), ("status", _u32), ("fail_page", _u32)]
+
+
+class PvOneResult(ctypes.Structure):
+    _fields_ = [("value", _u64), ("aux", _u64), ("status", _u64), ("seq", _u64)]
+
+
+class PvSmallOp(ctypes.Structure):
+    _fields_ = [("space", PvSpace), ("gva", _u64), ("len", _u64), ("direction", _u32), ("reserved", _u32),
+                ("pre_hpa", _u64 * SMALL_PAGES)]
+
+
+class PvSmallResult(ctypes.Structure):
+    _fields_ = [("op", PvOpResult), ("page_hpa", _u64 * SMALL_PAGES), ("page_status", _u32 * SMALL_PAGES),
+                ("seq", _u64)]
 
 _lock = threading.Lock()
 _lib = None

@@ -20,6 +20,10 @@ cudaError_t launch_copy_plan(const uint8_t*, uint64_t, const pv_space*, const pv
                              uint64_t, uint64_t*, uint32_t*, uint64_t*, uint64_t*, cudaStream_t);
 cudaError_t launch_copy_stamp(const uint64_t*, uint64_t, uint64_t, const uint64_t*, const uint64_t*, uint64_t*,
                               uint64_t, uint32_t, uint32_t*, cudaStream_t);
+cudaError_t launch_walk_one(const uint8_t*, uint64_t, const pv_space&, uint64_t, uint32_t, pv_one_result*, uint64_t,
+                            cudaStream_t);
+cudaError_t launch_copy_small(uint8_t*, uint64_t, const pv_small_op&, uint8_t*, uint64_t, pv_small_result*, uint8_t*,
+                              uint32_t, uint64_t, cudaStream_t);
 cudaError_t launch_copy_exec(uint8_t*, uint64_t, const pv_op*, uint64_t, const uint64_t*, uint64_t, uint32_t,
                              const uint64_t*, const uint32_t*, const uint64_t*, const uint64_t*, uint8_t*,
                              uint64_t, pv_op_result*, uint8_t*, const uint32_t*, cudaStream_t);
@@ -375,6 +379,34 @@ int pv_map_commit(uint8_t* image, uint64_t image_bytes, uint64_t base, uint64_t 
   return rc(launch_map_commit(image, image_bytes, base, root_pfn, vas, n, need, frames, n_frames, frame_off, hot,
                               data_first ? 1u : 0u, targets, target_add, leaf_flags, out_data, dirty,
                               (cudaStream_t)stream));
+}
+
+int pv_walk_one(const uint8_t* image, uint64_t image_bytes, const pv_space* space, uint64_t va, uint32_t flags,
+                pv_one_result* out, uint64_t seq, void* stream) {
+  if (!image || !space || !out || image_bytes % kPageSize) return PV_EINVAL;
+  if (flags & ~(uint32_t)PV_OUT_PFN) return PV_EINVAL;
+  return rc(launch_walk_one(image, image_bytes, *space, va, flags, out, seq, (cudaStream_t)stream));
+}
+
+int pv_copy_small(uint8_t* image, uint64_t image_bytes, const pv_small_op* op, uint8_t* buf, uint64_t buf_bytes,
+                  pv_small_result* out, uint8_t* dirty, uint64_t seq, void* stream) {
+  if (!image || !op || !out || image_bytes % kPageSize) return PV_EINVAL;
+  if (op->direction != PV_TO_GUEST && op->direction != PV_FROM_GUEST) return PV_EINVAL;
+  const uint64_t n = page_span(op->gva, op->len);
+  if (n > PV_SMALL_PAGES) return PV_EINVAL;
+  if (n != 0 && !buf) return PV_EINVAL;
+  return rc(launch_copy_small(image, image_bytes, *op, buf, buf_bytes, out, dirty, (uint32_t)n, seq,
+                              (cudaStream_t)stream));
+}
+
+void* pv_host_alloc(uint64_t bytes) {
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, bytes, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) return nullptr;
+  return p;
+}
+
+void pv_host_free(void* p) {
+  if (p) cudaFreeHost(p);
 }
 
 uint64_t pv_copy_ordered_scratch_bytes(uint64_t n_pages, uint64_t image_bytes) {

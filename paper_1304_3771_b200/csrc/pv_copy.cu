@@ -425,6 +425,107 @@ exec_bulk_kernel(uint8_t* __restrict__ image, uint64_t image_bytes, const pv_op*
   if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// ---- per-call path: one op per launch, request in the parameters -----------
+
+__global__ void walk_one_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, pv_space sp, uint64_t va,
+                                uint32_t flags, pv_one_result* out, uint64_t seq) {
+  uint64_t value = 0, aux = 0;
+  const uint32_t st = translate_global(image, image_bytes, sp, va, &value, &aux);
+  if (st == PV_ST_OK && !(flags & PV_OUT_PFN)) value = (value << kPageShift) | (va & kPageMask);
+  out->value = value;
+  out->aux = aux;
+  out->status = st;
+  __threadfence_system();
+  *reinterpret_cast<volatile uint64_t*>(&out->seq) = seq;
+}
+
+constexpr int kSmallTpb = 256;
+static_assert(PV_SMALL_PAGES <= kSmallTpb, "one plan thread per page");
+
+// One CTA: thread k translates page k (or takes the caller's FIFO hit), the
+// op's first failing page is a shared atomicMin, then warp w copies pages
+// w, w + 8, ... below it (memvirt.py:615-627 prefix semantics).
+__global__ void __launch_bounds__(kSmallTpb)
+copy_small_kernel(uint8_t* __restrict__ image, uint64_t image_bytes, pv_small_op op, uint8_t* __restrict__ buf,
+                  uint64_t buf_bytes, pv_small_result* out, uint8_t* __restrict__ dirty, uint32_t n_pages,
+                  uint64_t seq) {
+  __shared__ uint64_t s_hpa[PV_SMALL_PAGES];
+  __shared__ uint32_t s_bad;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_bad = n_pages;
+  __syncthreads();
+  uint64_t value = 0, aux = 0;
+  uint32_t st = PV_ST_OK;
+  if (tid < n_pages) {
+    const uint64_t cur = op_page_va(op.gva, tid);
+    const uint64_t done = cur - op.gva;
+    const uint64_t chunk = min(op.len - done, kPageSize - (cur & kPageMask));
+    const uint64_t hit = op.pre_hpa[tid];
+    if (hit != 0) {
+      value = hit - 1;  // the caller's translation (a FIFO hit): the byte hpa
+    } else {
+      st = translate_global(image, image_bytes, op.space, cur, &value, &aux);
+      if (st == PV_ST_OK) value = (value << kPageShift) | (cur & kPageMask);
+    }
+    if (st == PV_ST_OK && (value + chunk > image_bytes || value + chunk < value))
+      st = PV_ST_DATA_OOR;  // memvirt.py:156-158
+    s_hpa[tid] = value;
+    out->page_hpa[tid] = value;
+    out->page_status[tid] = st;
+    if (st != PV_ST_OK) atomicMin(&s_bad, tid);
+  }
+  __syncthreads();
+  const uint32_t bad = s_bad;
+  if (tid == bad) {
+    pv_op_result r;
+    r.copied = op_page_va(op.gva, tid) - op.gva;
+    r.value = value;
+    r.aux = aux;
+    r.status = st;
+    r.fail_page = tid;
+    out->op = r;
+  } else if (tid == 0 && bad == n_pages) {
+    pv_op_result r;
+    r.copied = op.len;
+    r.value = r.aux = 0;
+    r.status = PV_ST_OK;
+    r.fail_page = 0;
+    out->op = r;
+  }
+  const uint64_t pol = policy_evict_first();
+  for (uint32_t k = warp; k < bad; k += kSmallTpb / 32) {
+    const uint64_t cur = op_page_va(op.gva, k);
+    const uint64_t done = cur - op.gva;
+    const uint32_t chunk = buf_clamp(done, (uint32_t)min(op.len - done, kPageSize - (cur & kPageMask)), buf_bytes);
+    const uint64_t hpa = s_hpa[k];
+    uint8_t* bp = buf + done;
+    if (op.direction == PV_TO_GUEST) {
+      warp_copy(image + hpa, bp, chunk, lane, pol);
+      if (dirty != nullptr && lane == 0) dirty[hpa >> kPageShift] = 1;
+    } else {
+      warp_copy(bp, image + hpa, chunk, lane, pol);
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence_system();
+    *reinterpret_cast<volatile uint64_t*>(&out->seq) = seq;
+  }
+}
+
+cudaError_t launch_walk_one(const uint8_t* image, uint64_t image_bytes, const pv_space& sp, uint64_t va,
+                            uint32_t flags, pv_one_result* out, uint64_t seq, cudaStream_t stream) {
+  walk_one_kernel<<<1, 1, 0, stream>>>(image, image_bytes, sp, va, flags, out, seq);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_copy_small(uint8_t* image, uint64_t image_bytes, const pv_small_op& op, uint8_t* buf,
+                              uint64_t buf_bytes, pv_small_result* out, uint8_t* dirty, uint32_t n_pages,
+                              uint64_t seq, cudaStream_t stream) {
+  copy_small_kernel<<<1, kSmallTpb, 0, stream>>>(image, image_bytes, op, buf, buf_bytes, out, dirty, n_pages, seq);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_copy_plan(const uint8_t* image, uint64_t image_bytes, const pv_space* spaces, const pv_op* ops,
                              uint64_t n_ops, const uint64_t* page_off, uint64_t n_pages, uint64_t* page_hpa,
                              uint32_t* page_status, uint64_t* page_aux, uint64_t* op_first_bad, cudaStream_t stream) {

@@ -14,10 +14,10 @@
 // FIRST; the consumer lets each byte take the value of the first arrival that
 // covers it (a per-block coverage map skips bytes a later writer already
 // set), which is exactly the state the in-order copies leave.  Chunks that
-// later writers overwrite completely never move: both warps first walk the
-// page's descriptors last-first until the chunks seen cover the whole page
-// (live_chunks, metadata only), and only those chunks are streamed; a fully
-// covered page is not even read.  The page is written back once.  The
+// later writers overwrite completely never move: both warps walk the page's
+// descriptors last-first and only the chunks that still reach an uncovered
+// byte are streamed (NeedIter, metadata only); the page is never read --
+// bytes no chunk covers are merged from the image at write-back, once.  The
 // pipeline is warp-private: no CTA-wide barriers on the per-chunk path.
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_run_length_encode.cuh>
@@ -229,14 +229,102 @@ __device__ __forceinline__ uint32_t apply_chunk_rev(PageSmem& W, uint32_t lane, 
   }
   return made_full;
 }
+// The chunks of one page that can still change it, last-first.  Walking the
+// page's chunk descriptors from the LAST one (program order) backwards, a
+// chunk matters only if it covers a byte no later chunk covers; every other
+// chunk is overwritten entirely and its payload never has to move.  Coverage
+// depends on (offset, len) only -- the metadata -- so the producer and the
+// consumer warp of a page slot each run this iterator and see the same
+// sequence without talking (their ring accounting, G / vhead, stays in
+// step).  Lane l tracks bytes [128 l, 128 l + 128) of the page (c[4]);
+// fullreg (warp-uniform) has bit l set once lane l's bytes are all covered,
+// which lets a window of 32 candidates be filtered in one step (a chunk whose
+// 128-byte regions are all covered is dead) before the exact per-chunk test.
+// Pages the batch covers completely stop after a few dozen chunks; pages it
+// never covers (e.g. an arena's first byte) still scan every descriptor but
+// move only the few chunks that reach their uncovered bytes.
+struct NeedIter {
+  const ChunkDesc* rd;  // candidate k (0 = last chunk in program order) at rd - k
+  uint32_t n, k0;       // candidates, current window start
+  uint32_t cand;        // window lanes not yet rejected (warp-uniform)
+  uint32_t meta_l;      // this lane's window candidate
+  uint64_t src_l;
+  uint32_t c[4];        // this lane's 128 coverage bits
+  uint32_t fullreg;     // bit l: lane l's bytes are all covered (warp-uniform)
+};
+
+__device__ __forceinline__ void need_window(NeedIter& it, uint32_t lane) {
+  const uint32_t k = it.k0 + lane;
+  bool maybe = false;
+  it.meta_l = 0;
+  it.src_l = 0;
+  if (k < it.n) {
+    const ChunkDesc d = *(it.rd - k);
+    it.meta_l = d.meta;
+    it.src_l = d.src;
+    const uint32_t off = (d.meta >> 4) & 0xFFF, len = d.meta >> 16;
+    if (len != 0) {
+      const uint32_t r0 = off >> 7, r1 = (off + len - 1) >> 7;
+      const uint32_t regions = (r1 == 31 ? 0xFFFFFFFFu : ((2u << r1) - 1u)) & ~((1u << r0) - 1u);
+      maybe = (regions & ~it.fullreg) != 0;
+    }
+  }
+  it.cand = __ballot_sync(0xFFFFFFFFu, maybe);
+}
+
+__device__ __forceinline__ void need_init(NeedIter& it, const ChunkDesc* __restrict__ desc, uint32_t b, uint32_t n,
+                                          uint32_t lane) {
+  it.rd = desc + b + n - 1;
+  it.n = n;
+  it.k0 = 0;
+  it.c[0] = it.c[1] = it.c[2] = it.c[3] = 0u;
+  it.fullreg = 0u;
+  need_window(it, lane);
+}
+
+// Next chunk that matters (its meta, and its source for the producer);
+// false when none is left.  Warp-collective.
+__device__ __forceinline__ bool need_next(NeedIter& it, uint32_t lane, uint32_t& meta, uint64_t& src) {
+  const int32_t mine = 128 * (int32_t)lane;
+  while (it.fullreg != 0xFFFFFFFFu) {
+    while (it.cand == 0u) {
+      it.k0 += 32;
+      if (it.k0 >= it.n) return false;
+      need_window(it, lane);
+    }
+    const int j = __ffs(it.cand) - 1;
+    it.cand &= it.cand - 1u;
+    const uint32_t mj = __shfl_sync(0xFFFFFFFFu, it.meta_l, j);
+    const int32_t off = (int32_t)((mj >> 4) & 0xFFF), len = (int32_t)(mj >> 16);
+    const int32_t lo = max(off - mine, 0), hi = min(off + len - mine, 128);
+    uint32_t m[4], fresh = 0u;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const int32_t wl = max(lo - 32 * w, 0), wh = min(hi - 32 * w, 32);
+      m[w] = wl < wh ? ((wh == 32 ? 0xFFFFFFFFu : ((1u << wh) - 1u)) & ~((1u << wl) - 1u)) : 0u;
+      fresh |= m[w] & ~it.c[w];
+    }
+    const uint64_t s = ((uint64_t)__shfl_sync(0xFFFFFFFFu, (uint32_t)(it.src_l >> 32), j) << 32) |
+                       __shfl_sync(0xFFFFFFFFu, (uint32_t)it.src_l, j);
+    if (__any_sync(0xFFFFFFFFu, fresh != 0u)) {
+#pragma unroll
+      for (int w = 0; w < 4; ++w) it.c[w] |= m[w];
+      it.fullreg = __ballot_sync(0xFFFFFFFFu, (it.c[0] & it.c[1] & it.c[2] & it.c[3]) == 0xFFFFFFFFu);
+      meta = mj;
+      src = s;
+      return true;
+    }
+  }
+  return false;
+}
 
 // One page slot per producer/consumer warp pair.  The producer warp walks
-// the page's chunk descriptors and keeps the ring full (TMA bulk copies,
-// completion on full[slot]); the consumer warp stages the destination page,
-// applies chunk after chunk in order and releases each ring slot on
-// empty[slot].  Ring bytes are packed back to back in virtual byte order;
-// before reusing bytes the producer waits for the release of the newest
-// chunk that still occupies them (releases are in order).
+// the page's chunks that matter (NeedIter) and keeps the ring full (TMA
+// bulk copies, completion on full[slot]); the consumer warp applies them in
+// the same order and releases each ring slot on empty[slot].  Ring bytes are
+// packed back to back in virtual byte order; before reusing bytes the
+// producer waits for the release of the newest chunk that still occupies
+// them (releases are in order).
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
@@ -244,25 +332,15 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 __device__ __forceinline__ void produce(PageSmem& P, const ChunkDesc* __restrict__ desc, uint32_t b, uint32_t n,
                                         uint32_t lane, uint64_t pol, uint32_t& G, uint32_t& vhead, uint32_t& hptr,
                                         int64_t& released) {
-  // chunks go into the ring last-first (k-th issued = chunk n-1-k of the page)
-  const ChunkDesc* rdesc = desc + b + n - 1;
-  ChunkDesc cur{0, 0, 0}, nxt{0, 0, 0};
-  if (lane < n) cur = *(rdesc - lane);
-  if (32 + lane < n) nxt = *(rdesc - (32 + lane));
-  uint32_t cb = 0;
-  for (uint32_t k = 0; k < n; ++k, ++G) {
-    if (k == cb + 32) {
-      cur = nxt;
-      cb += 32;
-      nxt = cb + 32 + lane < n ? *(rdesc - (cb + 32 + lane)) : ChunkDesc{0, 0, 0};
-    }
-    const uint32_t meta = __shfl_sync(0xFFFFFFFFu, cur.meta, k - cb);
-    const uint64_t src = ((uint64_t)__shfl_sync(0xFFFFFFFFu, (uint32_t)(cur.src >> 32), k - cb) << 32) |
-                         __shfl_sync(0xFFFFFFFFu, (uint32_t)cur.src, k - cb);
+  NeedIter it;
+  need_init(it, desc, b, n, lane);
+  uint32_t meta;
+  uint64_t src;
+  while (need_next(it, lane, meta, src)) {
     const uint32_t span = (((meta & 15) + (meta >> 16) + 15) >> 4) << 4;
     const uint32_t ve = vhead + span;
     // chunk G reuses slot G % kK (last held by chunk G - kK) and the ring
-    // bytes of every chunk whose virtual start is below ve - kRB
+    // bytes of every chunk whose virtual start is below ve - kWin
     if (G >= (uint32_t)kK && hptr < G - kK + 1) hptr = G - kK + 1;
     while (hptr < G && (int32_t)(P.vstart[hptr % kK] - (ve - kWin)) < 0) ++hptr;
     int64_t r = (int64_t)hptr - 1;
@@ -282,41 +360,8 @@ __device__ __forceinline__ void produce(PageSmem& P, const ChunkDesc* __restrict
       if (first < span) bulk_g2s(P.ring, src + first, span - first, &P.full[slot], pol);
     }
     vhead = ve;
+    ++G;
   }
-}
-
-// How many of a page's chunks (counted from the LAST one, program order) can
-// still change its bytes: walking the chunk descriptors last-first, the
-// chunks before the one that completes the page's coverage are overwritten
-// entirely by later writers, so neither their payload nor their turn in the
-// ring is needed.  Coverage only depends on (offset, len) -- the metadata --
-// so both warps of a page slot compute the same count without talking.
-// Lane l tracks bytes [128 l, 128 l + 128) of the page in four words.
-// *full: the live chunks cover every byte (the page need not be read first).
-__device__ __forceinline__ uint32_t live_chunks(const ChunkDesc* __restrict__ desc, uint32_t b, uint32_t n,
-                                                uint32_t lane, bool* full) {
-  uint32_t c[4] = {0u, 0u, 0u, 0u};
-  const int32_t mine = 128 * (int32_t)lane;
-  for (uint32_t k0 = 0; k0 < n; k0 += 32) {
-    const uint32_t meta = k0 + lane < n ? desc[b + n - 1 - (k0 + lane)].meta : 0u;
-    const uint32_t m = n - k0 < 32 ? n - k0 : 32;
-    for (uint32_t j = 0; j < m; ++j) {
-      const uint32_t mj = __shfl_sync(0xFFFFFFFFu, meta, (int)j);
-      const int32_t off = (int32_t)((mj >> 4) & 0xFFF), len = (int32_t)(mj >> 16);
-      const int32_t lo = max(off - mine, 0), hi = min(off + len - mine, 128);
-#pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        const int32_t wl = max(lo - 32 * w, 0), wh = min(hi - 32 * w, 32);
-        if (wl < wh) c[w] |= (wh == 32 ? 0xFFFFFFFFu : ((1u << wh) - 1u)) & ~((1u << wl) - 1u);
-      }
-      if (__all_sync(0xFFFFFFFFu, (c[0] & c[1] & c[2] & c[3]) == 0xFFFFFFFFu)) {
-        *full = true;
-        return k0 + j + 1;
-      }
-    }
-  }
-  *full = false;
-  return n;
 }
 
 __global__ void __launch_bounds__(kApPages * 64)
@@ -344,52 +389,59 @@ ordered_apply_kernel(uint8_t* __restrict__ image, const ChunkDesc* __restrict__ 
   for (uint32_t s = blockIdx.x * kApPages + pslot; s < n_segs; s += gridDim.x * kApPages) {
     const uint32_t key = seg_key[s];
     if (key == dead_key) continue;
-    const uint32_t b = seg_start[s], n_all = seg_len[s];
-    // only the last n chunks can change the page (live_chunks); both roles
-    // agree on n, so the ring accounting (G, vhead) stays in step
-    bool covered;
-    const uint32_t n = live_chunks(desc, b, n_all, lane, &covered);
+    const uint32_t b = seg_start[s], n = seg_len[s];
     if (producer) {
-      produce(P, desc, b + n_all - n, n, lane, pol, G, vhead, hptr, released);
+      produce(P, desc, b, n, lane, pol, G, vhead, hptr, released);
       continue;
     }
-    const uint64_t dst = (uint64_t)key << kPageShift;
-    if (!covered) {  // bytes no chunk writes keep the page's current contents
-#pragma unroll
-      for (int k = 0; k < 8; ++k)
-        reinterpret_cast<uint4*>(P.page)[lane + 32 * k] = reinterpret_cast<const uint4*>(image + dst)[lane + 32 * k];
-    }
+    // The page is assembled in SMEM from the chunks that matter only; bytes
+    // no chunk covers keep the image's contents, merged in at write-back.
     reinterpret_cast<uint4*>(P.cov)[lane] = make_uint4(0, 0, 0, 0);
-    uint32_t open_blocks = kPageSize / 16;  // blocks not yet final (warp-uniform)
     __syncwarp();
-    for (uint32_t k = 0; k < n; ++k, ++G) {
+    NeedIter it;
+    need_init(it, desc, b, n, lane);
+    uint32_t meta_it;
+    uint64_t src_it;
+    while (need_next(it, lane, meta_it, src_it)) {
       const uint32_t slot = G % kK;
       mbar_wait(&P.full[slot], (G / kK) & 1);
       const uint32_t meta = P.meta[slot];
       const uint32_t shift = meta & 15, len = meta >> 16;
-      if (open_blocks != 0 && len != 0) {
-        const int32_t off = (int32_t)((meta >> 4) & 0xFFF);
-        // dest byte 16j + x  <->  ring byte 16j + delta + x
-        const int32_t delta = (int32_t)(vhead % kRB + shift) - off;
-        const int32_t dq = delta >> 4;
-        const uint32_t dr = (uint32_t)delta & 15, sb = (dr & 3) * 8;
-        uint32_t full = 0;
-        switch (dr >> 2) {
-          case 0: full = apply_chunk_rev<0>(P, lane, off, (int32_t)len, dq, sb); break;
-          case 1: full = apply_chunk_rev<1>(P, lane, off, (int32_t)len, dq, sb); break;
-          case 2: full = apply_chunk_rev<2>(P, lane, off, (int32_t)len, dq, sb); break;
-          default: full = apply_chunk_rev<3>(P, lane, off, (int32_t)len, dq, sb); break;
-        }
-        open_blocks -= __reduce_add_sync(0xFFFFFFFFu, full);
+      const int32_t off = (int32_t)((meta >> 4) & 0xFFF);
+      // dest byte 16j + x  <->  ring byte 16j + delta + x
+      const int32_t delta = (int32_t)(vhead % kRB + shift) - off;
+      const int32_t dq = delta >> 4;
+      const uint32_t dr = (uint32_t)delta & 15, sb = (dr & 3) * 8;
+      switch (dr >> 2) {
+        case 0: apply_chunk_rev<0>(P, lane, off, (int32_t)len, dq, sb); break;
+        case 1: apply_chunk_rev<1>(P, lane, off, (int32_t)len, dq, sb); break;
+        case 2: apply_chunk_rev<2>(P, lane, off, (int32_t)len, dq, sb); break;
+        default: apply_chunk_rev<3>(P, lane, off, (int32_t)len, dq, sb); break;
       }
       vhead += ((shift + len + 15) >> 4) << 4;
-      __syncwarp();  // every lane's ring reads and page writes of chunk k are done
+      ++G;
+      __syncwarp();  // every lane's ring reads and page writes of this chunk are done
       if (lane == 0) mbar_arrive(&P.empty[slot]);
     }
     __syncwarp();
+    const uint64_t dst = (uint64_t)key << kPageShift;
+    uint4* out = reinterpret_cast<uint4*>(image + dst);
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
-      reinterpret_cast<uint4*>(image + dst)[lane + 32 * k] = reinterpret_cast<const uint4*>(P.page)[lane + 32 * k];
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t j = lane + 32 * k;
+      const uint32_t c = P.cov[j];
+      if (c == 0u) continue;  // no writer: the image keeps these bytes
+      const uint4 v = reinterpret_cast<const uint4*>(P.page)[j];
+      if (c == 0xFFFFu) {
+        out[j] = v;
+      } else {
+        const uint32_t m0 = nibble_bytes(c & 15), m1 = nibble_bytes((c >> 4) & 15), m2 = nibble_bytes((c >> 8) & 15),
+                       m3 = nibble_bytes(c >> 12);
+        const uint4 old = out[j];
+        out[j] = make_uint4((old.x & ~m0) | (v.x & m0), (old.y & ~m1) | (v.y & m1), (old.z & ~m2) | (v.z & m2),
+                            (old.w & ~m3) | (v.w & m3));
+      }
+    }
     if (dirty != nullptr && lane == 0) dirty[key] = 1;
     __syncwarp();
   }

@@ -123,44 +123,13 @@ def raise_for(status: int, value: int, aux: int, va: int, image_bytes: int, chun
 
 # ---- single-lane fast path ---------------------------------------------------
 
-class _OneLane:
-    """Reusable pinned + device words for batch-of-one translations."""
-
-    def __init__(self):
-        import torch
-
-        self.host = torch.zeros(16, dtype=torch.int64).pin_memory()
-        self.dev = torch.zeros(16, dtype=torch.int64, device="cuda")
-        self.out = torch.zeros(4, dtype=torch.int64).pin_memory()
-
-
-_tls = threading.local()
-
-
 def translate_one(image, space: Space, va: int, *, out_pfn: bool = False) -> tuple[int, int, int]:
-    """One walk/translation on the device: returns (status, value, aux)."""
-    lib = N.lib()
-    dev_img = image.device()
-    one = getattr(_tls, "one", None)
-    if one is None:
-        one = _tls.one = _OneLane()
-    h = one.host.numpy().view(np.uint64)
-    chunk0 = 0
-    h[0:4] = space.words()
-    h[4:8] = [0, 1, chunk0, 0]
-    h[8] = va & U64
-    h[9:12] = 0
-    s = _stream()
-    one.dev.copy_(one.host, non_blocking=True)
-    base = one.dev.data_ptr()
-    flags = (N.OUT_PFN if out_pfn else 0) | (N.HAS_TWO_STAGE if space.mode == N.TWO_STAGE else 0) | \
-        (N.HAS_4L if space.mode == N.ONE_STAGE_4L else 0)
-    N.check(lib.pv_translate(dev_img.data_ptr(), image.nbytes, base, base + 32, 1, 1, base + 64, flags, None,
-                             base + 72, base + 88, base + 80, s.cuda_stream), "pv_translate")
-    one.out.copy_(one.dev[9:13], non_blocking=True)
-    s.synchronize()
-    o = one.out.numpy().view(np.uint64)
-    return int(o[2]) & 0xFFFFFFFF, int(o[0]), int(o[1])
+    """One walk/translation on the device: returns (status, value, aux).
+    One pv_walk_one launch, request by value, result in pinned memory
+    (percall.py)."""
+    from . import percall
+
+    return percall.get().walk(image, space, va, out_pfn)
 
 
 # ---- K1: batched translation -------------------------------------------------

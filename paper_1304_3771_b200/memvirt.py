@@ -33,6 +33,7 @@ import numpy as np
 
 from . import _native as N
 from . import dataplane as dp
+from . import percall
 from .errors import (
     AlreadyMapped,
     OutOfRange,
@@ -994,6 +995,13 @@ def copy_user_buffer(direction: str, gva: Gva, length: int, host_buf, *, transla
         raise ValueError(f"unknown direction {direction!r}")
     if length <= 0:
         return 0
+    if ((gva + length - 1) >> PAGE_SHIFT) - (gva >> PAGE_SHIFT) < percall.SMALL_PAGES:
+        # one op of <= 64 pages (every driver copy of the reference): one
+        # launch through the per-call path
+        copied, err = _copy_small(direction, gva, length, host_buf, translator, host_mem)
+        if err is not None:
+            raise err
+        return copied
     import torch
 
     to_guest = direction == "to_guest"
@@ -1019,6 +1027,167 @@ def copy_user_buffer(direction: str, gva: Gva, length: int, host_buf, *, transla
     if err is not None:
         raise err
     return copied
+
+
+def _fifo_presim(cache: TranslationCache, pages: list[int]) -> list:
+    """Which pages of an op the FIFO cache will answer (their cached hpa
+    page) if the op runs to its end: lookup + insert-on-miss on a copy of the
+    cache (memvirt.py:357-368).  Pages of one op are distinct, so a miss's
+    insert only matters through the evictions it causes."""
+    entries = deque(cache._entries)
+    out = []
+    for p in pages:
+        hit = None
+        for key, val in entries:
+            if key == p:
+                hit = val
+                break
+        out.append(hit)
+        if hit is None:
+            if len(entries) >= cache.capacity:
+                entries.popleft()
+            entries.append((p, None))
+    return out
+
+
+def _fifo_replay(cache: TranslationCache, pages: list[int], res, n_looked: int, bad: int, status: int) -> None:
+    """Advance the real cache exactly as translate() would have over the
+    first ``n_looked`` pages: hits count, misses count and insert the
+    device's translation -- except a failing walk (no insert); a page whose
+    data access was out of range did translate, so it is inserted."""
+    for k in range(n_looked):
+        hit = cache.lookup(pages[k])
+        if hit is None and (k < bad or dp.kind(status) == N.ST_DATA_OOR):
+            cache.insert(pages[k], int(res.page_hpa[k]) >> PAGE_SHIFT)
+
+
+def _copy_small(direction, gva, length, host_buf, translator, host_mem):
+    """copy_user_buffer of an op of at most percall.SMALL_PAGES pages, one
+    pv_copy_small launch per run (the hybrid resolver's shim restarts a run
+    at the trapped page, resolve_hybrid_with_fixup, memvirt.py:685-696).
+    Same outcomes, cache state and counters as the batch path."""
+    pc = percall.get()
+    image = host_mem.backing
+    to_guest = direction == "to_guest"
+    d = N.TO_GUEST if to_guest else N.FROM_GUEST
+    stage = pc.stage
+    if to_guest:
+        data = host_buf[0:length]
+        avail = len(data)
+        if avail:
+            stage[:avail] = np.frombuffer(data, dtype=np.uint8) if not isinstance(data, np.ndarray) else data
+    else:
+        avail = length
+    space = getattr(translator, "device_space", None)
+    if space is None:
+        return _copy_small_foreign(direction, gva, length, host_buf, translator, host_mem, pc, avail)
+    cache = translator.cache if getattr(translator, "use_cache", False) else None
+    retry = getattr(translator, "_on_trap", None)
+    count = getattr(translator, "_count", None)
+    done = 0
+    shimmed = False
+    while True:
+        cur0 = gva + done
+        rest = length - done
+        n = ((cur0 + rest - 1) >> PAGE_SHIFT) - (cur0 >> PAGE_SHIFT) + 1
+        pages = pre = None
+        if cache is not None:
+            pages = [((cur0 >> PAGE_SHIFT) + k) for k in range(n)]
+            hits = _fifo_presim(cache, pages)
+            pre = [None if h is None else (h << PAGE_SHIFT) | (cur0 & PAGE_MASK if k == 0 else 0)
+                   for k, h in enumerate(hits)]
+        res = pc.copy(image, space, cur0, rest, d, done, avail, pre)
+        op = res.op
+        status = int(op.status)
+        bad = n if status == N.ST_OK else int(op.fail_page)
+        if to_guest:
+            percall.write_through(image, res, cur0, rest, bad, stage, done, avail)
+        if cache is not None:
+            _fifo_replay(cache, pages, res, n if status == N.ST_OK else bad + 1, bad, status)
+        if status == N.ST_OK:
+            if count is not None:
+                count(n)
+            copied = length
+            break
+        copied = done + int(op.copied)
+        k = dp.kind(status)
+        cur = gva + copied
+        if k in (N.ST_TRAP, N.ST_TRAP2) and retry is not None:
+            if shimmed and bad == 0:
+                if count is not None:
+                    count(1)
+                _finish_from_guest(to_guest, host_buf, stage, copied)
+                return copied, TrapFixupFailed(f"still trapping at {cur:#010x} after shim fixup")
+            if count is not None:
+                count(bad)
+            trap = TrapExit(cur if k == N.ST_TRAP else int(op.aux), status & 0xF, int(op.value),
+                            (status >> 16) & 0x1FF)
+            err = retry(trap)
+            if err is not None:
+                if count is not None:
+                    count(1)
+                if isinstance(err, PageFault):
+                    err.bytes_copied = copied
+                _finish_from_guest(to_guest, host_buf, stage, copied)
+                return copied, err
+            done = copied
+            shimmed = True
+            continue
+        if count is not None:
+            count(bad + 1)
+        chunk = min(length - copied, PAGE_SIZE - (cur & PAGE_MASK))
+        _finish_from_guest(to_guest, host_buf, stage, copied)
+        try:
+            dp.raise_for(status, int(op.value), int(op.aux), cur, image.nbytes, chunk=chunk, bytes_copied=copied)
+        except Exception as exc:  # noqa: BLE001
+            return copied, exc
+        return copied, None
+    _finish_from_guest(to_guest, host_buf, stage, copied)
+    return copied, None
+
+
+def _finish_from_guest(to_guest, host_buf, stage, copied):
+    if not to_guest and copied:
+        host_buf[0:copied] = stage[:copied].tobytes()
+
+
+def _copy_small_foreign(direction, gva, length, host_buf, translator, host_mem, pc, avail):
+    """Small copy through a duck-typed translator: its translate() runs per
+    page on the host (it is the caller's object), stopping at the first
+    exception; the bytes of the pages before it move in one launch."""
+    image = host_mem.backing
+    to_guest = direction == "to_guest"
+    pre = []
+    err = None
+    copied = 0
+    while copied < length:
+        cur = gva + copied
+        chunk = min(length - copied, PAGE_SIZE - (cur & PAGE_MASK))
+        try:
+            hpa = translator.translate(Gva(cur))
+        except PageFault as fault:
+            fault.bytes_copied = copied
+            err = fault
+            break
+        except Exception as exc:  # noqa: BLE001
+            err = exc
+            break
+        n = max(0, min(chunk, avail - copied)) if to_guest else chunk
+        if hpa < 0 or hpa + n > host_mem.size_bytes:
+            err = OutOfRange(f"access [{hpa:#x}, +{n}) beyond {host_mem.size_bytes:#x}")
+            break
+        pre.append(host_mem.base + hpa)
+        copied += chunk
+    if pre:
+        span = copied  # bytes of the pages that translated
+        space = dp.Space(0, 0, 0, N.ONE_STAGE)
+        res = pc.copy(image, space, gva, span, N.TO_GUEST if to_guest else N.FROM_GUEST, 0, avail, pre)
+        if int(res.op.status) != N.ST_OK:
+            raise RuntimeError(f"pv_copy_small failed on pre-translated pages: status {int(res.op.status):#x}")
+        if to_guest:
+            percall.write_through(image, res, gva, span, len(pre), pc.stage, 0, avail)
+    _finish_from_guest(to_guest, host_buf, pc.stage, copied)
+    return copied, err
 
 
 def _copy_device(direction, gva, length, buf, translator, host_mem, space, first_shimmed=False, buf_bytes=None):
