@@ -52,6 +52,8 @@ def parse():
                     "timing (point-to-point over NCCL = NVLink peer copies) and report its time (default at N > 1)")
     ap.add_argument("--no-gather", action="store_true", help="skip the result return to rank 0 at N > 1")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true", help="skip the full-size parity check against the oracle "
+                    "after the timed steps")
     ap.add_argument("--no-graph", action="store_true", help="launch the C5 step phases eagerly instead of "
                     "replaying CUDA graphs of them")
     ap.add_argument("--cpu-sample-vas", type=int, default=16 << 20)
@@ -213,6 +215,7 @@ class Workload:
         self.image.device()  # allocate + push tables
         self.vas = torch.from_numpy(np.concatenate(vas_parts).view(np.int32)).to("cuda")
         self.tplan = dp.TranslatePlan(t_spaces, bounds)
+        self.t_spaces, self.t_bounds, self.c_spaces = t_spaces, bounds, c_spaces
         n = self.n_vas
         self.out = (torch.empty(n, dtype=torch.int64, device="cuda"), torch.empty(n, dtype=torch.int32, device="cuda"),
                     torch.zeros(n, dtype=torch.int64, device="cuda"))
@@ -358,6 +361,9 @@ def run_ours(args, rank, world, local):
 
     total_ms, tr_ms, copy_ms, exec_ms, plan_ms = shard.max_over_ranks(
         [total_ms, tr_ms, copy_ms, exec_ms, plan_ms], world, device="cuda")
+    parity = None
+    if not args.no_parity:
+        parity = verify_parity(wl, cpu_threads())
     want_gather = (args.gather or (world > 1 and _pg())) and not args.no_gather
     gather = gather_results(wl, rank, world) if (want_gather and wl.name == "c5") else None
     K = args.steps
@@ -409,6 +415,7 @@ def run_ours(args, rank, world, local):
                           "gather_sol": walker_sol(wl.n_vas * K / (tr_ms / 1e3)),
                           "ncu": load_json_profile("walker_ncu.json")},
         "faulting_lanes": n_faults,
+        "parity": parity,
         "gather_to_rank0": gather,
         "gpu_launches": (4 + (1 if wl.n_vas >= 8 * 296 * 2048 else 0) + 1
                          + (2 if wl.cplan.shims is not None else 0)) * K,
@@ -425,6 +432,77 @@ def run_ours(args, rank, world, local):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(wl, args)
     return line
+
+
+def verify_parity(wl, threads: int, n_ops: int = 64) -> dict:
+    """Full-size parity of the timed configuration (after the timed steps),
+    against the C oracle (oracle/pvoracle.c -- test infrastructure, used here
+    only as the checker):
+
+    * every lane of the translate batch (value + status) equals
+      ``O.translate`` of the same VA over the same tables;
+    * ``n_ops`` copy ops spread over the batch: the destination bytes in HBM,
+      at the pages the ORACLE translates the op's VAs to, equal the op's
+      source bytes (copy_user_buffer semantics, memvirt.py:604-628).
+
+    The oracle walks a host copy of the device image: the whole image when it
+    is small, else the host-private region (every node of the C5 shadow and
+    hybrid tables lives there; data pages are never read by a walk)."""
+    import torch
+
+    from oracle import oracle as O
+    from paper_1304_3771_b200 import _native as N
+    from paper_1304_3771_b200 import image as I
+
+    t0 = time.perf_counter()
+    img = wl.image
+    dev = img.device()
+    torch.cuda.synchronize()
+    span = img.nbytes if img.nbytes <= (4 << 30) else wl.cfg.host_private
+    if span < img.nbytes and any(sp.mode != N.ONE_STAGE for sp in wl.t_spaces + wl.c_spaces):
+        raise RuntimeError("private-region parity needs one-stage (shadow / hybrid) spaces")
+    ref = I._zeroed_host(img.nbytes)
+    step = 256 << 20
+    for a in range(0, span, step):
+        ref[a:min(a + step, span)] = dev[a:min(a + step, span)].cpu().numpy()
+    value = wl.out[0].cpu().numpy().view(np.uint64)
+    status = wl.out[1].cpu().numpy().view(np.uint32)
+    vas = wl.vas.cpu().numpy().view(np.uint32)
+    lane_bad = 0
+    for begin, end, si in wl.t_bounds:
+        sp = wl.t_spaces[si]
+        v, st, _ = O.translate(ref, O.space(sp.s1_base, sp.s1_root_pfn, sp.s2_root_pfn, sp.mode),
+                               vas[begin:end].astype(np.uint64), threads=threads)
+        lane_bad += int(((v != value[begin:end]) | (st != status[begin:end])).sum())
+    t_lanes = time.perf_counter() - t0
+    # copy ops: evenly spaced sample
+    ops = wl.cplan.host_ops
+    pick = np.unique(np.linspace(0, len(ops) - 1, min(n_ops, len(ops))).astype(np.int64))
+    lib = N.lib()
+    s = torch.cuda.current_stream().cuda_stream
+    byte_bad, bytes_checked = 0, 0
+    for i in pick.tolist():
+        gva, ln, off, si = (int(x) for x in ops[i])
+        sp = wl.c_spaces[si]
+        n_pg = ((gva + ln - 1) >> 12) - (gva >> 12) + 1
+        page_vas = ((gva >> 12) + np.arange(n_pg, dtype=np.uint64)) << np.uint64(12)
+        v, st, _ = O.translate(ref, O.space(sp.s1_base, sp.s1_root_pfn, sp.s2_root_pfn, sp.mode), page_vas,
+                               want_pfn=True, threads=threads)
+        if (st != 0).any():
+            byte_bad += ln
+            continue
+        pfns = torch.from_numpy(v.astype(np.int64)).cuda()
+        got = torch.empty(n_pg * 4096, dtype=torch.uint8, device="cuda")
+        N.check(lib.pv_gather_pages(dev.data_ptr(), img.nbytes, pfns.data_ptr(), n_pg, got.data_ptr(), s),
+                "pv_gather_pages")
+        head = gva & 0xFFF
+        byte_bad += int((got[head:head + ln] != wl.src[off:off + ln]).sum().item())
+        bytes_checked += ln
+    return {"lanes": int(len(vas)), "lane_mismatches": lane_bad, "ops_checked": int(len(pick)),
+            "bytes_checked": bytes_checked, "byte_mismatches": byte_bad,
+            "oracle": "oracle/pvoracle.c (O.translate over a host copy of the image, %d threads)" % threads,
+            "seconds": round(time.perf_counter() - t0, 2), "lanes_seconds": round(t_lanes, 2),
+            "ok": lane_bad == 0 and byte_bad == 0}
 
 
 def gather_results(wl, rank, world):
@@ -615,10 +693,22 @@ def run_c2(args, rank, world, local):
     K = args.steps
     payload = int(W.c2_trace(args.c2_ops)[2].sum())
     peak, peak_kind = peaks()
-    # algorithmic HBM bytes of one apply launch: every payload byte read once,
-    # every destination page read (staged) and written back once
-    dst_pages = int(torch.unique(plan.page_hpa >> 12).numel())
-    alg_bytes = int(lens.sum()) + 2 * 4096 * dst_pages
+    # algorithmic HBM bytes of one apply launch: only the bytes that survive
+    # last-writer-wins have to move -- each distinct destination byte is read
+    # once from its last writer's payload and written once.  (Per process the
+    # ops' byte ranges are merged; processes write disjoint arenas.)
+    surviving = 0
+    for p in np.unique(procs).tolist():
+        sel = procs == p
+        a = np.sort(gvas[sel])
+        order = np.argsort(gvas[sel], kind="stable")
+        e = (gvas[sel] + lens[sel])[order]
+        run_end = np.maximum.accumulate(e)
+        starts = np.concatenate([[True], a[1:] > run_end[:-1]])
+        idx = np.flatnonzero(starts)
+        ends = np.concatenate([run_end[idx[1:] - 1], [run_end[-1]]])
+        surviving += int((ends - a[idx]).sum())
+    alg_bytes = 2 * surviving
     per_launch_ms = kern_ms / max(int(n_apply.value), 1)
     ach = alg_bytes / (per_launch_ms / 1e3) / 1e9
     return {
@@ -634,9 +724,12 @@ def run_c2(args, rank, world, local):
         "ordered_apply_ms_per_step": apply_ms / K,
         "roofline": {"bound": "hbm", "kernel": "ordered_apply_kernel", "achieved": ach, "peak": peak,
                      "unit": "GB/s", "frac": ach / peak, "peak_source": peak_kind,
-                     "traffic": traffic_for(load_traffic("c2"), "ordered_apply", alg_bytes), "launch_ms": per_launch_ms, "alg_bytes_per_launch": alg_bytes,
-                     "note": "payload bytes read once + each destination page staged and written back once, "
-                             "over the apply kernel's event-timed launch duration (pv_timing)"},
+                     "traffic": traffic_for(load_traffic("c2"), "ordered_apply", alg_bytes), "launch_ms": per_launch_ms,
+                     "alg_bytes_per_launch": alg_bytes, "payload_bytes_per_step": int(lens.sum()),
+                     "note": "bytes that survive last-writer-wins (each distinct destination byte read once from "
+                             "its last writer and written once) over the apply kernel's event-timed launch "
+                             "duration (pv_timing); the kernel no longer moves overwritten payload, so it is "
+                             "latency-bound (~2k destination pages, a few dependent TMA loads each), not HBM-bound"},
         "launch": launch_mode,
         "gpu_launches": 14 * K, "gpu_launches_note": "per step: frame pack, identify, classify, plan, 6 FIFO-replay "
                                                      "kernels (runs, spec, link, block, verify, apply), stamp, exec "
@@ -927,7 +1020,7 @@ def run_e2e(wl, args, world):
         tdist.barrier()
     torch.cuda.synchronize()
     tr_s = cp_s = 0.0
-    steps = max(1, min(args.steps, 3))
+    steps = max(1, args.steps)
     for _ in range(steps):
         a, b = one_step()
         tr_s += a
@@ -1099,14 +1192,92 @@ def _oracle_inputs(wl):
     return proc_vas, proc_ops
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _pyref_worker(args):
+    """One core of the Python reference (devfsim from baseline/_ref, unmodified):
+    a shadow guest with 16,384 pages mapped in shuffled order (the C1 world,
+    SURVEY.md 8(d)), then the hot loops timed with perf_counter:
+    ProcessTranslator.translate (uncached, memvirt.py:585-601) over random VAs
+    and HardwareHasAccess.copy_to_user (hybrid resolver, backend.py:152-162)
+    of 4 MiB ops at +0x80 (the C5 op shape)."""
+    worker, n_vas, n_ops = args
+    import random as _r
+    import types as _t
+
+    sys.path.insert(0, os.path.join(ROOT, "baseline", "_ref"))
+    from devfsim import backend as rb
+    from devfsim import memvirt as rm
+
+    memv = rm.MemoryVirtualizer(host_bytes=128 << 20)
+    guest = memv.add_guest(0, "shadow", 96 << 20)
+    space = memv.create_process(guest)
+    order = list(range(16384))
+    _r.Random(1304).shuffle(order)
+    for pg in order:
+        memv.map_process_page(space, 0x1000_0000 + pg * 4096)
+    rng = _r.Random(3771 + worker)
+    vas = [0x1000_0000 + rng.randrange(64 << 20) for _ in range(n_vas)]
+    tr = memv.translator(space, use_cache=False)
+    t0 = time.perf_counter()
+    for va in vas:
+        tr.translate(va)
+    t_tr = time.perf_counter() - t0
+    rec = rb.GuestProcessRecord(_t.SimpleNamespace(id=0, mem_mode="shadow"), space, memv)
+    acc = rb.HardwareHasAccess(rec, memv)
+    data = bytes(rng.randrange(256) for _ in range(4096)) * 1024
+    t0 = time.perf_counter()
+    for i in range(n_ops):
+        acc.copy_to_user(0x1000_0000 + (i % 15) * (4 << 20) + 0x80, data)
+    t_cp = time.perf_counter() - t0
+    return n_vas / t_tr, n_ops * len(data) / t_cp / 1e9
+
+
+def python_reference_baseline(cores: int, n_vas: int = 300_000, n_ops: int = 48) -> dict | None:
+    """The reference's own CPU path (pure Python, GIL-bound: one process per
+    core, SURVEY.md 8(d) "CPU reference timing"), timed on this box beside
+    the C port: per-core rates (median over workers) and the K-core
+    aggregate.  None when baseline/_ref is not staged."""
+    if not os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "devfsim")):
+        return None
+    import multiprocessing as mp
+
+    t0 = time.perf_counter()
+    with mp.get_context("spawn").Pool(cores) as pool:
+        rows = pool.map(_pyref_worker, [(w, n_vas, n_ops) for w in range(cores)])
+    tps = [r[0] for r in rows]
+    gbs = [r[1] for r in rows]
+    return {"kind": "reference (devfsim, unmodified pure Python from baseline/_ref)", "cores": cores,
+            "cpu": cpu_model(),
+            "translations_per_s_per_core": statistics.median(tps), "translations_per_s": sum(tps),
+            "copy_gbs_per_core": statistics.median(gbs), "copy_gbs": sum(gbs),
+            "sample": f"per core: C1 shadow world (16,384 shuffled pages), {n_vas} uncached translate() calls + "
+                      f"{n_ops} x 4 MiB HardwareHasAccess.copy_to_user",
+            "wall_s": round(time.perf_counter() - t0, 1)}
+
+
 def cpu_baseline(wl, args):
     threads = cpu_threads()
     proc_vas, proc_ops = _oracle_inputs(wl)
+    # one untimed pass first: the sample's destination pages are faulted in
+    # once (the reference arm's warm-up steps do the same), so both arms time
+    # the same steady state
+    cpu_sample(wl.memv, proc_vas, proc_ops, args.cpu_sample_vas, args.cpu_sample_bytes, threads)
     tps, gbs, sample = cpu_sample(wl.memv, proc_vas, proc_ops, args.cpu_sample_vas, args.cpu_sample_bytes, threads)
     return {"value": tps, "unit": "translations/s", "cores": threads, "kind": "port", "sample": sample,
-            "copy": {"value": gbs, "unit": "GB/s"},
-            "note": "oracle/pvoracle.c (C restatement of memvirt.py walk/copy_user_buffer, OpenMP); the "
-                    "reference itself is pure Python and cannot run on the GPU box"}
+            "cpu": cpu_model(), "copy": {"value": gbs, "unit": "GB/s"},
+            "note": "oracle/pvoracle.c (C restatement of memvirt.py walk/copy_user_buffer, OpenMP, all host "
+                    "threads); the reference's own Python path is timed beside it (python_reference)",
+            "python_reference": python_reference_baseline(threads)}
 
 
 class _HostOnlyWorkload:
@@ -1138,23 +1309,30 @@ def run_reference(args, rank, world):
     wl = _HostOnlyWorkload(args.workload, args.scale)
     threads = cpu_threads()
     proc_vas, proc_ops = _oracle_inputs(wl)
+    # the same bounded sample the repo arm's cpu_baseline times (one step = one sample)
     for _ in range(max(args.warmup, 0)):
-        cpu_sample(wl.memv, proc_vas, proc_ops, args.cpu_sample_vas // 4, args.cpu_sample_bytes // 4, threads)
-    vals, gbs = [], []
+        cpu_sample(wl.memv, proc_vas, proc_ops, args.cpu_sample_vas, args.cpu_sample_bytes, threads)
+    vals, gbs, secs = [], [], []
     for _ in range(args.steps):
-        tps, g, sample = cpu_sample(wl.memv, proc_vas, proc_ops, args.cpu_sample_vas // 4, args.cpu_sample_bytes // 4,
+        t0 = time.perf_counter()
+        tps, g, sample = cpu_sample(wl.memv, proc_vas, proc_ops, args.cpu_sample_vas, args.cpu_sample_bytes,
                                     threads)
+        secs.append(time.perf_counter() - t0)
         vals.append(tps)
         gbs.append(g)
     v = statistics.median(vals)
     return {
         "metric": METRIC, "value": v, "unit": "translations/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
+        "warmup": args.warmup, "ms_per_step": statistics.median(secs) * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u64",
         "data": "synthetic", "impl": "reference",
         "config": config_of(wl, world) if args.workload == "c5" else {"workload": "C1"},
         "copy": {"value": statistics.median(gbs), "unit": "GB/s"},
-        "cpu_baseline": {"value": v, "unit": "translations/s", "cores": threads, "kind": "port",
-                         "sample": sample + " per step"},
+        "cpu_baseline": {"value": v, "unit": "translations/s", "cores": threads, "kind": "port", "cpu": cpu_model(),
+                         "sample": sample + " per step",
+                         "note": "oracle/pvoracle.c: the reference's path restated in C (OpenMP, all host threads), "
+                                 "a stronger baseline than the reference's own Python, which is timed beside it",
+                         "python_reference": python_reference_baseline(threads)},
         "e2e": {"value": v, "unit": "translations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
@@ -1180,10 +1358,13 @@ def main():
         line = runner(args, rank, world, local)
     if rank == 0 and line is not None:
         print(json.dumps(line), flush=True)
+    bad = line is not None and isinstance(line.get("parity"), dict) and not line["parity"].get("ok", True)
     if world > 1 and _pg():
         import torch.distributed as tdist
 
         tdist.destroy_process_group()
+    if bad:
+        sys.exit(f"parity mismatch against the oracle: {line['parity']}")
 
 
 if __name__ == "__main__":
