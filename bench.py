@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true", help="skip the full-size parity check against the oracle "
                     "after the timed steps")
+    ap.add_argument("--serial-step", action="store_true", help="time C5/C1 steps with the walk and the copy "
+                    "phases back to back (default: the walk on a second stream beside plan + exec)")
     ap.add_argument("--no-graph", action="store_true", help="launch the C5 step phases eagerly instead of "
                     "replaying CUDA graphs of them")
     ap.add_argument("--cpu-sample-vas", type=int, default=16 << 20)
@@ -241,33 +243,38 @@ def run_ours(args, rank, world, local):
     plan = wl.cplan
     stream = torch.cuda.current_stream()
     s = stream.cuda_stream
-    owner, _ = dp._owner_map(img)
+    owner = dp._owner_map(img)
     shim_scratch = dp._shim_scratch(img, plan.n_pages) if plan.shims is not None else None
     hint = dp.exec_hint(plan, wl.src.data_ptr())
 
     def phase_translate():
         dp.translate_lanes(img, wl.tplan, wl.vas, out=wl.out)
 
+    def phase_translate_conc():  # the same walk sized to share every SM with the exec (PV_CONCURRENT)
+        dp.translate_lanes(img, wl.tplan, wl.vas, out=wl.out, concurrent=True)
+
     def phase_plan():  # fills + plan + trap shim + conflict stamp
         cs = torch.cuda.current_stream().cuda_stream
         plan.first_bad.fill_(-1)
         plan.results.zero_()
         plan.conflict.zero_()
-        N.check(lib.pv_copy_plan(dev.data_ptr(), img.nbytes, plan.spaces.data_ptr(), plan.ops.data_ptr(),
-                                 plan.n_ops, plan.page_off.data_ptr(), plan.n_pages, N.TO_GUEST,
-                                 plan.page_hpa.data_ptr(), plan.page_status.data_ptr(), plan.page_aux.data_ptr(),
-                                 plan.first_bad.data_ptr(), None, 0, None, cs), "plan")
+        # a captured step keeps this epoch: its stamps (epoch, chunk) and table-node marks repeat
+        # identically, never a conflict
+        epoch = owner.next_epoch()
+        N.check(lib.pv_copy_plan_nodes(dev.data_ptr(), img.nbytes, plan.spaces.data_ptr(), plan.ops.data_ptr(),
+                                       plan.n_ops, plan.page_off.data_ptr(), plan.n_pages,
+                                       plan.page_hpa.data_ptr(), plan.page_status.data_ptr(),
+                                       plan.page_aux.data_ptr(), plan.first_bad.data_ptr(), owner.nodes.data_ptr(),
+                                       owner.npages, epoch, cs), "plan")
         if plan.shims is not None:  # the hybrid resolver's trap shim (none trap in C5: empty passes)
             N.check(lib.pv_copy_shim(dev.data_ptr(), img.nbytes, plan.spaces.data_ptr(), plan.shims.data_ptr(),
                                      plan.ops.data_ptr(), plan.n_ops, plan.page_off.data_ptr(), plan.n_pages,
                                      plan.page_hpa.data_ptr(), plan.page_status.data_ptr(), plan.first_bad.data_ptr(),
                                      img.dirty_map().data_ptr(), plan.shim_written.data_ptr(), shim_scratch.data_ptr(),
                                      shim_scratch.numel(), cs), "shim")
-        # a captured step keeps this epoch: its stamps (epoch, chunk) repeat identically, never a conflict
-        img._epoch += 1
         N.check(lib.pv_copy_stamp(plan.page_off.data_ptr(), plan.n_ops, plan.n_pages, plan.page_hpa.data_ptr(),
-                                  plan.first_bad.data_ptr(), owner.data_ptr(), img.npages, img._epoch,
-                                  plan.conflict.data_ptr(), cs), "stamp")
+                                  plan.first_bad.data_ptr(), owner.map.data_ptr(), img.npages, epoch,
+                                  plan.conflict.data_ptr(), owner.nodes.data_ptr(), cs), "stamp")
 
     def phase_exec():
         cs = torch.cuda.current_stream().cuda_stream
@@ -299,6 +306,24 @@ def run_ours(args, rank, world, local):
         ev[4].record(stream)
         img.note_device_write()
 
+    side = torch.cuda.Stream()
+
+    def step_overlap(ev):
+        """One step with the walk on a second stream beside plan + exec: the
+        walk is bound by the SM->L2 request port, the exec by HBM bandwidth,
+        and they are independent (different guests' requests; the batch
+        writes no table page -- the stamp pass's table-hazard check)."""
+        ev[0].record(stream)
+        side.wait_event(ev[0])
+        with torch.cuda.stream(side):
+            graphs[3].replay() if graphs else phase_translate_conc()
+            ev[2].record(side)
+        graphs[1].replay() if graphs else phase_plan()
+        graphs[2].replay() if graphs else phase_exec()
+        stream.wait_event(ev[2])
+        ev[1].record(stream)
+        img.note_device_write()
+
     def barrier():
         if world > 1 and tdist.is_initialized():
             tdist.barrier()
@@ -311,8 +336,8 @@ def run_ours(args, rank, world, local):
         # CUDA graphs of the three phases (the kernels and their arguments are identical every step),
         # replayed between the per-phase events: no per-launch host/driver gaps inside a phase
         try:
-            gs = [torch.cuda.CUDAGraph() for _ in range(3)]
-            for g, fn in zip(gs, (phase_translate, phase_plan, phase_exec)):
+            gs = [torch.cuda.CUDAGraph() for _ in range(4)]
+            for g, fn in zip(gs, (phase_translate, phase_plan, phase_exec, phase_translate_conc)):
                 with torch.cuda.graph(g):
                     fn()
             img.note_device_write()
@@ -320,6 +345,7 @@ def run_ours(args, rank, world, local):
             graphs = gs
             for _ in range(2):
                 step([torch.cuda.Event(enable_timing=True) for _ in range(5)])
+                step_overlap([torch.cuda.Event(enable_timing=True) for _ in range(3)])
             torch.cuda.synchronize()
             launch_mode = "cuda_graph"
         except Exception as exc:  # noqa: BLE001 - eager launches are the same kernels
@@ -330,25 +356,38 @@ def run_ours(args, rank, world, local):
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
+    overlap = not args.serial_step
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
-    barrier()
-    torch.cuda.synchronize()
+    ovs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
+    # the timed region: K steps (walk beside plan + exec unless --serial-step)
+    barrier()
+    torch.cuda.synchronize()
     t_start.record(stream)
     for k in range(args.steps):
-        step(evs[k])
+        step_overlap(ovs[k]) if overlap else step(evs[k])
     t_end.record(stream)
     torch.cuda.synchronize()
     barrier()
+    total_ms = t_start.elapsed_time(t_end)
+    if overlap:
+        # per-phase figures (value, rooflines): K more steps with the phases back to back
+        barrier()
+        torch.cuda.synchronize()
+        for k in range(args.steps):
+            step(evs[k])
+        torch.cuda.synchronize()
+        barrier()
     clk = clocks.stop()
     # correctness of the timed configuration: no conflicts, every op complete
     assert int(plan.conflict.item()) == 0, "conflicting destinations in the bench batch"
     res = plan.results.cpu().numpy().view(np.uint64)
     assert (res[:, 3] & 0xFFFFFFFF == 0).all() and (res[:, 0] == plan.host_ops[:, 1]).all()
     n_faults = int((wl.out[1] != 0).sum().item())
-    total_ms = t_start.elapsed_time(t_end)
     tr_ms = sum(e[0].elapsed_time(e[1]) for e in evs)
+    serial_ms = sum(e[0].elapsed_time(e[4]) for e in evs)
+    ov_walk_ms = sum(e[0].elapsed_time(e[2]) for e in ovs) if overlap else None
     plan_ms = sum(e[2].elapsed_time(e[3]) for e in evs)
     exec_ms = sum(e[3].elapsed_time(e[4]) for e in evs)
     copy_ms = sum(e[1].elapsed_time(e[4]) for e in evs)
@@ -359,8 +398,8 @@ def run_ours(args, rank, world, local):
               "exec_ms": {"best": ex_steps[0], "median": statistics.median(ex_steps)}, "rank": rank}
     from paper_1304_3771_b200 import shard
 
-    total_ms, tr_ms, copy_ms, exec_ms, plan_ms = shard.max_over_ranks(
-        [total_ms, tr_ms, copy_ms, exec_ms, plan_ms], world, device="cuda")
+    total_ms, tr_ms, copy_ms, exec_ms, plan_ms, serial_ms = shard.max_over_ranks(
+        [total_ms, tr_ms, copy_ms, exec_ms, plan_ms, serial_ms], world, device="cuda")
     parity = None
     if not args.no_parity:
         parity = verify_parity(wl, cpu_threads())
@@ -379,6 +418,8 @@ def run_ours(args, rank, world, local):
     exec_achieved = 2 * wl.copy_bytes * K / (exec_ms / 1e3) / 1e9
     walk_bytes = 16 * wl.n_vas  # u32 VA in + u64 hpa + u32 status out
     walk_achieved = walk_bytes * K / (tr_ms / 1e3) / 1e9
+    walk_bytes_pte = walk_bytes + 8 * _leaf_ptes(wl)  # + 8 B per distinct leaf PTE
+    walk_achieved_pte = walk_bytes_pte * K / (tr_ms / 1e3) / 1e9
     traffic = load_traffic(args.workload)
     line = {
         "metric": METRIC,
@@ -398,6 +439,15 @@ def run_ours(args, rank, world, local):
                  "ms_per_step": copy_ms / K, "exec_ms_per_step": exec_ms / K,
                  "plan_shim_stamp_ms_per_step": plan_ms / K},
         "translate_ms_per_step": tr_ms / K,
+        "step": {"mode": "overlapped" if overlap else "serial",
+                 "ms": total_ms / K, "serial_ms": serial_ms / K,
+                 "translations_per_s": wl.total_vas * K / (total_ms / 1e3),
+                 "copy_gbs": wl.total_copy_bytes * K / (total_ms / 1e3) / 1e9,
+                 "walk_ms_in_overlap": None if ov_walk_ms is None else ov_walk_ms / K,
+                 "hbm_floor_ms": (2 * wl.copy_bytes + walk_bytes + 8 * _leaf_ptes(wl)) / (peak * 1e6),
+                 "note": "ms_per_step = one step with the walk on a second stream beside plan + exec "
+                         "(PV_CONCURRENT: one walker CTA per SM next to the exec's); value, copy and the "
+                         "rooflines come from K more steps with the phases back to back (serial_ms)"},
         "per_step": spread,
         "roofline": {"bound": "hbm",
                      "kernel": "pv_copy_exec (" + ("exec_bulk_kernel, TMA" if hint else "exec_kernel, LSU") + ")",
@@ -410,8 +460,11 @@ def run_ours(args, rank, world, local):
                           "peak": peak, "unit": "GB/s", "frac": walk_achieved / peak,
                           "traffic": traffic_for(traffic, "translate", walk_bytes),
                           "algorithmic_bytes_per_launch": walk_bytes,
-                          "note": "16 B/translation (u32 VA in, u64 hpa + u32 status out); leaf-PTE gathers "
-                                  "are extra traffic",
+                          "with_leaf_ptes": {"algorithmic_bytes_per_launch": walk_bytes_pte,
+                                             "distinct_leaf_ptes": _leaf_ptes(wl), "achieved": walk_achieved_pte,
+                                             "frac": walk_achieved_pte / peak},
+                          "note": "16 B/translation (u32 VA in, u64 hpa + u32 status out); with_leaf_ptes adds "
+                                  "SURVEY.md 8(d)'s 8 B per distinct leaf PTE touched",
                           "gather_sol": walker_sol(wl.n_vas * K / (tr_ms / 1e3)),
                           "ncu": load_json_profile("walker_ncu.json")},
         "faulting_lanes": n_faults,
@@ -432,6 +485,16 @@ def run_ours(args, rank, world, local):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(wl, args)
     return line
+
+
+def _leaf_ptes(wl) -> int:
+    """Distinct leaf PTEs the walk reads (+ 8 B each): one per
+    distinct (process, page) among the batch's VAs."""
+    n = getattr(wl, "_leaf_ptes", None)
+    if n is None:
+        n = sum(len(np.unique(np.asarray(v) >> 12)) for _, _, v in wl.proc_vas)
+        wl._leaf_ptes = n
+    return n
 
 
 def verify_parity(wl, threads: int, n_ops: int = 64) -> dict:

@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define PV_ABI_VERSION 3
+#define PV_ABI_VERSION 4
 
 /* ---- return codes ------------------------------------------------------ */
 #define PV_SUCCESS 0
@@ -141,6 +141,9 @@ int pv_index_encode(const uint8_t* image, uint64_t image_bytes,
 #define PV_VA32 0x1u    /* vas is uint32_t[] (else uint64_t[])             */
 #define PV_OUT_PFN 0x2u /* value = leaf pfn (walk); else address with the
                            page offset of the va (translate / resolve)     */
+#define PV_CONCURRENT 0x4u /* size the walk for a kernel running beside it:
+                              one CTA per SM (the rest of each SM's
+                              registers and shared memory stay free) */
 #define PV_HAS_4L 0x40000000u        /* some space of the batch is
                            PV_ONE_STAGE_4L (selects the generic kernel)    */
 #define PV_HAS_TWO_STAGE 0x80000000u /* some space of the batch is
@@ -257,7 +260,8 @@ int pv_fifo_replay(const void* vas, uint32_t flags, const uint64_t* lane_idx,
  * all-ones first).  For PV_TO_GUEST it also stamps destination pages in
  * page_owner[] (device, one u64 per image page; NULL disables) with
  * (epoch << 40 | page + 1), one stamp per live chunk, and sets *conflict
- * (device u32) when two chunks of the batch write one hpa page.
+ * (device u32) to PV_CONFLICT_OVERLAP when two chunks of the batch write
+ * one hpa page.
  *
  * pv_copy_exec moves the bytes for every page below its op's first failing
  * page and fills results[] (device, n_ops).  dirty[] (device, one byte per
@@ -284,13 +288,35 @@ int pv_copy_exec(uint8_t* image, uint64_t image_bytes, const pv_op* ops,
                  pv_op_result* results, uint8_t* dirty,
                  const uint32_t* abort_flag, void* stream);
 
+/* pv_copy_plan (without the stamp) that also marks, in node_map[] (device,
+ * one u32 per image page, node_pages >= image_bytes / 4096 entries), every
+ * page-table node page any page's walk reads with `epoch` (non-zero; the
+ * same epoch as the stamp pass that follows).  The table-hazard check of a
+ * to_guest batch: a copy in program order translates page k, then writes
+ * chunk k, so a chunk that lands on a table node changes the walks of the
+ * pages after it (memvirt.py:615-627); a batch cannot reproduce that and
+ * must run page by page instead. */
+int pv_copy_plan_nodes(const uint8_t* image, uint64_t image_bytes,
+                       const pv_space* spaces, const pv_op* ops, uint64_t n_ops,
+                       const uint64_t* page_off, uint64_t n_pages,
+                       uint64_t* page_hpa, uint32_t* page_status, uint64_t* page_aux,
+                       uint64_t* op_first_bad, uint32_t* node_map, uint64_t node_pages,
+                       uint32_t epoch, void* stream);
+
+/* *conflict bits (device u32) set by the stamp pass; the exec stands down
+ * on any. */
+#define PV_CONFLICT_OVERLAP 0x1u /* two chunks write one hpa page: ordered apply */
+#define PV_CONFLICT_TABLE 0x2u   /* a chunk writes a node page marked in node_map: page by page */
+
 /* The conflict pass of pv_copy_plan on its own (run it after
  * pv_copy_fifo_replay when the cache may have changed destinations).
- * owner_pages = number of u64 entries in page_owner. */
+ * owner_pages = number of u64 entries in page_owner.  node_map (device,
+ * may be NULL): the marks of pv_copy_plan_nodes with the same epoch; a live
+ * chunk whose destination page is marked sets PV_CONFLICT_TABLE. */
 int pv_copy_stamp(const uint64_t* page_off, uint64_t n_ops, uint64_t n_pages,
                   const uint64_t* page_hpa, const uint64_t* op_first_bad,
                   uint64_t* page_owner, uint64_t owner_pages, uint32_t epoch,
-                  uint32_t* conflict, void* stream);
+                  uint32_t* conflict, const uint32_t* node_map, void* stream);
 
 /* Replays the FIFO cache over a copy plan: lookup l is page look_page[l]
  * of op look_op[l] (pages of an op consecutive and in order, ops of a

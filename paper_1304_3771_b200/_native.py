@@ -18,7 +18,7 @@ from .errors import NativeUnavailable
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpv.so")
 
 # ---- constants mirrored from include/pv.h --------------------------------
-ABI_VERSION = 3
+ABI_VERSION = 4
 SUCCESS = 0
 EINVAL = -22
 ENOMEM = -12
@@ -41,12 +41,15 @@ FLAG_PS = 0x80
 
 VA32 = 0x1
 OUT_PFN = 0x2
+CONCURRENT = 0x4  # pv.h PV_CONCURRENT: one walker CTA per SM
 HAS_TWO_STAGE = 0x80000000
 HAS_4L = 0x40000000
 
 TO_GUEST = 0
 FROM_GUEST = 1
 COPY_ALIGNED16 = 0x100
+CONFLICT_OVERLAP = 0x1  # pv.h PV_CONFLICT_OVERLAP: ordered apply
+CONFLICT_TABLE = 0x2    # pv.h PV_CONFLICT_TABLE: page by page
 
 FOP_WORDS = 17     # FileOp words (kind + 16 fields), pv.h PV_FOP_WORDS
 FRAME_BYTES = 40   # sizeof(pv_frame)
@@ -65,7 +68,7 @@ FIFO_WORDS = 2 * FIFO_MAX + 4  # pv_fifo
 # every symbol include/pv.h declares
 EXPORTS = (
     "pv_abi_version", "pv_translate_chunk", "pv_status_name", "pv_translate",
-    "pv_fifo_replay", "pv_copy_plan", "pv_copy_stamp", "pv_copy_exec",
+    "pv_fifo_replay", "pv_copy_plan", "pv_copy_plan_nodes", "pv_copy_stamp", "pv_copy_exec",
     "pv_copy_fifo_replay", "pv_scatter_pages", "pv_gather_pages", "pv_stream_sync", "pv_index_encode",
     "pv_fifo_scratch_bytes", "pv_copy_ordered_scratch_bytes", "pv_copy_ordered", "pv_result_encode",
     "pv_result_decode", "pv_timing", "pv_timing_ms", "pv_copy_shim_scratch_bytes", "pv_copy_shim",
@@ -101,7 +104,8 @@ _SIGNATURES = {
     "pv_result_decode": (ctypes.c_int, [_p, _u64, _p, _u64, _p, _p, _p]),
     "pv_copy_ordered": (ctypes.c_int, [_p, _u64, _p, _u64, _p, _u64, _p, _p, _p, _p, _p, _u64, _p, _p, _p, _u64, _p]),
     "pv_copy_plan": (ctypes.c_int, [_p, _u64, _p, _p, _u64, _p, _u64, _u32, _p, _p, _p, _p, _p, _u32, _p, _p]),
-    "pv_copy_stamp": (ctypes.c_int, [_p, _u64, _u64, _p, _p, _p, _u64, _u32, _p, _p]),
+    "pv_copy_plan_nodes": (ctypes.c_int, [_p, _u64, _p, _p, _u64, _p, _u64, _p, _p, _p, _p, _p, _u64, _u32, _p]),
+    "pv_copy_stamp": (ctypes.c_int, [_p, _u64, _u64, _p, _p, _p, _u64, _u32, _p, _p, _p]),
     "pv_copy_exec": (ctypes.c_int, [_p, _u64, _p, _u64, _p, _u64, _u32, _p, _p, _p, _p, _p, _u64, _p, _p, _p, _p]),
     "pv_copy_fifo_replay": (ctypes.c_int, [_p, _p, _p, _p, _p, _p, _u32, _u64, _u64, _u32, _p, _u64, _p, _p, _p,
                                             _p, _u64, _p]),

@@ -17,9 +17,9 @@ cudaError_t launch_index_encode(const uint8_t*, uint64_t, const uint64_t*, const
                                 uint32_t*, const uint8_t*, cudaStream_t);
 uint64_t translate_chunk();
 cudaError_t launch_copy_plan(const uint8_t*, uint64_t, const pv_space*, const pv_op*, uint64_t, const uint64_t*,
-                             uint64_t, uint64_t*, uint32_t*, uint64_t*, uint64_t*, cudaStream_t);
+                             uint64_t, uint64_t*, uint32_t*, uint64_t*, uint64_t*, uint32_t*, uint32_t, cudaStream_t);
 cudaError_t launch_copy_stamp(const uint64_t*, uint64_t, uint64_t, const uint64_t*, const uint64_t*, uint64_t*,
-                              uint64_t, uint32_t, uint32_t*, cudaStream_t);
+                              uint64_t, uint32_t, uint32_t*, const uint32_t*, cudaStream_t);
 cudaError_t launch_walk_one(const uint8_t*, uint64_t, const pv_space&, uint64_t, uint32_t, pv_one_result*, uint64_t,
                             cudaStream_t);
 cudaError_t launch_copy_small(uint8_t*, uint64_t, const pv_small_op&, uint8_t*, uint64_t, pv_small_result*, uint8_t*,
@@ -226,11 +226,11 @@ int pv_translate(const uint8_t* image, uint64_t image_bytes, const pv_space* spa
   if (image_bytes % kPageSize) return PV_EINVAL;
   // 4-byte walk codes carry leaf pfns in 28 bits (pv_translate.cu stage_codes)
   if (image_bytes >= (1ull << 40)) return PV_EINVAL;
-  if (flags & ~(uint32_t)(PV_VA32 | PV_OUT_PFN | PV_HAS_TWO_STAGE | PV_HAS_4L)) return PV_EINVAL;
+  if (flags & ~(uint32_t)(PV_VA32 | PV_OUT_PFN | PV_CONCURRENT | PV_HAS_TWO_STAGE | PV_HAS_4L)) return PV_EINVAL;
   const bool two = flags & PV_HAS_TWO_STAGE;
   if (index != nullptr && (!index->slot_of || !index->leaf_codes || !index->slot_page)) return PV_EINVAL;
   return rc(launch_translate(image, image_bytes, spaces, segs, n_segs, n_chunks, vas,
-                             flags & (PV_VA32 | PV_OUT_PFN | PV_HAS_4L), two, index,
+                             flags & (PV_VA32 | PV_OUT_PFN | PV_CONCURRENT | PV_HAS_4L), two, index,
                              out_value, out_status, out_aux, (cudaStream_t)stream));
 }
 
@@ -268,23 +268,36 @@ int pv_copy_plan(const uint8_t* image, uint64_t image_bytes, const pv_space* spa
   if (image_bytes % kPageSize) return PV_EINVAL;
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e = launch_copy_plan(image, image_bytes, spaces, ops, n_ops, page_off, n_pages, page_hpa, page_status,
-                                   page_aux, op_first_bad, s);
+                                   page_aux, op_first_bad, nullptr, 0, s);
   if (e != cudaSuccess) return rc(e);
   if (direction == PV_TO_GUEST && page_owner != nullptr) {
     if (!conflict) return PV_EINVAL;
     e = launch_copy_stamp(page_off, n_ops, n_pages, page_hpa, op_first_bad, page_owner, image_bytes / kPageSize,
-                          epoch, conflict, s);
+                          epoch, conflict, nullptr, s);
   }
   return rc(e);
 }
 
+int pv_copy_plan_nodes(const uint8_t* image, uint64_t image_bytes, const pv_space* spaces, const pv_op* ops,
+                       uint64_t n_ops, const uint64_t* page_off, uint64_t n_pages, uint64_t* page_hpa,
+                       uint32_t* page_status, uint64_t* page_aux, uint64_t* op_first_bad, uint32_t* node_map,
+                       uint64_t node_pages, uint32_t epoch, void* stream) {
+  if (n_pages == 0) return PV_SUCCESS;
+  if (!image || !spaces || !ops || !page_off || !page_hpa || !page_status || !op_first_bad || !node_map ||
+      n_ops == 0)
+    return PV_EINVAL;
+  if (image_bytes % kPageSize || node_pages < image_bytes / kPageSize || epoch == 0) return PV_EINVAL;
+  return rc(launch_copy_plan(image, image_bytes, spaces, ops, n_ops, page_off, n_pages, page_hpa, page_status,
+                             page_aux, op_first_bad, node_map, epoch, (cudaStream_t)stream));
+}
+
 int pv_copy_stamp(const uint64_t* page_off, uint64_t n_ops, uint64_t n_pages, const uint64_t* page_hpa,
                   const uint64_t* op_first_bad, uint64_t* page_owner, uint64_t owner_pages, uint32_t epoch,
-                  uint32_t* conflict, void* stream) {
+                  uint32_t* conflict, const uint32_t* node_map, void* stream) {
   if (n_pages == 0) return PV_SUCCESS;
   if (!page_off || !page_hpa || !op_first_bad || !page_owner || !conflict) return PV_EINVAL;
   return rc(launch_copy_stamp(page_off, n_ops, n_pages, page_hpa, op_first_bad, page_owner, owner_pages, epoch,
-                              conflict, (cudaStream_t)stream));
+                              conflict, node_map, (cudaStream_t)stream));
 }
 
 int pv_copy_exec(uint8_t* image, uint64_t image_bytes, const pv_op* ops, uint64_t n_ops, const uint64_t* page_off,

@@ -32,8 +32,11 @@ __host__ __device__ __forceinline__ uint64_t node_limit(uint64_t image_bytes, ui
   return base >= image_bytes ? 0 : (image_bytes - base) >> kPageShift;
 }
 
+template <bool kCoherent = false>
 __device__ __forceinline__ uint64_t ld_word(const uint8_t* image, uint64_t base, uint64_t pfn, uint32_t idx) {
-  return __ldg(reinterpret_cast<const unsigned long long*>(image + base + (pfn << kPageShift)) + idx);
+  const auto* p = reinterpret_cast<const unsigned long long*>(image + base + (pfn << kPageShift)) + idx;
+  // coherent (L2) loads for walks that must see this kernel's own writes
+  return kCoherent ? __ldcg(p) : __ldg(p);
 }
 
 // L2 cache-policy descriptors: streamed data (VAs, results, payload) is
@@ -74,18 +77,52 @@ __device__ __forceinline__ uint32_t classify(uint64_t w, uint32_t level, uint32_
   return PV_ST_OK;
 }
 
+// Table-node marks (the to_guest table-hazard check, pv_copy_plan_nodes):
+// node_map[absolute image page] = epoch for every node a walk reads.  Most
+// walks share their upper nodes, so the mark is a read (an L1 hit) and a
+// store only when the page is not marked yet.
+struct NodeMarks {
+  uint32_t* map;  // one u32 per image page, or nullptr (no marking)
+  uint32_t epoch;
+};
+
+// The node pages one walk reads, in order (a copy_small table-hazard check).
+struct NodeList {
+  static constexpr uint32_t kCap = 16;  // 6 levels (two stages), 2 pages each when a window is unaligned
+  uint64_t page[kCap];
+  uint32_t n;
+};
+
+__device__ __forceinline__ void mark_node(NodeList* nl, uint64_t base, uint64_t node) {
+  if (nl == nullptr) return;
+  const uint64_t at = base + (node << kPageShift);
+  if (nl->n < NodeList::kCap) nl->page[nl->n++] = at >> kPageShift;
+  if ((at & kPageMask) && nl->n < NodeList::kCap) nl->page[nl->n++] = (at >> kPageShift) + 1;
+}
+
+__device__ __forceinline__ void mark_node(const NodeMarks* nm, uint64_t base, uint64_t node) {
+  if (nm == nullptr) return;
+  const uint64_t at = base + (node << kPageShift);  // a window base need not be page aligned
+  uint32_t* p = nm->map + (at >> kPageShift);
+  if (*reinterpret_cast<volatile uint32_t*>(p) != nm->epoch) *p = nm->epoch;
+  if ((at & kPageMask) && *reinterpret_cast<volatile uint32_t*>(p + 1) != nm->epoch) p[1] = nm->epoch;
+}
+
 // Full three-level walk through global memory (L1/L2 cached).  On success
 // returns PV_ST_OK with *out = leaf target pfn.  On a trap *out = node pfn.
+// With nm != nullptr every node read is marked (mark_node).
+template <bool kCoherent = false, class M = const NodeMarks*>
 __device__ __forceinline__ uint32_t walk_global(const uint8_t* __restrict__ image, uint64_t image_bytes,
                                                 uint64_t base, uint64_t root, uint64_t va, uint32_t stage2,
-                                                uint64_t* out) {
+                                                uint64_t* out, M nm = nullptr) {
   const uint64_t lim = node_limit(image_bytes, base);
   uint64_t node = root, trap_node = 0;
   const uint32_t idx[3] = {top_index(va), mid_index(va), leaf_index(va)};
 #pragma unroll
   for (uint32_t l = 0; l < 3; ++l) {
     if (node >= lim) return (stage2 ? PV_ST_NODE_OOR2 : PV_ST_NODE_OOR) | (l + 1);
-    const uint64_t w = ld_word(image, base, node, idx[l]);
+    mark_node(nm, base, node);
+    const uint64_t w = ld_word<kCoherent>(image, base, node, idx[l]);
     const uint32_t st = classify(w, l + 1, idx[l], stage2, &node, &trap_node);
     if (st != PV_ST_OK) {
       *out = trap_node;
@@ -99,8 +136,10 @@ __device__ __forceinline__ uint32_t walk_global(const uint8_t* __restrict__ imag
 // Extension geometry PV_ONE_STAGE_4L: 4 levels of 512 entries over 48-bit
 // VAs, 2 MiB leaves at level 3 (PV_FLAG_PS).  Returns the 4 KiB frame of
 // va (for a 2 MiB leaf: its pfn + va's 4 KiB index inside it).
+template <bool kCoherent = false, class M = const NodeMarks*>
 __device__ __forceinline__ uint32_t walk4_global(const uint8_t* __restrict__ image, uint64_t image_bytes,
-                                                 uint64_t base, uint64_t root, uint64_t va, uint64_t* out) {
+                                                 uint64_t base, uint64_t root, uint64_t va, uint64_t* out,
+                                                 M nm = nullptr) {
   const uint64_t lim = node_limit(image_bytes, base);
   const uint32_t idx[4] = {(uint32_t)(va >> 39) & 511u, (uint32_t)(va >> 30) & 511u, (uint32_t)(va >> 21) & 511u,
                            (uint32_t)(va >> 12) & 511u};
@@ -108,7 +147,8 @@ __device__ __forceinline__ uint32_t walk4_global(const uint8_t* __restrict__ ima
 #pragma unroll
   for (uint32_t l = 0; l < 4; ++l) {
     if (node >= lim) return PV_ST_NODE_OOR | (l + 1);
-    const uint64_t w = ld_word(image, base, node, idx[l]);
+    mark_node(nm, base, node);
+    const uint64_t w = ld_word<kCoherent>(image, base, node, idx[l]);
     if (w & kFlagTrapping) {
       *out = node;
       return PV_ST_TRAP | (l + 1) | (idx[l] << 16);
@@ -127,16 +167,17 @@ __device__ __forceinline__ uint32_t walk4_global(const uint8_t* __restrict__ ima
 // Translate `va` through a space with global-memory walks.  On success
 // *value = leaf pfn of the final stage.  On failure *value / *aux follow the
 // pv.h status conventions (va or gpa for faults, node pfn for traps).
+template <bool kCoherent = false, class M = const NodeMarks*>
 __device__ __forceinline__ uint32_t translate_global(const uint8_t* __restrict__ image, uint64_t image_bytes,
                                                      const pv_space& sp, uint64_t va, uint64_t* value,
-                                                     uint64_t* aux) {
+                                                     uint64_t* aux, M nm = nullptr) {
   uint64_t r = 0;
   if (sp.mode == PV_ONE_STAGE_4L) {
-    const uint32_t st4 = walk4_global(image, image_bytes, sp.s1_base, sp.s1_root_pfn, va, &r);
+    const uint32_t st4 = walk4_global<kCoherent>(image, image_bytes, sp.s1_base, sp.s1_root_pfn, va, &r, nm);
     *value = (st4 == PV_ST_OK || PV_ST_KIND(st4) == PV_ST_TRAP) ? r : va;
     return st4;
   }
-  uint32_t st = walk_global(image, image_bytes, sp.s1_base, sp.s1_root_pfn, va, 0, &r);
+  uint32_t st = walk_global<kCoherent>(image, image_bytes, sp.s1_base, sp.s1_root_pfn, va, 0, &r, nm);
   if (st != PV_ST_OK) {
     *value = (PV_ST_KIND(st) == PV_ST_TRAP) ? r : va;
     return st;
@@ -146,7 +187,7 @@ __device__ __forceinline__ uint32_t translate_global(const uint8_t* __restrict__
     return PV_ST_OK;
   }
   const uint64_t gpa = (r << kPageShift) | (va & kPageMask);
-  st = walk_global(image, image_bytes, 0, sp.s2_root_pfn, gpa, 1, &r);
+  st = walk_global<kCoherent>(image, image_bytes, 0, sp.s2_root_pfn, gpa, 1, &r, nm);
   if (st != PV_ST_OK) {
     if (PV_ST_KIND(st) == PV_ST_TRAP2) {
       *value = r;

@@ -37,11 +37,13 @@ constexpr int kExecTpb = 256;
 constexpr int kExecWarps = kExecTpb / 32;
 constexpr int kExecPpw = 4;  // pages per exec warp
 
+template <bool kMark>
 __global__ void __launch_bounds__(kPlanTpb)
 plan_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const pv_space* __restrict__ spaces,
             const pv_op* __restrict__ ops, uint64_t n_ops, const uint64_t* __restrict__ page_off, uint64_t n_pages,
             uint64_t* __restrict__ page_hpa, uint32_t* __restrict__ page_status, uint64_t* __restrict__ page_aux,
-            unsigned long long* __restrict__ op_first_bad) {
+            unsigned long long* __restrict__ op_first_bad, NodeMarks marks) {
+  const NodeMarks* nm = kMark ? &marks : nullptr;
   const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t * kPlanPpt < n_pages; t += nthreads) {
     const uint64_t p0 = t * kPlanPpt;
@@ -62,7 +64,7 @@ plan_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const pv_sp
       const uint64_t done = cur - o.gva;
       const uint64_t chunk = min(o.len - done, kPageSize - (cur & kPageMask));
       uint64_t value = 0, aux = 0;
-      uint32_t st = translate_global(image, image_bytes, sp, cur, &value, &aux);
+      uint32_t st = translate_global(image, image_bytes, sp, cur, &value, &aux, nm);
       if (st == PV_ST_OK) {
         value = (value << kPageShift) | (cur & kPageMask);
         // host_mem.write / read bounds check (memvirt.py:156-158).
@@ -80,12 +82,16 @@ plan_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const pv_sp
 __global__ void __launch_bounds__(kPlanTpb)
 stamp_kernel(const uint64_t* __restrict__ page_off, uint64_t n_ops, uint64_t n_pages,
              const uint64_t* __restrict__ page_hpa, const unsigned long long* __restrict__ op_first_bad,
-             unsigned long long* __restrict__ owner, uint64_t owner_pages, uint32_t epoch, uint32_t* conflict) {
+             unsigned long long* __restrict__ owner, uint64_t owner_pages, uint32_t epoch, uint32_t* conflict,
+             const uint32_t* __restrict__ node_map) {
   const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t * kPlanPpt < n_pages; t += nthreads) {
-    // one detected conflict decides the batch (the exec kernel stands down):
-    // stop stamping, so heavily overlapping batches do not serialise on atomics
-    if (*reinterpret_cast<volatile const uint32_t*>(conflict)) return;
+    // a table hazard decides the batch (the host runs it page by page);
+    // an overlap only stops the stamping (heavily overlapping batches do
+    // not serialise on atomics) while the hazard check goes on
+    const uint32_t seen_conflict = *reinterpret_cast<volatile const uint32_t*>(conflict);
+    if (seen_conflict & PV_CONFLICT_TABLE) return;
+    if (seen_conflict && node_map == nullptr) return;
     const uint64_t p0 = t * kPlanPpt;
     uint64_t op = upper_search(page_off, 0, n_ops, p0);
     uint64_t op_end = __ldg(page_off + op + 1);
@@ -98,14 +104,20 @@ stamp_kernel(const uint64_t* __restrict__ page_off, uint64_t n_ops, uint64_t n_p
       if (k >= op_first_bad[op]) continue;
       const uint64_t hp = page_hpa[p] >> kPageShift;
       if (hp >= owner_pages) continue;
+      if (node_map != nullptr && __ldg(node_map + hp) == epoch) {  // writes a node the batch walks
+        atomicOr(conflict, PV_CONFLICT_TABLE);
+        return;
+      }
+      if (*reinterpret_cast<volatile const uint32_t*>(conflict) & PV_CONFLICT_OVERLAP) continue;
       const unsigned long long mine = ((unsigned long long)epoch << 40) | (p + 1);
       const unsigned long long seen = *reinterpret_cast<volatile const unsigned long long*>(owner + hp);
       if ((seen >> 40) == epoch && seen != mine) {  // already stamped by another chunk of this batch
-        atomicOr(conflict, 1u);
-        return;
+        atomicOr(conflict, PV_CONFLICT_OVERLAP);
+        if (node_map == nullptr) return;
+        continue;
       }
       const unsigned long long old = atomicMax(owner + hp, mine);
-      if ((old >> 40) == epoch && old != mine) atomicOr(conflict, 1u);
+      if ((old >> 40) == epoch && old != mine) atomicOr(conflict, PV_CONFLICT_OVERLAP);
     }
   }
 }
@@ -442,39 +454,118 @@ __global__ void walk_one_kernel(const uint8_t* __restrict__ image, uint64_t imag
 constexpr int kSmallTpb = 256;
 static_assert(PV_SMALL_PAGES <= kSmallTpb, "one plan thread per page");
 
+// Translation of page k of a small op: the caller's FIFO hit, or a walk
+// (kCoherent: L2 loads that see this kernel's earlier writes).
+template <bool kCoherent, class M>
+__device__ __forceinline__ uint32_t small_page(const uint8_t* __restrict__ image, uint64_t image_bytes,
+                                               const pv_small_op& op, uint32_t k, uint64_t* value, uint64_t* aux,
+                                               M nodes) {
+  const uint64_t cur = op_page_va(op.gva, k);
+  const uint64_t done = cur - op.gva;
+  const uint64_t chunk = min(op.len - done, kPageSize - (cur & kPageMask));
+  const uint64_t hit = op.pre_hpa[k];
+  uint32_t st = PV_ST_OK;
+  if (hit != 0) {
+    *value = hit - 1;  // the caller's translation (a FIFO hit): the byte hpa
+  } else {
+    st = translate_global<kCoherent>(image, image_bytes, op.space, cur, value, aux, nodes);
+    if (st == PV_ST_OK) *value = (*value << kPageShift) | (cur & kPageMask);
+  }
+  if (st == PV_ST_OK && (*value + chunk > image_bytes || *value + chunk < *value))
+    st = PV_ST_DATA_OOR;  // memvirt.py:156-158
+  return st;
+}
+
+// The table-hazard form of copy_small_kernel, on one warp: page k is
+// translated (coherent walk) and its chunk written before page k + 1 is
+// translated (memvirt.py:615-627).
+__device__ __noinline__ void small_sequential(uint8_t* __restrict__ image, uint64_t image_bytes,
+                                              const pv_small_op& op, uint8_t* __restrict__ buf, uint64_t buf_bytes,
+                                              pv_small_result* out, uint8_t* __restrict__ dirty, uint32_t n_pages,
+                                              uint32_t lane) {
+  const uint64_t pol = policy_evict_first();
+  pv_op_result r;
+  r.copied = op.len;
+  r.value = r.aux = 0;
+  r.status = PV_ST_OK;
+  r.fail_page = 0;
+  for (uint32_t k = 0; k < n_pages; ++k) {
+    uint64_t value = 0, aux = 0;
+    uint32_t st = 0;
+    if (lane == 0) st = small_page<true>(image, image_bytes, op, k, &value, &aux, (NodeList*)nullptr);
+    st = __shfl_sync(0xffffffffu, st, 0);
+    value = __shfl_sync(0xffffffffu, value, 0);
+    aux = __shfl_sync(0xffffffffu, aux, 0);
+    if (lane == 0) {
+      out->page_hpa[k] = value;
+      out->page_status[k] = st;
+    }
+    const uint64_t cur = op_page_va(op.gva, k);
+    const uint64_t done = cur - op.gva;
+    if (st != PV_ST_OK) {
+      r.copied = done;
+      r.value = value;
+      r.aux = aux;
+      r.status = st;
+      r.fail_page = k;
+      break;
+    }
+    const uint32_t chunk = buf_clamp(done, (uint32_t)min(op.len - done, kPageSize - (cur & kPageMask)), buf_bytes);
+    warp_copy(image + value, buf + done, chunk, lane, pol);
+    if (dirty != nullptr && lane == 0) dirty[value >> kPageShift] = 1;
+    __threadfence();  // the chunk is in L2 before the next page's walk reads it
+    __syncwarp();
+  }
+  if (lane == 0) out->op = r;
+}
+
 // One CTA: thread k translates page k (or takes the caller's FIFO hit), the
 // op's first failing page is a shared atomicMin, then warp w copies pages
-// w, w + 8, ... below it (memvirt.py:615-627 prefix semantics).
+// w, w + 8, ... below it (memvirt.py:615-627 prefix semantics).  A to_guest
+// op whose chunk k lands on a table node the walk of a later page reads (a
+// table hazard) runs page by page instead -- walk k, write k, walk k + 1
+// through coherent loads -- exactly like copy_user_buffer.
 __global__ void __launch_bounds__(kSmallTpb)
 copy_small_kernel(uint8_t* __restrict__ image, uint64_t image_bytes, pv_small_op op, uint8_t* __restrict__ buf,
                   uint64_t buf_bytes, pv_small_result* out, uint8_t* __restrict__ dirty, uint32_t n_pages,
                   uint64_t seq) {
   __shared__ uint64_t s_hpa[PV_SMALL_PAGES];
-  __shared__ uint32_t s_bad;
+  __shared__ NodeList s_nodes[PV_SMALL_PAGES];
+  __shared__ uint32_t s_bad, s_hazard;
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) s_bad = n_pages;
+  const bool to_guest = op.direction == PV_TO_GUEST;
+  if (tid == 0) {
+    s_bad = n_pages;
+    s_hazard = 0;
+  }
   __syncthreads();
   uint64_t value = 0, aux = 0;
   uint32_t st = PV_ST_OK;
   if (tid < n_pages) {
-    const uint64_t cur = op_page_va(op.gva, tid);
-    const uint64_t done = cur - op.gva;
-    const uint64_t chunk = min(op.len - done, kPageSize - (cur & kPageMask));
-    const uint64_t hit = op.pre_hpa[tid];
-    if (hit != 0) {
-      value = hit - 1;  // the caller's translation (a FIFO hit): the byte hpa
-    } else {
-      st = translate_global(image, image_bytes, op.space, cur, &value, &aux);
-      if (st == PV_ST_OK) value = (value << kPageShift) | (cur & kPageMask);
-    }
-    if (st == PV_ST_OK && (value + chunk > image_bytes || value + chunk < value))
-      st = PV_ST_DATA_OOR;  // memvirt.py:156-158
+    s_nodes[tid].n = 0;
+    st = small_page<false>(image, image_bytes, op, tid, &value, &aux, to_guest ? &s_nodes[tid] : nullptr);
     s_hpa[tid] = value;
     out->page_hpa[tid] = value;
     out->page_status[tid] = st;
     if (st != PV_ST_OK) atomicMin(&s_bad, tid);
   }
   __syncthreads();
+  if (to_guest && tid < s_bad) {  // chunk tid is written: does a later page walk its page?
+    const uint64_t dst = s_hpa[tid] >> kPageShift;
+    for (uint32_t j = tid + 1; j < n_pages; ++j)
+      for (uint32_t i = 0; i < s_nodes[j].n; ++i)
+        if (s_nodes[j].page[i] == dst) s_hazard = 1;
+  }
+  __syncthreads();
+  if (s_hazard) {
+    if (warp == 0) small_sequential(image, image_bytes, op, buf, buf_bytes, out, dirty, n_pages, lane);
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence_system();
+      *reinterpret_cast<volatile uint64_t*>(&out->seq) = seq;
+    }
+    return;
+  }
   const uint32_t bad = s_bad;
   if (tid == bad) {
     pv_op_result r;
@@ -528,21 +619,30 @@ cudaError_t launch_copy_small(uint8_t* image, uint64_t image_bytes, const pv_sma
 
 cudaError_t launch_copy_plan(const uint8_t* image, uint64_t image_bytes, const pv_space* spaces, const pv_op* ops,
                              uint64_t n_ops, const uint64_t* page_off, uint64_t n_pages, uint64_t* page_hpa,
-                             uint32_t* page_status, uint64_t* page_aux, uint64_t* op_first_bad, cudaStream_t stream) {
+                             uint32_t* page_status, uint64_t* page_aux, uint64_t* op_first_bad, uint32_t* node_map,
+                             uint32_t epoch, cudaStream_t stream) {
   if (n_pages == 0) return cudaSuccess;
   const uint64_t threads = (n_pages + kPlanPpt - 1) / kPlanPpt;
   uint64_t grid = (threads + kPlanTpb - 1) / kPlanTpb;
-  const uint64_t cap = resident_grid((const void*)plan_kernel, kPlanTpb, 0);
-  if (grid > cap) grid = cap;
-  plan_kernel<<<(unsigned)grid, kPlanTpb, 0, stream>>>(image, image_bytes, spaces, ops, n_ops, page_off, n_pages,
-                                                       page_hpa, page_status, page_aux,
-                                                       reinterpret_cast<unsigned long long*>(op_first_bad));
+  const NodeMarks marks{node_map, epoch};
+  auto* fb = reinterpret_cast<unsigned long long*>(op_first_bad);
+  if (node_map != nullptr) {
+    const uint64_t cap = resident_grid((const void*)plan_kernel<true>, kPlanTpb, 0);
+    if (grid > cap) grid = cap;
+    plan_kernel<true><<<(unsigned)grid, kPlanTpb, 0, stream>>>(image, image_bytes, spaces, ops, n_ops, page_off,
+                                                               n_pages, page_hpa, page_status, page_aux, fb, marks);
+  } else {
+    const uint64_t cap = resident_grid((const void*)plan_kernel<false>, kPlanTpb, 0);
+    if (grid > cap) grid = cap;
+    plan_kernel<false><<<(unsigned)grid, kPlanTpb, 0, stream>>>(image, image_bytes, spaces, ops, n_ops, page_off,
+                                                                n_pages, page_hpa, page_status, page_aux, fb, marks);
+  }
   return cudaGetLastError();
 }
 
 cudaError_t launch_copy_stamp(const uint64_t* page_off, uint64_t n_ops, uint64_t n_pages, const uint64_t* page_hpa,
                               const uint64_t* op_first_bad, uint64_t* owner, uint64_t owner_pages, uint32_t epoch,
-                              uint32_t* conflict, cudaStream_t stream) {
+                              uint32_t* conflict, const uint32_t* node_map, cudaStream_t stream) {
   if (n_pages == 0) return cudaSuccess;
   const uint64_t threads = (n_pages + kPlanPpt - 1) / kPlanPpt;
   uint64_t grid = (threads + kPlanTpb - 1) / kPlanTpb;
@@ -550,7 +650,7 @@ cudaError_t launch_copy_stamp(const uint64_t* page_off, uint64_t n_ops, uint64_t
   if (grid > cap) grid = cap;
   stamp_kernel<<<(unsigned)grid, kPlanTpb, 0, stream>>>(
       page_off, n_ops, n_pages, page_hpa, reinterpret_cast<const unsigned long long*>(op_first_bad),
-      reinterpret_cast<unsigned long long*>(owner), owner_pages, epoch, conflict);
+      reinterpret_cast<unsigned long long*>(owner), owner_pages, epoch, conflict, node_map);
   return cudaGetLastError();
 }
 

@@ -28,9 +28,14 @@
 //   apply   : winners write their word into the image (marking the dirty map);
 //   rewalk  : reached simple traps re-walk the hybrid table (the retry) and
 //             become ordinary translations; unreached ones get their trap
-//             status back and re-enter the first-failure minimum.
+//             status back and re-enter the first-failure minimum;
+//   stop    : every op after the cut moves nothing (first failing page 0):
+//             the host re-plans those ops once its per-op shim has run, so
+//             no byte may move through the pre-shim tables.  With a shim row
+//             of guest_bytes 0 (a replaced trap_shim) nothing is simple and
+//             the first trapping op is the cut.
 // The passes after eval run as one cooperative kernel that returns at once
-// when eval found nothing, so a trap-free batch pays two launches.  The scratch area is left
+// when eval found no trap at all, so a trap-free batch pays two launches.  The scratch area is left
 // zeroed after each call (the claim table cleans up after itself).
 #include <cooperative_groups.h>
 
@@ -44,6 +49,7 @@ constexpr int kShimTpb = 256;
 struct ShimScratch {
   unsigned long long* count;  // [0] simple traps listed
   unsigned long long* cut;    // [1] ~(first cut op), 0 = none
+  unsigned long long* traps;  // [2] trapping pages seen by eval (simple or not)
   unsigned long long* list_p; // page index (bit 63: reached, bit 62: winner)
   unsigned long long* list_w; // shim word
   unsigned long long* list_op;
@@ -64,7 +70,8 @@ static ShimScratch carve(void* scratch, uint64_t n_pages) {
   const uint64_t cap = table_cap(n_pages);
   s.count = w;
   s.cut = w + 1;
-  s.list_p = w + 2;
+  s.traps = w + 2;
+  s.list_p = w + 3;
   s.list_w = s.list_p + n_pages;
   s.list_op = s.list_w + n_pages;
   s.keys = s.list_op + n_pages;
@@ -73,7 +80,7 @@ static ShimScratch carve(void* scratch, uint64_t n_pages) {
   return s;
 }
 
-size_t shim_scratch_bytes(uint64_t n_pages) { return (2 + 3 * n_pages + 2 * table_cap(n_pages)) * 8; }
+size_t shim_scratch_bytes(uint64_t n_pages) { return (3 + 3 * n_pages + 2 * table_cap(n_pages)) * 8; }
 
 __device__ __forceinline__ uint64_t hash_slot(uint64_t k) {
   k ^= k >> 33;
@@ -117,7 +124,10 @@ shim_eval_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const 
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n_pages; p += stride) {
     const uint32_t st = page_status[p];
-    if (PV_ST_KIND(st) != PV_ST_TRAP || PV_ST_LEVEL(st) != 3) continue;
+    if (PV_ST_KIND(st) == PV_ST_TRAP2) atomicAdd(sc.traps, 1ull);
+    if (PV_ST_KIND(st) != PV_ST_TRAP) continue;
+    atomicAdd(sc.traps, 1ull);
+    if (PV_ST_LEVEL(st) != 3) continue;
     uint64_t op, k;
     op_of(page_off, n_ops, p, &op, &k);
     const pv_op o = ops[op];
@@ -152,17 +162,14 @@ __device__ __forceinline__ uint64_t find_slot(const ShimScratch& sc, uint64_t ke
   return h;
 }
 
-__global__ void __launch_bounds__(kShimTpb)
-shim_resolve_kernel(ShimScratch sc, uint8_t* __restrict__ image, uint64_t image_bytes,
-                    const pv_space* __restrict__ spaces, const pv_op* __restrict__ ops, uint64_t n_ops,
-                    const uint64_t* __restrict__ page_off, uint64_t n_pages, uint64_t* __restrict__ page_hpa,
-                    uint32_t* __restrict__ page_status, unsigned long long* __restrict__ op_first_bad,
-                    uint8_t* __restrict__ dirty, unsigned long long* __restrict__ n_written) {
-  const uint64_t n = *sc.count;
-  if (n == 0) return;  // uniform across the grid: nothing trapped simply
-  cg::grid_group grid = cg::this_grid();
-  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
+// Steps 1-5 (only when eval listed simple traps).
+__device__ __noinline__ void shim_fix(cg::grid_group& grid, uint64_t tid, uint64_t nthr, uint64_t n,
+                                      const ShimScratch& sc, uint8_t* __restrict__ image, uint64_t image_bytes,
+                                      const pv_space* __restrict__ spaces, const pv_op* __restrict__ ops,
+                                      uint64_t n_ops, const uint64_t* __restrict__ page_off, uint64_t n_pages,
+                                      uint64_t* __restrict__ page_hpa, uint32_t* __restrict__ page_status,
+                                      unsigned long long* __restrict__ op_first_bad, uint8_t* __restrict__ dirty,
+                                      unsigned long long* __restrict__ n_written) {
   // 1. the first failing page of every op holding a simple trap is recomputed
   for (uint64_t i = tid; i < n; i += nthr) op_first_bad[sc.list_op[i]] = kNone;
   grid.sync();
@@ -249,9 +256,40 @@ shim_resolve_kernel(ShimScratch sc, uint8_t* __restrict__ image, uint64_t image_
     if (st != PV_ST_OK) atomicMin(op_first_bad + op, (unsigned long long)k);
   }
   grid.sync();
+  if (tid == 0) *sc.cut = 0;  // step 6 computes the cut after the shim
+  grid.sync();
+}
+
+__global__ void __launch_bounds__(kShimTpb)
+shim_resolve_kernel(ShimScratch sc, uint8_t* __restrict__ image, uint64_t image_bytes,
+                    const pv_space* __restrict__ spaces, const pv_op* __restrict__ ops, uint64_t n_ops,
+                    const uint64_t* __restrict__ page_off, uint64_t n_pages, uint64_t* __restrict__ page_hpa,
+                    uint32_t* __restrict__ page_status, unsigned long long* __restrict__ op_first_bad,
+                    uint8_t* __restrict__ dirty, unsigned long long* __restrict__ n_written) {
+  if (*sc.traps == 0) return;  // uniform across the grid: nothing trapped
+  const uint64_t n = *sc.count;
+  cg::grid_group grid = cg::this_grid();
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
+  if (n != 0) shim_fix(grid, tid, nthr, n, sc, image, image_bytes, spaces, ops, n_ops, page_off, n_pages, page_hpa,
+                       page_status, op_first_bad, dirty, n_written);
+  // 6. stop: the cut after the shim is the first op whose first failing page
+  //    still traps; the ops after it move nothing
+  for (uint64_t op = tid; op < n_ops; op += nthr) {
+    const unsigned long long fb = op_first_bad[op];
+    if (fb == kNone) continue;
+    const uint32_t kd = PV_ST_KIND(page_status[__ldg(page_off + op) + fb]);
+    if (kd == PV_ST_TRAP || kd == PV_ST_TRAP2) atomicMax(sc.cut, ~(unsigned long long)op);
+  }
+  grid.sync();
+  const unsigned long long cut = ~*sc.cut;
+  if (cut != kNone)
+    for (uint64_t op = cut + 1 + tid; op < n_ops; op += nthr) op_first_bad[op] = 0;
+  grid.sync();
   if (tid == 0) {  // leave the scratch zero-filled
     *sc.count = 0;
     *sc.cut = 0;
+    *sc.traps = 0;
   }
 }
 

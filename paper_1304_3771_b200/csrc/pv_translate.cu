@@ -478,7 +478,8 @@ static cudaError_t launch_generic(const uint8_t* image, uint64_t image_bytes, co
 template <bool kTwo, bool kVa32, bool kPfn>
 static cudaError_t launch_t(const uint8_t* image, uint64_t image_bytes, const pv_space* spaces, const pv_seg* segs,
                             uint32_t n_segs, uint64_t n_chunks, const void* vas, const pv_index* idx,
-                            uint64_t* out_value, uint32_t* out_status, uint64_t* out_aux, cudaStream_t stream) {
+                            uint64_t* out_value, uint32_t* out_status, uint64_t* out_aux, bool concurrent,
+                            cudaStream_t stream) {
   // one-stage walks: 512-thread CTAs x 4 lanes (2 CTAs/SM) measured best on
   // C5 (scripts/ab_walk.sh: 0.848 ms vs 0.858 at 1024 x 2 and 0.923 at 128 x 16)
 #ifndef PV_TR_MINB
@@ -491,6 +492,14 @@ static cudaError_t launch_t(const uint8_t* image, uint64_t image_bytes, const pv
                 : translate_kernel<kTwo, kVa32, kPfn, 512, PV_TR_MINB>;
   const int tpb = kTwo ? PV_TR2_TPB : 512;
   uint64_t grid = resident_grid((const void*)k, tpb, 0);
+  if (concurrent) {
+    // PV_CONCURRENT: one CTA per SM, so a kernel launched beside the walk
+    // (the copy exec: one 192 KiB CTA per SM) finds room on every SM
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms > 0 && grid > (uint64_t)sms) grid = (uint64_t)sms;
+  }
   if (grid > n_chunks) grid = n_chunks;
   if (grid == 0) return cudaSuccess;
   const uint32_t* slot_of = idx != nullptr ? idx->slot_of : nullptr;
@@ -538,7 +547,7 @@ cudaError_t launch_translate(const uint8_t* image, uint64_t image_bytes, const p
 #define PV_DISPATCH(T, V, P)                                                                                    \
   if (two_stage == T && va32 == V && pfn == P)                                                                  \
     return launch_t<T, V, P>(image, image_bytes, spaces, segs, n_segs, n_chunks, vas, idx, out_value, \
-                             out_status, out_aux, stream);
+                             out_status, out_aux, flags & PV_CONCURRENT, stream);
   PV_DISPATCH(false, false, false)
   PV_DISPATCH(false, false, true)
   PV_DISPATCH(false, true, false)

@@ -171,6 +171,11 @@ class LeafIndex:
       the map is cleared or the next translate launch (:meth:`sync_device_writes`).
     Leaf nodes that are not indexed are walked through the raw PTEs, so the
     index can only change speed, never results.
+
+    Threads: every change runs under the image lock and records ``_ready``
+    on its stream; a translate on another stream waits for that event
+    (:meth:`wait_ready`) before it reads the codes, and replaced tensors stay
+    alive (``_retired``) until the next device-wide synchronisation.
     """
 
     def __init__(self, image):
@@ -184,7 +189,8 @@ class LeafIndex:
         self.codes = torch.zeros(512, dtype=torch.int32, device="cuda")
         self.seen_dev_epoch = image.dev_write_epoch
         self._scanned: dict = {}  # space -> image.host_epoch of its last scan
-        self._abi = PvIndex()
+        self._ready = None        # (stream handle, event) after the last change
+        self._retired: list = []  # replaced tensors other streams may still read
 
     @property
     def n_slots(self) -> int:
@@ -230,11 +236,40 @@ class LeafIndex:
             out.append(leaf[leaf < lim].astype(np.int64) + base // PAGE_SIZE)
         return np.unique(np.concatenate(out)) if out else np.zeros(0, dtype=np.int64)
 
+    def _changed(self) -> None:
+        import torch
+
+        stream = torch.cuda.current_stream()
+        if torch.cuda.is_current_stream_capturing():
+            return
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        self._ready = (stream.cuda_stream, ev)
+
+    def wait_ready(self) -> None:
+        """Order the current stream after the index's last change."""
+        import torch
+
+        ready = self._ready
+        # a capture starts from a synchronised device (torch.cuda.graph), and
+        # a capturing stream may not wait on uncaptured work
+        if ready is not None and ready[0] != torch.cuda.current_stream().cuda_stream and \
+                not torch.cuda.is_current_stream_capturing():
+            torch.cuda.current_stream().wait_event(ready[1])
+
+    def release_retired(self) -> None:
+        """Drop replaced tensors (call after a device-wide synchronisation)."""
+        self._retired.clear()
+
     def ensure(self, spaces: list["Space"]) -> None:
         """Index the leaf nodes ``spaces`` reach.  A space is rescanned only
         after host writes changed the image (tables are edited host-side;
         a structural change the scan misses only costs speed: unindexed leaf
         nodes are walked raw)."""
+        with self.image._lock:
+            self._ensure(spaces)
+
+    def _ensure(self, spaces: list["Space"]) -> None:
         import torch
 
         dev = self.image.device()
@@ -252,13 +287,16 @@ class LeafIndex:
         slots = np.arange(first, first + len(new), dtype=np.int64)
         self.slot_of_host[new] = slots.astype(np.uint32)
         self.pages = np.concatenate([self.pages, new])
+        self.wait_ready()
         slot_page = torch.from_numpy(self.pages.copy()).to("cuda")
         codes = torch.empty(self.n_slots * 512, dtype=torch.int32, device="cuda")
         if first:
             codes[: first * 512].copy_(self.codes[: first * 512])
+        self._retired += [self.slot_page, self.codes]
         self.slot_page, self.codes = slot_page, codes
         self.slot_of[torch.from_numpy(new).to("cuda")] = torch.from_numpy(slots.astype(np.int32)).to("cuda")
         self._encode(dev, None, first, len(new), None)
+        self._changed()
 
     def _encode(self, dev, slots, first, n, dirty) -> None:
         lib = N.lib()
@@ -274,27 +312,38 @@ class LeafIndex:
         if len(s):
             import torch
 
-            self._encode(dev, torch.from_numpy(s).to("cuda"), 0, len(s), None)
+            with self.image._lock:
+                self.wait_ready()
+                self._encode(dev, torch.from_numpy(s).to("cuda"), 0, len(s), None)
+                self._changed()
 
     def sync_device_writes(self) -> None:
-        """Re-encode indexed pages the device wrote since the last sync."""
+        """Re-encode indexed pages the device wrote since the last sync (after
+        the writes of every stream, see MemoryImage.wait_writers)."""
         img = self.image
-        if self.seen_dev_epoch != img.dev_write_epoch and self.n_slots and img.on_device:
-            self._encode(img._dev, None, 0, self.n_slots, img.dirty_map())
-        self.seen_dev_epoch = img.dev_write_epoch
+        with img._lock:
+            epoch = img.dev_write_epoch
+            if self.seen_dev_epoch != epoch and self.n_slots and img.on_device:
+                img.wait_writers()
+                self.wait_ready()
+                self._encode(img._dev, None, 0, self.n_slots, img.dirty_map())
+                self._changed()
+            self.seen_dev_epoch = epoch
 
     def abi(self) -> PvIndex:
-        self._abi.slot_of = self.slot_of.data_ptr()
-        self._abi.leaf_codes = self.codes.data_ptr()
-        self._abi.slot_page = self.slot_page.data_ptr()
-        self._abi.n_slots = self.n_slots
-        return self._abi
+        """pv_index of the current tensors (a fresh struct per call: threads
+        never share one), after ordering the stream behind the last change."""
+        with self.image._lock:
+            self.wait_ready()
+            return PvIndex(self.slot_of.data_ptr(), self.codes.data_ptr(), self.slot_page.data_ptr(), self.n_slots)
 
 
 def leaf_index(image) -> LeafIndex:
     if image.leaf_index is None:
-        image.device()
-        image.leaf_index = LeafIndex(image)
+        with image._lock:
+            if image.leaf_index is None:
+                image.device()
+                image.leaf_index = LeafIndex(image)
     return image.leaf_index
 
 
@@ -322,12 +371,13 @@ class TranslatePlan:
             self._indexed = True
 
 
-def translate_lanes(image, plan: TranslatePlan, vas, *, out_pfn: bool = False, out=None):
+def translate_lanes(image, plan: TranslatePlan, vas, *, out_pfn: bool = False, out=None, concurrent: bool = False):
     """Translate every lane of ``vas`` (int64 or int32 cuda tensor).
 
     Returns ``(value int64, status int32, aux int64)`` device tensors, written
     asynchronously on the current stream.  ``out`` may pass preallocated
-    tensors of the same shapes.
+    tensors of the same shapes.  ``concurrent``: the walk shares the GPU with
+    a kernel on another stream (pv.h PV_CONCURRENT, one CTA per SM).
     """
     import torch
 
@@ -340,7 +390,8 @@ def translate_lanes(image, plan: TranslatePlan, vas, *, out_pfn: bool = False, o
         aux = torch.zeros(n, dtype=torch.int64, device="cuda")
     else:
         value, status, aux = out
-    flags = (N.VA32 if vas.dtype == torch.int32 else 0) | (N.OUT_PFN if out_pfn else 0)
+    flags = (N.VA32 if vas.dtype == torch.int32 else 0) | (N.OUT_PFN if out_pfn else 0) | \
+        (N.CONCURRENT if concurrent else 0)
     if plan.two:
         flags |= N.HAS_TWO_STAGE
     if plan.four:
@@ -352,7 +403,8 @@ def translate_lanes(image, plan: TranslatePlan, vas, *, out_pfn: bool = False, o
             li.ensure(plan.host_spaces)
             plan._indexed = True
         li.sync_device_writes()
-        idx = ctypes.byref(li.abi())
+        idx_abi = li.abi()
+        idx = ctypes.byref(idx_abi)
     N.check(lib.pv_translate(dev_img.data_ptr(), image.nbytes, plan.spaces.data_ptr(), plan.segs.data_ptr(),
                              plan.n_segs, plan.n_chunks, vas.data_ptr(), flags, idx, value.data_ptr(),
                              status.data_ptr(), aux.data_ptr(), _stream().cuda_stream), "pv_translate")
@@ -608,31 +660,70 @@ def exec_hint(plan: "CopyPlan", buf_ptr: int) -> int:
     return N.COPY_ALIGNED16 if plan.aligned16(buf_ptr) else 0
 
 
-def _owner_map(image):
-    """Per-image conflict stamp map (one u64 per page) and epoch counter."""
-    import torch
+def _stream_key() -> int:
+    return _stream().cuda_stream
 
-    if getattr(image, "_owner", None) is None:
-        image._owner = torch.zeros(image.npages, dtype=torch.int64, device="cuda")
-        image._epoch = 0
-    image._epoch += 1
-    if image._epoch >= 1 << 24:
-        image._owner.zero_()
-        image._epoch = 1
-    return image._owner, image._epoch
+
+def _per_stream(obj, name: str, make):
+    """State of ``obj`` private to the current CUDA stream (created by
+    ``make()`` on first use).  Calls on one stream run in order and may reuse
+    it; calls on another stream (another host thread, SURVEY.md 8(b)
+    threading) never share it."""
+    table = obj.__dict__.setdefault("_per_stream_state", {})
+    key = (name, _stream_key())
+    st = table.get(key)
+    if st is None:
+        st = table[key] = make()
+    return st
+
+
+class OwnerMap:
+    """Conflict maps of one (image, stream): ``map`` holds one u64 per page,
+    the stamps (epoch << 40 | chunk + 1) of pv_copy_stamp; ``nodes`` one u32
+    per page, the table-node marks of pv_copy_plan_nodes.  Each to_guest
+    batch takes a new epoch, so neither map is cleared between batches."""
+
+    def __init__(self, npages: int):
+        import torch
+
+        self.map = torch.zeros(npages, dtype=torch.int64, device="cuda")
+        self.nodes = torch.zeros(npages, dtype=torch.int32, device="cuda")
+        self.npages = npages
+        self.epoch = 0
+
+    def next_epoch(self) -> int:
+        self.epoch += 1
+        if self.epoch >= 1 << 24:
+            self.map.zero_()
+            self.nodes.zero_()
+            self.epoch = 1
+        return self.epoch
+
+
+def _owner_map(image) -> OwnerMap:
+    """The current stream's conflict stamp map of ``image``."""
+    return _per_stream(image, "owner", lambda: OwnerMap(image.npages))
+
+
+class _Grow:
+    """A zero-filled device byte buffer that grows on demand."""
+
+    def __init__(self):
+        self.t = None
+
+    def get(self, need: int):
+        import torch
+
+        if self.t is None or self.t.numel() < need:
+            self.t = torch.zeros(max(need, 1), dtype=torch.uint8, device="cuda")
+        return self.t
 
 
 def _shim_scratch(image, n_pages: int):
-    """Per-image zero-filled scratch of pv_copy_shim (grown on demand; every
-    call leaves it zero-filled)."""
-    import torch
-
+    """The current stream's zero-filled scratch of pv_copy_shim for
+    ``image`` (grown on demand; every call leaves it zero-filled)."""
     need = int(N.lib().pv_copy_shim_scratch_bytes(n_pages))
-    cur = getattr(image, "_shim_scratch", None)
-    if cur is None or cur.numel() < need:
-        cur = torch.zeros(need, dtype=torch.uint8, device="cuda")
-        image._shim_scratch = cur
-    return cur
+    return _per_stream(image, "shim", _Grow).get(need)
 
 
 def copy_launch(image, plan: CopyPlan, direction: int, buf, *, fifo_dev=None, fifo_cap: int = 10,
@@ -644,6 +735,13 @@ def copy_launch(image, plan: CopyPlan, direction: int, buf, *, fifo_dev=None, fi
     another stream; only the exec waits for it, the plan passes overlap it.
     ``buf_bytes`` (default ``buf.numel()``): bytes of ``buf`` the ops may
     touch; chunks reaching past it move only what the buffer holds."""
+    with image._lock:  # enqueue atomically w.r.t. MemoryImage.pull (threads)
+        _copy_launch(image, plan, direction, buf, fifo_dev, fifo_cap, detect_conflicts, track_dirty, buf_ready,
+                     buf_bytes)
+
+
+def _copy_launch(image, plan, direction, buf, fifo_dev, fifo_cap, detect_conflicts, track_dirty, buf_ready,
+                 buf_bytes) -> None:
     lib = N.lib()
     dev_img = image.device()
     s = _stream().cuda_stream
@@ -653,10 +751,22 @@ def copy_launch(image, plan: CopyPlan, direction: int, buf, *, fifo_dev=None, fi
     plan.results.zero_()
     plan.conflict.zero_()
     if plan.n_pages:
-        N.check(lib.pv_copy_plan(dev_img.data_ptr(), image.nbytes, plan.spaces.data_ptr(), plan.ops.data_ptr(),
-                                 plan.n_ops, plan.page_off.data_ptr(), plan.n_pages, direction,
-                                 plan.page_hpa.data_ptr(), plan.page_status.data_ptr(), plan.page_aux.data_ptr(),
-                                 plan.first_bad.data_ptr(), None, 0, None, s), "pv_copy_plan")
+        stamp = direction == N.TO_GUEST and detect_conflicts
+        if stamp:
+            # a to_guest batch marks the table nodes its walks read: a chunk
+            # landing on one is a table hazard (pv_copy_plan_nodes)
+            owner = _owner_map(image)
+            epoch = owner.next_epoch()
+            N.check(lib.pv_copy_plan_nodes(dev_img.data_ptr(), image.nbytes, plan.spaces.data_ptr(),
+                                           plan.ops.data_ptr(), plan.n_ops, plan.page_off.data_ptr(), plan.n_pages,
+                                           plan.page_hpa.data_ptr(), plan.page_status.data_ptr(),
+                                           plan.page_aux.data_ptr(), plan.first_bad.data_ptr(),
+                                           owner.nodes.data_ptr(), owner.npages, epoch, s), "pv_copy_plan_nodes")
+        else:
+            N.check(lib.pv_copy_plan(dev_img.data_ptr(), image.nbytes, plan.spaces.data_ptr(), plan.ops.data_ptr(),
+                                     plan.n_ops, plan.page_off.data_ptr(), plan.n_pages, direction,
+                                     plan.page_hpa.data_ptr(), plan.page_status.data_ptr(), plan.page_aux.data_ptr(),
+                                     plan.first_bad.data_ptr(), None, 0, None, s), "pv_copy_plan")
         if plan.shims is not None:
             scratch = _shim_scratch(image, plan.n_pages)
             N.check(lib.pv_copy_shim(dev_img.data_ptr(), image.nbytes, plan.spaces.data_ptr(), plan.shims.data_ptr(),
@@ -679,11 +789,10 @@ def copy_launch(image, plan: CopyPlan, direction: int, buf, *, fifo_dev=None, fi
                                             plan.first_bad.data_ptr(), scratch.data_ptr(), nbytes, s),
                     "pv_copy_fifo_replay")
         abort = None
-        if direction == N.TO_GUEST and detect_conflicts:
-            owner, epoch = _owner_map(image)
+        if stamp:
             N.check(lib.pv_copy_stamp(plan.page_off.data_ptr(), plan.n_ops, plan.n_pages, plan.page_hpa.data_ptr(),
-                                      plan.first_bad.data_ptr(), owner.data_ptr(), image.npages, epoch,
-                                      plan.conflict.data_ptr(), s), "pv_copy_stamp")
+                                      plan.first_bad.data_ptr(), owner.map.data_ptr(), image.npages, epoch,
+                                      plan.conflict.data_ptr(), owner.nodes.data_ptr(), s), "pv_copy_stamp")
             abort = plan.conflict.data_ptr()
         dirty = image.dirty_map().data_ptr() if (direction == N.TO_GUEST and track_dirty) else None
         # batches whose buffer and guest pages are 16-byte co-aligned move
@@ -731,13 +840,13 @@ def copy_ordered(image, plan: CopyPlan, buf, buf_bytes: int | None = None) -> No
     dev_img = image.device()
     nbytes = int(lib.pv_copy_ordered_scratch_bytes(plan.n_pages, image.nbytes))
     scratch = torch.empty(max(nbytes, 1), dtype=torch.uint8, device="cuda")
-    N.check(lib.pv_copy_ordered(dev_img.data_ptr(), image.nbytes, plan.ops.data_ptr(), plan.n_ops,
-                                plan.page_off.data_ptr(), plan.n_pages, plan.page_hpa.data_ptr(),
-                                plan.page_status.data_ptr(), plan.page_aux.data_ptr(), plan.first_bad.data_ptr(),
-                                buf.data_ptr(), buf.numel() if buf_bytes is None else buf_bytes,
-                                plan.results.data_ptr(), image.dirty_map().data_ptr(),
-                                scratch.data_ptr(), nbytes, _stream().cuda_stream), "pv_copy_ordered")
-    image.note_device_write()
+    with image.writing():
+        N.check(lib.pv_copy_ordered(dev_img.data_ptr(), image.nbytes, plan.ops.data_ptr(), plan.n_ops,
+                                    plan.page_off.data_ptr(), plan.n_pages, plan.page_hpa.data_ptr(),
+                                    plan.page_status.data_ptr(), plan.page_aux.data_ptr(), plan.first_bad.data_ptr(),
+                                    buf.data_ptr(), buf.numel() if buf_bytes is None else buf_bytes,
+                                    plan.results.data_ptr(), image.dirty_map().data_ptr(),
+                                    scratch.data_ptr(), nbytes, _stream().cuda_stream), "pv_copy_ordered")
 
 
 def copy_ops(image, spaces: list[Space], ops: np.ndarray, direction: int, buf, *, caches=None, fifo_groups=None,
@@ -748,14 +857,22 @@ def copy_ops(image, spaces: list[Space], ops: np.ndarray, direction: int, buf, *
     state is replayed on the device and written back.  When the stamp pass
     finds two chunks of a to_guest batch writing one hpa page, the exec kernel
     stands down and the batch runs through the ordered path
-    (:func:`copy_ordered`), which reproduces last-writer-wins exactly.
+    (:func:`copy_ordered`), which reproduces last-writer-wins exactly.  When a
+    chunk would land on a page-table node the batch walks (a table hazard,
+    pv_copy_plan_nodes), nothing moves and the batch runs page by page in
+    program order instead (:func:`_copy_pagewise`).
     """
     cap = fifo_capacity(caches) if caches is not None else 10
     plan = CopyPlan(spaces, ops, fifo_groups=fifo_groups if caches is not None else None, shims=shims)
     fifo_dev = _to_dev(pack_fifo(caches)) if caches is not None else None
     copy_launch(image, plan, direction, buf, fifo_dev=fifo_dev, fifo_cap=cap, detect_conflicts=detect_conflicts,
                 buf_ready=buf_ready, buf_bytes=buf_bytes)
-    if direction == N.TO_GUEST and detect_conflicts and int(plan.conflict.item()):
+    conflict = int(plan.conflict.item()) if direction == N.TO_GUEST and detect_conflicts else 0
+    if conflict & N.CONFLICT_TABLE:
+        if plan.shims is not None and int(plan.shim_written.item()):
+            image.note_device_write()
+        return _copy_pagewise(image, spaces, plan.host_ops, direction, buf, caches, fifo_groups, shims, buf_bytes)
+    if conflict:
         copy_ordered(image, plan, buf, buf_bytes)
     results = decode_results(plan.results.cpu().numpy())
     if plan.shims is not None and int(plan.shim_written.item()):
@@ -765,16 +882,54 @@ def copy_ops(image, spaces: list[Space], ops: np.ndarray, direction: int, buf, *
     return results
 
 
+def _copy_pagewise(image, spaces, ops, direction, buf, caches, fifo_groups, shims, buf_bytes) -> list[OpOutcome]:
+    """A to_guest batch with a table hazard, one page at a time in program
+    order: each page is a one-chunk batch (translated -- through its
+    process's FIFO cache when there is one -- then written), so later pages
+    walk the tables earlier chunks wrote, exactly like copy_user_buffer
+    (memvirt.py:615-627).  With hybrid spaces (``shims``), the batch stops
+    at the first op whose page still traps after the device shim: the caller
+    finishes that op through the per-op shim and re-plans the rest."""
+    group_of = {}
+    if caches is not None:
+        for g, members in enumerate(fifo_groups):
+            for i in members:
+                group_of[int(i)] = g
+    out = []
+    stopped = False
+    for i, row in enumerate(np.asarray(ops, dtype=np.uint64).reshape(-1, 4)):
+        gva, length, off, sp = (int(x) for x in row)
+        if stopped:
+            out.append(OpOutcome(status=N.ST_OK, copied=0, value=0, aux=0, fail_page=0))
+            continue
+        g = group_of.get(i)
+        sub_caches = None if g is None else [caches[g]]
+        res = OpOutcome(status=N.ST_OK, copied=length, value=0, aux=0, fail_page=0)
+        done, k = 0, 0
+        while done < length:
+            cur = (gva + done) & U64
+            chunk = min(length - done, PAGE_SIZE - (cur & PAGE_MASK))
+            sub = np.array([[cur, chunk, off + done, 0]], dtype=np.uint64)
+            r = copy_ops(image, [spaces[sp]], sub, direction, buf, caches=sub_caches,
+                         fifo_groups=[[0]] if sub_caches is not None else None, detect_conflicts=False,
+                         shims=None if shims is None else [shims[sp]], buf_bytes=buf_bytes)[0]
+            if r.status != N.ST_OK:
+                res = OpOutcome(status=r.status, copied=done, value=r.value, aux=r.aux, fail_page=k)
+                stopped = shims is not None and kind(r.status) in (N.ST_TRAP, N.ST_TRAP2)
+                break
+            done += chunk
+            k += 1
+        out.append(res)
+    return out
+
+
 
 
 # ---- batched table construction (pv_map_plan / pv_map_commit) ------------------
 
 def _map_scratch(image):
-    import torch
-
-    if getattr(image, "_map_scratch", None) is None:
-        image._map_scratch = torch.empty(int(N.lib().pv_map_scratch_bytes()), dtype=torch.uint8, device="cuda")
-    return image._map_scratch
+    """The current stream's pv_map_plan scratch for ``image``."""
+    return _per_stream(image, "map", _Grow).get(int(N.lib().pv_map_scratch_bytes()))
 
 
 class TableBuild:
@@ -818,11 +973,11 @@ class TableBuild:
         pages = (self.base >> PAGE_SHIFT) + frames
         hot = image._maybe_nonzero[pages] if len(frames) else np.zeros(0, bool)
         hot_d = _to_dev(hot.astype(np.uint8)) if hot.any() else None
-        N.check(lib.pv_map_commit(dev.data_ptr(), image.nbytes, self.base, self.root, self.vas.data_ptr(),
-                                  self.vas.numel(), self.need.data_ptr(), None if fr is None else fr.data_ptr(),
-                                  len(frames), frame_off.data_ptr(), None if hot_d is None else hot_d.data_ptr(),
-                                  1 if data_first else 0, None if targets is None else targets.data_ptr(), target_add,
-                                  leaf_flags, None if out_data is None else out_data.data_ptr(),
-                                  image.dirty_map().data_ptr(), _stream().cuda_stream), "pv_map_commit")
-        image.note_device_write()
+        with image.writing():
+            N.check(lib.pv_map_commit(dev.data_ptr(), image.nbytes, self.base, self.root, self.vas.data_ptr(),
+                                      self.vas.numel(), self.need.data_ptr(), None if fr is None else fr.data_ptr(),
+                                      len(frames), frame_off.data_ptr(), None if hot_d is None else hot_d.data_ptr(),
+                                      1 if data_first else 0, None if targets is None else targets.data_ptr(), target_add,
+                                      leaf_flags, None if out_data is None else out_data.data_ptr(),
+                                      image.dirty_map().data_ptr(), _stream().cuda_stream), "pv_map_commit")
         image.host_epoch += 1  # table structure changed: leaf-index scans must look again

@@ -169,12 +169,16 @@ class _BatchMixin:
         # can resolve exactly (pv_copy_shim).  Any other trap changes the
         # shadow table for every later page on the host, so the batch is cut
         # at that op, which finishes through the per-op shim loop, and the
-        # rest is re-planned.
+        # rest is re-planned.  The device stops every op after the cut (no
+        # byte moves through the pre-shim tables); with a replaced trap_shim
+        # (device_shim None) nothing is fixed on the device and the first
+        # trapping op is the cut.
         results = []
         start = 0
+        shim = tr.device_shim or dp.NO_SHIM
         while start < len(rows):
             part = rows[start:]
-            outs = dp.copy_ops(image, [space], part, direction, buf, shims=[tr.device_shim], buf_ready=buf_ready)
+            outs = dp.copy_ops(image, [space], part, direction, buf, shims=[shim], buf_ready=buf_ready)
             cut = next((i for i, o in enumerate(outs) if dp.kind(o.status) in (N.ST_TRAP, N.ST_TRAP2)), None)
             upto = len(outs) if cut is None else cut
             for o, r in zip(outs[:upto], part[:upto]):

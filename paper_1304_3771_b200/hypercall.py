@@ -210,16 +210,20 @@ def _frame_error(status: int, ops_row=None):
 
 
 _SCRATCH: dict = {}
+_SCRATCH_LOCK = threading.Lock()
 
 
 def _cached(name: str, nbytes: int):
-    """Per-size device scratch reused across calls on the current stream."""
+    """Device scratch reused across calls on the current stream; every
+    stream (every host thread issuing on its own stream) has its own."""
     import torch
 
-    t = _SCRATCH.get(name)
-    if t is None or t.numel() < nbytes:
-        t = torch.empty(max(nbytes, 1), dtype=torch.uint8, device="cuda")
-        _SCRATCH[name] = t
+    key = (name, _stream())
+    with _SCRATCH_LOCK:
+        t = _SCRATCH.get(key)
+        if t is None or t.numel() < nbytes:
+            t = torch.empty(max(nbytes, 1), dtype=torch.uint8, device="cuda")
+            _SCRATCH[key] = t
     return t
 
 

@@ -20,10 +20,19 @@ Coherence is page-granular and lazy:
   the map and gathers exactly those pages back (``pv_gather_pages`` + one D2H).
 
 A timed data-plane loop therefore never synchronises with the host.
+
+Threads (calls on distinct streams are safe): every kernel
+launch that writes the image is enqueued under the image lock
+(:meth:`MemoryImage.writing`), which also records the writing stream's
+last event; :meth:`pull` holds the same lock, waits for every stream and
+then gathers, so no device write can slip between reading the dirty map
+and clearing it; the leaf index makes its stream wait for other streams'
+writes before re-encoding (:meth:`wait_writers`).
 """
 
 from __future__ import annotations
 
+import contextlib
 import threading
 
 import numpy as np
@@ -71,6 +80,7 @@ class MemoryImage:
         self.host_epoch = 0       # bumped by every push of host writes into HBM
         self.leaf_index = None    # dataplane.LeafIndex, created on first indexed translate
         self._lock = threading.RLock()
+        self._writers: dict = {}  # cuda stream handle -> event after its last image write
 
     @classmethod
     def adopt(cls, buf) -> "MemoryImage":
@@ -140,8 +150,39 @@ class MemoryImage:
         return self._dev_dirty
 
     def note_device_write(self) -> None:
-        self._dev_dirty_any = True
-        self.dev_write_epoch += 1
+        import torch
+
+        with self._lock:
+            stream = torch.cuda.current_stream()
+            if not torch.cuda.is_current_stream_capturing():
+                ev = self._writers.get(stream.cuda_stream)
+                if ev is None:
+                    ev = self._writers[stream.cuda_stream] = torch.cuda.Event()
+                ev.record(stream)
+            self._dev_dirty_any = True
+            self.dev_write_epoch += 1
+
+    @contextlib.contextmanager
+    def writing(self):
+        """Enqueue image-writing kernels inside this block: it holds the image
+        lock (so :meth:`pull` never interleaves with the enqueue) and notes
+        the device write after it."""
+        with self._lock:
+            yield
+            self.note_device_write()
+
+    def wait_writers(self) -> None:
+        """Make the current stream wait for every other stream's last image
+        write (no host synchronisation)."""
+        import torch
+
+        if torch.cuda.is_current_stream_capturing():
+            return  # a capture starts from a synchronised device (torch.cuda.graph)
+        with self._lock:
+            stream = torch.cuda.current_stream()
+            for handle, ev in self._writers.items():
+                if handle != stream.cuda_stream:
+                    stream.wait_event(ev)
 
     def push(self) -> None:
         """Scatter host-dirty pages into HBM."""
@@ -180,6 +221,9 @@ class MemoryImage:
                 return
             lib = _native.lib()
             stream = torch.cuda.current_stream()
+            # device writes of every stream (other host threads) land first;
+            # new ones cannot be enqueued while the lock is held
+            torch.cuda.synchronize()
             if self.leaf_index is not None:
                 self.leaf_index.sync_device_writes()  # before the dirty map is cleared
             dmap = self._dev_dirty.cpu().numpy()
@@ -196,6 +240,8 @@ class MemoryImage:
             self._dev_dirty.zero_()
             stream.synchronize()
             self._dev_dirty_any = False
+            if self.leaf_index is not None:
+                self.leaf_index.release_retired()  # every stream drained above
 
     def sync(self) -> None:
         """Make host and device agree (pull device writes, push host writes)."""

@@ -1271,9 +1271,9 @@ def _copy_foreign_translator(direction, gva, length, buf, translator, host_mem, 
             return copied, OutOfRange(f"access [{hpa:#x}, +{n}) beyond {host_mem.size_bytes:#x}")
         if direction == "to_guest":
             if n:
-                dev[start:start + n].copy_(buf[copied:copied + n])
-                image._dev_dirty[start >> PAGE_SHIFT:((start + n - 1) >> PAGE_SHIFT) + 1] = 1
-                image.note_device_write()
+                with image.writing():
+                    dev[start:start + n].copy_(buf[copied:copied + n])
+                    image._dev_dirty[start >> PAGE_SHIFT:((start + n - 1) >> PAGE_SHIFT) + 1] = 1
         else:
             buf[copied:copied + chunk].copy_(dev[start:start + chunk])
         copied += chunk

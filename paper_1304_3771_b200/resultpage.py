@@ -97,10 +97,10 @@ def encode_batch(host_mem, page_hpas, records) -> list[Exception | None]:
     hp = dp._to_dev((hpas + np.uint64(host_mem.base)).view(np.int64))
     of = dp._to_dev(offs.view(np.int64))
     status = torch.empty(n, dtype=torch.int32, device="cuda")
-    N.check(lib.pv_result_encode(dev.data_ptr(), image.nbytes, hp.data_ptr(), hdr.data_ptr(), buf.data_ptr(),
-                                 of.data_ptr(), n, status.data_ptr(), image.dirty_map().data_ptr(),
-                                 dp._stream().cuda_stream), "pv_result_encode")
-    image.note_device_write()
+    with image.writing():
+        N.check(lib.pv_result_encode(dev.data_ptr(), image.nbytes, hp.data_ptr(), hdr.data_ptr(), buf.data_ptr(),
+                                     of.data_ptr(), n, status.data_ptr(), image.dirty_map().data_ptr(),
+                                     dp._stream().cuda_stream), "pv_result_encode")
     out = []
     for i, st in enumerate(status.cpu().numpy().view(np.uint32).tolist()):
         if st == N.ST_OK:

@@ -20,6 +20,7 @@ import pytest
 import scenarios as S
 from conftest import load_json
 from oracle import oracle as O
+from paper_1304_3771_b200 import dataplane as dp
 from paper_1304_3771_b200 import errors as er
 from paper_1304_3771_b200 import has as be
 from paper_1304_3771_b200 import memvirt as mv
@@ -166,5 +167,5 @@ def test_shim_trap_free_batch_unchanged(c4hw):
     gva = W.C1_GVA + int(ok[0]) * 4096
     out = acc.copy_to_user_batch([gva], [100], b"x" * 100)
     assert out == [100]
-    scratch = getattr(img, "_shim_scratch", None)
-    assert scratch is not None and int(scratch[:16].sum()) == 0
+    scratch = dp._per_stream(img, "shim", dp._Grow).t  # the current stream's scratch
+    assert scratch is not None and int(scratch[:24].sum()) == 0
