@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import argparse
 import ctypes
+import hashlib
 import json
 import os
 import statistics
@@ -54,8 +55,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true", help="skip the full-size parity check against the oracle "
                     "after the timed steps")
-    ap.add_argument("--serial-step", action="store_true", help="time C5/C1 steps with the walk and the copy "
-                    "phases back to back (default: the walk on a second stream beside plan + exec)")
+    ap.add_argument("--overlap", action="store_true", help="time C5/C1 steps with the walk on a second stream "
+                    "beside plan + exec (A/B option: measured slower than back-to-back phases, "
+                    "profiles/r02_overlap_ab.md)")
     ap.add_argument("--no-graph", action="store_true", help="launch the C5 step phases eagerly instead of "
                     "replaying CUDA graphs of them")
     ap.add_argument("--cpu-sample-vas", type=int, default=16 << 20)
@@ -159,19 +161,25 @@ class Workload:
         if name == "c5":
             cfg = W.C5Config() if scale == 1 else W.C5Config().scaled(scale)
             self.cfg = cfg
-            wd = W.build_c5(cfg, device=True)  # tables built in HBM (pv_map_*)
-            self.world = wd
-            self.memv = wd.memv
             owned = shard.owned_guests(cfg.guests, rank, world)
             self.owned = owned
+            # a rank of an N-rank job holds the host-private region + its own guests' slots in HBM
+            # (pv_image_create); one rank holds everything
+            wd = W.build_c5(cfg, device=True, resident_guests=owned if world > 1 else None)
+            self.world = wd
+            self.memv = wd.memv
             t_spaces, bounds, vas_parts, self.proc_vas = [], [], [], []
+            self.proc_lane0 = []  # global lane offset of every (guest, process) batch: guest order, then process
             lane = 0
             for g in owned:
+                g0 = g * cfg.vas_per_guest
                 for p, v in enumerate(W.c5_vas(cfg, g)):
                     t_spaces.append(W.c5_shadow_space(wd, g, p))
                     bounds.append((lane, lane + len(v), len(t_spaces) - 1))
                     vas_parts.append(v)
                     self.proc_vas.append((g, p, v))
+                    self.proc_lane0.append(g0)
+                    g0 += len(v)
                     lane += len(v)
             self.n_vas = lane
             self.total_vas = cfg.guests * cfg.vas_per_guest
@@ -197,20 +205,28 @@ class Workload:
             self.owned = [0]
             tr = memv.translator(space, use_cache=False)
             t_spaces = [tr.device_space]
-            v = W.c1_vas().astype(np.uint32)
+            v_all = W.c1_vas().astype(np.uint32)
+            # one guest, one process: the VA range splits evenly over the ranks (the
+            # image is replicated, walks are read-only) and the 64 MiB copy_to_user into page-aligned,
+            # disjoint destination ranges, each written by exactly one rank
+            lo, hi = len(v_all) * rank // world, len(v_all) * (rank + 1) // world
+            v = v_all[lo:hi]
             vas_parts = [v]
             bounds = [(0, len(v), 0)]
-            # one guest, one process: at N > 1 every rank runs its own replica of the batch
             self.n_vas = len(v)
-            self.total_vas = len(v) * world
+            self.total_vas = len(v_all)
             self.proc_vas = [(0, 0, v)]
+            self.proc_lane0 = [lo]
             c_spaces = [tr.device_space]
             c_shims = None
-            n = 64 << 20
-            ops_all = np.array([[W.C1_GVA, n, 0, 0]], dtype=np.uint64)
+            total = 64 << 20
+            pages = total // 4096
+            p0, p1 = pages * rank // world, pages * (rank + 1) // world
+            n = (p1 - p0) * 4096
+            ops_all = np.array([[W.C1_GVA + p0 * 4096, n, 0, 0]], dtype=np.uint64)
             self.proc_ops = [(0, 0, ops_all[:, :2], np.zeros(1, np.uint64))]
             self.copy_bytes = n
-            self.total_copy_bytes = n * world
+            self.total_copy_bytes = total
             self.c1_space = space
         self.build_s = time.time() - t0
         self.image = self.memv.host_mem.backing
@@ -356,7 +372,7 @@ def run_ours(args, rank, world, local):
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
-    overlap = not args.serial_step
+    overlap = args.overlap
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
     ovs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     t_start = torch.cuda.Event(enable_timing=True)
@@ -445,9 +461,11 @@ def run_ours(args, rank, world, local):
                  "copy_gbs": wl.total_copy_bytes * K / (total_ms / 1e3) / 1e9,
                  "walk_ms_in_overlap": None if ov_walk_ms is None else ov_walk_ms / K,
                  "hbm_floor_ms": (2 * wl.copy_bytes + walk_bytes + 8 * _leaf_ptes(wl)) / (peak * 1e6),
-                 "note": "ms_per_step = one step with the walk on a second stream beside plan + exec "
-                         "(PV_CONCURRENT: one walker CTA per SM next to the exec's); value, copy and the "
-                         "rooflines come from K more steps with the phases back to back (serial_ms)"},
+                 "note": ("ms_per_step = one step with the walk on a second stream beside plan + exec "
+                          "(PV_CONCURRENT: one walker CTA per SM next to the exec's); value, copy and the "
+                          "rooflines come from K more steps with the phases back to back (serial_ms)")
+                 if overlap else ("phases back to back (--overlap puts the walk beside plan + exec: both "
+                                  "need every SM's L2 request port, measured slower, profiles/r02_overlap_ab.md)")},
         "per_step": spread,
         "roofline": {"bound": "hbm",
                      "kernel": "pv_copy_exec (" + ("exec_bulk_kernel, TMA" if hint else "exec_kernel, LSU") + ")",
@@ -470,6 +488,9 @@ def run_ours(args, rank, world, local):
         "faulting_lanes": n_faults,
         "parity": parity,
         "gather_to_rank0": gather,
+        "hbm_image": {"image_bytes": img.nbytes, "device_bytes": img.device_bytes,
+                      "resident": "all" if not img.partial else
+                      "host-private region + owned guests' slots (pv_image_create) + one shared hole"},
         "gpu_launches": (4 + (1 if wl.n_vas >= 8 * 296 * 2048 else 0) + 1
                          + (2 if wl.cplan.shims is not None else 0)) * K,
         "launch": launch_mode,
@@ -594,10 +615,16 @@ def gather_results(wl, rank, world):
     dt = time.perf_counter() - t0
     (dt,) = shard.max_over_ranks([dt], world, device="cuda")
     nbytes = cfg.guests * cfg.vas_per_guest * 12
-    ok = None
+    ok = digest = None
     if rank == 0:
         ok = sorted(got) == list(range(cfg.guests))
-    return {"ms": dt * 1e3, "bytes": nbytes, "remote_bytes": nbytes * (world - 1) // world, "complete": ok}
+        h = hashlib.sha256()
+        for g in range(cfg.guests):  # every guest's results, in guest order (equal at any N)
+            h.update(got[g]["value"].cpu().numpy().tobytes())
+            h.update(got[g]["status"].cpu().numpy().tobytes())
+        digest = h.hexdigest()
+    return {"ms": dt * 1e3, "bytes": nbytes, "remote_bytes": nbytes * (world - 1) // world, "complete": ok,
+            "digest": digest}
 
 
 def c2_device_payload(lens: np.ndarray):
@@ -1064,13 +1091,27 @@ def run_e2e(wl, args, world):
     from paper_1304_3771_b200 import memvirt as mv
 
     io = {}
+    # results: one PV_OUT_PACKED word per lane (the hpa, or the status and value of the exception the
+    # lane raises).  At N > 1 the words of every rank land in one host buffer all ranks map
+    # (shard.SharedHostBuffer): rank 0 holds every guest's results after the step's barrier.
+    shared = None
+    pg = world > 1 and _pg()
+    if pg:
+        from paper_1304_3771_b200 import shard as _sh
+
+        shared = _sh.SharedHostBuffer(wl.total_vas * 8, int(os.environ.get("RANK", "0")), world, tag="pv_e2e")
+        outs = [(shared.view(torch.int64, l0, len(v)), None, None)
+                for l0, (_, _, v) in zip(wl.proc_lane0, wl.proc_vas)]
+    else:
+        outs = None
 
     def one_step():
         t0 = time.perf_counter()
-        mv.translate_many([(translators[(g, p)], t) for t, g, p in host_vas])
+        io["res"] = mv.translate_many([(translators[(g, p)], t) for t, g, p in host_vas], packed=True, out=outs)
+        if pg:
+            tdist.barrier()  # every rank's words are in the shared buffer: rank 0 holds all results
         t1 = time.perf_counter()
-        # counted from the tensors moved: VAs in; values + per-chunk fault flags (+ the statuses of
-        # chunks that faulted) out -- see dataplane.translate_host_many
+        # counted from the tensors moved: VAs in; one lane word out -- see dataplane.translate_host_many
         io["h2d"], io["d2h"] = dp.last_host_io["h2d"], dp.last_host_io["d2h"]
         for t, g, p, ops in payload:
             outs = recs[(g, p)].copy_to_user_batch(ops[:, 0], ops[:, 1], t)
@@ -1093,10 +1134,42 @@ def run_e2e(wl, args, world):
     tr_s, cp_s = shard.max_over_ranks([tr_s, cp_s], world, device="cuda")
     h2d = io["h2d"] + sum(t.numel() for t, *_ in payload)
     d2h = io["d2h"] + sum(len(ops) * 32 for *_, ops in payload)
+    # the lane words delivered to the host decode to the device-resident results of the timed step
+    # (which verify_parity checked against the oracle)
+    dev_v = wl.out[0].cpu().numpy().view(np.uint64)
+    dev_s = wl.out[1].cpu().numpy().view(np.uint32)
+    lane, same = 0, True
+    for (words, _, aux), (_, _, v) in zip(io["res"], wl.proc_vas):
+        uv, us = dp.unpack_lanes(words.numpy(), None if aux.stride(0) == 0 else aux.numpy())
+        same &= bool(np.array_equal(uv, dev_v[lane:lane + len(v)]) and np.array_equal(us, dev_s[lane:lane + len(v)]))
+        lane += len(v)
+    returned = None
+    if pg:
+        # the words rank 0 reads in the shared buffer are every rank's own results
+        mine = hashlib.sha256()
+        for l0, (_, _, v) in zip(wl.proc_lane0, wl.proc_vas):
+            mine.update(shared.view(torch.int64, l0, len(v)).numpy().tobytes())
+        got = [None] * world
+        tdist.all_gather_object(got, (mine.hexdigest(), list(zip(wl.proc_lane0, [len(v) for *_, v in wl.proc_vas]))))
+        ok = None
+        if int(os.environ.get("RANK", "0")) == 0:
+            ok = True
+            for digest, spans in got:
+                h = hashlib.sha256()
+                for l0, n in spans:
+                    h.update(shared.view(torch.int64, l0, n).numpy().tobytes())
+                ok &= h.hexdigest() == digest
+        returned = {"to_rank0": "shared host buffer (/dev/shm, cudaHostRegister'd by every rank): each rank's "
+                                "D2H writes its guests' lane words where rank 0 reads them; one barrier per step",
+                    "bytes": wl.total_vas * 8, "verified": ok}
+        shared.close()
     return {"value": wl.total_vas * steps / tr_s, "unit": "translations/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "copy": {"value": wl.total_copy_bytes * steps / cp_s / 1e9, "unit": "GB/s"},
-            "steps": steps, "api": "memvirt.translate_many (ProcessTranslator.translate_batch over every process) + "
+            "steps": steps, "results": "one PV_OUT_PACKED word per lane (hpa, or status + value)",
+            "lanes_equal_device_results": same,
+            "gather_to_rank0": returned,
+            "api": "memvirt.translate_many(packed=True) (ProcessTranslator.translate_batch over every process) + "
                    "HardwareHasAccess.copy_to_user_batch"}
 
 

@@ -141,6 +141,8 @@ int pv_index_encode(const uint8_t* image, uint64_t image_bytes,
 #define PV_VA32 0x1u    /* vas is uint32_t[] (else uint64_t[])             */
 #define PV_OUT_PFN 0x2u /* value = leaf pfn (walk); else address with the
                            page offset of the va (translate / resolve)     */
+#define PV_OUT_PACKED 0x8u /* one u64 per lane in out_value (out_status may be
+                              NULL): see pv_translate */
 #define PV_CONCURRENT 0x4u /* size the walk for a kernel running beside it:
                               one CTA per SM (the rest of each SM's
                               registers and shared memory stay free) */
@@ -209,7 +211,20 @@ const char* pv_status_name(uint32_t status);
  * build per-segment stage tables in library-internal scratch taken from the
  * device's default stream-ordered pool (cudaMallocAsync / cudaFreeAsync on
  * `stream`, 16.5 KiB per segment; the pool keeps up to 256 MiB cached).
+ *
+ * PV_OUT_PACKED: out_value[i] carries the whole lane result (8 bytes instead
+ * of 12 to store and to move to the host): a lane that translated is its
+ * value (an hpa / pfn, below 2^40), any other lane is PV_PACKED_ERR | compact
+ * status << 42 | value, compact status = (status & 0xFFF) | index << 12
+ * (21 bits; index = status >> 16).  A value that needs more than 42 bits (a
+ * TDP-stage fault gpa from a wild guest PTE, a u64 VA) is written to
+ * out_aux[i] and the lane's low 42 bits read PV_PACKED_SPILL_VALUE; out_aux
+ * must then be non-NULL unless the batch is PV_VA32 and one-stage (those
+ * never spill).  out_status is not written and may be NULL.
  */
+#define PV_PACKED_ERR (1ull << 63)
+#define PV_PACKED_VALUE_BITS 42
+#define PV_PACKED_SPILL_VALUE ((1ull << 42) - 1)
 int pv_translate(const uint8_t* image, uint64_t image_bytes,
                  const pv_space* spaces, const pv_seg* segs, uint32_t n_segs,
                  uint64_t n_chunks, const void* vas, uint32_t flags,
@@ -396,6 +411,21 @@ typedef struct pv_small_result {
 } pv_small_result;
 int pv_copy_small(uint8_t* image, uint64_t image_bytes, const pv_small_op* op /* host */, uint8_t* buf,
                   uint64_t buf_bytes, pv_small_result* out, uint8_t* dirty, uint64_t seq, void* stream);
+
+/* ---- per-rank residency ------------------------------------
+ * A zero-filled device image of image_bytes whose byte offsets are the
+ * reference's hpas (memvirt.py:433-480 slot carving), with HBM behind only
+ * the byte ranges [ranges[2i], ranges[2i+1]) (host array; widened to the
+ * VMM granularity, 2 MiB).  Every other page is backed by one shared
+ * zero-filled hole of hole_bytes (0: 256 MiB) mapped repeatedly, so a stray
+ * access reads junk instead of faulting.  One reserved virtual range: every
+ * kernel addresses it like a flat allocation.  *out_device_bytes = HBM
+ * actually allocated (resident ranges + hole).  Replaces the flat image
+ * allocation of a guest-sharded rank (each GPU holds the host-private region
+ * and its own guests' slots). */
+int pv_image_create(uint64_t image_bytes, const uint64_t* ranges, uint32_t n_ranges, uint64_t hole_bytes,
+                    uint8_t** out_ptr, void** out_handle, uint64_t* out_device_bytes);
+int pv_image_destroy(void* handle);
 
 /* Host-mapped pinned memory (cudaHostAllocMapped | Portable): the device
  * reads and writes it through the same pointer (UVA). */

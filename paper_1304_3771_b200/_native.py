@@ -42,6 +42,10 @@ FLAG_PS = 0x80
 VA32 = 0x1
 OUT_PFN = 0x2
 CONCURRENT = 0x4  # pv.h PV_CONCURRENT: one walker CTA per SM
+OUT_PACKED = 0x8  # pv.h PV_OUT_PACKED: one u64 per lane
+PACKED_ERR = 1 << 63
+PACKED_VALUE_BITS = 42
+PACKED_SPILL_VALUE = (1 << 42) - 1
 HAS_TWO_STAGE = 0x80000000
 HAS_4L = 0x40000000
 
@@ -74,7 +78,7 @@ EXPORTS = (
     "pv_result_decode", "pv_timing", "pv_timing_ms", "pv_copy_shim_scratch_bytes", "pv_copy_shim",
     "pv_map_scratch_bytes", "pv_map_plan", "pv_map_commit",
     "pv_frame_pack", "pv_frame_identify", "pv_frame_assemble_scratch_bytes", "pv_frame_assemble",
-    "pv_walk_one", "pv_copy_small", "pv_host_alloc", "pv_host_free",
+    "pv_walk_one", "pv_copy_small", "pv_host_alloc", "pv_host_free", "pv_image_create", "pv_image_destroy",
 )
 
 _u64 = ctypes.c_uint64
@@ -116,6 +120,8 @@ _SIGNATURES = {
     "pv_timing_ms": (ctypes.c_double, [ctypes.c_char_p, _p]),
     "pv_walk_one": (ctypes.c_int, [_p, _u64, _p, _u64, _u32, _p, _u64, _p]),
     "pv_copy_small": (ctypes.c_int, [_p, _u64, _p, _p, _u64, _p, _p, _u64, _p]),
+    "pv_image_create": (ctypes.c_int, [_u64, _p, _u32, _u64, _p, _p, _p]),
+    "pv_image_destroy": (ctypes.c_int, [_p]),
     "pv_host_alloc": (_p, [_u64]),
     "pv_host_free": (None, [_p]),
 }

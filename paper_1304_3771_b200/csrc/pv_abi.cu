@@ -222,15 +222,19 @@ int pv_translate(const uint8_t* image, uint64_t image_bytes, const pv_space* spa
                  uint32_t n_segs, uint64_t n_chunks, const void* vas, uint32_t flags, const pv_index* index,
                  uint64_t* out_value, uint32_t* out_status, uint64_t* out_aux, void* stream) {
   if (n_chunks == 0) return PV_SUCCESS;
-  if (!image || !spaces || !segs || !vas || !out_value || !out_status || n_segs == 0) return PV_EINVAL;
+  const bool packed = flags & PV_OUT_PACKED;
+  if (!image || !spaces || !segs || !vas || !out_value || (!out_status && !packed) || n_segs == 0) return PV_EINVAL;
   if (image_bytes % kPageSize) return PV_EINVAL;
   // 4-byte walk codes carry leaf pfns in 28 bits (pv_translate.cu stage_codes)
   if (image_bytes >= (1ull << 40)) return PV_EINVAL;
-  if (flags & ~(uint32_t)(PV_VA32 | PV_OUT_PFN | PV_CONCURRENT | PV_HAS_TWO_STAGE | PV_HAS_4L)) return PV_EINVAL;
+  if (flags & ~(uint32_t)(PV_VA32 | PV_OUT_PFN | PV_OUT_PACKED | PV_CONCURRENT | PV_HAS_TWO_STAGE | PV_HAS_4L))
+    return PV_EINVAL;
   const bool two = flags & PV_HAS_TWO_STAGE;
+  // packed lanes spill wide values into out_aux (only u64 VAs, TDP stages and 4-level walks can)
+  if (packed && !out_aux && (!(flags & PV_VA32) || two || (flags & PV_HAS_4L))) return PV_EINVAL;
   if (index != nullptr && (!index->slot_of || !index->leaf_codes || !index->slot_page)) return PV_EINVAL;
   return rc(launch_translate(image, image_bytes, spaces, segs, n_segs, n_chunks, vas,
-                             flags & (PV_VA32 | PV_OUT_PFN | PV_CONCURRENT | PV_HAS_4L), two, index,
+                             flags & (PV_VA32 | PV_OUT_PFN | PV_OUT_PACKED | PV_CONCURRENT | PV_HAS_4L), two, index,
                              out_value, out_status, out_aux, (cudaStream_t)stream));
 }
 

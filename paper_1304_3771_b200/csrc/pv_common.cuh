@@ -201,6 +201,21 @@ __device__ __forceinline__ uint32_t translate_global(const uint8_t* __restrict__
   return PV_ST_OK;
 }
 
+// PV_OUT_PACKED lane word (pv.h): the value when the lane translated, else
+// PV_PACKED_ERR | compact status << 42 | value (a value wider than 42 bits
+// spills: *spill is set and the low bits read PV_PACKED_SPILL_VALUE).
+__device__ __forceinline__ uint64_t pack_lane(uint32_t st, uint64_t v, bool* spill) {
+  *spill = false;
+  if (st == PV_ST_OK) return v;
+  const uint64_t compact = (uint64_t)((st & 0xFFFu) | (((st >> 16) & 0x1FFu) << 12));
+  uint64_t low = v;
+  if (v >> PV_PACKED_VALUE_BITS) {
+    *spill = true;
+    low = PV_PACKED_SPILL_VALUE;
+  }
+  return PV_PACKED_ERR | (compact << PV_PACKED_VALUE_BITS) | low;
+}
+
 __host__ __device__ __forceinline__ uint64_t page_span(uint64_t gva, uint64_t len) {
   return len == 0 ? 0 : ((gva + len - 1) >> kPageShift) - (gva >> kPageShift) + 1;
 }

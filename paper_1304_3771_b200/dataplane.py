@@ -371,13 +371,37 @@ class TranslatePlan:
             self._indexed = True
 
 
-def translate_lanes(image, plan: TranslatePlan, vas, *, out_pfn: bool = False, out=None, concurrent: bool = False):
+def unpack_lanes(packed, aux=None) -> tuple[np.ndarray, np.ndarray]:
+    """(value uint64, status uint32) of PV_OUT_PACKED lane words (pv.h):
+    a word without PV_PACKED_ERR is the value of a lane that translated;
+    otherwise bits 42-62 hold the compact status and bits 0-41 the value, or
+    PV_PACKED_SPILL_VALUE when the value was wider and lives in ``aux``."""
+    w = np.asarray(packed).view(np.uint64)
+    err = (w >> np.uint64(63)).astype(bool)
+    compact = ((w >> np.uint64(N.PACKED_VALUE_BITS)) & np.uint64(0x1FFFFF)).astype(np.uint32)
+    status = np.where(err, (compact & np.uint32(0xFFF)) | ((compact >> np.uint32(12)) << np.uint32(16)),
+                      np.uint32(0)).astype(np.uint32)
+    low = w & np.uint64(N.PACKED_SPILL_VALUE)
+    value = np.where(err, low, w)
+    spill = err & (low == np.uint64(N.PACKED_SPILL_VALUE))
+    if spill.any():
+        if aux is None:
+            raise ValueError("spilled lanes need the aux array")
+        value = value.copy()
+        value[spill] = np.asarray(aux).view(np.uint64)[spill]
+    return value, status
+
+
+def translate_lanes(image, plan: TranslatePlan, vas, *, out_pfn: bool = False, out=None, concurrent: bool = False,
+                    packed: bool = False):
     """Translate every lane of ``vas`` (int64 or int32 cuda tensor).
 
     Returns ``(value int64, status int32, aux int64)`` device tensors, written
     asynchronously on the current stream.  ``out`` may pass preallocated
     tensors of the same shapes.  ``concurrent``: the walk shares the GPU with
     a kernel on another stream (pv.h PV_CONCURRENT, one CTA per SM).
+    ``packed``: value holds PV_OUT_PACKED lane words (:func:`unpack_lanes`)
+    and status is None.
     """
     import torch
 
@@ -386,12 +410,12 @@ def translate_lanes(image, plan: TranslatePlan, vas, *, out_pfn: bool = False, o
     n = vas.numel()
     if out is None:
         value = torch.empty(n, dtype=torch.int64, device="cuda")
-        status = torch.empty(n, dtype=torch.int32, device="cuda")
+        status = None if packed else torch.empty(n, dtype=torch.int32, device="cuda")
         aux = torch.zeros(n, dtype=torch.int64, device="cuda")
     else:
         value, status, aux = out
     flags = (N.VA32 if vas.dtype == torch.int32 else 0) | (N.OUT_PFN if out_pfn else 0) | \
-        (N.CONCURRENT if concurrent else 0)
+        (N.CONCURRENT if concurrent else 0) | (N.OUT_PACKED if packed else 0)
     if plan.two:
         flags |= N.HAS_TWO_STAGE
     if plan.four:
@@ -407,7 +431,8 @@ def translate_lanes(image, plan: TranslatePlan, vas, *, out_pfn: bool = False, o
         idx = ctypes.byref(idx_abi)
     N.check(lib.pv_translate(dev_img.data_ptr(), image.nbytes, plan.spaces.data_ptr(), plan.segs.data_ptr(),
                              plan.n_segs, plan.n_chunks, vas.data_ptr(), flags, idx, value.data_ptr(),
-                             status.data_ptr(), aux.data_ptr(), _stream().cuda_stream), "pv_translate")
+                             None if status is None else status.data_ptr(),
+                             None if aux is None else aux.data_ptr(), _stream().cuda_stream), "pv_translate")
     return value, status, aux
 
 
@@ -421,13 +446,19 @@ def translate_host_pipelined(image, space: Space, host_vas, chunk: int = 1 << 23
 last_host_io = {"h2d": 0, "d2h": 0}
 
 
-def translate_host_many(image, jobs, chunk: int = 1 << 23):
+def translate_host_many(image, jobs, chunk: int = 1 << 23, *, packed: bool = False, out=None):
     """Translate several host VA tensors (``jobs = [(space, vas), ...]``) in
     one pipeline: chunks of every job stream through two device buffer sets,
     H2D of chunk i+1 and D2H of chunk i-1 run on side streams while chunk i
     translates, one synchronisation at the end.  Returns per job pinned
     ``(value int64, status int32, aux int64)``; ``aux`` only travels for
-    two-stage spaces (one-stage walks never produce a TDP-stage trap)."""
+    two-stage spaces (one-stage walks never produce a TDP-stage trap).
+
+    ``packed``: per job ``(words int64, None, aux)`` with one PV_OUT_PACKED
+    word per lane (8 bytes back instead of 12; :func:`unpack_lanes`); aux
+    travels for two-stage spaces and u64 VAs (spilled values).  ``out``: per
+    job the pinned host tensors to fill (e.g. views of a buffer shared with
+    another process); ``None`` entries are allocated."""
     import torch
 
     outs, work = [], []
@@ -439,22 +470,28 @@ def translate_host_many(image, jobs, chunk: int = 1 << 23):
         if host_vas.dtype == torch.int64:
             dtype = torch.int64
         srcs.append((space, host_vas))
-    for space, host_vas in srcs:
+    for k, (space, host_vas) in enumerate(srcs):
         src = host_vas if host_vas.dtype == dtype else host_vas.to(dtype)
         if not src.is_pinned():
             src = src.pin_memory()
         n = src.numel()
         two = space.mode == N.TWO_STAGE
-        value = torch.empty(n, dtype=torch.int64, pin_memory=True)
-        status = torch.empty(n, dtype=torch.int32, pin_memory=True)
+        need_aux = two or (packed and dtype == torch.int64)
+        given = out[k] if out is not None and out[k] is not None else (None, None, None)
+        value = given[0] if given[0] is not None else torch.empty(n, dtype=torch.int64, pin_memory=True)
+        status = None if packed else (given[1] if given[1] is not None else
+                                      torch.empty(n, dtype=torch.int32, pin_memory=True))
         # one-stage walks never produce a TDP-stage trap: aux is identically 0
-        aux = torch.empty(n, dtype=torch.int64, pin_memory=True) if two else \
-            torch.zeros(1, dtype=torch.int64).expand(n)
+        if need_aux:
+            aux = given[2] if given[2] is not None else torch.empty(n, dtype=torch.int64, pin_memory=True)
+        else:
+            aux = torch.zeros(1, dtype=torch.int64).expand(n)
         outs.append((value, status, aux))
         for start in range(0, n, chunk):
-            work.append((space, two, src, value, status, aux, start, min(chunk, n - start)))
+            work.append((space, need_aux, src, value, status, aux, start, min(chunk, n - start)))
+    per_lane_out = 8 if packed else 12
     last_host_io["h2d"] = sum(w[2].element_size() * w[7] for w in work)
-    last_host_io["d2h"] = sum(w[7] * (20 if w[1] else 12) for w in work)  # value + status (+ aux)
+    last_host_io["d2h"] = sum(w[7] * (per_lane_out + (8 if w[1] else 0)) for w in work)  # value (+ status) (+ aux)
     if not work:
         return outs
     compute = torch.cuda.current_stream()
@@ -463,9 +500,10 @@ def translate_host_many(image, jobs, chunk: int = 1 << 23):
     bufs = []
     for _ in range(2):
         bufs.append((torch.empty(chunk, dtype=dtype, device="cuda"), torch.empty(chunk, dtype=torch.int64, device="cuda"),
-                     torch.empty(chunk, dtype=torch.int32, device="cuda"), torch.zeros(chunk, dtype=torch.int64, device="cuda"),
+                     None if packed else torch.empty(chunk, dtype=torch.int32, device="cuda"),
+                     torch.zeros(chunk, dtype=torch.int64, device="cuda"),
                      torch.cuda.Event(), torch.cuda.Event(), torch.cuda.Event()))
-    for i, (space, two, src, value, status, aux, start, m) in enumerate(work):
+    for i, (space, need_aux, src, value, status, aux, start, m) in enumerate(work):
         d_vas, d_val, d_st, d_aux, ev_in, ev_done, ev_out = bufs[i % 2]
         if i >= 2:
             h2d.wait_event(ev_out)  # buffers of chunk i-2 fully drained
@@ -475,15 +513,17 @@ def translate_host_many(image, jobs, chunk: int = 1 << 23):
         compute.wait_event(ev_in)
         if (space, m) not in plans:
             plans[(space, m)] = TranslatePlan([space], [(0, m, 0)], image=image)
-        if two:
+        if need_aux:
             d_aux[:m].zero_()
-        translate_lanes(image, plans[(space, m)], d_vas[:m], out=(d_val[:m], d_st[:m], d_aux[:m]))
+        translate_lanes(image, plans[(space, m)], d_vas[:m],
+                        out=(d_val[:m], None if packed else d_st[:m], d_aux[:m]), packed=packed)
         ev_done.record(compute)
         d2h.wait_event(ev_done)
         with torch.cuda.stream(d2h):
             value[start:start + m].copy_(d_val[:m], non_blocking=True)
-            status[start:start + m].copy_(d_st[:m], non_blocking=True)
-            if two:
+            if not packed:
+                status[start:start + m].copy_(d_st[:m], non_blocking=True)
+            if need_aux:
                 aux[start:start + m].copy_(d_aux[:m], non_blocking=True)
             ev_out.record(d2h)
     d2h.synchronize()

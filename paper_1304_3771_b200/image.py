@@ -79,6 +79,10 @@ class MemoryImage:
         self.dev_write_epoch = 0  # bumped by every device write (leaf-index coherence)
         self.host_epoch = 0       # bumped by every push of host writes into HBM
         self.leaf_index = None    # dataplane.LeafIndex, created on first indexed translate
+        self._resident = None     # per-page bool mask of the pages held in HBM (None: all)
+        self._res_ranges = None   # the resident byte ranges
+        self._vmm = None          # pv_image_create handle of a partially resident image
+        self.device_bytes = 0     # HBM held by the device image
         self._lock = threading.RLock()
         self._writers: dict = {}  # cuda stream handle -> event after its last image write
 
@@ -93,6 +97,73 @@ class MemoryImage:
 
     def __len__(self) -> int:
         return self.nbytes
+
+    # ---- residency (guest-sharded ranks) --------------------
+    def set_residency(self, ranges) -> None:
+        """Hold only the byte ranges ``[(first, end), ...]`` in HBM (call
+        before the first :meth:`device`).  Offsets stay the reference's hpas;
+        the rest of the image lives on the host mirror only -- the control
+        plane builds it there, and it is never pushed to or pulled from the
+        device (pv_image_create backs it with a shared junk hole)."""
+        if self._dev is not None:
+            raise RuntimeError("residency must be set before the device image exists")
+        mask = np.zeros(self.npages, dtype=np.bool_)
+        rr = []
+        for first, end in ranges:
+            first, end = int(first), int(end)
+            if not 0 <= first <= end <= self.nbytes or first % PAGE_SIZE or end % PAGE_SIZE:
+                raise ValueError(f"bad resident range [{first:#x}, {end:#x})")
+            mask[first >> PAGE_SHIFT:end >> PAGE_SHIFT] = True
+            rr.append((first, end))
+        self._resident = mask
+        self._res_ranges = rr
+
+    @property
+    def partial(self) -> bool:
+        return self._resident is not None
+
+    def resident(self, first: int, end: int) -> bool:
+        """Every page of bytes [first, end) is held in HBM."""
+        if self._resident is None:
+            return True
+        if end <= first:
+            return True
+        return bool(self._resident[first >> PAGE_SHIFT:((end - 1) >> PAGE_SHIFT) + 1].all())
+
+    def _alloc_device(self):
+        import ctypes
+
+        import torch
+
+        if self._resident is None:
+            self.device_bytes = self.nbytes
+            return torch.zeros(self.nbytes, dtype=torch.uint8, device="cuda")
+        lib = _native.lib()
+        flat = np.asarray([x for r in self._res_ranges for x in r], dtype=np.uint64)
+        ptr, handle, held = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_uint64()
+        _native.check(lib.pv_image_create(self.nbytes, flat.ctypes.data if len(flat) else None, len(self._res_ranges),
+                                          0, ctypes.byref(ptr), ctypes.byref(handle), ctypes.byref(held)),
+                      "pv_image_create")
+        self._vmm = handle.value
+        self.device_bytes = int(held.value)
+        dev = torch.cuda.current_device()
+
+        class _Cai:  # zero-copy torch view of the reserved range
+            __cuda_array_interface__ = {"shape": (self.nbytes,), "typestr": "|u1", "data": (ptr.value, False),
+                                        "version": 3, "strides": None}
+
+        t = torch.as_tensor(_Cai(), device=f"cuda:{dev}")
+        assert t.data_ptr() == ptr.value
+        return t
+
+    def __del__(self):
+        vmm = getattr(self, "_vmm", None)
+        if vmm:
+            try:
+                self._dev = None
+                _native.lib().pv_image_destroy(vmm)
+            except Exception:  # noqa: BLE001 - interpreter shutdown
+                pass
 
     # ---- host side --------------------------------------------------------
     def host_for_read(self) -> np.ndarray:
@@ -139,7 +210,7 @@ class MemoryImage:
         with self._lock:
             if self._dev is None:
                 _native.lib()  # fail loudly without a GPU / the library
-                self._dev = torch.zeros(self.nbytes, dtype=torch.uint8, device="cuda")
+                self._dev = self._alloc_device()
                 self._dev_dirty = torch.zeros(self.npages, dtype=torch.uint8, device="cuda")
             if self._host_dirty_any:
                 self.push()
@@ -189,7 +260,8 @@ class MemoryImage:
         import torch
 
         with self._lock:
-            pages = np.flatnonzero(self._host_dirty)
+            dirty = self._host_dirty if self._resident is None else (self._host_dirty & self._resident)
+            pages = np.flatnonzero(dirty)
             if len(pages) == 0 or self._dev is None:
                 self._host_dirty_any = False
                 return
@@ -227,6 +299,8 @@ class MemoryImage:
             if self.leaf_index is not None:
                 self.leaf_index.sync_device_writes()  # before the dirty map is cleared
             dmap = self._dev_dirty.cpu().numpy()
+            if self._resident is not None:
+                dmap &= self._resident  # writes that landed in the hole are junk
             pages = np.flatnonzero(dmap)
             host2d = self.host.reshape(self.npages, PAGE_SIZE)
             for s in range(0, len(pages), _STAGE_PAGES):

@@ -211,6 +211,7 @@ class FrameAllocator:
 
     def __init__(self, mem: PhysMem, first_pfn: int, n_pages: int):
         self._mem = mem
+        self._first = first_pfn
         self._cursor = first_pfn
         self._end = first_pfn + max(n_pages, 0)
         self._freed: deque[int] = deque()
@@ -721,10 +722,20 @@ class MemoryVirtualizer:
 DEVICE_MAP_MIN = 4096
 
 
-def _device_map_ok(mem: PhysMem, n: int) -> bool:
+def _device_map_ok(mem: PhysMem, n: int, alloc: "FrameAllocator | None" = None) -> bool:
+    """Build on the device?  On a partially resident image (a guest-sharded
+    rank) only when every node the builder reads or writes is in HBM: the
+    allocator's frames (``alloc``), else the whole window."""
     import os
 
-    return mem.backing.on_device and n >= DEVICE_MAP_MIN and os.environ.get("PV_DEVICE_MAP", "1") != "0"
+    img = mem.backing
+    if not (img.on_device and n >= DEVICE_MAP_MIN and os.environ.get("PV_DEVICE_MAP", "1") != "0"):
+        return False
+    if not img.partial:
+        return True
+    if alloc is not None:
+        return img.resident(mem.base + alloc._first * PAGE_SIZE, mem.base + alloc._end * PAGE_SIZE)
+    return img.resident(mem.base, mem.base + mem.size_bytes)
 
 
 def _device_map(mem: PhysMem, root: PageTableRoot, alloc: FrameAllocator, vas: np.ndarray,
@@ -774,8 +785,9 @@ def _bulk_map(mem: PhysMem, root: PageTableRoot, alloc: FrameAllocator, vas: np.
               targets: np.ndarray, leaf_flags: int) -> None:
     """TableEditor(mem, root, alloc.alloc).map(va, target) for each pair in
     order, vectorised (node frames are the only allocations)."""
-    if _device_map_ok(mem, len(vas)) and not (vas & PAGE_MASK).any() and \
-            _device_map(mem, root, alloc, vas, targets, leaf_flags):
+    if _device_map_ok(mem, len(vas), alloc) and mem.backing.resident(
+            mem.base + root.root_pfn * PAGE_SIZE, mem.base + (root.root_pfn + 1) * PAGE_SIZE) and \
+            not (vas & PAGE_MASK).any() and _device_map(mem, root, alloc, vas, targets, leaf_flags):
         return
     bm = _BulkMapper(mem, root.root_pfn, vas)
     if not _distinct_pages(vas) or not bm.plan():
@@ -814,7 +826,8 @@ def _bulk_process_map(memv: MemoryVirtualizer, space: ProcessSpace, gvas: np.nda
     """Vectorised map_process_page over ``gvas``; False if not applicable."""
     if (gvas & PAGE_MASK).any() or (gvas < 0).any():
         return False
-    if _device_map_ok(space.guest.mem, len(gvas)):
+    if _device_map_ok(space.guest.mem, len(gvas)) and (
+            space.shadow_root is None or _device_map_ok(memv.host_mem, len(gvas), memv.host_alloc)):
         return _device_process_map(memv, space, gvas)
     if not _distinct_pages(gvas):
         return False
@@ -949,12 +962,16 @@ def translate_batch(translator: ProcessTranslator, gvas, *, use_cache: bool | No
             aux.cpu().numpy().view(np.uint64))
 
 
-def translate_many(pairs, *, chunk: int = 1 << 23):
+def translate_many(pairs, *, chunk: int = 1 << 23, packed: bool = False, out=None):
     """``translate_batch`` for several uncached translators at once, host
     tensors in and out: ``pairs = [(translator, host_vas), ...]`` -> one
     pipelined H2D / translate / D2H stream over every pair (they must share
     one physical memory).  Returns ``[(hpa, status, aux), ...]`` as pinned
-    host tensors."""
+    host tensors; ``packed=True`` returns ``[(words, None, aux), ...]`` with
+    one lane word per VA (hpa, or the status and value of the exception the
+    lane raises; ``dataplane.unpack_lanes``), 8 bytes per lane instead of 12.
+    ``out``: per pair pinned host tensors to fill (see
+    ``dataplane.translate_host_many``)."""
     import torch
 
     if not pairs:
@@ -969,7 +986,7 @@ def translate_many(pairs, *, chunk: int = 1 << 23):
         if not isinstance(vas, torch.Tensor):
             vas = torch.from_numpy(np.ascontiguousarray(np.asarray(vas, dtype=np.uint64)).view(np.int64))
         jobs.append((tr.device_space, vas))
-    return dp.translate_host_many(image, jobs, chunk=chunk)
+    return dp.translate_host_many(image, jobs, chunk=chunk, packed=packed, out=out)
 
 
 def lane_error(status: int, value: int, aux: int, va: int, image_bytes: int) -> Exception | None:

@@ -88,3 +88,59 @@ def max_over_ranks(values: Iterable[float], world: int, device=None) -> list[flo
     t = torch.tensor(vals, dtype=torch.float64, device=None if _host_backend() else device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return t.tolist()
+
+
+class SharedHostBuffer:
+    """One host buffer every rank of the box maps (the rank-0 result return
+    of the end-to-end path): rank 0 creates it in /dev/shm
+    (or /tmp when /dev/shm is too small), every rank maps it MAP_SHARED and
+    registers it with CUDA (cudaHostRegister), so each rank's device-to-host
+    copies of its own guests' results land directly in the buffer rank 0
+    reads -- the return costs one barrier, no extra copy and no collective.
+    """
+
+    def __init__(self, nbytes: int, rank: int, world: int, tag: str = "pv"):
+        import os
+        import shutil
+        import uuid
+
+        import torch
+        import torch.distributed as dist
+
+        self.nbytes = max(int(nbytes), 8)
+        self.rank = rank
+        path = [None]
+        if rank == 0:
+            base = "/dev/shm"
+            if not os.path.isdir(base) or shutil.disk_usage(base).free < 2 * self.nbytes:
+                base = "/tmp"
+            path[0] = os.path.join(base, f"{tag}_{os.getpid()}_{uuid.uuid4().hex[:8]}")
+            with open(path[0], "wb") as f:
+                f.truncate(self.nbytes)
+        if world > 1:
+            dist.broadcast_object_list(path, src=0)
+        self.path = path[0]
+        self.bytes = torch.from_file(self.path, shared=True, size=self.nbytes, dtype=torch.uint8)
+        rc = torch.cuda.cudart().cudaHostRegister(self.bytes.data_ptr(), self.nbytes, 0)
+        self.registered = int(rc) == 0
+        if not self.registered:
+            raise RuntimeError(f"cudaHostRegister of the shared result buffer failed ({rc})")
+        self.world = world
+
+    def view(self, dtype, offset_elems: int, count: int):
+        """A typed view of ``count`` elements at element offset ``offset_elems``."""
+        return self.bytes.view(dtype)[offset_elems:offset_elems + count]
+
+    def close(self) -> None:
+        import os
+
+        import torch
+        import torch.distributed as dist
+
+        if self.registered:
+            torch.cuda.cudart().cudaHostUnregister(self.bytes.data_ptr())
+            self.registered = False
+        if self.world > 1 and dist.is_initialized():
+            dist.barrier()
+        if self.rank == 0 and self.path and os.path.exists(self.path):
+            os.unlink(self.path)

@@ -99,13 +99,31 @@ class C5World:
     hybrid_roots: list = field(default_factory=list)  # [guest][proc] PageTableRoot
 
 
-def build_c5(cfg: C5Config, device: bool = False) -> C5World:
-    """The whole 8-guest world (every rank builds the same image, so hpas are
-    identical across ranks; a rank only touches its own guests' pages).
-    ``device``: allocate the HBM image first so the tables are built there
-    (pv_map_plan / pv_map_commit) instead of on the host mirror."""
+def c5_slot(cfg: C5Config, g: int) -> tuple[int, int]:
+    """Byte range of guest g's slot: the host-private region comes first,
+    then the slots in guest order (memvirt.py:433-480 carving)."""
+    base = cfg.host_private + g * cfg.guest_bytes
+    return base, base + cfg.guest_bytes
+
+
+def c5_residency(cfg: C5Config, guests) -> list[tuple[int, int]]:
+    """What a rank owning ``guests`` holds in HBM: the
+    host-private region (every table node of the walks) + its guests' slots."""
+    return [(0, cfg.host_private)] + [c5_slot(cfg, g) for g in guests]
+
+
+def build_c5(cfg: C5Config, device: bool = False, resident_guests=None) -> C5World:
+    """The whole 8-guest world (every rank builds the same control plane, so
+    hpas are identical across ranks; a rank only touches its own guests'
+    pages).  ``device``: allocate the HBM image first so the tables are built
+    there (pv_map_plan / pv_map_commit) instead of on the host mirror.
+    ``resident_guests``: hold only the host-private region and these guests'
+    slots in HBM (a guest-sharded rank); the other guests' tables are built
+    on the host mirror and never reach the device."""
     cls = type("C5Virtualizer", (mv.MemoryVirtualizer,), {"HOST_PRIVATE_BYTES": cfg.host_private})
     memv = cls(host_bytes=cfg.host_private + cfg.guests * cfg.guest_bytes)
+    if resident_guests is not None:
+        memv.host_mem.backing.set_residency(c5_residency(cfg, resident_guests))
     if device:
         memv.host_mem.backing.device()
     world = C5World(cfg, memv)

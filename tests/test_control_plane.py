@@ -15,7 +15,7 @@ import numpy as np
 import pytest
 
 import scenarios as S
-from conftest import load_json, status_outcome
+from conftest import ROOT, load_json, status_outcome
 from oracle import oracle as O
 from paper_1304_3771_b200 import errors as er
 from paper_1304_3771_b200 import has as be
@@ -304,3 +304,39 @@ def test_c1_copy_oracle_digest(mode):
     e, h, m = O.cache_state(oc)
     assert [h, m, [list(x) for x in e]] == g["cache"]
     assert S.sha(raw.tobytes()) == g["image_sha"]
+
+
+def test_table_editor_fault_level_quirk_matches_reference():
+    """TableEditor._descend names the fault level with ``index is top``
+    (memvirt.py:290): for a missing node on the mid level whose mid index
+    equals the top index (CPython caches those small ints), the reference
+    reports level 1.  Differential against the reference itself."""
+    import os
+    import sys
+
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "devfsim")):
+        pytest.skip("baseline/_ref not staged (run __graft_entry__.build())")
+    if ref_dir not in sys.path:
+        sys.path.append(ref_dir)
+    import devfsim.memvirt as rm
+
+    from paper_1304_3771_b200 import memvirt as mm
+
+    def outcomes(m):
+        memv = m.MemoryVirtualizer(32 << 20)
+        guest = memv.add_guest(0, "shadow", 8 << 20)
+        space = memv.create_process(guest)
+        memv.map_process_page(space, (1 << 30) | (7 << 21))  # top entry 1 present, mid 7 present
+        ed = m.TableEditor(guest.mem, space.guest_root, guest.os_alloc.alloc)
+        out = []
+        for top in range(4):
+            for mid in (0, 1, 2, 3, 7, 300):
+                va = (top << 30) | (mid << 21) | (5 << 12)
+                try:
+                    out.append(("ok", int(ed.entry_at(va).target_pfn)))
+                except Exception as e:  # noqa: BLE001
+                    out.append((type(e).__name__, int(getattr(e, "va", -1)), int(getattr(e, "level", -1))))
+        return out
+
+    assert outcomes(mm) == outcomes(rm)

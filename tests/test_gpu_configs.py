@@ -120,11 +120,15 @@ def test_bench_two_ranks_one_device(cuda, tmp_path):
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    common = ["--steps", "2", "--warmup", "3", "--scale", "8", "--gather", "--no-e2e", "--no-cpu-baseline"]
+    one = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "1"] + common, cwd=root,
+                         capture_output=True, text=True, timeout=600)
+    assert one.returncode == 0, one.stderr[-2000:]
+    single = json.loads([ln for ln in one.stdout.splitlines() if ln.startswith("{")][-1])
     env = dict(os.environ, PV_BENCH_SHARED_DEVICE="1", MASTER_ADDR="127.0.0.1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", "29541", os.path.join(root, "bench.py"),
-           "--gpus", "2", "--steps", "2", "--warmup", "3", "--scale", "8", "--gather", "--no-e2e",
-           "--no-cpu-baseline"]
+           "--gpus", "2"] + [c for c in common if c != "--no-e2e"]
     p = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert p.returncode == 0, p.stderr[-2000:]
     lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
@@ -133,6 +137,19 @@ def test_bench_two_ranks_one_device(cuda, tmp_path):
     assert line["n_gpus"] == 2 and line["value"] > 0 and line["faulting_lanes"] == 0
     assert line["gather_to_rank0"]["complete"] is True
     assert line["config"]["sharding"] == "guest g -> rank g mod 2"
+    assert line["parity"]["ok"] is True and single["parity"]["ok"] is True
+    # every guest's results, returned to rank 0, bit-identical to the one-rank run
+    assert line["gather_to_rank0"]["digest"] == single["gather_to_rank0"]["digest"] is not None
+    # each rank holds the host-private region + its 4 guests' slots (+ the hole), not the whole world
+    cfg = W.C5Config().scaled(8)
+    img = line["hbm_image"]
+    assert single["hbm_image"]["device_bytes"] == img["image_bytes"]
+    owned = cfg.host_private + 4 * cfg.guest_bytes
+    assert owned <= img["device_bytes"] <= owned + (256 << 20), img
+    assert img["device_bytes"] < 0.6 * img["image_bytes"]
+    # end to end at N = 2: both ranks' lane words land in the host buffer rank 0 reads
+    e2e = line["e2e"]
+    assert e2e["lanes_equal_device_results"] is True and e2e["gather_to_rank0"]["verified"] is True
 
 
 @pytest.mark.gpu
