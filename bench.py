@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=["c5", "c1", "c2", "c3", "c4"], default="c5")
     ap.add_argument("--c2-ops", type=int, default=10_000_000)
-    ap.add_argument("--c1-mode", choices=["shadow", "tdp"], default="shadow",
+    ap.add_argument("--c1-mode", choices=["shadow", "tdp", "4l"], default="shadow",
                     help="C1 translator: shadow table (one stage) or guest table + TDP (two stages)")
     ap.add_argument("--scale", type=int, default=1, help="shrink C5 by this factor (testing only)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true", help="skip the full-size parity check against the oracle "
                     "after the timed steps")
+    ap.add_argument("--unpacked", dest="packed", action="store_false", help="C5/C1: the walk writes the "
+                    "(u64 value, u32 status) arrays instead of PV_OUT_PACKED lane words (8 B per lane; the "
+                    "default, decoded for the parity check)")
     ap.add_argument("--overlap", action="store_true", help="time C5/C1 steps with the walk on a second stream "
                     "beside plan + exec (A/B option: measured slower than back-to-back phases, "
                     "profiles/r02_overlap_ab.md)")
@@ -198,6 +201,33 @@ class Workload:
             self.copy_bytes = buf_off
             self.total_copy_bytes = cfg.guests * cfg.copy_bytes_per_guest
             ops_all = np.concatenate(rows)
+        elif c1_mode == "4l":
+            # BASELINE configs[0] as written: a 4-level 4 KiB table (extension geometry, parity pinned
+            # by the C restatement orc_walk4 only); no e2e / CPU arm (no reference API for it)
+            from paper_1304_3771_b200 import ext4l as X
+
+            mem, t4 = X.build_c1_4l()
+            self.c1_mode = c1_mode
+            self.memv = None
+            self.image_mem = mem
+            self.owned = [0]
+            t_spaces = [t4.space]
+            v_all = X.c1_4l_vas()
+            lo, hi = len(v_all) * rank // world, len(v_all) * (rank + 1) // world
+            v = v_all[lo:hi]
+            vas_parts = [v]
+            bounds = [(0, len(v), 0)]
+            self.n_vas, self.total_vas = len(v), len(v_all)
+            self.proc_vas, self.proc_lane0 = [(0, 0, v)], [lo]
+            c_spaces, c_shims = [t4.space], None
+            total = 64 << 20
+            pages = total // 4096
+            p0, p1 = pages * rank // world, pages * (rank + 1) // world
+            n = (p1 - p0) * 4096
+            ops_all = np.array([[X.C1_4L_VA + p0 * 4096, n, 0, 0]], dtype=np.uint64)
+            self.proc_ops = [(0, 0, ops_all[:, :2], np.zeros(1, np.uint64))]
+            self.copy_bytes, self.total_copy_bytes = n, total
+            self.c1_space = None
         else:
             memv, guest, space = W.build_c1(c1_mode)
             self.c1_mode = c1_mode
@@ -229,9 +259,10 @@ class Workload:
             self.total_copy_bytes = total
             self.c1_space = space
         self.build_s = time.time() - t0
-        self.image = self.memv.host_mem.backing
+        self.image = self.memv.host_mem.backing if self.memv is not None else self.image_mem.backing
         self.image.device()  # allocate + push tables
-        self.vas = torch.from_numpy(np.concatenate(vas_parts).view(np.int32)).to("cuda")
+        allv = np.concatenate(vas_parts)
+        self.vas = torch.from_numpy(allv.view(np.int32 if allv.dtype == np.uint32 else np.int64)).to("cuda")
         self.tplan = dp.TranslatePlan(t_spaces, bounds)
         self.t_spaces, self.t_bounds, self.c_spaces = t_spaces, bounds, c_spaces
         n = self.n_vas
@@ -264,7 +295,10 @@ def run_ours(args, rank, world, local):
     hint = dp.exec_hint(plan, wl.src.data_ptr())
 
     def phase_translate():
-        dp.translate_lanes(img, wl.tplan, wl.vas, out=wl.out)
+        if args.packed:  # PV_OUT_PACKED: one u64 per lane, no status array
+            dp.translate_lanes(img, wl.tplan, wl.vas, out=(wl.out[0], None, wl.out[2]), packed=True)
+        else:
+            dp.translate_lanes(img, wl.tplan, wl.vas, out=wl.out)
 
     def phase_translate_conc():  # the same walk sized to share every SM with the exec (PV_CONCURRENT)
         dp.translate_lanes(img, wl.tplan, wl.vas, out=wl.out, concurrent=True)
@@ -400,6 +434,22 @@ def run_ours(args, rank, world, local):
     assert int(plan.conflict.item()) == 0, "conflicting destinations in the bench batch"
     res = plan.results.cpu().numpy().view(np.uint64)
     assert (res[:, 3] & 0xFFFFFFFF == 0).all() and (res[:, 0] == plan.host_ops[:, 1]).all()
+    other = None
+    if args.packed:  # decode the timed step's lane words for the checks below
+        v, st_ = dp.unpack_lanes(wl.out[0].cpu().numpy(), wl.out[2].cpu().numpy())
+        wl.out[0].copy_(torch.from_numpy(v.view(np.int64)))
+        wl.out[1].copy_(torch.from_numpy(st_.view(np.int32)))
+        # A/B in the same run: the walk in the (value, status) form, K launches, same lanes and results
+        o2 = (torch.empty_like(wl.out[0]), torch.empty_like(wl.out[1]), torch.zeros_like(wl.out[2]))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        dp.translate_lanes(img, wl.tplan, wl.vas, out=o2)
+        e0.record(stream)
+        for _ in range(args.steps):
+            dp.translate_lanes(img, wl.tplan, wl.vas, out=o2)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        other = {"form": "unpacked (u64 value + u32 status)", "translate_ms_per_step": e0.elapsed_time(e1) / args.steps,
+                 "launch": "eager", "results_equal": bool(torch.equal(o2[0], wl.out[0]) and torch.equal(o2[1], wl.out[1]))}
     n_faults = int((wl.out[1] != 0).sum().item())
     tr_ms = sum(e[0].elapsed_time(e[1]) for e in evs)
     serial_ms = sum(e[0].elapsed_time(e[4]) for e in evs)
@@ -427,12 +477,12 @@ def run_ours(args, rank, world, local):
 
     # e2e through the public API with host buffers
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and wl.memv is not None:
         e2e = run_e2e(wl, args, world)
 
     peak, peak_kind = peaks()
     exec_achieved = 2 * wl.copy_bytes * K / (exec_ms / 1e3) / 1e9
-    walk_bytes = 16 * wl.n_vas  # u32 VA in + u64 hpa + u32 status out
+    walk_bytes = (12 if args.packed else 16) * wl.n_vas  # u32 VA in + u64 hpa (+ u32 status) out
     walk_achieved = walk_bytes * K / (tr_ms / 1e3) / 1e9
     walk_bytes_pte = walk_bytes + 8 * _leaf_ptes(wl)  # + 8 B per distinct leaf PTE
     walk_achieved_pte = walk_bytes_pte * K / (tr_ms / 1e3) / 1e9
@@ -455,6 +505,8 @@ def run_ours(args, rank, world, local):
                  "ms_per_step": copy_ms / K, "exec_ms_per_step": exec_ms / K,
                  "plan_shim_stamp_ms_per_step": plan_ms / K},
         "translate_ms_per_step": tr_ms / K,
+        "walk_form": "PV_OUT_PACKED (one u64 per lane)" if args.packed else "unpacked (u64 value + u32 status)",
+        "walk_other_form": other,
         "step": {"mode": "overlapped" if overlap else "serial",
                  "ms": total_ms / K, "serial_ms": serial_ms / K,
                  "translations_per_s": wl.total_vas * K / (total_ms / 1e3),
@@ -481,9 +533,10 @@ def run_ours(args, rank, world, local):
                           "with_leaf_ptes": {"algorithmic_bytes_per_launch": walk_bytes_pte,
                                              "distinct_leaf_ptes": _leaf_ptes(wl), "achieved": walk_achieved_pte,
                                              "frac": walk_achieved_pte / peak},
-                          "note": "16 B/translation (u32 VA in, u64 hpa + u32 status out); with_leaf_ptes adds "
+                          "note": ("12 B/translation (u32 VA in, one u64 lane word out)" if args.packed else
+                                   "16 B/translation (u32 VA in, u64 hpa + u32 status out)") + "; with_leaf_ptes adds "
                                   "SURVEY.md 8(d)'s 8 B per distinct leaf PTE touched",
-                          "gather_sol": walker_sol(wl.n_vas * K / (tr_ms / 1e3)),
+                          "gather_sol": walker_sol(wl.n_vas * K / (tr_ms / 1e3), args.packed),
                           "ncu": load_json_profile("walker_ncu.json")},
         "faulting_lanes": n_faults,
         "parity": parity,
@@ -503,7 +556,7 @@ def run_ours(args, rank, world, local):
         "build_s": wl.build_s,
         "provenance": provenance(),
     }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and wl.memv is not None:
         line["cpu_baseline"] = cpu_baseline(wl, args)
     return line
 
@@ -551,7 +604,7 @@ def verify_parity(wl, threads: int, n_ops: int = 64) -> dict:
         ref[a:min(a + step, span)] = dev[a:min(a + step, span)].cpu().numpy()
     value = wl.out[0].cpu().numpy().view(np.uint64)
     status = wl.out[1].cpu().numpy().view(np.uint32)
-    vas = wl.vas.cpu().numpy().view(np.uint32)
+    vas = wl.vas.cpu().numpy().view(np.uint32 if wl.vas.dtype == torch.int32 else np.uint64)
     lane_bad = 0
     for begin, end, si in wl.t_bounds:
         sp = wl.t_spaces[si]
@@ -1100,14 +1153,14 @@ def run_e2e(wl, args, world):
         from paper_1304_3771_b200 import shard as _sh
 
         shared = _sh.SharedHostBuffer(wl.total_vas * 8, int(os.environ.get("RANK", "0")), world, tag="pv_e2e")
-        outs = [(shared.view(torch.int64, l0, len(v)), None, None)
-                for l0, (_, _, v) in zip(wl.proc_lane0, wl.proc_vas)]
-    else:
-        outs = None
+        res_out = [(shared.view(torch.int64, l0, len(v)), None, None)
+                   for l0, (_, _, v) in zip(wl.proc_lane0, wl.proc_vas)]
+    else:  # caller-owned pinned result buffers, reused every step
+        res_out = [(torch.empty(len(v), dtype=torch.int64, pin_memory=True), None, None) for _, _, v in wl.proc_vas]
 
     def one_step():
         t0 = time.perf_counter()
-        io["res"] = mv.translate_many([(translators[(g, p)], t) for t, g, p in host_vas], packed=True, out=outs)
+        io["res"] = mv.translate_many([(translators[(g, p)], t) for t, g, p in host_vas], packed=True, out=res_out)
         if pg:
             tdist.barrier()  # every rank's words are in the shared buffer: rank 0 holds all results
         t1 = time.perf_counter()
@@ -1191,16 +1244,18 @@ class _Prebuilt:
         return self.root
 
 
-def walker_sol(lanes_per_s: float):
+def walker_sol(lanes_per_s: float, packed: bool = False):
     """The walker against the measured speed of light of its access pattern
-    (random 4-byte gathers + 16 B/lane stream; profiles/walker_sol.json)."""
+    (random 4-byte gathers + the lane stream: 12 B/lane unpacked, 8 B/lane
+    packed out; profiles/walker_sol.json)."""
     try:
         with open(os.path.join(ROOT, "profiles", "walker_sol.json")) as f:
             sol = json.load(f)
     except Exception:  # noqa: BLE001
         return None
-    return {"achieved": lanes_per_s, "probe": sol["lanes_per_s"], "unit": "lanes/s",
-            "frac": lanes_per_s / sol["lanes_per_s"], "source": "profiles/walker_sol.json"}
+    probe = sol.get("lanes_per_s_packed", sol["lanes_per_s"]) if packed else sol["lanes_per_s"]
+    return {"achieved": lanes_per_s, "probe": probe, "unit": "lanes/s", "frac": lanes_per_s / probe,
+            "form": "packed (8 B out)" if packed else "unpacked (12 B out)", "source": "profiles/walker_sol.json"}
 
 
 def load_traffic(workload: str) -> dict:
@@ -1258,8 +1313,11 @@ def config_of(wl, world):
                       f"{c.guests * c.copy_bytes_per_guest >> 20} MiB payload per step, whole job)",
                 "scale": 1 if wl.cfg.guest_bytes == 8 << 30 else "reduced"}
     return {"workload": f"C1: 1 {wl.c1_mode} guest, 16384 shuffled pages, 1M random-VA translations + 64 MiB "
-                        "copy_to_user", "mode": wl.c1_mode, "geometry": "reference 3-level 2/9/9/12",
-            "parallelism": f"replicas x{world} (one process: every rank runs the full batch on its own image)",
+                        "copy_to_user", "mode": wl.c1_mode,
+            "geometry": "4-level 9/9/9/9/12 (extension, parity unpinned by the reference)" if wl.c1_mode == "4l"
+            else "reference 3-level 2/9/9/12",
+            "parallelism": f"lane-split x{world} (one process: the VA range and the copy's destination pages "
+                           "split evenly over the ranks, image replicated, no collective)",
             "l2": "inputs smaller than L2 (not flushed)"}
 
 
@@ -1279,8 +1337,12 @@ def cpu_sample(memv, proc_vas, proc_ops, n_vas: int, n_bytes: int, threads: int)
     sys.path.insert(0, ROOT)
     from oracle import oracle as O
 
-    # the host mirror holds every table byte (tables are written host-side)
-    img = memv.host_mem.backing.host
+    # the oracle walks the host mirror: bring every table node current first (tables built in HBM
+    # reach the host lazily, image.py); C5's nodes all live in the host-private region, the copies
+    # only write data pages
+    backing = memv.host_mem.backing
+    span = getattr(memv, "HOST_PRIVATE_BYTES", backing.nbytes) if backing.nbytes > (4 << 30) else backing.nbytes
+    img = backing.host_for_read(0, span)
     # translations: first processes' VAs (shadow walks)
     done = 0
     t_tr = 0.0

@@ -104,8 +104,9 @@ __device__ __forceinline__ void mark_node(const NodeMarks* nm, uint64_t base, ui
   if (nm == nullptr) return;
   const uint64_t at = base + (node << kPageShift);  // a window base need not be page aligned
   uint32_t* p = nm->map + (at >> kPageShift);
-  if (*reinterpret_cast<volatile uint32_t*>(p) != nm->epoch) *p = nm->epoch;
-  if ((at & kPageMask) && *reinterpret_cast<volatile uint32_t*>(p + 1) != nm->epoch) p[1] = nm->epoch;
+  // a plain (L1-cached) read: a stale value only costs a redundant store
+  if (*p != nm->epoch) *p = nm->epoch;
+  if ((at & kPageMask) && p[1] != nm->epoch) p[1] = nm->epoch;
 }
 
 // Full three-level walk through global memory (L1/L2 cached).  On success

@@ -92,6 +92,7 @@ stamp_kernel(const uint64_t* __restrict__ page_off, uint64_t n_ops, uint64_t n_p
     const uint32_t seen_conflict = *reinterpret_cast<volatile const uint32_t*>(conflict);
     if (seen_conflict & PV_CONFLICT_TABLE) return;
     if (seen_conflict && node_map == nullptr) return;
+    bool overlap = seen_conflict & PV_CONFLICT_OVERLAP;  // stamping is over; the hazard check goes on
     const uint64_t p0 = t * kPlanPpt;
     uint64_t op = upper_search(page_off, 0, n_ops, p0);
     uint64_t op_end = __ldg(page_off + op + 1);
@@ -108,16 +109,21 @@ stamp_kernel(const uint64_t* __restrict__ page_off, uint64_t n_ops, uint64_t n_p
         atomicOr(conflict, PV_CONFLICT_TABLE);
         return;
       }
-      if (*reinterpret_cast<volatile const uint32_t*>(conflict) & PV_CONFLICT_OVERLAP) continue;
+      if (overlap) continue;
       const unsigned long long mine = ((unsigned long long)epoch << 40) | (p + 1);
       const unsigned long long seen = *reinterpret_cast<volatile const unsigned long long*>(owner + hp);
       if ((seen >> 40) == epoch && seen != mine) {  // already stamped by another chunk of this batch
         atomicOr(conflict, PV_CONFLICT_OVERLAP);
         if (node_map == nullptr) return;
+        overlap = true;
         continue;
       }
       const unsigned long long old = atomicMax(owner + hp, mine);
-      if ((old >> 40) == epoch && old != mine) atomicOr(conflict, PV_CONFLICT_OVERLAP);
+      if ((old >> 40) == epoch && old != mine) {
+        atomicOr(conflict, PV_CONFLICT_OVERLAP);
+        if (node_map == nullptr) return;
+        overlap = true;
+      }
     }
   }
 }

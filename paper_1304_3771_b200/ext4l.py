@@ -151,3 +151,36 @@ def c3_sequential(region_bytes: int = 16 << 30) -> np.ndarray:
 
 def c3_strided(region_bytes: int = 16 << 30) -> np.ndarray:
     return (C3_VA + np.arange(0, region_bytes, LARGE + PAGE, dtype=np.uint64) + np.uint64(0x18)).astype(np.uint64)
+
+
+# ---- C1 in 4-level geometry (BASELINE configs[0] as written) ----------------------
+
+C1_4L_VA = 0x7F00_1000_0000
+C1_4L_NODE_BYTES = 16 << 20
+
+
+def build_c1_4l(n_pages: int = 16384, host_bytes: int = 128 << 20, seed: int = 1304):
+    """BASELINE configs[0] literally: one address space under a 4-level
+    4 KiB page table, 16,384 data pages mapped at C1_4L_VA in
+    ``random.Random(1304).shuffle`` order (scattered frames, like the
+    reference-geometry C1 of SURVEY.md 8(d)).  Image = node pool + data
+    frames; nodes come from the pool's FIFO allocator in VA-walk order."""
+    import random
+
+    mem = PhysMem(host_bytes)
+    alloc = FrameAllocator(mem, 1, C1_4L_NODE_BYTES // PAGE - 1)
+    t = Table4(mem, alloc)
+    order = list(range(n_pages))
+    random.Random(seed).shuffle(order)
+    data0 = C1_4L_NODE_BYTES // PAGE
+    for k, p in enumerate(order):
+        t.map_4k(C1_4L_VA + p * PAGE, data0 + k)
+    return mem, t
+
+
+def c1_4l_vas(n: int = 1_000_000, seed: int = 3771) -> np.ndarray:
+    """Random(3771).randrange(64 MiB) offsets from C1_4L_VA."""
+    import random
+
+    rng = random.Random(seed)
+    return np.array([C1_4L_VA + rng.randrange(64 << 20) for _ in range(n)], dtype=np.uint64)

@@ -76,6 +76,8 @@ class MemoryImage:
         self._dev = None          # torch.uint8 [nbytes]
         self._dev_dirty = None    # torch.uint8 [npages]
         self._dev_dirty_any = False
+        self._pending = np.zeros(self.npages, dtype=np.bool_)  # device-written, not yet gathered
+        self._pending_any = False
         self.dev_write_epoch = 0  # bumped by every device write (leaf-index coherence)
         self.host_epoch = 0       # bumped by every push of host writes into HBM
         self.leaf_index = None    # dataplane.LeafIndex, created on first indexed translate
@@ -166,20 +168,38 @@ class MemoryImage:
                 pass
 
     # ---- host side --------------------------------------------------------
-    def host_for_read(self) -> np.ndarray:
-        if self._dev_dirty_any:
-            self.pull()
+    # Device writes are pulled back lazily and only where the host looks:
+    # a host read / write of bytes [first, end) gathers the device-written
+    # pages of that range (``_pending``), so one read_word after a C5 step
+    # moves one page, not the 8 GiB the step wrote.
+    def host_for_read(self, first: int = 0, end: int | None = None) -> np.ndarray:
+        """Host array, current with device writes in bytes [first, end)
+        (default: the whole image)."""
+        if self._dev_dirty_any or self._pending_any:
+            self.pull(first, self.nbytes if end is None else end)
         return self.host
 
     def host_for_write(self, first: int, end: int) -> np.ndarray:
-        """Host array, after marking bytes [first, end) dirty."""
-        if self._dev_dirty_any:
-            self.pull()
+        """Host array, current in bytes [first, end), after marking them
+        dirty (``end <= first``: current everywhere, nothing marked)."""
+        if self._dev_dirty_any or self._pending_any:
+            if end > first:
+                self.pull(first, end)
+            else:
+                self.pull()
         if end > first:
             span = slice(first >> PAGE_SHIFT, ((end - 1) >> PAGE_SHIFT) + 1)
             self._host_dirty[span] = True
             self._maybe_nonzero[span] = True
             self._host_dirty_any = True
+        return self.host
+
+    def host_for_write_pages(self, pages) -> np.ndarray:
+        """Host array, current in ``pages``, after marking them dirty."""
+        pages = np.asarray(pages, dtype=np.int64)
+        if self._dev_dirty_any or self._pending_any:
+            self.pull_pages(pages)
+        self.mark_host_pages(pages)
         return self.host
 
     def mark_host_pages(self, pages) -> None:
@@ -188,10 +208,15 @@ class MemoryImage:
         self._host_dirty_any = True
 
     def zero_pages(self, pages: np.ndarray) -> None:
-        """Zero whole pages (frame allocation); free for never-written ones."""
-        if self._dev_dirty_any:
-            self.pull()
+        """Zero whole pages (frame allocation); free for never-written ones.
+        A page the device wrote is simply overwritten (never pulled)."""
         pages = np.asarray(pages, dtype=np.int64)
+        if self._dev_dirty_any:
+            self._collect_pending()
+        if self._pending_any:
+            dev_written = pages[self._pending[pages]]
+            self._pending[dev_written] = False
+            self._maybe_nonzero[dev_written] = True
         hot = pages[self._maybe_nonzero[pages]]
         if len(hot):
             self.host.reshape(self.npages, PAGE_SIZE)[hot] = 0
@@ -283,39 +308,73 @@ class MemoryImage:
             self._host_dirty_any = False
             self.host_epoch += 1
 
-    def pull(self) -> None:
-        """Gather device-written pages back into the host mirror."""
+    def _collect_pending(self) -> None:
+        """Move the device dirty map into ``_pending`` (host bitmap of pages
+        the device wrote and the host has not gathered yet)."""
         import torch
 
         with self._lock:
             if not self._dev_dirty_any or self._dev is None:
                 self._dev_dirty_any = False
                 return
-            lib = _native.lib()
             stream = torch.cuda.current_stream()
             # device writes of every stream (other host threads) land first;
             # new ones cannot be enqueued while the lock is held
             torch.cuda.synchronize()
             if self.leaf_index is not None:
                 self.leaf_index.sync_device_writes()  # before the dirty map is cleared
-            dmap = self._dev_dirty.cpu().numpy()
+            dmap = self._dev_dirty.cpu().numpy().astype(np.bool_)
             if self._resident is not None:
                 dmap &= self._resident  # writes that landed in the hole are junk
-            pages = np.flatnonzero(dmap)
-            host2d = self.host.reshape(self.npages, PAGE_SIZE)
-            for s in range(0, len(pages), _STAGE_PAGES):
-                idx = pages[s:s + _STAGE_PAGES]
-                pfns = torch.from_numpy(idx.astype(np.uint64).view(np.int64)).to("cuda", non_blocking=True)
-                dst = torch.empty(len(idx) * PAGE_SIZE, dtype=torch.uint8, device="cuda")
-                _native.check(lib.pv_gather_pages(self._dev.data_ptr(), self.nbytes, pfns.data_ptr(), len(idx),
-                                                  dst.data_ptr(), stream.cuda_stream), "pv_gather_pages")
-                host2d[idx] = dst.cpu().numpy().reshape(len(idx), PAGE_SIZE)
-                self._maybe_nonzero[idx] = True
+            self._pending |= dmap
+            self._maybe_nonzero |= dmap  # frame zeroing must not skip them (TableBuild.commit)
+            self._pending_any = bool(self._pending.any())
             self._dev_dirty.zero_()
             stream.synchronize()
             self._dev_dirty_any = False
             if self.leaf_index is not None:
                 self.leaf_index.release_retired()  # every stream drained above
+
+    def pull(self, first: int = 0, end: int | None = None) -> None:
+        """Gather the device-written pages of bytes [first, end) (default:
+        all) back into the host mirror."""
+        end = self.nbytes if end is None else end
+        if end <= first:
+            return
+        with self._lock:
+            self._collect_pending()
+            if not self._pending_any:
+                return
+            lo, hi = first >> PAGE_SHIFT, ((end - 1) >> PAGE_SHIFT) + 1
+            self._gather(np.flatnonzero(self._pending[lo:hi]) + lo)
+
+    def pull_pages(self, pages) -> None:
+        """Gather the device-written pages among ``pages``."""
+        with self._lock:
+            self._collect_pending()
+            if not self._pending_any:
+                return
+            pages = np.unique(np.asarray(pages, dtype=np.int64))
+            self._gather(pages[self._pending[pages]])
+
+    def _gather(self, pages: np.ndarray) -> None:
+        import torch
+
+        if len(pages) == 0:
+            return
+        lib = _native.lib()
+        stream = torch.cuda.current_stream()
+        host2d = self.host.reshape(self.npages, PAGE_SIZE)
+        for s in range(0, len(pages), _STAGE_PAGES):
+            idx = pages[s:s + _STAGE_PAGES]
+            pfns = torch.from_numpy(idx.astype(np.uint64).view(np.int64)).to("cuda", non_blocking=True)
+            dst = torch.empty(len(idx) * PAGE_SIZE, dtype=torch.uint8, device="cuda")
+            _native.check(lib.pv_gather_pages(self._dev.data_ptr(), self.nbytes, pfns.data_ptr(), len(idx),
+                                              dst.data_ptr(), stream.cuda_stream), "pv_gather_pages")
+            host2d[idx] = dst.cpu().numpy().reshape(len(idx), PAGE_SIZE)
+            self._maybe_nonzero[idx] = True
+        self._pending[pages] = False
+        self._pending_any = bool(self._pending.any())
 
     def sync(self) -> None:
         """Make host and device agree (pull device writes, push host writes)."""

@@ -168,7 +168,7 @@ class PhysMem:
     def read(self, addr: int, length: int) -> bytes:
         self._check(addr, length)
         off = self._base + addr
-        return self._img.host_for_read()[off:off + length].tobytes()
+        return self._img.host_for_read(off, off + length)[off:off + length].tobytes()
 
     def write(self, addr: int, data) -> None:
         data = bytes(data)
@@ -179,7 +179,7 @@ class PhysMem:
 
     def read_word(self, pfn: int, index: int) -> int:
         off = self._base + pfn * PAGE_SIZE + index * ENTRY_SIZE
-        return _LE64.unpack_from(self._img.host_for_read(), off)[0]
+        return _LE64.unpack_from(self._img.host_for_read(off, off + ENTRY_SIZE), off)[0]
 
     def write_word(self, pfn: int, index: int, word: int) -> None:
         off = self._base + pfn * PAGE_SIZE + index * ENTRY_SIZE
@@ -465,9 +465,8 @@ class _BulkMapper:
         if len(new_leaf_idx):
             offs = base_w + mid_node[new_leaf_idx] * 512 + self.mid[new_leaf_idx]
             words = (leaf_pfns.astype(np.uint64) << np.uint64(PAGE_SHIFT)) | np.uint64(FLAG_PRESENT | FLAG_WRITABLE)
-            img.host_for_write(0, 0)
+            img.host_for_write_pages(np.unique(offs * 8 // PAGE_SIZE))
             u64[offs] = words
-            img.mark_host_pages(np.unique(offs * 8 // PAGE_SIZE))
             for pfn, i in zip(leaf_pfns.tolist(), new_leaf_idx.tolist()):
                 leaf_of_tm[int(tm[i])] = pfn
         leaf_node = self.leaf_node.copy()
@@ -478,9 +477,8 @@ class _BulkMapper:
                 np.searchsorted(np.unique(keys), keys)]
         offs = base_w + leaf_node * 512 + self.leaf
         words = (targets.astype(np.uint64) << np.uint64(PAGE_SHIFT)) | np.uint64(leaf_flags)
-        img.host_for_write(0, 0)
+        img.host_for_write_pages(np.unique(offs * 8 // PAGE_SIZE))
         u64[offs] = words
-        img.mark_host_pages(np.unique(offs * 8 // PAGE_SIZE))
         assert n == len(offs)
 
 

@@ -96,7 +96,22 @@ def main():
     ref = calls(rm, rb, n)
     out = {k: {"ours_us": round(ours[k], 2), "ref_us": round(ref[k], 2), "speedup": round(ref[k] / ours[k], 2)}
            for k in ours}
-    print(json.dumps({"calls": out, "n": n, "gpu": torch.cuda.get_device_name(0),
+    # where a per-call walk's time goes: the device round trip alone (one launch + result in pinned
+    # memory, no translator layers) and a generic GPU round trip (one tiny torch kernel + sync)
+    from paper_1304_3771_b200 import dataplane as dp
+    from paper_1304_3771_b200 import percall
+
+    memv, space, _ = build(memvirt, has, "shadow")
+    img = memv.host_mem.backing
+    sp = memv.translator(space, use_cache=False).device_space
+    pc = percall.get()
+    floor = {"percall.walk (one pv_walk_one launch + spin on pinned result)":
+             per_call_us(lambda: pc.walk(img, sp, BUF + 0x123, False), n)}
+    x = torch.zeros(1, device="cuda")
+    s = torch.cuda.current_stream()
+    floor["torch: one tiny kernel + stream synchronize"] = per_call_us(lambda: (x.add_(1), s.synchronize()), n)
+    floor = {k: round(v, 2) for k, v in floor.items()}
+    print(json.dumps({"calls": out, "device_round_trip_us": floor, "n": n, "gpu": torch.cuda.get_device_name(0),
                       "cpu": open("/proc/cpuinfo").read().split("model name")[1].split("\n")[0].strip(": \t")},
                      indent=1))
 

@@ -33,12 +33,12 @@ __global__ void __launch_bounds__(512, 2) k(const uint32_t* __restrict__ idx, co
     for (int j = 0; j < L; ++j) v[j] = ld_idx(idx + wb + j * 32 + lane);
 #pragma unroll
     for (int j = 0; j < L; ++j) r[j] = __ldg(tab + (v[j] & mask));
-    if (MODE == 0) {
+    if (MODE == 0 || MODE == 2) {
 #pragma unroll
       for (int j = 0; j < L; ++j) {
         const uint64_t i = wb + j * 32 + lane;
         o64[i] = ((uint64_t)r[j] << 12) | (v[j] & 0xFFF);
-        o32[i] = r[j] & 3;
+        if (MODE == 0) o32[i] = r[j] & 3;  // MODE 2: the PV_OUT_PACKED form, 8 B out per lane
       }
     } else {
       // the buffer written two steps ago must have been read out by its bulk store
@@ -111,10 +111,12 @@ int main() {
   cudaMemset(tab, 1, (uint64_t)words * 4);
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  void (*fns[3])(const uint32_t*, const uint32_t*, uint32_t, uint64_t, uint64_t*, uint32_t*) = {k<0>, k<1>, kvec};
-  const char* names[3] = {"register stores", "smem + bulk stores", "4 lanes/thread, v4 io"};
+  void (*fns[4])(const uint32_t*, const uint32_t*, uint32_t, uint64_t, uint64_t*, uint32_t*) = {k<0>, k<1>, kvec,
+                                                                                              k<2>};
+  const char* names[4] = {"register stores", "smem + bulk stores", "4 lanes/thread, v4 io",
+                          "register stores, 8 B out (packed)"};
   uint64_t* check = (uint64_t*)malloc(1 << 20);
-  for (int m = 0; m < 3; ++m) {
+  for (int m = 0; m < 4; ++m) {
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);

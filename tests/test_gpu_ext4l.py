@@ -80,3 +80,28 @@ def test_4l_copy_roundtrip_across_page_sizes(cuda):
     assert X.walk4(mem, t.root, gva) == X.walk4(mem, t.root, gva - 5)
     with pytest.raises(er.PageFault):
         X.walk4(mem, t.root, X.C3_VA + region + 4096)
+
+
+def test_c1_in_4level_geometry(cuda):
+    """BASELINE configs[0] as written (4-level 4 KiB table, 16,384 shuffled
+    pages, 1 M random VAs + a 64 MiB copy_to_user, aligned and +0x800) vs
+    the C restatement."""
+    mem, t = X.build_c1_4l()
+    vas = X.c1_4l_vas()
+    st = _check(mem, t, vas)
+    assert (st == 0).all()
+    # faults past the mapped region and above it at every level
+    rng = np.random.default_rng(7)
+    wild = np.concatenate([X.C1_4L_VA + rng.integers(64 << 20, 1 << 32, 50_000, dtype=np.int64).astype(np.uint64),
+                           rng.integers(0, 1 << 48, 50_000, dtype=np.int64).astype(np.uint64)])
+    st = _check(mem, t, wild)
+    assert (st != 0).any()
+    sp = t.space
+    for off, n in ((0, 64 << 20), (0x800, (64 << 20) - 4096)):
+        src = torch.randint(0, 256, (n,), dtype=torch.uint8, device="cuda")
+        raw = mem.backing.host_for_read().copy()
+        outs = dp.copy_ops(mem.backing, [sp], np.array([[X.C1_4L_VA + off, n, 0, 0]], np.uint64), N.TO_GUEST, src)
+        assert outs[0].status == 0 and outs[0].copied == n
+        O.copy(raw, O.space(sp.s1_base, sp.s1_root_pfn, 0, N.ONE_STAGE_4L).reshape(1, 4),
+               np.array([[X.C1_4L_VA + off, n, 0, 0]], np.uint64), src.cpu().numpy(), 0, threads=0)
+        assert np.array_equal(mem.backing.host_for_read(), raw)

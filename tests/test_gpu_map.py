@@ -126,7 +126,8 @@ def test_c5_scaled_world_device_equals_host(cuda, monkeypatch):
     cfg = W.C5Config().scaled(32)
     monkeypatch.setenv("PV_DEVICE_MAP", "1")
     a = W.build_c5(cfg, device=True)
-    assert a.memv.host_mem.backing._dev_dirty_any or a.memv.host_mem.backing.host_epoch > 0
+    img = a.memv.host_mem.backing
+    assert img._dev_dirty_any or img._pending_any or img.host_epoch > 0
     da = _digest(a.memv)
     del a
     monkeypatch.setenv("PV_DEVICE_MAP", "0")
