@@ -53,7 +53,9 @@ def full(rep: str, out: str) -> None:
         f.write("\n".join(lines))
 
 
-def launches(path: str, out: str, pattern: str = r"translate_kernel|plan_kernel|stamp_kernel|exec_kernel|fifo") -> None:
+def launches(path: str, out: str,
+             pattern: str = r"translate|plan_kernel|stamp_kernel|exec|shim|stage_table|fifo|ordered|frame|index|"
+                            r"encode|map_|pair|classify|identify|cub::|Device") -> None:
     rows = list(csv.reader(open(path)))
     hdr = None
     items = []
