@@ -55,9 +55,12 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true", help="skip the full-size parity check against the oracle "
                     "after the timed steps")
-    ap.add_argument("--unpacked", dest="packed", action="store_false", help="C5/C1: the walk writes the "
-                    "(u64 value, u32 status) arrays instead of PV_OUT_PACKED lane words (8 B per lane; the "
-                    "default, decoded for the parity check)")
+    ap.add_argument("--walk-form", choices=["words", "packed", "unpacked"], default="words",
+                    help="C5/C1: what the walk writes per lane -- a 4-byte pv_translate_words word + exception "
+                    "records (default), a PV_OUT_PACKED u64, or the (u64 value, u32 status) pair; decoded for "
+                    "the parity check, and the next form is timed beside it in the same run")
+    ap.add_argument("--unpacked", dest="walk_form", action="store_const", const="unpacked",
+                    help="same as --walk-form unpacked")
     ap.add_argument("--overlap", action="store_true", help="time C5/C1 steps with the walk on a second stream "
                     "beside plan + exec (A/B option: measured slower than back-to-back phases, "
                     "profiles/r02_overlap_ab.md)")
@@ -294,8 +297,18 @@ def run_ours(args, rank, world, local):
     shim_scratch = dp._shim_scratch(img, plan.n_pages) if plan.shims is not None else None
     hint = dp.exec_hint(plan, wl.src.data_ptr())
 
+    form = args.walk_form
+    if form == "words":  # one 4-byte word per lane + exception records (pv_translate_words)
+        w_words = torch.empty(wl.n_vas, dtype=torch.int32, device="cuda")
+        w_cap = min(wl.n_vas, 1 << 20)
+        w_rec = torch.empty(w_cap * N.EXC_WORDS, dtype=torch.int64, device="cuda")
+        w_cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+
     def phase_translate():
-        if args.packed:  # PV_OUT_PACKED: one u64 per lane, no status array
+        if form == "words":
+            w_cnt.zero_()
+            dp.translate_words(img, wl.tplan, wl.vas, w_words, w_rec, w_cnt)
+        elif form == "packed":  # PV_OUT_PACKED: one u64 per lane, no status array
             dp.translate_lanes(img, wl.tplan, wl.vas, out=(wl.out[0], None, wl.out[2]), packed=True)
         else:
             dp.translate_lanes(img, wl.tplan, wl.vas, out=wl.out)
@@ -435,21 +448,41 @@ def run_ours(args, rank, world, local):
     res = plan.results.cpu().numpy().view(np.uint64)
     assert (res[:, 3] & 0xFFFFFFFF == 0).all() and (res[:, 0] == plan.host_ops[:, 1]).all()
     other = None
-    if args.packed:  # decode the timed step's lane words for the checks below
-        v, st_ = dp.unpack_lanes(wl.out[0].cpu().numpy(), wl.out[2].cpu().numpy())
+    n_exc = None
+    if form != "unpacked":  # decode the timed step's lane words for the checks below
+        if form == "words":
+            n_exc = int(w_cnt.item())
+            assert n_exc <= w_cap, "more exception lanes than the bench's record list holds"
+            exc = dp.LaneExceptions.from_records(w_rec[:n_exc * N.EXC_WORDS].cpu().numpy())
+            v, st_, _ = dp.unpack_words(w_words.cpu().numpy(), wl.vas.cpu().numpy(), exc)
+        else:
+            v, st_ = dp.unpack_lanes(wl.out[0].cpu().numpy(), wl.out[2].cpu().numpy())
         wl.out[0].copy_(torch.from_numpy(v.view(np.int64)))
         wl.out[1].copy_(torch.from_numpy(st_.view(np.int32)))
-        # A/B in the same run: the walk in the (value, status) form, K launches, same lanes and results
+        # A/B in the same run: the walk in the next wider form, K launches, same lanes and results
         o2 = (torch.empty_like(wl.out[0]), torch.empty_like(wl.out[1]), torch.zeros_like(wl.out[2]))
+        wide = form == "words"  # words -> PV_OUT_PACKED u64; packed -> (value, status)
+
+        def other_walk():
+            if wide:
+                dp.translate_lanes(img, wl.tplan, wl.vas, out=(o2[0], None, o2[2]), packed=True)
+            else:
+                dp.translate_lanes(img, wl.tplan, wl.vas, out=o2)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        dp.translate_lanes(img, wl.tplan, wl.vas, out=o2)
+        other_walk()
         e0.record(stream)
         for _ in range(args.steps):
-            dp.translate_lanes(img, wl.tplan, wl.vas, out=o2)
+            other_walk()
         e1.record(stream)
         torch.cuda.synchronize()
-        other = {"form": "unpacked (u64 value + u32 status)", "translate_ms_per_step": e0.elapsed_time(e1) / args.steps,
-                 "launch": "eager", "results_equal": bool(torch.equal(o2[0], wl.out[0]) and torch.equal(o2[1], wl.out[1]))}
+        if wide:
+            ov, os_ = dp.unpack_lanes(o2[0].cpu().numpy(), o2[2].cpu().numpy())
+            same = bool(np.array_equal(ov, v) and np.array_equal(os_, st_))
+        else:
+            same = bool(torch.equal(o2[0], wl.out[0]) and torch.equal(o2[1], wl.out[1]))
+        other = {"form": "PV_OUT_PACKED (one u64 per lane)" if wide else "unpacked (u64 value + u32 status)",
+                 "translate_ms_per_step": e0.elapsed_time(e1) / args.steps, "launch": "eager",
+                 "results_equal": same}
     n_faults = int((wl.out[1] != 0).sum().item())
     tr_ms = sum(e[0].elapsed_time(e[1]) for e in evs)
     serial_ms = sum(e[0].elapsed_time(e[4]) for e in evs)
@@ -482,7 +515,8 @@ def run_ours(args, rank, world, local):
 
     peak, peak_kind = peaks()
     exec_achieved = 2 * wl.copy_bytes * K / (exec_ms / 1e3) / 1e9
-    walk_bytes = (12 if args.packed else 16) * wl.n_vas  # u32 VA in + u64 hpa (+ u32 status) out
+    # u32 VA in + (u32 word | u64 lane word | u64 hpa + u32 status) out
+    walk_bytes = {"words": 8, "packed": 12, "unpacked": 16}[form] * wl.n_vas
     walk_achieved = walk_bytes * K / (tr_ms / 1e3) / 1e9
     walk_bytes_pte = walk_bytes + 8 * _leaf_ptes(wl)  # + 8 B per distinct leaf PTE
     walk_achieved_pte = walk_bytes_pte * K / (tr_ms / 1e3) / 1e9
@@ -505,7 +539,10 @@ def run_ours(args, rank, world, local):
                  "ms_per_step": copy_ms / K, "exec_ms_per_step": exec_ms / K,
                  "plan_shim_stamp_ms_per_step": plan_ms / K},
         "translate_ms_per_step": tr_ms / K,
-        "walk_form": "PV_OUT_PACKED (one u64 per lane)" if args.packed else "unpacked (u64 value + u32 status)",
+        "walk_form": {"words": "pv_translate_words (one u32 per lane + exception records)",
+                      "packed": "PV_OUT_PACKED (one u64 per lane)",
+                      "unpacked": "unpacked (u64 value + u32 status)"}[form],
+        "exception_records": n_exc,
         "walk_other_form": other,
         "step": {"mode": "overlapped" if overlap else "serial",
                  "ms": total_ms / K, "serial_ms": serial_ms / K,
@@ -533,10 +570,12 @@ def run_ours(args, rank, world, local):
                           "with_leaf_ptes": {"algorithmic_bytes_per_launch": walk_bytes_pte,
                                              "distinct_leaf_ptes": _leaf_ptes(wl), "achieved": walk_achieved_pte,
                                              "frac": walk_achieved_pte / peak},
-                          "note": ("12 B/translation (u32 VA in, one u64 lane word out)" if args.packed else
-                                   "16 B/translation (u32 VA in, u64 hpa + u32 status out)") + "; with_leaf_ptes adds "
+                          "note": {"words": "8 B/translation (u32 VA in, one u32 lane word out)",
+                                   "packed": "12 B/translation (u32 VA in, one u64 lane word out)",
+                                   "unpacked": "16 B/translation (u32 VA in, u64 hpa + u32 status out)"}[form]
+                                  + "; with_leaf_ptes adds "
                                   "SURVEY.md 8(d)'s 8 B per distinct leaf PTE touched",
-                          "gather_sol": walker_sol(wl.n_vas * K / (tr_ms / 1e3), args.packed),
+                          "gather_sol": walker_sol(wl.n_vas * K / (tr_ms / 1e3), form),
                           "ncu": load_json_profile("walker_ncu.json")},
         "faulting_lanes": n_faults,
         "parity": parity,
@@ -1144,23 +1183,24 @@ def run_e2e(wl, args, world):
     from paper_1304_3771_b200 import memvirt as mv
 
     io = {}
-    # results: one PV_OUT_PACKED word per lane (the hpa, or the status and value of the exception the
-    # lane raises).  At N > 1 the words of every rank land in one host buffer all ranks map
-    # (shard.SharedHostBuffer): rank 0 holds every guest's results after the step's barrier.
+    # results: one pv_translate_words word per lane (the frame number, or the status of the exception
+    # the lane raises; the lanes whose exception value is not their own va also return a record) -- 4
+    # bytes back per 4-byte VA in.  At N > 1 the words of every rank land in one host buffer all ranks
+    # map (shard.SharedHostBuffer): rank 0 holds every guest's results after the step's barrier.
     shared = None
     pg = world > 1 and _pg()
     if pg:
         from paper_1304_3771_b200 import shard as _sh
 
-        shared = _sh.SharedHostBuffer(wl.total_vas * 8, int(os.environ.get("RANK", "0")), world, tag="pv_e2e")
-        res_out = [(shared.view(torch.int64, l0, len(v)), None, None)
+        shared = _sh.SharedHostBuffer(wl.total_vas * 4, int(os.environ.get("RANK", "0")), world, tag="pv_e2e")
+        res_out = [(shared.view(torch.int32, l0, len(v)), None, None)
                    for l0, (_, _, v) in zip(wl.proc_lane0, wl.proc_vas)]
     else:  # caller-owned pinned result buffers, reused every step
-        res_out = [(torch.empty(len(v), dtype=torch.int64, pin_memory=True), None, None) for _, _, v in wl.proc_vas]
+        res_out = [(torch.empty(len(v), dtype=torch.int32, pin_memory=True), None, None) for _, _, v in wl.proc_vas]
 
     def one_step():
         t0 = time.perf_counter()
-        io["res"] = mv.translate_many([(translators[(g, p)], t) for t, g, p in host_vas], packed=True, out=res_out)
+        io["res"] = mv.translate_many([(translators[(g, p)], t) for t, g, p in host_vas], words=True, out=res_out)
         if pg:
             tdist.barrier()  # every rank's words are in the shared buffer: rank 0 holds all results
         t1 = time.perf_counter()
@@ -1192,8 +1232,8 @@ def run_e2e(wl, args, world):
     dev_v = wl.out[0].cpu().numpy().view(np.uint64)
     dev_s = wl.out[1].cpu().numpy().view(np.uint32)
     lane, same = 0, True
-    for (words, _, aux), (_, _, v) in zip(io["res"], wl.proc_vas):
-        uv, us = dp.unpack_lanes(words.numpy(), None if aux.stride(0) == 0 else aux.numpy())
+    for (words, _, exc), (t, _, _), (_, _, v) in zip(io["res"], host_vas, wl.proc_vas):
+        uv, us, _ = dp.unpack_words(words.numpy(), t.numpy(), exc)
         same &= bool(np.array_equal(uv, dev_v[lane:lane + len(v)]) and np.array_equal(us, dev_s[lane:lane + len(v)]))
         lane += len(v)
     returned = None
@@ -1201,7 +1241,7 @@ def run_e2e(wl, args, world):
         # the words rank 0 reads in the shared buffer are every rank's own results
         mine = hashlib.sha256()
         for l0, (_, _, v) in zip(wl.proc_lane0, wl.proc_vas):
-            mine.update(shared.view(torch.int64, l0, len(v)).numpy().tobytes())
+            mine.update(shared.view(torch.int32, l0, len(v)).numpy().tobytes())
         got = [None] * world
         tdist.all_gather_object(got, (mine.hexdigest(), list(zip(wl.proc_lane0, [len(v) for *_, v in wl.proc_vas]))))
         ok = None
@@ -1210,19 +1250,20 @@ def run_e2e(wl, args, world):
             for digest, spans in got:
                 h = hashlib.sha256()
                 for l0, n in spans:
-                    h.update(shared.view(torch.int64, l0, n).numpy().tobytes())
+                    h.update(shared.view(torch.int32, l0, n).numpy().tobytes())
                 ok &= h.hexdigest() == digest
         returned = {"to_rank0": "shared host buffer (/dev/shm, cudaHostRegister'd by every rank): each rank's "
                                 "D2H writes its guests' lane words where rank 0 reads them; one barrier per step",
-                    "bytes": wl.total_vas * 8, "verified": ok}
+                    "bytes": wl.total_vas * 4, "verified": ok}
         shared.close()
     return {"value": wl.total_vas * steps / tr_s, "unit": "translations/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "copy": {"value": wl.total_copy_bytes * steps / cp_s / 1e9, "unit": "GB/s"},
-            "steps": steps, "results": "one PV_OUT_PACKED word per lane (hpa, or status + value)",
+            "steps": steps, "results": "one pv_translate_words word per lane (frame number, or status; "
+                                       "exception records for lanes whose value is not their va)",
             "lanes_equal_device_results": same,
             "gather_to_rank0": returned,
-            "api": "memvirt.translate_many(packed=True) (ProcessTranslator.translate_batch over every process) + "
+            "api": "memvirt.translate_many(words=True) (ProcessTranslator.translate_batch over every process) + "
                    "HardwareHasAccess.copy_to_user_batch"}
 
 
@@ -1244,18 +1285,22 @@ class _Prebuilt:
         return self.root
 
 
-def walker_sol(lanes_per_s: float, packed: bool = False):
+def walker_sol(lanes_per_s: float, form: str = "unpacked"):
     """The walker against the measured speed of light of its access pattern
     (random 4-byte gathers + the lane stream: 12 B/lane unpacked, 8 B/lane
-    packed out; profiles/walker_sol.json)."""
+    packed, 4 B/lane as words out; profiles/walker_sol.json)."""
     try:
         with open(os.path.join(ROOT, "profiles", "walker_sol.json")) as f:
             sol = json.load(f)
     except Exception:  # noqa: BLE001
         return None
-    probe = sol.get("lanes_per_s_packed", sol["lanes_per_s"]) if packed else sol["lanes_per_s"]
+    key = {"words": "lanes_per_s_words", "packed": "lanes_per_s_packed"}.get(form, "lanes_per_s")
+    if key not in sol:
+        return None
+    probe = sol[key]
     return {"achieved": lanes_per_s, "probe": probe, "unit": "lanes/s", "frac": lanes_per_s / probe,
-            "form": "packed (8 B out)" if packed else "unpacked (12 B out)", "source": "profiles/walker_sol.json"}
+            "form": {"words": "words (4 B out)", "packed": "packed (8 B out)"}.get(form, "unpacked (12 B out)"),
+            "source": "profiles/walker_sol.json"}
 
 
 def load_traffic(workload: str) -> dict:

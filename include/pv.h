@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define PV_ABI_VERSION 4
+#define PV_ABI_VERSION 5
 
 /* ---- return codes ------------------------------------------------------ */
 #define PV_SUCCESS 0
@@ -231,6 +231,42 @@ int pv_translate(const uint8_t* image, uint64_t image_bytes,
                  const pv_index* index,
                  uint64_t* out_value, uint32_t* out_status, uint64_t* out_aux,
                  void* stream);
+
+/* ---- K1, 4-byte lane words -------------------------------------------------
+ * The same batch walk as pv_translate (same replacements, spaces, segs,
+ * vas, flags except PV_OUT_PACKED, index), with one 4-byte word per lane in
+ * out_word -- half the bytes of PV_OUT_PACKED to store and to move to the
+ * host, which bounds a host-fed batch (the VAs go in at 4 bytes per lane):
+ *   bit 31 clear   the lane translated: the word is its frame number (the
+ *                  hpa / gpa >> 12; the value is word << 12 | (va & 0xFFF),
+ *                  or the word itself under PV_OUT_PFN);
+ *   PV_W32_ERR     the lane raises: bits 0-20 hold the compact status (as
+ *                  PV_OUT_PACKED: (status & 0xFFF) | index << 12), and
+ *     | PV_W32_VA  the exception's value is the lane's own va (page faults
+ *                  and out-of-range nodes of a one-stage walk), or
+ *     otherwise    the value (and the TDP-stage trap gpa, aux) is in an
+ *                  exception record: exc[k] for some k < *exc_count, with
+ *                  exc[k].lane = lane_base + lane.
+ * *exc_count (device) is advanced atomically and never reset here (zero it
+ * before the first call of a series that shares it); records past exc_cap
+ * are counted but not written -- the caller re-runs with a larger list.
+ * Record order is unspecified (one record per lane). */
+#define PV_W32_ERR 0x80000000u
+#define PV_W32_VA 0x40000000u
+#define PV_W32_COMPACT_MASK 0x1FFFFFu
+typedef struct pv_exc {
+  uint64_t lane;   /* lane_base + lane index of the batch                   */
+  uint64_t value;  /* the exception's value (trap node, gpa, ...)          */
+  uint64_t aux;    /* TDP-stage trap gpa (0 otherwise)                      */
+  uint32_t status; /* full status word                                      */
+  uint32_t reserved;
+} pv_exc;
+int pv_translate_words(const uint8_t* image, uint64_t image_bytes,
+                       const pv_space* spaces, const pv_seg* segs, uint32_t n_segs,
+                       uint64_t n_chunks, const void* vas, uint32_t flags,
+                       const pv_index* index, uint32_t* out_word,
+                       pv_exc* exc, uint64_t exc_cap, unsigned long long* exc_count,
+                       uint64_t lane_base, void* stream);
 
 /* ---- K4: FIFO cache replay --------------------------------------------------
  * Applies the per-process FIFO translation cache (memvirt.py:336-374,

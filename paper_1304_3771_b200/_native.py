@@ -18,7 +18,7 @@ from .errors import NativeUnavailable
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpv.so")
 
 # ---- constants mirrored from include/pv.h --------------------------------
-ABI_VERSION = 4
+ABI_VERSION = 5
 SUCCESS = 0
 EINVAL = -22
 ENOMEM = -12
@@ -46,6 +46,10 @@ OUT_PACKED = 0x8  # pv.h PV_OUT_PACKED: one u64 per lane
 PACKED_ERR = 1 << 63
 PACKED_VALUE_BITS = 42
 PACKED_SPILL_VALUE = (1 << 42) - 1
+W32_ERR = 0x80000000  # pv.h pv_translate_words lane words
+W32_VA = 0x40000000
+W32_COMPACT_MASK = 0x1FFFFF
+EXC_WORDS = 4         # sizeof(pv_exc) / 8
 HAS_TWO_STAGE = 0x80000000
 HAS_4L = 0x40000000
 
@@ -71,7 +75,7 @@ FIFO_WORDS = 2 * FIFO_MAX + 4  # pv_fifo
 
 # every symbol include/pv.h declares
 EXPORTS = (
-    "pv_abi_version", "pv_translate_chunk", "pv_status_name", "pv_translate",
+    "pv_abi_version", "pv_translate_chunk", "pv_status_name", "pv_translate", "pv_translate_words",
     "pv_fifo_replay", "pv_copy_plan", "pv_copy_plan_nodes", "pv_copy_stamp", "pv_copy_exec",
     "pv_copy_fifo_replay", "pv_scatter_pages", "pv_gather_pages", "pv_stream_sync", "pv_index_encode",
     "pv_fifo_scratch_bytes", "pv_copy_ordered_scratch_bytes", "pv_copy_ordered", "pv_result_encode",
@@ -90,6 +94,7 @@ _SIGNATURES = {
     "pv_translate_chunk": (_u64, []),
     "pv_status_name": (ctypes.c_char_p, [_u32]),
     "pv_translate": (ctypes.c_int, [_p, _u64, _p, _p, _u32, _u64, _p, _u32, _p, _p, _p, _p, _p]),
+    "pv_translate_words": (ctypes.c_int, [_p, _u64, _p, _p, _u32, _u64, _p, _u32, _p, _p, _p, _u64, _p, _u64, _p]),
     "pv_index_encode": (ctypes.c_int, [_p, _u64, _p, _p, _u64, _u64, _p, _p, _p]),
     "pv_fifo_replay": (ctypes.c_int, [_p, _u32, _p, _p, _p, _u32, _u64, _u64, _u32, _p, _p, _p, _p, _u64, _p]),
     "pv_fifo_scratch_bytes": (_u64, [_u64, _u64, _u32]),

@@ -12,7 +12,7 @@
 namespace pv {
 cudaError_t launch_translate(const uint8_t*, uint64_t, const pv_space*, const pv_seg*, uint32_t, uint64_t,
                              const void*, uint32_t, bool, const pv_index*, uint64_t*, uint32_t*, uint64_t*,
-                             cudaStream_t);
+                             const ExcSink*, cudaStream_t);
 cudaError_t launch_index_encode(const uint8_t*, uint64_t, const uint64_t*, const uint64_t*, uint64_t, uint64_t,
                                 uint32_t*, const uint8_t*, cudaStream_t);
 uint64_t translate_chunk();
@@ -235,7 +235,26 @@ int pv_translate(const uint8_t* image, uint64_t image_bytes, const pv_space* spa
   if (index != nullptr && (!index->slot_of || !index->leaf_codes || !index->slot_page)) return PV_EINVAL;
   return rc(launch_translate(image, image_bytes, spaces, segs, n_segs, n_chunks, vas,
                              flags & (PV_VA32 | PV_OUT_PFN | PV_OUT_PACKED | PV_CONCURRENT | PV_HAS_4L), two, index,
-                             out_value, out_status, out_aux, (cudaStream_t)stream));
+                             out_value, out_status, out_aux, nullptr, (cudaStream_t)stream));
+}
+
+int pv_translate_words(const uint8_t* image, uint64_t image_bytes, const pv_space* spaces, const pv_seg* segs,
+                       uint32_t n_segs, uint64_t n_chunks, const void* vas, uint32_t flags, const pv_index* index,
+                       uint32_t* out_word, pv_exc* exc, uint64_t exc_cap, unsigned long long* exc_count,
+                       uint64_t lane_base, void* stream) {
+  if (n_chunks == 0) return PV_SUCCESS;
+  if (!image || !spaces || !segs || !vas || !out_word || !exc_count || (!exc && exc_cap) || n_segs == 0)
+    return PV_EINVAL;
+  if (image_bytes % kPageSize) return PV_EINVAL;
+  // frame numbers fill 28 bits of a word (and of the walk codes)
+  if (image_bytes >= (1ull << 40)) return PV_EINVAL;
+  if (flags & ~(uint32_t)(PV_VA32 | PV_OUT_PFN | PV_CONCURRENT | PV_HAS_TWO_STAGE | PV_HAS_4L)) return PV_EINVAL;
+  if (index != nullptr && (!index->slot_of || !index->leaf_codes || !index->slot_page)) return PV_EINVAL;
+  const ExcSink sink{exc, exc_cap, exc_count, lane_base};
+  return rc(launch_translate(image, image_bytes, spaces, segs, n_segs, n_chunks, vas,
+                             flags & (PV_VA32 | PV_OUT_PFN | PV_CONCURRENT | PV_HAS_4L), flags & PV_HAS_TWO_STAGE,
+                             index, reinterpret_cast<uint64_t*>(out_word), nullptr, nullptr, &sink,
+                             (cudaStream_t)stream));
 }
 
 int pv_index_encode(const uint8_t* image, uint64_t image_bytes, const uint64_t* slot_page, const uint64_t* slots,

@@ -217,6 +217,40 @@ __device__ __forceinline__ uint64_t pack_lane(uint32_t st, uint64_t v, bool* spi
   return PV_PACKED_ERR | (compact << PV_PACKED_VALUE_BITS) | low;
 }
 
+// Output forms of a translate launch (pv_translate / pv_translate_words).
+constexpr uint32_t kOutSplit = 0;   // u64 value + u32 status (+ aux)
+constexpr uint32_t kOutPacked = 1;  // PV_OUT_PACKED u64 lane words
+constexpr uint32_t kOutWord = 2;    // pv_translate_words: u32 lane words + exception records
+
+// Exception list of a kOutWord launch (pv.h pv_translate_words).
+struct ExcSink {
+  pv_exc* rec;
+  uint64_t cap;
+  unsigned long long* count;
+  uint64_t lane_base;
+};
+
+// 4-byte lane word (pv.h pv_translate_words) of lane i; appends the lane's
+// exception record when the word alone cannot carry its value.  v: the frame
+// number of a lane that translated, else the exception's value.
+__device__ __forceinline__ uint32_t word_lane(uint32_t st, uint64_t v, uint64_t va, uint64_t aux, uint64_t i,
+                                              const ExcSink& x) {
+  if (st == PV_ST_OK) return (uint32_t)v;
+  const uint32_t compact = (st & 0xFFFu) | (((st >> 16) & 0x1FFu) << 12);
+  if (v == va && PV_ST_KIND(st) != PV_ST_TRAP2) return PV_W32_ERR | PV_W32_VA | compact;
+  const unsigned long long k = atomicAdd(x.count, 1ull);
+  if (k < x.cap) {
+    pv_exc r;
+    r.lane = x.lane_base + i;
+    r.value = v;
+    r.aux = aux;
+    r.status = st;
+    r.reserved = 0;
+    x.rec[k] = r;
+  }
+  return PV_W32_ERR | compact;
+}
+
 __host__ __device__ __forceinline__ uint64_t page_span(uint64_t gva, uint64_t len) {
   return len == 0 ? 0 : ((gva + len - 1) >> kPageShift) - (gva >> kPageShift) + 1;
 }

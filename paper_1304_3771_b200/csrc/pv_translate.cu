@@ -222,7 +222,7 @@ translate_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const 
                  const uint32_t* __restrict__ slot_of, const uint32_t* __restrict__ leaf_codes,
                  const uint64_t* __restrict__ slot_page,
                  uint64_t* __restrict__ out_value, uint32_t* __restrict__ out_status, uint64_t* __restrict__ out_aux,
-                 bool packed) {
+                 uint32_t mode, ExcSink sink) {
   constexpr int VPT = (int)(kChunk / TPB);
   __shared__ __align__(16) uint32_t codes1[4 * 512];
   __shared__ __align__(16) uint32_t codes2[kTwo ? 4 * 512 : 1];
@@ -366,8 +366,12 @@ translate_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const 
             const uint64_t i = lane0 + (uint64_t)j * TPB + threadIdx.x;
             if (i >= seg_end) continue;
             const uint64_t pfn = lc[j] >> 2;
+            if (mode == kOutWord) {
+              st_u32_stream(reinterpret_cast<uint32_t*>(out_value) + i, (uint32_t)pfn, pol_stream);
+              continue;
+            }
             st_u64_stream(out_value + i, kPfn ? pfn : ((pfn << kPageShift) | (va[j] & kPageMask)), pol_stream);
-            if (!packed) st_u32_stream(out_status + i, PV_ST_OK, pol_stream);
+            if (mode == kOutSplit) st_u32_stream(out_status + i, PV_ST_OK, pol_stream);
           }
           continue;
         }
@@ -416,8 +420,14 @@ translate_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const 
       const uint64_t i = lane0 + (uint64_t)j * TPB + threadIdx.x;
       if (i >= seg_end) continue;
       uint64_t v = val[j];
+      if (mode == kOutWord) {
+        st_u32_stream(reinterpret_cast<uint32_t*>(out_value) + i,
+                      word_lane(st[j], v, (uint64_t)va[j], kTwo ? aux[j] : 0, i, sink),
+                      pol_stream);
+        continue;
+      }
       if (!kPfn && st[j] == PV_ST_OK) v = (v << kPageShift) | (va[j] & kPageMask);
-      if (packed) {
+      if (mode == kOutPacked) {
         bool spill;
         st_u64_stream(out_value + i, pack_lane(st[j], v, &spill), pol_stream);
         if (spill && out_aux != nullptr) out_aux[i] = v;
@@ -444,7 +454,8 @@ __global__ void __launch_bounds__(kGenTpb)
 translate_generic_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes,
                          const pv_space* __restrict__ spaces, const pv_seg* __restrict__ segs, uint32_t n_segs,
                          uint64_t n_chunks, const void* __restrict__ vas, uint64_t* __restrict__ out_value,
-                         uint32_t* __restrict__ out_status, uint64_t* __restrict__ out_aux, bool packed) {
+                         uint32_t* __restrict__ out_status, uint64_t* __restrict__ out_aux, uint32_t mode,
+                         ExcSink sink) {
   for (uint64_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
     uint32_t lo = 0, hi = n_segs;
     while (hi - lo > 1) {
@@ -461,8 +472,13 @@ translate_generic_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes
       const uint64_t va = kVa32 ? (uint64_t)((const uint32_t*)vas)[i] : ((const uint64_t*)vas)[i];
       uint64_t v = 0, a = 0;
       const uint32_t st = translate_global(image, image_bytes, sp, va, &v, &a);
+      if (mode == kOutWord) {
+        reinterpret_cast<uint32_t*>(out_value)[i] =
+            word_lane(st, v, va, PV_ST_KIND(st) == PV_ST_TRAP2 ? a : 0, i, sink);
+        continue;
+      }
       if (!kPfn && st == PV_ST_OK) v = (v << kPageShift) | (va & kPageMask);
-      if (packed) {
+      if (mode == kOutPacked) {
         bool spill;
         out_value[i] = pack_lane(st, v, &spill);
         if (spill && out_aux != nullptr) out_aux[i] = v;
@@ -478,14 +494,14 @@ translate_generic_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes
 template <bool kVa32, bool kPfn>
 static cudaError_t launch_generic(const uint8_t* image, uint64_t image_bytes, const pv_space* spaces,
                                   const pv_seg* segs, uint32_t n_segs, uint64_t n_chunks, const void* vas,
-                                  uint64_t* out_value, uint32_t* out_status, uint64_t* out_aux, bool packed,
-                                  cudaStream_t stream) {
+                                  uint64_t* out_value, uint32_t* out_status, uint64_t* out_aux, uint32_t mode,
+                                  const ExcSink& sink, cudaStream_t stream) {
   auto k = translate_generic_kernel<kVa32, kPfn>;
   uint64_t grid = resident_grid((const void*)k, kGenTpb, 0);
   if (grid > n_chunks) grid = n_chunks;
   if (grid == 0) return cudaSuccess;
   k<<<(unsigned)grid, kGenTpb, 0, stream>>>(image, image_bytes, spaces, segs, n_segs, n_chunks, vas, out_value,
-                                         out_status, out_aux, packed);
+                                         out_status, out_aux, mode, sink);
   return cudaGetLastError();
 }
 
@@ -493,7 +509,7 @@ template <bool kTwo, bool kVa32, bool kPfn>
 static cudaError_t launch_t(const uint8_t* image, uint64_t image_bytes, const pv_space* spaces, const pv_seg* segs,
                             uint32_t n_segs, uint64_t n_chunks, const void* vas, const pv_index* idx,
                             uint64_t* out_value, uint32_t* out_status, uint64_t* out_aux, bool concurrent,
-                            bool packed, cudaStream_t stream) {
+                            uint32_t mode, const ExcSink& sink, cudaStream_t stream) {
   // one-stage walks: 512-thread CTAs x 4 lanes (2 CTAs/SM) measured best on
   // C5 (scripts/ab_walk.sh: 0.848 ms vs 0.858 at 1024 x 2 and 0.923 at 128 x 16)
 #ifndef PV_TR_MINB
@@ -522,7 +538,7 @@ static cudaError_t launch_t(const uint8_t* image, uint64_t image_bytes, const pv
   if (n_chunks < 8 * grid) {
     // few chunks per CTA: each CTA stages its (usually one) segment itself
     k<<<(unsigned)grid, tpb, 0, stream>>>(image, image_bytes, spaces, segs, n_segs, n_chunks, vas, nullptr, nullptr,
-                                          slot_of, leaf_codes, slot_page, out_value, out_status, out_aux, packed);
+                                          slot_of, leaf_codes, slot_page, out_value, out_status, out_aux, mode, sink);
     return cudaGetLastError();
   }
   // per-segment stage tables: stream-ordered scratch (per call, so calls on
@@ -536,7 +552,7 @@ static cudaError_t launch_t(const uint8_t* image, uint64_t image_bytes, const pv
   stage_table_kernel<<<dim3(n_segs, 4, kTwo ? 2 : 1), 512, 0, stream>>>(image, image_bytes, spaces, segs, kTwo,
                                                                          slot_of, g_codes, g_stages);
   k<<<(unsigned)grid, tpb, 0, stream>>>(image, image_bytes, spaces, segs, n_segs, n_chunks, vas, g_codes, g_stages,
-                                        slot_of, leaf_codes, slot_page, out_value, out_status, out_aux, packed);
+                                        slot_of, leaf_codes, slot_page, out_value, out_status, out_aux, mode, sink);
   e = cudaGetLastError();
   cudaFreeAsync(tab, stream);
   return e;
@@ -545,23 +561,26 @@ static cudaError_t launch_t(const uint8_t* image, uint64_t image_bytes, const pv
 cudaError_t launch_translate(const uint8_t* image, uint64_t image_bytes, const pv_space* spaces, const pv_seg* segs,
                              uint32_t n_segs, uint64_t n_chunks, const void* vas, uint32_t flags, bool two_stage,
                              const pv_index* idx, uint64_t* out_value, uint32_t* out_status, uint64_t* out_aux,
-                             cudaStream_t stream) {
+                             const ExcSink* words, cudaStream_t stream) {
   const bool va32 = flags & PV_VA32, pfn = flags & PV_OUT_PFN;
+  // words != nullptr: pv_translate_words (out_value holds u32 lane words)
+  const uint32_t mode = words != nullptr ? kOutWord : (flags & PV_OUT_PACKED) ? kOutPacked : kOutSplit;
+  const ExcSink sink = words != nullptr ? *words : ExcSink{nullptr, 0, nullptr, 0};
   if (flags & PV_HAS_4L) {
     if (va32) return pfn ? launch_generic<true, true>(image, image_bytes, spaces, segs, n_segs, n_chunks, vas,
-                                                      out_value, out_status, out_aux, flags & PV_OUT_PACKED, stream)
+                                                      out_value, out_status, out_aux, mode, sink, stream)
                          : launch_generic<true, false>(image, image_bytes, spaces, segs, n_segs, n_chunks, vas,
-                                                       out_value, out_status, out_aux, flags & PV_OUT_PACKED, stream);
+                                                       out_value, out_status, out_aux, mode, sink, stream);
     return pfn ? launch_generic<false, true>(image, image_bytes, spaces, segs, n_segs, n_chunks, vas, out_value,
-                                             out_status, out_aux, flags & PV_OUT_PACKED, stream)
+                                             out_status, out_aux, mode, sink, stream)
                : launch_generic<false, false>(image, image_bytes, spaces, segs, n_segs, n_chunks, vas, out_value,
-                                              out_status, out_aux, flags & PV_OUT_PACKED, stream);
+                                              out_status, out_aux, mode, sink, stream);
   }
   if (image_bytes >= (1ull << 40)) return cudaErrorInvalidValue;  // leaf pfns / slots must fit 28-bit codes
 #define PV_DISPATCH(T, V, P)                                                                                    \
   if (two_stage == T && va32 == V && pfn == P)                                                                  \
     return launch_t<T, V, P>(image, image_bytes, spaces, segs, n_segs, n_chunks, vas, idx, out_value, \
-                             out_status, out_aux, flags & PV_CONCURRENT, flags & PV_OUT_PACKED, stream);
+                             out_status, out_aux, flags & PV_CONCURRENT, mode, sink, stream);
   PV_DISPATCH(false, false, false)
   PV_DISPATCH(false, false, true)
   PV_DISPATCH(false, true, false)

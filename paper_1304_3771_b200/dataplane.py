@@ -392,6 +392,97 @@ def unpack_lanes(packed, aux=None) -> tuple[np.ndarray, np.ndarray]:
     return value, status
 
 
+class LaneExceptions:
+    """Exception records of a pv_translate_words batch (pv.h pv_exc): the
+    lanes whose 4-byte word cannot carry the exception's value (traps, TDP
+    stage faults), job-local lane index order unspecified."""
+
+    __slots__ = ("lane", "value", "aux", "status")
+
+    def __init__(self, lane=None, value=None, aux=None, status=None):
+        self.lane = np.zeros(0, np.int64) if lane is None else lane
+        self.value = np.zeros(0, np.uint64) if value is None else value
+        self.aux = np.zeros(0, np.uint64) if aux is None else aux
+        self.status = np.zeros(0, np.uint32) if status is None else status
+
+    def __len__(self) -> int:
+        return len(self.lane)
+
+    @classmethod
+    def from_records(cls, recs: np.ndarray) -> "LaneExceptions":
+        r = np.asarray(recs).view(np.uint64).reshape(-1, N.EXC_WORDS)
+        return cls(r[:, 0].astype(np.int64), r[:, 1].copy(), r[:, 2].copy(), (r[:, 3] & np.uint64(0xFFFFFFFF)).astype(np.uint32))
+
+
+def unpack_words(words, vas, exc: LaneExceptions | None = None, *, out_pfn: bool = False):
+    """(value uint64, status uint32, aux uint64) of pv_translate_words lane
+    words (pv.h): a word without PV_W32_ERR is the lane's frame number (value
+    = frame << 12 | va & 0xFFF, or the frame under ``out_pfn``); otherwise bits
+    0-20 are the compact status and the value is the lane's va (PV_W32_VA) or
+    comes from its exception record in ``exc``."""
+    w = np.asarray(words).view(np.uint32)
+    v = np.asarray(vas)
+    va = v.view(np.uint32).astype(np.uint64) if v.dtype.itemsize == 4 else v.view(np.uint64)
+    err = (w & np.uint32(N.W32_ERR)) != 0
+    compact = w & np.uint32(N.W32_COMPACT_MASK)
+    status = np.where(err, (compact & np.uint32(0xFFF)) | ((compact >> np.uint32(12)) << np.uint32(16)),
+                      np.uint32(0)).astype(np.uint32)
+    frame = w.astype(np.uint64)
+    value = frame if out_pfn else (frame << np.uint64(PAGE_SHIFT)) | (va & np.uint64(0xFFF))
+    value = np.where(err, va, value)
+    aux = np.zeros(len(w), np.uint64)
+    need = err & ((w & np.uint32(N.W32_VA)) == 0)
+    if need.any():
+        if exc is None:
+            raise ValueError("lanes with exception records need the LaneExceptions of the batch")
+        have = np.zeros(len(w), bool)
+        have[exc.lane] = True
+        if not np.array_equal(have, need):
+            raise ValueError("exception records do not match the lanes that need them")
+        value[exc.lane] = exc.value
+        aux[exc.lane] = exc.aux
+    return value, status, aux
+
+
+def translate_words(image, plan: TranslatePlan, vas, words, exc_rec, exc_count, lane_base: int = 0, *,
+                    out_pfn: bool = False, concurrent: bool = False) -> None:
+    """pv_translate_words over every lane of ``vas`` (int64 or int32 cuda
+    tensor) into ``words`` (int32 cuda tensor, one per lane); exception
+    records go to ``exc_rec`` (int64 cuda tensor of N.EXC_WORDS words per
+    record, may be empty) and are counted in ``exc_count`` (int64 cuda
+    tensor, one element, not reset here), asynchronously on the current
+    stream."""
+    import torch
+
+    lib = N.lib()
+    dev_img = image.device()
+    flags = (N.VA32 if vas.dtype == torch.int32 else 0) | (N.OUT_PFN if out_pfn else 0) | \
+        (N.CONCURRENT if concurrent else 0)
+    if plan.two:
+        flags |= N.HAS_TWO_STAGE
+    if plan.four:
+        flags |= N.HAS_4L
+    idx = _plan_index(image, plan)
+    cap = exc_rec.numel() // N.EXC_WORDS
+    N.check(lib.pv_translate_words(dev_img.data_ptr(), image.nbytes, plan.spaces.data_ptr(), plan.segs.data_ptr(),
+                                   plan.n_segs, plan.n_chunks, vas.data_ptr(), flags, idx, words.data_ptr(),
+                                   exc_rec.data_ptr() if cap else None, cap, exc_count.data_ptr(), lane_base,
+                                   _stream().cuda_stream), "pv_translate_words")
+
+
+def _plan_index(image, plan: TranslatePlan):
+    """byref(pv_index) for a plan that walks through the leaf index, else None."""
+    if not plan.use_index:
+        return None
+    li = leaf_index(image)
+    if not plan._indexed:
+        li.ensure(plan.host_spaces)
+        plan._indexed = True
+    li.sync_device_writes()
+    idx_abi = li.abi()
+    return ctypes.byref(idx_abi)
+
+
 def translate_lanes(image, plan: TranslatePlan, vas, *, out_pfn: bool = False, out=None, concurrent: bool = False,
                     packed: bool = False):
     """Translate every lane of ``vas`` (int64 or int32 cuda tensor).
@@ -420,15 +511,7 @@ def translate_lanes(image, plan: TranslatePlan, vas, *, out_pfn: bool = False, o
         flags |= N.HAS_TWO_STAGE
     if plan.four:
         flags |= N.HAS_4L
-    idx = None
-    if plan.use_index:
-        li = leaf_index(image)
-        if not plan._indexed:
-            li.ensure(plan.host_spaces)
-            plan._indexed = True
-        li.sync_device_writes()
-        idx_abi = li.abi()
-        idx = ctypes.byref(idx_abi)
+    idx = _plan_index(image, plan)
     N.check(lib.pv_translate(dev_img.data_ptr(), image.nbytes, plan.spaces.data_ptr(), plan.segs.data_ptr(),
                              plan.n_segs, plan.n_chunks, vas.data_ptr(), flags, idx, value.data_ptr(),
                              None if status is None else status.data_ptr(),
@@ -446,7 +529,8 @@ def translate_host_pipelined(image, space: Space, host_vas, chunk: int = 1 << 23
 last_host_io = {"h2d": 0, "d2h": 0}
 
 
-def translate_host_many(image, jobs, chunk: int = 1 << 23, *, packed: bool = False, out=None):
+def translate_host_many(image, jobs, chunk: int = 1 << 23, *, packed: bool = False, words: bool = False, out=None,
+                        exc_cap: int = 1 << 20):
     """Translate several host VA tensors (``jobs = [(space, vas), ...]``) in
     one pipeline: chunks of every job stream through two device buffer sets,
     H2D of chunk i+1 and D2H of chunk i-1 run on side streams while chunk i
@@ -458,8 +542,18 @@ def translate_host_many(image, jobs, chunk: int = 1 << 23, *, packed: bool = Fal
     word per lane (8 bytes back instead of 12; :func:`unpack_lanes`); aux
     travels for two-stage spaces and u64 VAs (spilled values).  ``out``: per
     job the pinned host tensors to fill (e.g. views of a buffer shared with
-    another process); ``None`` entries are allocated."""
+    another process); ``None`` entries are allocated.
+
+    ``words``: per job ``(words int32, None, LaneExceptions)`` -- one
+    pv_translate_words lane word per VA (4 bytes back, as many as the VAs
+    going in; :func:`unpack_words`) plus the exception records of the lanes
+    whose value the word cannot carry, fetched after the pipeline drains (a
+    batch with more than ``exc_cap`` such lanes runs again with room for all
+    of them)."""
     import torch
+
+    if words:
+        return _translate_host_words(image, jobs, chunk, out, exc_cap)
 
     outs, work = [], []
     dtype = torch.int32
@@ -529,6 +623,79 @@ def translate_host_many(image, jobs, chunk: int = 1 << 23, *, packed: bool = Fal
     d2h.synchronize()
     compute.synchronize()
     return outs
+
+
+def _translate_host_words(image, jobs, chunk: int, out, exc_cap: int):
+    """translate_host_many(words=True): the same two-buffer-set pipeline with
+    4-byte lane words each way; the exception records of every chunk append
+    to one device list read once at the end."""
+    import torch
+
+    srcs, dtype = [], torch.int32
+    for space, host_vas in jobs:
+        if host_vas.dtype not in (torch.int32, torch.int64):
+            host_vas = host_vas.to(torch.int64)
+        if host_vas.dtype == torch.int64:
+            dtype = torch.int64
+        srcs.append((space, host_vas))
+    outs, work, base = [], [], []
+    lane0 = 0
+    for k, (space, host_vas) in enumerate(srcs):
+        src = host_vas if host_vas.dtype == dtype else host_vas.to(dtype)
+        if not src.is_pinned():
+            src = src.pin_memory()
+        n = src.numel()
+        given = out[k] if out is not None and out[k] is not None else (None, None, None)
+        w = given[0] if given[0] is not None else torch.empty(n, dtype=torch.int32, pin_memory=True)
+        if w.dtype != torch.int32 or w.numel() != n:
+            raise ValueError("words=True fills int32 tensors of one word per VA")
+        outs.append(w)
+        base.append(lane0)
+        for start in range(0, n, chunk):
+            work.append((space, src, w, lane0, start, min(chunk, n - start)))
+        lane0 += n
+    total = lane0
+    cap = min(total, exc_cap)
+    compute = torch.cuda.current_stream()
+    dev_exc = torch.empty(max(cap, 1) * N.EXC_WORDS, dtype=torch.int64, device="cuda")
+    dev_cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    if work:
+        h2d, d2h = torch.cuda.Stream(), torch.cuda.Stream()
+        plans = {}
+        bufs = [(torch.empty(chunk, dtype=dtype, device="cuda"), torch.empty(chunk, dtype=torch.int32, device="cuda"),
+                 torch.cuda.Event(), torch.cuda.Event(), torch.cuda.Event()) for _ in range(2)]
+        for i, (space, src, w, l0, start, m) in enumerate(work):
+            d_vas, d_w, ev_in, ev_done, ev_out = bufs[i % 2]
+            if i >= 2:
+                h2d.wait_event(ev_out)  # buffers of chunk i-2 fully drained
+            with torch.cuda.stream(h2d):
+                d_vas[:m].copy_(src[start:start + m], non_blocking=True)
+                ev_in.record(h2d)
+            compute.wait_event(ev_in)
+            if (space, m) not in plans:
+                plans[(space, m)] = TranslatePlan([space], [(0, m, 0)], image=image)
+            translate_words(image, plans[(space, m)], d_vas[:m], d_w[:m], dev_exc[:cap * N.EXC_WORDS], dev_cnt,
+                            l0 + start)
+            ev_done.record(compute)
+            d2h.wait_event(ev_done)
+            with torch.cuda.stream(d2h):
+                w[start:start + m].copy_(d_w[:m], non_blocking=True)
+                ev_out.record(d2h)
+        d2h.synchronize()
+    n_exc = int(dev_cnt.item())
+    if n_exc > cap:  # more exception lanes than the list holds: once more with room for all
+        return _translate_host_words(image, jobs, chunk, out, n_exc)
+    last_host_io["h2d"] = sum(w[1].element_size() * w[5] for w in work)
+    last_host_io["d2h"] = 4 * total + 8 + n_exc * 8 * N.EXC_WORDS
+    excs = [LaneExceptions() for _ in outs]
+    if n_exc:
+        recs = dev_exc[:n_exc * N.EXC_WORDS].cpu().numpy()
+        allx = LaneExceptions.from_records(recs)
+        job = np.searchsorted(np.asarray(base, np.int64), allx.lane, side="right") - 1
+        for k in np.unique(job):
+            sel = job == k
+            excs[k] = LaneExceptions(allx.lane[sel] - base[k], allx.value[sel], allx.aux[sel], allx.status[sel])
+    return [(w, None, x) for w, x in zip(outs, excs)]
 
 
 # ---- K4: FIFO cache state packing -------------------------------------------

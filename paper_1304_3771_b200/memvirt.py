@@ -960,15 +960,19 @@ def translate_batch(translator: ProcessTranslator, gvas, *, use_cache: bool | No
             aux.cpu().numpy().view(np.uint64))
 
 
-def translate_many(pairs, *, chunk: int = 1 << 23, packed: bool = False, out=None):
+def translate_many(pairs, *, chunk: int = 1 << 23, packed: bool = False, words: bool = False, out=None):
     """``translate_batch`` for several uncached translators at once, host
     tensors in and out: ``pairs = [(translator, host_vas), ...]`` -> one
     pipelined H2D / translate / D2H stream over every pair (they must share
     one physical memory).  Returns ``[(hpa, status, aux), ...]`` as pinned
     host tensors; ``packed=True`` returns ``[(words, None, aux), ...]`` with
     one lane word per VA (hpa, or the status and value of the exception the
-    lane raises; ``dataplane.unpack_lanes``), 8 bytes per lane instead of 12.
-    ``out``: per pair pinned host tensors to fill (see
+    lane raises; ``dataplane.unpack_lanes``), 8 bytes per lane instead of 12;
+    ``words=True`` returns ``[(words, None, exceptions), ...]`` with one
+    4-byte word per VA (the frame number, or the status of the exception the
+    lane raises) and the exception records of the lanes whose value the word
+    cannot carry (``dataplane.unpack_words``) -- as many bytes back as VAs
+    in.  ``out``: per pair pinned host tensors to fill (see
     ``dataplane.translate_host_many``)."""
     import torch
 
@@ -984,7 +988,7 @@ def translate_many(pairs, *, chunk: int = 1 << 23, packed: bool = False, out=Non
         if not isinstance(vas, torch.Tensor):
             vas = torch.from_numpy(np.ascontiguousarray(np.asarray(vas, dtype=np.uint64)).view(np.int64))
         jobs.append((tr.device_space, vas))
-    return dp.translate_host_many(image, jobs, chunk=chunk, packed=packed, out=out)
+    return dp.translate_host_many(image, jobs, chunk=chunk, packed=packed, words=words, out=out)
 
 
 def lane_error(status: int, value: int, aux: int, va: int, image_bytes: int) -> Exception | None:

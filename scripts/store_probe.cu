@@ -33,7 +33,10 @@ __global__ void __launch_bounds__(512, 2) k(const uint32_t* __restrict__ idx, co
     for (int j = 0; j < L; ++j) v[j] = ld_idx(idx + wb + j * 32 + lane);
 #pragma unroll
     for (int j = 0; j < L; ++j) r[j] = __ldg(tab + (v[j] & mask));
-    if (MODE == 0 || MODE == 2) {
+    if (MODE == 3) {  // pv_translate_words: one 4-byte frame word out per lane
+#pragma unroll
+      for (int j = 0; j < L; ++j) o32[wb + j * 32 + lane] = r[j];
+    } else if (MODE == 0 || MODE == 2) {
 #pragma unroll
       for (int j = 0; j < L; ++j) {
         const uint64_t i = wb + j * 32 + lane;
@@ -111,12 +114,12 @@ int main() {
   cudaMemset(tab, 1, (uint64_t)words * 4);
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  void (*fns[4])(const uint32_t*, const uint32_t*, uint32_t, uint64_t, uint64_t*, uint32_t*) = {k<0>, k<1>, kvec,
-                                                                                              k<2>};
-  const char* names[4] = {"register stores", "smem + bulk stores", "4 lanes/thread, v4 io",
-                          "register stores, 8 B out (packed)"};
+  void (*fns[5])(const uint32_t*, const uint32_t*, uint32_t, uint64_t, uint64_t*, uint32_t*) = {k<0>, k<1>, kvec,
+                                                                                              k<2>, k<3>};
+  const char* names[5] = {"register stores", "smem + bulk stores", "4 lanes/thread, v4 io",
+                          "register stores, 8 B out (packed)", "register stores, 4 B out (words)"};
   uint64_t* check = (uint64_t*)malloc(1 << 20);
-  for (int m = 0; m < 4; ++m) {
+  for (int m = 0; m < 5; ++m) {
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
@@ -130,9 +133,14 @@ int main() {
     float ms = 0;
     cudaEventElapsedTime(&ms, a, b);
     ms /= reps;
-    cudaMemcpy(check, o64 + (n - 131072), 1 << 20, cudaMemcpyDeviceToHost);
     uint64_t bad = 0;
-    for (int i = 0; i < 131072; ++i) bad += check[i] != ((0x01010101ull << 12) | (h[n - 131072 + i] & 0xFFF));
+    if (m == 4) {
+      cudaMemcpy(check, o32 + (n - 131072), 131072 * 4, cudaMemcpyDeviceToHost);
+      for (int i = 0; i < 131072; ++i) bad += ((const uint32_t*)check)[i] != 0x01010101u;
+    } else {
+      cudaMemcpy(check, o64 + (n - 131072), 1 << 20, cudaMemcpyDeviceToHost);
+      for (int i = 0; i < 131072; ++i) bad += check[i] != ((0x01010101ull << 12) | (h[n - 131072 + i] & 0xFFF));
+    }
     printf("%-22s %.3f ms  %.1f G lanes/s  mismatches %llu  [%s]\n", names[m], ms, n / ms / 1e6,
            (unsigned long long)bad, cudaGetErrorString(cudaGetLastError()));
   }

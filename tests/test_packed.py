@@ -38,3 +38,39 @@ def test_unpack_lanes_round_trip():
     v, s = dp.unpack_lanes(words.view(np.int64), aux.view(np.int64))
     assert np.array_equal(v, np.array(vals, dtype=np.uint64))
     assert np.array_equal(s, np.array(sts, dtype=np.uint32))
+
+
+def test_unpack_words_decodes_every_form():
+    """pv_translate_words lane words (include/pv.h) on CPU: frames, faults
+    whose value is the lane's va, and lanes resolved from exception records."""
+    rng = np.random.default_rng(6)
+    n = 5000
+    vas = rng.integers(0, 1 << 32, n).astype(np.uint32)
+    frames = rng.integers(0, 1 << 28, n).astype(np.uint64)
+    kind = rng.integers(0, 3, n)  # 0 ok, 1 va-valued fault, 2 record
+    st = np.where(kind == 0, 0, np.where(kind == 1, 0x013, 0x062 | (17 << 16))).astype(np.uint32)
+    compact = (st & 0xFFF) | (((st >> 16) & 0x1FF) << 12)
+    words = np.where(kind == 0, frames, np.where(kind == 1, N.W32_ERR | N.W32_VA | compact,
+                                                  N.W32_ERR | compact)).astype(np.uint32)
+    rec_lanes = np.flatnonzero(kind == 2)
+    rec_vals = rng.integers(0, 1 << 62, len(rec_lanes)).astype(np.uint64)
+    rec_aux = rng.integers(0, 1 << 40, len(rec_lanes)).astype(np.uint64)
+    order = rng.permutation(len(rec_lanes))
+    recs = np.zeros((len(rec_lanes), N.EXC_WORDS), np.uint64)
+    recs[:, 0] = rec_lanes[order]
+    recs[:, 1] = rec_vals[order]
+    recs[:, 2] = rec_aux[order]
+    recs[:, 3] = st[rec_lanes[order]]
+    exc = dp.LaneExceptions.from_records(recs.view(np.int64))
+    v, s, a = dp.unpack_words(words.view(np.int32), vas.view(np.int32), exc)
+    want = np.where(kind == 0, (frames << np.uint64(12)) | (vas.astype(np.uint64) & np.uint64(0xFFF)),
+                    vas.astype(np.uint64))
+    want[rec_lanes] = rec_vals
+    assert np.array_equal(v, want) and np.array_equal(s, st)
+    assert np.array_equal(a[rec_lanes], rec_aux) and not a[kind != 2].any()
+    try:
+        dp.unpack_words(words, vas, None)
+    except ValueError:
+        pass
+    else:
+        raise AssertionError("record lanes without records must not decode")
