@@ -448,6 +448,32 @@ typedef struct pv_small_result {
 int pv_copy_small(uint8_t* image, uint64_t image_bytes, const pv_small_op* op /* host */, uint8_t* buf,
                   uint64_t buf_bytes, pv_small_result* out, uint8_t* dirty, uint64_t seq, void* stream);
 
+/* ---- per-call server ---------------------------------------------------------
+ * The same two per-call operations without a kernel launch per call: a
+ * resident one-CTA server kernel on a library-private non-blocking stream of
+ * the current device polls a request mailbox in mapped pinned host memory,
+ * serves the request with the device code of pv_walk_one / pv_copy_small and
+ * publishes the reply there; the call returns when the reply is in *out.
+ * Ordered after the work queued on `stream`: when the stream is idle
+ * (cudaStreamQuery) the server serves the request, otherwise it is launched
+ * on the stream (pv_walk_one / pv_copy_small into the mailbox) and the call
+ * waits for it.  The first served call -- and the first after
+ * PV_SERVER_IDLE_US (default 200) microseconds without a request, after which
+ * the server exits by itself so device-wide synchronisation never waits
+ * longer -- launches the server.  Work queued on OTHER streams is not waited
+ * for (as with the launches above).  Calls from several host threads are
+ * serialised.  While resident the server holds one CTA slot of one SM;
+ * pv_server_stop parks it (synchronous) before batch kernels that size their
+ * grids to fill every SM.  out->seq is the call's request number. */
+int pv_server_walk(const uint8_t* image, uint64_t image_bytes, const pv_space* space /* host */,
+                   uint64_t va, uint32_t flags, pv_one_result* out /* host */, void* stream);
+int pv_server_copy_small(uint8_t* image, uint64_t image_bytes, const pv_small_op* op /* host */,
+                         uint8_t* buf, uint64_t buf_bytes, pv_small_result* out /* host */,
+                         uint8_t* dirty, void* stream);
+int pv_server_stop(void);
+/* 1 while the server of the current device may be resident. */
+int pv_server_resident(void);
+
 /* ---- per-rank residency ------------------------------------
  * A zero-filled device image of image_bytes whose byte offsets are the
  * reference's hpas (memvirt.py:433-480 slot carving), with HBM behind only

@@ -82,7 +82,8 @@ EXPORTS = (
     "pv_result_decode", "pv_timing", "pv_timing_ms", "pv_copy_shim_scratch_bytes", "pv_copy_shim",
     "pv_map_scratch_bytes", "pv_map_plan", "pv_map_commit",
     "pv_frame_pack", "pv_frame_identify", "pv_frame_assemble_scratch_bytes", "pv_frame_assemble",
-    "pv_walk_one", "pv_copy_small", "pv_host_alloc", "pv_host_free", "pv_image_create", "pv_image_destroy",
+    "pv_walk_one", "pv_copy_small", "pv_server_walk", "pv_server_copy_small", "pv_server_stop",
+    "pv_server_resident", "pv_host_alloc", "pv_host_free", "pv_image_create", "pv_image_destroy",
 )
 
 _u64 = ctypes.c_uint64
@@ -125,6 +126,10 @@ _SIGNATURES = {
     "pv_timing_ms": (ctypes.c_double, [ctypes.c_char_p, _p]),
     "pv_walk_one": (ctypes.c_int, [_p, _u64, _p, _u64, _u32, _p, _u64, _p]),
     "pv_copy_small": (ctypes.c_int, [_p, _u64, _p, _p, _u64, _p, _p, _u64, _p]),
+    "pv_server_walk": (ctypes.c_int, [_p, _u64, _p, _u64, _u32, _p, _p]),
+    "pv_server_copy_small": (ctypes.c_int, [_p, _u64, _p, _p, _u64, _p, _p, _p]),
+    "pv_server_stop": (ctypes.c_int, []),
+    "pv_server_resident": (ctypes.c_int, []),
     "pv_image_create": (ctypes.c_int, [_u64, _p, _u32, _u64, _p, _p, _p]),
     "pv_image_destroy": (ctypes.c_int, [_p]),
     "pv_host_alloc": (_p, [_u64]),

@@ -2,6 +2,10 @@
 //
 // Thin validation + launch layer: no allocation of user-visible memory, no
 // exceptions across the boundary, CUDA errors returned as PV_ECUDA - err.
+#include <atomic>
+#include <chrono>
+#include <cstdlib>
+#include <cstring>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -433,6 +437,213 @@ int pv_copy_small(uint8_t* image, uint64_t image_bytes, const pv_small_op* op, u
   if (n != 0 && !buf) return PV_EINVAL;
   return rc(launch_copy_small(image, image_bytes, *op, buf, buf_bytes, out, dirty, (uint32_t)n, seq,
                               (cudaStream_t)stream));
+}
+
+}  // extern "C"
+
+namespace {
+// One per-call server per device (pv_copy.cu server_kernel): its mailbox,
+// private non-blocking stream and request counter; requests of all host
+// threads are serialised by the mutex.
+struct ServerSlot {
+  std::mutex mu;
+  ServerBox* box = nullptr;
+  cudaStream_t stream = nullptr;
+  uint64_t seq = 0;
+};
+constexpr int kMaxDevices = 64;
+ServerSlot g_server[kMaxDevices];
+
+uint64_t server_idle_ns() {
+  static const uint64_t v = [] {
+    const char* e = std::getenv("PV_SERVER_IDLE_US");
+    const long us = e ? std::atol(e) : 200;
+    return (uint64_t)(us > 0 ? us : 200) * 1000ull;
+  }();
+  return v;
+}
+
+// Post the request `fill` writes into the mailbox and wait for its reply
+// (slot lock held by the caller).  Launches the server when it is not
+// resident; returns a PV_ code.
+int server_box(ServerSlot& S) {
+  if (S.box != nullptr) return PV_SUCCESS;
+  cudaStream_t st = nullptr;
+  const cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return PV_ECUDA - (int)e;
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, sizeof(ServerBox), cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
+    cudaStreamDestroy(st);
+    return PV_ENOMEM;
+  }
+  std::memset(p, 0, sizeof(ServerBox));
+  S.stream = st;
+  S.box = static_cast<ServerBox*>(p);
+  S.box->state = kServerExited;
+  return PV_SUCCESS;
+}
+
+template <class Fill>
+int server_roundtrip(ServerSlot& S, Fill fill) {
+  const int rb = server_box(S);
+  if (rb != PV_SUCCESS) return rb;
+  ServerBox* box = S.box;
+  fill(box->req);
+  const uint64_t sq = ++S.seq;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  box->req_seq = sq;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  auto launch = [&]() -> int {
+    box->state = kServerLaunched;
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    const cudaError_t e = launch_server(box, server_idle_ns(), S.stream);
+    return e == cudaSuccess ? PV_SUCCESS : PV_ECUDA - (int)e;
+  };
+  if (box->state == kServerExited) {
+    const int r = launch();
+    if (r != PV_SUCCESS) return r;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  for (uint64_t it = 1; box->rep_seq != sq; ++it) {
+    if ((it & 1023) == 0) {
+      // the server may have idled out just before the request landed
+      if (box->state == kServerExited && box->rep_seq != sq) {
+        const int r = launch();
+        if (r != PV_SUCCESS) return r;
+      }
+      const cudaError_t e = cudaStreamQuery(S.stream);
+      if (e != cudaSuccess && e != cudaErrorNotReady) return PV_ECUDA - (int)e;
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(30))
+        return PV_ECUDA - (int)cudaErrorLaunchTimeout;
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  return PV_SUCCESS;
+}
+
+ServerSlot* server_slot() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return nullptr;
+  return &g_server[dev];
+}
+}  // namespace
+
+extern "C" {
+
+// Spin until *seq_word == sq (a stream-ordered per-call launch publishing
+// into the mailbox), checking `stream` for errors now and then.
+static int wait_published(const volatile uint64_t* seq_word, uint64_t sq, cudaStream_t stream) {
+  const auto t0 = std::chrono::steady_clock::now();
+  for (uint64_t it = 1; *seq_word != sq; ++it) {
+    if ((it & 1023) == 0) {
+      const cudaError_t e = cudaStreamQuery(stream);
+      if (e != cudaSuccess && e != cudaErrorNotReady) return PV_ECUDA - (int)e;
+      if (e == cudaSuccess && *seq_word != sq) return PV_ECUDA - (int)cudaErrorUnknown;
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(30))
+        return PV_ECUDA - (int)cudaErrorLaunchTimeout;
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  return PV_SUCCESS;
+}
+
+int pv_server_walk(const uint8_t* image, uint64_t image_bytes, const pv_space* space, uint64_t va, uint32_t flags,
+                   pv_one_result* out, void* stream) {
+  if (!image || !space || !out || image_bytes % kPageSize) return PV_EINVAL;
+  if (flags & ~(uint32_t)PV_OUT_PFN) return PV_EINVAL;
+  ServerSlot* S = server_slot();
+  if (!S) return PV_EINVAL;
+  std::lock_guard<std::mutex> lk(S->mu);
+  int r;
+  const cudaError_t q = cudaStreamQuery((cudaStream_t)stream);
+  if (q == cudaSuccess) {
+    r = server_roundtrip(*S, [&](ServerReq& req) {
+      req.kind = kServerWalk;
+      req.flags = flags;
+      req.image = (uint64_t)image;
+      req.image_bytes = image_bytes;
+      req.va = va;
+      req.op.space = *space;
+    });
+  } else if (q == cudaErrorNotReady) {  // queued work first: the stream-ordered launch
+    r = server_box(*S);
+    if (r != PV_SUCCESS) return r;
+    const uint64_t sq = ++S->seq;
+    const cudaError_t e = launch_walk_one(image, image_bytes, *space, va, flags, &S->box->one, sq,
+                                          (cudaStream_t)stream);
+    if (e != cudaSuccess) return PV_ECUDA - (int)e;
+    r = wait_published(&S->box->one.seq, sq, (cudaStream_t)stream);
+  } else {
+    return PV_ECUDA - (int)q;
+  }
+  if (r != PV_SUCCESS) return r;
+  out->value = S->box->one.value;
+  out->aux = S->box->one.aux;
+  out->status = S->box->one.status;
+  out->seq = S->seq;
+  return PV_SUCCESS;
+}
+
+int pv_server_copy_small(uint8_t* image, uint64_t image_bytes, const pv_small_op* op, uint8_t* buf,
+                         uint64_t buf_bytes, pv_small_result* out, uint8_t* dirty, void* stream) {
+  if (!image || !op || !out || image_bytes % kPageSize) return PV_EINVAL;
+  if (op->direction != PV_TO_GUEST && op->direction != PV_FROM_GUEST) return PV_EINVAL;
+  const uint64_t n = page_span(op->gva, op->len);
+  if (n > PV_SMALL_PAGES) return PV_EINVAL;
+  if (n != 0 && !buf) return PV_EINVAL;
+  ServerSlot* S = server_slot();
+  if (!S) return PV_EINVAL;
+  std::lock_guard<std::mutex> lk(S->mu);
+  int r;
+  const cudaError_t q = cudaStreamQuery((cudaStream_t)stream);
+  if (q == cudaSuccess) {
+    r = server_roundtrip(*S, [&](ServerReq& req) {
+      req.kind = kServerCopy;
+      req.flags = 0;
+      req.image = (uint64_t)image;
+      req.image_bytes = image_bytes;
+      req.buf = (uint64_t)buf;
+      req.buf_bytes = buf_bytes;
+      req.dirty = (uint64_t)dirty;
+      req.n_pages = (uint32_t)n;
+      std::memcpy(&req.op, op, sizeof(pv_small_op) - sizeof(uint64_t) * (PV_SMALL_PAGES - n));
+    });
+  } else if (q == cudaErrorNotReady) {
+    r = server_box(*S);
+    if (r != PV_SUCCESS) return r;
+    const uint64_t sq = ++S->seq;
+    const cudaError_t e = launch_copy_small(image, image_bytes, *op, buf, buf_bytes, &S->box->small, dirty,
+                                            (uint32_t)n, sq, (cudaStream_t)stream);
+    if (e != cudaSuccess) return PV_ECUDA - (int)e;
+    r = wait_published(&S->box->small.seq, sq, (cudaStream_t)stream);
+  } else {
+    return PV_ECUDA - (int)q;
+  }
+  if (r != PV_SUCCESS) return r;
+  const pv_small_result& res = S->box->small;
+  out->op = res.op;
+  std::memcpy(out->page_hpa, res.page_hpa, n * sizeof(uint64_t));
+  std::memcpy(out->page_status, res.page_status, n * sizeof(uint32_t));
+  out->seq = S->seq;
+  return PV_SUCCESS;
+}
+
+int pv_server_stop(void) {
+  ServerSlot* S = server_slot();
+  if (!S) return PV_EINVAL;
+  std::lock_guard<std::mutex> lk(S->mu);
+  if (S->box == nullptr || S->box->state == kServerExited) return PV_SUCCESS;
+  const int r = server_roundtrip(*S, [&](ServerReq& q) { q.kind = kServerStop; });
+  if (r != PV_SUCCESS) return r;
+  const cudaError_t e = cudaStreamSynchronize(S->stream);
+  return e == cudaSuccess ? PV_SUCCESS : PV_ECUDA - (int)e;
+}
+
+int pv_server_resident(void) {
+  ServerSlot* S = server_slot();
+  if (!S) return 0;
+  std::lock_guard<std::mutex> lk(S->mu);
+  return S->box != nullptr && S->box->state != kServerExited;
 }
 
 void* pv_host_alloc(uint64_t bytes) {

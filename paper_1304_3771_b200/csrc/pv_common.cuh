@@ -277,6 +277,30 @@ __device__ __forceinline__ uint64_t upper_search(const uint64_t* __restrict__ of
   return lo;
 }
 
+// Per-call server mailbox (pv_copy.cu server_kernel, pv_abi.cu pv_server_*):
+// mapped pinned host memory, one per device.
+constexpr uint32_t kServerWalk = 1, kServerCopy = 2, kServerStop = 3;
+constexpr uint64_t kServerRunning = 1, kServerExited = 2, kServerLaunched = 3;
+struct ServerReq {
+  uint32_t kind;
+  uint32_t flags;
+  uint64_t image, image_bytes, buf, buf_bytes, dirty, va;
+  uint32_t n_pages;
+  uint32_t reserved;
+  pv_small_op op;  // op.space is the walk's space
+};
+static_assert(sizeof(ServerReq) % 8 == 0, "the server pulls requests in 8-byte words");
+struct ServerBox {
+  volatile uint64_t req_seq;  // written by the host after the request
+  uint64_t pad0[15];
+  ServerReq req;
+  alignas(128) volatile uint64_t rep_seq;  // written by the server after the reply
+  volatile uint64_t state;                 // kServer* (host: launched; server: running / exited)
+  pv_one_result one;
+  pv_small_result small;
+};
+cudaError_t launch_server(ServerBox* box, uint64_t idle_ns, cudaStream_t stream);
+
 // Grid size that fills every SM with resident CTAs of `func` (cached per
 // function and device; defined in pv_abi.cu).
 uint64_t resident_grid(const void* func, int tpb, size_t smem);

@@ -531,10 +531,12 @@ __device__ __noinline__ void small_sequential(uint8_t* __restrict__ image, uint6
 // op whose chunk k lands on a table node the walk of a later page reads (a
 // table hazard) runs page by page instead -- walk k, write k, walk k + 1
 // through coherent loads -- exactly like copy_user_buffer.
-__global__ void __launch_bounds__(kSmallTpb)
-copy_small_kernel(uint8_t* __restrict__ image, uint64_t image_bytes, pv_small_op op, uint8_t* __restrict__ buf,
-                  uint64_t buf_bytes, pv_small_result* out, uint8_t* __restrict__ dirty, uint32_t n_pages,
-                  uint64_t seq) {
+// The op's body on one CTA of kSmallTpb threads (all threads call it; it ends
+// with a barrier).  out->op, page_hpa, page_status are written; the caller
+// publishes the completion.
+__device__ __noinline__ void copy_small_body(uint8_t* __restrict__ image, uint64_t image_bytes, const pv_small_op& op,
+                                             uint8_t* __restrict__ buf, uint64_t buf_bytes, pv_small_result* out,
+                                             uint8_t* __restrict__ dirty, uint32_t n_pages) {
   __shared__ uint64_t s_hpa[PV_SMALL_PAGES];
   __shared__ NodeList s_nodes[PV_SMALL_PAGES];
   __shared__ uint32_t s_bad, s_hazard;
@@ -566,10 +568,6 @@ copy_small_kernel(uint8_t* __restrict__ image, uint64_t image_bytes, pv_small_op
   if (s_hazard) {
     if (warp == 0) small_sequential(image, image_bytes, op, buf, buf_bytes, out, dirty, n_pages, lane);
     __syncthreads();
-    if (tid == 0) {
-      __threadfence_system();
-      *reinterpret_cast<volatile uint64_t*>(&out->seq) = seq;
-    }
     return;
   }
   const uint32_t bad = s_bad;
@@ -604,10 +602,112 @@ copy_small_kernel(uint8_t* __restrict__ image, uint64_t image_bytes, pv_small_op
     }
   }
   __syncthreads();
-  if (tid == 0) {
+}
+
+__global__ void __launch_bounds__(kSmallTpb)
+copy_small_kernel(uint8_t* __restrict__ image, uint64_t image_bytes, pv_small_op op, uint8_t* __restrict__ buf,
+                  uint64_t buf_bytes, pv_small_result* out, uint8_t* __restrict__ dirty, uint32_t n_pages,
+                  uint64_t seq) {
+  copy_small_body(image, image_bytes, op, buf, buf_bytes, out, dirty, n_pages);
+  if (threadIdx.x == 0) {
     __threadfence_system();
     *reinterpret_cast<volatile uint64_t*>(&out->seq) = seq;
   }
+}
+
+// ---- per-call server: one resident CTA serving walk_one / copy_small requests
+// posted in mapped pinned host memory (no launch per call).  Thread 0 polls
+// the request sequence word with system-scope acquire loads; a request is
+// pulled into shared memory by every thread at once (one link round trip),
+// served by the same device code as walk_one_kernel / copy_small_kernel, and
+// completed by a system-scope release of the reply sequence.  After idle_ns
+// without a request the server marks itself exited, looks once more (a request
+// posted meanwhile is served) and returns, so a device-wide synchronisation
+// waits at most that long.
+
+__device__ __forceinline__ uint64_t ld_acquire_sys_u64(const volatile uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys_u64(volatile uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void __launch_bounds__(kSmallTpb) server_kernel(ServerBox* box, uint64_t idle_ns) {
+  __shared__ __align__(16) ServerReq s_req;
+  __shared__ uint64_t s_seq;
+  __shared__ uint32_t s_stop;
+  const uint32_t tid = threadIdx.x;
+  uint64_t last = 0;
+  if (tid == 0) last = ld_acquire_sys_u64(&box->rep_seq);
+  for (;;) {
+    if (tid == 0) {
+      const uint64_t t0 = globaltimer_ns();
+      uint32_t stop = 0;
+      uint64_t sq;
+      for (;;) {
+        sq = ld_acquire_sys_u64(&box->req_seq);
+        if (sq != last) break;
+        if (globaltimer_ns() - t0 > idle_ns) {
+          st_release_sys_u64(&box->state, kServerExited);
+          __threadfence_system();
+          sq = ld_acquire_sys_u64(&box->req_seq);
+          if (sq != last) {
+            st_release_sys_u64(&box->state, kServerRunning);
+            break;
+          }
+          stop = 1;
+          break;
+        }
+      }
+      s_seq = sq;
+      s_stop = stop;
+    }
+    __syncthreads();
+    if (s_stop) return;
+    {  // pull the request (one round trip: every thread loads 8 bytes)
+      const volatile uint64_t* src = reinterpret_cast<const volatile uint64_t*>(&box->req);
+      uint64_t* dst = reinterpret_cast<uint64_t*>(&s_req);
+      for (uint32_t i = tid; i < sizeof(ServerReq) / 8; i += blockDim.x) dst[i] = src[i];
+    }
+    __syncthreads();
+    const uint32_t kind = s_req.kind;
+    if (kind == kServerWalk) {
+      if (tid == 0) {
+        uint64_t value = 0, aux = 0;
+        const uint64_t va = s_req.va;
+        const uint32_t st = translate_global(reinterpret_cast<const uint8_t*>(s_req.image), s_req.image_bytes,
+                                             s_req.op.space, va, &value, &aux);
+        if (st == PV_ST_OK && !(s_req.flags & PV_OUT_PFN)) value = (value << kPageShift) | (va & kPageMask);
+        box->one.value = value;
+        box->one.aux = aux;
+        box->one.status = st;
+      }
+    } else if (kind == kServerCopy) {
+      copy_small_body(reinterpret_cast<uint8_t*>(s_req.image), s_req.image_bytes, s_req.op,
+                      reinterpret_cast<uint8_t*>(s_req.buf), s_req.buf_bytes, &box->small,
+                      reinterpret_cast<uint8_t*>(s_req.dirty), s_req.n_pages);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      if (kind == kServerStop) st_release_sys_u64(&box->state, kServerExited);
+      __threadfence_system();
+      st_release_sys_u64(&box->rep_seq, s_seq);
+      last = s_seq;
+    }
+    if (kind == kServerStop) return;
+  }
+}
+
+cudaError_t launch_server(ServerBox* box, uint64_t idle_ns, cudaStream_t stream) {
+  server_kernel<<<1, kSmallTpb, 0, stream>>>(box, idle_ns);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_walk_one(const uint8_t* image, uint64_t image_bytes, const pv_space& sp, uint64_t va,

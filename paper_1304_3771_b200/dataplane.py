@@ -28,6 +28,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native as N
+from . import percall
 from .errors import OutOfRange, PageFault, TrapExit
 
 PAGE_SIZE = 4096
@@ -452,6 +453,7 @@ def translate_words(image, plan: TranslatePlan, vas, words, exc_rec, exc_count, 
     record, may be empty) and are counted in ``exc_count`` (int64 cuda
     tensor, one element, not reset here), asynchronously on the current
     stream."""
+    percall.park()  # the per-call server must not hold a CTA slot this grid counts on
     import torch
 
     lib = N.lib()
@@ -494,6 +496,7 @@ def translate_lanes(image, plan: TranslatePlan, vas, *, out_pfn: bool = False, o
     ``packed``: value holds PV_OUT_PACKED lane words (:func:`unpack_lanes`)
     and status is None.
     """
+    percall.park()  # the per-call server must not hold a CTA slot this grid counts on
     import torch
 
     lib = N.lib()
@@ -949,6 +952,7 @@ def copy_launch(image, plan: CopyPlan, direction: int, buf, *, fifo_dev=None, fi
 
 def _copy_launch(image, plan, direction, buf, fifo_dev, fifo_cap, detect_conflicts, track_dirty, buf_ready,
                  buf_bytes) -> None:
+    percall.park()  # the per-call server must not hold a CTA slot this grid counts on
     lib = N.lib()
     dev_img = image.device()
     s = _stream().cuda_stream
@@ -1041,6 +1045,7 @@ def decode_results(res: np.ndarray) -> list[OpOutcome]:
 def copy_ordered(image, plan: CopyPlan, buf, buf_bytes: int | None = None) -> None:
     """Ordered execution of a planned to_guest batch whose chunks share
     destination pages (pv_copy_ordered): exact last-writer-wins."""
+    percall.park()  # the per-call server must not hold a CTA slot this grid counts on
     import torch
 
     lib = N.lib()

@@ -6,14 +6,22 @@ backend.py:92-104; memvirt.py:585-628).  A batch pipeline (descriptor
 tensors, plan / stamp / exec launches, result copies) costs hundreds of
 microseconds per such call; this path costs one kernel launch:
 
-* the request travels in the kernel's parameters (``pv_walk_one`` /
-  ``pv_copy_small``, include/pv.h) -- no H2D copy, no device allocation;
-* results land in host-mapped pinned memory (``pv_host_alloc``) and are
-  published last with a sequence number the caller spins on -- no D2H copy,
-  no stream synchronisation unless the stream still has earlier work queued;
+* the request goes to a resident server kernel through a mailbox in
+  host-mapped pinned memory (``pv_server_walk`` / ``pv_server_copy_small``,
+  include/pv.h): no launch, no H2D copy, no device allocation per call --
+  one link round trip there and back (``profiles/r02_percall_latency.json``);
+  when the calling thread's stream still has work queued, the same request
+  is launched on that stream instead (``pv_walk_one`` / ``pv_copy_small``)
+  so the call stays ordered behind it;
+* results are published last with a sequence number the library spins on
+  (one ctypes call per operation);
 * payloads move between the op's pinned staging buffer and HBM inside the
   same kernel (zero-copy over the PCIe/C2C link), so a 4 KiB copy_to_user is
-  one launch end to end.
+  one request end to end.
+
+``PV_PERCALL_SERVER=0`` launches a kernel per call instead (the A/B form).
+Batch launches park the server first (:func:`park`): while resident it holds
+a CTA slot of one SM that grids sized to fill every SM count on.
 
 One :class:`PerCall` per host thread (thread-local), so calls from different
 threads never share a result block; each call runs on the thread's current
@@ -24,6 +32,7 @@ it before.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 
 import numpy as np
@@ -38,6 +47,16 @@ STAGE_BYTES = SMALL_PAGES * PAGE_SIZE
 
 _tls = threading.local()
 _SPIN = 20000  # result polls before falling back to a stream synchronisation
+_SERVER = os.environ.get("PV_PERCALL_SERVER", "1") != "0"
+_server_used = False
+
+
+def park() -> None:
+    """Stop the per-call server if it may be resident (before a batch launch)."""
+    global _server_used
+    if _server_used:
+        _server_used = False
+        N.check(N.lib().pv_server_stop(), "pv_server_stop")
 
 
 class PerCall:
@@ -89,12 +108,18 @@ class PerCall:
         sp = self.space
         sp.s1_base, sp.s1_root_pfn, sp.s2_root_pfn, sp.mode = space.s1_base, space.s1_root_pfn, \
             space.s2_root_pfn, space.mode
-        self.seq += 1
         stream = _raw_stream(dev)
-        N.check(self.lib.pv_walk_one(dev.data_ptr(), image.nbytes, self.space_ref, va & 0xFFFFFFFFFFFFFFFF,
-                                     N.OUT_PFN if out_pfn else 0, self.one_ptr, self.seq, stream),
-                "pv_walk_one")
-        self._wait(self.one, self.seq, stream)
+        if _SERVER:
+            global _server_used
+            _server_used = True
+            N.check(self.lib.pv_server_walk(dev.data_ptr(), image.nbytes, self.space_ref, va & 0xFFFFFFFFFFFFFFFF,
+                                            N.OUT_PFN if out_pfn else 0, self.one_ptr, stream), "pv_server_walk")
+        else:
+            self.seq += 1
+            N.check(self.lib.pv_walk_one(dev.data_ptr(), image.nbytes, self.space_ref, va & 0xFFFFFFFFFFFFFFFF,
+                                         N.OUT_PFN if out_pfn else 0, self.one_ptr, self.seq, stream),
+                    "pv_walk_one")
+            self._wait(self.one, self.seq, stream)
         one = self.one
         return int(one.status) & 0xFFFFFFFF, int(one.value), int(one.aux)
 
@@ -118,14 +143,21 @@ class PerCall:
             for k, h in enumerate(pre):
                 if h is not None:
                     op.pre_hpa[k] = h + 1
-        self.seq += 1
         stream = _raw_stream(dev)
         # no device dirty marks: the caller writes the same bytes through to
         # the host mirror (write_through), so no page goes device-stale
-        N.check(self.lib.pv_copy_small(dev.data_ptr(), image.nbytes, self.op_ref, self.stage_ptr + buf_off,
-                                       max(avail - buf_off, 0), self.small_ptr, None, self.seq,
-                                       stream), "pv_copy_small")
-        self._wait(self.small, self.seq, stream)
+        if _SERVER:
+            global _server_used
+            _server_used = True
+            N.check(self.lib.pv_server_copy_small(dev.data_ptr(), image.nbytes, self.op_ref, self.stage_ptr + buf_off,
+                                                  max(avail - buf_off, 0), self.small_ptr, None, stream),
+                    "pv_server_copy_small")
+        else:
+            self.seq += 1
+            N.check(self.lib.pv_copy_small(dev.data_ptr(), image.nbytes, self.op_ref, self.stage_ptr + buf_off,
+                                           max(avail - buf_off, 0), self.small_ptr, None, self.seq,
+                                           stream), "pv_copy_small")
+            self._wait(self.small, self.seq, stream)
         return self.small
 
 

@@ -91,22 +91,30 @@ def main():
 
     from paper_1304_3771_b200 import has, memvirt
 
-    ours = calls(memvirt, has, n)
+    from paper_1304_3771_b200 import percall
+
+    ours = calls(memvirt, has, n)  # the resident per-call server (default)
+    percall.park()
+    percall._SERVER = False
+    launch = calls(memvirt, has, n)  # one kernel launch per call (PV_PERCALL_SERVER=0)
+    percall._SERVER = True
     torch.cuda.synchronize()
     ref = calls(rm, rb, n)
-    out = {k: {"ours_us": round(ours[k], 2), "ref_us": round(ref[k], 2), "speedup": round(ref[k] / ours[k], 2)}
+    out = {k: {"ours_us": round(ours[k], 2), "ours_launch_per_call_us": round(launch[k], 2),
+               "ref_us": round(ref[k], 2), "speedup": round(ref[k] / ours[k], 2)}
            for k in ours}
     # where a per-call walk's time goes: the device round trip alone (one launch + result in pinned
     # memory, no translator layers) and a generic GPU round trip (one tiny torch kernel + sync)
-    from paper_1304_3771_b200 import dataplane as dp
-    from paper_1304_3771_b200 import percall
-
     memv, space, _ = build(memvirt, has, "shadow")
     img = memv.host_mem.backing
     sp = memv.translator(space, use_cache=False).device_space
     pc = percall.get()
-    floor = {"percall.walk (one pv_walk_one launch + spin on pinned result)":
-             per_call_us(lambda: pc.walk(img, sp, BUF + 0x123, False), n)}
+    floor = {"percall.walk (server: one mailbox round trip)": per_call_us(lambda: pc.walk(img, sp, BUF + 0x123, False), n)}
+    percall.park()
+    percall._SERVER = False
+    floor["percall.walk (one pv_walk_one launch + spin on pinned result)"] = \
+        per_call_us(lambda: pc.walk(img, sp, BUF + 0x123, False), n)
+    percall._SERVER = True
     x = torch.zeros(1, device="cuda")
     s = torch.cuda.current_stream()
     floor["torch: one tiny kernel + stream synchronize"] = per_call_us(lambda: (x.add_(1), s.synchronize()), n)
