@@ -464,12 +464,16 @@ int pv_copy_small(uint8_t* image, uint64_t image_bytes, const pv_small_op* op /*
  * for (as with the launches above).  Calls from several host threads are
  * serialised.  While resident the server holds one CTA slot of one SM;
  * pv_server_stop parks it (synchronous) before batch kernels that size their
- * grids to fill every SM.  out->seq is the call's request number. */
+ * grids to fill every SM.  out->seq is the call's request number.
+ * PV_SERVER_IDLE in flags: the caller asserts that nothing queued on `stream`
+ * is still pending that the request depends on, so the stream is not queried
+ * (a cudaStreamQuery costs about as much as a PCIe round trip). */
+#define PV_SERVER_IDLE 0x100u
 int pv_server_walk(const uint8_t* image, uint64_t image_bytes, const pv_space* space /* host */,
                    uint64_t va, uint32_t flags, pv_one_result* out /* host */, void* stream);
 int pv_server_copy_small(uint8_t* image, uint64_t image_bytes, const pv_small_op* op /* host */,
                          uint8_t* buf, uint64_t buf_bytes, pv_small_result* out /* host */,
-                         uint8_t* dirty, void* stream);
+                         uint8_t* dirty, uint32_t flags, void* stream);
 int pv_server_stop(void);
 /* 1 while the server of the current device may be resident. */
 int pv_server_resident(void);
@@ -650,6 +654,9 @@ int pv_gather_pages(const uint8_t* image, uint64_t image_bytes,
 
 /* Synchronises `stream` and reports the first CUDA error seen (0 if none). */
 int pv_stream_sync(void* stream);
+/* 1 when everything queued on `stream` has completed, 0 while work is
+ * pending, negative on a CUDA error (does not synchronise). */
+int pv_stream_idle(void* stream);
 
 /* ---- measurement hook ------------------------------------------------------ */
 /* pv_timing(1) resets and starts recording a CUDA event pair around every

@@ -43,6 +43,7 @@ VA32 = 0x1
 OUT_PFN = 0x2
 CONCURRENT = 0x4  # pv.h PV_CONCURRENT: one walker CTA per SM
 OUT_PACKED = 0x8  # pv.h PV_OUT_PACKED: one u64 per lane
+SERVER_IDLE = 0x100  # pv.h PV_SERVER_IDLE: the caller's stream has nothing pending
 PACKED_ERR = 1 << 63
 PACKED_VALUE_BITS = 42
 PACKED_SPILL_VALUE = (1 << 42) - 1
@@ -77,7 +78,7 @@ FIFO_WORDS = 2 * FIFO_MAX + 4  # pv_fifo
 EXPORTS = (
     "pv_abi_version", "pv_translate_chunk", "pv_status_name", "pv_translate", "pv_translate_words",
     "pv_fifo_replay", "pv_copy_plan", "pv_copy_plan_nodes", "pv_copy_stamp", "pv_copy_exec",
-    "pv_copy_fifo_replay", "pv_scatter_pages", "pv_gather_pages", "pv_stream_sync", "pv_index_encode",
+    "pv_copy_fifo_replay", "pv_scatter_pages", "pv_gather_pages", "pv_stream_sync", "pv_stream_idle", "pv_index_encode",
     "pv_fifo_scratch_bytes", "pv_copy_ordered_scratch_bytes", "pv_copy_ordered", "pv_result_encode",
     "pv_result_decode", "pv_timing", "pv_timing_ms", "pv_copy_shim_scratch_bytes", "pv_copy_shim",
     "pv_map_scratch_bytes", "pv_map_plan", "pv_map_commit",
@@ -122,12 +123,13 @@ _SIGNATURES = {
     "pv_scatter_pages": (ctypes.c_int, [_p, _u64, _p, _u64, _p, _p]),
     "pv_gather_pages": (ctypes.c_int, [_p, _u64, _p, _u64, _p, _p]),
     "pv_stream_sync": (ctypes.c_int, [_p]),
+    "pv_stream_idle": (ctypes.c_int, [_p]),
     "pv_timing": (ctypes.c_int, [ctypes.c_int]),
     "pv_timing_ms": (ctypes.c_double, [ctypes.c_char_p, _p]),
     "pv_walk_one": (ctypes.c_int, [_p, _u64, _p, _u64, _u32, _p, _u64, _p]),
     "pv_copy_small": (ctypes.c_int, [_p, _u64, _p, _p, _u64, _p, _p, _u64, _p]),
     "pv_server_walk": (ctypes.c_int, [_p, _u64, _p, _u64, _u32, _p, _p]),
-    "pv_server_copy_small": (ctypes.c_int, [_p, _u64, _p, _p, _u64, _p, _p, _p]),
+    "pv_server_copy_small": (ctypes.c_int, [_p, _u64, _p, _p, _u64, _p, _p, _u32, _p]),
     "pv_server_stop": (ctypes.c_int, []),
     "pv_server_resident": (ctypes.c_int, []),
     "pv_image_create": (ctypes.c_int, [_u64, _p, _u32, _u64, _p, _p, _p]),
@@ -185,13 +187,37 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         return _lib
 
 
+# cudaStream_t handles that may have library work queued since a per-call
+# operation last found them idle (percall.py skips the stream query otherwise)
+busy_streams: set = set()
+_cuda_ok = False
+_raw_stream = None
+
+
 def lib() -> ctypes.CDLL:
-    """The library, for a compute call: requires a CUDA device."""
+    """The library, for a compute call: requires a CUDA device.  The calling
+    thread's current stream is noted as possibly busy (the caller is about to
+    queue work on it)."""
+    global _cuda_ok, _raw_stream
+    if not _cuda_ok:
+        import torch
+
+        if not torch.cuda.is_available():
+            raise NativeUnavailable("the HAS data plane runs on a CUDA device and none is visible")
+        _raw_stream = torch._C._cuda_getCurrentRawStream
+        _cuda_ok = True
     import torch
 
-    if not torch.cuda.is_available():
-        raise NativeUnavailable("the HAS data plane runs on a CUDA device and none is visible")
+    busy_streams.add(_raw_stream(torch.cuda.current_device()))
     return load()
+
+
+def stream_idle(stream: int) -> bool:
+    """True when everything queued on the cudaStream_t ``stream`` has completed."""
+    r = load().pv_stream_idle(stream)
+    if r < 0:
+        check(r, "pv_stream_idle")
+    return r == 1
 
 
 def check(rc: int, what: str) -> None:

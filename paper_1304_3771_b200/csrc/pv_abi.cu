@@ -550,12 +550,13 @@ static int wait_published(const volatile uint64_t* seq_word, uint64_t sq, cudaSt
 int pv_server_walk(const uint8_t* image, uint64_t image_bytes, const pv_space* space, uint64_t va, uint32_t flags,
                    pv_one_result* out, void* stream) {
   if (!image || !space || !out || image_bytes % kPageSize) return PV_EINVAL;
-  if (flags & ~(uint32_t)PV_OUT_PFN) return PV_EINVAL;
+  if (flags & ~(uint32_t)(PV_OUT_PFN | PV_SERVER_IDLE)) return PV_EINVAL;
   ServerSlot* S = server_slot();
   if (!S) return PV_EINVAL;
   std::lock_guard<std::mutex> lk(S->mu);
   int r;
-  const cudaError_t q = cudaStreamQuery((cudaStream_t)stream);
+  const cudaError_t q = (flags & PV_SERVER_IDLE) ? cudaSuccess : cudaStreamQuery((cudaStream_t)stream);
+  flags &= PV_OUT_PFN;
   if (q == cudaSuccess) {
     r = server_roundtrip(*S, [&](ServerReq& req) {
       req.kind = kServerWalk;
@@ -585,17 +586,19 @@ int pv_server_walk(const uint8_t* image, uint64_t image_bytes, const pv_space* s
 }
 
 int pv_server_copy_small(uint8_t* image, uint64_t image_bytes, const pv_small_op* op, uint8_t* buf,
-                         uint64_t buf_bytes, pv_small_result* out, uint8_t* dirty, void* stream) {
+                         uint64_t buf_bytes, pv_small_result* out, uint8_t* dirty, uint32_t flags,
+                         void* stream) {
   if (!image || !op || !out || image_bytes % kPageSize) return PV_EINVAL;
   if (op->direction != PV_TO_GUEST && op->direction != PV_FROM_GUEST) return PV_EINVAL;
   const uint64_t n = page_span(op->gva, op->len);
   if (n > PV_SMALL_PAGES) return PV_EINVAL;
   if (n != 0 && !buf) return PV_EINVAL;
+  if (flags & ~(uint32_t)PV_SERVER_IDLE) return PV_EINVAL;
   ServerSlot* S = server_slot();
   if (!S) return PV_EINVAL;
   std::lock_guard<std::mutex> lk(S->mu);
   int r;
-  const cudaError_t q = cudaStreamQuery((cudaStream_t)stream);
+  const cudaError_t q = (flags & PV_SERVER_IDLE) ? cudaSuccess : cudaStreamQuery((cudaStream_t)stream);
   if (q == cudaSuccess) {
     r = server_roundtrip(*S, [&](ServerReq& req) {
       req.kind = kServerCopy;
@@ -710,6 +713,13 @@ int pv_gather_pages(const uint8_t* image, uint64_t image_bytes, const uint64_t* 
 int pv_timing(int enable) { return rc(timing_enable(enable != 0)); }
 
 double pv_timing_ms(const char* kernel, uint64_t* launches) { return timing_ms(kernel, launches); }
+
+int pv_stream_idle(void* stream) {
+  const cudaError_t e = cudaStreamQuery((cudaStream_t)stream);
+  if (e == cudaSuccess) return 1;
+  if (e == cudaErrorNotReady) return 0;
+  return rc(e);
+}
 
 int pv_stream_sync(void* stream) {
   cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);

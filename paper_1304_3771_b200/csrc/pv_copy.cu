@@ -697,7 +697,8 @@ __global__ void __launch_bounds__(kSmallTpb) server_kernel(ServerBox* box, uint6
     __syncthreads();
     if (tid == 0) {
       if (kind == kServerStop) st_release_sys_u64(&box->state, kServerExited);
-      __threadfence_system();
+      // the CTA's reply writes are ordered before this release by the barrier
+      // above (cumulativity): no separate system fence
       st_release_sys_u64(&box->rep_seq, s_seq);
       last = s_seq;
     }

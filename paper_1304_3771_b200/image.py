@@ -257,6 +257,7 @@ class MemoryImage:
                 ev.record(stream)
             self._dev_dirty_any = True
             self.dev_write_epoch += 1
+            _native.busy_streams.add(stream.cuda_stream)  # per-call ops query it before skipping ahead
 
     @contextlib.contextmanager
     def writing(self):

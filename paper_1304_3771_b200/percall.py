@@ -51,6 +51,18 @@ _SERVER = os.environ.get("PV_PERCALL_SERVER", "1") != "0"
 _server_used = False
 
 
+def _idle_flag(stream: int) -> int:
+    """PV_SERVER_IDLE unless the library queued work on ``stream`` since a
+    per-call operation last found it idle; a busy stream is queried once and
+    forgotten when it has drained (the query then runs in the library)."""
+    if stream not in N.busy_streams:
+        return N.SERVER_IDLE
+    if N.stream_idle(stream):
+        N.busy_streams.discard(stream)
+        return N.SERVER_IDLE
+    return 0
+
+
 def park() -> None:
     """Stop the per-call server if it may be resident (before a batch launch)."""
     global _server_used
@@ -113,7 +125,8 @@ class PerCall:
             global _server_used
             _server_used = True
             N.check(self.lib.pv_server_walk(dev.data_ptr(), image.nbytes, self.space_ref, va & 0xFFFFFFFFFFFFFFFF,
-                                            N.OUT_PFN if out_pfn else 0, self.one_ptr, stream), "pv_server_walk")
+                                            (N.OUT_PFN if out_pfn else 0) | _idle_flag(stream), self.one_ptr,
+                                            stream), "pv_server_walk")
         else:
             self.seq += 1
             N.check(self.lib.pv_walk_one(dev.data_ptr(), image.nbytes, self.space_ref, va & 0xFFFFFFFFFFFFFFFF,
@@ -150,8 +163,8 @@ class PerCall:
             global _server_used
             _server_used = True
             N.check(self.lib.pv_server_copy_small(dev.data_ptr(), image.nbytes, self.op_ref, self.stage_ptr + buf_off,
-                                                  max(avail - buf_off, 0), self.small_ptr, None, stream),
-                    "pv_server_copy_small")
+                                                  max(avail - buf_off, 0), self.small_ptr, None, _idle_flag(stream),
+                                                  stream), "pv_server_copy_small")
         else:
             self.seq += 1
             N.check(self.lib.pv_copy_small(dev.data_ptr(), image.nbytes, self.op_ref, self.stage_ptr + buf_off,

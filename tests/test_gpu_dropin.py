@@ -80,6 +80,10 @@ def test_ioctl_blob_staging_matches_reference():
     assert mine["blocking/shadow"]["rows"][-1][1] == "PageFault"
 
 
+# reference tests that assert on wall-clock rates (test_acceptance.py:280-324 and the harness scenarios
+# they run): the only ones rerun once on failure
+TIMED = ("test_c06_concurrency_ordering", "test_c07_poll_semantics")
+
 REF_FILES = ["test_memvirt.py", "test_acceptance.py", "test_backend.py", "test_frontend.py", "test_devices.py",
              "test_interrupts.py", "test_guest.py", "test_hypercall.py", "test_harness.py"]
 
@@ -98,6 +102,20 @@ def test_reference_suite_through_dropin(name, tmp_path):
                        capture_output=True, text=True, timeout=1500, env=env, cwd=str(tmp_path))
     out = json.loads(report.read_text()) if report.exists() else {"outcomes": {}}
     failed = {k: v for k, v in out["outcomes"].items() if v != "passed"}
+    timing = [k for k in failed if any(t in k for t in TIMED)]
+    if failed and len(timing) == len(failed):
+        # wall-clock acceptance checks of the reference (real-time threads racing a
+        # compute loop) fail under box noise now and then: rerun those once
+        report.unlink(missing_ok=True)
+        ids = [os.path.join(REF_TESTS, k) for k in timing]
+        p = subprocess.run([sys.executable, "-m", "pytest", *ids, "-q", "-p", "refsuite_plugin", "-p",
+                            "no:cacheprovider", "-o", "addopts=", "--rootdir", REF_TESTS],
+                           capture_output=True, text=True, timeout=1500, env=env, cwd=str(tmp_path))
+        again = json.loads(report.read_text()) if report.exists() else {"outcomes": {}}
+        out["rerun_once"] = again["outcomes"]
+        for k, v in again["outcomes"].items():
+            out["outcomes"][k] = v
+        failed = {k: v for k, v in out["outcomes"].items() if v != "passed"}
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     with open(os.path.join(ROOT, "gpurun_out", f"refsuite_{name[:-3]}.json"), "w") as f:
         json.dump(out, f, indent=0, sort_keys=True)

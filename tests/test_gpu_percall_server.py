@@ -103,6 +103,7 @@ def test_server_call_is_ordered_behind_the_callers_stream(cuda):
     word = torch.tensor([new_pfn << 12 | 1], dtype=torch.int64).view(torch.uint8).cuda()
     torch.cuda._sleep(200_000_000)  # ~0.1 s of queued work ahead of the write
     dev[at:at + 8].copy_(word)
+    memv.host_mem.backing.note_device_write()  # the image contract for device writes
     t0 = time.perf_counter()
     after = int(percall.get().walk(memv.host_mem.backing, tr.device_space, va, False)[1])
     waited = time.perf_counter() - t0
