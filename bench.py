@@ -61,6 +61,10 @@ def parse():
                     "the parity check, and the next form is timed beside it in the same run")
     ap.add_argument("--unpacked", dest="walk_form", action="store_const", const="unpacked",
                     help="same as --walk-form unpacked")
+    ap.add_argument("--split-sms", type=int, default=None, help="C5/C1: run the walk on its own partition of at "
+                    "least this many SMs beside plan + exec on the rest (green contexts, pv_sm_split); 0 = phases "
+                    "back to back (default: 64 for C5 -- the best of 40-72 on one B200, scripts/split_sweep.sh --, "
+                    "0 otherwise); value and the rooflines always come from K steps with the phases back to back")
     ap.add_argument("--overlap", action="store_true", help="time C5/C1 steps with the walk on a second stream "
                     "beside plan + exec (A/B option: measured slower than back-to-back phases, "
                     "profiles/r02_overlap_ab.md)")
@@ -387,12 +391,44 @@ def run_ours(args, rank, world, local):
         ev[1].record(stream)
         img.note_device_write()
 
+    split, split_note = None, None
+    split_sms = args.split_sms if args.split_sms is not None else (64 if wl.name == "c5" else 0)
+    if split_sms and not args.overlap:
+        try:
+            split = dp.SmSplit(split_sms)
+        except Exception as exc:  # noqa: BLE001 - no green contexts: the phases run back to back
+            split_note = f"SM split unavailable ({type(exc).__name__}: {str(exc)[:100]}): phases back to back"
+
+    def step_split(ev):
+        """One step with the walk on SM partition 0 beside plan + exec on
+        partition 1 (disjoint SMs; the batch writes no table page -- the
+        stamp pass's table-hazard check -- so the walk reads the same tables
+        either way)."""
+        ev[0].record(stream)
+        for k in (0, 1):
+            split.streams[k].wait_event(ev[0])
+        with split.on(0) as sa:
+            phase_translate()
+            ev[2].record(sa)
+        with split.on(1) as sb:
+            ev[3].record(sb)
+            phase_plan()
+            ev[4].record(sb)
+            phase_exec()
+            ev[5].record(sb)
+        stream.wait_event(ev[2])
+        stream.wait_event(ev[5])
+        ev[1].record(stream)
+        img.note_device_write()
+
     def barrier():
         if world > 1 and tdist.is_initialized():
             tdist.barrier()
 
     for _ in range(args.warmup):
         step([torch.cuda.Event(enable_timing=True) for _ in range(5)])
+        if split is not None:
+            step_split([torch.cuda.Event(enable_timing=True) for _ in range(6)])
     torch.cuda.synchronize()
     launch_mode = "eager"
     if not args.no_graph:
@@ -419,9 +455,10 @@ def run_ours(args, rank, world, local):
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
-    overlap = args.overlap
+    overlap = args.overlap or split is not None
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
-    ovs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    ovs = [[torch.cuda.Event(enable_timing=True) for _ in range(6 if split is not None else 3)]
+           for _ in range(args.steps)]
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     # the timed region: K steps (walk beside plan + exec unless --serial-step)
@@ -429,11 +466,19 @@ def run_ours(args, rank, world, local):
     torch.cuda.synchronize()
     t_start.record(stream)
     for k in range(args.steps):
-        step_overlap(ovs[k]) if overlap else step(evs[k])
+        if split is not None:
+            step_split(ovs[k])
+        elif overlap:
+            step_overlap(ovs[k])
+        else:
+            step(evs[k])
     t_end.record(stream)
     torch.cuda.synchronize()
     barrier()
     total_ms = t_start.elapsed_time(t_end)
+    split_out = None
+    if split is not None:  # the split steps' lane results, compared with the serial steps' below
+        split_out = (w_words if form == "words" else wl.out[0]).clone()
     if overlap:
         # per-phase figures (value, rooflines): K more steps with the phases back to back
         barrier()
@@ -442,6 +487,9 @@ def run_ours(args, rank, world, local):
             step(evs[k])
         torch.cuda.synchronize()
         barrier()
+    same_split = None
+    if split_out is not None:
+        same_split = bool(torch.equal(split_out, w_words if form == "words" else wl.out[0]))
     clk = clocks.stop()
     # correctness of the timed configuration: no conflicts, every op complete
     assert int(plan.conflict.item()) == 0, "conflicting destinations in the bench batch"
@@ -487,6 +535,13 @@ def run_ours(args, rank, world, local):
     tr_ms = sum(e[0].elapsed_time(e[1]) for e in evs)
     serial_ms = sum(e[0].elapsed_time(e[4]) for e in evs)
     ov_walk_ms = sum(e[0].elapsed_time(e[2]) for e in ovs) if overlap else None
+    split_phases = None
+    if split is not None:
+        split_phases = {"sms": {"walk": split.sms[0], "plan_exec": split.sms[1]},
+                        "walk_ms": sum(e[0].elapsed_time(e[2]) for e in ovs) / args.steps,
+                        "plan_ms": sum(e[3].elapsed_time(e[4]) for e in ovs) / args.steps,
+                        "exec_ms": sum(e[4].elapsed_time(e[5]) for e in ovs) / args.steps,
+                        "lanes_equal_serial_step": same_split}
     plan_ms = sum(e[2].elapsed_time(e[3]) for e in evs)
     exec_ms = sum(e[3].elapsed_time(e[4]) for e in evs)
     copy_ms = sum(e[1].elapsed_time(e[4]) for e in evs)
@@ -544,17 +599,24 @@ def run_ours(args, rank, world, local):
                       "unpacked": "unpacked (u64 value + u32 status)"}[form],
         "exception_records": n_exc,
         "walk_other_form": other,
-        "step": {"mode": "overlapped" if overlap else "serial",
+        "step": {"mode": ("split" if split is not None else "overlapped") if overlap else "serial",
+                 "split": split_phases, "split_note": split_note,
                  "ms": total_ms / K, "serial_ms": serial_ms / K,
                  "translations_per_s": wl.total_vas * K / (total_ms / 1e3),
                  "copy_gbs": wl.total_copy_bytes * K / (total_ms / 1e3) / 1e9,
                  "walk_ms_in_overlap": None if ov_walk_ms is None else ov_walk_ms / K,
                  "hbm_floor_ms": (2 * wl.copy_bytes + walk_bytes + 8 * _leaf_ptes(wl)) / (peak * 1e6),
-                 "note": ("ms_per_step = one step with the walk on a second stream beside plan + exec "
-                          "(PV_CONCURRENT: one walker CTA per SM next to the exec's); value, copy and the "
-                          "rooflines come from K more steps with the phases back to back (serial_ms)")
-                 if overlap else ("phases back to back (--overlap puts the walk beside plan + exec: both "
-                                  "need every SM's L2 request port, measured slower, profiles/r02_overlap_ab.md)")},
+                 "note": ("ms_per_step = one step with the walk on its own SM partition (green context, "
+                          "pv_sm_split) beside plan + exec on the rest; both read/write HBM at once, so each runs "
+                          "slower than alone but the step is shorter than back to back (serial_ms); value, copy "
+                          "and the rooflines come from K more steps with the phases back to back, and the split "
+                          "step's lane results equal theirs (split.lanes_equal_serial_step)")
+                 if split is not None else
+                 ("ms_per_step = one step with the walk on a second stream beside plan + exec "
+                  "(PV_CONCURRENT: one walker CTA per SM next to the exec's); value, copy and the "
+                  "rooflines come from K more steps with the phases back to back (serial_ms)")
+                 if overlap else ("phases back to back (--split-sms N puts the walk on its own SM partition "
+                                  "beside plan + exec)")},
         "per_step": spread,
         "roofline": {"bound": "hbm",
                      "kernel": "pv_copy_exec (" + ("exec_bulk_kernel, TMA" if hint else "exec_kernel, LSU") + ")",

@@ -658,6 +658,22 @@ int pv_stream_sync(void* stream);
  * pending, negative on a CUDA error (does not synchronise). */
 int pv_stream_idle(void* stream);
 
+/* ---- SM partitions ------------------------------------------------------------
+ * Two disjoint SM sets of the current device (green contexts): a group of at
+ * least first_sms SMs and the rest, one non-blocking stream on each (created
+ * once per (device, first_sms) and kept).  Kernels launched on a stream run
+ * only on its SMs, so a walk (bound by the SM->L2 request rate) and a page
+ * copy (bound by HBM) can share the device side by side without competing
+ * for the same SMs.  *sms_first / *sms_rest: the SM counts (may be NULL).
+ * PV_EINVAL when the split is impossible, PV_ECUDA - cudaErrorNotSupported
+ * when the driver has no green contexts. */
+int pv_sm_split(uint32_t first_sms, void** stream_first, void** stream_rest,
+                uint32_t* sms_first, uint32_t* sms_rest);
+/* Grids of the calling thread's subsequent launches are sized for `sms` SMs
+ * (0: the whole device) -- set it to the partition's count while launching
+ * into a pv_sm_split stream.  Returns the previous value. */
+uint32_t pv_set_sm_budget(uint32_t sms);
+
 /* ---- measurement hook ------------------------------------------------------ */
 /* pv_timing(1) resets and starts recording a CUDA event pair around every
  * launch of the library's dominant kernels (on the stream they are launched

@@ -15,7 +15,8 @@ import threading
 
 from .errors import NativeUnavailable
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpv.so")
+# PV_LIB: another build of the same library (A/B experiments of compile-time variants)
+LIB_PATH = os.environ.get("PV_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpv.so")
 
 # ---- constants mirrored from include/pv.h --------------------------------
 ABI_VERSION = 5
@@ -78,7 +79,7 @@ FIFO_WORDS = 2 * FIFO_MAX + 4  # pv_fifo
 EXPORTS = (
     "pv_abi_version", "pv_translate_chunk", "pv_status_name", "pv_translate", "pv_translate_words",
     "pv_fifo_replay", "pv_copy_plan", "pv_copy_plan_nodes", "pv_copy_stamp", "pv_copy_exec",
-    "pv_copy_fifo_replay", "pv_scatter_pages", "pv_gather_pages", "pv_stream_sync", "pv_stream_idle", "pv_index_encode",
+    "pv_copy_fifo_replay", "pv_scatter_pages", "pv_gather_pages", "pv_stream_sync", "pv_stream_idle", "pv_sm_split", "pv_set_sm_budget", "pv_index_encode",
     "pv_fifo_scratch_bytes", "pv_copy_ordered_scratch_bytes", "pv_copy_ordered", "pv_result_encode",
     "pv_result_decode", "pv_timing", "pv_timing_ms", "pv_copy_shim_scratch_bytes", "pv_copy_shim",
     "pv_map_scratch_bytes", "pv_map_plan", "pv_map_commit",
@@ -124,6 +125,8 @@ _SIGNATURES = {
     "pv_gather_pages": (ctypes.c_int, [_p, _u64, _p, _u64, _p, _p]),
     "pv_stream_sync": (ctypes.c_int, [_p]),
     "pv_stream_idle": (ctypes.c_int, [_p]),
+    "pv_sm_split": (ctypes.c_int, [_u32, _p, _p, _p, _p]),
+    "pv_set_sm_budget": (_u32, [_u32]),
     "pv_timing": (ctypes.c_int, [ctypes.c_int]),
     "pv_timing_ms": (ctypes.c_double, [ctypes.c_char_p, _p]),
     "pv_walk_one": (ctypes.c_int, [_p, _u64, _p, _u64, _u32, _p, _u64, _p]),

@@ -11,6 +11,8 @@
 #include <vector>
 #include <unordered_map>
 
+#include <cuda.h>
+
 #include "pv_common.cuh"
 
 namespace pv {
@@ -119,25 +121,37 @@ double timing_ms(const char* name, uint64_t* launches) {
   return ms;
 }
 
+// SMs the calling thread's launches size their grids for (0: the device's);
+// set by pv_set_sm_budget while the thread launches into an SM partition.
+static thread_local uint32_t t_sm_budget = 0;
+
 uint64_t resident_grid(const void* func, int tpb, size_t smem) {
   static std::mutex mu;
-  static std::unordered_map<uint64_t, uint64_t> cache;
+  static std::unordered_map<uint64_t, std::pair<uint64_t, uint64_t>> cache;  // -> (sms, per_sm)
   int dev = 0;
   cudaGetDevice(&dev);
   const uint64_t key = (reinterpret_cast<uint64_t>(func) << 8) ^ (uint64_t)dev ^ ((uint64_t)smem << 48);
+  uint64_t sms_dev = 0, per = 0;
   {
     std::lock_guard<std::mutex> g(mu);
     auto it = cache.find(key);
-    if (it != cache.end()) return it->second;
+    if (it != cache.end()) {
+      sms_dev = it->second.first;
+      per = it->second.second;
+    }
   }
-  int sms = 148, per_sm = 1;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, func, tpb, smem);
-  if (per_sm < 1) per_sm = 1;
-  const uint64_t g = (uint64_t)sms * (uint64_t)per_sm;
-  std::lock_guard<std::mutex> lk(mu);
-  cache[key] = g;
-  return g;
+  if (per == 0) {
+    int sms = 148, per_sm = 1;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, func, tpb, smem);
+    if (per_sm < 1) per_sm = 1;
+    sms_dev = (uint64_t)sms;
+    per = (uint64_t)per_sm;
+    std::lock_guard<std::mutex> lk(mu);
+    cache[key] = {sms_dev, per};
+  }
+  const uint64_t sms = (t_sm_budget != 0 && t_sm_budget < sms_dev) ? t_sm_budget : sms_dev;
+  return sms * per;
 }
 
 cudaError_t ensure_dynamic_smem(const void* func, size_t bytes) {
@@ -713,6 +727,84 @@ int pv_gather_pages(const uint8_t* image, uint64_t image_bytes, const uint64_t* 
 int pv_timing(int enable) { return rc(timing_enable(enable != 0)); }
 
 double pv_timing_ms(const char* kernel, uint64_t* launches) { return timing_ms(kernel, launches); }
+
+}  // extern "C"
+
+// ---- SM partitions (green contexts through driver entry points: no libcuda link)
+namespace {
+struct SmSplit {
+  uint32_t want = 0;
+  void* green[2] = {nullptr, nullptr};
+  cudaStream_t stream[2] = {nullptr, nullptr};
+  uint32_t sms[2] = {0, 0};
+};
+std::mutex g_split_mu;
+std::unordered_map<uint64_t, SmSplit> g_splits;  // (device << 32 | want) -> partition
+
+template <class F>
+bool driver_fn(const char* name, F* fn) {
+  cudaDriverEntryPointQueryResult q;
+  void* p = nullptr;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess ||
+      p == nullptr)
+    return false;
+  *fn = reinterpret_cast<F>(p);
+  return true;
+}
+}  // namespace
+
+extern "C" {
+
+int pv_sm_split(uint32_t first_sms, void** stream_first, void** stream_rest, uint32_t* sms_first,
+                uint32_t* sms_rest) {
+  if (!stream_first || !stream_rest || first_sms == 0) return PV_EINVAL;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return rc(e);
+  std::lock_guard<std::mutex> lk(g_split_mu);
+  SmSplit& P = g_splits[((uint64_t)dev << 32) | first_sms];
+  if (P.stream[0] == nullptr) {
+    CUresult (*getres)(CUdevice, CUdevResource*, CUdevResourceType) = nullptr;
+    CUresult (*split)(CUdevResource*, unsigned*, const CUdevResource*, CUdevResource*, unsigned, unsigned) = nullptr;
+    CUresult (*gendesc)(CUdevResourceDesc*, CUdevResource*, unsigned) = nullptr;
+    CUresult (*gcreate)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned) = nullptr;
+    CUresult (*gstream)(CUstream*, CUgreenCtx, unsigned, int) = nullptr;
+    CUresult (*getdev)(CUdevice*, int) = nullptr;
+    if (!driver_fn("cuDeviceGetDevResource", &getres) || !driver_fn("cuDevSmResourceSplitByCount", &split) ||
+        !driver_fn("cuDevResourceGenerateDesc", &gendesc) || !driver_fn("cuGreenCtxCreate", &gcreate) ||
+        !driver_fn("cuGreenCtxStreamCreate", &gstream) || !driver_fn("cuDeviceGet", &getdev))
+      return PV_ECUDA - (int)cudaErrorNotSupported;
+    CUdevice cd;
+    CUdevResource all, grp[1], rem;
+    unsigned nb = 1;
+    if (getdev(&cd, dev) != CUDA_SUCCESS || getres(cd, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS ||
+        first_sms >= all.sm.smCount || split(grp, &nb, &all, &rem, 0, first_sms) != CUDA_SUCCESS || nb != 1)
+      return PV_EINVAL;
+    CUdevResource* parts[2] = {&grp[0], &rem};
+    for (int i = 0; i < 2; ++i) {
+      CUdevResourceDesc d;
+      CUgreenCtx g;
+      CUstream cs;
+      if (gendesc(&d, parts[i], 1) != CUDA_SUCCESS || gcreate(&g, d, cd, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS ||
+          gstream(&cs, g, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS)
+        return PV_ECUDA - (int)cudaErrorNotSupported;
+      P.green[i] = g;
+      P.stream[i] = (cudaStream_t)cs;
+      P.sms[i] = parts[i]->sm.smCount;
+    }
+  }
+  *stream_first = P.stream[0];
+  *stream_rest = P.stream[1];
+  if (sms_first) *sms_first = P.sms[0];
+  if (sms_rest) *sms_rest = P.sms[1];
+  return PV_SUCCESS;
+}
+
+uint32_t pv_set_sm_budget(uint32_t sms) {
+  const uint32_t old = t_sm_budget;
+  t_sm_budget = sms;
+  return old;
+}
 
 int pv_stream_idle(void* stream) {
   const cudaError_t e = cudaStreamQuery((cudaStream_t)stream);

@@ -288,6 +288,9 @@ exec_kernel(uint8_t* __restrict__ image, uint64_t image_bytes, const pv_op* __re
 #ifndef PV_BULK_STAGES
 #define PV_BULK_STAGES 6
 #endif
+#ifndef PV_BULK_EVICT_FIRST
+#define PV_BULK_EVICT_FIRST 0  // evict-first bulk copies measured slower (exec 2.79 vs 2.75 ms, scripts/ab_evict.sh)
+#endif
 constexpr int kBulkWarps = PV_BULK_WARPS;
 constexpr int kBulkStages = PV_BULK_STAGES;
 constexpr size_t kBulkSmem = (size_t)kBulkWarps * kBulkStages * kPageSize;
@@ -399,9 +402,18 @@ exec_bulk_kernel(uint8_t* __restrict__ image, uint64_t image_bytes, const pv_op*
       const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&bars[wid][st]);
       const uint32_t sm = (uint32_t)__cvta_generic_to_shared(ring + (size_t)st * kPageSize);
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(mid) : "memory");
+#if PV_BULK_EVICT_FIRST
+      // streamed payload: evict-first in L2, so it does not push out what a walk beside it keeps there
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+              sm),
+          "l"(src + head), "r"(mid), "r"(bar), "l"(pol)
+          : "memory");
+#else
       asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sm),
                    "l"(src + head), "r"(mid), "r"(bar)
                    : "memory");
+#endif
     }
   };
   for (uint64_t j = 0; j + 1 < (uint64_t)kBulkStages && j < n; ++j) issue_load(j);
@@ -426,8 +438,14 @@ exec_bulk_kernel(uint8_t* __restrict__ image, uint64_t image_bytes, const pv_op*
             : "memory");
         parity ^= 1u << st;
         const uint32_t sm = (uint32_t)__cvta_generic_to_shared(ring + (size_t)st * kPageSize);
+#if PV_BULK_EVICT_FIRST
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst + head),
+                     "r"(sm), "r"(mid), "l"(pol)
+                     : "memory");
+#else
         asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + head), "r"(sm), "r"(mid)
                      : "memory");
+#endif
       }
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");  // one group per slot, empty or not
     }

@@ -19,6 +19,7 @@ Status words are decoded back into the reference's exceptions by
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import os
 import struct
@@ -391,6 +392,38 @@ def unpack_lanes(packed, aux=None) -> tuple[np.ndarray, np.ndarray]:
         value = value.copy()
         value[spill] = np.asarray(aux).view(np.uint64)[spill]
     return value, status
+
+
+class SmSplit:
+    """Two disjoint SM partitions of the current device (pv_sm_split, green
+    contexts): ``streams[0]`` runs on a group of at least ``first_sms`` SMs,
+    ``streams[1]`` on the rest.  ``with split.on(k):`` makes partition k's
+    stream current and sizes the library's grids for its SMs, so a walk (SM->L2
+    request bound) on one partition and a page copy (HBM bound) on the other
+    run side by side without sharing SMs."""
+
+    def __init__(self, first_sms: int):
+        import torch
+
+        lib = N.lib()
+        a, b = ctypes.c_void_p(), ctypes.c_void_p()
+        na, nb = ctypes.c_uint32(), ctypes.c_uint32()
+        N.check(lib.pv_sm_split(first_sms, ctypes.byref(a), ctypes.byref(b), ctypes.byref(na), ctypes.byref(nb)),
+                "pv_sm_split")
+        self.streams = (torch.cuda.ExternalStream(a.value), torch.cuda.ExternalStream(b.value))
+        self.sms = (int(na.value), int(nb.value))
+
+    @contextlib.contextmanager
+    def on(self, k: int):
+        import torch
+
+        lib = N.lib()
+        with torch.cuda.stream(self.streams[k]):
+            old = lib.pv_set_sm_budget(self.sms[k])
+            try:
+                yield self.streams[k]
+            finally:
+                lib.pv_set_sm_budget(old)
 
 
 class LaneExceptions:
