@@ -5,7 +5,7 @@
 tag=${1:-prof}
 mkdir -p gpurun_out
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"^(translate|stage|plan|stamp|exec|shim)" -c 16 --csv \
-  --log-file gpurun_out/${tag}_launches_c5.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline \
+  --log-file gpurun_out/${tag}_launches_c5.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --split-sms 0 \
   > gpurun_out/${tag}_launch_c5.json 2> gpurun_out/${tag}_launch_c5.err
 echo "c5 launch list rc=$?"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name-base demangled -k regex:"pv::|CUB_" -c 60 --csv \
@@ -14,7 +14,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --kernel-n
 echo "c2 launch list rc=$?"
 timeout 1200 ncu --set full --clock-control none --import-source on \
   -k regex:"translate_kernel|exec_bulk_kernel|exec_kernel" -c 2 -o gpurun_out/${tag}_c5_full \
-  python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/${tag}_c5_full.log 2>&1
+  python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --split-sms 0 > gpurun_out/${tag}_c5_full.log 2>&1
 echo "c5 full rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on \
   -k regex:"ordered_apply_kernel|fifo_verify_kernel|plan_kernel" -c 3 -o gpurun_out/${tag}_c2_full \
