@@ -518,9 +518,12 @@ static cudaError_t launch_t(const uint8_t* image, uint64_t image_bytes, const pv
 #ifndef PV_TR2_TPB
 #define PV_TR2_TPB 512  // two-stage walks: 512 x 4 lanes, 2 CTAs/SM (C1 TDP 37.5 vs 28.2 G/s at 256 x 8)
 #endif
+#ifndef PV_TR1_TPB
+#define PV_TR1_TPB 512
+#endif
   auto k = kTwo ? translate_kernel<kTwo, kVa32, kPfn, PV_TR2_TPB, (PV_TR2_TPB == 256 ? 3 : 1024 / PV_TR2_TPB)>
-                : translate_kernel<kTwo, kVa32, kPfn, 512, PV_TR_MINB>;
-  const int tpb = kTwo ? PV_TR2_TPB : 512;
+                : translate_kernel<kTwo, kVa32, kPfn, PV_TR1_TPB, PV_TR_MINB * 512 / PV_TR1_TPB>;
+  const int tpb = kTwo ? PV_TR2_TPB : PV_TR1_TPB;
   uint64_t grid = resident_grid((const void*)k, tpb, 0);
   if (concurrent) {
     // PV_CONCURRENT: one CTA per SM, so a kernel launched beside the walk
