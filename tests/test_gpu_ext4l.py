@@ -57,9 +57,23 @@ def test_4l_faults_traps_and_aliasing(cuda):
     vas += [X.C3_VA + (1 << 30) + rng.randrange(1 << 20) for _ in range(100)]
     vas += [(rng.randrange(1, 1 << 16) << 48) | (X.C3_VA + rng.randrange(region)) for _ in range(1000)]  # alias
     vas += [rng.randrange(1 << 48) for _ in range(1000)]
-    st = _check(mem, t, np.array(vas, dtype=np.uint64))
+    vas = np.array(vas, dtype=np.uint64)
+    st = _check(mem, t, vas)
     kinds = {int(x) & 0xFF0 for x in st}
     assert {0x000, 0x010, 0x040, 0x080} <= kinds
+    # the generic kernel's 4-byte lane words (+ exception records for the traps) decode to the same lanes
+    plan = dp.TranslatePlan([t.space], [(0, len(vas), 0)])
+    d = torch.tensor(vas.view(np.int64), device="cuda")
+    v, s, _ = dp.translate_lanes(mem.backing, plan, d)
+    w = torch.empty(len(vas), dtype=torch.int32, device="cuda")
+    rec = torch.empty(len(vas) * N.EXC_WORDS, dtype=torch.int64, device="cuda")
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    dp.translate_words(mem.backing, plan, d, w, rec, cnt)
+    n = int(cnt.item())
+    assert n == int(((st & 0xFF0) == 0x040).sum())  # traps carry their node: one record each
+    exc = dp.LaneExceptions.from_records(rec[:n * N.EXC_WORDS].cpu().numpy())
+    wv, ws, _ = dp.unpack_words(w.cpu().numpy(), vas, exc)
+    assert np.array_equal(ws, st) and np.array_equal(wv, v.cpu().numpy().view(np.uint64))
     levels = {int(x) & 0xF for x in st if int(x) & 0xFF0 == 0x010}
     assert {1, 3, 4} <= levels
 

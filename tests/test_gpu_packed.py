@@ -164,3 +164,13 @@ def test_translate_many_words_equal_split(cuda, mode):
         assert np.array_equal(us, s.numpy().view(np.uint32)) and np.array_equal(uv, v.numpy().view(np.uint64))
         assert np.array_equal(ua, a.numpy().view(np.uint64))
     assert dp.last_host_io["d2h"] >= 4 * sum(h.numel() for _, h in jobs)
+
+
+def test_translate_many_words_empty_inputs(cuda):
+    memv, space = _c4("shadow")
+    tr = memv.translator(space, use_cache=False)
+    assert mv.translate_many([], words=True) == []
+    (w, none, exc), = mv.translate_many([(tr, torch.zeros(0, dtype=torch.int32).pin_memory())], words=True)
+    assert w.numel() == 0 and none is None and len(exc) == 0
+    v, s, a = dp.unpack_words(w.numpy(), np.zeros(0, np.uint32), exc)
+    assert len(v) == len(s) == len(a) == 0
