@@ -644,6 +644,13 @@ int pv_result_decode(const uint8_t* image, uint64_t image_bytes, const uint64_t*
                      uint64_t n, uint32_t* header, uint32_t* status, void* stream);
 
 /* ---- utility kernels used by the host runtime ---------------------------- */
+/* Copy `bytes` from pinned (device-mapped) host memory to device memory with
+ * SM loads over the host link instead of a copy engine, so small descriptor
+ * uploads do not queue behind a large host-to-device transfer already in
+ * flight on another stream (a copy batch whose payload is still arriving).
+ * dst and src 16-byte aligned. */
+int pv_upload(void* dst, const void* src, uint64_t bytes, void* stream);
+
 /* Scatter `n` whole pages from a (pinned) host staging area into the image:
  * page i of src goes to image page pfns[i].  pfns device, src device. */
 int pv_scatter_pages(uint8_t* image, uint64_t image_bytes, const uint64_t* pfns,

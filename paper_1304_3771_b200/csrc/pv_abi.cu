@@ -187,6 +187,17 @@ cudaError_t stream_scratch(void** p, size_t bytes, cudaStream_t stream) {
   return cudaMallocAsync(p, bytes < 256 ? 256 : bytes, stream);
 }
 
+// Host -> device copy done by SMs reading host-mapped pinned memory over the
+// link (16 bytes per load), so it never queues behind copy-engine transfers
+// already in flight (pv_upload).
+__global__ void __launch_bounds__(256) upload_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src,
+                                                     uint64_t n16, uint8_t* __restrict__ dst_tail,
+                                                     const uint8_t* __restrict__ src_tail, uint32_t tail) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride) dst[i] = src[i];
+  if (blockIdx.x == 0 && threadIdx.x < tail) dst_tail[threadIdx.x] = src_tail[threadIdx.x];
+}
+
 __global__ void scatter_pages_kernel(uint8_t* __restrict__ image, uint64_t image_pages,
                                      const uint64_t* __restrict__ pfns, uint64_t n, const uint8_t* __restrict__ src) {
   for (uint64_t i = blockIdx.x; i < n; i += gridDim.x) {
@@ -712,6 +723,20 @@ int pv_scatter_pages(uint8_t* image, uint64_t image_bytes, const uint64_t* pfns,
   if (!image || !pfns || !src || image_bytes % kPageSize) return PV_EINVAL;
   const uint64_t grid = n < 4096 ? n : 4096;
   scatter_pages_kernel<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(image, image_bytes / kPageSize, pfns, n, src);
+  return rc(cudaGetLastError());
+}
+
+int pv_upload(void* dst, const void* src, uint64_t bytes, void* stream) {
+  if (bytes == 0) return PV_SUCCESS;
+  if (!dst || !src || (reinterpret_cast<uintptr_t>(dst) & 15) || (reinterpret_cast<uintptr_t>(src) & 15))
+    return PV_EINVAL;
+  const uint64_t n16 = bytes / 16;
+  uint64_t grid = (n16 + 255) / 256;
+  if (grid > 148) grid = 148;
+  if (grid == 0) grid = 1;
+  upload_kernel<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(
+      static_cast<uint4*>(dst), static_cast<const uint4*>(src), n16, static_cast<uint8_t*>(dst) + n16 * 16,
+      static_cast<const uint8_t*>(src) + n16 * 16, (uint32_t)(bytes & 15));
   return rc(cudaGetLastError());
 }
 

@@ -85,6 +85,51 @@ def _to_dev(arr: np.ndarray, stream=None):
     return t.to("cuda", non_blocking=True)
 
 
+_UPLOAD_MAX = 1 << 20  # arrays up to this size go through pv_upload (SM loads), larger ones through DMA
+_uploads_in_flight: list = []  # (event, pinned block) until the stream has passed the upload
+
+
+def _to_dev_many(arrays):
+    """Device copies of several host arrays, the small ones (< 1 MiB together
+    per array) packed into one pinned block and moved by one pv_upload
+    kernel: SM loads over the host link, which do not queue behind a large
+    H2D already in flight on another stream (a copy batch's payload), so the
+    batch's plan runs while its payload is still arriving."""
+    import torch
+
+    arrs = [np.ascontiguousarray(a) for a in arrays]
+    if torch.cuda.is_current_stream_capturing():
+        return [_to_dev(a) for a in arrs]
+    small = [i for i, a in enumerate(arrs) if a.nbytes <= _UPLOAD_MAX]
+    out = [None] * len(arrs)
+    for i, a in enumerate(arrs):
+        if i not in small:
+            out[i] = _to_dev(a)
+    if small:
+        offs, total = [], 0
+        for i in small:
+            offs.append(total)
+            total += (arrs[i].nbytes + 15) & ~15
+        total = max(total, 16)
+        host = torch.empty(total, dtype=torch.uint8, pin_memory=True)
+        hv = host.numpy()
+        for i, o in zip(small, offs):
+            hv[o:o + arrs[i].nbytes] = arrs[i].reshape(-1).view(np.uint8)
+        dev = torch.empty(total, dtype=torch.uint8, device="cuda")
+        stream = _stream()
+        N.check(N.lib().pv_upload(dev.data_ptr(), host.data_ptr(), total, stream.cuda_stream), "pv_upload")
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        while _uploads_in_flight and _uploads_in_flight[0][0].query():
+            _uploads_in_flight.pop(0)
+        _uploads_in_flight.append((ev, host))
+        for i, o in zip(small, offs):
+            a = arrs[i]
+            dt = torch.from_numpy(a.reshape(-1)[:0]).dtype
+            out[i] = dev[o:o + a.nbytes].view(dt).view(a.shape)
+    return out
+
+
 def _stream():
     import torch
 
@@ -840,9 +885,11 @@ class CopyPlan:
         self.n_pages = int(page_off[-1])
         self.host_ops = ops
         self.host_page_off = page_off
-        self.spaces = _to_dev(_i64([sp.words() for sp in spaces]).reshape(-1, 4))
-        self.ops = _to_dev(ops.view(np.int64))
-        self.page_off = _to_dev(page_off.view(np.int64))
+        up = [_i64([sp.words() for sp in spaces]).reshape(-1, 4), ops.view(np.int64), page_off.view(np.int64)]
+        if shims is not None and any(sh is not None for sh in shims):
+            up.append(_i64([(sh or NO_SHIM).words() for sh in shims]).reshape(-1, 4))
+        up = _to_dev_many(up)
+        self.spaces, self.ops, self.page_off = up[0], up[1], up[2]
         np_ = max(self.n_pages, 1)
         self.page_hpa = torch.empty(np_, dtype=torch.int64, device="cuda")
         self.page_status = torch.empty(np_, dtype=torch.int32, device="cuda")
@@ -851,8 +898,8 @@ class CopyPlan:
         self.results = torch.empty((max(self.n_ops, 1), 4), dtype=torch.int64, device="cuda")
         self.conflict = torch.zeros(1, dtype=torch.int32, device="cuda")
         self.shims = None
-        if shims is not None and any(sh is not None for sh in shims):
-            self.shims = _to_dev(_i64([(sh or NO_SHIM).words() for sh in shims]).reshape(-1, 4))
+        if len(up) > 3:
+            self.shims = up[3]
             self.shim_written = torch.zeros(1, dtype=torch.int64, device="cuda")
         self.fifo_groups = fifo_groups
         if fifo_groups is not None:
@@ -875,11 +922,10 @@ class CopyPlan:
             lpg = np.concatenate(look_page) if look_page else np.zeros(0, np.int64)
             self.fifo_lookups = int(lk_off[-1])
             self.fifo_win = _windows(lk_off)
-            self.fifo_look_op = _to_dev(lop.astype(np.uint32).view(np.int32)) if len(lop) else \
-                torch.zeros(1, dtype=torch.int32, device="cuda")
-            self.fifo_look_page = _to_dev(lpg) if len(lpg) else torch.zeros(1, dtype=torch.int64, device="cuda")
-            self.fifo_off = _to_dev(lk_off)
-            self.fifo_win_d = _to_dev(self.fifo_win)
+            lop = lop.astype(np.uint32).view(np.int32) if len(lop) else np.zeros(1, np.int32)
+            lpg = lpg if len(lpg) else np.zeros(1, np.int64)
+            self.fifo_look_op, self.fifo_look_page, self.fifo_off, self.fifo_win_d = _to_dev_many(
+                [lop, lpg, lk_off, self.fifo_win])
             self.fifo_scratch = None
 
 
@@ -1109,7 +1155,7 @@ def copy_ops(image, spaces: list[Space], ops: np.ndarray, direction: int, buf, *
     """
     cap = fifo_capacity(caches) if caches is not None else 10
     plan = CopyPlan(spaces, ops, fifo_groups=fifo_groups if caches is not None else None, shims=shims)
-    fifo_dev = _to_dev(pack_fifo(caches)) if caches is not None else None
+    fifo_dev = _to_dev_many([pack_fifo(caches).view(np.int64)])[0] if caches is not None else None
     copy_launch(image, plan, direction, buf, fifo_dev=fifo_dev, fifo_cap=cap, detect_conflicts=detect_conflicts,
                 buf_ready=buf_ready, buf_bytes=buf_bytes)
     conflict = int(plan.conflict.item()) if direction == N.TO_GUEST and detect_conflicts else 0

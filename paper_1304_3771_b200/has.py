@@ -181,12 +181,12 @@ class _BatchMixin:
             outs = dp.copy_ops(image, [space], part, direction, buf, shims=[shim], buf_ready=buf_ready)
             cut = next((i for i, o in enumerate(outs) if dp.kind(o.status) in (N.ST_TRAP, N.ST_TRAP2)), None)
             upto = len(outs) if cut is None else cut
-            for o, r in zip(outs[:upto], part[:upto]):
-                if o.status == N.ST_OK:
-                    tr._count(int(dp.page_spans(r[None, 0], r[None, 1])[0]))
-                else:
-                    tr._count(o.fail_page + 1)
+            spans = dp.page_spans(part[:upto, 0], part[:upto, 1])  # _HybridResolver: one translation per page
+            n = 0
+            for o, r, sp in zip(outs[:upto], part[:upto], spans.tolist()):
+                n += sp if o.status == N.ST_OK else o.fail_page + 1
                 results.append(_decode_outcome(o, r, image.nbytes))
+            tr._count(n)
             if cut is None:
                 break
             r = part[cut]

@@ -64,9 +64,16 @@ def _idle_flag(stream: int) -> int:
 
 
 def park() -> None:
-    """Stop the per-call server if it may be resident (before a batch launch)."""
+    """Stop the per-call server if it may be resident (before a batch launch).
+    Not while the current stream is being captured into a CUDA graph (the stop
+    synchronises the server's stream); the server then leaves on its own
+    after its idle time."""
     global _server_used
     if _server_used:
+        import torch
+
+        if torch.cuda.is_current_stream_capturing():
+            return
         _server_used = False
         N.check(N.lib().pv_server_stop(), "pv_server_stop")
 
