@@ -318,7 +318,13 @@ def run_ours(args, rank, world, local):
             dp.translate_lanes(img, wl.tplan, wl.vas, out=wl.out)
 
     def phase_translate_conc():  # the same walk sized to share every SM with the exec (PV_CONCURRENT)
-        dp.translate_lanes(img, wl.tplan, wl.vas, out=wl.out, concurrent=True)
+        if form == "words":
+            w_cnt.zero_()
+            dp.translate_words(img, wl.tplan, wl.vas, w_words, w_rec, w_cnt, concurrent=True)
+        elif form == "packed":
+            dp.translate_lanes(img, wl.tplan, wl.vas, out=(wl.out[0], None, wl.out[2]), packed=True, concurrent=True)
+        else:
+            dp.translate_lanes(img, wl.tplan, wl.vas, out=wl.out, concurrent=True)
 
     def phase_plan():  # fills + plan + trap shim + conflict stamp
         cs = torch.cuda.current_stream().cuda_stream

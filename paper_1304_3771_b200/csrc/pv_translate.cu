@@ -521,13 +521,21 @@ static cudaError_t launch_t(const uint8_t* image, uint64_t image_bytes, const pv
 #ifndef PV_TR1_TPB
 #define PV_TR1_TPB 512
 #endif
+#ifndef PV_CONC_TPB
+#define PV_CONC_TPB 256  // PV_CONCURRENT one-stage walks: 256 x 8 lanes, <= 64 registers
+#endif
   auto k = kTwo ? translate_kernel<kTwo, kVa32, kPfn, PV_TR2_TPB, (PV_TR2_TPB == 256 ? 3 : 1024 / PV_TR2_TPB)>
                 : translate_kernel<kTwo, kVa32, kPfn, PV_TR1_TPB, PV_TR_MINB * 512 / PV_TR1_TPB>;
-  const int tpb = kTwo ? PV_TR2_TPB : PV_TR1_TPB;
+  int tpb = kTwo ? PV_TR2_TPB : PV_TR1_TPB;
+  if (concurrent && !kTwo) {
+    // PV_CONCURRENT: a small CTA (256 threads x <= 64 registers, 8 KiB of
+    // SMEM) per SM, so it fits beside the copy exec's CTA (256 threads x 166
+    // registers, 192 KiB of SMEM) on every SM: the two kernels co-reside
+    k = translate_kernel<kTwo, kVa32, kPfn, PV_CONC_TPB, 1024 / PV_CONC_TPB>;
+    tpb = PV_CONC_TPB;
+  }
   uint64_t grid = resident_grid((const void*)k, tpb, 0);
   if (concurrent) {
-    // PV_CONCURRENT: one CTA per SM, so a kernel launched beside the walk
-    // (the copy exec: one 192 KiB CTA per SM) finds room on every SM
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
