@@ -986,6 +986,8 @@ def run_c2(args, rank, world, local):
                                                      "(stands down), ordered keys (+ results), apply; CUB select / "
                                                      "radix sort / RLE / scan kernels not counted",
         "clocks": clk, "build_s": build_s,
+        "cpu_baseline": (c2_cpu_baseline(memv, spaces, procs, gvas, lens, cpu_threads())
+                         if rank == 0 and world == 1 and not args.no_cpu_baseline else None),
     }
 
 
@@ -1551,6 +1553,101 @@ def _pyref_worker(args):
         acc.copy_to_user(0x1000_0000 + (i % 15) * (4 << 20) + 0x80, data)
     t_cp = time.perf_counter() - t0
     return n_vas / t_tr, n_ops * len(data) / t_cp / 1e9
+
+
+def _pyref_c2_worker(args):
+    """One core of the reference's C2 path (devfsim from baseline/_ref,
+    unmodified): a TDP guest (software HAS, blocking transport), the
+    EventDevice, one process with a 256-page arena; IOCTL_SNAPSHOT ops with
+    arg_len = randint(64, 4096) at arena + randrange(1 MiB - 4096) issued by a
+    guest thread through Frontend.vfs_dispatch (frontend.py:124-170 ->
+    hypercall -> Backend.execute_fileop, blob staging backend.py:526-534),
+    the dispatch loop timed with perf_counter."""
+    worker, n_ops = args
+    import random as _r
+
+    sys.path.insert(0, os.path.join(ROOT, "baseline", "_ref"))
+    from devfsim.devices import IOCTL_SNAPSHOT, EventDevice
+    from devfsim.hypercall import FileOp, FileOpKind
+    from devfsim.workloads import open_device
+    from devfsim.world import World
+
+    world = World()
+    try:
+        guest = world.add_guest(vcpus=1, mem_mode="tdp")
+        evt = world.add_device(EventDevice(1, "evt", world.clock))
+        world.set_mode(guest, evt, "blocking")
+        process = world.new_process(guest)
+        world.map_buffer(process, 0x2000_0000, 256)
+        frontend = world.frontends[guest.id]
+        rng = _r.Random(3771 + worker)
+        ops = [(0x2000_0000 + rng.randrange((1 << 20) - 4096), rng.randint(64, 4096)) for _ in range(n_ops)]
+        box = {}
+
+        def body(t):
+            file = frontend.files["/dev/evt"]
+            handle = open_device(frontend, t, file)
+            t0 = time.perf_counter()
+            for gva, ln in ops:
+                frontend.vfs_dispatch(t, file, FileOp(kind=FileOpKind.IOCTL, handle=handle, cmd=IOCTL_SNAPSHOT,
+                                                      arg_gva=gva, arg_len=ln))
+            box["s"] = time.perf_counter() - t0
+
+        thread = world.new_thread(process)
+        thread.start(body)
+        thread.join(300.0)
+        return n_ops / box["s"]
+    finally:
+        world.close()
+
+
+def c2_cpu_baseline(memv, spaces, procs, gvas, lens, cores: int, py_ops: int = 1000) -> dict:
+    """C2 on the host cores: the oracle port (oracle/pvoracle.c) stages the
+    whole trace's blobs -- every op's 2-stage translations through its
+    process's FIFO-10 cache, then the copy, in program order per process (one
+    thread per process; processes write disjoint arenas) -- and the
+    reference's own Python forwarding path is timed per core beside it."""
+    import concurrent.futures as cf
+
+    sys.path.insert(0, ROOT)
+    from oracle import oracle as O
+
+    img = memv.host_mem.backing.host_for_read().copy()
+    sp = np.stack([O.space(s.s1_base, s.s1_root_pfn, s.s2_root_pfn, s.mode) for s in
+                   (memv.translator(x, use_cache=False).device_space for x in spaces)])
+    # every op's blob is the same function of its byte index (devices.py:162-166), so one 4 KiB snapshot
+    # serves as every op's source (buffer offset 0): the same bytes as the device payload, 4 KiB of memory
+    buf = ((np.arange(4096, dtype=np.int64) * 7 + 3) & 0xFF).astype(np.uint8)
+    rows = np.stack([gvas, lens, np.zeros_like(gvas), procs], 1).astype(np.uint64)
+
+    def one(p):
+        sel = rows[procs == p]
+        cache = O.new_cache(10).reshape(1, -1)
+        return O.copy(img, sp, sel, buf, 0, caches=cache, op_cache=np.zeros(len(sel), np.int32))
+
+    n_procs = len(spaces)
+    with cf.ThreadPoolExecutor(n_procs) as ex:
+        list(ex.map(one, range(n_procs)))  # warm: page-in of the image copy and the payload
+        t0 = time.perf_counter()
+        res = list(ex.map(one, range(n_procs)))
+        dt = time.perf_counter() - t0
+    ok = all(((r[:, 3] & 0xFFFFFFFF) == 0).all() for r in res)
+    out = {"value": len(gvas) / dt, "unit": "ioctls/s", "cores": n_procs, "kind": "port",
+           "sample": f"the whole trace ({len(gvas)} ops): blob staging only (2-stage translations through the "
+                     "FIFO-10 caches + copies), one thread per process", "cpu": cpu_model(), "all_ok": bool(ok)}
+    if os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "devfsim")):
+        import multiprocessing as mp
+
+        t0 = time.perf_counter()
+        with mp.get_context("spawn").Pool(cores) as pool:
+            rates = pool.map(_pyref_c2_worker, [(w, py_ops) for w in range(cores)])
+        out["python_reference"] = {
+            "kind": "reference (devfsim, unmodified pure Python from baseline/_ref)", "cores": cores,
+            "ioctls_per_s_per_core": statistics.median(rates), "ioctls_per_s": sum(rates),
+            "sample": f"per core: {py_ops} IOCTL_SNAPSHOT ops through Frontend.vfs_dispatch (blocking, TDP guest, "
+                      "software HAS): forwarding + driver + blob staging",
+            "wall_s": round(time.perf_counter() - t0, 1)}
+    return out
 
 
 def python_reference_baseline(cores: int, n_vas: int = 300_000, n_ops: int = 48) -> dict | None:
