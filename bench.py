@@ -1058,6 +1058,10 @@ def run_c3(args, rank, world, local):
                      "unit": "GB/s", "frac": ach / peak, "peak_source": peak_kind,
                      "note": "20 B/translation (u64 VA in, u64 hpa + u32 status out)"},
         "launch": launch_mode, "gpu_launches": args.steps, "clocks": clk, "build_s": build_s,
+        "cpu_baseline": (translate_cpu_baseline(mem.backing.host_for_read(), [t.space.s1_base, t.space.s1_root_pfn, 0,
+                                                                              t.space.mode], vas_h,
+                                                "4-level walks over the 16 GiB mixed-page mapping")
+                         if rank == 0 and world == 1 and not args.no_cpu_baseline else None),
     }
 
 
@@ -1214,6 +1218,10 @@ def run_c4(args, rank, world, local):
         "launch": launch_mode,
         "gpu_launches": 7 * K, "gpu_launches_note": "translate, plan, shim eval + cooperative resolve, stamp, exec per step (+ leaf-index re-encode)",
         "clocks": clk, "build_s": build_s,
+        "cpu_baseline": (translate_cpu_baseline(img.host_for_read(), [tr.device_space.s1_base, tr.device_space.s1_root_pfn,
+                                                                       0, N.ONE_STAGE], vas_h.astype(np.uint64),
+                                                "shadow walks with 30 % corrupted leaves")
+                         if rank == 0 and world == 1 and not args.no_cpu_baseline else None),
     }
 
 
@@ -1671,6 +1679,26 @@ def python_reference_baseline(cores: int, n_vas: int = 300_000, n_ops: int = 48)
             "sample": f"per core: C1 shadow world (16,384 shuffled pages), {n_vas} uncached translate() calls + "
                       f"{n_ops} x 4 MiB HardwareHasAccess.copy_to_user",
             "wall_s": round(time.perf_counter() - t0, 1)}
+
+
+def translate_cpu_baseline(img: np.ndarray, space_words, vas: np.ndarray, note: str) -> dict:
+    """The oracle port's batch translation (oracle/pvoracle.c, all host
+    threads) over the same lanes as the device step, one untimed pass then
+    the median of three."""
+    sys.path.insert(0, ROOT)
+    from oracle import oracle as O
+
+    threads = cpu_threads()
+    sp = np.asarray(space_words, dtype=np.uint64)
+    v = np.ascontiguousarray(vas, dtype=np.uint64)
+    O.translate(img, sp, v, threads=threads)
+    ts = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        O.translate(img, sp, v, threads=threads)
+        ts.append(time.perf_counter() - t0)
+    return {"value": len(v) / statistics.median(ts), "unit": "translations/s", "cores": threads, "kind": "port",
+            "sample": f"the step's {len(v)} translations ({note})", "cpu": cpu_model()}
 
 
 def cpu_baseline(wl, args):

@@ -8,6 +8,6 @@ run c1 --workload c1 --steps 10 --warmup 3
 run c1tdp --workload c1 --c1-mode tdp --steps 10 --warmup 3 --no-cpu-baseline
 run c1_4l --workload c1 --c1-mode 4l --steps 10 --warmup 3
 run c2 --workload c2 --steps 10 --warmup 3
-run c4 --workload c4 --steps 10 --warmup 3 --no-cpu-baseline
-run c3 --workload c3 --steps 10 --warmup 3 --no-cpu-baseline
+run c4 --workload c4 --steps 10 --warmup 3
+run c3 --workload c3 --steps 10 --warmup 3
 run ref --impl reference --steps 3 --warmup 1
