@@ -172,10 +172,8 @@ def raise_for(status: int, value: int, aux: int, va: int, image_bytes: int, chun
 
 def translate_one(image, space: Space, va: int, *, out_pfn: bool = False) -> tuple[int, int, int]:
     """One walk/translation on the device: returns (status, value, aux).
-    One pv_walk_one launch, request by value, result in pinned memory
-    (percall.py)."""
-    from . import percall
-
+    One request to the per-call server (or one pv_walk_one launch), result
+    in pinned memory (percall.py)."""
     return percall.get().walk(image, space, va, out_pfn)
 
 

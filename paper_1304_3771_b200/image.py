@@ -74,6 +74,7 @@ class MemoryImage:
         self._maybe_nonzero = np.zeros(self.npages, dtype=np.bool_) if host is None else \
             np.ones(self.npages, dtype=np.bool_)
         self._dev = None          # torch.uint8 [nbytes]
+        self._dev_key = None      # (_dev, data_ptr, device index) (device_ptr)
         self._dev_dirty = None    # torch.uint8 [npages]
         self._dev_dirty_any = False
         self._pending = np.zeros(self.npages, dtype=np.bool_)  # device-written, not yet gathered
@@ -240,6 +241,18 @@ class MemoryImage:
             if self._host_dirty_any:
                 self.push()
             return self._dev
+
+    def device_ptr(self) -> tuple[int, int]:
+        """(data pointer, device index) of the HBM image, current with every
+        host write -- the per-call fast path of :meth:`device` (no lock when
+        the image is resident and no host write is pending)."""
+        d = self._dev
+        if d is None or self._host_dirty_any:
+            d = self.device()
+        k = self._dev_key
+        if k is None or k[0] is not d:
+            k = self._dev_key = (d, d.data_ptr(), d.device.index)
+        return k[1], k[2]
 
     def dirty_map(self):
         """Device page map that writing kernels set (call after device())."""

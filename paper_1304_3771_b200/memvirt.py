@@ -873,14 +873,23 @@ class ProcessTranslator:
         self.space = space
         self.cache = cache
         self.use_cache = use_cache
+        self._ds = None  # (shadow root, guest root, tdp root, mode, dp.Space) of the last device_space
 
     @property
     def device_space(self) -> dp.Space:
         space = self.space
-        if space.guest.mem_mode == "shadow":
-            return dp.Space(self._memv.host_mem.base, space.shadow_root.root_pfn, 0, N.ONE_STAGE)
-        return dp.Space(space.guest.mem.base, space.guest_root.root_pfn, space.guest.tdp_root.root_pfn,
-                        N.TWO_STAGE)
+        guest = space.guest
+        c = self._ds
+        # roots are frozen objects: the cached descriptor stands while the same ones are in place
+        if c is not None and c[0] is space.shadow_root and c[1] is space.guest_root and c[2] is guest.tdp_root \
+                and c[3] == guest.mem_mode:
+            return c[4]
+        if guest.mem_mode == "shadow":
+            ds = dp.Space(self._memv.host_mem.base, space.shadow_root.root_pfn, 0, N.ONE_STAGE)
+        else:
+            ds = dp.Space(guest.mem.base, space.guest_root.root_pfn, guest.tdp_root.root_pfn, N.TWO_STAGE)
+        self._ds = (space.shadow_root, space.guest_root, guest.tdp_root, guest.mem_mode, ds)
+        return ds
 
     @property
     def image(self) -> MemoryImage:

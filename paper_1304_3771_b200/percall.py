@@ -82,7 +82,12 @@ class PerCall:
     """Pinned request / result blocks and staging of one host thread."""
 
     def __init__(self):
+        global _raw
         lib = N.lib()
+        if _raw is None:
+            import torch
+
+            _raw = torch._C._cuda_getCurrentRawStream
         self.lib = lib
         self._blocks = []
 
@@ -104,6 +109,8 @@ class PerCall:
         self.op = N.PvSmallOp()
         self.op_ref = ctypes.byref(self.op)
         self.seq = 0
+        self._spaces = {}
+        self._op_space = None
 
     def __del__(self):
         lib = getattr(self, "lib", None)
@@ -121,25 +128,36 @@ class PerCall:
         if block.seq != seq:
             raise RuntimeError("per-call kernel did not publish its result")
 
+    def _space_ref(self, space):
+        """byref of a pv_space holding ``space`` (one struct per distinct space, reused)."""
+        ref = self._spaces.get(space)
+        if ref is None:
+            if len(self._spaces) > 4096:
+                self._spaces.clear()
+            st = N.PvSpace(space.s1_base, space.s1_root_pfn, space.s2_root_pfn, space.mode)
+            ref = self._spaces[space] = ctypes.byref(st)
+        return ref
+
     def walk(self, image, space, va: int, out_pfn: bool) -> tuple[int, int, int]:
-        """(status, value, aux) of one walk / translation (pv_walk_one)."""
-        dev = image.device()
-        sp = self.space
-        sp.s1_base, sp.s1_root_pfn, sp.s2_root_pfn, sp.mode = space.s1_base, space.s1_root_pfn, \
-            space.s2_root_pfn, space.mode
-        stream = _raw_stream(dev)
+        """(status, value, aux) of one walk / translation (pv_server_walk, or
+        pv_walk_one with PV_PERCALL_SERVER=0)."""
         if _SERVER:
             global _server_used
             _server_used = True
-            N.check(self.lib.pv_server_walk(dev.data_ptr(), image.nbytes, self.space_ref, va & 0xFFFFFFFFFFFFFFFF,
-                                            (N.OUT_PFN if out_pfn else 0) | _idle_flag(stream), self.one_ptr,
-                                            stream), "pv_server_walk")
-        else:
-            self.seq += 1
-            N.check(self.lib.pv_walk_one(dev.data_ptr(), image.nbytes, self.space_ref, va & 0xFFFFFFFFFFFFFFFF,
-                                         N.OUT_PFN if out_pfn else 0, self.one_ptr, self.seq, stream),
-                    "pv_walk_one")
-            self._wait(self.one, self.seq, stream)
+            dev_ptr, dev_index = image.device_ptr()
+            stream = _raw(dev_index)
+            rc = self.lib.pv_server_walk(dev_ptr, image.nbytes, self._space_ref(space), va & 0xFFFFFFFFFFFFFFFF,
+                                         (N.OUT_PFN if out_pfn else 0) | _idle_flag(stream), self.one_ptr, stream)
+            if rc:
+                N.check(rc, "pv_server_walk")
+            one = self.one
+            return one.status & 0xFFFFFFFF, one.value, one.aux
+        dev = image.device()
+        stream = _raw_stream(dev)
+        self.seq += 1
+        N.check(self.lib.pv_walk_one(dev.data_ptr(), image.nbytes, self._space_ref(space), va & 0xFFFFFFFFFFFFFFFF,
+                                     N.OUT_PFN if out_pfn else 0, self.one_ptr, self.seq, stream), "pv_walk_one")
+        self._wait(self.one, self.seq, stream)
         one = self.one
         return int(one.status) & 0xFFFFFFFF, int(one.value), int(one.aux)
 
@@ -149,11 +167,13 @@ class PerCall:
         (bytes [buf_off, avail)) and the image (pv_copy_small).  ``pre``:
         per-page byte hpas the caller resolved (None = walk on the device).
         Returns the pinned result block (valid until the next call)."""
-        dev = image.device()
+        dev_ptr, dev_index = image.device_ptr()
         op = self.op
-        sp = op.space
-        sp.s1_base, sp.s1_root_pfn, sp.s2_root_pfn, sp.mode = space.s1_base, space.s1_root_pfn, \
-            space.s2_root_pfn, space.mode
+        if self._op_space is not space:  # the pv_space inside the op, refilled when the space changes
+            sp = op.space
+            sp.s1_base, sp.s1_root_pfn, sp.s2_root_pfn, sp.mode = space.s1_base, space.s1_root_pfn, \
+                space.s2_root_pfn, space.mode
+            self._op_space = space
         op.gva = gva & 0xFFFFFFFFFFFFFFFF
         op.len = length
         op.direction = direction
@@ -163,18 +183,20 @@ class PerCall:
             for k, h in enumerate(pre):
                 if h is not None:
                     op.pre_hpa[k] = h + 1
-        stream = _raw_stream(dev)
+        stream = _raw(dev_index)
         # no device dirty marks: the caller writes the same bytes through to
         # the host mirror (write_through), so no page goes device-stale
         if _SERVER:
             global _server_used
             _server_used = True
-            N.check(self.lib.pv_server_copy_small(dev.data_ptr(), image.nbytes, self.op_ref, self.stage_ptr + buf_off,
-                                                  max(avail - buf_off, 0), self.small_ptr, None, _idle_flag(stream),
-                                                  stream), "pv_server_copy_small")
+            rc = self.lib.pv_server_copy_small(dev_ptr, image.nbytes, self.op_ref, self.stage_ptr + buf_off,
+                                               max(avail - buf_off, 0), self.small_ptr, None, _idle_flag(stream),
+                                               stream)
+            if rc:
+                N.check(rc, "pv_server_copy_small")
         else:
             self.seq += 1
-            N.check(self.lib.pv_copy_small(dev.data_ptr(), image.nbytes, self.op_ref, self.stage_ptr + buf_off,
+            N.check(self.lib.pv_copy_small(dev_ptr, image.nbytes, self.op_ref, self.stage_ptr + buf_off,
                                            max(avail - buf_off, 0), self.small_ptr, None, self.seq,
                                            stream), "pv_copy_small")
             self._wait(self.small, self.seq, stream)
