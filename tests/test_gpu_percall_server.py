@@ -33,6 +33,18 @@ def _walks(pc, img, sp, vas):
     return [pc.walk(img, sp, int(v), False) for v in vas]
 
 
+def _resident_after(call) -> bool:
+    """Whether the server is resident right after ``call`` (it leaves on its
+    own after 200 us idle: a GC pause between the two may outlast that, so
+    a few tries)."""
+    lib = N.lib()
+    for _ in range(5):
+        call()
+        if lib.pv_server_resident() == 1:
+            return True
+    return False
+
+
 @pytest.mark.parametrize("mode", ["shadow", "tdp"])
 def test_server_walks_equal_launches_and_oracle(cuda, mode):
     memv, space = W.build_c1(mode)[0::2]
@@ -45,7 +57,7 @@ def test_server_walks_equal_launches_and_oracle(cuda, mode):
                           rng.integers(0, 1 << 32, 500)]).astype(np.uint64)
     pc = percall.get()
     got = _walks(pc, img, sp, vas)
-    assert N.lib().pv_server_resident() == 1
+    assert _resident_after(lambda: pc.walk(img, sp, int(vas[0]), False))
     percall.park()
     assert N.lib().pv_server_resident() == 0
     percall._SERVER = False
@@ -72,16 +84,15 @@ def test_server_walks_equal_launches_and_oracle(cuda, mode):
 def test_server_exits_when_idle_and_device_sync_returns(cuda):
     memv, guest, space = W.build_c1("shadow")
     tr = memv.translator(space, use_cache=False)
-    tr.translate(W.C1_GVA + 5)
     lib = N.lib()
-    assert lib.pv_server_resident() == 1
+    assert _resident_after(lambda: tr.translate(W.C1_GVA + 5))
     t0 = time.perf_counter()
     torch.cuda.synchronize()  # waits for the server's idle exit, not forever
     assert time.perf_counter() - t0 < 0.5
     assert lib.pv_server_resident() == 0
     # and it comes back on the next call
     assert tr.translate(W.C1_GVA + 5) == tr.translate(W.C1_GVA + 5)
-    assert lib.pv_server_resident() == 1
+    assert _resident_after(lambda: tr.translate(W.C1_GVA + 5))
 
 
 def test_server_call_is_ordered_behind_the_callers_stream(cuda):
@@ -174,9 +185,8 @@ def test_server_threads(cuda):
 def test_batch_launch_parks_the_server(cuda):
     memv, guest, space = W.build_c1("shadow")
     tr = memv.translator(space, use_cache=False)
-    tr.translate(W.C1_GVA)
-    assert N.lib().pv_server_resident() == 1
     vas = W.c1_vas(100_000)
+    assert _resident_after(lambda: tr.translate(W.C1_GVA))
     hpa, st, aux = tr.translate_batch(vas)
     assert N.lib().pv_server_resident() == 0
     assert (st == 0).all()
