@@ -52,6 +52,9 @@ def parse():
     ap.add_argument("--gather", action="store_true", help="return every guest's translations to rank 0 after "
                     "timing (point-to-point over NCCL = NVLink peer copies) and report its time (default at N > 1)")
     ap.add_argument("--no-gather", action="store_true", help="skip the result return to rank 0 at N > 1")
+    ap.add_argument("--no-peer-return", action="store_true", help="C5 at N > 1: the walk writes its lane words "
+                    "into local memory instead of straight into rank 0's HBM (shard.PeerResultBuffer); the "
+                    "results then return by the separate gather (--gather)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true", help="skip the full-size parity check against the oracle "
                     "after the timed steps")
@@ -288,6 +291,7 @@ def run_ours(args, rank, world, local):
 
     from paper_1304_3771_b200 import _native as N
     from paper_1304_3771_b200 import dataplane as dp
+    from paper_1304_3771_b200 import shard
 
     torch.cuda.set_device(local)
     wl = Workload(args.workload, rank, world, args.scale, args.c1_mode)
@@ -308,10 +312,23 @@ def run_ours(args, rank, world, local):
         w_rec = torch.empty(w_cap * N.EXC_WORDS, dtype=torch.int64, device="cuda")
         w_cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
 
+    # C5 at N > 1: every rank's walk stores its lane words straight into rank 0's HBM (one buffer, rank-major
+    # sections) -- the result return fused into the walk over NVLink / NVSwitch peer memory
+    peer, peer_off, peer_note = None, 0, None
+    if form == "words" and wl.name == "c5" and world > 1 and _pg() and not args.no_peer_return:
+        counts = [None] * world
+        tdist.all_gather_object(counts, int(wl.n_vas))
+        peer_off = sum(counts[:rank])
+        try:
+            peer = shard.PeerResultBuffer(4 * sum(counts), rank, world)
+        except Exception as exc:  # noqa: BLE001 - no peer mapping: local output + the separate gather
+            peer_note = f"peer mapping unavailable ({type(exc).__name__}: {str(exc)[:100]})"
+    w_out = (peer.ptr + 4 * peer_off) if peer is not None else (w_words if form == "words" else None)
+
     def phase_translate():
         if form == "words":
             w_cnt.zero_()
-            dp.translate_words(img, wl.tplan, wl.vas, w_words, w_rec, w_cnt)
+            dp.translate_words(img, wl.tplan, wl.vas, w_out, w_rec, w_cnt)
         elif form == "packed":  # PV_OUT_PACKED: one u64 per lane, no status array
             dp.translate_lanes(img, wl.tplan, wl.vas, out=(wl.out[0], None, wl.out[2]), packed=True)
         else:
@@ -320,7 +337,7 @@ def run_ours(args, rank, world, local):
     def phase_translate_conc():  # the same walk sized to share every SM with the exec (PV_CONCURRENT)
         if form == "words":
             w_cnt.zero_()
-            dp.translate_words(img, wl.tplan, wl.vas, w_words, w_rec, w_cnt, concurrent=True)
+            dp.translate_words(img, wl.tplan, wl.vas, w_out, w_rec, w_cnt, concurrent=True)
         elif form == "packed":
             dp.translate_lanes(img, wl.tplan, wl.vas, out=(wl.out[0], None, wl.out[2]), packed=True, concurrent=True)
         else:
@@ -493,6 +510,26 @@ def run_ours(args, rank, world, local):
             step(evs[k])
         torch.cuda.synchronize()
         barrier()
+    peer_return = None
+    if peer is not None:
+        # this rank's words, read back from rank 0's memory: what the checks below decode; rank 0 checks that
+        # its buffer holds every rank's section as that rank computed it
+        peer.copy_out(w_words.data_ptr(), 4 * peer_off, 4 * wl.n_vas, stream.cuda_stream)
+        torch.cuda.synchronize()
+        mine = hashlib.sha256(w_words.cpu().numpy().tobytes()).hexdigest()
+        sections = [None] * world
+        tdist.all_gather_object(sections, (peer_off, int(wl.n_vas), mine))
+        verified = None
+        if rank == 0:
+            full = torch.empty(sum(n for _, n, _ in sections), dtype=torch.int32, device="cuda")
+            peer.copy_out(full.data_ptr(), 0, 4 * full.numel(), stream.cuda_stream)
+            host = full.cpu().numpy()
+            verified = all(hashlib.sha256(host[o:o + n].tobytes()).hexdigest() == d for o, n, d in sections)
+        peer_return = {"mode": "peer stores fused into the walk: each rank's walk writes its lane words "
+                               "straight into rank 0's HBM (CUDA IPC mapping, NVLink / NVSwitch)",
+                       "bytes": 4 * sum(n for _, n, _ in sections),
+                       "remote_bytes": 4 * sum(n for r, (_, n, _) in enumerate(sections) if r != 0),
+                       "in_timed_region": True, "verified": verified}
     same_split = None
     if split_out is not None:
         same_split = bool(torch.equal(split_out, w_words if form == "words" else wl.out[0]))
@@ -563,7 +600,7 @@ def run_ours(args, rank, world, local):
     parity = None
     if not args.no_parity:
         parity = verify_parity(wl, cpu_threads())
-    want_gather = (args.gather or (world > 1 and _pg())) and not args.no_gather
+    want_gather = (args.gather or (world > 1 and _pg() and peer is None)) and not args.no_gather
     gather = gather_results(wl, rank, world) if (want_gather and wl.name == "c5") else None
     K = args.steps
     trans_per_s = wl.total_vas * K / (tr_ms / 1e3) if world > 0 else 0.0
@@ -648,6 +685,7 @@ def run_ours(args, rank, world, local):
         "faulting_lanes": n_faults,
         "parity": parity,
         "gather_to_rank0": gather,
+        "results_to_rank0": peer_return if peer is not None else peer_note,
         "hbm_image": {"image_bytes": img.nbytes, "device_bytes": img.device_bytes,
                       "resident": "all" if not img.partial else
                       "host-private region + owned guests' slots (pv_image_create) + one shared hole"},
@@ -665,6 +703,8 @@ def run_ours(args, rank, world, local):
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline and wl.memv is not None:
         line["cpu_baseline"] = cpu_baseline(wl, args)
+    if peer is not None:
+        peer.close()
     return line
 
 

@@ -681,6 +681,24 @@ int pv_sm_split(uint32_t first_sms, void** stream_first, void** stream_rest,
  * into a pv_sm_split stream.  Returns the previous value. */
 uint32_t pv_set_sm_budget(uint32_t sms);
 
+/* ---- results straight into rank 0's HBM --------------------
+ * Rank 0 allocates the job's result buffer (pv_peer_alloc: device memory of
+ * the current device + a PV_PEER_HANDLE_BYTES IPC handle it sends to the other
+ * ranks); every other rank maps it (pv_peer_open: a device pointer into rank
+ * 0's memory, peer access over NVLink / NVSwitch enabled on first use) and
+ * passes a slice of it as the OUTPUT of its walk (pv_translate_words
+ * out_word), so each lane word is stored into rank 0's memory by the kernel
+ * that computes it: the result return is fused into the walk, no gather step
+ * and no collective.  pv_peer_close unmaps, pv_peer_free (rank 0) frees. */
+#define PV_PEER_HANDLE_BYTES 64
+int pv_peer_alloc(uint64_t bytes, void** dev_ptr, uint8_t* handle);
+int pv_peer_open(const uint8_t* handle, void** dev_ptr);
+int pv_peer_close(void* dev_ptr);
+int pv_peer_free(void* dev_ptr);
+/* Stream-ordered copy between any two device / pinned host pointers (peer
+ * mappings included). */
+int pv_memcpy(void* dst, const void* src, uint64_t bytes, void* stream);
+
 /* ---- measurement hook ------------------------------------------------------ */
 /* pv_timing(1) resets and starts recording a CUDA event pair around every
  * launch of the library's dominant kernels (on the stream they are launched

@@ -79,7 +79,8 @@ FIFO_WORDS = 2 * FIFO_MAX + 4  # pv_fifo
 EXPORTS = (
     "pv_abi_version", "pv_translate_chunk", "pv_status_name", "pv_translate", "pv_translate_words",
     "pv_fifo_replay", "pv_copy_plan", "pv_copy_plan_nodes", "pv_copy_stamp", "pv_copy_exec",
-    "pv_copy_fifo_replay", "pv_scatter_pages", "pv_gather_pages", "pv_stream_sync", "pv_stream_idle", "pv_upload", "pv_sm_split", "pv_set_sm_budget", "pv_index_encode",
+    "pv_copy_fifo_replay", "pv_scatter_pages", "pv_gather_pages", "pv_stream_sync", "pv_stream_idle", "pv_upload", "pv_sm_split", "pv_set_sm_budget", "pv_peer_alloc", "pv_peer_open", "pv_peer_close",
+    "pv_peer_free", "pv_memcpy", "pv_index_encode",
     "pv_fifo_scratch_bytes", "pv_copy_ordered_scratch_bytes", "pv_copy_ordered", "pv_result_encode",
     "pv_result_decode", "pv_timing", "pv_timing_ms", "pv_copy_shim_scratch_bytes", "pv_copy_shim",
     "pv_map_scratch_bytes", "pv_map_plan", "pv_map_commit",
@@ -128,6 +129,11 @@ _SIGNATURES = {
     "pv_upload": (ctypes.c_int, [_p, _p, _u64, _p]),
     "pv_sm_split": (ctypes.c_int, [_u32, _p, _p, _p, _p]),
     "pv_set_sm_budget": (_u32, [_u32]),
+    "pv_peer_alloc": (ctypes.c_int, [_u64, _p, _p]),
+    "pv_peer_open": (ctypes.c_int, [_p, _p]),
+    "pv_peer_close": (ctypes.c_int, [_p]),
+    "pv_peer_free": (ctypes.c_int, [_p]),
+    "pv_memcpy": (ctypes.c_int, [_p, _p, _u64, _p]),
     "pv_timing": (ctypes.c_int, [ctypes.c_int]),
     "pv_timing_ms": (ctypes.c_double, [ctypes.c_char_p, _p]),
     "pv_walk_one": (ctypes.c_int, [_p, _u64, _p, _u64, _u32, _p, _u64, _p]),

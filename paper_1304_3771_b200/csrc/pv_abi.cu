@@ -825,6 +825,40 @@ int pv_sm_split(uint32_t first_sms, void** stream_first, void** stream_rest, uin
   return PV_SUCCESS;
 }
 
+int pv_peer_alloc(uint64_t bytes, void** dev_ptr, uint8_t* handle) {
+  if (!dev_ptr || !handle || bytes == 0) return PV_EINVAL;
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e != cudaSuccess) return e == cudaErrorMemoryAllocation ? PV_ENOMEM : rc(e);
+  cudaIpcMemHandle_t h;
+  e = cudaIpcGetMemHandle(&h, p);
+  if (e != cudaSuccess) {
+    cudaFree(p);
+    return rc(e);
+  }
+  static_assert(sizeof(cudaIpcMemHandle_t) == PV_PEER_HANDLE_BYTES, "IPC handle size");
+  std::memcpy(handle, &h, sizeof(h));
+  *dev_ptr = p;
+  return PV_SUCCESS;
+}
+
+int pv_peer_open(const uint8_t* handle, void** dev_ptr) {
+  if (!handle || !dev_ptr) return PV_EINVAL;
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  return rc(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+}
+
+int pv_peer_close(void* dev_ptr) { return dev_ptr ? rc(cudaIpcCloseMemHandle(dev_ptr)) : PV_EINVAL; }
+
+int pv_peer_free(void* dev_ptr) { return dev_ptr ? rc(cudaFree(dev_ptr)) : PV_EINVAL; }
+
+int pv_memcpy(void* dst, const void* src, uint64_t bytes, void* stream) {
+  if (bytes == 0) return PV_SUCCESS;
+  if (!dst || !src) return PV_EINVAL;
+  return rc(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, (cudaStream_t)stream));
+}
+
 uint32_t pv_set_sm_budget(uint32_t sms) {
   const uint32_t old = t_sm_budget;
   t_sm_budget = sms;

@@ -524,7 +524,8 @@ def unpack_words(words, vas, exc: LaneExceptions | None = None, *, out_pfn: bool
 def translate_words(image, plan: TranslatePlan, vas, words, exc_rec, exc_count, lane_base: int = 0, *,
                     out_pfn: bool = False, concurrent: bool = False) -> None:
     """pv_translate_words over every lane of ``vas`` (int64 or int32 cuda
-    tensor) into ``words`` (int32 cuda tensor, one per lane); exception
+    tensor) into ``words`` (int32 cuda tensor, one per lane, or a raw device
+    address -- e.g. a slice of rank 0's shard.PeerResultBuffer); exception
     records go to ``exc_rec`` (int64 cuda tensor of N.EXC_WORDS words per
     record, may be empty) and are counted in ``exc_count`` (int64 cuda
     tensor, one element, not reset here), asynchronously on the current
@@ -543,7 +544,8 @@ def translate_words(image, plan: TranslatePlan, vas, words, exc_rec, exc_count, 
     idx = _plan_index(image, plan)
     cap = exc_rec.numel() // N.EXC_WORDS
     N.check(lib.pv_translate_words(dev_img.data_ptr(), image.nbytes, plan.spaces.data_ptr(), plan.segs.data_ptr(),
-                                   plan.n_segs, plan.n_chunks, vas.data_ptr(), flags, idx, words.data_ptr(),
+                                   plan.n_segs, plan.n_chunks, vas.data_ptr(), flags, idx,
+                                   words if isinstance(words, int) else words.data_ptr(),
                                    exc_rec.data_ptr() if cap else None, cap, exc_count.data_ptr(), lane_base,
                                    _stream().cuda_stream), "pv_translate_words")
 

@@ -144,3 +144,59 @@ class SharedHostBuffer:
             dist.barrier()
         if self.rank == 0 and self.path and os.path.exists(self.path):
             os.unlink(self.path)
+
+
+class PeerResultBuffer:
+    """The job's lane words in rank 0's HBM: rank 0
+    allocates ``nbytes`` with an IPC handle (pv_peer_alloc), every other rank
+    maps it (pv_peer_open: a device pointer into rank 0's memory over NVLink /
+    NVSwitch) and hands a slice of it to its walk as the output, so each word
+    is stored into rank 0's memory by the kernel that computes it -- the
+    result return is fused into the walk (no gather step, no collective).
+    ``ptr`` is this rank's device address of the buffer."""
+
+    def __init__(self, nbytes: int, rank: int, world: int):
+        import ctypes
+
+        import torch.distributed as dist
+
+        from . import _native as N
+
+        lib = N.lib()
+        self.rank, self.world, self.nbytes = rank, world, int(nbytes)
+        ptr = ctypes.c_void_p()
+        handle = (ctypes.c_uint8 * 64)()
+        box = [None]
+        if rank == 0:
+            N.check(lib.pv_peer_alloc(self.nbytes, ctypes.byref(ptr), handle), "pv_peer_alloc")
+            box[0] = bytes(handle)
+        if world > 1:
+            dist.broadcast_object_list(box, src=0)
+        if rank != 0:
+            h = (ctypes.c_uint8 * 64).from_buffer_copy(box[0])
+            N.check(lib.pv_peer_open(h, ctypes.byref(ptr)), "pv_peer_open")
+        self.ptr = int(ptr.value)
+
+    def copy_out(self, dst_ptr: int, offset: int, nbytes: int, stream: int) -> None:
+        """Stream-ordered copy of ``nbytes`` at byte ``offset`` of the buffer to ``dst_ptr``."""
+        from . import _native as N
+
+        N.check(N.lib().pv_memcpy(dst_ptr, self.ptr + offset, nbytes, stream), "pv_memcpy")
+
+    def close(self) -> None:
+        """Unmap (ranks > 0) after a barrier; rank 0 frees after every rank unmapped."""
+        import torch
+        import torch.distributed as dist
+
+        from . import _native as N
+
+        torch.cuda.synchronize()
+        if self.world > 1 and dist.is_initialized():
+            dist.barrier()
+        if self.rank != 0:
+            N.lib().pv_peer_close(self.ptr)
+        if self.world > 1 and dist.is_initialized():
+            dist.barrier()
+        if self.rank == 0:
+            N.lib().pv_peer_free(self.ptr)
+        self.ptr = 0

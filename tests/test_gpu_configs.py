@@ -136,6 +136,9 @@ def test_bench_two_ranks_one_device(cuda, tmp_path):
     line = json.loads(lines[0])
     assert line["n_gpus"] == 2 and line["value"] > 0 and line["faulting_lanes"] == 0
     assert line["gather_to_rank0"]["complete"] is True
+    # the walk of rank 1 stored its lane words straight into rank 0's buffer (peer mapping), in the timed step
+    r0 = line["results_to_rank0"]
+    assert isinstance(r0, dict) and r0["verified"] is True and r0["in_timed_region"] is True, r0
     assert line["config"]["sharding"] == "guest g -> rank g mod 2"
     assert line["parity"]["ok"] is True and single["parity"]["ok"] is True
     # every guest's results, returned to rank 0, bit-identical to the one-rank run
