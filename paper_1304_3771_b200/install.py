@@ -65,9 +65,41 @@ def _swappable(obj) -> bool:
     return isinstance(obj, type) or isinstance(obj, types.FunctionType)
 
 
-def install(devfsim=None):
+def warm() -> None:
+    """Bring the device path up before its first use: the CUDA context, the
+    library's kernels (lazily loaded on first launch), the per-call server
+    and the pinned per-call blocks -- about a second of one-time cost that
+    would otherwise land inside the first translate / copy_to_user a caller
+    times.  A no-op without a CUDA device."""
+    import numpy as np
+    import torch
+
+    if not torch.cuda.is_available():
+        return
+    from . import memvirt as mv
+
+    for mode in ("shadow", "tdp"):
+        memv = mv.MemoryVirtualizer()
+        guest = memv.add_guest(0, mode)
+        space = memv.create_process(guest)
+        memv.map_region(space, 0x2000_0000, 4)
+        for cached in (False, True):
+            tr = memv.translator(space, mv.TranslationCache()) if cached else memv.translator(space, use_cache=False)
+            tr.translate(0x2000_0010)  # per-call server
+            tr.translate_batch(np.arange(0x2000_0000, 0x2000_5000, 0x800, dtype=np.uint64))
+            data = bytes(3 * 4096)
+            mv.copy_user_buffer("to_guest", 0x2000_0800, len(data), data, translator=tr, host_mem=memv.host_mem)
+            back = bytearray(len(data))
+            mv.copy_user_buffer("from_guest", 0x2000_0800, len(back), back, translator=tr, host_mem=memv.host_mem)
+    torch.cuda.synchronize()
+
+
+def install(devfsim=None, *, warm_device: bool = True):
     """Swap this package into ``devfsim`` (a module or its import name;
-    default ``"devfsim"``).  Returns the ``devfsim`` package."""
+    default ``"devfsim"``).  Returns the ``devfsim`` package.
+    ``warm_device``: bring the device path up now (:func:`warm`), so the
+    reference's callers never pay the one-time CUDA start-up inside an
+    operation they time."""
     if devfsim is None or isinstance(devfsim, str):
         devfsim = importlib.import_module(devfsim or "devfsim")
     root = devfsim.__name__
@@ -115,6 +147,8 @@ def install(devfsim=None):
     _rebind(_package_modules(root), swap)
 
     _installed[root] = devfsim
+    if warm_device:
+        warm()
     return devfsim
 
 
