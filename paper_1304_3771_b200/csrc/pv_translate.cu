@@ -316,7 +316,19 @@ translate_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const 
       bool simple = true;
 #pragma unroll
       for (int j = 0; j < VPT; ++j) {
+#ifdef PV_PROBE_FAKE_CODES
+        // probe build only (wrong results): the code of a hashed (top, mid) computed in registers
+        // instead of the shared-memory table read -- the same spread of leaf-index gathers without the
+        // SMEM lookup and its bank conflicts (scripts/ab_smem_lookup.sh)
+        if (j == 0) {
+          fc[0] = codes1[(top_index(va[0]) << 9) | mid_index(va[0])];  // one real lookup per thread and chunk
+        } else {
+          const uint32_t h = (((top_index(va[j]) << 9) | mid_index(va[j])) * 2654435761u) >> 21;
+          fc[j] = (fc[0] & 0xFu) | (((fc[0] >> 4) + h % 1300u) << 4);
+        }
+#else
         fc[j] = codes1[(top_index(va[j]) << 9) | mid_index(va[j])];
+#endif
         const bool valid = lane0 + (uint64_t)j * TPB + threadIdx.x < seg_end;
         simple &= !valid || (fc[j] & 0xFu) == (1u | kCodeIndexed);
       }
