@@ -670,14 +670,8 @@ def translate_host_many(image, jobs, chunk: int = 1 << 23, *, packed: bool = Fal
     if not work:
         return outs
     compute = torch.cuda.current_stream()
-    h2d, d2h = torch.cuda.Stream(), torch.cuda.Stream()
-    plans = {}
-    bufs = []
-    for _ in range(2):
-        bufs.append((torch.empty(chunk, dtype=dtype, device="cuda"), torch.empty(chunk, dtype=torch.int64, device="cuda"),
-                     None if packed else torch.empty(chunk, dtype=torch.int32, device="cuda"),
-                     torch.zeros(chunk, dtype=torch.int64, device="cuda"),
-                     torch.cuda.Event(), torch.cuda.Event(), torch.cuda.Event()))
+    h2d, d2h, bufs = _pipe(dtype, chunk, False)
+    h2d.wait_stream(compute)  # the caller's earlier work first
     for i, (space, need_aux, src, value, status, aux, start, m) in enumerate(work):
         d_vas, d_val, d_st, d_aux, ev_in, ev_done, ev_out = bufs[i % 2]
         if i >= 2:
@@ -686,11 +680,9 @@ def translate_host_many(image, jobs, chunk: int = 1 << 23, *, packed: bool = Fal
             d_vas[:m].copy_(src[start:start + m], non_blocking=True)
             ev_in.record(h2d)
         compute.wait_event(ev_in)
-        if (space, m) not in plans:
-            plans[(space, m)] = TranslatePlan([space], [(0, m, 0)], image=image)
         if need_aux:
             d_aux[:m].zero_()
-        translate_lanes(image, plans[(space, m)], d_vas[:m],
+        translate_lanes(image, _host_plan(image, space, m), d_vas[:m],
                         out=(d_val[:m], None if packed else d_st[:m], d_aux[:m]), packed=packed)
         ev_done.record(compute)
         d2h.wait_event(ev_done)
@@ -704,6 +696,46 @@ def translate_host_many(image, jobs, chunk: int = 1 << 23, *, packed: bool = Fal
     d2h.synchronize()
     compute.synchronize()
     return outs
+
+
+_pipe_tls = threading.local()
+
+
+def _pipe(dtype, chunk: int, words: bool):
+    """The calling thread's side streams, device chunk buffers and events of
+    the host pipeline, reused across calls (every call drains them before it
+    returns)."""
+    import torch
+
+    cache = getattr(_pipe_tls, "cache", None)
+    if cache is None:
+        cache = _pipe_tls.cache = {}
+    key = (torch.cuda.current_device(), dtype, chunk, words)
+    st = cache.get(key)
+    if st is None:
+        if words:
+            bufs = [(torch.empty(chunk, dtype=dtype, device="cuda"), torch.empty(chunk, dtype=torch.int32, device="cuda"),
+                     torch.cuda.Event(), torch.cuda.Event(), torch.cuda.Event()) for _ in range(2)]
+        else:
+            bufs = [(torch.empty(chunk, dtype=dtype, device="cuda"), torch.empty(chunk, dtype=torch.int64, device="cuda"),
+                     torch.empty(chunk, dtype=torch.int32, device="cuda"), torch.zeros(chunk, dtype=torch.int64, device="cuda"),
+                     torch.cuda.Event(), torch.cuda.Event(), torch.cuda.Event()) for _ in range(2)]
+        st = cache[key] = (torch.cuda.Stream(), torch.cuda.Stream(), bufs)
+    return st
+
+
+def _host_plan(image, space: Space, m: int) -> "TranslatePlan":
+    """The one-segment TranslatePlan of ``m`` lanes through ``space``, kept on
+    the image across calls (descriptors are uploaded once)."""
+    cache = getattr(image, "_host_plans", None)
+    if cache is None:
+        cache = image._host_plans = {}
+    plan = cache.get((space, m))
+    if plan is None:
+        if len(cache) > 512:
+            cache.clear()
+        plan = cache[(space, m)] = TranslatePlan([space], [(0, m, 0)], image=image)
+    return plan
 
 
 def _translate_host_words(image, jobs, chunk: int, out, exc_cap: int):
@@ -741,10 +773,8 @@ def _translate_host_words(image, jobs, chunk: int, out, exc_cap: int):
     dev_exc = torch.empty(max(cap, 1) * N.EXC_WORDS, dtype=torch.int64, device="cuda")
     dev_cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
     if work:
-        h2d, d2h = torch.cuda.Stream(), torch.cuda.Stream()
-        plans = {}
-        bufs = [(torch.empty(chunk, dtype=dtype, device="cuda"), torch.empty(chunk, dtype=torch.int32, device="cuda"),
-                 torch.cuda.Event(), torch.cuda.Event(), torch.cuda.Event()) for _ in range(2)]
+        h2d, d2h, bufs = _pipe(dtype, chunk, True)
+        h2d.wait_stream(compute)  # the caller's earlier work (and the counter reset above) first
         for i, (space, src, w, l0, start, m) in enumerate(work):
             d_vas, d_w, ev_in, ev_done, ev_out = bufs[i % 2]
             if i >= 2:
@@ -753,10 +783,8 @@ def _translate_host_words(image, jobs, chunk: int, out, exc_cap: int):
                 d_vas[:m].copy_(src[start:start + m], non_blocking=True)
                 ev_in.record(h2d)
             compute.wait_event(ev_in)
-            if (space, m) not in plans:
-                plans[(space, m)] = TranslatePlan([space], [(0, m, 0)], image=image)
-            translate_words(image, plans[(space, m)], d_vas[:m], d_w[:m], dev_exc[:cap * N.EXC_WORDS], dev_cnt,
-                            l0 + start)
+            translate_words(image, _host_plan(image, space, m), d_vas[:m], d_w[:m], dev_exc[:cap * N.EXC_WORDS],
+                            dev_cnt, l0 + start)
             ev_done.record(compute)
             d2h.wait_event(ev_done)
             with torch.cuda.stream(d2h):
