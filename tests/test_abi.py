@@ -46,6 +46,24 @@ def test_argument_validation_needs_no_gpu():
                             ctypes.c_void_p(8), 0, None, ctypes.c_void_p(8), ctypes.c_void_p(8), None,
                             None) == N.EINVAL
     assert lib.pv_index_encode(None, 4096, None, None, 0, 1, None, None, None) == N.EINVAL
+    # 4-byte lane words: frames must fit 28 bits (images below 2^40 bytes); PV_OUT_PACKED is not a words flag
+    p8 = ctypes.c_void_p(8)
+    cnt = ctypes.c_void_p(8)
+    assert lib.pv_translate_words(None, 4096, p8, p8, 1, 1, p8, 0, None, p8, None, 0, cnt, 0, None) == N.EINVAL
+    assert lib.pv_translate_words(p8, 1 << 40, p8, p8, 1, 1, p8, 0, None, p8, None, 0, cnt, 0, None) == N.EINVAL
+    assert lib.pv_translate_words(p8, 4096, p8, p8, 1, 1, p8, N.OUT_PACKED, None, p8, None, 0, cnt, 0,
+                                  None) == N.EINVAL
+    assert lib.pv_translate_words(p8, 4096, p8, p8, 1, 1, p8, 0, None, p8, None, 5, cnt, 0, None) == N.EINVAL
+    # per-call server / uploads / peer buffers: argument errors come back before any CUDA call
+    assert lib.pv_server_walk(None, 4096, p8, 0, 0, p8, None) == N.EINVAL
+    assert lib.pv_server_walk(p8, 4096, p8, 0, 0x4, p8, None) == N.EINVAL  # unknown flag
+    assert lib.pv_server_copy_small(p8, 4096, None, p8, 0, p8, None, 0, None) == N.EINVAL
+    assert lib.pv_upload(ctypes.c_void_p(16), ctypes.c_void_p(17), 64, None) == N.EINVAL  # misaligned source
+    assert lib.pv_upload(None, None, 0, None) == N.SUCCESS  # nothing to move
+    assert lib.pv_peer_open(None, None) == N.EINVAL
+    assert lib.pv_peer_alloc(0, None, None) == N.EINVAL
+    assert lib.pv_sm_split(0, None, None, None, None) == N.EINVAL
+    assert lib.pv_memcpy(None, None, 0, None) == N.SUCCESS
 
 
 def test_compute_entry_points_fail_loudly_without_gpu():
