@@ -20,7 +20,6 @@ def main():
     backing = wl.memv.host_mem.backing
     full = backing.host_for_read()
     span = wl.memv.HOST_PRIVATE_BYTES
-    fresh = np.empty(full.nbytes, np.uint8) if False else None
     copy_priv = full[:span].copy()
     threads = B.cpu_threads()
     print("threads", threads, "cpus", os.cpu_count(), "affinity", len(os.sched_getaffinity(0)))

@@ -5,7 +5,6 @@ import io
 import os
 import pstats
 import random
-import struct
 import sys
 import time
 
