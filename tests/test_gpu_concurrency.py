@@ -219,3 +219,40 @@ def test_four_threads_large_overlapping_batches_match_one_thread(cuda):
     for p in range(4):
         assert got[p] == seq[p], p
     assert _state(memv, recs) == seq_state
+
+
+@pytest.mark.parametrize("has_mode", ["software", "hardware"])
+def test_per_call_threads_match_sequential_reference(cuda, has_mode):
+    """Three threads making the reference's one-call-per-op calls at once
+    (each through the per-call server, each on its own stream), while a
+    fourth runs batches on another process: every per-call outcome, the
+    caches and the final memory equal the reference run one after another."""
+    import torch
+
+    traps = (5, 9, 30) if has_mode == "hardware" else ()
+    scripts = [_script(300 + p, rounds=2, n_ops=24) for p in range(4)]
+    ref, mine = _impl("ref"), _impl("mine")
+
+    memv, recs = _world(ref, 4, traps)
+    cls = ref.be.SoftwareHasAccess if has_mode == "software" else ref.be.HardwareHasAccess
+    expect = [_run_ref(ref, memv, r, cls(r, memv), sc) for r, sc in zip(recs, scripts)]
+    expect_state = _state(memv, recs)
+
+    memv, recs = _world(mine, 4, traps)
+    cls = mine.be.SoftwareHasAccess if has_mode == "software" else mine.be.HardwareHasAccess
+    accs = [cls(r, memv) for r in recs]
+    streams = [torch.cuda.Stream() for _ in recs]
+
+    def per_call(i):
+        with torch.cuda.stream(streams[i]):
+            return _run_ref(mine, memv, recs[i], accs[i], scripts[i])
+
+    fns = [lambda i=i: per_call(i) for i in range(3)]
+    fns.append(lambda: _run_mine(memv, recs[3], accs[3], scripts[3], streams[3]))
+    got = _threads(fns)
+    torch.cuda.synchronize()
+    for p in range(4):
+        assert len(expect[p]) == len(got[p])
+        for j, (a, b) in enumerate(zip(expect[p], got[p])):
+            assert a == b, (p, j, str(a)[:200], str(b)[:200])
+    assert _state(memv, recs) == expect_state
