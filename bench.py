@@ -310,9 +310,7 @@ def run_ours(args, rank, world, local):
     form = args.walk_form
     if form == "words":  # one 4-byte word per lane + exception records (pv_translate_words)
         w_words = torch.empty(wl.n_vas, dtype=torch.int32, device="cuda")
-        w_cap = min(wl.n_vas, 1 << 20)
-        w_rec = torch.empty(w_cap * N.EXC_WORDS, dtype=torch.int64, device="cuda")
-        w_cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+        w_exc = dp.ExcList(min(wl.n_vas, 1 << 20))
 
     # C5 at N > 1: every rank's walk stores its lane words straight into rank 0's HBM (one buffer, rank-major
     # sections) -- the result return fused into the walk over NVLink / NVSwitch peer memory
@@ -329,8 +327,8 @@ def run_ours(args, rank, world, local):
 
     def phase_translate():
         if form == "words":
-            w_cnt.zero_()
-            dp.translate_words(img, wl.tplan, wl.vas, w_out, w_rec, w_cnt)
+            w_exc.reset()
+            dp.translate_words(img, wl.tplan, wl.vas, w_out, w_exc)
         elif form == "packed":  # PV_OUT_PACKED: one u64 per lane, no status array
             dp.translate_lanes(img, wl.tplan, wl.vas, out=(wl.out[0], None, wl.out[2]), packed=True)
         else:
@@ -338,8 +336,8 @@ def run_ours(args, rank, world, local):
 
     def phase_translate_conc():  # the same walk sized to share every SM with the exec (PV_CONCURRENT)
         if form == "words":
-            w_cnt.zero_()
-            dp.translate_words(img, wl.tplan, wl.vas, w_out, w_rec, w_cnt, concurrent=True)
+            w_exc.reset()
+            dp.translate_words(img, wl.tplan, wl.vas, w_out, w_exc, concurrent=True)
         elif form == "packed":
             dp.translate_lanes(img, wl.tplan, wl.vas, out=(wl.out[0], None, wl.out[2]), packed=True, concurrent=True)
         else:
@@ -544,9 +542,8 @@ def run_ours(args, rank, world, local):
     n_exc = None
     if form != "unpacked":  # decode the timed step's lane words for the checks below
         if form == "words":
-            n_exc = int(w_cnt.item())
-            assert n_exc <= w_cap, "more exception lanes than the bench's record list holds"
-            exc = dp.LaneExceptions.from_records(w_rec[:n_exc * N.EXC_WORDS].cpu().numpy())
+            exc, n_exc, overflow = w_exc.read()
+            assert not overflow, "more exception lanes than the bench's record list holds"
             v, st_, _ = dp.unpack_words(w_words.cpu().numpy(), wl.vas.cpu().numpy(), exc)
         else:
             v, st_ = dp.unpack_lanes(wl.out[0].cpu().numpy(), wl.out[2].cpu().numpy())
@@ -1169,8 +1166,13 @@ def run_c4(args, rank, world, local):
                                      saved.data_ptr(), s), "scatter")
         img.note_device_write()
 
+    # the walk writes 4-byte lane words; traps (their node pfns) go to the exception records
+    w_words = torch.empty(len(vas_h), dtype=torch.int32, device="cuda")
+    w_exc = dp.ExcList(len(vas_h))
+
     def phase_translate():
-        dp.translate_lanes(img, tplan, vas, out=out)
+        w_exc.reset()
+        dp.translate_words(img, tplan, vas, w_words, w_exc)
 
     def phase_copy():
         cplan.shim_written.zero_()
@@ -1232,7 +1234,17 @@ def run_c4(args, rank, world, local):
     cp_ms = sum(e[1].elapsed_time(e[2]) for e in evs)
     tr_ms, cp_ms = shard.max_over_ranks([tr_ms, cp_ms], world, device="cuda")
     K = args.steps
-    st = out[1].cpu().numpy().view(np.uint32)
+    exc, n_exc, overflow = w_exc.read()
+    assert not overflow
+    wv, st, wa = dp.unpack_words(w_words.cpu().numpy(), vas_h, exc)
+    # the same lanes in the (value, status, aux) form: the words decode to exactly them
+    restore()
+    dp.translate_lanes(img, tplan, vas, out=out)
+    torch.cuda.synchronize()
+    words_equal = bool(np.array_equal(st, out[1].cpu().numpy().view(np.uint32))
+                       and np.array_equal(wv, out[0].cpu().numpy().view(np.uint64))
+                       and np.array_equal(wa, out[2].cpu().numpy().view(np.uint64)))
+    assert words_equal, "C4 lane words differ from the (value, status, aux) form"
     kinds = {hex(k): int(c) for k, c in zip(*np.unique(st & 0xFF0, return_counts=True))}
     res = cplan.results.cpu().numpy().view(np.uint64)
     n_fixed = [int(f.item()) for f in fixed]
@@ -1240,7 +1252,7 @@ def run_c4(args, rank, world, local):
     assert 0x10 in [int(k, 16) for k in kinds] and 0x40 in [int(k, 16) for k in kinds]
     total_lanes = 1 << 20
     peak, peak_kind = peaks()
-    walk_ach = 16 * len(vas_h) * K / (tr_ms / 1e3) / 1e9
+    walk_ach = 8 * len(vas_h) * K / (tr_ms / 1e3) / 1e9
     copied = int(res[:, 0].sum())
     return {
         "metric": METRIC, "value": total_lanes * K / (tr_ms / 1e3), "unit": "translations/s", "n_gpus": world,
@@ -1256,7 +1268,10 @@ def run_c4(args, rank, world, local):
         "translate_ms_per_step": tr_ms / K,
         "roofline": {"bound": "hbm", "kernel": "translate_kernel", "achieved": walk_ach, "peak": peak,
                      "unit": "GB/s", "frac": walk_ach / peak, "peak_source": peak_kind,
-                     "note": "16 B/translation; 1 M lanes fit L2, so this line is latency-bound, not HBM-bound"},
+                     "note": "8 B/translation (u32 VA in, one u32 lane word out; traps add a 32-byte exception "
+                             "record); 1 M lanes fit L2, so this line is latency-bound, not HBM-bound"},
+        "walk_form": "pv_translate_words (one u32 per lane + exception records)",
+        "exception_records": n_exc, "words_equal_unpacked": words_equal,
         "launch": launch_mode,
         "gpu_launches": 7 * K, "gpu_launches_note": "translate, plan, shim eval + cooperative resolve, stamp, exec per step (+ leaf-index re-encode)",
         "clocks": clk, "build_s": build_s,

@@ -245,12 +245,16 @@ int pv_translate(const uint8_t* image, uint64_t image_bytes,
  *     | PV_W32_VA  the exception's value is the lane's own va (page faults
  *                  and out-of-range nodes of a one-stage walk), or
  *     otherwise    the value (and the TDP-stage trap gpa, aux) is in an
- *                  exception record: exc[k] for some k < *exc_count, with
- *                  exc[k].lane = lane_base + lane.
- * *exc_count (device) is advanced atomically and never reset here (zero it
- * before the first call of a series that shares it); records past exc_cap
- * are counted but not written -- the caller re-runs with a larger list.
- * Record order is unspecified (one record per lane). */
+ *                  exception record with .lane = lane_base + lane.
+ * The records are striped over PV_EXC_STRIPES counters so a fault-heavy
+ * batch does not serialise on one atomic: exc_count (device) holds
+ * PV_EXC_STRIPES counters, stripe s owns records exc[s * per .. (s+1) * per)
+ * with per = exc_cap / PV_EXC_STRIPES, and its counter is advanced by one
+ * atomic per warp; counters are never reset here (zero them before the first
+ * call of a series that shares them); a stripe's records past `per` are
+ * counted but not written -- the caller re-runs with a larger list.  Record
+ * order within a stripe is unspecified (one record per lane). */
+#define PV_EXC_STRIPES 32
 #define PV_W32_ERR 0x80000000u
 #define PV_W32_VA 0x40000000u
 #define PV_W32_COMPACT_MASK 0x1FFFFFu

@@ -52,6 +52,7 @@ W32_ERR = 0x80000000  # pv.h pv_translate_words lane words
 W32_VA = 0x40000000
 W32_COMPACT_MASK = 0x1FFFFF
 EXC_WORDS = 4         # sizeof(pv_exc) / 8
+EXC_STRIPES = 32      # pv.h PV_EXC_STRIPES
 HAS_TWO_STAGE = 0x80000000
 HAS_4L = 0x40000000
 

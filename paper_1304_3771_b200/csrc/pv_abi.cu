@@ -279,7 +279,7 @@ int pv_translate_words(const uint8_t* image, uint64_t image_bytes, const pv_spac
   if (image_bytes >= (1ull << 40)) return PV_EINVAL;
   if (flags & ~(uint32_t)(PV_VA32 | PV_OUT_PFN | PV_CONCURRENT | PV_HAS_TWO_STAGE | PV_HAS_4L)) return PV_EINVAL;
   if (index != nullptr && (!index->slot_of || !index->leaf_codes || !index->slot_page)) return PV_EINVAL;
-  const ExcSink sink{exc, exc_cap, exc_count, lane_base};
+  const ExcSink sink{exc, exc_cap / PV_EXC_STRIPES, exc_count, lane_base};
   return rc(launch_translate(image, image_bytes, spaces, segs, n_segs, n_chunks, vas,
                              flags & (PV_VA32 | PV_OUT_PFN | PV_CONCURRENT | PV_HAS_4L), flags & PV_HAS_TWO_STAGE,
                              index, reinterpret_cast<uint64_t*>(out_word), nullptr, nullptr, &sink,

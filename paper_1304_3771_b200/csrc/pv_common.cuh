@@ -225,28 +225,54 @@ constexpr uint32_t kOutWord = 2;    // pv_translate_words: u32 lane words + exce
 // Exception list of a kOutWord launch (pv.h pv_translate_words).
 struct ExcSink {
   pv_exc* rec;
-  uint64_t cap;
-  unsigned long long* count;
+  uint64_t per;               // records per stripe (exc_cap / PV_EXC_STRIPES)
+  unsigned long long* count;  // PV_EXC_STRIPES counters
   uint64_t lane_base;
 };
 
 // 4-byte lane word (pv.h pv_translate_words) of lane i; appends the lane's
 // exception record when the word alone cannot carry its value.  v: the frame
 // number of a lane that translated, else the exception's value.
-__device__ __forceinline__ uint32_t word_lane(uint32_t st, uint64_t v, uint64_t va, uint64_t aux, uint64_t i,
-                                              const ExcSink& x) {
+// The 4-byte word of a lane (v: its frame number, or its exception's value)
+// and whether the lane needs an exception record (its value is not its own
+// va, or it carries a TDP-stage gpa: `has_aux`).
+__device__ __forceinline__ uint32_t word_code(uint32_t st, uint64_t v, uint64_t va, bool has_aux, bool* need) {
+  *need = false;
   if (st == PV_ST_OK) return (uint32_t)v;
   const uint32_t compact = (st & 0xFFFu) | (((st >> 16) & 0x1FFu) << 12);
-  if (v == va && PV_ST_KIND(st) != PV_ST_TRAP2) return PV_W32_ERR | PV_W32_VA | compact;
-  const unsigned long long k = atomicAdd(x.count, 1ull);
-  if (k < x.cap) {
+  if (v == va && !has_aux) return PV_W32_ERR | PV_W32_VA | compact;
+  *need = true;
+  return PV_W32_ERR | compact;
+}
+
+// Every thread of the warp that reaches the call takes part (the slots of a
+// warp's records are reserved with one atomic: a fault-heavy batch -- C4: a
+// trap on one lane in ten -- would otherwise serialise on the counter).
+__device__ __forceinline__ uint32_t word_lane(uint32_t st, uint64_t v, uint64_t va, uint64_t aux, uint64_t i,
+                                              const ExcSink& x) {
+  const uint32_t compact = (st & 0xFFFu) | (((st >> 16) & 0x1FFu) << 12);
+  const bool ok = st == PV_ST_OK;
+  const bool va_valued = !ok && v == va && PV_ST_KIND(st) != PV_ST_TRAP2;
+  const bool need = !ok && !va_valued;
+  const unsigned mask = __activemask();
+  const unsigned b = __ballot_sync(mask, need);
+  if (ok) return (uint32_t)v;
+  if (va_valued) return PV_W32_ERR | PV_W32_VA | compact;
+  const int me = (int)(threadIdx.x & 31u);
+  const int leader = __ffs(b) - 1;
+  const uint32_t stripe = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) % PV_EXC_STRIPES;
+  unsigned long long base = 0;
+  if (me == leader) base = atomicAdd(x.count + stripe, (unsigned long long)__popc(b));
+  base = __shfl_sync(b, base, leader);
+  const unsigned long long k = base + (unsigned long long)__popc(b & ((1u << me) - 1u));
+  if (k < x.per) {
     pv_exc r;
     r.lane = x.lane_base + i;
     r.value = v;
     r.aux = aux;
     r.status = st;
     r.reserved = 0;
-    x.rec[k] = r;
+    x.rec[stripe * x.per + k] = r;
   }
   return PV_W32_ERR | compact;
 }

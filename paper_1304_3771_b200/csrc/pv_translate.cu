@@ -427,17 +427,58 @@ translate_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const 
         }
       }
     }
+    if (mode == kOutWord) {
+      // 4-byte words: the thread's lanes that need an exception record are
+      // counted first, so the warp reserves all its records of this chunk
+      // with ONE atomic (a per-lane or per-j atomic would put an L2 round
+      // trip per lane group on the critical path of a fault-heavy walk)
+      uint32_t word[VPT];
+      unsigned bal[VPT];
+      const unsigned mask = __activemask();
+      uint32_t total = 0;
+#pragma unroll
+      for (int j = 0; j < VPT; ++j) {
+        const bool valid = lane0 + (uint64_t)j * TPB + threadIdx.x < seg_end;
+        bool need = false;
+        word[j] = word_code(st[j], val[j], (uint64_t)va[j], kTwo && PV_ST_KIND(st[j]) == PV_ST_TRAP2, &need);
+        bal[j] = __ballot_sync(mask, valid && need);
+        total += __popc(bal[j]);
+      }
+      if (total) {
+        const int me = (int)(threadIdx.x & 31u), leader = __ffs(mask) - 1;
+        const uint32_t stripe = (blockIdx.x * (TPB >> 5) + (threadIdx.x >> 5)) % PV_EXC_STRIPES;
+        unsigned long long base = 0;
+        if (me == leader) base = atomicAdd(sink.count + stripe, (unsigned long long)total);
+        base = __shfl_sync(mask, base, leader);
+#pragma unroll
+        for (int j = 0; j < VPT; ++j) {
+          if (bal[j] >> me & 1u) {
+            const unsigned long long k = base + __popc(bal[j] & ((1u << me) - 1u));
+            if (k < sink.per) {
+              pv_exc r;
+              r.lane = sink.lane_base + lane0 + (uint64_t)j * TPB + threadIdx.x;
+              r.value = val[j];
+              r.aux = kTwo ? aux[j] : 0;
+              r.status = st[j];
+              r.reserved = 0;
+              sink.rec[stripe * sink.per + k] = r;
+            }
+          }
+          base += __popc(bal[j]);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < VPT; ++j) {
+        const uint64_t i = lane0 + (uint64_t)j * TPB + threadIdx.x;
+        if (i < seg_end) st_u32_stream(reinterpret_cast<uint32_t*>(out_value) + i, word[j], pol_stream);
+      }
+      continue;
+    }
 #pragma unroll
     for (int j = 0; j < VPT; ++j) {
       const uint64_t i = lane0 + (uint64_t)j * TPB + threadIdx.x;
       if (i >= seg_end) continue;
       uint64_t v = val[j];
-      if (mode == kOutWord) {
-        st_u32_stream(reinterpret_cast<uint32_t*>(out_value) + i,
-                      word_lane(st[j], v, (uint64_t)va[j], kTwo ? aux[j] : 0, i, sink),
-                      pol_stream);
-        continue;
-      }
       if (!kPfn && st[j] == PV_ST_OK) v = (v << kPageShift) | (va[j] & kPageMask);
       if (mode == kOutPacked) {
         bool spill;

@@ -491,6 +491,45 @@ class LaneExceptions:
         return cls(r[:, 0].astype(np.int64), r[:, 1].copy(), r[:, 2].copy(), (r[:, 3] & np.uint64(0xFFFFFFFF)).astype(np.uint32))
 
 
+class ExcList:
+    """The device exception list of pv_translate_words (pv.h): PV_EXC_STRIPES
+    counters and room for ``cap`` records (``cap / PV_EXC_STRIPES`` per
+    stripe).  ``reset()`` zeroes the counters on the current stream;
+    ``read()`` returns ``(LaneExceptions, total, overflow)`` -- overflow: some
+    stripe counted more records than it holds (re-run with ``needed()``)."""
+
+    def __init__(self, cap: int):
+        import torch
+
+        self.per = -(-int(cap) // N.EXC_STRIPES) if cap > 0 else 0
+        self.rec = torch.empty(max(self.per * N.EXC_STRIPES, 1) * N.EXC_WORDS, dtype=torch.int64, device="cuda")
+        self.cnt = torch.zeros(N.EXC_STRIPES, dtype=torch.int64, device="cuda")
+        self._last = np.zeros(N.EXC_STRIPES, np.int64)
+
+    @property
+    def cap(self) -> int:
+        return self.per * N.EXC_STRIPES
+
+    def reset(self) -> None:
+        """Zero the counters (stream-ordered; graph-capturable)."""
+        self.cnt.zero_()
+
+    def needed(self) -> int:
+        """A capacity that holds every stripe's records of the last :meth:`read`."""
+        return int(self._last.max()) * N.EXC_STRIPES
+
+    def read(self):
+        counts = self._last = self.cnt.cpu().numpy()
+        total = int(counts.sum())
+        overflow = bool((counts > self.per).any())
+        take = np.minimum(counts, self.per)
+        if total == 0:
+            return LaneExceptions(), 0, overflow
+        recs = self.rec[: self.per * N.EXC_STRIPES * N.EXC_WORDS].view(N.EXC_STRIPES, self.per, N.EXC_WORDS)
+        parts = [recs[st, : int(t)].cpu().numpy() for st, t in enumerate(take) if t]
+        return LaneExceptions.from_records(np.concatenate(parts)), total, overflow
+
+
 def unpack_words(words, vas, exc: LaneExceptions | None = None, *, out_pfn: bool = False):
     """(value uint64, status uint32, aux uint64) of pv_translate_words lane
     words (pv.h): a word without PV_W32_ERR is the lane's frame number (value
@@ -521,15 +560,13 @@ def unpack_words(words, vas, exc: LaneExceptions | None = None, *, out_pfn: bool
     return value, status, aux
 
 
-def translate_words(image, plan: TranslatePlan, vas, words, exc_rec, exc_count, lane_base: int = 0, *,
+def translate_words(image, plan: TranslatePlan, vas, words, exc: ExcList, lane_base: int = 0, *,
                     out_pfn: bool = False, concurrent: bool = False) -> None:
     """pv_translate_words over every lane of ``vas`` (int64 or int32 cuda
     tensor) into ``words`` (int32 cuda tensor, one per lane, or a raw device
     address -- e.g. a slice of rank 0's shard.PeerResultBuffer); exception
-    records go to ``exc_rec`` (int64 cuda tensor of N.EXC_WORDS words per
-    record, may be empty) and are counted in ``exc_count`` (int64 cuda
-    tensor, one element, not reset here), asynchronously on the current
-    stream."""
+    records go to ``exc`` (an :class:`ExcList`, not reset here),
+    asynchronously on the current stream."""
     percall.park()  # the per-call server must not hold a CTA slot this grid counts on
     import torch
 
@@ -542,11 +579,11 @@ def translate_words(image, plan: TranslatePlan, vas, words, exc_rec, exc_count, 
     if plan.four:
         flags |= N.HAS_4L
     idx = _plan_index(image, plan)
-    cap = exc_rec.numel() // N.EXC_WORDS
+    cap = exc.cap
     N.check(lib.pv_translate_words(dev_img.data_ptr(), image.nbytes, plan.spaces.data_ptr(), plan.segs.data_ptr(),
                                    plan.n_segs, plan.n_chunks, vas.data_ptr(), flags, idx,
                                    words if isinstance(words, int) else words.data_ptr(),
-                                   exc_rec.data_ptr() if cap else None, cap, exc_count.data_ptr(), lane_base,
+                                   exc.rec.data_ptr() if cap else None, cap, exc.cnt.data_ptr(), lane_base,
                                    _stream().cuda_stream), "pv_translate_words")
 
 
@@ -770,8 +807,7 @@ def _translate_host_words(image, jobs, chunk: int, out, exc_cap: int):
     total = lane0
     cap = min(total, exc_cap)
     compute = torch.cuda.current_stream()
-    dev_exc = torch.empty(max(cap, 1) * N.EXC_WORDS, dtype=torch.int64, device="cuda")
-    dev_cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    exc_list = ExcList(cap)
     if work:
         h2d, d2h, bufs = _pipe(dtype, chunk, True)
         h2d.wait_stream(compute)  # the caller's earlier work (and the counter reset above) first
@@ -783,23 +819,20 @@ def _translate_host_words(image, jobs, chunk: int, out, exc_cap: int):
                 d_vas[:m].copy_(src[start:start + m], non_blocking=True)
                 ev_in.record(h2d)
             compute.wait_event(ev_in)
-            translate_words(image, _host_plan(image, space, m), d_vas[:m], d_w[:m], dev_exc[:cap * N.EXC_WORDS],
-                            dev_cnt, l0 + start)
+            translate_words(image, _host_plan(image, space, m), d_vas[:m], d_w[:m], exc_list, l0 + start)
             ev_done.record(compute)
             d2h.wait_event(ev_done)
             with torch.cuda.stream(d2h):
                 w[start:start + m].copy_(d_w[:m], non_blocking=True)
                 ev_out.record(d2h)
         d2h.synchronize()
-    n_exc = int(dev_cnt.item())
-    if n_exc > cap:  # more exception lanes than the list holds: once more with room for all
-        return _translate_host_words(image, jobs, chunk, out, n_exc)
+    allx, n_exc, overflow = exc_list.read()
+    if overflow:  # a stripe ran out of room: once more with room for every stripe's records
+        return _translate_host_words(image, jobs, chunk, out, exc_list.needed())
     last_host_io["h2d"] = sum(w[1].element_size() * w[5] for w in work)
-    last_host_io["d2h"] = 4 * total + 8 + n_exc * 8 * N.EXC_WORDS
+    last_host_io["d2h"] = 4 * total + 8 * N.EXC_STRIPES + n_exc * 8 * N.EXC_WORDS
     excs = [LaneExceptions() for _ in outs]
     if n_exc:
-        recs = dev_exc[:n_exc * N.EXC_WORDS].cpu().numpy()
-        allx = LaneExceptions.from_records(recs)
         job = np.searchsorted(np.asarray(base, np.int64), allx.lane, side="right") - 1
         for k in np.unique(job):
             sel = job == k

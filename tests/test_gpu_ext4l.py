@@ -66,12 +66,11 @@ def test_4l_faults_traps_and_aliasing(cuda):
     d = torch.tensor(vas.view(np.int64), device="cuda")
     v, s, _ = dp.translate_lanes(mem.backing, plan, d)
     w = torch.empty(len(vas), dtype=torch.int32, device="cuda")
-    rec = torch.empty(len(vas) * N.EXC_WORDS, dtype=torch.int64, device="cuda")
-    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
-    dp.translate_words(mem.backing, plan, d, w, rec, cnt)
-    n = int(cnt.item())
+    xl = dp.ExcList(len(vas))
+    dp.translate_words(mem.backing, plan, d, w, xl)
+    exc, n, overflow = xl.read()
+    assert not overflow
     assert n == int(((st & 0xFF0) == 0x040).sum())  # traps carry their node: one record each
-    exc = dp.LaneExceptions.from_records(rec[:n * N.EXC_WORDS].cpu().numpy())
     wv, ws, _ = dp.unpack_words(w.cpu().numpy(), vas, exc)
     assert np.array_equal(ws, st) and np.array_equal(wv, v.cpu().numpy().view(np.uint64))
     levels = {int(x) & 0xF for x in st if int(x) & 0xFF0 == 0x010}

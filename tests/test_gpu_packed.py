@@ -77,13 +77,13 @@ def _split(img, plan, d):
 
 
 def _words(img, plan, d, cap, lane_base=0, out_pfn=False):
+    """(words, records counted, LaneExceptions written, overflow)."""
     w = torch.empty(d.numel(), dtype=torch.int32, device="cuda")
-    rec = torch.empty(cap * 4, dtype=torch.int64, device="cuda")
-    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
-    dp.translate_words(img, plan, d, w, rec, cnt, lane_base, out_pfn=out_pfn)
-    n = int(cnt.item())
-    recs = rec[:min(n, cap) * 4].cpu().numpy()
-    return w.cpu().numpy(), n, recs
+    exc = dp.ExcList(cap)
+    dp.translate_words(img, plan, d, w, exc, lane_base, out_pfn=out_pfn)
+    got, n, overflow = exc.read()
+    _words.last = exc
+    return w.cpu().numpy(), n, got, overflow
 
 
 @pytest.mark.parametrize("mode", ["shadow", "tdp"])
@@ -103,9 +103,8 @@ def test_word_lanes_equal_split(cuda, mode, va64):
     plan = dp.TranslatePlan([tr.device_space], [(0, len(vas), 0)], image=img)
     d = torch.from_numpy(vas.view(np.int64) if va64 else vas.astype(np.uint32).view(np.int32)).cuda()
     v, s, a = _split(img, plan, d)
-    w, n, recs = _words(img, plan, d, cap=len(vas), lane_base=1000)
-    exc = dp.LaneExceptions.from_records(recs)
-    assert n == len(exc) and len(set(exc.lane.tolist())) == n
+    w, n, exc, overflow = _words(img, plan, d, cap=len(vas), lane_base=1000)
+    assert not overflow and n == len(exc) and len(set(exc.lane.tolist())) == n
     exc.lane -= 1000
     assert np.array_equal(exc.status, s[exc.lane])
     uv, us, ua = dp.unpack_words(w, d.cpu().numpy(), exc)
@@ -119,24 +118,28 @@ def test_word_lanes_equal_split(cuda, mode, va64):
     assert np.array_equal(np.sort(exc.lane), np.flatnonzero(need))
     # PV_OUT_PFN: the same words' frames are the walk's pfns
     vp, sp_, _ = dp.translate_lanes(img, plan, d, out_pfn=True)
-    wp, _, recs_p = _words(img, plan, d, cap=len(vas), out_pfn=True)
-    pv_, ps_, _ = dp.unpack_words(wp, d.cpu().numpy(), dp.LaneExceptions.from_records(recs_p), out_pfn=True)
+    wp, _, exc_p, _ = _words(img, plan, d, cap=len(vas), out_pfn=True)
+    pv_, ps_, _ = dp.unpack_words(wp, d.cpu().numpy(), exc_p, out_pfn=True)
     assert np.array_equal(pv_, vp.cpu().numpy().view(np.uint64)) and np.array_equal(ps_, sp_.cpu().numpy().view(np.uint32))
 
 
 def test_word_lanes_overflowing_list(cuda):
     """Records past exc_cap are counted, not written; the words stay exact."""
-    memv, space = _c4("tdp")
+    memv, space = _c4("shadow")  # traps: one record per trapping lane
     tr = memv.translator(space, use_cache=False)
     img = memv.host_mem.backing
     rng = np.random.default_rng(12)
     vas = (W.C1_GVA + rng.integers(0, 64 << 20, 200_000)).astype(np.uint32)
     plan = dp.TranslatePlan([tr.device_space], [(0, len(vas), 0)], image=img)
     d = torch.from_numpy(vas.view(np.int32)).cuda()
-    w_full, n, _ = _words(img, plan, d, cap=len(vas))
-    assert n > 16
-    w_small, n_small, recs = _words(img, plan, d, cap=16)
-    assert n_small == n and len(recs) == 16 * 4
+    w_full, n, exc_full, overflow = _words(img, plan, d, cap=len(vas))
+    assert n > 64 and not overflow
+    # 64 records of room: 2 per stripe; every record is counted, each stripe writes what fits
+    w_small, n_small, exc_small, overflow = _words(img, plan, d, cap=64)
+    counts = _words.last._last
+    assert overflow and n_small == n == int(counts.sum())
+    assert len(exc_small) == int(np.minimum(counts, 2).sum())
+    assert set(exc_small.lane.tolist()) <= set(exc_full.lane.tolist())
     assert np.array_equal(w_small, w_full)
 
 

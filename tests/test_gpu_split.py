@@ -44,16 +44,15 @@ def test_walk_beside_copy_on_partitions_equals_serial(cuda):
     src = torch.randint(0, 256, (n,), dtype=torch.uint8, device="cuda",
                         generator=torch.Generator("cuda").manual_seed(3))
 
-    def walk(words, cnt):
-        rec_ = torch.empty(4 * 1024, dtype=torch.int64, device="cuda")
-        dp.translate_words(img, plan, d, words, rec_, cnt)
+    def walk(words, exc):
+        dp.translate_words(img, plan, d, words, exc)
 
     serial_w = torch.empty(len(vas), dtype=torch.int32, device="cuda")
-    walk(serial_w, torch.zeros(1, dtype=torch.int64, device="cuda"))
+    walk(serial_w, dp.ExcList(4096))
     torch.cuda.synchronize()
     split = dp.SmSplit(64)
     w = torch.empty_like(serial_w)
-    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    cnt = dp.ExcList(4096)
     ev = torch.cuda.Event()
     ev.record()
     for k in (0, 1):
@@ -65,7 +64,7 @@ def test_walk_beside_copy_on_partitions_equals_serial(cuda):
     torch.cuda.synchronize()
     assert out == [n]
     assert torch.equal(w, serial_w)
-    assert int(cnt.item()) == 0
+    assert cnt.read()[1] == 0
     # the copy landed: read it back through the reference-style API
     got = np.frombuffer(bytes(acc.copy_from_user(W.C1_GVA + 4096 + 12345, 4096)), dtype=np.uint8)
     assert np.array_equal(got, src[12345:12345 + 4096].cpu().numpy())
