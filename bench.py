@@ -1166,13 +1166,13 @@ def run_c4(args, rank, world, local):
                                      saved.data_ptr(), s), "scatter")
         img.note_device_write()
 
-    # the walk writes 4-byte lane words; traps (their node pfns) go to the exception records
+    # beside the timed (value, status, aux) walk: the same lanes in 4-byte words, traps (their node pfns)
+    # in exception records -- checked equal after the timed steps
     w_words = torch.empty(len(vas_h), dtype=torch.int32, device="cuda")
     w_exc = dp.ExcList(len(vas_h))
 
     def phase_translate():
-        w_exc.reset()
-        dp.translate_words(img, tplan, vas, w_words, w_exc)
+        dp.translate_lanes(img, tplan, vas, out=out)
 
     def phase_copy():
         cplan.shim_written.zero_()
@@ -1234,15 +1234,16 @@ def run_c4(args, rank, world, local):
     cp_ms = sum(e[1].elapsed_time(e[2]) for e in evs)
     tr_ms, cp_ms = shard.max_over_ranks([tr_ms, cp_ms], world, device="cuda")
     K = args.steps
+    st = out[1].cpu().numpy().view(np.uint32)
+    # the same lanes in 4-byte words + exception records decode to exactly the timed step's lanes
+    restore()
+    w_exc.reset()
+    dp.translate_words(img, tplan, vas, w_words, w_exc)
+    torch.cuda.synchronize()
     exc, n_exc, overflow = w_exc.read()
     assert not overflow
-    wv, st, wa = dp.unpack_words(w_words.cpu().numpy(), vas_h, exc)
-    # the same lanes in the (value, status, aux) form: the words decode to exactly them
-    restore()
-    dp.translate_lanes(img, tplan, vas, out=out)
-    torch.cuda.synchronize()
-    words_equal = bool(np.array_equal(st, out[1].cpu().numpy().view(np.uint32))
-                       and np.array_equal(wv, out[0].cpu().numpy().view(np.uint64))
+    wv, ws, wa = dp.unpack_words(w_words.cpu().numpy(), vas_h, exc)
+    words_equal = bool(np.array_equal(ws, st) and np.array_equal(wv, out[0].cpu().numpy().view(np.uint64))
                        and np.array_equal(wa, out[2].cpu().numpy().view(np.uint64)))
     assert words_equal, "C4 lane words differ from the (value, status, aux) form"
     kinds = {hex(k): int(c) for k, c in zip(*np.unique(st & 0xFF0, return_counts=True))}
@@ -1252,7 +1253,7 @@ def run_c4(args, rank, world, local):
     assert 0x10 in [int(k, 16) for k in kinds] and 0x40 in [int(k, 16) for k in kinds]
     total_lanes = 1 << 20
     peak, peak_kind = peaks()
-    walk_ach = 8 * len(vas_h) * K / (tr_ms / 1e3) / 1e9
+    walk_ach = 16 * len(vas_h) * K / (tr_ms / 1e3) / 1e9
     copied = int(res[:, 0].sum())
     return {
         "metric": METRIC, "value": total_lanes * K / (tr_ms / 1e3), "unit": "translations/s", "n_gpus": world,
@@ -1268,9 +1269,10 @@ def run_c4(args, rank, world, local):
         "translate_ms_per_step": tr_ms / K,
         "roofline": {"bound": "hbm", "kernel": "translate_kernel", "achieved": walk_ach, "peak": peak,
                      "unit": "GB/s", "frac": walk_ach / peak, "peak_source": peak_kind,
-                     "note": "8 B/translation (u32 VA in, one u32 lane word out; traps add a 32-byte exception "
-                             "record); 1 M lanes fit L2, so this line is latency-bound, not HBM-bound"},
-        "walk_form": "pv_translate_words (one u32 per lane + exception records)",
+                     "note": "16 B/translation (u32 VA in, u64 value + u32 status out); 1 M lanes fit L2, so this "
+                             "line is latency-bound, not HBM-bound"},
+        "walk_form": "unpacked (u64 value + u32 status); the 4-byte word form (one u32 per lane + an exception "
+                     "record per trapping lane) is checked equal beside it",
         "exception_records": n_exc, "words_equal_unpacked": words_equal,
         "launch": launch_mode,
         "gpu_launches": 7 * K, "gpu_launches_note": "translate, plan, shim eval + cooperative resolve, stamp, exec per step (+ leaf-index re-encode)",
