@@ -31,6 +31,8 @@ def test_upload_does_not_wait_for_a_big_h2d(cuda):
     big_d = torch.empty_like(big_h, device="cuda")
     side = torch.cuda.Stream()
     small = np.arange(1024, dtype=np.int64)
+    dp._to_dev_many([small])  # warm the pinned-block cache: only the GPU timeline is under test
+    torch.cuda.synchronize()
     e0, e_big, e_small = (torch.cuda.Event(enable_timing=True) for _ in range(3))
     torch.cuda.synchronize()
     e0.record()
