@@ -672,7 +672,9 @@ int pv_stream_idle(void* stream);
 /* ---- SM partitions ------------------------------------------------------------
  * Two disjoint SM sets of the current device (green contexts): a group of at
  * least first_sms SMs and the rest, one non-blocking stream on each (created
- * once per (device, first_sms) and kept).  Kernels launched on a stream run
+ * once per (device, first_sms) and kept).  The split is at single-SM
+ * granularity (both sets spread over every GPC; PV_SM_SPLIT_FINE=0 in the
+ * environment keeps the driver's co-scheduled groups of 8).  Kernels launched on a stream run
  * only on its SMs, so a walk (bound by the SM->L2 request rate) and a page
  * copy (bound by HBM) can share the device side by side without competing
  * for the same SMs.  *sms_first / *sms_rest: the SM counts (may be NULL).

@@ -802,8 +802,13 @@ int pv_sm_split(uint32_t first_sms, void** stream_first, void** stream_rest, uin
     CUdevice cd;
     CUdevResource all, grp[1], rem;
     unsigned nb = 1;
+    // partitions at single-SM granularity (CU_DEV_SM_RESOURCE_SPLIT_IGNORE_SM_COSCHEDULING): both sides then
+    // spread over every GPC instead of taking whole ones, which measured 4-5 % faster for the C5 walk beside
+    // the copy (profiles/r02_split_ab.md); PV_SM_SPLIT_FINE=0 keeps the co-scheduled 8-SM groups
+    const char* fine = std::getenv("PV_SM_SPLIT_FINE");
+    const unsigned use = (fine && fine[0] == '0') ? 0u : CU_DEV_SM_RESOURCE_SPLIT_IGNORE_SM_COSCHEDULING;
     if (getdev(&cd, dev) != CUDA_SUCCESS || getres(cd, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS ||
-        first_sms >= all.sm.smCount || split(grp, &nb, &all, &rem, 0, first_sms) != CUDA_SUCCESS || nb != 1)
+        first_sms >= all.sm.smCount || split(grp, &nb, &all, &rem, use, first_sms) != CUDA_SUCCESS || nb != 1)
       return PV_EINVAL;
     CUdevResource* parts[2] = {&grp[0], &rem};
     for (int i = 0; i < 2; ++i) {
