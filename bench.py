@@ -414,11 +414,18 @@ def run_ours(args, rank, world, local):
         ev[1].record(stream)
         img.note_device_write()
 
-    split, split_note = None, None
+    split, split_note, split_cands, split_tune = None, None, [], None
     split_sms = args.split_sms if args.split_sms is not None else (64 if wl.name == "c5" else 0)
     if split_sms and not args.overlap:
         try:
-            split = dp.SmSplit(split_sms)
+            # the driver's co-scheduled 8-SM groups and single-SM granularity place the two SM sets differently
+            # over the GPCs; which is faster depends on the box, so both are timed before the timed region
+            split_cands = [dp.SmSplit(split_sms, fine=False)]
+            try:
+                split_cands.append(dp.SmSplit(split_sms, fine=True))
+            except Exception:  # noqa: BLE001 - the coarse split alone
+                pass
+            split = split_cands[0]
         except Exception as exc:  # noqa: BLE001 - no green contexts: the phases run back to back
             split_note = f"SM split unavailable ({type(exc).__name__}: {str(exc)[:100]}): phases back to back"
 
@@ -475,6 +482,23 @@ def run_ours(args, rank, world, local):
             launch_mode = f"eager (graph capture failed: {type(exc).__name__}: {str(exc)[:120]})"
             torch.cuda.synchronize()
 
+    if len(split_cands) > 1:
+        split_tune = {}
+        for cand in split_cands:
+            split = cand
+            for _ in range(2):
+                step_split([torch.cuda.Event(enable_timing=True) for _ in range(6)])
+            torch.cuda.synchronize()
+            t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0e.record(stream)
+            for _ in range(5):
+                step_split([torch.cuda.Event(enable_timing=True) for _ in range(6)])
+            t1e.record(stream)
+            torch.cuda.synchronize()
+            split_tune["fine" if cand.fine else "coarse"] = t0e.elapsed_time(t1e) / 5
+        (best,) = shard.max_over_ranks([1.0 if split_tune.get("fine", 1e9) < split_tune["coarse"] else 0.0], world,
+                                       device="cuda")  # every rank takes the same choice
+        split = split_cands[1] if best > 0.5 else split_cands[0]
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
@@ -580,6 +604,8 @@ def run_ours(args, rank, world, local):
     split_phases = None
     if split is not None:
         split_phases = {"sms": {"walk": split.sms[0], "plan_exec": split.sms[1]},
+                        "granularity": "single SM" if split.fine else "co-scheduled 8-SM groups",
+                        "tuned_ms_per_step": split_tune,
                         "walk_ms": sum(e[0].elapsed_time(e[2]) for e in ovs) / args.steps,
                         "plan_ms": sum(e[3].elapsed_time(e[4]) for e in ovs) / args.steps,
                         "exec_ms": sum(e[4].elapsed_time(e[5]) for e in ovs) / args.steps,

@@ -672,15 +672,17 @@ int pv_stream_idle(void* stream);
 /* ---- SM partitions ------------------------------------------------------------
  * Two disjoint SM sets of the current device (green contexts): a group of at
  * least first_sms SMs and the rest, one non-blocking stream on each (created
- * once per (device, first_sms) and kept).  The split is at single-SM
- * granularity (both sets spread over every GPC; PV_SM_SPLIT_FINE=0 in the
- * environment keeps the driver's co-scheduled groups of 8).  Kernels launched on a stream run
+ * once per (device, first_sms, flags) and kept).  flags: PV_SM_SPLIT_FINE
+ * splits at single-SM granularity instead of the driver's co-scheduled groups
+ * of 8 SMs (another placement of the two sets over the GPCs; which one is
+ * faster depends on the box -- bench.py times both and keeps the faster).  Kernels launched on a stream run
  * only on its SMs, so a walk (bound by the SM->L2 request rate) and a page
  * copy (bound by HBM) can share the device side by side without competing
  * for the same SMs.  *sms_first / *sms_rest: the SM counts (may be NULL).
  * PV_EINVAL when the split is impossible, PV_ECUDA - cudaErrorNotSupported
  * when the driver has no green contexts. */
-int pv_sm_split(uint32_t first_sms, void** stream_first, void** stream_rest,
+#define PV_SM_SPLIT_FINE 0x1u
+int pv_sm_split(uint32_t first_sms, uint32_t flags, void** stream_first, void** stream_rest,
                 uint32_t* sms_first, uint32_t* sms_rest);
 /* Grids of the calling thread's subsequent launches are sized for `sms` SMs
  * (0: the whole device) -- set it to the partition's count while launching

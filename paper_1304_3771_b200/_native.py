@@ -45,6 +45,7 @@ OUT_PFN = 0x2
 CONCURRENT = 0x4  # pv.h PV_CONCURRENT: one walker CTA per SM
 OUT_PACKED = 0x8  # pv.h PV_OUT_PACKED: one u64 per lane
 SERVER_IDLE = 0x100  # pv.h PV_SERVER_IDLE: the caller's stream has nothing pending
+SM_SPLIT_FINE = 0x1  # pv.h PV_SM_SPLIT_FINE
 PACKED_ERR = 1 << 63
 PACKED_VALUE_BITS = 42
 PACKED_SPILL_VALUE = (1 << 42) - 1
@@ -128,7 +129,7 @@ _SIGNATURES = {
     "pv_stream_sync": (ctypes.c_int, [_p]),
     "pv_stream_idle": (ctypes.c_int, [_p]),
     "pv_upload": (ctypes.c_int, [_p, _p, _u64, _p]),
-    "pv_sm_split": (ctypes.c_int, [_u32, _p, _p, _p, _p]),
+    "pv_sm_split": (ctypes.c_int, [_u32, _u32, _p, _p, _p, _p]),
     "pv_set_sm_budget": (_u32, [_u32]),
     "pv_peer_alloc": (ctypes.c_int, [_u64, _p, _p]),
     "pv_peer_open": (ctypes.c_int, [_p, _p]),

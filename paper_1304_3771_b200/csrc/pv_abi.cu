@@ -780,14 +780,14 @@ bool driver_fn(const char* name, F* fn) {
 
 extern "C" {
 
-int pv_sm_split(uint32_t first_sms, void** stream_first, void** stream_rest, uint32_t* sms_first,
+int pv_sm_split(uint32_t first_sms, uint32_t flags, void** stream_first, void** stream_rest, uint32_t* sms_first,
                 uint32_t* sms_rest) {
-  if (!stream_first || !stream_rest || first_sms == 0) return PV_EINVAL;
+  if (!stream_first || !stream_rest || first_sms == 0 || (flags & ~(uint32_t)PV_SM_SPLIT_FINE)) return PV_EINVAL;
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return rc(e);
   std::lock_guard<std::mutex> lk(g_split_mu);
-  SmSplit& P = g_splits[((uint64_t)dev << 32) | first_sms];
+  SmSplit& P = g_splits[((uint64_t)dev << 33) | ((uint64_t)(flags & PV_SM_SPLIT_FINE) << 32) | first_sms];
   if (P.stream[0] == nullptr) {
     CUresult (*getres)(CUdevice, CUdevResource*, CUdevResourceType) = nullptr;
     CUresult (*split)(CUdevResource*, unsigned*, const CUdevResource*, CUdevResource*, unsigned, unsigned) = nullptr;
@@ -802,11 +802,10 @@ int pv_sm_split(uint32_t first_sms, void** stream_first, void** stream_rest, uin
     CUdevice cd;
     CUdevResource all, grp[1], rem;
     unsigned nb = 1;
-    // partitions at single-SM granularity (CU_DEV_SM_RESOURCE_SPLIT_IGNORE_SM_COSCHEDULING): both sides then
-    // spread over every GPC instead of taking whole ones, which measured 4-5 % faster for the C5 walk beside
-    // the copy (profiles/r02_split_ab.md); PV_SM_SPLIT_FINE=0 keeps the co-scheduled 8-SM groups
-    const char* fine = std::getenv("PV_SM_SPLIT_FINE");
-    const unsigned use = (fine && fine[0] == '0') ? 0u : CU_DEV_SM_RESOURCE_SPLIT_IGNORE_SM_COSCHEDULING;
+    // PV_SM_SPLIT_FINE: single-SM granularity (CU_DEV_SM_RESOURCE_SPLIT_IGNORE_SM_COSCHEDULING) instead of
+    // the driver's co-scheduled 8-SM groups -- a different placement of the two sets over the GPCs, faster on
+    // some boxes and slower on others (profiles/r02_split_ab.md)
+    const unsigned use = (flags & PV_SM_SPLIT_FINE) ? CU_DEV_SM_RESOURCE_SPLIT_IGNORE_SM_COSCHEDULING : 0u;
     if (getdev(&cd, dev) != CUDA_SUCCESS || getres(cd, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS ||
         first_sms >= all.sm.smCount || split(grp, &nb, &all, &rem, use, first_sms) != CUDA_SUCCESS || nb != 1)
       return PV_EINVAL;

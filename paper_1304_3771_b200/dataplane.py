@@ -445,14 +445,15 @@ class SmSplit:
     request bound) on one partition and a page copy (HBM bound) on the other
     run side by side without sharing SMs."""
 
-    def __init__(self, first_sms: int):
+    def __init__(self, first_sms: int, fine: bool = False):
         import torch
 
         lib = N.lib()
         a, b = ctypes.c_void_p(), ctypes.c_void_p()
         na, nb = ctypes.c_uint32(), ctypes.c_uint32()
-        N.check(lib.pv_sm_split(first_sms, ctypes.byref(a), ctypes.byref(b), ctypes.byref(na), ctypes.byref(nb)),
-                "pv_sm_split")
+        N.check(lib.pv_sm_split(first_sms, N.SM_SPLIT_FINE if fine else 0, ctypes.byref(a), ctypes.byref(b),
+                                ctypes.byref(na), ctypes.byref(nb)), "pv_sm_split")
+        self.fine = fine
         self.streams = (torch.cuda.ExternalStream(a.value), torch.cuda.ExternalStream(b.value))
         self.sms = (int(na.value), int(nb.value))
 

@@ -62,7 +62,7 @@ def test_argument_validation_needs_no_gpu():
     assert lib.pv_upload(None, None, 0, None) == N.SUCCESS  # nothing to move
     assert lib.pv_peer_open(None, None) == N.EINVAL
     assert lib.pv_peer_alloc(0, None, None) == N.EINVAL
-    assert lib.pv_sm_split(0, None, None, None, None) == N.EINVAL
+    assert lib.pv_sm_split(0, 0, None, None, None, None) == N.EINVAL
     assert lib.pv_memcpy(None, None, 0, None) == N.SUCCESS
 
 
