@@ -21,10 +21,13 @@ class _G:
         self.id, self.mem_mode = 0, "shadow"
 
 
-def test_split_partitions_are_disjoint_and_cover_the_device(cuda):
-    sp = dp.SmSplit(48)
+@pytest.mark.parametrize("fine", [False, True])
+def test_split_partitions_are_disjoint_and_cover_the_device(cuda, fine):
+    sp = dp.SmSplit(48, fine=fine)
     total = torch.cuda.get_device_properties(0).multi_processor_count
     assert sp.sms[0] >= 48 and sp.sms[0] + sp.sms[1] == total
+    if fine:
+        assert sp.sms[0] == 48  # single-SM granularity: exactly the count asked for
     lib = N.lib()
     with sp.on(1):
         assert lib.pv_set_sm_budget(sp.sms[1]) == sp.sms[1]  # set inside the block
