@@ -418,13 +418,15 @@ def run_ours(args, rank, world, local):
     split_sms = args.split_sms if args.split_sms is not None else (64 if wl.name == "c5" else 0)
     if split_sms and not args.overlap:
         try:
-            # the driver's co-scheduled 8-SM groups and single-SM granularity place the two SM sets differently
-            # over the GPCs; which is faster depends on the box, so both are timed before the timed region
-            split_cands = [dp.SmSplit(split_sms, fine=False)]
-            try:
-                split_cands.append(dp.SmSplit(split_sms, fine=True))
-            except Exception:  # noqa: BLE001 - the coarse split alone
-                pass
+            # the placement of the two SM sets over the GPCs (the driver's co-scheduled 8-SM groups, single-SM
+            # granularity, either one interleaved) changes the step by a few %, and which is fastest depends on
+            # the box: all are timed before the timed region and the fastest is kept
+            split_cands = [dp.SmSplit(split_sms)]
+            for fine, inter in ((True, False), (False, True), (True, True)):
+                try:
+                    split_cands.append(dp.SmSplit(split_sms, fine=fine, interleave=inter))
+                except Exception:  # noqa: BLE001 - a placement the driver refuses is skipped
+                    pass
             split = split_cands[0]
         except Exception as exc:  # noqa: BLE001 - no green contexts: the phases run back to back
             split_note = f"SM split unavailable ({type(exc).__name__}: {str(exc)[:100]}): phases back to back"
@@ -495,10 +497,9 @@ def run_ours(args, rank, world, local):
                 step_split([torch.cuda.Event(enable_timing=True) for _ in range(6)])
             t1e.record(stream)
             torch.cuda.synchronize()
-            split_tune["fine" if cand.fine else "coarse"] = t0e.elapsed_time(t1e) / 5
-        (best,) = shard.max_over_ranks([1.0 if split_tune.get("fine", 1e9) < split_tune["coarse"] else 0.0], world,
-                                       device="cuda")  # every rank takes the same choice
-        split = split_cands[1] if best > 0.5 else split_cands[0]
+            split_tune[cand.placement] = t0e.elapsed_time(t1e) / 5
+        times = shard.max_over_ranks([split_tune[c.placement] for c in split_cands], world, device="cuda")
+        split = split_cands[min(range(len(split_cands)), key=lambda k: times[k])]  # every rank: the same choice
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
@@ -604,7 +605,7 @@ def run_ours(args, rank, world, local):
     split_phases = None
     if split is not None:
         split_phases = {"sms": {"walk": split.sms[0], "plan_exec": split.sms[1]},
-                        "granularity": "single SM" if split.fine else "co-scheduled 8-SM groups",
+                        "placement": split.placement,
                         "tuned_ms_per_step": split_tune,
                         "walk_ms": sum(e[0].elapsed_time(e[2]) for e in ovs) / args.steps,
                         "plan_ms": sum(e[3].elapsed_time(e[4]) for e in ovs) / args.steps,

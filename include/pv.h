@@ -682,6 +682,9 @@ int pv_stream_idle(void* stream);
  * PV_EINVAL when the split is impossible, PV_ECUDA - cudaErrorNotSupported
  * when the driver has no green contexts. */
 #define PV_SM_SPLIT_FINE 0x1u
+/* the device is cut into groups (8 SMs, or 1 with PV_SM_SPLIT_FINE) and the
+ * first set takes every other group: both sets interleave over the GPCs */
+#define PV_SM_SPLIT_INTERLEAVE 0x2u
 int pv_sm_split(uint32_t first_sms, uint32_t flags, void** stream_first, void** stream_rest,
                 uint32_t* sms_first, uint32_t* sms_rest);
 /* Grids of the calling thread's subsequent launches are sized for `sms` SMs

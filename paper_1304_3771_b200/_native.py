@@ -46,6 +46,7 @@ CONCURRENT = 0x4  # pv.h PV_CONCURRENT: one walker CTA per SM
 OUT_PACKED = 0x8  # pv.h PV_OUT_PACKED: one u64 per lane
 SERVER_IDLE = 0x100  # pv.h PV_SERVER_IDLE: the caller's stream has nothing pending
 SM_SPLIT_FINE = 0x1  # pv.h PV_SM_SPLIT_FINE
+SM_SPLIT_INTERLEAVE = 0x2  # pv.h PV_SM_SPLIT_INTERLEAVE
 PACKED_ERR = 1 << 63
 PACKED_VALUE_BITS = 42
 PACKED_SPILL_VALUE = (1 << 42) - 1

@@ -782,12 +782,14 @@ extern "C" {
 
 int pv_sm_split(uint32_t first_sms, uint32_t flags, void** stream_first, void** stream_rest, uint32_t* sms_first,
                 uint32_t* sms_rest) {
-  if (!stream_first || !stream_rest || first_sms == 0 || (flags & ~(uint32_t)PV_SM_SPLIT_FINE)) return PV_EINVAL;
+  if (!stream_first || !stream_rest || first_sms == 0 ||
+      (flags & ~(uint32_t)(PV_SM_SPLIT_FINE | PV_SM_SPLIT_INTERLEAVE)))
+    return PV_EINVAL;
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return rc(e);
   std::lock_guard<std::mutex> lk(g_split_mu);
-  SmSplit& P = g_splits[((uint64_t)dev << 33) | ((uint64_t)(flags & PV_SM_SPLIT_FINE) << 32) | first_sms];
+  SmSplit& P = g_splits[((uint64_t)dev << 34) | ((uint64_t)(flags & 3u) << 32) | first_sms];
   if (P.stream[0] == nullptr) {
     CUresult (*getres)(CUdevice, CUdevResource*, CUdevResourceType) = nullptr;
     CUresult (*split)(CUdevResource*, unsigned*, const CUdevResource*, CUdevResource*, unsigned, unsigned) = nullptr;
@@ -800,26 +802,54 @@ int pv_sm_split(uint32_t first_sms, uint32_t flags, void** stream_first, void** 
         !driver_fn("cuGreenCtxStreamCreate", &gstream) || !driver_fn("cuDeviceGet", &getdev))
       return PV_ECUDA - (int)cudaErrorNotSupported;
     CUdevice cd;
-    CUdevResource all, grp[1], rem;
-    unsigned nb = 1;
+    CUdevResource all, rem;
     // PV_SM_SPLIT_FINE: single-SM granularity (CU_DEV_SM_RESOURCE_SPLIT_IGNORE_SM_COSCHEDULING) instead of
-    // the driver's co-scheduled 8-SM groups -- a different placement of the two sets over the GPCs, faster on
-    // some boxes and slower on others (profiles/r02_split_ab.md)
+    // the driver's co-scheduled 8-SM groups; PV_SM_SPLIT_INTERLEAVE: the device is cut into groups of that
+    // granularity and the first set takes every other group.  Each is a different placement of the two
+    // sets over the GPCs; which is fastest depends on the box (profiles/r02_split_ab.md)
     const unsigned use = (flags & PV_SM_SPLIT_FINE) ? CU_DEV_SM_RESOURCE_SPLIT_IGNORE_SM_COSCHEDULING : 0u;
     if (getdev(&cd, dev) != CUDA_SUCCESS || getres(cd, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS ||
-        first_sms >= all.sm.smCount || split(grp, &nb, &all, &rem, use, first_sms) != CUDA_SUCCESS || nb != 1)
+        first_sms >= all.sm.smCount)
       return PV_EINVAL;
-    CUdevResource* parts[2] = {&grp[0], &rem};
+    std::vector<CUdevResource> groups;
+    std::vector<CUdevResource> sets[2];
+    if (flags & PV_SM_SPLIT_INTERLEAVE) {
+      const unsigned g = (flags & PV_SM_SPLIT_FINE) ? 1u : 8u;
+      unsigned nb = 0;
+      if (split(nullptr, &nb, &all, nullptr, use, g) != CUDA_SUCCESS || nb == 0) return PV_EINVAL;
+      groups.resize(nb);
+      if (split(groups.data(), &nb, &all, &rem, use, g) != CUDA_SUCCESS) return PV_EINVAL;
+      groups.resize(nb);
+      unsigned have = 0;
+      std::vector<bool> taken(nb, false);
+      for (unsigned pass = 0; pass < 2 && have < first_sms; ++pass)  // even groups first, then odd ones
+        for (unsigned k = pass; k < nb && have < first_sms; k += 2) {
+          taken[k] = true;
+          have += groups[k].sm.smCount;
+        }
+      for (unsigned k = 0; k < nb; ++k) sets[taken[k] ? 0 : 1].push_back(groups[k]);
+      if (rem.sm.smCount) sets[1].push_back(rem);
+    } else {
+      CUdevResource grp[1];
+      unsigned nb = 1;
+      if (split(grp, &nb, &all, &rem, use, first_sms) != CUDA_SUCCESS || nb != 1) return PV_EINVAL;
+      sets[0].push_back(grp[0]);
+      sets[1].push_back(rem);
+    }
+    if (sets[0].empty() || sets[1].empty()) return PV_EINVAL;
     for (int i = 0; i < 2; ++i) {
       CUdevResourceDesc d;
       CUgreenCtx g;
       CUstream cs;
-      if (gendesc(&d, parts[i], 1) != CUDA_SUCCESS || gcreate(&g, d, cd, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS ||
+      if (gendesc(&d, sets[i].data(), (unsigned)sets[i].size()) != CUDA_SUCCESS ||
+          gcreate(&g, d, cd, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS ||
           gstream(&cs, g, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS)
         return PV_ECUDA - (int)cudaErrorNotSupported;
       P.green[i] = g;
       P.stream[i] = (cudaStream_t)cs;
-      P.sms[i] = parts[i]->sm.smCount;
+      uint32_t n = 0;
+      for (const auto& r : sets[i]) n += r.sm.smCount;
+      P.sms[i] = n;
     }
   }
   *stream_first = P.stream[0];

@@ -445,15 +445,17 @@ class SmSplit:
     request bound) on one partition and a page copy (HBM bound) on the other
     run side by side without sharing SMs."""
 
-    def __init__(self, first_sms: int, fine: bool = False):
+    def __init__(self, first_sms: int, fine: bool = False, interleave: bool = False):
         import torch
 
         lib = N.lib()
         a, b = ctypes.c_void_p(), ctypes.c_void_p()
         na, nb = ctypes.c_uint32(), ctypes.c_uint32()
-        N.check(lib.pv_sm_split(first_sms, N.SM_SPLIT_FINE if fine else 0, ctypes.byref(a), ctypes.byref(b),
-                                ctypes.byref(na), ctypes.byref(nb)), "pv_sm_split")
-        self.fine = fine
+        flags = (N.SM_SPLIT_FINE if fine else 0) | (N.SM_SPLIT_INTERLEAVE if interleave else 0)
+        N.check(lib.pv_sm_split(first_sms, flags, ctypes.byref(a), ctypes.byref(b), ctypes.byref(na),
+                                ctypes.byref(nb)), "pv_sm_split")
+        self.fine, self.interleave = fine, interleave
+        self.placement = ("interleaved " if interleave else "") + ("single SMs" if fine else "8-SM groups")
         self.streams = (torch.cuda.ExternalStream(a.value), torch.cuda.ExternalStream(b.value))
         self.sms = (int(na.value), int(nb.value))
 

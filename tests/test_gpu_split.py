@@ -22,8 +22,9 @@ class _G:
 
 
 @pytest.mark.parametrize("fine", [False, True])
-def test_split_partitions_are_disjoint_and_cover_the_device(cuda, fine):
-    sp = dp.SmSplit(48, fine=fine)
+@pytest.mark.parametrize("interleave", [False, True])
+def test_split_partitions_are_disjoint_and_cover_the_device(cuda, fine, interleave):
+    sp = dp.SmSplit(48, fine=fine, interleave=interleave)
     total = torch.cuda.get_device_properties(0).multi_processor_count
     assert sp.sms[0] >= 48 and sp.sms[0] + sp.sms[1] == total
     if fine:
