@@ -1,9 +1,11 @@
 #!/bin/bash
-# TMA bulk copies with / without the L2 evict-first hint: serial C5 step and the split step.
+# TMA bulk copies without (the default) / with the L2 evict-first hint: serial C5 step and the split step.
+# The variant library: cd paper_1304_3771_b200/csrc && nvcc <the Makefile's flags> -DPV_BULK_EVICT_FIRST=1 \
+#   -o ../../scripts/libpv_evict.so <the Makefile's sources>
 mkdir -p gpurun_out
-for v in default noevict; do
+for v in default evict; do
   for n in 0 64 72; do
-    if [ $v = noevict ]; then export PV_LIB=$PWD/scripts/libpv_noevict.so; else unset PV_LIB; fi
+    if [ $v = evict ]; then export PV_LIB=$PWD/scripts/libpv_evict.so; else unset PV_LIB; fi
     timeout 900 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --no-parity --split-sms $n \
       > gpurun_out/ev_${v}_$n.json 2> gpurun_out/ev_${v}_$n.err
     python - "$v $n" gpurun_out/ev_${v}_$n.json <<'PY'
