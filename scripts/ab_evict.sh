@@ -1,7 +1,6 @@
 #!/bin/bash
 # TMA bulk copies without (the default) / with the L2 evict-first hint: serial C5 step and the split step.
-# The variant library: cd paper_1304_3771_b200/csrc && nvcc <the Makefile's flags> -DPV_BULK_EVICT_FIRST=1 \
-#   -o ../../scripts/libpv_evict.so <the Makefile's sources>
+# Variant: scripts/build_variant.sh evict -DPV_BULK_EVICT_FIRST=1
 mkdir -p gpurun_out
 for v in default evict; do
   for n in 0 64 72; do

@@ -1,6 +1,7 @@
 #!/bin/bash
 # Walker next-chunk VA prefetch (PV_TR_PREFETCH=1) in the serial and the split C5 step: the split walk is
 # latency-bound (its VA loads queue behind the copy's HBM traffic), the serial one port-bound.
+# Variant: scripts/build_variant.sh prefetch -DPV_TR_PREFETCH=1
 mkdir -p gpurun_out
 for v in default prefetch; do
   for n in 0 64; do

@@ -3,6 +3,7 @@
 # ~3 bank-conflict ways per warp access) vs a probe build that reads one real code per thread and
 # chunk and derives the other lanes' codes in registers (wrong results, the same spread of leaf-index
 # gathers): how much of the walk the SMEM lookup and its conflicts cost.  Serial C5 step, 10 steps.
+# Variant: scripts/build_variant.sh fakecodes -DPV_PROBE_FAKE_CODES
 mkdir -p gpurun_out
 for v in default fakecodes; do
   if [ $v = default ]; then unset PV_LIB; else export PV_LIB=$PWD/scripts/libpv_fakecodes.so; fi

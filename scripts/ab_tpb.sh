@@ -1,5 +1,6 @@
 #!/bin/bash
 # Walker CTA shape (512 x 4 lanes default, 256 x 8, 128 x 16 lanes per thread) in the serial and split C5 step.
+# Variants: scripts/build_variant.sh tpb256 -DPV_TR1_TPB=256; scripts/build_variant.sh tpb128 -DPV_TR1_TPB=128
 mkdir -p gpurun_out
 for v in default tpb256 tpb128; do
   for n in 0 64; do
