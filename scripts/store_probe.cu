@@ -9,6 +9,7 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o scripts/store_probe.bin scripts/store_probe.cu
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 __device__ __forceinline__ uint32_t ld_idx(const uint32_t* p) {
@@ -95,9 +96,10 @@ __global__ void __launch_bounds__(512, 2) kvec(const uint32_t* __restrict__ idx,
   }
 }
 
-int main() {
+int main(int argc, char** argv) {
   const uint64_t n = 128ull << 20;
-  const uint32_t words = 1u << 19;  // 2 MiB
+  const uint32_t words = argc > 1 ? (1u << atoi(argv[1])) : (1u << 19);  // 2 MiB by default (argv[1]: log2 words)
+  printf("table %u KiB\n", words / 256);
   uint32_t *idx, *tab, *o32;
   uint64_t* o64;
   cudaMalloc(&idx, n * 4);
