@@ -35,6 +35,12 @@
 
 namespace pv {
 
+#ifndef PV_TR_WARP_BALLOT
+#define PV_TR_WARP_BALLOT 1  // warp-uniform fast-path decision: C5 -2 %, C4 -6 % walk time (profiles/r02_smem_lookup_ab.md)
+#endif
+#ifndef PV_TR_DEDUP
+#define PV_TR_DEDUP 0  // A/B option: explicit warp dedup of leaf-code gathers (profiles/r02_smem_lookup_ab.md)
+#endif
 constexpr int kTpb = 256;
 constexpr int kVpt = 8;
 constexpr uint64_t kChunk = (uint64_t)kTpb * kVpt;  // lanes per chunk
@@ -332,20 +338,45 @@ translate_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const 
         const bool valid = lane0 + (uint64_t)j * TPB + threadIdx.x < seg_end;
         simple &= !valid || (fc[j] & 0xFu) == (1u | kCodeIndexed);
       }
+#if PV_TR_WARP_BALLOT
+      // warp-ballot fault handling (north star): the warp takes the fast path only when every lane of it
+      // can, so the branch is warp-uniform -- measured faster than a per-thread decision on both the
+      // fault-free C5 walk and the fault-heavy C4 one
+      simple = __all_sync(0xFFFFFFFFu, simple);
+#endif
       if (simple) {
         uint32_t lc[VPT];
 #pragma unroll
         for (int j = 0; j < VPT; ++j) {
           const bool valid = lane0 + (uint64_t)j * TPB + threadIdx.x < seg_end;
           lc[j] = 1u;
+#if PV_TR_DEDUP
+          // A/B option (north star: "a coalesced TLB-style dedup of repeated pages"): lanes of the warp
+          // that want the same leaf code elect one loader and receive the code by shuffle; default: the
+          // LSU merges same-sector requests of one warp instruction by itself
+          {
+            const uint32_t* a = leaf_codes + ((uint64_t)(fc[j] >> 4) << 9) + leaf_index(va[j]);
+            const unsigned peers = __match_any_sync(0xFFFFFFFFu, valid ? (unsigned long long)a : ~0ull);
+            const int leader = __ffs(peers) - 1;
+            uint32_t v = 1u;
+            if (valid && (int)(threadIdx.x & 31u) == leader)
+              asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol_table));
+            v = __shfl_sync(0xFFFFFFFFu, v, leader);
+            if (valid) lc[j] = v;
+          }
+#else
           if (valid)
             asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;"
                 : "=r"(lc[j])
                 : "l"(leaf_codes + ((uint64_t)(fc[j] >> 4) << 9) + leaf_index(va[j])), "l"(pol_table));
+#endif
         }
         bool present = true;
 #pragma unroll
         for (int j = 0; j < VPT; ++j) present &= (lc[j] & 3u) == 1u;
+#if PV_TR_WARP_BALLOT
+        present = __all_sync(0xFFFFFFFFu, present);
+#endif
         if (present && kTwo && two) {
           // stage 2 over the gpa: lc[] becomes the TDP leaf code (same shape)
           uint64_t gpa[VPT];
