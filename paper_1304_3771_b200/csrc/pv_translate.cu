@@ -388,6 +388,9 @@ translate_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const 
             const bool valid = lane0 + (uint64_t)j * TPB + threadIdx.x < seg_end;
             simple2 &= !valid || (fc[j] & 0xFu) == (1u | kCodeIndexed);
           }
+#if PV_TR_WARP_BALLOT
+          simple2 = __all_sync(0xFFFFFFFFu, simple2);
+#endif
           present = simple2;
           if (simple2) {
 #pragma unroll
@@ -401,6 +404,9 @@ translate_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const 
             }
 #pragma unroll
             for (int j = 0; j < VPT; ++j) present &= (lc[j] & 3u) == 1u;
+#if PV_TR_WARP_BALLOT
+            present = __all_sync(0xFFFFFFFFu, present);
+#endif
           }
         }
         if (present) {
