@@ -108,6 +108,27 @@ def peaks():
         return 6650.0, "fallback"
 
 
+class L2Flush:
+    """Evicts the L2 between timed steps of the workloads whose inputs fit in
+    it (C1, C3, C4): a 256 MiB write (2x the 126 MB L2) on the timing stream,
+    issued outside each step's event bracket."""
+
+    BYTES = 256 << 20
+
+    def __init__(self):
+        import torch
+
+        self.buf = torch.empty(self.BYTES, dtype=torch.uint8, device="cuda")
+        self.n = 0
+
+    def __call__(self):
+        self.n += 1
+        self.buf.fill_(self.n & 0xFF)
+
+    def note(self):
+        return f"L2 flushed between timed steps ({self.BYTES >> 20} MiB write outside each step's events)"
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
@@ -509,21 +530,30 @@ def run_ours(args, rank, world, local):
            for _ in range(args.steps)]
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
+    # C1's inputs fit in L2: flush it between steps, outside each step's bracket
+    flush = L2Flush() if wl.name != "c5" else None
+    brackets = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                for _ in range(args.steps)]
     # the timed region: K steps (walk beside plan + exec unless --serial-step)
     barrier()
     torch.cuda.synchronize()
     t_start.record(stream)
     for k in range(args.steps):
+        if flush is not None:
+            flush()
+        brackets[k][0].record(stream)
         if split is not None:
             step_split(ovs[k])
         elif overlap:
             step_overlap(ovs[k])
         else:
             step(evs[k])
+        brackets[k][1].record(stream)
     t_end.record(stream)
     torch.cuda.synchronize()
     barrier()
-    total_ms = t_start.elapsed_time(t_end)
+    total_ms = (t_start.elapsed_time(t_end) if flush is None
+                else sum(a.elapsed_time(b) for a, b in brackets))
     split_out = None
     if split is not None:  # the split steps' lane results, compared with the serial steps' below
         split_out = (w_words if form == "words" else wl.out[0]).clone()
@@ -532,6 +562,8 @@ def run_ours(args, rank, world, local):
         barrier()
         torch.cuda.synchronize()
         for k in range(args.steps):
+            if flush is not None:
+                flush()
             step(evs[k])
         torch.cuda.synchronize()
         barrier()
@@ -583,12 +615,15 @@ def run_ours(args, rank, world, local):
                 dp.translate_lanes(img, wl.tplan, wl.vas, out=(o2[0], None, o2[2]), packed=True)
             else:
                 dp.translate_lanes(img, wl.tplan, wl.vas, out=o2)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         other_walk()
-        e0.record(stream)
-        for _ in range(args.steps):
+        o_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                for _ in range(args.steps)]
+        for a, b in o_ev:
+            if flush is not None:
+                flush()
+            a.record(stream)
             other_walk()
-        e1.record(stream)
+            b.record(stream)
         torch.cuda.synchronize()
         if wide:
             ov, os_ = dp.unpack_lanes(o2[0].cpu().numpy(), o2[2].cpu().numpy())
@@ -596,7 +631,7 @@ def run_ours(args, rank, world, local):
         else:
             same = bool(torch.equal(o2[0], wl.out[0]) and torch.equal(o2[1], wl.out[1]))
         other = {"form": "PV_OUT_PACKED (one u64 per lane)" if wide else "unpacked (u64 value + u32 status)",
-                 "translate_ms_per_step": e0.elapsed_time(e1) / args.steps, "launch": "eager",
+                 "translate_ms_per_step": sum(a.elapsed_time(b) for a, b in o_ev) / args.steps, "launch": "eager",
                  "results_equal": same}
     n_faults = int((wl.out[1] != 0).sum().item())
     tr_ms = sum(e[0].elapsed_time(e[1]) for e in evs)
@@ -990,14 +1025,21 @@ def run_c2(args, rank, world, local):
         step(evs[k])
     torch.cuda.synchronize()
     clk = clocks.stop()
-    # the apply kernel's own launch time (for the roofline), from event-timed eager runs of the same phases
+    # per-kernel launch times (rooflines, dominant kernel), from event-timed eager runs of the same phases
     lib.pv_timing(1)
     for _ in range(3):
+        frames, _, _ = hc.pack_device(fops_d, vcpu_d, cr3_d, tag_d, n_frames=len(gvas))
+        hc.dispatch_device(frames, reg, tables)
         phase_plan()
         phase_apply()
     torch.cuda.synchronize()
     n_apply = ctypes.c_uint64(0)
     kern_ms = lib.pv_timing_ms(b"ordered_apply", ctypes.byref(n_apply))
+    kern_each = {}
+    for name in C2_TIMED_KERNELS:
+        n_l = ctypes.c_uint64(0)
+        t = lib.pv_timing_ms(name.encode(), ctypes.byref(n_l))
+        kern_each[name] = t / max(int(n_l.value), 1)
     lib.pv_timing(0)
     img.note_device_write()
     fwd_ms = sum(e[0].elapsed_time(e[1]) for e in evs)
@@ -1035,6 +1077,9 @@ def run_c2(args, rank, world, local):
     alg_bytes = 2 * surviving
     per_launch_ms = kern_ms / max(int(n_apply.value), 1)
     ach = alg_bytes / (per_launch_ms / 1e3) / 1e9
+    kern_each = dict(zip(kern_each, shard.max_over_ranks(list(kern_each.values()), world, device="cuda")))
+    kernels = c2_kernel_table(kern_each, len(gvas), plan.n_pages, per_launch_ms, alg_bytes, peak, peak_kind)
+    dominant = max(kernels, key=lambda k: kernels[k]["launch_ms"])
     return {
         "metric": METRIC, "value": args.c2_ops * K / (total_ms / 1e3), "unit": "ioctls/s", "n_gpus": world,
         "steps": K, "warmup": args.warmup, "ms_per_step": total_ms / K, "higher_is_better": True,
@@ -1042,18 +1087,17 @@ def run_c2(args, rank, world, local):
         "config": {"workload": f"C2: {args.c2_ops} IOCTL_SNAPSHOT ops forwarded as hypercall frames (frontend "
                                "pack, backend identify + reassemble) and their 64 B-4 KiB blobs staged by "
                                "copy_to_user into 8 processes' 1 MiB arenas of one TDP guest, software HAS (FIFO-10)",
-                   "parallelism": f"process-sharded x{world}"},
+                   "parallelism": f"process-sharded x{world}",
+                   "l2": f"inputs larger than L2 ({args.c2_ops} x 136 B FileOp rows + 40 B frames, "
+                         f"{payload / 1e9:.1f} GB of blobs per step)"},
         "copy": {"value": payload * K / (total_ms / 1e3) / 1e9, "unit": "GB/s (payload)"},
         "forward_ms_per_step": fwd_ms / K, "plan_fifo_ms_per_step": plan_ms / K,
         "ordered_apply_ms_per_step": apply_ms / K,
-        "roofline": {"bound": "hbm", "kernel": "ordered_apply_kernel", "achieved": ach, "peak": peak,
-                     "unit": "GB/s", "frac": ach / peak, "peak_source": peak_kind,
-                     "traffic": traffic_for(load_traffic("c2"), "ordered_apply", alg_bytes), "launch_ms": per_launch_ms,
-                     "alg_bytes_per_launch": alg_bytes, "payload_bytes_per_step": int(lens.sum()),
-                     "note": "bytes that survive last-writer-wins (each distinct destination byte read once from "
-                             "its last writer and written once) over the apply kernel's event-timed launch "
-                             "duration (pv_timing); the kernel no longer moves overwritten payload, so it is "
-                             "latency-bound (~2k destination pages, a few dependent TMA loads each), not HBM-bound"},
+        "roofline": dict(kernels[dominant], kernel=dominant + "_kernel", dominant_by="event-timed launch ms "
+                         "(pv_timing) among the step's kernels in `kernels`",
+                         traffic=traffic_for(load_traffic("c2"), dominant, kernels[dominant]["alg_bytes_per_launch"])),
+        "kernels": kernels,
+        "payload_bytes_per_step": int(lens.sum()),
         "launch": launch_mode,
         "gpu_launches": 14 * K, "gpu_launches_note": "per step: frame pack, identify, classify, plan, 6 FIFO-replay "
                                                      "kernels (runs, spec, link, block, verify, apply), stamp, exec "
@@ -1063,6 +1107,50 @@ def run_c2(args, rank, world, local):
         "cpu_baseline": (c2_cpu_baseline(memv, spaces, procs, gvas, lens, cpu_threads())
                          if rank == 0 and world == 1 and not args.no_cpu_baseline else None),
     }
+
+
+C2_TIMED_KERNELS = ("frame_pack", "frame_classify", "plan", "fifo_spec", "stamp", "ordered_keys", "ordered_sort")
+
+
+def c2_kernel_table(ms, n_ops, n_pages, apply_ms, apply_bytes, peak, peak_kind):
+    """Per-kernel launch times of a C2 step (pv_timing event pairs) with the
+    algorithmic HBM bytes each one must move and the
+    resulting fraction of the measured HBM peak.  Sizes: FileOp row 136 B,
+    frame 40 B, pv_op 32 B, pv_op_result 32 B, chunk descriptor 16 B."""
+    alg = {  # kernel -> (bytes per launch, how they are counted)
+        "frame_pack": (212 * n_ops, "per op: 136 B FileOp row + vcpu / cr3 / tag / frame slot (32 B) in, one 40 B "
+                                    "frame + 4 B status out"),
+        "frame_classify": (189 * n_ops, "per frame: 40 B frame + record + status in, 136 B op row + pair flag + "
+                                        "iota out"),
+        "plan": (48 * n_ops + 20 * n_pages, "per op: pv_op + page offset in, first-bad out; per page: hpa + status "
+                                           "+ aux out (table nodes hit L2)"),
+        "fifo_spec": (40 * n_ops + 44 * n_pages, "per FIFO-10 lookup: ref + op id + fresh hpa + status in, hit page "
+                                                "+ flags out, window start / end states (~10.5 B per lookup); per "
+                                                "op: pv_op + page offset.  Replays 32-lookup windows per warp (cache "
+                                                "state in lanes, shuffles / match_any): bound by issue and dependent "
+                                                "loads, not HBM"),
+        "stamp": (16 * n_ops + 24 * n_pages, "per page: hpa in + owner word read-modify-write; per op: page offset "
+                                             "+ first-bad"),
+        "ordered_keys": (80 * n_ops + 28 * n_pages, "per op: pv_op + page offset + first-bad in, result out; per "
+                                                    "page: hpa in, 4 B key + 16 B chunk descriptor out"),
+        "ordered_sort": (84 * n_pages, "CUB onesweep radix sort of (4 B key, 16 B descriptor) pairs: a key "
+                                       "histogram pass + two passes reading and writing every pair"),
+    }
+    out = {}
+    for k, t in ms.items():
+        if t <= 0:
+            continue
+        b, note = alg[k]
+        ach = b / (t / 1e3) / 1e9
+        out[k] = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                  "peak_source": peak_kind, "launch_ms": t, "alg_bytes_per_launch": b, "note": note}
+    ach = apply_bytes / (apply_ms / 1e3) / 1e9
+    out["ordered_apply"] = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                            "peak_source": peak_kind, "launch_ms": apply_ms, "alg_bytes_per_launch": apply_bytes,
+                            "note": "bytes that survive last-writer-wins (each distinct destination byte read once "
+                                    "from its last writer and written once); latency-bound (~2k destination pages, "
+                                    "a few dependent TMA loads each)"}
+    return out
 
 
 def run_c3(args, rank, world, local):
@@ -1108,16 +1196,18 @@ def run_c3(args, rank, world, local):
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    flush = L2Flush()  # 84 MB of lanes per step fit in L2: flushed between steps, outside the events
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     torch.cuda.synchronize()
-    e0.record(stream)
-    for _ in range(args.steps):
+    for e0, e1 in evs:
+        flush()
+        e0.record(stream)
         graph.replay() if graph else dp.translate_lanes(mem.backing, plan, vas, out=out)
-    e1.record(stream)
+        e1.record(stream)
     torch.cuda.synchronize()
     clk = clocks.stop()
     assert int((out[1] != 0).sum().item()) == 0
-    (ms,) = shard.max_over_ranks([e0.elapsed_time(e1)], world, device="cuda")
+    (ms,) = shard.max_over_ranks([sum(a.elapsed_time(b) for a, b in evs)], world, device="cuda")
     total = len(X.c3_sequential()) + len(X.c3_strided())
     peak, peak_kind = peaks()
     ach = 20 * len(vas_h) * args.steps / (ms / 1e3) / 1e9
@@ -1127,7 +1217,7 @@ def run_c3(args, rank, world, local):
         "scaling": "strong", "vs_baseline": None, "dtype": "u64 (integer walk)", "data": "synthetic",
         "config": {"workload": "C3 (extension geometry, parity unpinned): 16 GiB device mmap, alternating "
                                "2 MiB / 4 KiB leaves, 4-level 9/9/9/9/12 tables; sequential 4 KiB-stride + "
-                               "strided 2 MiB+4 KiB batches", "lanes": total},
+                               "strided 2 MiB+4 KiB batches", "lanes": total, "l2": flush.note()},
         "roofline": {"bound": "hbm", "kernel": "translate_generic_kernel", "achieved": ach, "peak": peak,
                      "unit": "GB/s", "frac": ach / peak, "peak_source": peak_kind,
                      "note": "20 B/translation (u64 VA in, u64 hpa + u32 status out)"},
@@ -1259,8 +1349,10 @@ def run_c4(args, rank, world, local):
         tdist.barrier()
     torch.cuda.synchronize()
     fixed = []
+    flush = L2Flush()  # 1 M lanes + 64 MiB of copies fit in L2: flushed between steps, outside the events
     for k in range(args.steps):
         restore()
+        flush()
         step(evs[k])
         fixed.append(cplan.shim_written.clone())
     torch.cuda.synchronize()
@@ -1297,7 +1389,7 @@ def run_c4(args, rank, world, local):
         "config": {"workload": "C4: C1 tables (16,384 shuffled pages), 20 % of shadow leaves not present, 10 % "
                                "trapping; 1 M translations (10 % uniform over 2^32) + 4096 x 16 KiB copy_to_user "
                                "through the hybrid resolver with the device trap shim",
-                   "lane_status_counts": kinds, "parallelism": f"lane/op-sharded x{world}"},
+                   "lane_status_counts": kinds, "parallelism": f"lane/op-sharded x{world}", "l2": flush.note()},
         "copy": {"value": copied * K / (cp_ms / 1e3) / 1e9 * world, "unit": "GB/s (payload copied)",
                  "ms_per_step": cp_ms / K, "slots_fixed_by_shim_per_step": n_fixed[0],
                  "ops_faulted": int(((res[:, 3] & 0xFFFFFFFF) != 0).sum())},
@@ -1535,7 +1627,8 @@ def config_of(wl, world):
             else "reference 3-level 2/9/9/12",
             "parallelism": f"lane-split x{world} (one process: the VA range and the copy's destination pages "
                            "split evenly over the ranks, image replicated, no collective)",
-            "l2": "inputs smaller than L2 (not flushed)"}
+            "l2": "inputs smaller than L2: L2 flushed between timed steps (256 MiB write outside each step's "
+                  "events)"}
 
 
 # ---- CPU baseline / reference arm ---------------------------------------------------

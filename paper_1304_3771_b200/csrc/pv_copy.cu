@@ -751,6 +751,7 @@ cudaError_t launch_copy_plan(const uint8_t* image, uint64_t image_bytes, const p
   uint64_t grid = (threads + kPlanTpb - 1) / kPlanTpb;
   const NodeMarks marks{node_map, epoch};
   auto* fb = reinterpret_cast<unsigned long long*>(op_first_bad);
+  void* tk = timing_begin("plan", stream);
   if (node_map != nullptr) {
     const uint64_t cap = resident_grid((const void*)plan_kernel<true>, kPlanTpb, 0);
     if (grid > cap) grid = cap;
@@ -762,6 +763,7 @@ cudaError_t launch_copy_plan(const uint8_t* image, uint64_t image_bytes, const p
     plan_kernel<false><<<(unsigned)grid, kPlanTpb, 0, stream>>>(image, image_bytes, spaces, ops, n_ops, page_off,
                                                                 n_pages, page_hpa, page_status, page_aux, fb, marks);
   }
+  timing_end(tk, stream);
   return cudaGetLastError();
 }
 
@@ -773,9 +775,11 @@ cudaError_t launch_copy_stamp(const uint64_t* page_off, uint64_t n_ops, uint64_t
   uint64_t grid = (threads + kPlanTpb - 1) / kPlanTpb;
   const uint64_t cap = resident_grid((const void*)stamp_kernel, kPlanTpb, 0);
   if (grid > cap) grid = cap;
+  void* tk = timing_begin("stamp", stream);
   stamp_kernel<<<(unsigned)grid, kPlanTpb, 0, stream>>>(
       page_off, n_ops, n_pages, page_hpa, reinterpret_cast<const unsigned long long*>(op_first_bad),
       reinterpret_cast<unsigned long long*>(owner), owner_pages, epoch, conflict, node_map);
+  timing_end(tk, stream);
   return cudaGetLastError();
 }
 

@@ -101,6 +101,72 @@ __device__ __forceinline__ Lookup load_lookup(const FifoStream& fs, uint64_t l, 
   return r;
 }
 
+// The same lookup in three stages, for a software-pipelined window loop
+// (fifo_spec_kernel): A loads the lookup's own words, B the words they point
+// at, C derives the Lookup (load_lookup's arithmetic, same results).  Stage B
+// of window w + 1 and stage A of window w + 2 are issued before window w is
+// replayed, so their loads are in flight during the replay.
+struct LookupA {
+  uint64_t ref;
+  uint32_t op;
+  bool valid;
+};
+struct LookupB {
+  LookupA a;
+  uint64_t fresh, gva, len, poff;  // lanes: gva holds the lane's va
+  uint32_t st;
+};
+
+__device__ __forceinline__ LookupA lookup_a(const FifoStream& fs, uint64_t l, bool valid) {
+  LookupA a;
+  a.valid = valid;
+  a.ref = valid ? fs.ref[l] : 0;
+  a.op = (valid && fs.op != nullptr) ? fs.op[l] : 0;
+  return a;
+}
+
+__device__ __forceinline__ LookupB lookup_b(const FifoStream& fs, const LookupA& a) {
+  LookupB b;
+  b.a = a;
+  b.fresh = b.gva = b.len = b.poff = 0;
+  b.st = 0;
+  if (!a.valid) return b;
+  b.st = fs.status[a.ref];
+  b.fresh = fs.value[a.ref];
+  if (fs.op == nullptr) {
+    b.gva = fs.va32 ? (uint64_t)((const uint32_t*)fs.vas)[a.ref] : ((const uint64_t*)fs.vas)[a.ref];
+  } else {
+    b.gva = fs.ops[a.op].gva;
+    b.len = fs.ops[a.op].len;
+    b.poff = fs.page_off[a.op];
+  }
+  return b;
+}
+
+__device__ __forceinline__ Lookup lookup_c(const FifoStream& fs, const LookupB& b, uint64_t l) {
+  Lookup r;
+  r.valid = b.a.valid;
+  r.key = r.fresh = r.off = r.chunk = 0;
+  r.op = kNoOp;
+  r.walk_ok = r.data_ok = false;
+  if (!r.valid) return r;
+  r.fresh = b.fresh;
+  r.data_ok = b.st == PV_ST_OK;
+  r.walk_ok = b.st == PV_ST_OK || b.st == PV_ST_DATA_OOR;
+  if (fs.op == nullptr) {
+    r.key = b.gva >> kPageShift;
+    r.off = b.gva & kPageMask;
+    r.op = (uint32_t)l;
+  } else {
+    const uint64_t cur = op_page_va(b.gva, b.a.ref - b.poff);
+    r.key = cur >> kPageShift;
+    r.off = cur & kPageMask;
+    r.chunk = min(b.len - (cur - b.gva), kPageSize - r.off);
+    r.op = b.a.op;
+  }
+  return r;
+}
+
 // Cache state distributed over a warp: lane i < len holds the i-th oldest
 // entry.  term_op: op whose pages are already terminated (copy plans).
 struct WarpState {
@@ -307,8 +373,14 @@ __device__ __forceinline__ bool run_of_slot(const uint64_t* run_off, uint32_t n_
   return r < run_off[n_procs];
 }
 
+// Software-pipelined window loads at 3 CTAs/SM (80 registers): fifo_spec
+// 0.578 -> 0.536 ms per C2 launch; at 4 CTAs/SM they spill (0.613 ms)
+// (profiles/r02_fifo_pipe_ab.md)
+#ifndef PV_FIFO_PIPE
+#define PV_FIFO_PIPE 1
+#endif
 #ifndef PV_FIFO_SPEC_MINB
-#define PV_FIFO_SPEC_MINB 4
+#define PV_FIFO_SPEC_MINB (PV_FIFO_PIPE ? 3 : 4)
 #endif
 __global__ void __launch_bounds__(256, PV_FIFO_SPEC_MINB) fifo_spec_kernel(FifoStream fs, const pv_fifo* __restrict__ fifo, Scratch sc, uint64_t n_slots_max,
                                  const uint64_t* __restrict__ run_off, unsigned long long* first_bad) {
@@ -337,12 +409,41 @@ __global__ void __launch_bounds__(256, PV_FIFO_SPEC_MINB) fifo_spec_kernel(FifoS
       s.term_op = kNoOp;
       from = wi0 - kWarmWindows;
     }
+#if PV_FIFO_PIPE
+    // software-pipelined: window v replays while window v + 1's pointed-at
+    // words and window v + 2's own words load
+    auto lk = [&](uint64_t v) { return lb + v * 32 + lane; };
+    LookupB nb = lookup_b(fs, lookup_a(fs, lk(from), lk(from) < le));
+    LookupA na = lookup_a(fs, lk(from + 1), from + 1 < wi1 && lk(from + 1) < le);
+    for (uint64_t v = from; v < wi1; ++v) {
+      const Lookup x = lookup_c(fs, nb, lk(v));
+      nb = lookup_b(fs, na);
+      na = lookup_a(fs, lk(v + 2), v + 2 < wi1 && lk(v + 2) < le);
+      const uint64_t l0 = lb + v * 32;
+      const uint32_t n = (uint32_t)(le > l0 ? (le - l0 < 32 ? le - l0 : 32) : 0);
+      bool hit, term, active;
+      uint64_t hp;
+      if (v < wi0) {  // warm-up window: state only
+        window_run(fs, x, n, lane, s, &hit, &hp, &term, &active, nullptr);
+        continue;
+      }
+      const uint64_t wi = v;
+      const uint64_t w = w0 + wi;
+      store_state(sc.spec_start + w * fs.state_words, fs.cap, lane, s);
+      uint64_t counts = 0;
+      window_run(fs, x, n, lane, s, &hit, &hp, &term, &active, &counts);
+      if (x.valid) {
+        sc.hitpage[lk(v)] = hp;
+        sc.flags[lk(v)] = (hit ? 1 : 0) | (term ? 2 : 0) | (active ? 4 : 0);
+      }
+#else
     for (uint64_t v = from; v < wi0; ++v) run_one(fs, lb, le, v, lane, s, nullptr, nullptr);
     for (uint64_t wi = wi0; wi < wi1; ++wi) {
       const uint64_t w = w0 + wi;
       store_state(sc.spec_start + w * fs.state_words, fs.cap, lane, s);
       uint64_t counts = 0;
       run_one(fs, lb, le, wi, lane, s, &sc, &counts);
+#endif
       store_state(sc.spec_end + w * fs.state_words, fs.cap, lane, s);
       if (lane == 0) {
         sc.win_counts[w] = counts;
@@ -586,7 +687,9 @@ cudaError_t launch_fifo_stream(const FifoStream& fs, pv_fifo* fifo, void* scratc
     const uint64_t cap = resident_grid((const void*)fifo_spec_kernel, 256, 0);
     if (grid > cap) grid = cap;
     if (grid == 0) grid = 1;
+    void* tk = timing_begin("fifo_spec", stream);
     fifo_spec_kernel<<<(unsigned)grid, 256, 0, stream>>>(fs, fifo, sc, runs_max, run_off, fb);
+    timing_end(tk, stream);
   }
   fifo_link_kernel<<<(unsigned)((n_windows + 255) / 256), 256, 0, stream>>>(fs, sc, n_windows);
   fifo_block_kernel<<<(unsigned)((n_windows + 255) / 256), 256, 0, stream>>>(fs, sc, n_windows);

@@ -270,8 +270,10 @@ cudaError_t launch_frame_pack(const uint64_t* ops, uint64_t n, const uint64_t* v
                               const uint64_t* tag, const uint64_t* frame_off, pv_frame* frames, uint32_t* status,
                               cudaStream_t stream) {
   if (n == 0) return cudaSuccess;
+  void* tk = timing_begin("frame_pack", stream);
   frame_pack_kernel<<<grid_for((const void*)frame_pack_kernel, n), kFrTpb, 0, stream>>>(ops, n, vcpu, cr3, tag,
                                                                                        frame_off, frames, status);
+  timing_end(tk, stream);
   return cudaGetLastError();
 }
 
@@ -318,8 +320,10 @@ cudaError_t launch_frame_assemble(const pv_frame* frames, uint64_t n, const uint
   void* temp = p + off;
   size_t temp_bytes = scratch_bytes > off ? scratch_bytes - off : 0;
 
+  void* tk = timing_begin("frame_classify", stream);
   frame_classify_kernel<<<grid_for((const void*)frame_classify_kernel, n), kFrTpb, 0, stream>>>(
       frames, n, record, ops_out, status, flag, keys, iota);
+  timing_end(tk, stream);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   // compact the pairing frames in order

@@ -533,14 +533,18 @@ cudaError_t launch_copy_ordered(uint8_t* image, uint64_t image_bytes, const pv_o
   {
     uint64_t g = (n_ops + 255) / 256;
     if (g > 8192) g = 8192;
+    void* tk = timing_begin("ordered_keys", stream);
     ordered_keys_kernel<<<(unsigned)g, 256, 0, stream>>>(ops, n_ops, page_off, page_hpa, page_status, page_aux,
                                                          reinterpret_cast<const unsigned long long*>(op_first_bad),
                                                          buf, buf_bytes, dead_key, s.keys_in, s.desc, results);
+    timing_end(tk, stream);
   }
   size_t tb = s.cub_bytes;
   // the 16-byte descriptors ride along as the sort's values (no index gather afterwards)
+  void* tks = timing_begin("ordered_sort", stream);
   cudaError_t e = cub::DeviceRadixSort::SortPairs(s.cub_tmp, tb, s.keys_in, s.keys_out, s.desc, s.desc_sorted,
                                                   (int)n_pages, 0, end_bit, stream);
+  timing_end(tks, stream);
   if (e != cudaSuccess) return e;
   tb = s.cub_bytes;
   e = cub::DeviceRunLengthEncode::Encode(s.cub_tmp, tb, s.keys_out, s.seg_key, s.seg_len, s.n_segs, (int)n_pages,

@@ -531,16 +531,49 @@ translate_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes, const 
 }
 
 // Generic form for batches that contain extension-geometry spaces
-// (PV_ONE_STAGE_4L): every lane walks through L1/L2-cached global loads
-// (translate_global), 8 lanes per thread.
+// (PV_ONE_STAGE_4L), 8 lanes per thread, each lane walked through
+// translate_global.  PV_GEN_LEVELSYNC=1 (A/B option) walks a 4-level chunk's
+// 8 lanes level by level instead (walk4_global's checks in the same order, the
+// 8 loads of a level in flight together): C3 -5 %, C1 4-level +19 % walk time
+// (profiles/r02_generic_ab.md), so lane-by-lane stays the default.
 #ifndef PV_GEN_TPB
 #define PV_GEN_TPB 256
+#endif
+#ifndef PV_GEN_LEVELSYNC
+#define PV_GEN_LEVELSYNC 0
+#endif
+#ifndef PV_GEN_MINB
+#define PV_GEN_MINB 0  // A/B option: minimum resident CTAs per SM for the register budget
 #endif
 constexpr int kGenTpb = PV_GEN_TPB;
 constexpr int kGenVpt = (int)(kChunk / kGenTpb);
 
 template <bool kVa32, bool kPfn>
+__device__ __forceinline__ void emit_lane(uint64_t i, uint32_t st, uint64_t v, uint64_t a, uint64_t va,
+                                          uint64_t* __restrict__ out_value, uint32_t* __restrict__ out_status,
+                                          uint64_t* __restrict__ out_aux, uint32_t mode, const ExcSink& sink) {
+  if (mode == kOutWord) {
+    reinterpret_cast<uint32_t*>(out_value)[i] = word_lane(st, v, va, PV_ST_KIND(st) == PV_ST_TRAP2 ? a : 0, i, sink);
+    return;
+  }
+  if (!kPfn && st == PV_ST_OK) v = (v << kPageShift) | (va & kPageMask);
+  if (mode == kOutPacked) {
+    bool spill;
+    out_value[i] = pack_lane(st, v, &spill);
+    if (spill && out_aux != nullptr) out_aux[i] = v;
+  } else {
+    out_value[i] = v;
+    out_status[i] = st;
+  }
+  if (out_aux != nullptr && PV_ST_KIND(st) == PV_ST_TRAP2) out_aux[i] = a;
+}
+
+template <bool kVa32, bool kPfn>
+#if PV_GEN_MINB > 1
+__global__ void __launch_bounds__(kGenTpb, PV_GEN_MINB)
+#else
 __global__ void __launch_bounds__(kGenTpb)
+#endif
 translate_generic_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes,
                          const pv_space* __restrict__ spaces, const pv_seg* __restrict__ segs, uint32_t n_segs,
                          uint64_t n_chunks, const void* __restrict__ vas, uint64_t* __restrict__ out_value,
@@ -555,6 +588,63 @@ translate_generic_kernel(const uint8_t* __restrict__ image, uint64_t image_bytes
     const pv_seg seg = segs[lo];
     const pv_space sp = spaces[seg.space];
     const uint64_t lane0 = seg.begin + (c - seg.chunk0) * kChunk;
+    if (PV_GEN_LEVELSYNC && sp.mode == PV_ONE_STAGE_4L) {
+      const uint64_t base = sp.s1_base, lim = node_limit(image_bytes, base);
+      uint64_t va[kGenVpt], node[kGenVpt];
+      uint32_t st[kGenVpt];
+      uint32_t live = 0;
+#pragma unroll
+      for (int j = 0; j < kGenVpt; ++j) {
+        const uint64_t i = lane0 + (uint64_t)j * kGenTpb + threadIdx.x;
+        va[j] = 0;
+        node[j] = sp.s1_root_pfn;
+        st[j] = PV_ST_OK;
+        if (i < seg.end) {
+          va[j] = kVa32 ? (uint64_t)((const uint32_t*)vas)[i] : ((const uint64_t*)vas)[i];
+          live |= 1u << j;
+        }
+      }
+#pragma unroll
+      for (uint32_t l = 0; l < 4; ++l) {
+        uint64_t w[kGenVpt];
+#pragma unroll
+        for (int j = 0; j < kGenVpt; ++j) {  // this level's loads, all in flight
+          w[j] = 0;
+          if (!((live >> j) & 1u)) continue;
+          if (node[j] >= lim) {
+            st[j] = PV_ST_NODE_OOR | (l + 1);
+            node[j] = va[j];
+            live &= ~(1u << j);
+          } else {
+            w[j] = ld_word(image, base, node[j], (uint32_t)(va[j] >> (39 - 9 * l)) & 511u);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < kGenVpt; ++j) {
+          if (!((live >> j) & 1u)) continue;
+          if (w[j] & kFlagTrapping) {  // value: the node holding the trapping entry
+            st[j] = PV_ST_TRAP | (l + 1) | ((((uint32_t)(va[j] >> (39 - 9 * l))) & 511u) << 16);
+            live &= ~(1u << j);
+          } else if (!(w[j] & kFlagPresent)) {
+            st[j] = PV_ST_FAULT | (l + 1);
+            node[j] = va[j];
+            live &= ~(1u << j);
+          } else if (l == 2 && (w[j] & PV_FLAG_PS)) {  // 2 MiB leaf: its 4 KiB frame of va
+            node[j] = (w[j] >> kPageShift) + ((va[j] >> kPageShift) & 511u);
+            live &= ~(1u << j);
+          } else {
+            node[j] = w[j] >> kPageShift;
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kGenVpt; ++j) {
+        const uint64_t i = lane0 + (uint64_t)j * kGenTpb + threadIdx.x;
+        if (i < seg.end) emit_lane<kVa32, kPfn>(i, st[j], node[j], 0, va[j], out_value, out_status, out_aux, mode,
+                                                sink);
+      }
+      continue;
+    }
 #pragma unroll
     for (int j = 0; j < kGenVpt; ++j) {
       const uint64_t i = lane0 + (uint64_t)j * kGenTpb + threadIdx.x;
