@@ -68,7 +68,8 @@ __global__ void ordered_keys_kernel(const pv_op* __restrict__ ops, uint64_t n_op
                                     const uint64_t* __restrict__ page_aux,
                                     const unsigned long long* __restrict__ first_bad, const uint8_t* __restrict__ buf,
                                     uint64_t buf_bytes, uint32_t dead_key, uint32_t* __restrict__ keys,
-                                    ChunkDesc* __restrict__ desc, pv_op_result* __restrict__ results) {
+                                    ChunkDesc* __restrict__ desc, uint32_t* __restrict__ iota,
+                                    pv_op_result* __restrict__ results) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_ops; i += stride) {
     const pv_op o = ops[i];
@@ -90,6 +91,7 @@ __global__ void ordered_keys_kernel(const pv_op* __restrict__ ops, uint64_t n_op
       d.meta = (uint32_t)(src & 15) | ((uint32_t)(hpa & kPageMask) << 4) | (len << 16);
       d.pad = 0;
       desc[p] = d;
+      if (iota != nullptr) iota[p] = (uint32_t)p;
     }
   }
 }
@@ -108,6 +110,9 @@ __global__ void ordered_keys_kernel(const pv_op* __restrict__ ops, uint64_t n_op
 #endif
 #ifndef PV_AP_WINDOW
 #define PV_AP_WINDOW 6144  // measured: 3.66 ms vs 6.56 ms at the full ring (C2), see DESIGN.md
+#endif
+#ifndef PV_ORD_INDEX
+#define PV_ORD_INDEX 0  // A/B option: sort (page, u32 chunk index) pairs; the apply gathers descriptors by index
 #endif
 constexpr int kApPages = PV_AP_PAGES;                    // page slots (producer + consumer warp each) per CTA
 constexpr int kK = PV_AP_K;                         // chunks in flight per page slot (mbarrier pairs)
@@ -244,7 +249,10 @@ __device__ __forceinline__ uint32_t apply_chunk_rev(PageSmem& W, uint32_t lane, 
 // never covers (e.g. an arena's first byte) still scan every descriptor but
 // move only the few chunks that reach their uncovered bytes.
 struct NeedIter {
-  const ChunkDesc* rd;  // candidate k (0 = last chunk in program order) at rd - k
+  const ChunkDesc* rd;  // candidate k (0 = last chunk in program order) at rd - k, or at desc[ix[last - k]]
+  const ChunkDesc* desc;
+  const uint32_t* ix;   // PV_ORD_INDEX: sorted chunk indices (nullptr: rd holds sorted descriptors)
+  uint32_t last;
   uint32_t n, k0;       // candidates, current window start
   uint32_t cand;        // window lanes not yet rejected (warp-uniform)
   uint32_t meta_l;      // this lane's window candidate
@@ -259,7 +267,7 @@ __device__ __forceinline__ void need_window(NeedIter& it, uint32_t lane) {
   it.meta_l = 0;
   it.src_l = 0;
   if (k < it.n) {
-    const ChunkDesc d = *(it.rd - k);
+    const ChunkDesc d = it.ix != nullptr ? it.desc[it.ix[it.last - k]] : *(it.rd - k);
     it.meta_l = d.meta;
     it.src_l = d.src;
     const uint32_t off = (d.meta >> 4) & 0xFFF, len = d.meta >> 16;
@@ -272,9 +280,12 @@ __device__ __forceinline__ void need_window(NeedIter& it, uint32_t lane) {
   it.cand = __ballot_sync(0xFFFFFFFFu, maybe);
 }
 
-__device__ __forceinline__ void need_init(NeedIter& it, const ChunkDesc* __restrict__ desc, uint32_t b, uint32_t n,
-                                          uint32_t lane) {
+__device__ __forceinline__ void need_init(NeedIter& it, const ChunkDesc* __restrict__ desc,
+                                          const uint32_t* __restrict__ ix, uint32_t b, uint32_t n, uint32_t lane) {
   it.rd = desc + b + n - 1;
+  it.desc = desc;
+  it.ix = ix;
+  it.last = b + n - 1;
   it.n = n;
   it.k0 = 0;
   it.c[0] = it.c[1] = it.c[2] = it.c[3] = 0u;
@@ -329,11 +340,12 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
 
-__device__ __forceinline__ void produce(PageSmem& P, const ChunkDesc* __restrict__ desc, uint32_t b, uint32_t n,
+__device__ __forceinline__ void produce(PageSmem& P, const ChunkDesc* __restrict__ desc,
+                                        const uint32_t* __restrict__ ix, uint32_t b, uint32_t n,
                                         uint32_t lane, uint64_t pol, uint32_t& G, uint32_t& vhead, uint32_t& hptr,
                                         int64_t& released) {
   NeedIter it;
-  need_init(it, desc, b, n, lane);
+  need_init(it, desc, ix, b, n, lane);
   uint32_t meta;
   uint64_t src;
   while (need_next(it, lane, meta, src)) {
@@ -366,7 +378,7 @@ __device__ __forceinline__ void produce(PageSmem& P, const ChunkDesc* __restrict
 
 __global__ void __launch_bounds__(kApPages * 64)
 ordered_apply_kernel(uint8_t* __restrict__ image, const ChunkDesc* __restrict__ desc,
-                     const uint32_t* __restrict__ seg_key, const uint32_t* __restrict__ seg_len,
+                     const uint32_t* __restrict__ ix, const uint32_t* __restrict__ seg_key, const uint32_t* __restrict__ seg_len,
                      const uint32_t* __restrict__ seg_start, const uint32_t* __restrict__ n_segs_dev,
                      uint32_t dead_key, uint8_t* __restrict__ dirty) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -391,7 +403,7 @@ ordered_apply_kernel(uint8_t* __restrict__ image, const ChunkDesc* __restrict__ 
     if (key == dead_key) continue;
     const uint32_t b = seg_start[s], n = seg_len[s];
     if (producer) {
-      produce(P, desc, b, n, lane, pol, G, vhead, hptr, released);
+      produce(P, desc, ix, b, n, lane, pol, G, vhead, hptr, released);
       continue;
     }
     // The page is assembled in SMEM from the chunks that matter only; bytes
@@ -399,7 +411,7 @@ ordered_apply_kernel(uint8_t* __restrict__ image, const ChunkDesc* __restrict__ 
     reinterpret_cast<uint4*>(P.cov)[lane] = make_uint4(0, 0, 0, 0);
     __syncwarp();
     NeedIter it;
-    need_init(it, desc, b, n, lane);
+    need_init(it, desc, ix, b, n, lane);
     uint32_t meta_it;
     uint64_t src_it;
     while (need_next(it, lane, meta_it, src_it)) {
@@ -462,14 +474,19 @@ __global__ void ordered_results_kernel(const pv_op* __restrict__ ops, uint64_t n
 struct OrderedScratch {
   uint32_t *keys_in, *keys_out, *seg_key, *seg_len, *seg_start, *n_segs;
   ChunkDesc *desc, *desc_sorted;
+  uint32_t *idx_in, *idx_out;  // PV_ORD_INDEX
   void* cub_tmp;
   size_t cub_bytes;
 };
 
 static size_t cub_need(uint64_t n, int end_bit) {
   size_t a = 0, b = 0, c = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, a, (uint32_t*)nullptr, (uint32_t*)nullptr, (ChunkDesc*)nullptr,
-                                  (ChunkDesc*)nullptr, (int)n, 0, end_bit);
+  if (PV_ORD_INDEX)
+    cub::DeviceRadixSort::SortPairs(nullptr, a, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                    (uint32_t*)nullptr, (int)n, 0, end_bit);
+  else
+    cub::DeviceRadixSort::SortPairs(nullptr, a, (uint32_t*)nullptr, (uint32_t*)nullptr, (ChunkDesc*)nullptr,
+                                    (ChunkDesc*)nullptr, (int)n, 0, end_bit);
   cub::DeviceRunLengthEncode::Encode(nullptr, b, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint32_t*)nullptr,
                                      (uint32_t*)nullptr, (int)n);
   cub::DeviceScan::ExclusiveSum(nullptr, c, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)n);
@@ -487,7 +504,7 @@ static int bits_for(uint64_t image_pages) {
 static uint64_t arr_bytes(uint64_t n, uint64_t elt) { return ((n + 1) * elt + 255) / 256 * 256; }
 
 size_t ordered_scratch_bytes(uint64_t n_pages, uint64_t image_pages) {
-  return 5 * arr_bytes(n_pages, 4) + 2 * arr_bytes(n_pages, sizeof(ChunkDesc)) + 256 +
+  return (PV_ORD_INDEX ? 7 : 5) * arr_bytes(n_pages, 4) + 2 * arr_bytes(n_pages, sizeof(ChunkDesc)) + 256 +
          cub_need(n_pages, bits_for(image_pages)) + 256;
 }
 
@@ -503,6 +520,13 @@ static OrderedScratch carve(void* base, uint64_t n, size_t cub_bytes) {
   p += arr_bytes(n, sizeof(ChunkDesc));
   s.desc_sorted = reinterpret_cast<ChunkDesc*>(p);
   p += arr_bytes(n, sizeof(ChunkDesc));
+  s.idx_in = s.idx_out = nullptr;
+  if (PV_ORD_INDEX) {
+    s.idx_in = reinterpret_cast<uint32_t*>(p);
+    p += arr_bytes(n, 4);
+    s.idx_out = reinterpret_cast<uint32_t*>(p);
+    p += arr_bytes(n, 4);
+  }
   s.n_segs = reinterpret_cast<uint32_t*>(p);
   p += 256;
   s.cub_tmp = p;
@@ -536,14 +560,18 @@ cudaError_t launch_copy_ordered(uint8_t* image, uint64_t image_bytes, const pv_o
     void* tk = timing_begin("ordered_keys", stream);
     ordered_keys_kernel<<<(unsigned)g, 256, 0, stream>>>(ops, n_ops, page_off, page_hpa, page_status, page_aux,
                                                          reinterpret_cast<const unsigned long long*>(op_first_bad),
-                                                         buf, buf_bytes, dead_key, s.keys_in, s.desc, results);
+                                                         buf, buf_bytes, dead_key, s.keys_in, s.desc, s.idx_in,
+                                                         results);
     timing_end(tk, stream);
   }
   size_t tb = s.cub_bytes;
   // the 16-byte descriptors ride along as the sort's values (no index gather afterwards)
   void* tks = timing_begin("ordered_sort", stream);
-  cudaError_t e = cub::DeviceRadixSort::SortPairs(s.cub_tmp, tb, s.keys_in, s.keys_out, s.desc, s.desc_sorted,
-                                                  (int)n_pages, 0, end_bit, stream);
+  cudaError_t e = PV_ORD_INDEX
+                      ? cub::DeviceRadixSort::SortPairs(s.cub_tmp, tb, s.keys_in, s.keys_out, s.idx_in, s.idx_out,
+                                                        (int)n_pages, 0, end_bit, stream)
+                      : cub::DeviceRadixSort::SortPairs(s.cub_tmp, tb, s.keys_in, s.keys_out, s.desc, s.desc_sorted,
+                                                        (int)n_pages, 0, end_bit, stream);
   timing_end(tks, stream);
   if (e != cudaSuccess) return e;
   tb = s.cub_bytes;
@@ -560,7 +588,8 @@ cudaError_t launch_copy_ordered(uint8_t* image, uint64_t image_bytes, const pv_o
   const uint64_t want = (n_pages + kApPages - 1) / kApPages;
   if (g2 > want) g2 = want;
   void* tk = timing_begin("ordered_apply", stream);
-  ordered_apply_kernel<<<(unsigned)g2, kApPages * 64, smem, stream>>>(image, s.desc_sorted, s.seg_key, s.seg_len,
+  ordered_apply_kernel<<<(unsigned)g2, kApPages * 64, smem, stream>>>(image, PV_ORD_INDEX ? s.desc : s.desc_sorted,
+                                                                      s.idx_out, s.seg_key, s.seg_len,
                                                                       s.seg_start, s.n_segs, dead_key, dirty);
   timing_end(tk, stream);
   return cudaGetLastError();

@@ -17,6 +17,6 @@ timeout 1200 ncu --set full --clock-control none --import-source on \
   python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --split-sms 0 > gpurun_out/${tag}_c5_full.log 2>&1
 echo "c5 full rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on \
-  -k regex:"ordered_apply_kernel|fifo_verify_kernel|plan_kernel" -c 3 -o gpurun_out/${tag}_c2_full \
+  -k regex:"ordered_apply_kernel|fifo_spec_kernel|plan_kernel|Onesweep" -c 5 -o gpurun_out/${tag}_c2_full \
   python bench.py --workload c2 --steps 1 --warmup 1 > gpurun_out/${tag}_c2_full.log 2>&1
 echo "c2 full rc=$?"
