@@ -1131,10 +1131,11 @@ def c2_kernel_table(ms, n_ops, n_pages, apply_ms, apply_bytes, peak, peak_kind):
                                                 "loads, not HBM"),
         "stamp": (16 * n_ops + 24 * n_pages, "per page: hpa in + owner word read-modify-write; per op: page offset "
                                              "+ first-bad"),
-        "ordered_keys": (80 * n_ops + 28 * n_pages, "per op: pv_op + page offset + first-bad in, result out; per "
-                                                    "page: hpa in, 4 B key + 16 B chunk descriptor out"),
-        "ordered_sort": (84 * n_pages, "CUB onesweep radix sort of (4 B key, 16 B descriptor) pairs: a key "
-                                       "histogram pass + two passes reading and writing every pair"),
+        "ordered_keys": (80 * n_ops + 32 * n_pages, "per op: pv_op + page offset + first-bad in, result out; per "
+                                                    "page: hpa in, 4 B key + 16 B chunk descriptor + 4 B index out"),
+        "ordered_sort": (36 * n_pages, "CUB onesweep radix sort of (4 B key, 4 B chunk index) pairs: a key "
+                                       "histogram pass + two passes reading and writing every pair (the product "
+                                       "build, PV_ORD_INDEX=1)"),
     }
     out = {}
     for k, t in ms.items():

@@ -62,7 +62,8 @@ __device__ __forceinline__ void write_result(const pv_op& o, uint64_t p0, uint64
 
 // One thread per op: the op's result (copied prefix / first failure), and
 // per page keys[p] = destination page of live page p (else the dead key,
-// which sorts last) and desc[p] = p's chunk descriptor (sorted along as the value).
+// which sorts last), desc[p] = p's chunk descriptor and iota[p] = p (the
+// sort's values; with PV_ORD_INDEX=0 the descriptors are the values).
 __global__ void ordered_keys_kernel(const pv_op* __restrict__ ops, uint64_t n_ops, const uint64_t* __restrict__ page_off,
                                     const uint64_t* __restrict__ page_hpa, const uint32_t* __restrict__ page_status,
                                     const uint64_t* __restrict__ page_aux,
@@ -111,8 +112,12 @@ __global__ void ordered_keys_kernel(const pv_op* __restrict__ ops, uint64_t n_op
 #ifndef PV_AP_WINDOW
 #define PV_AP_WINDOW 6144  // measured: 3.66 ms vs 6.56 ms at the full ring (C2), see DESIGN.md
 #endif
+// The sort carries u32 chunk indices, not the 16-byte descriptors: the
+// apply gathers the descriptors it scans by index.  C2: sort 0.533 -> 0.317
+// ms, apply 0.144 -> 0.244 ms, apply phase 0.939 -> 0.836 ms
+// (profiles/r02_ord_index_ab.md; PV_ORD_INDEX=0 sorts the descriptors).
 #ifndef PV_ORD_INDEX
-#define PV_ORD_INDEX 0  // A/B option: sort (page, u32 chunk index) pairs; the apply gathers descriptors by index
+#define PV_ORD_INDEX 1
 #endif
 constexpr int kApPages = PV_AP_PAGES;                    // page slots (producer + consumer warp each) per CTA
 constexpr int kK = PV_AP_K;                         // chunks in flight per page slot (mbarrier pairs)
