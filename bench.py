@@ -1483,10 +1483,12 @@ def run_e2e(wl, args, world):
     torch.cuda.synchronize()
     tr_s = cp_s = 0.0
     steps = max(1, args.steps)
+    tr_each = []
     for _ in range(steps):
         a, b = one_step()
         tr_s += a
         cp_s += b
+        tr_each.append(a)
     from paper_1304_3771_b200 import shard
 
     tr_s, cp_s = shard.max_over_ranks([tr_s, cp_s], world, device="cuda")
@@ -1524,7 +1526,12 @@ def run_e2e(wl, args, world):
     return {"value": wl.total_vas * steps / tr_s, "unit": "translations/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "copy": {"value": wl.total_copy_bytes * steps / cp_s / 1e9, "unit": "GB/s"},
-            "steps": steps, "results": "one pv_translate_words word per lane (frame number, or status; "
+            "steps": steps,
+            "translate_ms_per_step": {"mean": 1e3 * tr_s / steps, "best": 1e3 * min(tr_each),
+                                      "median": 1e3 * statistics.median(tr_each),
+                                      "note": "host-driven pipeline: value uses the mean (max over ranks); best / median "
+                                              "over this rank's steps"},
+            "results": "one pv_translate_words word per lane (frame number, or status; "
                                        "exception records for lanes whose value is not their va)",
             "lanes_equal_device_results": same,
             "gather_to_rank0": returned,
