@@ -741,21 +741,21 @@ def translate_host_many(image, jobs, chunk: int = 1 << 23, *, packed: bool = Fal
 _pipe_tls = threading.local()
 
 
-def _pipe(dtype, chunk: int, words: bool):
-    """The calling thread's side streams, device chunk buffers and events of
-    the host pipeline, reused across calls (every call drains them before it
-    returns)."""
+def _pipe(dtype, chunk: int, words: bool, nbuf: int = 2):
+    """The calling thread's side streams, ``nbuf`` device chunk buffer sets
+    and events of the host pipeline, reused across calls (every call drains
+    them before it returns)."""
     import torch
 
     cache = getattr(_pipe_tls, "cache", None)
     if cache is None:
         cache = _pipe_tls.cache = {}
-    key = (torch.cuda.current_device(), dtype, chunk, words)
+    key = (torch.cuda.current_device(), dtype, chunk, words, nbuf)
     st = cache.get(key)
     if st is None:
         if words:
             bufs = [(torch.empty(chunk, dtype=dtype, device="cuda"), torch.empty(chunk, dtype=torch.int32, device="cuda"),
-                     torch.cuda.Event(), torch.cuda.Event(), torch.cuda.Event()) for _ in range(2)]
+                     torch.cuda.Event(), torch.cuda.Event(), torch.cuda.Event()) for _ in range(nbuf)]
         else:
             bufs = [(torch.empty(chunk, dtype=dtype, device="cuda"), torch.empty(chunk, dtype=torch.int64, device="cuda"),
                      torch.empty(chunk, dtype=torch.int32, device="cuda"), torch.zeros(chunk, dtype=torch.int64, device="cuda"),
@@ -778,12 +778,18 @@ def _host_plan(image, space: Space, m: int) -> "TranslatePlan":
     return plan
 
 
+_WORD_BUFS = 2
+
+
 def _translate_host_words(image, jobs, chunk: int, out, exc_cap: int):
     """translate_host_many(words=True): the same two-buffer-set pipeline with
     4-byte lane words each way; the exception records of every chunk append
     to one device list read once at the end."""
     import torch
 
+    # pipeline shape (A/B knobs): lanes per chunk and chunk buffer sets in flight
+    chunk = int(os.environ.get("PV_HOST_WORD_CHUNK", chunk))
+    nbuf = int(os.environ.get("PV_HOST_WORD_BUFS", _WORD_BUFS))
     srcs, dtype = [], torch.int32
     for space, host_vas in jobs:
         if host_vas.dtype not in (torch.int32, torch.int64):
@@ -812,12 +818,12 @@ def _translate_host_words(image, jobs, chunk: int, out, exc_cap: int):
     compute = torch.cuda.current_stream()
     exc_list = ExcList(cap)
     if work:
-        h2d, d2h, bufs = _pipe(dtype, chunk, True)
+        h2d, d2h, bufs = _pipe(dtype, chunk, True, nbuf)
         h2d.wait_stream(compute)  # the caller's earlier work (and the counter reset above) first
         for i, (space, src, w, l0, start, m) in enumerate(work):
-            d_vas, d_w, ev_in, ev_done, ev_out = bufs[i % 2]
-            if i >= 2:
-                h2d.wait_event(ev_out)  # buffers of chunk i-2 fully drained
+            d_vas, d_w, ev_in, ev_done, ev_out = bufs[i % nbuf]
+            if i >= nbuf:
+                h2d.wait_event(ev_out)  # buffers of chunk i-nbuf fully drained
             with torch.cuda.stream(h2d):
                 d_vas[:m].copy_(src[start:start + m], non_blocking=True)
                 ev_in.record(h2d)
